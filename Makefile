@@ -1,0 +1,55 @@
+# Build recipe for the B200 matching engine and its CPU checkers.
+#
+#   make            -> paper_1303_1379_b200/libbmatch_b200.so  (sm_100a CUDA + host C-ABI)
+#                      oracle/liboracle.so                      (C restatement of the reference path)
+#   make ref        -> oracle/_ref/libbmatch_ref.so              (the reference compiled from its own
+#                      sources under /root/reference; only where that tree exists)
+#
+# Built artefacts are git-ignored but travel to the GPU box with the gpurun snapshot.
+
+NVCC      ?= nvcc
+CXX       ?= g++
+CC        ?= gcc
+ARCH      := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall -Xptxas -v \
+             -Iinclude -Ipaper_1303_1379_b200/csrc
+CXXFLAGS  := -O3 -std=c++17 -fPIC -Wall -Wextra -pthread -Iinclude
+CFLAGS    := -O2 -std=c11 -fPIC -Wall -Wextra
+
+PKG       := paper_1303_1379_b200
+CSRC      := $(PKG)/csrc
+BUILD     := build
+LIB       := $(PKG)/libbmatch_b200.so
+ORACLE    := oracle/liboracle.so
+
+REF_ROOT  ?= /root/reference/proj
+REF_SRCS  := algorithms baselines csr_graph gpu_match kernel_grid matching matrix_market
+REF_LIB   := oracle/_ref/libbmatch_ref.so
+
+.PHONY: all ref clean
+all: $(LIB) $(ORACLE)
+
+$(BUILD):
+	mkdir -p $(BUILD)
+
+$(BUILD)/bm_engine.o: $(CSRC)/bm_engine.cu $(CSRC)/bm_device.cuh include/bmatch_b200.h | $(BUILD)
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(BUILD)/ptxas.log || (cat $(BUILD)/ptxas.log; false)
+
+$(BUILD)/bm_host.o: $(CSRC)/bm_host.cpp include/bmatch_b200.h include/bmatch_b200_gen.h | $(BUILD)
+	$(CXX) $(CXXFLAGS) -c $< -o $@
+
+$(LIB): $(BUILD)/bm_engine.o $(BUILD)/bm_host.o
+	$(NVCC) $(ARCH) -shared -o $@ $^ -Xcompiler -pthread
+
+$(ORACLE): oracle/bm_oracle.c oracle/bm_oracle.h
+	$(CC) $(CFLAGS) -shared -o $@ oracle/bm_oracle.c
+
+ref: $(REF_LIB)
+
+$(REF_LIB): oracle/ref_capi.cpp $(foreach s,$(REF_SRCS),$(REF_ROOT)/src/$(s).cpp)
+	mkdir -p oracle/_ref
+	$(CXX) -std=c++20 -O3 -DNDEBUG -fPIC -shared -pthread -I$(REF_ROOT)/include \
+	    -o $@ oracle/ref_capi.cpp $(foreach s,$(REF_SRCS),$(REF_ROOT)/src/$(s).cpp)
+
+clean:
+	rm -rf $(BUILD) $(LIB) $(ORACLE)

@@ -1,0 +1,188 @@
+/*
+ * bmatch_b200.h — C ABI of the B200-native maximum-cardinality bipartite
+ * matching engine (APFB/APsB x GPUBFS/GPUBFS-WR, ALTERNATE + FIXMATCHING,
+ * arXiv 1303.1379).
+ *
+ * This is the drop-in boundary for the reference's hot path. Every entry
+ * point names the reference interface it replaces (paths relative to
+ * /root/reference/proj). Plain C types only: int32/int64 arrays, sizes,
+ * opaque handles. Host buffers are always caller-owned; the library never
+ * retains a host pointer after a call returns.
+ *
+ * Reference interfaces replaced:
+ *   apfb(g, init, grid, schedule, kernel, observer)        include/bmatch/gpu_match.hpp:133-135
+ *   apsb(g, init, grid, schedule, kernel, improved, obs)   include/bmatch/gpu_match.hpp:141-144
+ *   DriverResult{matching, counters}                       include/bmatch/gpu_match.hpp:126-129
+ *   PhaseCounters                                          include/bmatch/gpu_match.hpp:39-52
+ *   PhaseEvent / PhaseObserver                             include/bmatch/gpu_match.hpp:115-124
+ *   BipartiteCsr{nc,nr,cxadj(int64),cadj(int32)}           include/bmatch/csr_graph.hpp:18-31
+ *   MatchingState{rmatch,cmatch}                           include/bmatch/matching.hpp:15-25
+ *   cheap_matching (init)                                  src/matching.cpp:13-26
+ *   registry ids {apfb,apsb}-{gpubfs,wr}                   src/algorithms.cpp:19-27
+ *
+ * Error model (mirrors the reference's exceptions, see bm_status):
+ *   std::invalid_argument  -> BM_ERR_INVALID_ARG  (e.g. matching.cpp:71-73)
+ *   std::logic_error       -> BM_ERR_LOGIC        (gpu_match.cpp:77-80, 272-274)
+ *   std::runtime_error     -> BM_ERR_BOUND_EXCEEDED (nc+1 phase bound, gpu_match.cpp:317-320)
+ * The message of the last failure on the calling thread is bm_last_error().
+ * There is no CPU fallback: without a usable sm_100 device every compute
+ * entry point fails with BM_ERR_CUDA.
+ */
+#ifndef BMATCH_B200_H
+#define BMATCH_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BM_ABI_VERSION 1
+
+typedef enum bm_status {
+  BM_OK = 0,
+  BM_ERR_INVALID_ARG = 1,
+  BM_ERR_LOGIC = 2,
+  BM_ERR_BOUND_EXCEEDED = 3,
+  BM_ERR_CUDA = 4,
+  BM_ERR_OOM = 5,
+  BM_ERR_NCCL = 6
+} bm_status;
+
+/* Driver: APFB = augment along every path found per phase (gpu_match.hpp:131-135);
+ * APSB = break the level loop at the first level that finds a path (gpu_match.hpp:137-144). */
+typedef enum bm_driver { BM_DRIVER_APFB = 0, BM_DRIVER_APSB = 1 } bm_driver;
+
+/* BFS kernel: GPUBFS (Alg. 2, gpu_match.cpp:23-72) or GPUBFS-WR (Alg. 4, gpu_match.cpp:74-135). */
+typedef enum bm_bfs_kernel { BM_BFS_GPUBFS = 0, BM_BFS_WR = 1 } bm_bfs_kernel;
+
+/* Initial matching: GIVEN = use the caller's rmatch/cmatch (the reference's
+ * methodology: cheap_matching on the host, bench.cpp:52-63); GPU_GREEDY =
+ * parallel first-fit on the device; GPU_KS = degree-1 columns first, then
+ * parallel first-fit (one-sided Karp-Sipser priority). */
+typedef enum bm_init { BM_INIT_GIVEN = 0, BM_INIT_GPU_GREEDY = 1, BM_INIT_GPU_KS = 2 } bm_init;
+
+typedef struct bm_match_opts {
+  int32_t driver;            /* bm_driver */
+  int32_t bfs_kernel;        /* bm_bfs_kernel */
+  int32_t improved;          /* endpoint-encoded WR + alternate_wr (requires BM_BFS_WR),
+                                gpu_match.cpp:188-218; algorithms.cpp:19-27 enables it for apsb-wr */
+  int32_t init;              /* bm_init */
+  int32_t max_phases;        /* 0 = run to the maximum (bound nc+1); >0 = stop after that many
+                                outer iterations and return with *done = 0 (resumable) */
+  int32_t reserved[3];
+} bm_match_opts;
+
+/* PhaseCounters (gpu_match.hpp:39-52) plus the device-side work counters the
+ * roofline accounting needs. */
+typedef struct bm_counters {
+  int64_t outer_iterations;
+  int64_t bfs_launches_total;      /* sum of bfs_launches_per_iteration (BFS levels expanded) */
+  int64_t columns_scanned;         /* columns expanded (passed level + WR tests): reference counter */
+  int64_t alternations_attempted;  /* walks started */
+  int64_t fix_resets;
+  int64_t serial_retries;
+  int64_t edges_traversed;         /* E_trav: adjacency entries read by expanded columns */
+  int64_t columns_visited;         /* N_vis: columns newly labelled (bitmap claims) */
+  int64_t walk_steps;              /* L_walk: pair swaps performed by ALTERNATE */
+  int64_t frontier_entries;        /* frontier entries processed (incl. WR-skipped) */
+  int64_t cardinality;             /* final cardinality (count of rmatch >= 0) */
+  int64_t initial_cardinality;     /* cardinality of the (given or GPU-built) initial matching */
+  int64_t n_phase_records;         /* number of valid entries written to bfs_launches_per_iteration */
+  int64_t reserved[3];
+} bm_counters;
+
+/* PhaseEvent (gpu_match.hpp:115-123). rmatch/cmatch point at a host snapshot
+ * valid only during the callback. Return nonzero to abort the run
+ * (bm_run then returns BM_ERR_INVALID_ARG with "aborted by observer"). */
+typedef struct bm_phase_event {
+  int64_t iteration;
+  int32_t augmenting_path_found;
+  int32_t serial_retry;
+  int64_t cardinality_before;
+  int64_t cardinality_after;
+  int64_t bfs_launches;
+  const int32_t* rmatch; int32_t nr;
+  const int32_t* cmatch; int32_t nc;
+} bm_phase_event;
+
+typedef int (*bm_phase_cb)(const bm_phase_event* ev, void* user);
+
+typedef struct bm_handle bm_handle;
+
+/* ---- lifecycle ------------------------------------------------------- */
+int32_t     bm_abi_version(void);
+const char* bm_last_error(void);                       /* thread-local message of the last failure */
+const char* bm_status_string(int32_t status);
+int32_t     bm_device_count(void);                     /* 0 when no CUDA device is usable */
+bm_status   bm_create(int32_t device, bm_handle** out);
+bm_status   bm_destroy(bm_handle* h);
+/* Use an external CUDA stream (cudaStream_t passed as void*; NULL = the handle's own). */
+bm_status   bm_set_stream(bm_handle* h, void* stream);
+
+/* ---- graph: device-resident CSC (replaces BipartiteCsr, csr_graph.hpp:18-31) ----
+ * Copies cxadj[nc+1] (int64, cxadj[0]=0, non-decreasing) and cadj[E]
+ * (int32 row ids in [0,nr)) to HBM. Validation (check_csr, csr_graph.cpp:45-64,
+ * minus the per-column sortedness rule the kernels do not rely on) runs on the
+ * device; a violation returns BM_ERR_INVALID_ARG. E must be < 2^32. */
+bm_status   bm_upload_csc(bm_handle* h, int32_t nc, int32_t nr,
+                          const int64_t* cxadj, const int32_t* cadj);
+bm_status   bm_graph_info(bm_handle* h, int32_t* nc, int32_t* nr, int64_t* nedges);
+
+/* ---- matching: the reference-shaped one-call entry ----------------------
+ * Replaces apfb()/apsb() (gpu_match.hpp:133-144): rmatch[nr]/cmatch[nc] are
+ * the initial matching on input when opts->init == BM_INIT_GIVEN (ignored
+ * otherwise) and the maximum matching on output. bfs_launches_per_iteration
+ * (nullable) receives one entry per outer iteration, up to `cap` entries;
+ * counters->n_phase_records says how many were written. */
+bm_status   bm_match(bm_handle* h, const bm_match_opts* opts,
+                     int32_t* rmatch, int32_t* cmatch,
+                     int64_t* cardinality, bm_counters* counters,
+                     int64_t* bfs_launches_per_iteration, int64_t cap,
+                     bm_phase_cb cb, void* user);
+
+/* ---- device-resident path (inputs already in HBM; used by the bench) ---- */
+bm_status   bm_load_matching(bm_handle* h, const int32_t* rmatch, const int32_t* cmatch);
+/* Runs from the loaded initial matching (a device-to-device copy, so repeated
+ * runs start from the same state); the result stays on the device. *done is
+ * 1 when the matching is maximum, 0 when max_phases stopped it early
+ * (call bm_resume to continue). */
+bm_status   bm_run(bm_handle* h, const bm_match_opts* opts, int64_t* cardinality,
+                   bm_counters* counters, int64_t* bfs_launches_per_iteration,
+                   int64_t cap, bm_phase_cb cb, void* user, int32_t* done);
+bm_status   bm_resume(bm_handle* h, const bm_match_opts* opts, int64_t* cardinality,
+                      bm_counters* counters, int64_t* bfs_launches_per_iteration,
+                      int64_t cap, bm_phase_cb cb, void* user, int32_t* done);
+bm_status   bm_download_matching(bm_handle* h, int32_t* rmatch, int32_t* cmatch);
+/* Device time (ms, CUDA events on the handle's stream) of the driver kernel
+ * launches of the last bm_run/bm_resume/bm_match, and how many launches. */
+bm_status   bm_last_kernel_time(bm_handle* h, double* ms, int32_t* launches);
+
+/* ---- one BFS phase without ALTERNATE/FIX (parity probes) ----------------
+ * Mirrors run_phase up to expand_bfs (gpu_match.cpp:268-290) from the given
+ * matching and returns the phase arrays: bfs_array[nc] (levels, L0 = 2),
+ * predecessor[nr], and rmatch[nr] with -2 endpoint flags. Any pointer may be
+ * NULL. *launches receives the number of levels expanded. */
+bm_status   bm_bfs_phase(bm_handle* h, int32_t driver, int32_t bfs_kernel, int32_t improved,
+                         const int32_t* rmatch_in, const int32_t* cmatch_in,
+                         int32_t* bfs_array, int32_t* predecessor, int32_t* rmatch_out,
+                         int64_t* launches, int32_t* path_found);
+
+/* ---- GPU Berge certificate (replaces validate + is_maximum, matching.cpp:70-131) ----
+ * Runs on the device against the uploaded graph. *violations = number of
+ * validity violations (pending -2, asymmetry, non-edge, out of range);
+ * *is_max = 1 when no augmenting path exists (only meaningful when
+ * *violations == 0). */
+bm_status   bm_verify(bm_handle* h, const int32_t* rmatch, const int32_t* cmatch,
+                      int64_t* violations, int32_t* is_max, int64_t* cardinality);
+
+/* ---- host utilities (not on the hot path) -------------------------------- */
+/* First-fit greedy in ascending column order; restates matching.cpp:13-26. */
+bm_status   bm_host_cheap_matching(int32_t nc, int32_t nr, const int64_t* cxadj,
+                                   const int32_t* cadj, int32_t* rmatch, int32_t* cmatch);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BMATCH_B200_H */

@@ -1,0 +1,1400 @@
+// bm_engine.cu — B200 (sm_100a) maximum-cardinality bipartite matching engine.
+//
+// One cooperative, persistent kernel runs the whole augmenting-path driver of
+// arXiv 1303.1379 on the device: initial matching (optional), every phase's
+// level-synchronous BFS, ALTERNATE, FIXMATCHING and the termination test. The
+// host launches it once per bm_run (or once per phase when an observer is
+// attached) and reads one small control block back at the end. There is no
+// per-level host synchronisation at all; levels and stages are separated by a
+// software grid barrier (one atomic per CTA).
+//
+// Reference correspondence (paths relative to /root/reference/proj):
+//   setup stage            init_bfs_array / init_root / predecessor reset  src/gpu_match.cpp:8-21, 277-282
+//   expand_level           gpubfs / gpubfs_wr (Alg. 2 / Alg. 4)            src/gpu_match.cpp:23-135
+//   level loop             expand_bfs                                       src/gpu_match.cpp:247-266
+//   alternate stage        alternate / alternate_wr / alternate_walk       src/gpu_match.cpp:144-218
+//   fix stages             fix_matching (three rules)                       src/gpu_match.cpp:220-245
+//   phase loop             run_phase / run_driver / apfb / apsb             src/gpu_match.cpp:268-376
+//   greedy init            cheap_matching (first-fit), parallelised        src/matching.cpp:13-26
+//
+// What is B200-specific (and why it is not a translation of the reference):
+//   * The reference tests every column's level in every launch (O(nc) per
+//     level, gpu_match.cpp:48/105). Here each level is a frontier queue of
+//     16-byte entries {col, root, adj_begin, edge_prefix}; the edge prefix
+//     comes from one packed 64-bit atomicAdd per warp ((count<<33)|edges),
+//     so the next level can be split into equal *edge* tiles regardless of
+//     the degree skew (R-MAT hubs of 2e5 rows are split across CTAs).
+//   * "Unvisited" is a 1-bit-per-column bitmap (nc/8 bytes, L2 resident even
+//     at 1e8 columns) claimed with atomicOr, instead of a 4-byte gather into
+//     bfs_array; the bfs_array labels are still written (reference layout).
+//   * Per-phase O(n) passes (init, FIX, cardinality) are restricted to the
+//     columns/rows the phase touched: only those can be inconsistent after
+//     ALTERNATE, so the restricted FIX is exactly the reference's FIX.
+//   * The root of each tree rides in the frontier entry (no root[] gather).
+#include <algorithm>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "bm_device.cuh"
+#include "bmatch_b200.h"
+
+namespace bm {
+
+constexpr int kThreads = 512;         // threads per CTA
+constexpr int kItems = 4;             // edges per thread per round (memory-level parallelism)
+constexpr int kStartLevel = 2;        // L0 (gpu_match.cpp:275)
+constexpr int kUnvisited = kStartLevel - 1;
+constexpr int kFoundMark = kStartLevel - 2;
+constexpr unsigned long long kEdgeMask = (1ull << 33) - 1;
+
+enum CtlError : int {
+  kErrNone = 0,
+  kErrBound = 1,        // more than nc + 1 phases (gpu_match.cpp:317-320)
+  kErrInvalidInit = 2,  // initial matching is not a clean valid matching
+  kErrBarrier = 3,      // grid barrier watchdog fired
+  kErrWalk = 4,         // an ALTERNATE walk exceeded nc steps (cannot happen on valid state)
+  kErrLevels = 5,       // more BFS levels than columns (cannot happen)
+};
+
+struct alignas(128) Slot {
+  unsigned long long packed;  // (entries << 33) | edges, pushed by the previous level
+  unsigned tile;              // dynamic edge-tile counter while this level is expanded
+  unsigned pad[29];
+};
+
+struct PhaseRec {
+  long long launches;
+  long long before;
+  long long after;
+  int found;
+  int retry;
+};
+
+enum Stat : int {
+  kStTrav = 0,
+  kStCexp,
+  kStNvis,
+  kStEntries,
+  kStWalks,
+  kStSteps,
+  kStResets,
+  kStLevels,
+  kStRetries,
+  kNumStats
+};
+
+struct alignas(128) Ctrl {
+  unsigned bar_count;
+  unsigned bar_gen;
+  unsigned pad0[30];
+  Slot lvl[3];
+  Slot roots;
+  unsigned n_ep;
+  unsigned pad1[31];
+  unsigned path_found[2];
+  unsigned pad2[30];
+  unsigned long long invalid;
+  unsigned long long isolated;
+  unsigned long long pad3[14];
+  unsigned long long stats[kNumStats];
+  // run state carried between launches (written by block 0 / thread 0 on exit)
+  long long outer;
+  long long card;
+  long long isolated_cols;
+  long long init_card;
+  long long bfs_levels_last;
+  int cur;
+  int done;
+  int error;
+  int n_recs;
+  int path_found_last;
+  int phase_parity;
+};
+
+struct Params {
+  int nc, nr;
+  const unsigned* offs;  // nc + 1
+  const int* adj;        // E
+  int* rmatch;
+  int* cmatch;
+  int* pred;
+  int* bfs;
+  unsigned* vis;
+  int nvis_words;
+  int4* F0;
+  int4* F1;
+  int* FR;
+  int* EP;
+  Ctrl* ctl;
+  PhaseRec* recs;
+  int rec_cap;
+  int apsb;
+  int init_mode;
+  int fresh;
+  int max_phases;
+  int stop_after_bfs;
+  long long phase_bound;
+};
+
+struct Smem {
+  unsigned pre[kThreads + 1];
+  int col[kThreads];
+  int root[kThreads];
+  unsigned beg[kThreads];
+  unsigned tile;
+  unsigned long long cnt[kNumStats];  // per-CTA work counters, flushed to Ctrl at exit
+};
+
+// Warp-reduce a per-thread count and add it to the CTA's shared counter. Must
+// be called by every lane of the warp.
+__device__ __forceinline__ void flush_count(Smem& sm, int idx, unsigned v) {
+  v = warp_sum(v);
+  if (lane_id() == 0 && v) atomicAdd(&sm.cnt[idx], (unsigned long long)v);
+}
+
+// ---------------------------------------------------------------------------
+// Grid barrier. All CTAs are co-resident (cooperative launch). Thread 0 of
+// each CTA arrives with one atomic; the last arriver resets the count and
+// bumps the generation. __threadfence() on both sides orders every write of
+// the stage before every read of the next (and invalidates this SM's L1).
+__device__ __noinline__ void grid_sync(Ctrl* ctl) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned gen = ld_acq(&ctl->bar_gen);
+    __threadfence();
+    const unsigned arrived = atomicAdd(&ctl->bar_count, 1u);
+    if (arrived == gridDim.x - 1) {
+      st_rlx(&ctl->bar_count, 0u);
+      __threadfence();
+      atomicAdd(&ctl->bar_gen, 1u);
+    } else {
+      const long long t0 = clock64();
+      unsigned spins = 0;
+      while (ld_acq(&ctl->bar_gen) == gen) {
+        __nanosleep(64);
+        if (((++spins) & 0xfffu) == 0 && clock64() - t0 > (1ll << 37)) {  // ~70 s watchdog
+          ctl->error = kErrBarrier;
+          __threadfence_system();
+          __trap();
+        }
+      }
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ bool is_leader() { return blockIdx.x == 0 && threadIdx.x == 0; }
+
+__device__ __forceinline__ unsigned long long global_thread() {
+  return (unsigned long long)blockIdx.x * kThreads + threadIdx.x;
+}
+__device__ __forceinline__ unsigned long long global_threads() {
+  return (unsigned long long)gridDim.x * kThreads;
+}
+
+// Warp-aggregated append of frontier entries {col, root, begin, prefix} with
+// the matching discovered row in FR. One packed 64-bit atomic per warp gives
+// both the slot and the level-local edge prefix, so prefixes are monotone in
+// slot order (atomics on one address are totally ordered).
+__device__ __forceinline__ void push_entries(bool win, int col, int root, unsigned beg, unsigned deg,
+                                             int row, Slot* out, int4* F, int* FR,
+                                             unsigned out_base) {
+  const unsigned mask = __ballot_sync(kFull, win);
+  if (mask == 0) return;
+  const unsigned lane = lane_id();
+  const unsigned d = win ? deg : 0u;
+  const unsigned incl = warp_incl_scan(d);
+  const unsigned total = __shfl_sync(kFull, incl, 31);
+  const unsigned cnt = __popc(mask);
+  unsigned long long base = 0;
+  if (lane == 0)
+    base = atomicAdd(&out->packed, ((unsigned long long)cnt << 33) | (unsigned long long)total);
+  base = __shfl_sync(kFull, base, 0);
+  if (win) {
+    const unsigned rank = __popc(mask & ((1u << lane) - 1u));
+    const unsigned pos = out_base + (unsigned)(base >> 33) + rank;
+    const unsigned pre = (unsigned)(base & kEdgeMask) + (incl - d);
+    st_plain(F + pos, make_int4(col, root, (int)beg, (int)pre));
+    st_plain(FR + pos, row);
+  }
+}
+
+__device__ __forceinline__ void push_row(bool flag, int row, unsigned* counter, int* list) {
+  const unsigned mask = __ballot_sync(kFull, flag);
+  if (mask == 0) return;
+  const unsigned lane = lane_id();
+  unsigned base = 0;
+  if (lane == 0) base = atomicAdd(counter, (unsigned)__popc(mask));
+  base = __shfl_sync(kFull, base, 0);
+  if (flag) st_plain(list + base + __popc(mask & ((1u << lane) - 1u)), row);
+}
+
+// ---------------------------------------------------------------------------
+// One BFS level (GPUBFS, Alg. 2, gpu_match.cpp:42-70; GPUBFS-WR, Alg. 4,
+// gpu_match.cpp:99-133), over the frontier F[ls, ls+n) holding T edges.
+template <bool WR, bool IMP>
+__device__ void expand_level(const Params& p, Smem& sm, int4* F, unsigned ls,
+                             unsigned n, unsigned T, Slot* in, Slot* out, int level, int pf) {
+  if (T == 0) return;
+  const unsigned tid = threadIdx.x;
+  unsigned c_trav = 0, c_cexp = 0, c_nvis = 0, c_entries = 0;
+  const unsigned long long G = gridDim.x;
+  unsigned long long per = (T + 2 * G - 1) / (2 * G);
+  per = ((per + kThreads - 1) / kThreads) * kThreads;
+  if (per < (unsigned long long)kThreads) per = kThreads;
+  if (per > (unsigned long long)kThreads * kItems * 4) per = (unsigned long long)kThreads * kItems * 4;
+  const unsigned ET = (unsigned)per;
+  const unsigned ntiles = (unsigned)((T + (unsigned long long)ET - 1) / ET);
+  const unsigned out_base = ls + n;
+  unsigned* const path_flag = &p.ctl->path_found[pf];
+
+  for (;;) {
+    if (tid == 0) sm.tile = atomicAdd(&in->tile, 1u);
+    __syncthreads();
+    const unsigned tile = sm.tile;
+    __syncthreads();
+    if (tile >= ntiles) break;
+    const unsigned e0 = tile * ET;
+    const unsigned e1 = (T - e0 < ET) ? T : e0 + ET;
+
+    // Cooperative 512-ary search for the entry holding edge e0 (<= 3 rounds
+    // for 1e8 entries): the last i with prefix(i) <= e0.
+    unsigned lo = 0, hi = n;
+    while (hi - lo > 1) {
+      const unsigned stride = (hi - lo + kThreads - 1) / kThreads;
+      const unsigned idx = lo + tid * stride;
+      const bool ok = idx < hi && ld_cg_u(F + ls + idx) <= e0;
+      const int k = __syncthreads_count(ok);
+      lo = lo + (unsigned)(k - 1) * stride;
+      hi = min(lo + stride, hi);
+    }
+
+    unsigned i = lo;
+    unsigned e = e0;
+    while (e < e1) {
+      // Window of up to kThreads entries starting at i.
+      const unsigned wi = i + tid;
+      if (wi < n) {
+        const int4 ent = ld_cg(F + ls + wi);
+        bool skip = false;
+        if (WR) skip = ld_rlx(p.bfs + ent.y) < kUnvisited;  // early exit (gpu_match.cpp:106-108)
+        sm.col[tid] = ent.x;
+        sm.root[tid] = skip ? -1 : ent.y;
+        sm.beg[tid] = (unsigned)ent.z;
+        sm.pre[tid] = (unsigned)ent.w;
+        if ((unsigned)ent.w >= e0 && (unsigned)ent.w < e1) {
+          c_entries++;
+          if (!skip) c_cexp++;
+        }
+      } else {
+        sm.pre[tid] = T;
+        sm.root[tid] = -1;
+      }
+      if (tid == 0) sm.pre[kThreads] = (i + kThreads < n) ? ld_cg_u(F + ls + i + kThreads) : T;
+      __syncthreads();
+      const unsigned wend = min(e1, sm.pre[kThreads]);
+
+      for (unsigned base = e; base < wend; base += kThreads * kItems) {
+        int row[kItems], cm[kItems], sl[kItems];
+        unsigned w[kItems];
+#pragma unroll
+        for (int k = 0; k < kItems; ++k) {
+          const unsigned ee = base + k * kThreads + tid;
+          row[k] = -1;
+          sl[k] = 0;
+          if (ee < wend) {
+            int a = 0, b = kThreads;
+            while (b - a > 1) {
+              const int mid = (a + b) >> 1;
+              if (sm.pre[mid] <= ee) a = mid; else b = mid;
+            }
+            sl[k] = a;
+            if (!WR || sm.root[a] >= 0) {
+              row[k] = ld_ro(p.adj + sm.beg[a] + (ee - sm.pre[a]));
+              c_trav++;
+            }
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < kItems; ++k) cm[k] = row[k] >= 0 ? ld_rlx(p.rmatch + row[k]) : -3;
+#pragma unroll
+        for (int k = 0; k < kItems; ++k) w[k] = cm[k] >= 0 ? ld_rlx(p.vis + (cm[k] >> 5)) : kFull;
+#pragma unroll
+        for (int k = 0; k < kItems; ++k) {
+          bool win = false, ep = false;
+          const int c = cm[k];
+          if (c >= 0) {
+            const unsigned bit = 1u << (c & 31);
+            if (!(w[k] & bit)) {
+              const unsigned old = atomicOr(p.vis + (c >> 5), bit);
+              win = !(old & bit);
+            }
+          } else if (c == -1) {
+            ep = atomicCAS(p.rmatch + row[k], -1, -2) == -1;
+          }
+          const int col = sm.col[sl[k]];
+          const int root = WR ? sm.root[sl[k]] : col;
+          unsigned nbeg = 0, ndeg = 0;
+          if (win) {
+            st_plain(p.pred + row[k], col);
+            st_plain(p.bfs + c, level + 1);
+            nbeg = ld_ro(p.offs + c);
+            ndeg = ld_ro(p.offs + c + 1) - nbeg;
+            c_nvis++;
+          }
+          push_entries(win, c, root, nbeg, ndeg, row[k], out, F, p.FR, out_base);
+          if (ep) {
+            st_plain(p.pred + row[k], col);
+            if (WR) st_rlx(p.bfs + root, IMP ? -row[k] : kFoundMark);
+            if (ld_rlx(path_flag) == 0u) st_rlx(path_flag, 1u);
+          }
+          push_row(ep, row[k], &p.ctl->n_ep, p.EP);
+        }
+      }
+      e = wend;
+      i += kThreads;
+      __syncthreads();
+    }
+  }
+  flush_count(sm, kStTrav, c_trav);
+  flush_count(sm, kStCexp, c_cexp);
+  flush_count(sm, kStNvis, c_nvis);
+  flush_count(sm, kStEntries, c_entries);
+}
+
+// ALTERNATE walk (gpu_match.cpp:144-154): swap pairs toward the root, break
+// on a column another walk already claimed this phase.
+__device__ __forceinline__ void alternate_walk(const Params& p, unsigned& walks, unsigned& nsteps, int row) {
+  long long steps = 0;
+  while (row != -1) {
+    const int col = ld_cg(p.pred + row);
+    if (col < 0) break;
+    const int mr = ld_rlx(p.cmatch + col);
+    if (mr >= 0 && ld_cg(p.pred + mr) == col) break;
+    st_rlx(p.cmatch + col, row);
+    st_rlx(p.rmatch + row, col);
+    row = mr;
+    if (++steps > p.nc) {
+      p.ctl->error = kErrWalk;
+      break;
+    }
+  }
+  nsteps += (unsigned)steps;
+  walks++;
+}
+
+__device__ __forceinline__ void fix_row(const Params& p, unsigned& resets, int r) {
+  const int v = ld_cg(p.rmatch + r);
+  if (v == -2) {
+    st_plain(p.rmatch + r, -1);
+    resets++;
+  } else if (v >= 0 && ld_cg(p.cmatch + v) != r) {
+    st_plain(p.rmatch + r, -1);
+    resets++;
+  }
+  st_plain(p.pred + r, -1);
+}
+
+struct PhaseOut {
+  bool found;
+  long long launches;
+  long long after;
+};
+
+// One phase = run_phase (gpu_match.cpp:268-302) from the roots in F[cur].
+template <bool WR, bool IMP>
+__device__ PhaseOut run_phase(const Params& p, Smem& sm, int cur, int parity,
+                              bool serial_alt, long long isolated) {
+  Ctrl* ctl = p.ctl;
+  int4* F = cur ? p.F1 : p.F0;
+  int4* Fn = cur ? p.F0 : p.F1;
+  PhaseOut out{false, 0, 0};
+
+  // ---- BFS level loop (expand_bfs, gpu_match.cpp:247-266) ----
+  const unsigned long long rp = ld_rlx(&ctl->roots.packed);
+  const unsigned n0 = (unsigned)(rp >> 33);
+  unsigned n = n0;
+  unsigned T = (unsigned)(rp & kEdgeMask);
+  unsigned ls = 0;
+  unsigned n_next = 0;
+  int lv = 0;
+  bool found = false;
+  for (;;) {
+    Slot* in = lv == 0 ? &ctl->roots : &ctl->lvl[lv % 3];
+    Slot* outs = &ctl->lvl[(lv + 1) % 3];
+    if (is_leader() && lv >= 1) {
+      Slot* z = &ctl->lvl[(lv + 2) % 3];
+      z->packed = 0;
+      z->tile = 0;
+    }
+    expand_level<WR, IMP>(p, sm, F, ls, n, T, in, outs, kStartLevel + lv, parity);
+    grid_sync(ctl);
+    out.launches++;
+    const unsigned long long op = ld_rlx(&outs->packed);
+    n_next = (unsigned)(op >> 33);
+    found = ld_rlx(&ctl->path_found[parity]) != 0u;
+    if (p.apsb && found) break;
+    if (n_next == 0) break;
+    ls += n;
+    n = n_next;
+    T = (unsigned)(op & kEdgeMask);
+    ++lv;
+    if (lv > p.nc + 2) {
+      if (is_leader()) ctl->error = kErrLevels;
+      break;
+    }
+  }
+  const unsigned nvis = ls + n + n_next;  // every column claimed this phase
+  out.found = found;
+  if (p.stop_after_bfs) return out;
+
+  // ---- ALTERNATE (gpu_match.cpp:158-218) ----
+  if (is_leader()) ctl->path_found[parity ^ 1] = 0u;  // flag of the next phase
+  const unsigned n_ep = ld_rlx(&ctl->n_ep);
+  unsigned walks = 0, steps = 0, resets = 0;
+  if (!serial_alt) {
+    if (!IMP) {
+      for (unsigned long long k = global_thread(); k < n_ep; k += global_threads())
+        alternate_walk(p, walks, steps, ld_cg(p.EP + k));
+    } else {
+      for (unsigned long long k = global_thread(); k < n0; k += global_threads()) {
+        const int c = ld_cg(reinterpret_cast<const int*>(F + k));
+        const int mark = ld_rlx(p.bfs + c);
+        if (mark <= 0) alternate_walk(p, walks, steps, -mark);  // live levels are >= 1 (L0 = 2)
+      }
+    }
+  } else if (is_leader()) {
+    // Serial retry (gpu_match.cpp:328-343): one thread walks every endpoint
+    // in turn; the first walk cannot meet a claimed column, so the phase
+    // always augments when a path exists.
+    if (!IMP) {
+      for (unsigned k = 0; k < n_ep; ++k) alternate_walk(p, walks, steps, ld_cg(p.EP + k));
+    } else {
+      for (unsigned k = 0; k < n0; ++k) {
+        const int c = ld_cg(reinterpret_cast<const int*>(F + k));
+        const int mark = ld_rlx(p.bfs + c);
+        if (mark <= 0) alternate_walk(p, walks, steps, -mark);
+      }
+    }
+  }
+  flush_count(sm, kStWalks, walks);
+  flush_count(sm, kStSteps, steps);
+  grid_sync(ctl);
+
+  // ---- FIXMATCHING rows (rules 1 and 2), restricted to touched rows ----
+  for (unsigned long long k = global_thread(); k < nvis; k += global_threads()) {
+    const int r = ld_cg(p.FR + k);
+    if (r >= 0) fix_row(p, resets, r);
+  }
+  for (unsigned long long k = global_thread(); k < n_ep; k += global_threads())
+    fix_row(p, resets, ld_cg(p.EP + k));
+  for (unsigned long long k = global_thread(); k < (unsigned long long)p.nvis_words; k += global_threads())
+    st_plain(reinterpret_cast<int*>(p.vis) + k, 0);
+  if (is_leader()) {
+    for (int s = 0; s < 3; ++s) {
+      ctl->lvl[s].packed = 0;
+      ctl->lvl[s].tile = 0;
+    }
+    ctl->roots.packed = 0;
+    ctl->roots.tile = 0;
+  }
+  grid_sync(ctl);
+
+  // ---- FIXMATCHING columns (rule 3) + next phase's roots and bfs init ----
+  const unsigned wtotal = gridDim.x * (kThreads / 32);
+  const unsigned wid = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
+  for (unsigned long long b = (unsigned long long)wid * 32; b < nvis; b += (unsigned long long)wtotal * 32) {
+    const unsigned long long k = b + lane_id();
+    bool unmatched = false;
+    int c = 0;
+    unsigned beg = 0, deg = 0;
+    if (k < nvis) {
+      c = ld_cg(reinterpret_cast<const int*>(F + k));
+      int r = ld_cg(p.cmatch + c);
+      if (r >= 0 && ld_cg(p.rmatch + r) != c) {
+        st_plain(p.cmatch + c, -1);
+        resets++;
+        r = -1;
+      }
+      st_plain(p.bfs + c, r >= 0 ? kUnvisited : kStartLevel);  // init_bfs_array for next phase
+      if (r < 0) {
+        unmatched = true;
+        beg = ld_ro(p.offs + c);
+        deg = ld_ro(p.offs + c + 1) - beg;
+      }
+    }
+    push_entries(unmatched, c, c, beg, deg, -1, &ctl->roots, Fn, p.FR, 0u);
+  }
+  if (is_leader()) ctl->n_ep = 0u;
+  flush_count(sm, kStResets, resets);
+  grid_sync(ctl);
+  const unsigned long long np = ld_rlx(&ctl->roots.packed);
+  out.after = (long long)p.nc - isolated - (long long)(np >> 33);
+  return out;
+}
+
+// ---------------------------------------------------------------------------
+template <bool WR, bool IMP>
+__global__ void __launch_bounds__(kThreads, 2) driver_kernel(Params p) {
+  __shared__ Smem sm;
+  Ctrl* ctl = p.ctl;
+  if (threadIdx.x < kNumStats) sm.cnt[threadIdx.x] = 0;
+  __syncthreads();
+
+  int cur;
+  long long card, outer, isolated;
+  int recs = 0;
+
+  if (p.fresh) {
+    // ---- optional GPU initial matching (parallel first-fit with CAS) ----
+    if (p.init_mode != BM_INIT_GIVEN) {
+      for (int pass = (p.init_mode == BM_INIT_GPU_KS ? 0 : 1); pass < 2; ++pass) {
+        for (unsigned long long c = global_thread(); c < (unsigned long long)p.nc; c += global_threads()) {
+          if (ld_cg(p.cmatch + c) != -1) continue;
+          const unsigned b = ld_ro(p.offs + c), e = ld_ro(p.offs + c + 1);
+          if (pass == 0 && e - b != 1) continue;  // one-sided Karp-Sipser: degree-1 columns first
+          for (unsigned j = b; j < e; ++j) {
+            const int r = ld_ro(p.adj + j);
+            if (ld_rlx(p.rmatch + r) == -1 && atomicCAS(p.rmatch + r, -1, (int)c) == -1) {
+              st_plain(p.cmatch + c, r);
+              break;
+            }
+          }
+        }
+        grid_sync(ctl);
+      }
+    }
+    // ---- setup: validate init, bfs_array init, roots of phase 1 ----
+    unsigned long long bad = 0, iso = 0;
+    const unsigned wtotal = gridDim.x * (kThreads / 32);
+    const unsigned wid = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
+    for (unsigned long long b = (unsigned long long)wid * 32; b < (unsigned long long)p.nc;
+         b += (unsigned long long)wtotal * 32) {
+      const unsigned long long c = b + lane_id();
+      bool root = false;
+      unsigned beg = 0, deg = 0;
+      if (c < (unsigned long long)p.nc) {
+        const int r = ld_cg(p.cmatch + c);
+        if (r < -1 || r >= p.nr) bad++;
+        else if (r >= 0 && ld_cg(p.rmatch + r) != (int)c) bad++;
+        st_plain(p.bfs + c, r >= 0 ? kUnvisited : kStartLevel);
+        if (r < 0) {
+          beg = ld_ro(p.offs + c);
+          deg = ld_ro(p.offs + c + 1) - beg;
+          if (deg > 0) root = true; else iso++;
+        }
+      }
+      push_entries(root, (int)c, (int)c, beg, deg, -1, &ctl->roots, p.F0, p.FR, 0u);
+    }
+    for (unsigned long long r = global_thread(); r < (unsigned long long)p.nr; r += global_threads()) {
+      const int v = ld_cg(p.rmatch + r);
+      if (v < -1 || v >= p.nc) bad++;
+      else if (v >= 0 && ld_cg(p.cmatch + v) != (int)r) bad++;
+    }
+    bad = warp_sum(bad);
+    iso = warp_sum(iso);
+    if (lane_id() == 0) {
+      if (bad) atomicAdd(&ctl->invalid, bad);
+      if (iso) atomicAdd(&ctl->isolated, iso);
+    }
+    grid_sync(ctl);
+    if (ld_rlx(&ctl->invalid) != 0ull) {
+      if (is_leader()) ctl->error = kErrInvalidInit;
+      return;
+    }
+    isolated = (long long)ld_rlx(&ctl->isolated);
+    cur = 0;
+    card = (long long)p.nc - isolated - (long long)(ld_rlx(&ctl->roots.packed) >> 33);
+    outer = 0;
+    if (is_leader()) {
+      ctl->init_card = card;
+      ctl->isolated_cols = isolated;
+    }
+  } else {
+    cur = ctl->cur;
+    card = ctl->card;
+    outer = ctl->outer;
+    isolated = ctl->isolated_cols;
+  }
+  int parity = ctl->phase_parity;
+  if (p.fresh) parity = 0;
+
+  // ---- driver loop (run_driver, gpu_match.cpp:306-359) ----
+  bool done = false;
+  for (;;) {
+    if (outer + 1 > p.phase_bound) {
+      if (is_leader()) ctl->error = kErrBound;
+      break;
+    }
+    ++outer;
+    const long long before = card;
+    PhaseOut ph = run_phase<WR, IMP>(p, sm, cur, parity, false, isolated);
+    if (p.stop_after_bfs) {
+      if (is_leader()) {
+        ctl->bfs_levels_last = ph.launches;
+        ctl->path_found_last = ph.found ? 1 : 0;
+      }
+      done = true;
+      break;
+    }
+    cur ^= 1;
+    parity ^= 1;
+    long long launches = ph.launches;
+    long long after = ph.after;
+    bool retried = false;
+    if (ph.found && after <= before) {
+      PhaseOut rt = run_phase<WR, IMP>(p, sm, cur, parity, true, isolated);
+      cur ^= 1;
+      parity ^= 1;
+      launches += rt.launches;
+      after = rt.after;
+      ph.found = rt.found;
+      retried = true;
+    }
+    if (is_leader()) {
+      if (recs < p.rec_cap) {
+        PhaseRec r;
+        r.launches = launches;
+        r.before = before;
+        r.after = after;
+        r.found = ph.found ? 1 : 0;
+        r.retry = retried ? 1 : 0;
+        p.recs[recs] = r;
+      }
+      sm.cnt[kStLevels] += (unsigned long long)launches;
+      if (retried) sm.cnt[kStRetries]++;
+    }
+    ++recs;
+    card = after;
+    if (!ph.found) {
+      done = true;
+      break;
+    }
+    if (ld_rlx((const unsigned*)&ctl->error) != 0u) break;
+    if (recs >= p.max_phases || recs >= p.rec_cap) break;
+  }
+
+  // ---- flush counters and run state ----
+  __syncthreads();
+  if (threadIdx.x < kNumStats && sm.cnt[threadIdx.x]) atomicAdd(&ctl->stats[threadIdx.x], sm.cnt[threadIdx.x]);
+  if (is_leader()) {
+    ctl->cur = cur;
+    ctl->card = card;
+    ctl->outer = outer;
+    ctl->done = done ? 1 : 0;
+    ctl->n_recs = recs < p.rec_cap ? recs : p.rec_cap;
+    ctl->phase_parity = parity;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Upload-time validation (check_csr, csr_graph.cpp:45-64) and offset narrowing.
+__global__ void convert_offsets_kernel(const long long* in, unsigned* out, int nc, long long E,
+                                       unsigned long long* bad) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i <= nc;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long v = in[i];
+    bool ok = v >= 0 && v <= E;
+    if (i == 0 && v != 0) ok = false;
+    if (i == nc && v != E) ok = false;
+    if (i > 0 && in[i - 1] > v) ok = false;
+    if (!ok) atomicAdd(bad, 1ull);
+    out[i] = (unsigned)v;
+  }
+}
+
+// One warp per column: row range and strict ascending order (sortedness is
+// recorded, not required — the verifier falls back to a linear scan).
+__global__ void check_adj_kernel(const unsigned* offs, const int* adj, int nc, int nr,
+                                 unsigned long long* bad_range, unsigned long long* unsorted) {
+  const long long warps = (long long)gridDim.x * blockDim.x / 32;
+  const int lane = threadIdx.x & 31;
+  for (long long c = (blockIdx.x * (long long)blockDim.x + threadIdx.x) / 32; c < nc; c += warps) {
+    const unsigned b = offs[c], e = offs[c + 1];
+    unsigned long long br = 0, us = 0;
+    for (unsigned j = b + lane; j < e; j += 32) {
+      const int r = adj[j];
+      if (r < 0 || r >= nr) br++;
+      if (j > b && adj[j - 1] >= r) us++;
+    }
+    br = warp_sum(br);
+    us = warp_sum(us);
+    if (lane == 0) {
+      if (br) atomicAdd(bad_range, br);
+      if (us) atomicAdd(unsorted, us);
+    }
+  }
+}
+
+// Validity half of the Berge certificate (validate, matching.cpp:70-104).
+__global__ void validate_kernel(const unsigned* offs, const int* adj, int nc, int nr, int sorted,
+                                const int* rmatch, const int* cmatch,
+                                unsigned long long* violations, unsigned long long* matched) {
+  const long long tot = (long long)gridDim.x * blockDim.x;
+  unsigned long long bad = 0, m = 0;
+  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < nr; r += tot) {
+    const int c = rmatch[r];
+    if (c == -1) continue;
+    if (c < 0 || c >= nc) { bad++; continue; }  // -2 pending flag or out of range
+    if (cmatch[c] != (int)r) { bad++; continue; }
+    const unsigned b = offs[c], e = offs[c + 1];
+    bool has = false;
+    if (sorted) {
+      unsigned lo = b, hi = e;
+      while (lo < hi) {
+        const unsigned mid = lo + ((hi - lo) >> 1);
+        const int v = adj[mid];
+        if (v == (int)r) { has = true; break; }
+        if (v < (int)r) lo = mid + 1; else hi = mid;
+      }
+    } else {
+      for (unsigned j = b; j < e && !has; ++j) has = adj[j] == (int)r;
+    }
+    if (!has) bad++; else m++;
+  }
+  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < nc; c += tot) {
+    const int r = cmatch[c];
+    if (r == -1) continue;
+    if (r < 0 || r >= nr) { bad++; continue; }
+    if (rmatch[r] != (int)c) bad++;
+  }
+  bad = warp_sum(bad);
+  m = warp_sum(m);
+  if ((threadIdx.x & 31) == 0) {
+    if (bad) atomicAdd(violations, bad);
+    if (m) atomicAdd(matched, m);
+  }
+}
+
+}  // namespace bm
+
+// ===========================================================================
+// Host side: the C ABI.
+// ===========================================================================
+using namespace bm;
+
+namespace {
+
+thread_local std::string g_err;
+
+bm_status fail(bm_status s, const std::string& msg) {
+  g_err = msg;
+  return s;
+}
+
+bm_status cuda_fail(cudaError_t e, const char* what) {
+  const bm_status s = (e == cudaErrorMemoryAllocation) ? BM_ERR_OOM : BM_ERR_CUDA;
+  return fail(s, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define BM_CUDA(call)                                 \
+  do {                                                \
+    cudaError_t e_ = (call);                          \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
+  } while (0)
+
+template <typename T>
+void dfree(T*& p) {
+  if (p) cudaFree(p);
+  p = nullptr;
+}
+
+template <typename T>
+cudaError_t dalloc(T*& p, size_t count) {
+  dfree(p);
+  return cudaMalloc(reinterpret_cast<void**>(&p), std::max<size_t>(count, 1) * sizeof(T));
+}
+
+}  // namespace
+
+void bm_internal_set_error(const std::string& msg) { g_err = msg; }
+
+struct bm_handle {
+  int device = 0;
+  cudaStream_t own = nullptr;
+  cudaStream_t stream = nullptr;
+  int sms = 0;
+  int bps[3] = {0, 0, 0};  // co-resident CTAs per SM, per kernel variant
+  // graph
+  int nc = -1, nr = -1;
+  long long E = 0;
+  int sorted = 1;
+  unsigned* offs = nullptr;
+  int* adj = nullptr;
+  // state
+  int *rmatch = nullptr, *cmatch = nullptr, *pred = nullptr, *bfs = nullptr;
+  int *rmatch0 = nullptr, *cmatch0 = nullptr, *FR = nullptr, *EP = nullptr;
+  unsigned* vis = nullptr;
+  int nvis_words = 0;
+  int4* F[2] = {nullptr, nullptr};
+  Ctrl* ctl = nullptr;
+  PhaseRec* recs = nullptr;
+  int rec_cap = 4096;
+  bool has_init = false;
+  bool clean = false;   // pred == -1 and vis == 0 everywhere
+  bool resumable = false;
+  bm_match_opts run_opts{};
+  std::vector<long long> phase_launches;  // per outer iteration, current run
+  unsigned long long *scratch = nullptr;  // small device counters
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  double last_ms = 0.0;
+  int last_launches = 0;
+};
+
+namespace {
+
+bm_status check_handle(bm_handle* h, bool need_graph) {
+  if (!h) return fail(BM_ERR_INVALID_ARG, "null handle");
+  if (need_graph && h->nc < 0) return fail(BM_ERR_INVALID_ARG, "no graph uploaded (call bm_upload_csc first)");
+  return BM_OK;
+}
+
+bm_status check_opts(const bm_match_opts* o) {
+  if (!o) return fail(BM_ERR_INVALID_ARG, "null options");
+  if (o->driver != BM_DRIVER_APFB && o->driver != BM_DRIVER_APSB)
+    return fail(BM_ERR_INVALID_ARG, "unknown driver");
+  if (o->bfs_kernel != BM_BFS_GPUBFS && o->bfs_kernel != BM_BFS_WR)
+    return fail(BM_ERR_INVALID_ARG, "unknown bfs kernel");
+  if (o->init < BM_INIT_GIVEN || o->init > BM_INIT_GPU_KS)
+    return fail(BM_ERR_INVALID_ARG, "unknown init mode");
+  if (o->max_phases < 0) return fail(BM_ERR_INVALID_ARG, "max_phases must be >= 0");
+  // gpu_match.cpp:272-274
+  if (o->improved && o->bfs_kernel != BM_BFS_WR)
+    return fail(BM_ERR_LOGIC, "the endpoint-encoded alternation requires the with-root kernel");
+  return BM_OK;
+}
+
+int variant_of(int wr, int imp) { return wr ? (imp ? 2 : 1) : 0; }
+
+const void* kernel_ptr(int v) {
+  switch (v) {
+    case 0: return reinterpret_cast<const void*>(&driver_kernel<false, false>);
+    case 1: return reinterpret_cast<const void*>(&driver_kernel<true, false>);
+    default: return reinterpret_cast<const void*>(&driver_kernel<true, true>);
+  }
+}
+
+int grid_for(bm_handle* h, int v) {
+  const long long maxg = (long long)h->sms * std::max(1, h->bps[v]);
+  const long long work = std::max<long long>({(long long)h->nc, (long long)h->nr, h->E / 8, 1});
+  const long long want = (work + kThreads - 1) / kThreads;
+  return (int)std::max<long long>(1, std::min(maxg, want));
+}
+
+// Resets pred/vis when a previous call left them dirty, and the control block.
+bm_status prepare_fresh(bm_handle* h) {
+  if (!h->clean) {
+    BM_CUDA(cudaMemsetAsync(h->pred, 0xff, sizeof(int) * std::max(h->nr, 1), h->stream));
+    BM_CUDA(cudaMemsetAsync(h->vis, 0, sizeof(unsigned) * std::max(h->nvis_words, 1), h->stream));
+  }
+  BM_CUDA(cudaMemsetAsync(h->ctl, 0, sizeof(Ctrl), h->stream));
+  h->clean = false;
+  return BM_OK;
+}
+
+bm_status launch(bm_handle* h, int v, Params& p, float* ms) {
+  const int G = grid_for(h, v);
+  void* args[] = {&p};
+  BM_CUDA(cudaEventRecord(h->ev0, h->stream));
+  BM_CUDA(cudaLaunchCooperativeKernel(kernel_ptr(v), dim3(G), dim3(kThreads), args, 0, h->stream));
+  BM_CUDA(cudaEventRecord(h->ev1, h->stream));
+  BM_CUDA(cudaStreamSynchronize(h->stream));
+  BM_CUDA(cudaEventElapsedTime(ms, h->ev0, h->ev1));
+  return BM_OK;
+}
+
+Params make_params(bm_handle* h, const bm_match_opts& o) {
+  Params p{};
+  p.nc = h->nc;
+  p.nr = h->nr;
+  p.offs = h->offs;
+  p.adj = h->adj;
+  p.rmatch = h->rmatch;
+  p.cmatch = h->cmatch;
+  p.pred = h->pred;
+  p.bfs = h->bfs;
+  p.vis = h->vis;
+  p.nvis_words = h->nvis_words;
+  p.F0 = h->F[0];
+  p.F1 = h->F[1];
+  p.FR = h->FR;
+  p.EP = h->EP;
+  p.ctl = h->ctl;
+  p.recs = h->recs;
+  p.rec_cap = h->rec_cap;
+  p.apsb = o.driver == BM_DRIVER_APSB;
+  p.init_mode = o.init;
+  p.fresh = 1;
+  p.max_phases = h->rec_cap;
+  p.stop_after_bfs = 0;
+  p.phase_bound = (long long)h->nc + 1;
+  return p;
+}
+
+bm_status ctl_error_status(int err) {
+  switch (err) {
+    case kErrNone: return BM_OK;
+    case kErrBound:
+      return fail(BM_ERR_BOUND_EXCEEDED, "termination bound exceeded: more than nc + 1 phases");
+    case kErrInvalidInit:
+      return fail(BM_ERR_INVALID_ARG,
+                  "initial matching is not a clean valid matching (pending -2, out of range or asymmetric)");
+    case kErrBarrier: return fail(BM_ERR_CUDA, "grid barrier watchdog fired");
+    case kErrWalk: return fail(BM_ERR_CUDA, "ALTERNATE walk exceeded nc steps");
+    case kErrLevels: return fail(BM_ERR_CUDA, "BFS exceeded nc + 2 levels");
+    default: return fail(BM_ERR_CUDA, "unknown device error " + std::to_string(err));
+  }
+}
+
+// Shared by bm_run/bm_resume/bm_match: runs launches until done, the phase
+// budget is spent, or the observer aborts.
+bm_status drive(bm_handle* h, const bm_match_opts& o, bool fresh, int64_t* cardinality,
+                bm_counters* counters, int64_t* per_iter, int64_t cap, bm_phase_cb cb, void* user,
+                int32_t* done_out) {
+  const int v = variant_of(o.bfs_kernel == BM_BFS_WR, o.improved);
+  Params p = make_params(h, o);
+  p.fresh = fresh ? 1 : 0;
+  if (fresh) {
+    h->phase_launches.clear();
+    h->last_ms = 0.0;
+    h->last_launches = 0;
+  }
+  long long budget = o.max_phases > 0 ? o.max_phases : -1;
+  std::vector<PhaseRec> recs;
+  std::vector<int> snap_r, snap_c;
+  Ctrl ctl{};
+  bool done = false;
+  for (;;) {
+    int this_launch = cb ? 1 : h->rec_cap;
+    if (budget >= 0) this_launch = (int)std::min<long long>(this_launch, budget);
+    if (this_launch <= 0) break;
+    p.max_phases = this_launch;
+    float ms = 0.f;
+    bm_status s = launch(h, v, p, &ms);
+    if (s != BM_OK) return s;
+    h->last_ms += ms;
+    h->last_launches += 1;
+    BM_CUDA(cudaMemcpy(&ctl, h->ctl, sizeof(Ctrl), cudaMemcpyDeviceToHost));
+    if (ctl.error) {
+      h->resumable = false;
+      return ctl_error_status(ctl.error);
+    }
+    recs.resize(ctl.n_recs);
+    if (ctl.n_recs > 0)
+      BM_CUDA(cudaMemcpy(recs.data(), h->recs, sizeof(PhaseRec) * ctl.n_recs, cudaMemcpyDeviceToHost));
+    for (int i = 0; i < ctl.n_recs; ++i) {
+      h->phase_launches.push_back(recs[i].launches);
+      if (cb) {
+        snap_r.resize(h->nr);
+        snap_c.resize(h->nc);
+        BM_CUDA(cudaMemcpy(snap_r.data(), h->rmatch, sizeof(int) * h->nr, cudaMemcpyDeviceToHost));
+        BM_CUDA(cudaMemcpy(snap_c.data(), h->cmatch, sizeof(int) * h->nc, cudaMemcpyDeviceToHost));
+        bm_phase_event ev{};
+        ev.iteration = (int64_t)h->phase_launches.size();
+        ev.augmenting_path_found = recs[i].found;
+        ev.serial_retry = recs[i].retry;
+        ev.cardinality_before = recs[i].before;
+        ev.cardinality_after = recs[i].after;
+        ev.bfs_launches = recs[i].launches;
+        ev.rmatch = snap_r.data();
+        ev.nr = h->nr;
+        ev.cmatch = snap_c.data();
+        ev.nc = h->nc;
+        if (cb(&ev, user) != 0) {
+          h->resumable = false;
+          return fail(BM_ERR_INVALID_ARG, "aborted by observer");
+        }
+      }
+    }
+    if (budget >= 0) budget -= ctl.n_recs;
+    if (ctl.done) {
+      done = true;
+      break;
+    }
+    p.fresh = 0;
+    // Each relaunch resets the per-launch record counter; stats accumulate.
+    BM_CUDA(cudaMemsetAsync(&h->ctl->n_recs, 0, sizeof(int), h->stream));
+  }
+  h->resumable = !done;
+  h->run_opts = o;
+  h->clean = true;  // every completed phase leaves pred == -1 and vis == 0
+  if (cardinality) *cardinality = ctl.card;
+  if (done_out) *done_out = done ? 1 : 0;
+  if (counters) {
+    std::memset(counters, 0, sizeof(*counters));
+    counters->outer_iterations = (int64_t)h->phase_launches.size();
+    long long lt = 0;
+    for (long long x : h->phase_launches) lt += x;
+    counters->bfs_launches_total = lt;
+    counters->columns_scanned = (int64_t)ctl.stats[kStCexp];
+    counters->alternations_attempted = (int64_t)ctl.stats[kStWalks];
+    counters->fix_resets = (int64_t)ctl.stats[kStResets];
+    counters->serial_retries = (int64_t)ctl.stats[kStRetries];
+    counters->edges_traversed = (int64_t)ctl.stats[kStTrav];
+    counters->columns_visited = (int64_t)ctl.stats[kStNvis];
+    counters->walk_steps = (int64_t)ctl.stats[kStSteps];
+    counters->frontier_entries = (int64_t)ctl.stats[kStEntries];
+    counters->cardinality = ctl.card;
+    counters->initial_cardinality = ctl.init_card;
+    counters->n_phase_records = (int64_t)std::min<size_t>(h->phase_launches.size(), cap > 0 ? (size_t)cap : 0);
+  }
+  if (per_iter && cap > 0) {
+    const size_t k = std::min<size_t>(h->phase_launches.size(), (size_t)cap);
+    for (size_t i = 0; i < k; ++i) per_iter[i] = h->phase_launches[i];
+  }
+  return BM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t bm_abi_version(void) { return BM_ABI_VERSION; }
+
+const char* bm_last_error(void) { return g_err.c_str(); }
+
+const char* bm_status_string(int32_t s) {
+  switch (s) {
+    case BM_OK: return "ok";
+    case BM_ERR_INVALID_ARG: return "invalid argument";
+    case BM_ERR_LOGIC: return "logic error";
+    case BM_ERR_BOUND_EXCEEDED: return "termination bound exceeded";
+    case BM_ERR_CUDA: return "cuda error";
+    case BM_ERR_OOM: return "out of device memory";
+    case BM_ERR_NCCL: return "nccl error";
+    default: return "unknown status";
+  }
+}
+
+int32_t bm_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+  return n;
+}
+
+bm_status bm_create(int32_t device, bm_handle** out) {
+  if (!out) return fail(BM_ERR_INVALID_ARG, "null output pointer");
+  *out = nullptr;
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0)
+    return fail(BM_ERR_CUDA, std::string("no CUDA device available (the engine has no CPU fallback): ") +
+                                 (e != cudaSuccess ? cudaGetErrorString(e) : "0 devices"));
+  if (device < 0 || device >= n) return fail(BM_ERR_INVALID_ARG, "device index out of range");
+  BM_CUDA(cudaSetDevice(device));
+  cudaDeviceProp prop{};
+  BM_CUDA(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10)
+    return fail(BM_ERR_CUDA, std::string("device ") + prop.name + " is sm_" + std::to_string(prop.major) +
+                                 std::to_string(prop.minor) + "; this build targets sm_100a (B200)");
+  if (!prop.cooperativeLaunch) return fail(BM_ERR_CUDA, "device does not support cooperative launch");
+  auto* h = new bm_handle();
+  h->device = device;
+  h->sms = prop.multiProcessorCount;
+  for (int v = 0; v < 3; ++v) {
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&h->bps[v], kernel_ptr(v), kThreads, 0);
+    if (e != cudaSuccess || h->bps[v] < 1) {
+      delete h;
+      return fail(BM_ERR_CUDA, std::string("occupancy query failed: ") + cudaGetErrorString(e));
+    }
+  }
+  e = cudaStreamCreateWithFlags(&h->own, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreate(&h->ev0);
+  if (e == cudaSuccess) e = cudaEventCreate(&h->ev1);
+  if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void**>(&h->ctl), sizeof(Ctrl));
+  if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void**>(&h->recs), sizeof(PhaseRec) * h->rec_cap);
+  if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void**>(&h->scratch), sizeof(unsigned long long) * 4);
+  if (e != cudaSuccess) {
+    bm_destroy(h);
+    return cuda_fail(e, "bm_create");
+  }
+  h->stream = h->own;
+  *out = h;
+  return BM_OK;
+}
+
+bm_status bm_destroy(bm_handle* h) {
+  if (!h) return BM_OK;
+  cudaSetDevice(h->device);
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  dfree(h->offs);
+  dfree(h->adj);
+  dfree(h->rmatch);
+  dfree(h->cmatch);
+  dfree(h->pred);
+  dfree(h->bfs);
+  dfree(h->rmatch0);
+  dfree(h->cmatch0);
+  dfree(h->FR);
+  dfree(h->EP);
+  dfree(h->vis);
+  dfree(h->F[0]);
+  dfree(h->F[1]);
+  dfree(h->ctl);
+  dfree(h->recs);
+  dfree(h->scratch);
+  if (h->ev0) cudaEventDestroy(h->ev0);
+  if (h->ev1) cudaEventDestroy(h->ev1);
+  if (h->own) cudaStreamDestroy(h->own);
+  delete h;
+  return BM_OK;
+}
+
+bm_status bm_set_stream(bm_handle* h, void* stream) {
+  bm_status s = check_handle(h, false);
+  if (s != BM_OK) return s;
+  BM_CUDA(cudaSetDevice(h->device));
+  h->stream = stream ? static_cast<cudaStream_t>(stream) : h->own;
+  return BM_OK;
+}
+
+bm_status bm_upload_csc(bm_handle* h, int32_t nc, int32_t nr, const int64_t* cxadj, const int32_t* cadj) {
+  bm_status s = check_handle(h, false);
+  if (s != BM_OK) return s;
+  if (nc < 0 || nr < 0) return fail(BM_ERR_INVALID_ARG, "negative vertex count");
+  if (!cxadj) return fail(BM_ERR_INVALID_ARG, "null cxadj");
+  const long long E = cxadj[nc];
+  if (E < 0) return fail(BM_ERR_INVALID_ARG, "cxadj[nc] is negative");
+  if (E >= (1ll << 32) - 1) return fail(BM_ERR_INVALID_ARG, "edge count must be < 2^32 - 1 in this build");
+  if (E > 0 && !cadj) return fail(BM_ERR_INVALID_ARG, "null cadj");
+  BM_CUDA(cudaSetDevice(h->device));
+  BM_CUDA(cudaStreamSynchronize(h->stream));
+  h->nc = -1;
+  h->has_init = false;
+  h->resumable = false;
+  // graph
+  BM_CUDA(dalloc(h->offs, (size_t)nc + 1));
+  BM_CUDA(dalloc(h->adj, (size_t)E));
+  // state (sized by the graph)
+  BM_CUDA(dalloc(h->rmatch, nr));
+  BM_CUDA(dalloc(h->cmatch, nc));
+  BM_CUDA(dalloc(h->pred, nr));
+  BM_CUDA(dalloc(h->bfs, nc));
+  BM_CUDA(dalloc(h->rmatch0, nr));
+  BM_CUDA(dalloc(h->cmatch0, nc));
+  BM_CUDA(dalloc(h->FR, nc));
+  BM_CUDA(dalloc(h->EP, nr));
+  h->nvis_words = (nc + 31) / 32;
+  BM_CUDA(dalloc(h->vis, h->nvis_words));
+  BM_CUDA(dalloc(h->F[0], nc));
+  BM_CUDA(dalloc(h->F[1], nc));
+  // offsets: int64 staged in F[1] (16 B per column >= 8 B per offset), narrowed to u32
+  long long* staged = reinterpret_cast<long long*>(h->F[1]);
+  BM_CUDA(cudaMemcpyAsync(staged, cxadj, sizeof(long long) * ((size_t)nc + 1), cudaMemcpyHostToDevice, h->stream));
+  if (E > 0)
+    BM_CUDA(cudaMemcpyAsync(h->adj, cadj, sizeof(int) * (size_t)E, cudaMemcpyHostToDevice, h->stream));
+  BM_CUDA(cudaMemsetAsync(h->scratch, 0, sizeof(unsigned long long) * 4, h->stream));
+  const int blocks = std::max(1, std::min(h->sms * 8, (nc + 256) / 256));
+  convert_offsets_kernel<<<blocks, 256, 0, h->stream>>>(staged, h->offs, nc, E, h->scratch);
+  BM_CUDA(cudaGetLastError());
+  unsigned long long bad[3] = {0, 0, 0};
+  BM_CUDA(cudaMemcpyAsync(bad, h->scratch, sizeof(bad), cudaMemcpyDeviceToHost, h->stream));
+  BM_CUDA(cudaStreamSynchronize(h->stream));
+  if (bad[0]) return fail(BM_ERR_INVALID_ARG, "cxadj is not a valid offset array (cxadj[0]=0, non-decreasing, cxadj[nc]=E)");
+  if (nc > 0) {
+    const int wb = std::max(1, std::min(h->sms * 16, (int)(((long long)nc * 32 + 255) / 256)));
+    check_adj_kernel<<<wb, 256, 0, h->stream>>>(h->offs, h->adj, nc, nr, h->scratch + 1, h->scratch + 2);
+    BM_CUDA(cudaGetLastError());
+    BM_CUDA(cudaMemcpyAsync(bad, h->scratch, sizeof(bad), cudaMemcpyDeviceToHost, h->stream));
+    BM_CUDA(cudaStreamSynchronize(h->stream));
+    if (bad[1]) return fail(BM_ERR_INVALID_ARG, "row index out of range in cadj");
+  }
+  h->sorted = bad[2] == 0;
+  BM_CUDA(cudaMemsetAsync(h->pred, 0xff, sizeof(int) * std::max(nr, 1), h->stream));
+  BM_CUDA(cudaMemsetAsync(h->vis, 0, sizeof(unsigned) * std::max(h->nvis_words, 1), h->stream));
+  BM_CUDA(cudaStreamSynchronize(h->stream));
+  h->clean = true;
+  h->nc = nc;
+  h->nr = nr;
+  h->E = E;
+  return BM_OK;
+}
+
+bm_status bm_graph_info(bm_handle* h, int32_t* nc, int32_t* nr, int64_t* nedges) {
+  bm_status s = check_handle(h, true);
+  if (s != BM_OK) return s;
+  if (nc) *nc = h->nc;
+  if (nr) *nr = h->nr;
+  if (nedges) *nedges = h->E;
+  return BM_OK;
+}
+
+bm_status bm_load_matching(bm_handle* h, const int32_t* rmatch, const int32_t* cmatch) {
+  bm_status s = check_handle(h, true);
+  if (s != BM_OK) return s;
+  if ((!rmatch && h->nr > 0) || (!cmatch && h->nc > 0)) return fail(BM_ERR_INVALID_ARG, "null matching array");
+  BM_CUDA(cudaSetDevice(h->device));
+  if (h->nr > 0) BM_CUDA(cudaMemcpyAsync(h->rmatch0, rmatch, sizeof(int) * h->nr, cudaMemcpyHostToDevice, h->stream));
+  if (h->nc > 0) BM_CUDA(cudaMemcpyAsync(h->cmatch0, cmatch, sizeof(int) * h->nc, cudaMemcpyHostToDevice, h->stream));
+  BM_CUDA(cudaStreamSynchronize(h->stream));
+  h->has_init = true;
+  return BM_OK;
+}
+
+bm_status bm_run(bm_handle* h, const bm_match_opts* opts, int64_t* cardinality, bm_counters* counters,
+                 int64_t* per_iter, int64_t cap, bm_phase_cb cb, void* user, int32_t* done) {
+  bm_status s = check_handle(h, true);
+  if (s != BM_OK) return s;
+  s = check_opts(opts);
+  if (s != BM_OK) return s;
+  BM_CUDA(cudaSetDevice(h->device));
+  if (opts->init == BM_INIT_GIVEN) {
+    if (!h->has_init) return fail(BM_ERR_INVALID_ARG, "no initial matching loaded (bm_load_matching)");
+    BM_CUDA(cudaMemcpyAsync(h->rmatch, h->rmatch0, sizeof(int) * std::max(h->nr, 1), cudaMemcpyDeviceToDevice, h->stream));
+    BM_CUDA(cudaMemcpyAsync(h->cmatch, h->cmatch0, sizeof(int) * std::max(h->nc, 1), cudaMemcpyDeviceToDevice, h->stream));
+  } else {
+    BM_CUDA(cudaMemsetAsync(h->rmatch, 0xff, sizeof(int) * std::max(h->nr, 1), h->stream));
+    BM_CUDA(cudaMemsetAsync(h->cmatch, 0xff, sizeof(int) * std::max(h->nc, 1), h->stream));
+  }
+  s = prepare_fresh(h);
+  if (s != BM_OK) return s;
+  return drive(h, *opts, true, cardinality, counters, per_iter, cap, cb, user, done);
+}
+
+bm_status bm_resume(bm_handle* h, const bm_match_opts* opts, int64_t* cardinality, bm_counters* counters,
+                    int64_t* per_iter, int64_t cap, bm_phase_cb cb, void* user, int32_t* done) {
+  bm_status s = check_handle(h, true);
+  if (s != BM_OK) return s;
+  s = check_opts(opts);
+  if (s != BM_OK) return s;
+  if (!h->resumable) return fail(BM_ERR_INVALID_ARG, "nothing to resume");
+  if (opts->driver != h->run_opts.driver || opts->bfs_kernel != h->run_opts.bfs_kernel ||
+      opts->improved != h->run_opts.improved)
+    return fail(BM_ERR_INVALID_ARG, "resume must use the same driver/kernel as the stopped run");
+  BM_CUDA(cudaSetDevice(h->device));
+  BM_CUDA(cudaMemsetAsync(&h->ctl->n_recs, 0, sizeof(int), h->stream));
+  return drive(h, *opts, false, cardinality, counters, per_iter, cap, cb, user, done);
+}
+
+bm_status bm_download_matching(bm_handle* h, int32_t* rmatch, int32_t* cmatch) {
+  bm_status s = check_handle(h, true);
+  if (s != BM_OK) return s;
+  BM_CUDA(cudaSetDevice(h->device));
+  if (rmatch && h->nr > 0) BM_CUDA(cudaMemcpyAsync(rmatch, h->rmatch, sizeof(int) * h->nr, cudaMemcpyDeviceToHost, h->stream));
+  if (cmatch && h->nc > 0) BM_CUDA(cudaMemcpyAsync(cmatch, h->cmatch, sizeof(int) * h->nc, cudaMemcpyDeviceToHost, h->stream));
+  BM_CUDA(cudaStreamSynchronize(h->stream));
+  return BM_OK;
+}
+
+bm_status bm_last_kernel_time(bm_handle* h, double* ms, int32_t* launches) {
+  bm_status s = check_handle(h, false);
+  if (s != BM_OK) return s;
+  if (ms) *ms = h->last_ms;
+  if (launches) *launches = h->last_launches;
+  return BM_OK;
+}
+
+bm_status bm_match(bm_handle* h, const bm_match_opts* opts, int32_t* rmatch, int32_t* cmatch,
+                   int64_t* cardinality, bm_counters* counters, int64_t* per_iter, int64_t cap,
+                   bm_phase_cb cb, void* user) {
+  bm_status s = check_handle(h, true);
+  if (s != BM_OK) return s;
+  s = check_opts(opts);
+  if (s != BM_OK) return s;
+  if ((!rmatch && h->nr > 0) || (!cmatch && h->nc > 0)) return fail(BM_ERR_INVALID_ARG, "null matching array");
+  BM_CUDA(cudaSetDevice(h->device));
+  if (opts->init == BM_INIT_GIVEN) {
+    if (h->nr > 0) BM_CUDA(cudaMemcpyAsync(h->rmatch, rmatch, sizeof(int) * h->nr, cudaMemcpyHostToDevice, h->stream));
+    if (h->nc > 0) BM_CUDA(cudaMemcpyAsync(h->cmatch, cmatch, sizeof(int) * h->nc, cudaMemcpyHostToDevice, h->stream));
+  } else {
+    BM_CUDA(cudaMemsetAsync(h->rmatch, 0xff, sizeof(int) * std::max(h->nr, 1), h->stream));
+    BM_CUDA(cudaMemsetAsync(h->cmatch, 0xff, sizeof(int) * std::max(h->nc, 1), h->stream));
+  }
+  s = prepare_fresh(h);
+  if (s != BM_OK) return s;
+  int32_t done = 0;
+  bm_match_opts o = *opts;
+  o.max_phases = 0;  // the one-call entry always runs to the maximum
+  s = drive(h, o, true, cardinality, counters, per_iter, cap, cb, user, &done);
+  if (s != BM_OK) return s;
+  return bm_download_matching(h, rmatch, cmatch);
+}
+
+bm_status bm_bfs_phase(bm_handle* h, int32_t driver, int32_t bfs_kernel, int32_t improved,
+                       const int32_t* rmatch_in, const int32_t* cmatch_in, int32_t* bfs_array,
+                       int32_t* predecessor, int32_t* rmatch_out, int64_t* launches, int32_t* path_found) {
+  bm_status s = check_handle(h, true);
+  if (s != BM_OK) return s;
+  bm_match_opts o{};
+  o.driver = driver;
+  o.bfs_kernel = bfs_kernel;
+  o.improved = improved;
+  o.init = BM_INIT_GIVEN;
+  s = check_opts(&o);
+  if (s != BM_OK) return s;
+  if ((!rmatch_in && h->nr > 0) || (!cmatch_in && h->nc > 0)) return fail(BM_ERR_INVALID_ARG, "null matching array");
+  BM_CUDA(cudaSetDevice(h->device));
+  if (h->nr > 0) BM_CUDA(cudaMemcpyAsync(h->rmatch, rmatch_in, sizeof(int) * h->nr, cudaMemcpyHostToDevice, h->stream));
+  if (h->nc > 0) BM_CUDA(cudaMemcpyAsync(h->cmatch, cmatch_in, sizeof(int) * h->nc, cudaMemcpyHostToDevice, h->stream));
+  s = prepare_fresh(h);
+  if (s != BM_OK) return s;
+  const int v = variant_of(bfs_kernel == BM_BFS_WR, improved);
+  Params p = make_params(h, o);
+  p.stop_after_bfs = 1;
+  p.max_phases = 1;
+  float ms = 0.f;
+  s = launch(h, v, p, &ms);
+  if (s != BM_OK) return s;
+  h->resumable = false;
+  h->clean = false;
+  Ctrl ctl{};
+  BM_CUDA(cudaMemcpy(&ctl, h->ctl, sizeof(Ctrl), cudaMemcpyDeviceToHost));
+  if (ctl.error) return ctl_error_status(ctl.error);
+  if (bfs_array && h->nc > 0) BM_CUDA(cudaMemcpy(bfs_array, h->bfs, sizeof(int) * h->nc, cudaMemcpyDeviceToHost));
+  if (predecessor && h->nr > 0) BM_CUDA(cudaMemcpy(predecessor, h->pred, sizeof(int) * h->nr, cudaMemcpyDeviceToHost));
+  if (rmatch_out && h->nr > 0) BM_CUDA(cudaMemcpy(rmatch_out, h->rmatch, sizeof(int) * h->nr, cudaMemcpyDeviceToHost));
+  if (launches) *launches = ctl.bfs_levels_last;
+  if (path_found) *path_found = ctl.path_found_last;
+  return BM_OK;
+}
+
+bm_status bm_verify(bm_handle* h, const int32_t* rmatch, const int32_t* cmatch, int64_t* violations,
+                    int32_t* is_max, int64_t* cardinality) {
+  bm_status s = check_handle(h, true);
+  if (s != BM_OK) return s;
+  if ((!rmatch && h->nr > 0) || (!cmatch && h->nc > 0)) return fail(BM_ERR_INVALID_ARG, "null matching array");
+  BM_CUDA(cudaSetDevice(h->device));
+  if (h->nr > 0) BM_CUDA(cudaMemcpyAsync(h->rmatch, rmatch, sizeof(int) * h->nr, cudaMemcpyHostToDevice, h->stream));
+  if (h->nc > 0) BM_CUDA(cudaMemcpyAsync(h->cmatch, cmatch, sizeof(int) * h->nc, cudaMemcpyHostToDevice, h->stream));
+  BM_CUDA(cudaMemsetAsync(h->scratch, 0, sizeof(unsigned long long) * 4, h->stream));
+  const int blocks = std::max(1, std::min(h->sms * 8, (std::max(h->nc, h->nr) + 255) / 256));
+  validate_kernel<<<blocks, 256, 0, h->stream>>>(h->offs, h->adj, h->nc, h->nr, h->sorted, h->rmatch,
+                                                 h->cmatch, h->scratch, h->scratch + 1);
+  BM_CUDA(cudaGetLastError());
+  unsigned long long res[2] = {0, 0};
+  BM_CUDA(cudaMemcpyAsync(res, h->scratch, sizeof(res), cudaMemcpyDeviceToHost, h->stream));
+  BM_CUDA(cudaStreamSynchronize(h->stream));
+  h->resumable = false;
+  if (violations) *violations = (int64_t)res[0];
+  if (cardinality) *cardinality = (int64_t)res[1];
+  if (is_max) *is_max = 0;
+  if (res[0] != 0) return BM_OK;
+  // Maximality half (is_maximum, matching.cpp:106-131): one full GPUBFS
+  // phase from every unmatched column; a reached unmatched row is an
+  // augmenting path.
+  s = prepare_fresh(h);
+  if (s != BM_OK) return s;
+  bm_match_opts o{};
+  o.driver = BM_DRIVER_APFB;
+  o.bfs_kernel = BM_BFS_GPUBFS;
+  Params p = make_params(h, o);
+  p.stop_after_bfs = 1;
+  p.max_phases = 1;
+  float ms = 0.f;
+  s = launch(h, 0, p, &ms);
+  if (s != BM_OK) return s;
+  h->clean = false;
+  Ctrl ctl{};
+  BM_CUDA(cudaMemcpy(&ctl, h->ctl, sizeof(Ctrl), cudaMemcpyDeviceToHost));
+  if (ctl.error) return ctl_error_status(ctl.error);
+  if (is_max) *is_max = ctl.path_found_last ? 0 : 1;
+  return BM_OK;
+}
+
+}  // extern "C"

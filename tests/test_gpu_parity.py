@@ -1,0 +1,251 @@
+"""Parity of the sm_100a engine against the CPU oracle, through the C ABI.
+
+The bar (north_star): the cardinality is bit-exact with the reference on the
+same graph; the matched pairs may differ (race-resolved augmentation), so
+every output is also checked to be a valid matching with no augmenting path
+(validate + is_maximum, matching.cpp:70-131).
+"""
+import numpy as np
+import pytest
+
+import paper_1303_1379_b200 as bm
+from conftest import acceptance_corpus, fork_graph, fork_partial_matching
+
+pytestmark = pytest.mark.gpu
+
+CONFIGS = [  # algorithms.cpp:19-27
+    ("apfb-gpubfs", False, bm.BfsKernel.Gpubfs, False),
+    ("apfb-wr", False, bm.BfsKernel.GpubfsWr, False),
+    ("apsb-gpubfs", True, bm.BfsKernel.Gpubfs, False),
+    ("apsb-wr", True, bm.BfsKernel.GpubfsWr, True),
+]
+
+
+def _check(oracle, g, res, want, init_card=None):
+    m = res.matching
+    assert oracle.validate(g, m.rmatch, m.cmatch) == 0, g.name
+    assert bm.cardinality(m) == want, (g.name, bm.cardinality(m), want)
+    assert oracle.is_maximum(g, m.rmatch, m.cmatch) == 1, g.name
+    c = res.counters
+    assert 1 <= c.outer_iterations <= g.nc + 1
+    assert len(c.bfs_launches_per_iteration) == c.outer_iterations
+
+
+@pytest.fixture(scope="module")
+def corpus(oracle):
+    graphs = acceptance_corpus(1000)
+    return [(g, oracle.brute_force_maximum(g)) for g in graphs]
+
+
+@pytest.mark.parametrize("cfg", CONFIGS, ids=[c[0] for c in CONFIGS])
+def test_corpus_given_init(engine, oracle, corpus, cfg):
+    """acceptance.cpp:135-237 criterion 1 through the B200 engine (first-fit init)."""
+    _, shortest, kernel, improved = cfg
+    for g, want in corpus:
+        init = bm.cheap_matching(g)
+        res = engine.match(g, init, shortest=shortest, kernel=kernel, improved=improved)
+        _check(oracle, g, res, want)
+
+
+@pytest.mark.parametrize("init_mode", ["gpu_greedy", "gpu_ks"])
+def test_corpus_gpu_init(engine, oracle, corpus, init_mode):
+    for g, want in corpus[::3]:
+        for _, shortest, kernel, improved in CONFIGS:
+            res = engine.match(g, None, shortest=shortest, kernel=kernel, improved=improved, init_mode=init_mode)
+            _check(oracle, g, res, want)
+            # the GPU-built initial matching is maximal: no edge joins two free vertices
+            assert res.counters.initial_cardinality <= want
+
+
+def test_gpu_greedy_init_is_maximal(engine, oracle):
+    g = bm.generate_random_bipartite(5000, 4000, 3.0, 77)
+    res = engine.match(g, None, shortest=False, kernel=bm.BfsKernel.GpubfsWr, init_mode="gpu_greedy",
+                       )
+    assert res.counters.initial_cardinality > 0
+    # from an empty init the result is still maximum
+    _check(oracle, g, res, oracle.maximum(g))
+
+
+def test_fork_graph_bfs_trace(engine):
+    """test_gpu_match.cpp:51-71: GPUBFS on the fork graph, full expansion."""
+    g = fork_graph()
+    bfs, pred, rm, launches, found = engine.bfs_phase(g, fork_partial_matching(), kernel=bm.BfsKernel.Gpubfs)
+    assert bfs.tolist() == [2, 3]
+    assert pred.tolist() == [0, 1, 1]
+    assert rm.tolist() == [1, -2, -2]
+    assert launches == 2 and found
+
+
+def test_fork_graph_improved_root_encoding(engine):
+    """test_gpu_match.cpp:111-129: the root entry becomes -(endpoint row); the
+    serial reference keeps r2 (-2); under races either endpoint is valid."""
+    g = fork_graph()
+    bfs, pred, rm, launches, found = engine.bfs_phase(g, fork_partial_matching(), shortest=True,
+                                                      kernel=bm.BfsKernel.GpubfsWr, improved=True)
+    assert bfs[0] in (-1, -2)
+    assert bfs[1] == 3
+    assert rm.tolist() == [1, -2, -2]
+    assert found
+
+
+def test_bfs_levels_match_queue_bfs(engine, oracle):
+    """test_gpu_match.cpp:95-109: GPUBFS labels = queue-BFS depth + 2 (1 if unreachable)."""
+    import conftest
+    for i in range(60):
+        nc = 1 + conftest.splitmix64(2 * i + 21) % 300
+        nr = 1 + conftest.splitmix64(2 * i + 22) % 300
+        g = bm.generate_random_bipartite(nc, nr, [1.0, 2.0, 4.0, 8.0][i % 4], 500 + i)
+        init = bm.cheap_matching(g)
+        depth = oracle.depths(g, init.rmatch, init.cmatch)
+        bfs, *_ = engine.bfs_phase(g, init, kernel=bm.BfsKernel.Gpubfs)
+        want = np.where(depth >= 0, depth + 2, 1)
+        assert np.array_equal(bfs, want), i
+    # and at a size where many CTAs race on every level
+    g = bm.generate_random_bipartite(200000, 200000, 4.0, 3)
+    init = bm.cheap_matching(g)
+    depth = oracle.depths(g, init.rmatch, init.cmatch)
+    bfs, *_ = engine.bfs_phase(g, init, kernel=bm.BfsKernel.Gpubfs)
+    assert np.array_equal(bfs, np.where(depth >= 0, depth + 2, 1))
+
+
+def test_edge_cases(engine, oracle):
+    empty = bm.BipartiteCsr.from_edge_list(0, 0, [])
+    r = engine.match(empty, bm.MatchingState.unmatched(0, 0))
+    assert r.counters.outer_iterations == 1 and r.counters.bfs_launches_per_iteration == [1]
+    edgeless = bm.BipartiteCsr.from_edge_list(3, 4, [])
+    init = bm.MatchingState.unmatched(3, 4)
+    r = engine.match(edgeless, init)  # test_gpu_match.cpp:283-291
+    assert np.array_equal(r.matching.rmatch, init.rmatch) and r.counters.outer_iterations == 1
+    one = bm.BipartiteCsr.from_edge_list(1, 1, [(0, 0)])
+    r = engine.match(one, bm.MatchingState.unmatched(1, 1))
+    assert r.matching.rmatch.tolist() == [0] and r.matching.cmatch.tolist() == [0]
+    comp = bm.BipartiteCsr.from_edge_list(3, 3, [(c, rr) for c in range(3) for rr in range(3)])
+    r = engine.match(comp, bm.cheap_matching(comp), shortest=True, kernel=bm.BfsKernel.Gpubfs)
+    assert r.counters.outer_iterations == 1 and r.counters.bfs_launches_per_iteration == [1]
+    fork = fork_graph()
+    r = engine.match(fork, bm.cheap_matching(fork), kernel=bm.BfsKernel.Gpubfs)  # test_gpu_match.cpp:274-281
+    assert bm.cardinality(r.matching) == 2 and r.counters.outer_iterations == 1
+    r = engine.match(fork, fork_partial_matching(), shortest=True, kernel=bm.BfsKernel.GpubfsWr, improved=True)
+    assert bm.cardinality(r.matching) == 2 and oracle.is_maximum(fork, r.matching.rmatch, r.matching.cmatch) == 1
+
+
+def test_observer_phase_invariants(engine, oracle):
+    """test_gpu_match.cpp:357-377: every phase leaves a valid matching and a
+    monotone cardinality; the per-phase events match the counters."""
+    g = bm.generate_random_bipartite(20000, 20000, 3.0, 11)
+    for _, shortest, kernel, improved in CONFIGS:
+        events = []
+
+        def obs(ev):
+            assert oracle.validate(g, ev.state.rmatch, ev.state.cmatch) == 0
+            assert ev.cardinality_after >= ev.cardinality_before
+            assert bm.cardinality(ev.state) == ev.cardinality_after
+            events.append(ev)
+
+        res = engine.match(g, bm.cheap_matching(g), shortest=shortest, kernel=kernel, improved=improved,
+                           observer=obs)
+        assert len(events) == res.counters.outer_iterations
+        assert [e.bfs_launches for e in events] == res.counters.bfs_launches_per_iteration
+        assert not events[-1].augmenting_path_found
+        assert all(e.augmenting_path_found for e in events[:-1])
+
+
+def test_observer_exception_propagates(engine):
+    g = bm.generate_random_bipartite(1000, 1000, 2.0, 5)
+
+    def boom(ev):
+        raise KeyError("stop")
+
+    with pytest.raises(KeyError):
+        engine.match(g, bm.cheap_matching(g), observer=boom)
+
+
+def test_errors(engine):
+    g = fork_graph()
+    with pytest.raises(bm.LogicError):  # gpu_match.cpp:272-274
+        engine.match(g, bm.cheap_matching(g), kernel=bm.BfsKernel.Gpubfs, improved=True)
+    bad = bm.MatchingState(np.array([0, 0, -1], np.int32), np.array([0, -1], np.int32))  # asymmetric
+    with pytest.raises(ValueError):
+        engine.match(g, bad)
+    pending = bm.MatchingState(np.array([-2, -1, -1], np.int32), np.array([-1, -1], np.int32))
+    with pytest.raises(ValueError):
+        engine.match(g, pending)
+    broken = bm.BipartiteCsr(2, 3, np.array([0, 1, 4], np.int64), np.array([0, 0, 1, 5], np.int32))
+    with pytest.raises(ValueError):
+        engine.upload(broken)
+    nonmono = bm.BipartiteCsr(2, 3, np.array([0, 3, 2], np.int64), np.array([0, 1], np.int32))
+    with pytest.raises(ValueError):
+        engine.upload(nonmono)
+    # the engine stays usable after errors
+    r = engine.match(g, bm.cheap_matching(g))
+    assert bm.cardinality(r.matching) == 2
+
+
+def test_resident_run_and_resume(engine, oracle):
+    g = bm.generate_random_bipartite(100000, 100000, 8.0, 1)
+    init = bm.cheap_matching(g)
+    engine.upload(g)
+    engine.load_matching(init)
+    cards = []
+    for _ in range(3):
+        card, ct, done = engine.run(kernel=bm.BfsKernel.GpubfsWr)
+        assert done
+        cards.append(card)
+    assert cards == [99961] * 3  # reference known answer
+    m = engine.download()
+    assert oracle.validate(g, m.rmatch, m.cmatch) == 0
+    # stop after one phase, then resume to the maximum
+    card1, ct1, done1 = engine.run(kernel=bm.BfsKernel.GpubfsWr, max_phases=1)
+    assert not done1 and card1 > bm.cardinality(init)
+    card2, ct2, done2 = engine.run(kernel=bm.BfsKernel.GpubfsWr, resume=True)
+    assert done2 and card2 == 99961
+    assert ct2.outer_iterations >= 2
+
+
+@pytest.mark.parametrize("nc,deg,seed,want", [
+    (100000, 8.0, 1, 99961),     # C1; SURVEY §8c known answers produced by the reference
+    (200000, 6.0, 4242, 199472),  # acceptance criterion 7 instance
+    (1000000, 8.0, 1, 999679),
+])
+def test_reference_known_answers(engine, oracle, nc, deg, seed, want):
+    g = bm.generate_random_bipartite(nc, nc, deg, seed)
+    init = bm.cheap_matching(g)
+    for _, shortest, kernel, improved in CONFIGS:
+        res = engine.match(g, init, shortest=shortest, kernel=kernel, improved=improved)
+        _check(oracle, g, res, want)
+
+
+def test_planted_and_banded(engine, oracle):
+    g = bm.generate_planted(1_000_000, 16.0, 2024)
+    res = engine.match(g, bm.cheap_matching(g))
+    _check(oracle, g, res, 1_000_000)
+    res = engine.match(g, bm.cheap_matching(g), shortest=True, kernel=bm.BfsKernel.GpubfsWr, improved=True)
+    _check(oracle, g, res, 1_000_000)
+    gb, live = bm.generate_banded(1_000_000, 3, 0.05, 12345)
+    res = engine.match(gb, bm.cheap_matching(gb))
+    _check(oracle, gb, res, live)
+
+
+def test_rmat_skewed(engine, oracle):
+    g = bm.generate_rmat(18, 16.0, 2024)
+    want = oracle.maximum(g)
+    init = bm.cheap_matching(g)
+    for _, shortest, kernel, improved in CONFIGS:
+        res = engine.match(g, init, shortest=shortest, kernel=kernel, improved=improved)
+        _check(oracle, g, res, want)
+
+
+def test_verify_matches_oracle(engine, oracle):
+    g = bm.generate_random_bipartite(50000, 40000, 3.0, 8)
+    init = bm.cheap_matching(g)
+    v, ismax, card = engine.verify(g, init)
+    assert v == 0 and card == bm.cardinality(init)
+    assert ismax == (oracle.is_maximum(g, init.rmatch, init.cmatch) == 1)
+    res = engine.match(g, init)
+    v, ismax, card = engine.verify(g, res.matching)
+    assert v == 0 and ismax and card == oracle.maximum(g)
+    bad = res.matching.copy()
+    r = int(np.flatnonzero(bad.rmatch >= 0)[0])
+    bad.rmatch[r] = -2
+    v, _, _ = engine.verify(g, bad)
+    assert v == oracle.validate(g, bad.rmatch, bad.cmatch) > 0
