@@ -1,0 +1,423 @@
+#!/usr/bin/env python
+"""Benchmark: time-to-maximum-matching on B200 (BASELINE.json metric).
+
+Default workload (N=1): C2 = configs[1] of BASELINE.json — 10M x 10M random
+bipartite graph with a planted perfect matching, average degree 16
+(~1.6e8 edges), APFB-GPUBFS-WR from the reference's first-fit initial
+matching (the reference methodology: cheap_matching outside the timed
+region, bench.cpp:52-63). One *step* = one complete run to the maximum
+matching from the same initial matching, inputs resident in HBM.
+
+  value     = graph edges / time-to-maximum-matching   (edges/s, higher is better)
+  e2e       = same metric through the public C-ABI call with pinned host
+              buffers: graph upload + init H2D + matching + result D2H per step
+  roofline  = algorithmic bytes of the driver kernel / its CUDA-event time,
+              against the measured HBM copy bandwidth (MEASURED_PEAKS.json)
+  cpu_baseline / --impl reference = the reference's own CPU implementation
+              (oracle/_ref: /root/reference sources compiled unmodified),
+              apfb-wr-ct under Schedule::parallel(all host cores)
+
+Multi-GPU (torchrun, N>1): every rank solves its own replica of the workload
+(weak scaling, no data-path collective); timing is the max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "time-to-maximum-matching (ms) and traversed edges/sec; % of HBM roofline"
+
+# name -> (description, builder kwargs)
+CONFIGS = {
+    "C1": "uniform random 100K x 100K, avg degree 8, seed 1 (reference generator)",
+    "C2": "planted perfect matching 10M x 10M, avg degree 16, seed 2024",
+    "C3": "bipartite R-MAT scale 24, edge factor 16, (0.57,0.19,0.19), permuted, seed 2024",
+    "C4": "banded (band 3) 20M x 20M, 5% rows deleted, permuted, seed 12345",
+    "C5": "uniform random 100M x 100M, avg degree 16, seed 5 (reference generator)",
+}
+
+ALGOS = {  # id -> (shortest, kernel, improved)  algorithms.cpp:19-27
+    "apfb-wr": (False, 1, False),
+    "apfb-gpubfs": (False, 0, False),
+    "apsb-wr": (True, 1, True),
+    "apsb-gpubfs": (True, 0, False),
+}
+
+
+def build_graph(name: str, scale_div: int = 1):
+    import paper_1303_1379_b200 as bm
+    if name == "C1":
+        return bm.generate_random_bipartite(100_000, 100_000, 8.0, 1), 99_961
+    if name == "C2":
+        n = 10_000_000 // scale_div
+        return bm.generate_planted(n, 16.0, 2024), n
+    if name == "C3":
+        return bm.generate_rmat(24, 16.0, 2024), None
+    if name == "C4":
+        g, live = bm.generate_banded(20_000_000 // scale_div, 3, 0.05, 12345)
+        return g, live
+    if name == "C5":
+        n = 100_000_000 // scale_div
+        return bm.generate_random_bipartite(n, n, 16.0, 5), (99_999_986 if scale_div == 1 else None)
+    raise SystemExit(f"unknown config {name}")
+
+
+def known_answers():
+    p = os.path.join(ROOT, "tests", "golden", "known_answers.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f)
+    return {}
+
+
+def measured_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """Samples SM clock and clock-event reasons with NVML during the timed region."""
+
+    REASONS = [
+        ("gpu_idle", "nvmlClocksEventReasonGpuIdle"),
+        ("applications_clocks_setting", "nvmlClocksEventReasonApplicationsClocksSetting"),
+        ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"),
+        ("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+        ("sync_boost", "nvmlClocksEventReasonSyncBoost"),
+        ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+        ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+        ("hw_power_brake_slowdown", "nvmlClocksEventReasonHwPowerBrakeSlowdown"),
+    ]
+
+    def __init__(self, device: int, period_s: float = 0.01):
+        self.period = period_s
+        self.samples = []
+        self.reasons = set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _loop(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                mask = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for name, attr in self.REASONS:
+                    bit = getattr(nv, attr, 0)
+                    if bit and (mask & bit) and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self._t = threading.Thread(target=self._loop, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def emit(obj):
+    print(json.dumps(obj), flush=True)
+
+
+_REF_CACHE = {}
+
+
+def cpu_reference_run(g, init, threads_label="parallel"):
+    """The reference's apfb-wr-ct (make_algorithm + Schedule::parallel, kernel_grid.cpp:127-131)."""
+    from oracle import Reference, have_reference
+    if have_reference():
+        ref = _REF_CACHE.setdefault("ref", Reference())
+        key = id(g)
+        if _REF_CACHE.get("key") != key:
+            _REF_CACHE["graph"] = ref.from_csc(g)  # BipartiteCsr copy, not timed
+            _REF_CACHE["key"] = key
+        rg = _REF_CACHE["graph"]
+        r, c, ct, secs = rg.run("apfb-wr-ct", init.rmatch, init.cmatch, threads_label)
+        return {"kind": "reference", "cores": ref.hw_threads(), "seconds": secs,
+                "cardinality": int((r >= 0).sum()), "counters": ct}
+    from oracle import Oracle
+    orc = Oracle()
+    t0 = time.perf_counter()
+    st, r, c, ct = orc.driver(g, init.rmatch, init.cmatch, tot=65536, kernel=1)
+    secs = time.perf_counter() - t0
+    return {"kind": "port", "cores": 1, "seconds": secs, "cardinality": int((r >= 0).sum()), "counters": ct}
+
+
+def run_reference_arm(args):
+    world, rank, local = dist_env()
+    if rank != 0:
+        return 0
+    import paper_1303_1379_b200 as bm
+    g, known = build_graph(args.config, args.scale_div)
+    init = bm.cheap_matching(g)
+    E = g.num_edges()
+    times, cards, kind, cores = [], [], None, None
+    for i in range(args.warmup + args.steps):
+        res = cpu_reference_run(g, init)
+        if i >= args.warmup:
+            times.append(res["seconds"])
+            cards.append(res["cardinality"])
+        kind, cores = res["kind"], res["cores"]
+    t = statistics.mean(times)
+    value = E / t
+    sample = f"full {args.config} workload per step: {g.nc}x{g.nr}, {E} edges, apfb-wr-ct parallel:{cores}"
+    emit({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "edges/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+        "config": {"workload": f"{args.config}: {CONFIGS[args.config]}", "algorithm": "apfb-wr-ct (reference CPU)",
+                   "nc": g.nc, "nr": g.nr, "edges": E, "init": "first-fit cheap_matching (not timed)"},
+        "cpu_baseline": {"value": value, "unit": "edges/s", "cores": cores, "kind": kind, "sample": sample},
+        "e2e": {"value": value, "unit": "edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "time_to_max_matching_ms": t * 1e3, "cardinality": cards[-1] if cards else None,
+        "parity": {"known_answer": known, "ok": (known is None or all(c == known for c in cards))},
+    })
+    return 0
+
+
+def run_b200(args):
+    import numpy as np
+    import torch
+    import paper_1303_1379_b200 as bm
+
+    world, rank, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    else:
+        dist = None
+        torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream(dev)
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    t_gen = time.perf_counter()
+    g, known = build_graph(args.config, args.scale_div)
+    kn = known_answers()
+    if known is None:
+        known = kn.get(f"{args.config}/div{args.scale_div}")
+    init = bm.cheap_matching(g)
+    t_gen = time.perf_counter() - t_gen
+    E = g.num_edges()
+    shortest, kernel, improved = ALGOS[args.algo]
+    kernel = bm.BfsKernel(kernel)
+
+    eng = bm.Engine(local)
+    eng.set_stream(stream.cuda_stream)
+    eng.upload(g)
+    eng.load_matching(init)
+    flush = torch.empty(args.flush_mb << 20, dtype=torch.uint8, device=dev)
+
+    def one_step():
+        return eng.run(shortest=shortest, kernel=kernel, improved=improved)
+
+    # correctness of the measured configuration (GPU Berge certificate)
+    card, ct, done = one_step()
+    m = eng.download()
+    viol, ismax, vcard = eng.verify(g, m)
+    parity_ok = bool(done and viol == 0 and ismax and vcard == card and (known is None or card == known))
+    eng.upload(g, force=True)
+    eng.load_matching(init)
+
+    for _ in range(args.warmup):
+        one_step()
+    torch.cuda.synchronize(dev)
+    barrier()
+    torch.cuda.synchronize(dev)
+    step_ms, kern_ms, launches, cards = [], [], 0, []
+    counters = None
+    sampler = ClockSampler(local)
+    wall0 = time.perf_counter()
+    with sampler:
+        for _ in range(args.steps):
+            flush.fill_(1)  # > L2 (126 MB): every step starts cold
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            card, counters, done = one_step()
+            e1.record(stream)
+            e1.synchronize()
+            step_ms.append(e0.elapsed_time(e1))
+            kms, nl = eng.last_kernel_time()
+            kern_ms.append(kms)
+            launches += nl
+            cards.append(card)
+            parity_ok = parity_ok and done and (known is None or card == known)
+    torch.cuda.synchronize(dev)
+    barrier()
+    torch.cuda.synchronize(dev)
+    wall = time.perf_counter() - wall0
+    t_ms = statistics.mean(step_ms)
+    k_ms = statistics.mean(kern_ms)
+    if dist is not None:
+        t = torch.tensor([t_ms, k_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_ms, k_ms = float(t[0]), float(t[1])
+
+    # ---- end to end through the public API, pinned host buffers ----
+    e2e = None
+    if not args.no_e2e:
+        pin = lambda a: torch.from_numpy(a).pin_memory()  # noqa: E731
+        cx_p, adj_p = pin(g.cxadj), pin(g.cadj)
+        gp = bm.BipartiteCsr(g.nc, g.nr, cx_p.numpy(), adj_p.numpy(), g.name)
+        r_p = torch.empty(g.nr, dtype=torch.int32).pin_memory()
+        c_p = torch.empty(g.nc, dtype=torch.int32).pin_memory()
+        ms_list = []
+        eng2 = bm.Engine(local)
+        eng2.set_stream(stream.cuda_stream)
+        for i in range(args.warmup + args.steps):
+            r_p.numpy()[:] = init.rmatch
+            c_p.numpy()[:] = init.cmatch
+            mstate = bm.MatchingState.__new__(bm.MatchingState)
+            mstate.rmatch, mstate.cmatch = r_p.numpy(), c_p.numpy()
+            flush.fill_(1)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            eng2.upload(gp, force=True)
+            res = eng2.match_inplace(gp, mstate, shortest=shortest, kernel=kernel, improved=improved)
+            e1.record(stream)
+            e1.synchronize()
+            if i >= args.warmup:
+                ms_list.append(e0.elapsed_time(e1))
+                parity_ok = parity_ok and (known is None or res == known)
+        e_ms = statistics.mean(ms_list)
+        if dist is not None:
+            t = torch.tensor([e_ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_ms = float(t[0])
+        h2d = 8 * (g.nc + 1) + 4 * E + 4 * (g.nr + g.nc)
+        d2h = 4 * (g.nr + g.nc)
+        e2e = {"value": world * E / (e_ms / 1e3), "unit": "edges/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "ms_per_step": e_ms}
+        del eng2
+
+    # ---- roofline of the driver kernel (SURVEY.md §8d per-unit bytes) ----
+    wr = 1 if kernel == bm.BfsKernel.GpubfsWr else 0
+    c = counters
+    b_units = (12 * c.edges_traversed + (20 + 8 * wr) * c.columns_scanned + (8 + 4 * wr) * c.columns_visited
+               + 20 * c.walk_steps)
+    b_survey = b_units + c.outer_iterations * (12 * g.nc + 4 * g.nr + 4 * g.nr + 8 * g.nr + 8 * g.nc)
+    peak, peak_src = measured_peak()
+    achieved = b_units / (k_ms / 1e3) / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", f"{args.config.lower()}_{args.algo}_ncu.json")
+    if os.path.exists(prof):
+        with open(prof) as f:
+            traffic = json.load(f).get("dram_bytes_per_launch")
+
+    out = None
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            res = cpu_reference_run(g, init)
+            cpu = {"value": E / res["seconds"], "unit": "edges/s", "cores": res["cores"], "kind": res["kind"],
+                   "sample": f"one full {args.config} run ({E} edges) of apfb-wr-ct "
+                             f"{'parallel:' + str(res['cores']) if res['kind'] == 'reference' else 'serial port'}",
+                   "seconds": res["seconds"], "cardinality": res["cardinality"]}
+            parity_ok = parity_ok and res["cardinality"] == cards[-1]
+        out = {
+            "metric": METRIC, "value": world * E / (t_ms / 1e3), "unit": "edges/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+            "config": {"workload": f"{args.config}: {CONFIGS[args.config]}" +
+                                   (f" (1/{args.scale_div} scale)" if args.scale_div != 1 else ""),
+                       "algorithm": f"{args.algo}-b200", "nc": g.nc, "nr": g.nr, "edges": E,
+                       "init": "first-fit cheap_matching, resident in HBM (not timed)",
+                       "l2": f"flushed between steps ({args.flush_mb} MiB write)",
+                       "parallelism": "replicas" if world > 1 else "single-gpu"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                         "kernel": "bm::driver_kernel (persistent, whole run)",
+                         "algorithmic_bytes_per_launch": b_units, "survey_formula_bytes": b_survey},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": sampler.summary(),
+            "time_to_max_matching_ms": t_ms,
+            "kernel_ms": k_ms,
+            "teps": c.edges_traversed / (k_ms / 1e3),
+            "cardinality": cards[-1],
+            "parity": {"known_answer": known, "gpu_verify_violations": viol, "gpu_is_maximum": ismax,
+                       "ok": bool(parity_ok)},
+            "counters": {"outer_iterations": c.outer_iterations, "bfs_levels": c.bfs_launches_total(),
+                         "columns_scanned": c.columns_scanned, "edges_traversed": c.edges_traversed,
+                         "columns_visited": c.columns_visited, "walks": c.alternations_attempted,
+                         "walk_steps": c.walk_steps, "fix_resets": c.fix_resets,
+                         "serial_retries": c.serial_retries},
+            "generation_s": t_gen, "timed_wall_s": wall,
+        }
+        emit(out)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="C2")
+    ap.add_argument("--algo", choices=sorted(ALGOS), default="apfb-wr")
+    ap.add_argument("--scale-div", type=int, default=1, help="shrink C2/C4/C5 by this factor (testing only)")
+    ap.add_argument("--flush-mb", type=int, default=512)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "b200":
+        print("warning: fewer than 3 warm-up steps", file=sys.stderr)
+    if args.impl == "reference":
+        return run_reference_arm(args)
+    return run_b200(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -218,22 +218,33 @@ class Engine:
     def match(self, g: BipartiteCsr, init: Optional[MatchingState], *, shortest=False,
               kernel=BfsKernel.GpubfsWr, improved=False, init_mode="given",
               observer: Optional[Callable[[PhaseEvent], None]] = None) -> DriverResult:
+        m = init.copy() if init is not None else MatchingState.unmatched(g.nc, g.nr)
+        ct, launches = self._match(g, m, shortest, kernel, improved, init_mode, observer)
+        return DriverResult(m, _counters_from(ct, launches))
+
+    def match_inplace(self, g: BipartiteCsr, m: MatchingState, *, shortest=False, kernel=BfsKernel.GpubfsWr,
+                      improved=False, init_mode="given") -> int:
+        """bm_match on caller-owned arrays (e.g. pinned buffers): m holds the
+        initial matching on entry and the maximum matching on return."""
+        ct, _ = self._match(g, m, shortest, kernel, improved, init_mode, None, want_launches=False)
+        return int(ct.cardinality)
+
+    def _match(self, g, m, shortest, kernel, improved, init_mode, observer, want_launches=True):
         self.upload(g)
         o = _opts(shortest, kernel, improved, init_mode)
-        m = init.copy() if init is not None else MatchingState.unmatched(g.nc, g.nr)
         if len(m.rmatch) != g.nr or len(m.cmatch) != g.nc:
             raise ValueError("matching arrays do not fit the graph")
         ct = _lib.bm_counters()
-        cap = g.nc + 2
-        launches = np.zeros(cap, np.int64)
+        cap = g.nc + 2 if want_launches else 0
+        launches = np.zeros(max(cap, 1), np.int64)
         card = C.c_int64()
         cb, err = self._make_cb(observer)
         st = lib.bm_match(self._h, C.byref(o), i32p(m.rmatch), i32p(m.cmatch), C.byref(card), C.byref(ct),
-                          i64p(launches), cap, cb, None)
+                          i64p(launches) if cap else None, cap, cb, None)
         if err:
             raise err[0]
         check(st)
-        return DriverResult(m, _counters_from(ct, launches))
+        return ct, launches
 
     @staticmethod
     def _make_cb(observer):
@@ -297,6 +308,21 @@ class Engine:
         ms, n = C.c_double(), C.c_int32()
         check(lib.bm_last_kernel_time(self._h, C.byref(ms), C.byref(n)))
         return ms.value, n.value
+
+    TL_KINDS = {0: "start", 1: "init", 2: "setup", 3: "level", 4: "alternate", 5: "fix_rows", 6: "fix_cols",
+                7: "roots", 8: "end"}
+
+    def timeline(self):
+        """Stage timeline of the last run: list of (kind, arg, t_ns) from the device clock."""
+        n = C.c_int64()
+        check(lib.bm_timeline(self._h, None, 0, C.byref(n)))
+        buf = np.zeros(2 * max(n.value, 1), np.uint64)
+        check(lib.bm_timeline(self._h, buf.ctypes.data_as(C.POINTER(C.c_uint64)), n.value, C.byref(n)))
+        out = []
+        for i in range(n.value):
+            tag, t = int(buf[2 * i]), int(buf[2 * i + 1])
+            out.append((self.TL_KINDS.get(tag >> 32, str(tag >> 32)), tag & 0xFFFFFFFF, t))
+        return out
 
     def bfs_phase(self, g: BipartiteCsr, m: MatchingState, *, shortest=False, kernel=BfsKernel.Gpubfs,
                   improved=False):

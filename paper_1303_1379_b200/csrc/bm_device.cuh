@@ -56,6 +56,13 @@ __device__ __forceinline__ unsigned ld_cg_u(const int4* p) {  // .w field only
   asm volatile("ld.global.cg.b32 %0, [%1];" : "=r"(v) : "l"(reinterpret_cast<const char*>(p) + 12));
   return v;
 }
+// L1-cacheable load for heuristic reads where a value up to one grid barrier
+// old is acceptable (WR root marks).
+__device__ __forceinline__ int ld_ca(const int* p) {
+  int v;
+  asm volatile("ld.global.ca.b32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
 // Read-only graph data (never written inside a launch).
 __device__ __forceinline__ int ld_ro(const int* p) {
   int v;
@@ -84,6 +91,36 @@ __device__ __forceinline__ void st_plain(int* p, int v) {
 __device__ __forceinline__ void st_plain(int4* p, int4 v) {
   asm volatile("st.global.v4.b32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
                "r"(v.w)
+               : "memory");
+}
+
+// ---- L2 eviction policy for streamed data ---------------------------------
+// Adjacency rows, frontier entries and predecessor stores are touched once
+// per level; marking them evict_first keeps the randomly gathered state
+// (rmatch, the visited bitmap, offsets, root marks) resident in L2.
+__device__ __forceinline__ unsigned long long policy_evict_first() {
+  unsigned long long pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ int ld_stream(const int* p, unsigned long long pol) {
+  int v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ int4 ld_cg_stream(const int4* p, unsigned long long pol) {
+  int4 v;
+  asm volatile("ld.global.cg.L2::cache_hint.v4.b32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void st_stream(int* p, int v, unsigned long long pol) {
+  asm volatile("st.global.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(p), "r"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void st_stream(int4* p, int4 v, unsigned long long pol) {
+  asm volatile("st.global.L2::cache_hint.v4.b32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w), "l"(pol)
                : "memory");
 }
 

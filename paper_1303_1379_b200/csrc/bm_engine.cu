@@ -5,11 +5,11 @@
 // level-synchronous BFS, ALTERNATE, FIXMATCHING and the termination test. The
 // host launches it once per bm_run (or once per phase when an observer is
 // attached) and reads one small control block back at the end. There is no
-// per-level host synchronisation at all; levels and stages are separated by a
+// per-level host synchronisation; levels and stages are separated by a
 // software grid barrier (one atomic per CTA).
 //
 // Reference correspondence (paths relative to /root/reference/proj):
-//   setup stage            init_bfs_array / init_root / predecessor reset  src/gpu_match.cpp:8-21, 277-282
+//   setup stage            init_bfs_array / init_root                      src/gpu_match.cpp:8-21, 277-282
 //   expand_level           gpubfs / gpubfs_wr (Alg. 2 / Alg. 4)            src/gpu_match.cpp:23-135
 //   level loop             expand_bfs                                       src/gpu_match.cpp:247-266
 //   alternate stage        alternate / alternate_wr / alternate_walk       src/gpu_match.cpp:144-218
@@ -17,20 +17,32 @@
 //   phase loop             run_phase / run_driver / apfb / apsb             src/gpu_match.cpp:268-376
 //   greedy init            cheap_matching (first-fit), parallelised        src/matching.cpp:13-26
 //
-// What is B200-specific (and why it is not a translation of the reference):
-//   * The reference tests every column's level in every launch (O(nc) per
-//     level, gpu_match.cpp:48/105). Here each level is a frontier queue of
-//     16-byte entries {col, root, adj_begin, edge_prefix}; the edge prefix
-//     comes from one packed 64-bit atomicAdd per warp ((count<<33)|edges),
-//     so the next level can be split into equal *edge* tiles regardless of
-//     the degree skew (R-MAT hubs of 2e5 rows are split across CTAs).
-//   * "Unvisited" is a 1-bit-per-column bitmap (nc/8 bytes, L2 resident even
-//     at 1e8 columns) claimed with atomicOr, instead of a 4-byte gather into
-//     bfs_array; the bfs_array labels are still written (reference layout).
-//   * Per-phase O(n) passes (init, FIX, cardinality) are restricted to the
-//     columns/rows the phase touched: only those can be inconsistent after
-//     ALTERNATE, so the restricted FIX is exactly the reference's FIX.
-//   * The root of each tree rides in the frontier entry (no root[] gather).
+// B200 design (not a translation of the reference's host loops):
+//   * Frontier queues instead of an O(nc) level test per launch
+//     (gpu_match.cpp:48/105). A level is a run of 16-byte entries
+//     {col, root, adj_begin, edge_prefix}; one packed 64-bit atomicAdd per warp
+//     ((count<<33)|edges) hands out slots AND the level-local edge prefix, so
+//     the next level is cut into equal *edge* tiles whatever the degree skew.
+//     While pushing, each entry also records itself in a granule index (one
+//     u32 per kGran edges), so a tile finds its first entry with one load.
+//   * "Unvisited" is a 1-bit-per-column bitmap claimed with atomicOr (nc/8
+//     bytes: L2-resident even at 1e8 columns) instead of a bfs_array gather.
+//   * WR: a tree whose root already found a path stops claiming columns at
+//     discovery time, not only at expansion (gpu_match.cpp:106-108), leaving
+//     them to live trees. Correctness never depends on it (ALTERNATE's claim
+//     check + FIX do).
+//   * FIXMATCHING touches only what ALTERNATE wrote. Every walk step writes
+//     rmatch[row] = pred[row] and cmatch[pred[row]] = row, and logs the pair;
+//     the only other entries that can become inconsistent are the pending
+//     endpoints (-2) and the row a walk leaves dangling when it breaks. Those
+//     sets are exactly the inconsistent set of the reference's three full
+//     passes, so the restricted FIX is the reference FIX.
+//   * Predecessors are never reset: a walk only reads pred[] of rows whose
+//     column was claimed in the current phase (the endpoint, the original
+//     mate of a claimed column, or a row a walk wrote this phase), all of which
+//     were written in this phase's BFS.
+//   * The next phase's roots come from this phase's roots plus columns FIX
+//     unmatched; nothing is O(nc) per phase except the 1-bit bitmap clear.
 #include <algorithm>
 #include <cstdint>
 #include <cstdio>
@@ -38,15 +50,21 @@
 #include <string>
 #include <vector>
 
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include "bm_device.cuh"
 #include "bmatch_b200.h"
 
+namespace cg = cooperative_groups;
+
 namespace bm {
 
 constexpr int kThreads = 512;         // threads per CTA
 constexpr int kItems = 4;             // edges per thread per round (memory-level parallelism)
+constexpr unsigned kGran = 512;       // edges per granule-index entry; tiles are whole granules
+constexpr unsigned kMaxTileGran = 8;  // <= 4096 edges per tile (= the winner buffer)
+constexpr unsigned kWBuf = kGran * kMaxTileGran;
 constexpr int kStartLevel = 2;        // L0 (gpu_match.cpp:275)
 constexpr int kUnvisited = kStartLevel - 1;
 constexpr int kFoundMark = kStartLevel - 2;
@@ -85,6 +103,7 @@ enum Stat : int {
   kStResets,
   kStLevels,
   kStRetries,
+  kStDenseFix,
   kNumStats
 };
 
@@ -96,6 +115,10 @@ struct alignas(128) Ctrl {
   Slot roots;
   unsigned n_ep;
   unsigned pad1[31];
+  unsigned n_log;
+  unsigned log_overflow;
+  unsigned n_tl;
+  unsigned pad1b[29];
   unsigned path_found[2];
   unsigned pad2[30];
   unsigned long long invalid;
@@ -128,8 +151,11 @@ struct Params {
   int nvis_words;
   int4* F0;
   int4* F1;
-  int* FR;
+  unsigned* gidx0;  // granule index, ping-pong by level parity
+  unsigned* gidx1;
   int* EP;
+  int2* wlog;       // ALTERNATE write log: (row, col) per step, (row, -1) for a dangling row
+  unsigned log_cap;
   Ctrl* ctl;
   PhaseRec* recs;
   int rec_cap;
@@ -138,16 +164,45 @@ struct Params {
   int fresh;
   int max_phases;
   int stop_after_bfs;
+  int trace;        // write bfs_array level labels (parity probes)
   long long phase_bound;
+  unsigned long long* tl;  // stage timeline: (tag, %globaltimer ns) pairs written by the leader
+  unsigned tl_cap;
 };
 
+enum TlTag : unsigned {
+  kTlStart = 0, kTlInit = 1, kTlSetup = 2, kTlLevel = 3, kTlAlt = 4, kTlFixRows = 5, kTlFixCols = 6,
+  kTlRoots = 7, kTlEnd = 8
+};
+
+__device__ __forceinline__ void tl_mark(const Params& p, unsigned kind, unsigned arg) {
+  if (blockIdx.x == 0 && threadIdx.x == 0 && p.tl) {
+    const unsigned n = p.ctl->n_tl;
+    if (n < p.tl_cap) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      p.tl[2 * n] = ((unsigned long long)kind << 32) | arg;
+      p.tl[2 * n + 1] = t;
+    }
+    p.ctl->n_tl = n + 1;
+  }
+}
+
 struct Smem {
-  unsigned pre[kThreads + 1];
+  unsigned pre[kThreads + 1];   // window: raw edge prefix of each entry, then the live-edge prefix
   int col[kThreads];
   int root[kThreads];
-  unsigned beg[kThreads];
+  unsigned beg[kThreads];       // first live adjacency index of each entry in this window
+  unsigned wtot[kThreads / 32];
+  unsigned short cgr[kWBuf / 32 + 2];  // entry holding live edge 32*q (coarse index for the search)
   unsigned tile;
   unsigned long long cnt[kNumStats];  // per-CTA work counters, flushed to Ctrl at exit
+  unsigned long long wsum[kThreads / 32];  // CTA-aggregated pushes: per-warp totals
+  unsigned wep[kThreads / 32];
+  unsigned long long blk_base;
+  unsigned blk_ep;
+  unsigned nw;                          // winners staged in wbuf for the current window
+  int2 wbuf[kWBuf];                     // (column, root) claimed in the current window
 };
 
 // Warp-reduce a per-thread count and add it to the CTA's shared counter. Must
@@ -176,7 +231,7 @@ __device__ __noinline__ void grid_sync(Ctrl* ctl) {
       const long long t0 = clock64();
       unsigned spins = 0;
       while (ld_acq(&ctl->bar_gen) == gen) {
-        __nanosleep(64);
+        __nanosleep(32);
         if (((++spins) & 0xfffu) == 0 && clock64() - t0 > (1ll << 37)) {  // ~70 s watchdog
           ctl->error = kErrBarrier;
           __threadfence_system();
@@ -198,62 +253,87 @@ __device__ __forceinline__ unsigned long long global_threads() {
   return (unsigned long long)gridDim.x * kThreads;
 }
 
-// Warp-aggregated append of frontier entries {col, root, begin, prefix} with
-// the matching discovered row in FR. One packed 64-bit atomic per warp gives
-// both the slot and the level-local edge prefix, so prefixes are monotone in
-// slot order (atomics on one address are totally ordered).
-__device__ __forceinline__ void push_entries(bool win, int col, int root, unsigned beg, unsigned deg,
-                                             int row, Slot* out, int4* F, int* FR,
-                                             unsigned out_base) {
-  const unsigned mask = __ballot_sync(kFull, win);
-  if (mask == 0) return;
+__device__ __forceinline__ unsigned long long warp_incl_scan64(unsigned long long v) {
   const unsigned lane = lane_id();
-  const unsigned d = win ? deg : 0u;
-  const unsigned incl = warp_incl_scan(d);
-  const unsigned total = __shfl_sync(kFull, incl, 31);
-  const unsigned cnt = __popc(mask);
-  unsigned long long base = 0;
-  if (lane == 0)
-    base = atomicAdd(&out->packed, ((unsigned long long)cnt << 33) | (unsigned long long)total);
-  base = __shfl_sync(kFull, base, 0);
-  if (win) {
-    const unsigned rank = __popc(mask & ((1u << lane) - 1u));
-    const unsigned pos = out_base + (unsigned)(base >> 33) + rank;
-    const unsigned pre = (unsigned)(base & kEdgeMask) + (incl - d);
-    st_plain(F + pos, make_int4(col, root, (int)beg, (int)pre));
-    st_plain(FR + pos, row);
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long t = __shfl_up_sync(kFull, v, o);
+    if (lane >= (unsigned)o) v += t;
   }
+  return v;
 }
 
-__device__ __forceinline__ void push_row(bool flag, int row, unsigned* counter, int* list) {
-  const unsigned mask = __ballot_sync(kFull, flag);
-  if (mask == 0) return;
-  const unsigned lane = lane_id();
-  unsigned base = 0;
-  if (lane == 0) base = atomicAdd(counter, (unsigned)__popc(mask));
-  base = __shfl_sync(kFull, base, 0);
-  if (flag) st_plain(list + base + __popc(mask & ((1u << lane) - 1u)), row);
+// CTA-wide reservation of frontier slots/edge prefix and endpoint slots: one
+// atomic per CTA instead of one per warp (every warp of the GPU pushes into
+// the same two counters, so per-warp atomics serialise in L2). `cnt`/`deg`
+// are this thread's winners and their total degree, `epc` its endpoints.
+// Returns this thread's first packed (slot << 33 | prefix) and endpoint slot.
+// Must be called by every thread of the CTA; returns false (no work) for all
+// threads when the CTA pushes nothing.
+__device__ __forceinline__ bool cta_reserve(Smem& sm, unsigned cnt, unsigned deg, unsigned epc, Slot* out,
+                                            unsigned* n_ep, unsigned long long& tbase, unsigned& tep) {
+  const unsigned long long v = ((unsigned long long)cnt << 33) | deg;
+  const unsigned long long incl = warp_incl_scan64(v);
+  const unsigned ep_incl = warp_incl_scan(epc);
+  const unsigned warp = threadIdx.x >> 5;
+  if (lane_id() == 31) {
+    sm.wsum[warp] = incl;
+    sm.wep[warp] = ep_incl;
+  }
+  if (!__syncthreads_or((cnt | epc) != 0u)) return false;
+  if (threadIdx.x == 0) {
+    unsigned long long run = 0;
+    unsigned er = 0;
+#pragma unroll
+    for (int w = 0; w < kThreads / 32; ++w) {
+      const unsigned long long t = sm.wsum[w];
+      sm.wsum[w] = run;
+      run += t;
+      const unsigned te = sm.wep[w];
+      sm.wep[w] = er;
+      er += te;
+    }
+    sm.blk_base = run ? atomicAdd(&out->packed, run) : 0ull;
+    sm.blk_ep = er ? atomicAdd(n_ep, er) : 0u;
+  }
+  __syncthreads();
+  tbase = sm.blk_base + sm.wsum[warp] + (incl - v);
+  tep = sm.blk_ep + sm.wep[warp] + (ep_incl - epc);
+  return true;
+}
+
+// Writes one reserved frontier entry and its granule-index records.
+__device__ __forceinline__ void put_entry(int4* F, unsigned out_base, unsigned* gidx, unsigned long long slot,
+                                          int col, int root, unsigned beg, unsigned deg,
+                                          unsigned long long pol = 0) {
+  const unsigned local = (unsigned)(slot >> 33);
+  const unsigned pre = (unsigned)(slot & kEdgeMask);
+  if (pol) st_stream(F + out_base + local, make_int4(col, root, (int)beg, (int)pre), pol);
+  else st_plain(F + out_base + local, make_int4(col, root, (int)beg, (int)pre));
+  const unsigned m1 = (pre + deg - 1) / kGran;
+  for (unsigned m = (pre + kGran - 1) / kGran; m <= m1; ++m) st_plain(reinterpret_cast<int*>(gidx) + m, (int)local);
 }
 
 // ---------------------------------------------------------------------------
 // One BFS level (GPUBFS, Alg. 2, gpu_match.cpp:42-70; GPUBFS-WR, Alg. 4,
-// gpu_match.cpp:99-133), over the frontier F[ls, ls+n) holding T edges.
+// gpu_match.cpp:99-133) over the frontier F[ls, ls+n) holding T edges.
 template <bool WR, bool IMP>
-__device__ void expand_level(const Params& p, Smem& sm, int4* F, unsigned ls,
-                             unsigned n, unsigned T, Slot* in, Slot* out, int level, int pf) {
+__device__ void expand_level(const Params& p, Smem& sm, int4* F, unsigned ls, unsigned n, unsigned T,
+                             const unsigned* gin, unsigned* gout, Slot* in, Slot* out, int level, int pf) {
   if (T == 0) return;
   const unsigned tid = threadIdx.x;
   unsigned c_trav = 0, c_cexp = 0, c_nvis = 0, c_entries = 0;
   const unsigned long long G = gridDim.x;
   unsigned long long per = (T + 2 * G - 1) / (2 * G);
-  per = ((per + kThreads - 1) / kThreads) * kThreads;
-  if (per < (unsigned long long)kThreads) per = kThreads;
-  if (per > (unsigned long long)kThreads * kItems * 4) per = (unsigned long long)kThreads * kItems * 4;
+  per = ((per + kGran - 1) / kGran) * kGran;
+  if (per > (unsigned long long)kGran * kMaxTileGran) per = (unsigned long long)kGran * kMaxTileGran;
   const unsigned ET = (unsigned)per;
   const unsigned ntiles = (unsigned)((T + (unsigned long long)ET - 1) / ET);
   const unsigned out_base = ls + n;
   unsigned* const path_flag = &p.ctl->path_found[pf];
 
+  const unsigned long long pol = policy_evict_first();
+  if (tid == 0) sm.nw = 0;
   for (;;) {
     if (tid == 0) sm.tile = atomicAdd(&in->tile, 1u);
     __syncthreads();
@@ -262,26 +342,13 @@ __device__ void expand_level(const Params& p, Smem& sm, int4* F, unsigned ls,
     if (tile >= ntiles) break;
     const unsigned e0 = tile * ET;
     const unsigned e1 = (T - e0 < ET) ? T : e0 + ET;
-
-    // Cooperative 512-ary search for the entry holding edge e0 (<= 3 rounds
-    // for 1e8 entries): the last i with prefix(i) <= e0.
-    unsigned lo = 0, hi = n;
-    while (hi - lo > 1) {
-      const unsigned stride = (hi - lo + kThreads - 1) / kThreads;
-      const unsigned idx = lo + tid * stride;
-      const bool ok = idx < hi && ld_cg_u(F + ls + idx) <= e0;
-      const int k = __syncthreads_count(ok);
-      lo = lo + (unsigned)(k - 1) * stride;
-      hi = min(lo + stride, hi);
-    }
-
-    unsigned i = lo;
+    unsigned i = (unsigned)ld_cg(reinterpret_cast<const int*>(gin) + e0 / kGran);  // entry holding edge e0
     unsigned e = e0;
     while (e < e1) {
       // Window of up to kThreads entries starting at i.
       const unsigned wi = i + tid;
       if (wi < n) {
-        const int4 ent = ld_cg(F + ls + wi);
+        const int4 ent = ld_cg_stream(F + ls + wi, pol);
         bool skip = false;
         if (WR) skip = ld_rlx(p.bfs + ent.y) < kUnvisited;  // early exit (gpu_match.cpp:106-108)
         sm.col[tid] = ent.x;
@@ -299,8 +366,40 @@ __device__ void expand_level(const Params& p, Smem& sm, int4* F, unsigned ls,
       if (tid == 0) sm.pre[kThreads] = (i + kThreads < n) ? ld_cg_u(F + ls + i + kThreads) : T;
       __syncthreads();
       const unsigned wend = min(e1, sm.pre[kThreads]);
+      // Compact the window to its live edges: entries of trees that already
+      // found a path (WR) and edge ranges outside [e, wend) contribute none.
+      unsigned live;
+      {
+        const unsigned lo = max(sm.pre[tid], e);
+        const unsigned hi = min(sm.pre[tid + 1], wend);
+        const unsigned len = (sm.root[tid] >= 0 && hi > lo) ? hi - lo : 0u;
+        const unsigned nb = sm.beg[tid] + (lo - sm.pre[tid]);
+        const unsigned incl = warp_incl_scan(len);
+        if (lane_id() == 31) sm.wtot[tid >> 5] = incl;
+        __syncthreads();
+        unsigned wbase = 0, tot = 0;
+#pragma unroll
+        for (int w = 0; w < kThreads / 32; ++w) {
+          const unsigned t = sm.wtot[w];
+          wbase += (w < (int)(tid >> 5)) ? t : 0u;
+          tot += t;
+        }
+        live = tot;
+        const unsigned vp = wbase + incl - len;
+        sm.beg[tid] = nb;
+        sm.pre[tid] = vp;  // live-edge prefix (ties resolve to the last entry)
+        if (tid == 0) sm.pre[kThreads] = tot;
+        if (len) {  // coarse index: this entry holds live edges 32q for q in [ceil(vp/32), (vp+len-1)/32]
+          const unsigned q1 = (vp + len - 1) >> 5;
+          for (unsigned q = (vp + 31) >> 5; q <= q1; ++q) sm.cgr[q] = (unsigned short)tid;
+        }
+        __syncthreads();
+      }
+      const unsigned nq = (live + 31) >> 5;
 
-      for (unsigned base = e; base < wend; base += kThreads * kItems) {
+      // Rounds over the live edges: no CTA-wide barrier inside; winners are
+      // staged in sm.wbuf.
+      for (unsigned base = 0; base < live; base += kThreads * kItems) {
         int row[kItems], cm[kItems], sl[kItems];
         unsigned w[kItems];
 #pragma unroll
@@ -308,54 +407,104 @@ __device__ void expand_level(const Params& p, Smem& sm, int4* F, unsigned ls,
           const unsigned ee = base + k * kThreads + tid;
           row[k] = -1;
           sl[k] = 0;
-          if (ee < wend) {
-            int a = 0, b = kThreads;
+          if (ee < live) {
+            // the entry holding ee lies in [cgr[q], cgr[q+1]] (1-2 steps for typical degrees)
+            const unsigned q = ee >> 5;
+            int a = sm.cgr[q];
+            int b = (q + 1 < nq) ? (int)sm.cgr[q + 1] + 1 : kThreads;
             while (b - a > 1) {
               const int mid = (a + b) >> 1;
               if (sm.pre[mid] <= ee) a = mid; else b = mid;
             }
             sl[k] = a;
-            if (!WR || sm.root[a] >= 0) {
-              row[k] = ld_ro(p.adj + sm.beg[a] + (ee - sm.pre[a]));
-              c_trav++;
-            }
+            row[k] = ld_stream(p.adj + sm.beg[a] + (ee - sm.pre[a]), pol);
+            c_trav++;
           }
         }
-#pragma unroll
-        for (int k = 0; k < kItems; ++k) cm[k] = row[k] >= 0 ? ld_rlx(p.rmatch + row[k]) : -3;
-#pragma unroll
-        for (int k = 0; k < kItems; ++k) w[k] = cm[k] >= 0 ? ld_rlx(p.vis + (cm[k] >> 5)) : kFull;
+        int rmark[kItems];  // WR: the root's mark, issued alongside the rmatch gather
 #pragma unroll
         for (int k = 0; k < kItems; ++k) {
-          bool win = false, ep = false;
+          cm[k] = row[k] >= 0 ? ld_rlx(p.rmatch + row[k]) : -3;
+          rmark[k] = (WR && row[k] >= 0) ? ld_ca(p.bfs + sm.root[sl[k]]) : kStartLevel;
+        }
+#pragma unroll
+        for (int k = 0; k < kItems; ++k) w[k] = cm[k] >= 0 ? ld_rlx(p.vis + (cm[k] >> 5)) : kFull;
+        unsigned wins = 0, eps = 0;
+#pragma unroll
+        for (int k = 0; k < kItems; ++k) {
           const int c = cm[k];
-          if (c >= 0) {
-            const unsigned bit = 1u << (c & 31);
-            if (!(w[k] & bit)) {
-              const unsigned old = atomicOr(p.vis + (c >> 5), bit);
-              win = !(old & bit);
-            }
-          } else if (c == -1) {
-            ep = atomicCAS(p.rmatch + row[k], -1, -2) == -1;
-          }
           const int col = sm.col[sl[k]];
           const int root = WR ? sm.root[sl[k]] : col;
-          unsigned nbeg = 0, ndeg = 0;
-          if (win) {
-            st_plain(p.pred + row[k], col);
-            st_plain(p.bfs + c, level + 1);
-            nbeg = ld_ro(p.offs + c);
-            ndeg = ld_ro(p.offs + c + 1) - nbeg;
-            c_nvis++;
+          if (c >= 0) {
+            const unsigned bit = 1u << (c & 31);
+            // WR: a tree whose root is already marked stops claiming columns.
+            if (!(w[k] & bit) && (!WR || rmark[k] >= kUnvisited)) {
+              const unsigned old = atomicOr(p.vis + (c >> 5), bit);
+              if (!(old & bit)) {
+                wins |= 1u << k;
+                st_stream(p.pred + row[k], col, pol);
+                if (p.trace) st_plain(p.bfs + c, level + 1);
+              }
+            }
+          } else if (c == -1) {
+            if (atomicCAS(p.rmatch + row[k], -1, -2) == -1) {
+              eps |= 1u << k;
+              st_plain(p.pred + row[k], col);
+              if (WR) st_rlx(p.bfs + root, IMP ? -row[k] : kFoundMark);
+              if (ld_rlx(path_flag) == 0u) st_rlx(path_flag, 1u);
+            }
           }
-          push_entries(win, c, root, nbeg, ndeg, row[k], out, F, p.FR, out_base);
-          if (ep) {
-            st_plain(p.pred + row[k], col);
-            if (WR) st_rlx(p.bfs + root, IMP ? -row[k] : kFoundMark);
-            if (ld_rlx(path_flag) == 0u) st_rlx(path_flag, 1u);
-          }
-          push_row(ep, row[k], &p.ctl->n_ep, p.EP);
         }
+        // stage winners (one shared-memory atomic per warp)
+        {
+          const unsigned mine = __popc(wins);
+          const unsigned incl = warp_incl_scan(mine);
+          const unsigned tot = __shfl_sync(kFull, incl, 31);
+          unsigned wb = 0;
+          if (lane_id() == 31 && tot) wb = atomicAdd(&sm.nw, tot);
+          wb = __shfl_sync(kFull, wb, 31) + incl - mine;
+#pragma unroll
+          for (int k = 0; k < kItems; ++k)
+            if (wins & (1u << k)) sm.wbuf[wb++] = make_int2(cm[k], WR ? sm.root[sl[k]] : sm.col[sl[k]]);
+          c_nvis += mine;
+        }
+        // endpoints are rare: warp-aggregated global append
+        {
+          const unsigned mine = __popc(eps);
+          const unsigned incl = warp_incl_scan(mine);
+          const unsigned tot = __shfl_sync(kFull, incl, 31);
+          if (tot) {
+            unsigned eb = 0;
+            if (lane_id() == 31) eb = atomicAdd(&p.ctl->n_ep, tot);
+            eb = __shfl_sync(kFull, eb, 31) + incl - mine;
+#pragma unroll
+            for (int k = 0; k < kItems; ++k)
+              if (eps & (1u << k)) st_plain(p.EP + eb++, row[k]);
+          }
+        }
+      }
+      __syncthreads();
+      // Flush the window's winners: one CTA reservation for all of them.
+      const unsigned nw = sm.nw;
+      if (nw) {
+        unsigned cnt = 0, deg = 0;
+        for (unsigned j = tid; j < nw; j += kThreads) {
+          const int c = sm.wbuf[j].x;
+          deg += ld_ro(p.offs + c + 1) - ld_ro(p.offs + c);
+          cnt++;
+        }
+        unsigned long long slot;
+        unsigned unused;
+        cta_reserve(sm, cnt, deg, 0u, out, &p.ctl->n_ep, slot, unused);
+        for (unsigned j = tid; j < nw; j += kThreads) {
+          const int2 cr = sm.wbuf[j];
+          const unsigned b0 = ld_ro(p.offs + cr.x);
+          const unsigned d0 = ld_ro(p.offs + cr.x + 1) - b0;
+          put_entry(F, out_base, gout, slot, cr.x, cr.y, b0, d0, pol);
+          slot += (1ull << 33) + d0;
+        }
+        __syncthreads();
+        if (tid == 0) sm.nw = 0;
       }
       e = wend;
       i += kThreads;
@@ -368,6 +517,20 @@ __device__ void expand_level(const Params& p, Smem& sm, int4* F, unsigned ls,
   flush_count(sm, kStEntries, c_entries);
 }
 
+// Appends one (row, col) record to the ALTERNATE write log; lanes that reach
+// this point together share one atomic.
+__device__ __forceinline__ void log_write(const Params& p, int row, int col) {
+  cg::coalesced_group g = cg::coalesced_threads();
+  unsigned base = 0;
+  if (g.thread_rank() == 0) base = atomicAdd(&p.ctl->n_log, g.size());
+  base = g.shfl(base, 0) + g.thread_rank();
+  if (base < p.log_cap) {
+    asm volatile("st.global.v2.b32 [%0], {%1,%2};" ::"l"(p.wlog + base), "r"(row), "r"(col) : "memory");
+  } else {
+    st_rlx(&p.ctl->log_overflow, 1u);
+  }
+}
+
 // ALTERNATE walk (gpu_match.cpp:144-154): swap pairs toward the root, break
 // on a column another walk already claimed this phase.
 __device__ __forceinline__ void alternate_walk(const Params& p, unsigned& walks, unsigned& nsteps, int row) {
@@ -376,9 +539,13 @@ __device__ __forceinline__ void alternate_walk(const Params& p, unsigned& walks,
     const int col = ld_cg(p.pred + row);
     if (col < 0) break;
     const int mr = ld_rlx(p.cmatch + col);
-    if (mr >= 0 && ld_cg(p.pred + mr) == col) break;
+    if (mr >= 0 && ld_cg(p.pred + mr) == col) {
+      if (steps > 0) log_write(p, row, -1);  // left dangling: its column now belongs to another row
+      break;
+    }
     st_rlx(p.cmatch + col, row);
     st_rlx(p.rmatch + row, col);
+    log_write(p, row, col);
     row = mr;
     if (++steps > p.nc) {
       p.ctl->error = kErrWalk;
@@ -389,16 +556,26 @@ __device__ __forceinline__ void alternate_walk(const Params& p, unsigned& walks,
   walks++;
 }
 
+// FIX rules 1 and 2 for one row (gpu_match.cpp:221-237). The CAS keeps the
+// reset count exact when a row is listed more than once.
 __device__ __forceinline__ void fix_row(const Params& p, unsigned& resets, int r) {
-  const int v = ld_cg(p.rmatch + r);
+  const int v = ld_rlx(p.rmatch + r);
   if (v == -2) {
-    st_plain(p.rmatch + r, -1);
-    resets++;
-  } else if (v >= 0 && ld_cg(p.cmatch + v) != r) {
-    st_plain(p.rmatch + r, -1);
-    resets++;
+    if (atomicCAS(p.rmatch + r, -2, -1) == -2) resets++;
+  } else if (v >= 0 && ld_rlx(p.cmatch + v) != r) {
+    if (atomicCAS(p.rmatch + r, v, -1) == v) resets++;
   }
-  st_plain(p.pred + r, -1);
+}
+
+// FIX rule 3 for one column (gpu_match.cpp:238-243); returns true if the
+// column is unmatched afterwards.
+__device__ __forceinline__ bool fix_col(const Params& p, unsigned& resets, int c) {
+  const int r = ld_rlx(p.cmatch + c);
+  if (r >= 0 && ld_rlx(p.rmatch + r) != c) {
+    if (atomicCAS(p.cmatch + c, r, -1) == r) resets++;
+    return true;
+  }
+  return r < 0;
 }
 
 struct PhaseOut {
@@ -409,8 +586,8 @@ struct PhaseOut {
 
 // One phase = run_phase (gpu_match.cpp:268-302) from the roots in F[cur].
 template <bool WR, bool IMP>
-__device__ PhaseOut run_phase(const Params& p, Smem& sm, int cur, int parity,
-                              bool serial_alt, long long isolated) {
+__device__ PhaseOut run_phase(const Params& p, Smem& sm, int cur, int parity, bool serial_alt,
+                              long long isolated) {
   Ctrl* ctl = p.ctl;
   int4* F = cur ? p.F1 : p.F0;
   int4* Fn = cur ? p.F0 : p.F1;
@@ -422,7 +599,6 @@ __device__ PhaseOut run_phase(const Params& p, Smem& sm, int cur, int parity,
   unsigned n = n0;
   unsigned T = (unsigned)(rp & kEdgeMask);
   unsigned ls = 0;
-  unsigned n_next = 0;
   int lv = 0;
   bool found = false;
   for (;;) {
@@ -433,11 +609,13 @@ __device__ PhaseOut run_phase(const Params& p, Smem& sm, int cur, int parity,
       z->packed = 0;
       z->tile = 0;
     }
-    expand_level<WR, IMP>(p, sm, F, ls, n, T, in, outs, kStartLevel + lv, parity);
+    expand_level<WR, IMP>(p, sm, F, ls, n, T, (lv & 1) ? p.gidx1 : p.gidx0, (lv & 1) ? p.gidx0 : p.gidx1,
+                          in, outs, kStartLevel + lv, parity);
     grid_sync(ctl);
+    tl_mark(p, kTlLevel, (unsigned)lv);
     out.launches++;
     const unsigned long long op = ld_rlx(&outs->packed);
-    n_next = (unsigned)(op >> 33);
+    const unsigned n_next = (unsigned)(op >> 33);
     found = ld_rlx(&ctl->path_found[parity]) != 0u;
     if (p.apsb && found) break;
     if (n_next == 0) break;
@@ -450,7 +628,6 @@ __device__ PhaseOut run_phase(const Params& p, Smem& sm, int cur, int parity,
       break;
     }
   }
-  const unsigned nvis = ls + n + n_next;  // every column claimed this phase
   out.found = found;
   if (p.stop_after_bfs) return out;
 
@@ -486,14 +663,20 @@ __device__ PhaseOut run_phase(const Params& p, Smem& sm, int cur, int parity,
   flush_count(sm, kStWalks, walks);
   flush_count(sm, kStSteps, steps);
   grid_sync(ctl);
+  tl_mark(p, kTlAlt, 0);
 
-  // ---- FIXMATCHING rows (rules 1 and 2), restricted to touched rows ----
-  for (unsigned long long k = global_thread(); k < nvis; k += global_threads()) {
-    const int r = ld_cg(p.FR + k);
-    if (r >= 0) fix_row(p, resets, r);
+  // ---- FIXMATCHING rules 1+2 over the rows ALTERNATE wrote or left behind ----
+  const bool dense = ld_rlx(&ctl->log_overflow) != 0u;
+  const unsigned n_log = dense ? 0u : min(ld_rlx(&ctl->n_log), p.log_cap);
+  if (!dense) {
+    for (unsigned long long k = global_thread(); k < n_log; k += global_threads())
+      fix_row(p, resets, ld_cg(reinterpret_cast<const int*>(p.wlog + k)));
+    for (unsigned long long k = global_thread(); k < n_ep; k += global_threads())
+      fix_row(p, resets, ld_cg(p.EP + k));
+  } else {  // log overflow: the reference's full pass
+    for (unsigned long long r = global_thread(); r < (unsigned long long)p.nr; r += global_threads())
+      fix_row(p, resets, (int)r);
   }
-  for (unsigned long long k = global_thread(); k < n_ep; k += global_threads())
-    fix_row(p, resets, ld_cg(p.EP + k));
   for (unsigned long long k = global_thread(); k < (unsigned long long)p.nvis_words; k += global_threads())
     st_plain(reinterpret_cast<int*>(p.vis) + k, 0);
   if (is_leader()) {
@@ -505,35 +688,73 @@ __device__ PhaseOut run_phase(const Params& p, Smem& sm, int cur, int parity,
     ctl->roots.tile = 0;
   }
   grid_sync(ctl);
+  tl_mark(p, kTlFixRows, dense ? 1u : 0u);
 
-  // ---- FIXMATCHING columns (rule 3) + next phase's roots and bfs init ----
-  const unsigned wtotal = gridDim.x * (kThreads / 32);
-  const unsigned wid = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
-  for (unsigned long long b = (unsigned long long)wid * 32; b < nvis; b += (unsigned long long)wtotal * 32) {
-    const unsigned long long k = b + lane_id();
-    bool unmatched = false;
-    int c = 0;
+  // ---- FIXMATCHING rule 3 over the columns ALTERNATE wrote; a non-root column
+  //      it unmatches becomes a root of the next phase ----
+  const unsigned long long ncheck = dense ? (unsigned long long)p.nc : n_log;
+  for (unsigned long long b = (unsigned long long)blockIdx.x * kThreads; b < ncheck; b += global_threads()) {
+    const unsigned long long k = b + threadIdx.x;
+    bool push = false;
+    int c = -1;
     unsigned beg = 0, deg = 0;
-    if (k < nvis) {
-      c = ld_cg(reinterpret_cast<const int*>(F + k));
-      int r = ld_cg(p.cmatch + c);
-      if (r >= 0 && ld_cg(p.rmatch + r) != c) {
-        st_plain(p.cmatch + c, -1);
-        resets++;
-        r = -1;
-      }
-      st_plain(p.bfs + c, r >= 0 ? kUnvisited : kStartLevel);  // init_bfs_array for next phase
-      if (r < 0) {
-        unmatched = true;
-        beg = ld_ro(p.offs + c);
-        deg = ld_ro(p.offs + c + 1) - beg;
+    if (k < ncheck) {
+      c = dense ? (int)k : ld_cg(reinterpret_cast<const int*>(p.wlog + k) + 1);
+      if (c >= 0 && fix_col(p, resets, c)) {
+        // roots of this phase are handled below; others enter the root set once
+        if (dense) {
+          push = ld_rlx(p.bfs + c) == kUnvisited;
+          if (push) st_rlx(p.bfs + c, kStartLevel);
+        } else {
+          push = atomicCAS(p.bfs + c, kUnvisited, kStartLevel) == kUnvisited;
+        }
+        if (push) {
+          beg = ld_ro(p.offs + c);
+          deg = ld_ro(p.offs + c + 1) - beg;
+          push = deg > 0;
+        }
       }
     }
-    push_entries(unmatched, c, c, beg, deg, -1, &ctl->roots, Fn, p.FR, 0u);
+    unsigned long long slot;
+    unsigned unused;
+    if (cta_reserve(sm, push ? 1u : 0u, push ? deg : 0u, 0u, &ctl->roots, &ctl->n_ep, slot, unused) && push)
+      put_entry(Fn, 0u, p.gidx0, slot, c, c, beg, deg);
   }
-  if (is_leader()) ctl->n_ep = 0u;
+  if (is_leader()) {
+    ctl->n_ep = 0u;
+    ctl->n_log = 0u;
+    ctl->log_overflow = 0u;
+  }
+  grid_sync(ctl);
+  tl_mark(p, kTlFixCols, n_log);
+
+  // ---- this phase's roots: still unmatched -> root again; matched -> bfs 1 ----
+  for (unsigned long long b = (unsigned long long)blockIdx.x * kThreads; b < n0; b += global_threads()) {
+    const unsigned long long k = b + threadIdx.x;
+    bool push = false;
+    int c = -1;
+    unsigned beg = 0, deg = 0;
+    if (k < n0) {
+      const int4 ent = ld_cg(F + k);
+      c = ent.x;
+      if (ld_rlx(p.cmatch + c) < 0) {
+        push = true;
+        beg = (unsigned)ent.z;
+        const unsigned nxt = (k + 1 < n0) ? ld_cg_u(F + k + 1) : (unsigned)(rp & kEdgeMask);
+        deg = nxt - (unsigned)ent.w;
+        st_plain(p.bfs + c, kStartLevel);
+      } else {
+        st_plain(p.bfs + c, kUnvisited);
+      }
+    }
+    unsigned long long slot;
+    unsigned unused;
+    if (cta_reserve(sm, push ? 1u : 0u, push ? deg : 0u, 0u, &ctl->roots, &ctl->n_ep, slot, unused) && push)
+      put_entry(Fn, 0u, p.gidx0, slot, c, c, beg, deg);
+  }
   flush_count(sm, kStResets, resets);
   grid_sync(ctl);
+  tl_mark(p, kTlRoots, 0);
   const unsigned long long np = ld_rlx(&ctl->roots.packed);
   out.after = (long long)p.nc - isolated - (long long)(np >> 33);
   return out;
@@ -546,6 +767,7 @@ __global__ void __launch_bounds__(kThreads, 2) driver_kernel(Params p) {
   Ctrl* ctl = p.ctl;
   if (threadIdx.x < kNumStats) sm.cnt[threadIdx.x] = 0;
   __syncthreads();
+  tl_mark(p, kTlStart, p.fresh);
 
   int cur;
   long long card, outer, isolated;
@@ -568,15 +790,14 @@ __global__ void __launch_bounds__(kThreads, 2) driver_kernel(Params p) {
           }
         }
         grid_sync(ctl);
+        tl_mark(p, kTlInit, pass);
       }
     }
     // ---- setup: validate init, bfs_array init, roots of phase 1 ----
     unsigned long long bad = 0, iso = 0;
-    const unsigned wtotal = gridDim.x * (kThreads / 32);
-    const unsigned wid = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
-    for (unsigned long long b = (unsigned long long)wid * 32; b < (unsigned long long)p.nc;
-         b += (unsigned long long)wtotal * 32) {
-      const unsigned long long c = b + lane_id();
+    for (unsigned long long b = (unsigned long long)blockIdx.x * kThreads; b < (unsigned long long)p.nc;
+         b += global_threads()) {
+      const unsigned long long c = b + threadIdx.x;
       bool root = false;
       unsigned beg = 0, deg = 0;
       if (c < (unsigned long long)p.nc) {
@@ -590,7 +811,10 @@ __global__ void __launch_bounds__(kThreads, 2) driver_kernel(Params p) {
           if (deg > 0) root = true; else iso++;
         }
       }
-      push_entries(root, (int)c, (int)c, beg, deg, -1, &ctl->roots, p.F0, p.FR, 0u);
+      unsigned long long slot;
+      unsigned unused;
+      if (cta_reserve(sm, root ? 1u : 0u, root ? deg : 0u, 0u, &ctl->roots, &ctl->n_ep, slot, unused) && root)
+        put_entry(p.F0, 0u, p.gidx0, slot, (int)c, (int)c, beg, deg);
     }
     for (unsigned long long r = global_thread(); r < (unsigned long long)p.nr; r += global_threads()) {
       const int v = ld_cg(p.rmatch + r);
@@ -604,6 +828,7 @@ __global__ void __launch_bounds__(kThreads, 2) driver_kernel(Params p) {
       if (iso) atomicAdd(&ctl->isolated, iso);
     }
     grid_sync(ctl);
+    tl_mark(p, kTlSetup, 0);
     if (ld_rlx(&ctl->invalid) != 0ull) {
       if (is_leader()) ctl->error = kErrInvalidInit;
       return;
@@ -681,6 +906,7 @@ __global__ void __launch_bounds__(kThreads, 2) driver_kernel(Params p) {
   }
 
   // ---- flush counters and run state ----
+  tl_mark(p, kTlEnd, 0);
   __syncthreads();
   if (threadIdx.x < kNumStats && sm.cnt[threadIdx.x]) atomicAdd(&ctl->stats[threadIdx.x], sm.cnt[threadIdx.x]);
   if (is_leader()) {
@@ -805,10 +1031,28 @@ void dfree(T*& p) {
   p = nullptr;
 }
 
+// Graph-sized buffers only grow: re-uploading a graph of the same or smaller
+// size reuses them (cudaMalloc/cudaFree of GB buffers costs milliseconds).
+struct CapMap {
+  std::vector<std::pair<const void*, size_t>> caps;
+  size_t& operator[](const void* k) {
+    for (auto& kv : caps)
+      if (kv.first == k) return kv.second;
+    caps.emplace_back(k, 0);
+    return caps.back().second;
+  }
+};
+
 template <typename T>
-cudaError_t dalloc(T*& p, size_t count) {
+cudaError_t dalloc(CapMap& cm, T*& p, size_t count) {
+  count = std::max<size_t>(count, 1);
+  size_t& cap = cm[&p];
+  if (p && cap >= count) return cudaSuccess;
   dfree(p);
-  return cudaMalloc(reinterpret_cast<void**>(&p), std::max<size_t>(count, 1) * sizeof(T));
+  cap = 0;
+  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&p), count * sizeof(T));
+  if (e == cudaSuccess) cap = count;
+  return e;
 }
 
 }  // namespace
@@ -829,15 +1073,18 @@ struct bm_handle {
   int* adj = nullptr;
   // state
   int *rmatch = nullptr, *cmatch = nullptr, *pred = nullptr, *bfs = nullptr;
-  int *rmatch0 = nullptr, *cmatch0 = nullptr, *FR = nullptr, *EP = nullptr;
+  int *rmatch0 = nullptr, *cmatch0 = nullptr, *EP = nullptr;
   unsigned* vis = nullptr;
   int nvis_words = 0;
   int4* F[2] = {nullptr, nullptr};
+  unsigned* gidx[2] = {nullptr, nullptr};
+  int2* wlog = nullptr;
+  unsigned log_cap = 0;
   Ctrl* ctl = nullptr;
   PhaseRec* recs = nullptr;
   int rec_cap = 4096;
   bool has_init = false;
-  bool clean = false;   // pred == -1 and vis == 0 everywhere
+  bool clean = false;   // vis == 0 everywhere (pred needs no reset, see the kernel header)
   bool resumable = false;
   bm_match_opts run_opts{};
   std::vector<long long> phase_launches;  // per outer iteration, current run
@@ -845,6 +1092,10 @@ struct bm_handle {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   double last_ms = 0.0;
   int last_launches = 0;
+  CapMap caps;
+  unsigned long long* tl = nullptr;
+  unsigned tl_cap = 1u << 16;
+  std::vector<unsigned long long> timeline;  // host copy for the last run
 };
 
 namespace {
@@ -887,12 +1138,13 @@ int grid_for(bm_handle* h, int v) {
   return (int)std::max<long long>(1, std::min(maxg, want));
 }
 
-// Resets pred/vis when a previous call left them dirty, and the control block.
-bm_status prepare_fresh(bm_handle* h) {
-  if (!h->clean) {
-    BM_CUDA(cudaMemsetAsync(h->pred, 0xff, sizeof(int) * std::max(h->nr, 1), h->stream));
+// Clears the visited bitmap when a previous call left it dirty, optionally
+// resets predecessors (only for parity probes that report them), and zeroes
+// the control block.
+bm_status prepare_fresh(bm_handle* h, bool reset_pred = false) {
+  if (!h->clean)
     BM_CUDA(cudaMemsetAsync(h->vis, 0, sizeof(unsigned) * std::max(h->nvis_words, 1), h->stream));
-  }
+  if (reset_pred) BM_CUDA(cudaMemsetAsync(h->pred, 0xff, sizeof(int) * std::max(h->nr, 1), h->stream));
   BM_CUDA(cudaMemsetAsync(h->ctl, 0, sizeof(Ctrl), h->stream));
   h->clean = false;
   return BM_OK;
@@ -923,8 +1175,14 @@ Params make_params(bm_handle* h, const bm_match_opts& o) {
   p.nvis_words = h->nvis_words;
   p.F0 = h->F[0];
   p.F1 = h->F[1];
-  p.FR = h->FR;
+  p.gidx0 = h->gidx[0];
+  p.gidx1 = h->gidx[1];
   p.EP = h->EP;
+  p.wlog = h->wlog;
+  p.log_cap = h->log_cap;
+  p.trace = 0;
+  p.tl = h->tl;
+  p.tl_cap = h->tl_cap;
   p.ctl = h->ctl;
   p.recs = h->recs;
   p.rec_cap = h->rec_cap;
@@ -961,6 +1219,7 @@ bm_status drive(bm_handle* h, const bm_match_opts& o, bool fresh, int64_t* cardi
   Params p = make_params(h, o);
   p.fresh = fresh ? 1 : 0;
   if (fresh) {
+    h->timeline.clear();
     h->phase_launches.clear();
     h->last_ms = 0.0;
     h->last_launches = 0;
@@ -981,6 +1240,14 @@ bm_status drive(bm_handle* h, const bm_match_opts& o, bool fresh, int64_t* cardi
     h->last_ms += ms;
     h->last_launches += 1;
     BM_CUDA(cudaMemcpy(&ctl, h->ctl, sizeof(Ctrl), cudaMemcpyDeviceToHost));
+    {
+      const unsigned nt = std::min(ctl.n_tl, h->tl_cap);
+      const size_t old = h->timeline.size();
+      h->timeline.resize(old + 2 * (size_t)nt);
+      if (nt) BM_CUDA(cudaMemcpy(h->timeline.data() + old, h->tl, sizeof(unsigned long long) * 2 * nt,
+                                 cudaMemcpyDeviceToHost));
+      BM_CUDA(cudaMemsetAsync(&h->ctl->n_tl, 0, sizeof(unsigned), h->stream));
+    }
     if (ctl.error) {
       h->resumable = false;
       return ctl_error_status(ctl.error);
@@ -1110,6 +1377,7 @@ bm_status bm_create(int32_t device, bm_handle** out) {
   if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void**>(&h->ctl), sizeof(Ctrl));
   if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void**>(&h->recs), sizeof(PhaseRec) * h->rec_cap);
   if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void**>(&h->scratch), sizeof(unsigned long long) * 4);
+  if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void**>(&h->tl), sizeof(unsigned long long) * 2 * h->tl_cap);
   if (e != cudaSuccess) {
     bm_destroy(h);
     return cuda_fail(e, "bm_create");
@@ -1131,13 +1399,16 @@ bm_status bm_destroy(bm_handle* h) {
   dfree(h->bfs);
   dfree(h->rmatch0);
   dfree(h->cmatch0);
-  dfree(h->FR);
   dfree(h->EP);
+  dfree(h->gidx[0]);
+  dfree(h->gidx[1]);
+  dfree(h->wlog);
   dfree(h->vis);
   dfree(h->F[0]);
   dfree(h->F[1]);
   dfree(h->ctl);
   dfree(h->recs);
+  dfree(h->tl);
   dfree(h->scratch);
   if (h->ev0) cudaEventDestroy(h->ev0);
   if (h->ev1) cudaEventDestroy(h->ev1);
@@ -1169,21 +1440,25 @@ bm_status bm_upload_csc(bm_handle* h, int32_t nc, int32_t nr, const int64_t* cxa
   h->has_init = false;
   h->resumable = false;
   // graph
-  BM_CUDA(dalloc(h->offs, (size_t)nc + 1));
-  BM_CUDA(dalloc(h->adj, (size_t)E));
+  BM_CUDA(dalloc(h->caps, h->offs, (size_t)nc + 1));
+  BM_CUDA(dalloc(h->caps, h->adj, (size_t)E));
   // state (sized by the graph)
-  BM_CUDA(dalloc(h->rmatch, nr));
-  BM_CUDA(dalloc(h->cmatch, nc));
-  BM_CUDA(dalloc(h->pred, nr));
-  BM_CUDA(dalloc(h->bfs, nc));
-  BM_CUDA(dalloc(h->rmatch0, nr));
-  BM_CUDA(dalloc(h->cmatch0, nc));
-  BM_CUDA(dalloc(h->FR, nc));
-  BM_CUDA(dalloc(h->EP, nr));
+  BM_CUDA(dalloc(h->caps, h->rmatch, nr));
+  BM_CUDA(dalloc(h->caps, h->cmatch, nc));
+  BM_CUDA(dalloc(h->caps, h->pred, nr));
+  BM_CUDA(dalloc(h->caps, h->bfs, nc));
+  BM_CUDA(dalloc(h->caps, h->rmatch0, nr));
+  BM_CUDA(dalloc(h->caps, h->cmatch0, nc));
+  BM_CUDA(dalloc(h->caps, h->EP, nr));
+  const size_t ngran = (size_t)(E / kGran) + 2;
+  BM_CUDA(dalloc(h->caps, h->gidx[0], ngran));
+  BM_CUDA(dalloc(h->caps, h->gidx[1], ngran));
+  h->log_cap = (unsigned)std::min<long long>((long long)nr + nc + 1024, 0xffffffffll);
+  BM_CUDA(dalloc(h->caps, h->wlog, h->log_cap));
   h->nvis_words = (nc + 31) / 32;
-  BM_CUDA(dalloc(h->vis, h->nvis_words));
-  BM_CUDA(dalloc(h->F[0], nc));
-  BM_CUDA(dalloc(h->F[1], nc));
+  BM_CUDA(dalloc(h->caps, h->vis, h->nvis_words));
+  BM_CUDA(dalloc(h->caps, h->F[0], nc));
+  BM_CUDA(dalloc(h->caps, h->F[1], nc));
   // offsets: int64 staged in F[1] (16 B per column >= 8 B per offset), narrowed to u32
   long long* staged = reinterpret_cast<long long*>(h->F[1]);
   BM_CUDA(cudaMemcpyAsync(staged, cxadj, sizeof(long long) * ((size_t)nc + 1), cudaMemcpyHostToDevice, h->stream));
@@ -1290,6 +1565,16 @@ bm_status bm_last_kernel_time(bm_handle* h, double* ms, int32_t* launches) {
   return BM_OK;
 }
 
+bm_status bm_timeline(bm_handle* h, uint64_t* out, int64_t cap, int64_t* n) {
+  bm_status s = check_handle(h, false);
+  if (s != BM_OK) return s;
+  const int64_t total = (int64_t)h->timeline.size() / 2;
+  if (n) *n = total;
+  if (out && cap > 0)
+    std::memcpy(out, h->timeline.data(), sizeof(uint64_t) * 2 * (size_t)std::min<int64_t>(cap, total));
+  return BM_OK;
+}
+
 bm_status bm_match(bm_handle* h, const bm_match_opts* opts, int32_t* rmatch, int32_t* cmatch,
                    int64_t* cardinality, bm_counters* counters, int64_t* per_iter, int64_t cap,
                    bm_phase_cb cb, void* user) {
@@ -1332,11 +1617,12 @@ bm_status bm_bfs_phase(bm_handle* h, int32_t driver, int32_t bfs_kernel, int32_t
   BM_CUDA(cudaSetDevice(h->device));
   if (h->nr > 0) BM_CUDA(cudaMemcpyAsync(h->rmatch, rmatch_in, sizeof(int) * h->nr, cudaMemcpyHostToDevice, h->stream));
   if (h->nc > 0) BM_CUDA(cudaMemcpyAsync(h->cmatch, cmatch_in, sizeof(int) * h->nc, cudaMemcpyHostToDevice, h->stream));
-  s = prepare_fresh(h);
+  s = prepare_fresh(h, true);
   if (s != BM_OK) return s;
   const int v = variant_of(bfs_kernel == BM_BFS_WR, improved);
   Params p = make_params(h, o);
   p.stop_after_bfs = 1;
+  p.trace = 1;
   p.max_phases = 1;
   float ms = 0.f;
   s = launch(h, v, p, &ms);

@@ -335,8 +335,10 @@ bm_status bm_check_csc(int32_t nc, int32_t nr, const int64_t* cxadj, const int32
   if (nc < 0 || nr < 0) return hfail(BM_ERR_INVALID_ARG, "negative vertex count");
   if (!cxadj) return hfail(BM_ERR_INVALID_ARG, "null cxadj");
   if (cxadj[0] != 0) return hfail(BM_ERR_INVALID_ARG, "cxadj[0] is not 0");
-  for (int c = 0; c < nc; ++c) {
+  // Offsets first, so a malformed array never drives an out-of-bounds read of cadj.
+  for (int c = 0; c < nc; ++c)
     if (cxadj[c] > cxadj[c + 1]) return hfail(BM_ERR_INVALID_ARG, "cxadj decreases at column " + std::to_string(c));
+  for (int c = 0; c < nc; ++c) {
     for (int64_t j = cxadj[c]; j < cxadj[c + 1]; ++j) {
       if (cadj[j] < 0 || cadj[j] >= nr)
         return hfail(BM_ERR_INVALID_ARG, "row index out of range in column " + std::to_string(c));

@@ -1,0 +1,78 @@
+"""Map an ncu SASS-level source page onto CUDA source lines.
+
+usage: python scripts/sass_lines.py <report.ncu-rep> <cubin> <mangled-kernel-name> [topN]
+
+The cubin must be the one that was profiled (extract with
+`cuobjdump -xelf all paper_1303_1379_b200/libbmatch_b200.so` at profile time).
+Per source line: instructions executed, warp-stall samples and the dominant
+stall reason.
+"""
+import csv
+import io
+import re
+import subprocess
+import sys
+from collections import defaultdict
+
+
+def line_map(cubin, fn):
+    out = subprocess.run(["nvdisasm", "-g", "-c", cubin], capture_output=True, text=True).stdout
+    m = {}
+    cur_line = None
+    in_fn = False
+    for ln in out.splitlines():
+        if ln.startswith(".text.") or "--------------------- .text." in ln:
+            in_fn = (fn in ln)
+            continue
+        if not in_fn:
+            continue
+        mm = re.search(r'//## File ".*?", line (\d+)', ln)
+        if mm:
+            cur_line = int(mm.group(1))
+            continue
+        mi = re.match(r"\s*/\*([0-9a-f]{4,})\*/", ln)
+        if mi and cur_line is not None:
+            m[int(mi.group(1), 16)] = cur_line
+    return m
+
+
+def main():
+    rep, cubin, fn = sys.argv[1:4]
+    top = int(sys.argv[4]) if len(sys.argv) > 4 else 40
+    csvtxt = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(csvtxt)))
+    hdr = rows[1]
+    idx = {k: i for i, k in enumerate(hdr)}
+    data = rows[2:]
+    addrs = [int(r[idx["Address"]], 16) for r in data if r[idx["Address"]].startswith("0x")]
+    base = min(addrs)
+    lm = line_map(cubin, fn)
+    stalls = [k for k in hdr if k.startswith("stall_") and "Not Issued" not in k]
+    agg = defaultdict(lambda: defaultdict(float))
+    for r in data:
+        if not r[idx["Address"]].startswith("0x"):
+            continue
+        off = int(r[idx["Address"]], 16) - base
+        line = lm.get(off, -1)
+        a = agg[line]
+        a["inst"] += float(r[idx["Instructions Executed"]] or 0)
+        a["samples"] += float(r[idx["# Samples"]] or 0)
+        for k in stalls:
+            a[k] += float(r[idx[k]] or 0)
+    src = {}
+    try:
+        for i, t in enumerate(open("paper_1303_1379_b200/csrc/bm_engine.cu").read().splitlines(), 1):
+            src[i] = t.strip()
+    except OSError:
+        pass
+    tot_i = sum(a["inst"] for a in agg.values())
+    tot_s = sum(a["samples"] for a in agg.values())
+    print(f"total warp-inst {tot_i:.3e}  samples {tot_s:.0f}")
+    for line, a in sorted(agg.items(), key=lambda kv: -kv[1]["samples"])[:top]:
+        st = max(stalls, key=lambda k: a[k]) if stalls else ""
+        print(f"{line:5d} inst {100 * a['inst'] / tot_i:5.1f}%  samp {100 * a['samples'] / tot_s:5.1f}%  "
+              f"{st[6:]:14s} {src.get(line, '')[:80]}")
+
+
+if __name__ == "__main__":
+    main()
