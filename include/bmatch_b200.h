@@ -70,7 +70,9 @@ typedef struct bm_match_opts {
   int32_t init;              /* bm_init */
   int32_t max_phases;        /* 0 = run to the maximum (bound nc+1); >0 = stop after that many
                                 outer iterations and return with *done = 0 (resumable) */
-  int32_t reserved[3];
+  int32_t reserved[3];       /* reserved[0]: WR claim policy (tuning): 0 = the reference's (a
+                                found tree's columns are skipped at expansion only, default),
+                                1 = also stop claiming at discovery; others must be 0 */
 } bm_match_opts;
 
 /* PhaseCounters (gpu_match.hpp:39-52) plus the device-side work counters the
@@ -164,6 +166,12 @@ bm_status   bm_last_kernel_time(bm_handle* h, double* ms, int32_t* launches);
  * 4 ALTERNATE, 5 FIX rows, 6 FIX columns, 7 roots of the next phase, 8 end.
  * Written by one thread after each grid barrier (a few ns per stage). */
 bm_status   bm_timeline(bm_handle* h, uint64_t* out, int64_t cap, int64_t* n);
+
+/* Raw device counters of the last run (profiling): edges traversed, columns
+ * expanded/visited, frontier entries, walks, walk steps, FIX resets, levels,
+ * serial retries, dense-FIX fallbacks, then per-part CTA cycle totals
+ * (tile fetch, window setup, rounds, flush, grid barrier, other). */
+bm_status   bm_debug_stats(bm_handle* h, uint64_t* out, int64_t cap, int64_t* n);
 
 /* ---- one BFS phase without ALTERNATE/FIX (parity probes) ----------------
  * Mirrors run_phase up to expand_bfs (gpu_match.cpp:268-290) from the given

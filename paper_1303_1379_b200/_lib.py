@@ -14,7 +14,7 @@ import re
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libbmatch_b200.so")
+LIB_PATH = os.environ.get("BM_LIB") or os.path.join(_HERE, "libbmatch_b200.so")  # BM_LIB: alternative build (tuning)
 HEADERS = [
     os.path.join(os.path.dirname(_HERE), "include", "bmatch_b200.h"),
     os.path.join(os.path.dirname(_HERE), "include", "bmatch_b200_gen.h"),
@@ -104,6 +104,7 @@ _PROTOS = {
     "bm_download_matching": (C.c_int, [_vp, _i32p, _i32p]),
     "bm_last_kernel_time": (C.c_int, [_vp, C.POINTER(C.c_double), _i32p]),
     "bm_timeline": (C.c_int, [_vp, C.POINTER(C.c_uint64), C.c_int64, _i64p]),
+    "bm_debug_stats": (C.c_int, [_vp, C.POINTER(C.c_uint64), C.c_int64, _i64p]),
     "bm_bfs_phase": (C.c_int, [_vp, C.c_int32, C.c_int32, C.c_int32, _i32p, _i32p, _i32p, _i32p, _i32p,
                                _i64p, _i32p]),
     "bm_verify": (C.c_int, [_vp, _i32p, _i32p, _i64p, _i32p, _i64p]),

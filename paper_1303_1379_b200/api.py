@@ -142,8 +142,10 @@ class AlgorithmResult:
     counters: Optional[PhaseCounters] = None
 
 
-def _opts(shortest: bool, kernel: BfsKernel, improved: bool, init_mode: str, max_phases: int = 0):
+def _opts(shortest: bool, kernel: BfsKernel, improved: bool, init_mode: str, max_phases: int = 0,
+          claim_mode: int = 0):
     o = _lib.bm_match_opts()
+    o.reserved[0] = claim_mode
     o.driver = _lib.BM_DRIVER_APSB if shortest else _lib.BM_DRIVER_APFB
     o.bfs_kernel = int(kernel)
     o.improved = 1 if improved else 0
@@ -273,9 +275,9 @@ class Engine:
         check(lib.bm_load_matching(self._h, i32p(m.rmatch), i32p(m.cmatch)))
 
     def run(self, *, shortest=False, kernel=BfsKernel.GpubfsWr, improved=False, init_mode="given",
-            max_phases=0, observer=None, resume=False):
+            max_phases=0, observer=None, resume=False, claim_mode=0):
         """Device-resident run (bm_run / bm_resume). Returns (cardinality, counters, done)."""
-        o = _opts(shortest, kernel, improved, init_mode, max_phases)
+        o = _opts(shortest, kernel, improved, init_mode, max_phases, claim_mode)
         ct = _lib.bm_counters()
         nc = self._nc()
         cap = nc + 2
@@ -323,6 +325,16 @@ class Engine:
             tag, t = int(buf[2 * i]), int(buf[2 * i + 1])
             out.append((self.TL_KINDS.get(tag >> 32, str(tag >> 32)), tag & 0xFFFFFFFF, t))
         return out
+
+    STAT_NAMES = ["edges_traversed", "columns_scanned", "columns_visited", "frontier_entries", "walks",
+                  "walk_steps", "fix_resets", "levels", "serial_retries", "dense_fix", "cyc_tile", "cyc_window",
+                  "cyc_rounds", "cyc_flush", "cyc_barrier", "cyc_other"]
+
+    def debug_stats(self) -> dict:
+        buf = np.zeros(32, np.uint64)
+        n = C.c_int64()
+        check(lib.bm_debug_stats(self._h, buf.ctypes.data_as(C.POINTER(C.c_uint64)), 32, C.byref(n)))
+        return {name: int(buf[i]) for i, name in enumerate(self.STAT_NAMES[:n.value])}
 
     def bfs_phase(self, g: BipartiteCsr, m: MatchingState, *, shortest=False, kernel=BfsKernel.Gpubfs,
                   improved=False):

@@ -103,6 +103,27 @@ __device__ __forceinline__ unsigned long long policy_evict_first() {
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
   return pol;
 }
+__device__ __forceinline__ unsigned long long policy_evict_last() {
+  unsigned long long pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+// Coherent (L2) load with an L2 eviction-priority hint.
+__device__ __forceinline__ int ld_rlx_hint(const int* p, unsigned long long pol) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned ld_rlx_hint(const unsigned* p, unsigned long long pol) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned ld_ro_hint(const unsigned* p, unsigned long long pol) {
+  unsigned v;
+  asm("ld.global.nc.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+  return v;
+}
 __device__ __forceinline__ int ld_stream(const int* p, unsigned long long pol) {
   int v;
   asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
@@ -122,6 +143,10 @@ __device__ __forceinline__ void st_stream(int4* p, int4 v, unsigned long long po
   asm volatile("st.global.L2::cache_hint.v4.b32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
                "r"(v.w), "l"(pol)
                : "memory");
+}
+
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(p));
 }
 
 // ---- warp helpers ----------------------------------------------------------

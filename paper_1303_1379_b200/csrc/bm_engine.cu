@@ -60,7 +60,10 @@ namespace cg = cooperative_groups;
 
 namespace bm {
 
-constexpr int kThreads = 512;         // threads per CTA
+#ifndef BM_THREADS
+#define BM_THREADS 256
+#endif
+constexpr int kThreads = BM_THREADS;  // threads per CTA (1024 / kThreads CTAs per SM at <= 64 registers)
 constexpr int kItems = 4;             // edges per thread per round (memory-level parallelism)
 constexpr unsigned kGran = 512;       // edges per granule-index entry; tiles are whole granules
 constexpr unsigned kMaxTileGran = 8;  // <= 4096 edges per tile (= the winner buffer)
@@ -104,6 +107,12 @@ enum Stat : int {
   kStLevels,
   kStRetries,
   kStDenseFix,
+  kStCycTile,     // CTA cycles (thread 0's view) per part of expand_level and in grid barriers
+  kStCycWindow,
+  kStCycRounds,
+  kStCycFlush,
+  kStCycBarrier,
+  kStCycOther,
   kNumStats
 };
 
@@ -165,6 +174,7 @@ struct Params {
   int max_phases;
   int stop_after_bfs;
   int trace;        // write bfs_array level labels (parity probes)
+  int claim_mode;   // WR claim check at discovery: 0 none (reference, default), 1 coherent root-mark check
   long long phase_bound;
   unsigned long long* tl;  // stage timeline: (tag, %globaltimer ns) pairs written by the leader
   unsigned tl_cap;
@@ -246,6 +256,8 @@ __device__ __noinline__ void grid_sync(Ctrl* ctl) {
 
 __device__ __forceinline__ bool is_leader() { return blockIdx.x == 0 && threadIdx.x == 0; }
 
+__device__ __forceinline__ long long clk() { return clock64(); }
+
 __device__ __forceinline__ unsigned long long global_thread() {
   return (unsigned long long)blockIdx.x * kThreads + threadIdx.x;
 }
@@ -318,7 +330,7 @@ __device__ __forceinline__ void put_entry(int4* F, unsigned out_base, unsigned* 
 // One BFS level (GPUBFS, Alg. 2, gpu_match.cpp:42-70; GPUBFS-WR, Alg. 4,
 // gpu_match.cpp:99-133) over the frontier F[ls, ls+n) holding T edges.
 template <bool WR, bool IMP>
-__device__ void expand_level(const Params& p, Smem& sm, int4* F, unsigned ls, unsigned n, unsigned T,
+__device__ __forceinline__ void expand_level(const Params& p, Smem& sm, int4* F, unsigned ls, unsigned n, unsigned T,
                              const unsigned* gin, unsigned* gout, Slot* in, Slot* out, int level, int pf) {
   if (T == 0) return;
   const unsigned tid = threadIdx.x;
@@ -333,12 +345,24 @@ __device__ void expand_level(const Params& p, Smem& sm, int4* F, unsigned ls, un
   unsigned* const path_flag = &p.ctl->path_found[pf];
 
   const unsigned long long pol = policy_evict_first();
+#ifndef BM_KEEP
+#define BM_KEEP 1
+#endif
+  // BM_KEEP: 0 default priority for the gathered state; 1 rmatch evict_last;
+  // 2 rmatch + visited bitmap + offsets evict_last.
+  const unsigned long long keep = policy_evict_last();
   if (tid == 0) sm.nw = 0;
+  long long t_a = clk();
   for (;;) {
     if (tid == 0) sm.tile = atomicAdd(&in->tile, 1u);
     __syncthreads();
     const unsigned tile = sm.tile;
     __syncthreads();
+    if (tid == 0) {
+      const long long t = clk();
+      sm.cnt[kStCycTile] += t - t_a;
+      t_a = t;
+    }
     if (tile >= ntiles) break;
     const unsigned e0 = tile * ET;
     const unsigned e1 = (T - e0 < ET) ? T : e0 + ET;
@@ -396,6 +420,14 @@ __device__ void expand_level(const Params& p, Smem& sm, int4* F, unsigned ls, un
         __syncthreads();
       }
       const unsigned nq = (live + 31) >> 5;
+      if (tid == 0) {
+        const long long t = clk();
+        sm.cnt[kStCycWindow] += t - t_a;
+        t_a = t;
+      }
+      // Prefetch the next window's entries while this window's rounds run.
+      if (wend < e1 && i + kThreads + tid < n)
+        prefetch_l2(F + ls + i + kThreads + tid);
 
       // Rounds over the live edges: no CTA-wide barrier inside; winners are
       // staged in sm.wbuf.
@@ -421,14 +453,14 @@ __device__ void expand_level(const Params& p, Smem& sm, int4* F, unsigned ls, un
             c_trav++;
           }
         }
-        int rmark[kItems];  // WR: the root's mark, issued alongside the rmatch gather
 #pragma unroll
-        for (int k = 0; k < kItems; ++k) {
-          cm[k] = row[k] >= 0 ? ld_rlx(p.rmatch + row[k]) : -3;
-          rmark[k] = (WR && row[k] >= 0) ? ld_ca(p.bfs + sm.root[sl[k]]) : kStartLevel;
-        }
+        for (int k = 0; k < kItems; ++k)
+          cm[k] = row[k] >= 0 ? (BM_KEEP >= 1 ? ld_rlx_hint(p.rmatch + row[k], keep) : ld_rlx(p.rmatch + row[k]))
+                              : -3;
 #pragma unroll
-        for (int k = 0; k < kItems; ++k) w[k] = cm[k] >= 0 ? ld_rlx(p.vis + (cm[k] >> 5)) : kFull;
+        for (int k = 0; k < kItems; ++k)
+          w[k] = cm[k] >= 0 ? (BM_KEEP >= 2 ? ld_rlx_hint(p.vis + (cm[k] >> 5), keep) : ld_rlx(p.vis + (cm[k] >> 5)))
+                            : kFull;
         unsigned wins = 0, eps = 0;
 #pragma unroll
         for (int k = 0; k < kItems; ++k) {
@@ -438,10 +470,12 @@ __device__ void expand_level(const Params& p, Smem& sm, int4* F, unsigned ls, un
           if (c >= 0) {
             const unsigned bit = 1u << (c & 31);
             // WR: a tree whose root is already marked stops claiming columns.
-            if (!(w[k] & bit) && (!WR || rmark[k] >= kUnvisited)) {
+            // optional (claim_mode 1): a tree whose root is already marked stops claiming columns
+            if (!(w[k] & bit) && (!WR || p.claim_mode == 0 || ld_rlx(p.bfs + root) >= kUnvisited)) {
               const unsigned old = atomicOr(p.vis + (c >> 5), bit);
               if (!(old & bit)) {
                 wins |= 1u << k;
+                prefetch_l2(p.offs + c);  // the flush reads offs[c], offs[c+1]
                 st_stream(p.pred + row[k], col, pol);
                 if (p.trace) st_plain(p.bfs + c, level + 1);
               }
@@ -484,24 +518,42 @@ __device__ void expand_level(const Params& p, Smem& sm, int4* F, unsigned ls, un
         }
       }
       __syncthreads();
+      if (tid == 0) {
+        const long long t = clk();
+        sm.cnt[kStCycRounds] += t - t_a;
+        t_a = t;
+      }
       // Flush the window's winners: one CTA reservation for all of them.
       const unsigned nw = sm.nw;
       if (nw) {
-        unsigned cnt = 0, deg = 0;
-        for (unsigned j = tid; j < nw; j += kThreads) {
-          const int c = sm.wbuf[j].x;
-          deg += ld_ro(p.offs + c + 1) - ld_ro(p.offs + c);
-          cnt++;
-        }
         unsigned long long slot;
         unsigned unused;
-        cta_reserve(sm, cnt, deg, 0u, out, &p.ctl->n_ep, slot, unused);
-        for (unsigned j = tid; j < nw; j += kThreads) {
-          const int2 cr = sm.wbuf[j];
-          const unsigned b0 = ld_ro(p.offs + cr.x);
-          const unsigned d0 = ld_ro(p.offs + cr.x + 1) - b0;
-          put_entry(F, out_base, gout, slot, cr.x, cr.y, b0, d0, pol);
-          slot += (1ull << 33) + d0;
+        if (nw <= (unsigned)kThreads) {  // one winner per thread: a single pass
+          const bool has = tid < nw;
+          int2 cr = make_int2(0, 0);
+          unsigned b0 = 0, d0 = 0;
+          if (has) {
+            cr = sm.wbuf[tid];
+            b0 = ld_ro(p.offs + cr.x);
+            d0 = ld_ro(p.offs + cr.x + 1) - b0;
+          }
+          cta_reserve(sm, has ? 1u : 0u, d0, 0u, out, &p.ctl->n_ep, slot, unused);
+          if (has) put_entry(F, out_base, gout, slot, cr.x, cr.y, b0, d0, pol);
+        } else {
+          unsigned cnt = 0, deg = 0;
+          for (unsigned j = tid; j < nw; j += kThreads) {
+            const int c = sm.wbuf[j].x;
+            deg += ld_ro(p.offs + c + 1) - ld_ro(p.offs + c);
+            cnt++;
+          }
+          cta_reserve(sm, cnt, deg, 0u, out, &p.ctl->n_ep, slot, unused);
+          for (unsigned j = tid; j < nw; j += kThreads) {
+            const int2 cr = sm.wbuf[j];
+            const unsigned b0 = ld_ro(p.offs + cr.x);
+            const unsigned d0 = ld_ro(p.offs + cr.x + 1) - b0;
+            put_entry(F, out_base, gout, slot, cr.x, cr.y, b0, d0, pol);
+            slot += (1ull << 33) + d0;
+          }
         }
         __syncthreads();
         if (tid == 0) sm.nw = 0;
@@ -509,6 +561,11 @@ __device__ void expand_level(const Params& p, Smem& sm, int4* F, unsigned ls, un
       e = wend;
       i += kThreads;
       __syncthreads();
+      if (tid == 0) {
+        const long long t = clk();
+        sm.cnt[kStCycFlush] += t - t_a;
+        t_a = t;
+      }
     }
   }
   flush_count(sm, kStTrav, c_trav);
@@ -611,8 +668,10 @@ __device__ PhaseOut run_phase(const Params& p, Smem& sm, int cur, int parity, bo
     }
     expand_level<WR, IMP>(p, sm, F, ls, n, T, (lv & 1) ? p.gidx1 : p.gidx0, (lv & 1) ? p.gidx0 : p.gidx1,
                           in, outs, kStartLevel + lv, parity);
+    const long long tb = clk();
     grid_sync(ctl);
-    tl_mark(p, kTlLevel, (unsigned)lv);
+    if (threadIdx.x == 0) sm.cnt[kStCycBarrier] += clk() - tb;
+    tl_mark(p, kTlLevel, n);
     out.launches++;
     const unsigned long long op = ld_rlx(&outs->packed);
     const unsigned n_next = (unsigned)(op >> 33);
@@ -754,15 +813,15 @@ __device__ PhaseOut run_phase(const Params& p, Smem& sm, int cur, int parity, bo
   }
   flush_count(sm, kStResets, resets);
   grid_sync(ctl);
-  tl_mark(p, kTlRoots, 0);
   const unsigned long long np = ld_rlx(&ctl->roots.packed);
+  tl_mark(p, kTlRoots, (unsigned)(np >> 33));
   out.after = (long long)p.nc - isolated - (long long)(np >> 33);
   return out;
 }
 
 // ---------------------------------------------------------------------------
 template <bool WR, bool IMP>
-__global__ void __launch_bounds__(kThreads, 2) driver_kernel(Params p) {
+__global__ void __launch_bounds__(kThreads, 1024 / kThreads) driver_kernel(Params p) {
   __shared__ Smem sm;
   Ctrl* ctl = p.ctl;
   if (threadIdx.x < kNumStats) sm.cnt[threadIdx.x] = 0;
@@ -1115,6 +1174,8 @@ bm_status check_opts(const bm_match_opts* o) {
   if (o->init < BM_INIT_GIVEN || o->init > BM_INIT_GPU_KS)
     return fail(BM_ERR_INVALID_ARG, "unknown init mode");
   if (o->max_phases < 0) return fail(BM_ERR_INVALID_ARG, "max_phases must be >= 0");
+  if (o->reserved[0] < 0 || o->reserved[0] > 1 || o->reserved[1] || o->reserved[2])
+    return fail(BM_ERR_INVALID_ARG, "reserved option fields must be 0 (reserved[0] in 0..1)");
   // gpu_match.cpp:272-274
   if (o->improved && o->bfs_kernel != BM_BFS_WR)
     return fail(BM_ERR_LOGIC, "the endpoint-encoded alternation requires the with-root kernel");
@@ -1181,6 +1242,7 @@ Params make_params(bm_handle* h, const bm_match_opts& o) {
   p.wlog = h->wlog;
   p.log_cap = h->log_cap;
   p.trace = 0;
+  p.claim_mode = o.reserved[0];
   p.tl = h->tl;
   p.tl_cap = h->tl_cap;
   p.ctl = h->ctl;
@@ -1562,6 +1624,16 @@ bm_status bm_last_kernel_time(bm_handle* h, double* ms, int32_t* launches) {
   if (s != BM_OK) return s;
   if (ms) *ms = h->last_ms;
   if (launches) *launches = h->last_launches;
+  return BM_OK;
+}
+
+bm_status bm_debug_stats(bm_handle* h, uint64_t* out, int64_t cap, int64_t* n) {
+  bm_status s = check_handle(h, false);
+  if (s != BM_OK) return s;
+  Ctrl ctl{};
+  BM_CUDA(cudaMemcpy(&ctl, h->ctl, sizeof(Ctrl), cudaMemcpyDeviceToHost));
+  if (n) *n = kNumStats;
+  for (int64_t i = 0; i < std::min<int64_t>(cap, kNumStats); ++i) out[i] = ctl.stats[i];
   return BM_OK;
 }
 

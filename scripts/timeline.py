@@ -30,6 +30,7 @@ def main():
     card, ct, done = eng.run(shortest=shortest, kernel=bm.BfsKernel(kernel), improved=improved)
     ms, _ = eng.last_kernel_time()
     tl = eng.timeline()
+    dstats = eng.debug_stats()
     per_kind = defaultdict(float)
     levels = []
     phases = []
@@ -57,6 +58,7 @@ def main():
                                                  "columns_visited", "walk_steps", "alternations_attempted",
                                                  "fix_resets", "frontier_entries"]},
         "launches_per_phase": ct.bfs_launches_per_iteration,
+        "debug_stats": dstats,
     }
     print(json.dumps(out))
 
