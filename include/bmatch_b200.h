@@ -70,10 +70,31 @@ typedef struct bm_match_opts {
   int32_t init;              /* bm_init */
   int32_t max_phases;        /* 0 = run to the maximum (bound nc+1); >0 = stop after that many
                                 outer iterations and return with *done = 0 (resumable) */
-  int32_t reserved[3];       /* reserved[0]: WR claim policy (tuning): 0 = the reference's (a
-                                found tree's columns are skipped at expansion only, default),
-                                1 = also stop claiming at discovery; others must be 0 */
+  int32_t claim_policy;      /* bm_claim_policy (WR only): which trees may claim a column */
+  int32_t endpoint_policy;   /* bm_endpoint_policy (WR only): how many free rows a tree may hold */
+  int32_t reserved;          /* must be 0 */
 } bm_match_opts;
+
+/* Column claims under GPUBFS-WR. REFERENCE: a tree whose root already found a
+ * path keeps claiming columns at discovery; they are skipped at expansion
+ * (gpu_match.cpp:106-108). AT_DISCOVERY: such a tree also stops claiming, which
+ * leaves the columns to live trees (one coherent root-mark read per claim). */
+typedef enum bm_claim_policy { BM_CLAIM_REFERENCE = 0, BM_CLAIM_AT_DISCOVERY = 1 } bm_claim_policy;
+
+/* Free-row (endpoint) claims under GPUBFS-WR. AUTO = ONE_PER_TREE for the WR
+ * kernels. EVERY: every free row a tree reaches is flagged -2 (gpu_match.cpp:
+ * 120-125); all but one are wasted, since a tree augments along one path, and
+ * they are unavailable to other trees until FIX. ONE_PER_TREE: the first free
+ * row a tree claims is recorded at its root (atomic CAS on bfs_array[root]);
+ * a tree that already holds one releases any further row it flagged, so the
+ * row stays available to other trees in the same phase. Correctness does not
+ * depend on it (ALTERNATE's claim check + FIX do; the last phase is still a
+ * full BFS that finds no path). GPUBFS has no roots and always uses EVERY. */
+typedef enum bm_endpoint_policy {
+  BM_EP_AUTO = 0,
+  BM_EP_EVERY = 1,
+  BM_EP_ONE_PER_TREE = 2
+} bm_endpoint_policy;
 
 /* PhaseCounters (gpu_match.hpp:39-52) plus the device-side work counters the
  * roofline accounting needs. */

@@ -31,6 +31,8 @@ BM_ERR_NCCL = 6
 BM_DRIVER_APFB, BM_DRIVER_APSB = 0, 1
 BM_BFS_GPUBFS, BM_BFS_WR = 0, 1
 BM_INIT_GIVEN, BM_INIT_GPU_GREEDY, BM_INIT_GPU_KS = 0, 1, 2
+BM_CLAIM_REFERENCE, BM_CLAIM_AT_DISCOVERY = 0, 1
+BM_EP_AUTO, BM_EP_EVERY, BM_EP_ONE_PER_TREE = 0, 1, 2
 
 
 class bm_match_opts(C.Structure):
@@ -40,7 +42,9 @@ class bm_match_opts(C.Structure):
         ("improved", C.c_int32),
         ("init", C.c_int32),
         ("max_phases", C.c_int32),
-        ("reserved", C.c_int32 * 3),
+        ("claim_policy", C.c_int32),
+        ("endpoint_policy", C.c_int32),
+        ("reserved", C.c_int32),
     ]
 
 

@@ -143,9 +143,10 @@ class AlgorithmResult:
 
 
 def _opts(shortest: bool, kernel: BfsKernel, improved: bool, init_mode: str, max_phases: int = 0,
-          claim_mode: int = 0):
+          claim_mode: int = 0, endpoint_policy: int = 0):
     o = _lib.bm_match_opts()
-    o.reserved[0] = claim_mode
+    o.claim_policy = claim_mode
+    o.endpoint_policy = endpoint_policy
     o.driver = _lib.BM_DRIVER_APSB if shortest else _lib.BM_DRIVER_APFB
     o.bfs_kernel = int(kernel)
     o.improved = 1 if improved else 0
@@ -275,9 +276,10 @@ class Engine:
         check(lib.bm_load_matching(self._h, i32p(m.rmatch), i32p(m.cmatch)))
 
     def run(self, *, shortest=False, kernel=BfsKernel.GpubfsWr, improved=False, init_mode="given",
-            max_phases=0, observer=None, resume=False, claim_mode=0):
-        """Device-resident run (bm_run / bm_resume). Returns (cardinality, counters, done)."""
-        o = _opts(shortest, kernel, improved, init_mode, max_phases, claim_mode)
+            max_phases=0, observer=None, resume=False, claim_mode=0, endpoint_policy=0):
+        """Device-resident run (bm_run / bm_resume). Returns (cardinality, counters, done).
+        claim_mode / endpoint_policy: bm_claim_policy / bm_endpoint_policy (WR tuning knobs)."""
+        o = _opts(shortest, kernel, improved, init_mode, max_phases, claim_mode, endpoint_policy)
         ct = _lib.bm_counters()
         nc = self._nc()
         cap = nc + 2

@@ -174,7 +174,8 @@ struct Params {
   int max_phases;
   int stop_after_bfs;
   int trace;        // write bfs_array level labels (parity probes)
-  int claim_mode;   // WR claim check at discovery: 0 none (reference, default), 1 coherent root-mark check
+  int claim_mode;   // WR claim check at discovery: 0 none (reference), 1 coherent root-mark check
+  int ep_one;       // WR endpoint policy: 1 = one free row per tree (root-mark CAS), 0 = every row (reference)
   long long phase_bound;
   unsigned long long* tl;  // stage timeline: (tag, %globaltimer ns) pairs written by the leader
   unsigned tl_cap;
@@ -481,11 +482,22 @@ __device__ __forceinline__ void expand_level(const Params& p, Smem& sm, int4* F,
               }
             }
           } else if (c == -1) {
-            if (atomicCAS(p.rmatch + row[k], -1, -2) == -1) {
-              eps |= 1u << k;
-              st_plain(p.pred + row[k], col);
-              if (WR) st_rlx(p.bfs + root, IMP ? -row[k] : kFoundMark);
-              if (ld_rlx(path_flag) == 0u) st_rlx(path_flag, 1u);
+            // ONE_PER_TREE: a tree that already holds an endpoint leaves the row alone
+            const bool one = WR && p.ep_one;
+            if ((!one || ld_rlx(p.bfs + root) >= kUnvisited) && atomicCAS(p.rmatch + row[k], -1, -2) == -1) {
+              bool mine = true;
+              if (one) {
+                // the root's mark is the tree's endpoint slot: first CAS wins, a loser releases the row
+                mine = atomicCAS(p.bfs + root, kStartLevel, IMP ? -row[k] : kFoundMark) == kStartLevel;
+                if (!mine) st_rlx(p.rmatch + row[k], -1);
+              } else if (WR) {
+                st_rlx(p.bfs + root, IMP ? -row[k] : kFoundMark);  // gpu_match.cpp:122-123
+              }
+              if (mine) {
+                eps |= 1u << k;
+                st_plain(p.pred + row[k], col);
+                if (ld_rlx(path_flag) == 0u) st_rlx(path_flag, 1u);
+              }
             }
           }
         }
@@ -1174,8 +1186,11 @@ bm_status check_opts(const bm_match_opts* o) {
   if (o->init < BM_INIT_GIVEN || o->init > BM_INIT_GPU_KS)
     return fail(BM_ERR_INVALID_ARG, "unknown init mode");
   if (o->max_phases < 0) return fail(BM_ERR_INVALID_ARG, "max_phases must be >= 0");
-  if (o->reserved[0] < 0 || o->reserved[0] > 1 || o->reserved[1] || o->reserved[2])
-    return fail(BM_ERR_INVALID_ARG, "reserved option fields must be 0 (reserved[0] in 0..1)");
+  if (o->claim_policy < BM_CLAIM_REFERENCE || o->claim_policy > BM_CLAIM_AT_DISCOVERY)
+    return fail(BM_ERR_INVALID_ARG, "unknown claim policy");
+  if (o->endpoint_policy < BM_EP_AUTO || o->endpoint_policy > BM_EP_ONE_PER_TREE)
+    return fail(BM_ERR_INVALID_ARG, "unknown endpoint policy");
+  if (o->reserved) return fail(BM_ERR_INVALID_ARG, "reserved option field must be 0");
   // gpu_match.cpp:272-274
   if (o->improved && o->bfs_kernel != BM_BFS_WR)
     return fail(BM_ERR_LOGIC, "the endpoint-encoded alternation requires the with-root kernel");
@@ -1242,7 +1257,8 @@ Params make_params(bm_handle* h, const bm_match_opts& o) {
   p.wlog = h->wlog;
   p.log_cap = h->log_cap;
   p.trace = 0;
-  p.claim_mode = o.reserved[0];
+  p.claim_mode = o.claim_policy;
+  p.ep_one = (o.bfs_kernel == BM_BFS_WR && o.endpoint_policy != BM_EP_EVERY) ? 1 : 0;
   p.tl = h->tl;
   p.tl_cap = h->tl_cap;
   p.ctl = h->ctl;
@@ -1683,6 +1699,7 @@ bm_status bm_bfs_phase(bm_handle* h, int32_t driver, int32_t bfs_kernel, int32_t
   o.bfs_kernel = bfs_kernel;
   o.improved = improved;
   o.init = BM_INIT_GIVEN;
+  o.endpoint_policy = BM_EP_EVERY;  // the probe reports the reference's -2 flags
   s = check_opts(&o);
   if (s != BM_OK) return s;
   if ((!rmatch_in && h->nr > 0) || (!cmatch_in && h->nc > 0)) return fail(BM_ERR_INVALID_ARG, "null matching array");
