@@ -25,8 +25,9 @@
 //     the next level is cut into equal *edge* tiles whatever the degree skew.
 //     While pushing, each entry also records itself in a granule index (one
 //     u32 per kGran edges), so a tile finds its first entry with one load.
-//   * "Unvisited" is a 1-bit-per-column bitmap claimed with atomicOr (nc/8
-//     bytes: L2-resident even at 1e8 columns) instead of a bfs_array gather.
+//   * "Unvisited" is one bit (bit 30) of the column's mate entry in rmatch,
+//     claimed with atomicOr: the rmatch[row] gather every traversed edge makes
+//     anyway also answers the visited test, instead of a bfs_array gather.
 //   * WR: a tree whose root already found a path stops claiming columns at
 //     discovery time, not only at expansion (gpu_match.cpp:106-108), leaving
 //     them to live trees. Correctness never depends on it (ALTERNATE's claim
@@ -44,6 +45,7 @@
 //   * The next phase's roots come from this phase's roots plus columns FIX
 //     unmatched; nothing is O(nc) per phase except the 1-bit bitmap clear.
 #include <algorithm>
+#include <cstdlib>
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
@@ -64,14 +66,32 @@ namespace bm {
 #define BM_THREADS 256
 #endif
 constexpr int kThreads = BM_THREADS;  // threads per CTA (1024 / kThreads CTAs per SM at <= 64 registers)
-constexpr int kItems = 4;             // edges per thread per round (memory-level parallelism)
+#ifndef BM_ITEMS
+#define BM_ITEMS 4
+#endif
+#ifndef BM_MINB
+#define BM_MINB (1024 / BM_THREADS)
+#endif
+constexpr int kItems = BM_ITEMS;      // edges per thread per round (memory-level parallelism)
 constexpr unsigned kGran = 512;       // edges per granule-index entry; tiles are whole granules
 constexpr unsigned kMaxTileGran = 8;  // <= 4096 edges per tile (= the winner buffer)
 constexpr unsigned kWBuf = kGran * kMaxTileGran;
+#ifndef BM_BATCH
+#define BM_BATCH 1  // issue all of a thread's claim atomics before consuming any
+#endif
+#ifndef BM_SOLO_EDGES
+#define BM_SOLO_EDGES 4096
+#endif
+constexpr unsigned kSoloEdges = BM_SOLO_EDGES;  // widest level block 0 expands alone
 constexpr int kStartLevel = 2;        // L0 (gpu_match.cpp:275)
 constexpr int kUnvisited = kStartLevel - 1;
 constexpr int kFoundMark = kStartLevel - 2;
 constexpr unsigned long long kEdgeMask = (1ull << 33) - 1;
+// "Column visited this phase" lives in bit 30 of its mate's rmatch entry: the
+// gather rmatch[row] that finds a row's column also says whether that column
+// was claimed, so a traversed edge costs one random access, not two. Needs
+// nc < 2^30; cleared by sweep_visited() when the BFS ends.
+constexpr int kVisBit = 1 << 30;
 
 enum CtlError : int {
   kErrNone = 0,
@@ -130,6 +150,15 @@ struct alignas(128) Ctrl {
   unsigned pad1b[29];
   unsigned path_found[2];
   unsigned pad2[30];
+  // hand-over from a solo run of narrow levels (block 0 alone) to the grid
+  int solo_lv;
+  int solo_stop;
+  unsigned solo_ls;
+  unsigned solo_n;
+  unsigned solo_T;
+  int solo_found;
+  long long solo_launches;
+  unsigned pad2b[24];
   unsigned long long invalid;
   unsigned long long isolated;
   unsigned long long pad3[14];
@@ -156,8 +185,8 @@ struct Params {
   int* cmatch;
   int* pred;
   int* bfs;
-  unsigned* vis;
-  int nvis_words;
+  unsigned* dead;   // WR: 1 bit per column, set when the tree rooted there holds an endpoint
+  int ndead_words;
   int4* F0;
   int4* F1;
   unsigned* gidx0;  // granule index, ping-pong by level parity
@@ -176,6 +205,7 @@ struct Params {
   int trace;        // write bfs_array level labels (parity probes)
   int claim_mode;   // WR claim check at discovery: 0 none (reference), 1 coherent root-mark check
   int ep_one;       // WR endpoint policy: 1 = one free row per tree (root-mark CAS), 0 = every row (reference)
+  unsigned solo_edges;  // levels with at most this many frontier edges run on block 0 alone (0 = never)
   long long phase_bound;
   unsigned long long* tl;  // stage timeline: (tag, %globaltimer ns) pairs written by the leader
   unsigned tl_cap;
@@ -327,6 +357,17 @@ __device__ __forceinline__ void put_entry(int4* F, unsigned out_base, unsigned* 
   for (unsigned m = (pre + kGran - 1) / kGran; m <= m1; ++m) st_plain(reinterpret_cast<int*>(gidx) + m, (int)local);
 }
 
+// WR early-exit test (gpu_match.cpp:106-108) against the dead-root bitmap:
+// nc/8 bytes that stay in L2, instead of a bfs_array[root] gather per entry.
+// bfs_array[root] still carries the reference's mark (and the endpoint for
+// the improved walk); the bit only mirrors "marked".
+__device__ __forceinline__ bool root_dead(const Params& p, int root) {
+  return (ld_rlx(p.dead + (root >> 5)) >> (root & 31)) & 1u;
+}
+__device__ __forceinline__ void mark_dead(const Params& p, int root) {
+  atomicOr(p.dead + (root >> 5), 1u << (root & 31));
+}
+
 // ---------------------------------------------------------------------------
 // One BFS level (GPUBFS, Alg. 2, gpu_match.cpp:42-70; GPUBFS-WR, Alg. 4,
 // gpu_match.cpp:99-133) over the frontier F[ls, ls+n) holding T edges.
@@ -346,6 +387,9 @@ __device__ __forceinline__ void expand_level(const Params& p, Smem& sm, int4* F,
   unsigned* const path_flag = &p.ctl->path_found[pf];
 
   const unsigned long long pol = policy_evict_first();
+#ifndef BM_PF
+#define BM_PF 2
+#endif
 #ifndef BM_KEEP
 #define BM_KEEP 1
 #endif
@@ -375,7 +419,7 @@ __device__ __forceinline__ void expand_level(const Params& p, Smem& sm, int4* F,
       if (wi < n) {
         const int4 ent = ld_cg_stream(F + ls + wi, pol);
         bool skip = false;
-        if (WR) skip = ld_rlx(p.bfs + ent.y) < kUnvisited;  // early exit (gpu_match.cpp:106-108)
+        if (WR) skip = root_dead(p, ent.y);  // early exit (gpu_match.cpp:106-108)
         sm.col[tid] = ent.x;
         sm.root[tid] = skip ? -1 : ent.y;
         sm.beg[tid] = (unsigned)ent.z;
@@ -434,7 +478,6 @@ __device__ __forceinline__ void expand_level(const Params& p, Smem& sm, int4* F,
       // staged in sm.wbuf.
       for (unsigned base = 0; base < live; base += kThreads * kItems) {
         int row[kItems], cm[kItems], sl[kItems];
-        unsigned w[kItems];
 #pragma unroll
         for (int k = 0; k < kItems; ++k) {
           const unsigned ee = base + k * kThreads + tid;
@@ -458,40 +501,46 @@ __device__ __forceinline__ void expand_level(const Params& p, Smem& sm, int4* F,
         for (int k = 0; k < kItems; ++k)
           cm[k] = row[k] >= 0 ? (BM_KEEP >= 1 ? ld_rlx_hint(p.rmatch + row[k], keep) : ld_rlx(p.rmatch + row[k]))
                               : -3;
-#pragma unroll
-        for (int k = 0; k < kItems; ++k)
-          w[k] = cm[k] >= 0 ? (BM_KEEP >= 2 ? ld_rlx_hint(p.vis + (cm[k] >> 5), keep) : ld_rlx(p.vis + (cm[k] >> 5)))
-                            : kFull;
         unsigned wins = 0, eps = 0;
+        // Column claims: issue every item's atomic before consuming any result
+        // (kItems claims in flight per thread instead of one).
+        int old[kItems];
+#pragma unroll
+        for (int k = 0; k < kItems; ++k) {
+          const int c = cm[k];  // mate of the row; kVisBit set = its column was claimed this phase
+          old[k] = kVisBit;
+          if (BM_BATCH && c >= 0 && !(c & kVisBit) &&
+              (!WR || p.claim_mode == 0 || !root_dead(p, sm.root[sl[k]])))
+            old[k] = atomicOr(p.rmatch + row[k], kVisBit);
+        }
 #pragma unroll
         for (int k = 0; k < kItems; ++k) {
           const int c = cm[k];
           const int col = sm.col[sl[k]];
           const int root = WR ? sm.root[sl[k]] : col;
           if (c >= 0) {
-            const unsigned bit = 1u << (c & 31);
-            // WR: a tree whose root is already marked stops claiming columns.
-            // optional (claim_mode 1): a tree whose root is already marked stops claiming columns
-            if (!(w[k] & bit) && (!WR || p.claim_mode == 0 || ld_rlx(p.bfs + root) >= kUnvisited)) {
-              const unsigned old = atomicOr(p.vis + (c >> 5), bit);
-              if (!(old & bit)) {
-                wins |= 1u << k;
-                prefetch_l2(p.offs + c);  // the flush reads offs[c], offs[c+1]
-                st_stream(p.pred + row[k], col, pol);
-                if (p.trace) st_plain(p.bfs + c, level + 1);
-              }
+            if (!BM_BATCH && !(c & kVisBit) && (!WR || p.claim_mode == 0 || !root_dead(p, root)))
+              old[k] = atomicOr(p.rmatch + row[k], kVisBit);
+            if (!(old[k] & kVisBit)) {
+              wins |= 1u << k;
+              if (BM_PF == 2) prefetch_l2(p.offs + c);  // the flush reads offs[c], offs[c+1]
+              if (BM_PF == 1) asm volatile("prefetch.global.L2 [%0];" ::"l"(p.offs + c));
+              st_stream(p.pred + row[k], col, pol);
+              if (p.trace) st_plain(p.bfs + c, level + 1);
             }
           } else if (c == -1) {
             // ONE_PER_TREE: a tree that already holds an endpoint leaves the row alone
             const bool one = WR && p.ep_one;
-            if ((!one || ld_rlx(p.bfs + root) >= kUnvisited) && atomicCAS(p.rmatch + row[k], -1, -2) == -1) {
+            if ((!one || !root_dead(p, root)) && atomicCAS(p.rmatch + row[k], -1, -2) == -1) {
               bool mine = true;
               if (one) {
                 // the root's mark is the tree's endpoint slot: first CAS wins, a loser releases the row
                 mine = atomicCAS(p.bfs + root, kStartLevel, IMP ? -row[k] : kFoundMark) == kStartLevel;
                 if (!mine) st_rlx(p.rmatch + row[k], -1);
+                else mark_dead(p, root);
               } else if (WR) {
                 st_rlx(p.bfs + root, IMP ? -row[k] : kFoundMark);  // gpu_match.cpp:122-123
+                mark_dead(p, root);
               }
               if (mine) {
                 eps |= 1u << k;
@@ -647,6 +696,25 @@ __device__ __forceinline__ bool fix_col(const Params& p, unsigned& resets, int c
   return r < 0;
 }
 
+// Clears the visited bits the BFS left in rmatch (one streaming pass, int4).
+__device__ __forceinline__ void sweep_visited(const Params& p) {
+  int4* r4 = reinterpret_cast<int4*>(p.rmatch);
+  const unsigned long long n4 = (unsigned long long)p.nr / 4;
+  for (unsigned long long k = global_thread(); k < n4; k += global_threads()) {
+    int4 v = ld_cg(r4 + k);
+    const int4 o = v;
+    if (v.x >= 0) v.x &= ~kVisBit;
+    if (v.y >= 0) v.y &= ~kVisBit;
+    if (v.z >= 0) v.z &= ~kVisBit;
+    if (v.w >= 0) v.w &= ~kVisBit;
+    if (v.x != o.x || v.y != o.y || v.z != o.z || v.w != o.w) st_plain(r4 + k, v);
+  }
+  for (unsigned long long r = n4 * 4 + global_thread(); r < (unsigned long long)p.nr; r += global_threads()) {
+    const int v = ld_cg(p.rmatch + r);
+    if (v >= 0 && (v & kVisBit)) st_plain(p.rmatch + r, v & ~kVisBit);
+  }
+}
+
 struct PhaseOut {
   bool found;
   long long launches;
@@ -670,7 +738,23 @@ __device__ PhaseOut run_phase(const Params& p, Smem& sm, int cur, int parity, bo
   unsigned ls = 0;
   int lv = 0;
   bool found = false;
+  // Narrow levels (at most solo_edges frontier edges) run on block 0 alone,
+  // back to back with CTA barriers only — a grid barrier costs more than such
+  // a level's work. The other CTAs wait at one grid barrier and take over
+  // when the frontier widens again or the BFS ends.
   for (;;) {
+    const bool solo = T <= p.solo_edges;
+    if (solo && blockIdx.x != 0) {
+      grid_sync(ctl);  // block 0's hand-over
+      lv = ld_rlx(&ctl->solo_lv);
+      ls = (unsigned)ld_rlx(&ctl->solo_ls);
+      n = (unsigned)ld_rlx(&ctl->solo_n);
+      T = (unsigned)ld_rlx(&ctl->solo_T);
+      found = ld_rlx(&ctl->solo_found) != 0;
+      out.launches = (long long)ld_rlx((const unsigned long long*)&ctl->solo_launches);
+      if (ld_rlx(&ctl->solo_stop)) break;
+      continue;
+    }
     Slot* in = lv == 0 ? &ctl->roots : &ctl->lvl[lv % 3];
     Slot* outs = &ctl->lvl[(lv + 1) % 3];
     if (is_leader() && lv >= 1) {
@@ -678,28 +762,50 @@ __device__ PhaseOut run_phase(const Params& p, Smem& sm, int cur, int parity, bo
       z->packed = 0;
       z->tile = 0;
     }
+    if (solo) __syncthreads();
     expand_level<WR, IMP>(p, sm, F, ls, n, T, (lv & 1) ? p.gidx1 : p.gidx0, (lv & 1) ? p.gidx0 : p.gidx1,
                           in, outs, kStartLevel + lv, parity);
     const long long tb = clk();
-    grid_sync(ctl);
+    if (solo) {
+      __threadfence_block();
+      __syncthreads();
+    } else {
+      grid_sync(ctl);
+    }
     if (threadIdx.x == 0) sm.cnt[kStCycBarrier] += clk() - tb;
     tl_mark(p, kTlLevel, n);
     out.launches++;
     const unsigned long long op = ld_rlx(&outs->packed);
     const unsigned n_next = (unsigned)(op >> 33);
     found = ld_rlx(&ctl->path_found[parity]) != 0u;
-    if (p.apsb && found) break;
-    if (n_next == 0) break;
-    ls += n;
-    n = n_next;
-    T = (unsigned)(op & kEdgeMask);
-    ++lv;
-    if (lv > p.nc + 2) {
-      if (is_leader()) ctl->error = kErrLevels;
-      break;
+    bool stop = (p.apsb && found) || n_next == 0;
+    if (!stop) {
+      ls += n;
+      n = n_next;
+      T = (unsigned)(op & kEdgeMask);
+      ++lv;
+      if (lv > p.nc + 2) {
+        if (is_leader()) ctl->error = kErrLevels;
+        stop = true;
+      }
     }
+    if (solo && (stop || T > p.solo_edges)) {  // block 0 hands the BFS back to the grid
+      if (threadIdx.x == 0) {
+        ctl->solo_lv = lv;
+        ctl->solo_stop = stop ? 1 : 0;
+        ctl->solo_ls = ls;
+        ctl->solo_n = n;
+        ctl->solo_T = T;
+        ctl->solo_found = found ? 1 : 0;
+        ctl->solo_launches = out.launches;
+      }
+      grid_sync(ctl);
+    }
+    if (stop) break;
   }
   out.found = found;
+  sweep_visited(p);
+  grid_sync(ctl);
   if (p.stop_after_bfs) return out;
 
   // ---- ALTERNATE (gpu_match.cpp:158-218) ----
@@ -748,8 +854,9 @@ __device__ PhaseOut run_phase(const Params& p, Smem& sm, int cur, int parity, bo
     for (unsigned long long r = global_thread(); r < (unsigned long long)p.nr; r += global_threads())
       fix_row(p, resets, (int)r);
   }
-  for (unsigned long long k = global_thread(); k < (unsigned long long)p.nvis_words; k += global_threads())
-    st_plain(reinterpret_cast<int*>(p.vis) + k, 0);
+  if (WR)
+    for (unsigned long long k = global_thread(); k < (unsigned long long)p.ndead_words; k += global_threads())
+      st_plain(reinterpret_cast<int*>(p.dead) + k, 0);
   if (is_leader()) {
     for (int s = 0; s < 3; ++s) {
       ctl->lvl[s].packed = 0;
@@ -833,7 +940,7 @@ __device__ PhaseOut run_phase(const Params& p, Smem& sm, int cur, int parity, bo
 
 // ---------------------------------------------------------------------------
 template <bool WR, bool IMP>
-__global__ void __launch_bounds__(kThreads, 1024 / kThreads) driver_kernel(Params p) {
+__global__ void __launch_bounds__(kThreads, BM_MINB) driver_kernel(Params p) {
   __shared__ Smem sm;
   Ctrl* ctl = p.ctl;
   if (threadIdx.x < kNumStats) sm.cnt[threadIdx.x] = 0;
@@ -1145,8 +1252,8 @@ struct bm_handle {
   // state
   int *rmatch = nullptr, *cmatch = nullptr, *pred = nullptr, *bfs = nullptr;
   int *rmatch0 = nullptr, *cmatch0 = nullptr, *EP = nullptr;
-  unsigned* vis = nullptr;
-  int nvis_words = 0;
+  unsigned* dead = nullptr;
+  int ndead_words = 0;
   int4* F[2] = {nullptr, nullptr};
   unsigned* gidx[2] = {nullptr, nullptr};
   int2* wlog = nullptr;
@@ -1155,7 +1262,6 @@ struct bm_handle {
   PhaseRec* recs = nullptr;
   int rec_cap = 4096;
   bool has_init = false;
-  bool clean = false;   // vis == 0 everywhere (pred needs no reset, see the kernel header)
   bool resumable = false;
   bm_match_opts run_opts{};
   std::vector<long long> phase_launches;  // per outer iteration, current run
@@ -1218,15 +1324,42 @@ int grid_for(bm_handle* h, int v) {
 // resets predecessors (only for parity probes that report them), and zeroes
 // the control block.
 bm_status prepare_fresh(bm_handle* h, bool reset_pred = false) {
-  if (!h->clean)
-    BM_CUDA(cudaMemsetAsync(h->vis, 0, sizeof(unsigned) * std::max(h->nvis_words, 1), h->stream));
   if (reset_pred) BM_CUDA(cudaMemsetAsync(h->pred, 0xff, sizeof(int) * std::max(h->nr, 1), h->stream));
   BM_CUDA(cudaMemsetAsync(h->ctl, 0, sizeof(Ctrl), h->stream));
-  h->clean = false;
+  BM_CUDA(cudaMemsetAsync(h->dead, 0, sizeof(unsigned) * std::max(h->ndead_words, 1), h->stream));
   return BM_OK;
 }
 
+// Tuning hook: BM_PERSIST_MB=<n> marks the first n MB of rmatch as a
+// persisting L2 access-policy window on the handle's stream.
+void apply_persist(bm_handle* h) {
+  const char* e = getenv("BM_PERSIST_MB");
+  if (!e || !h->rmatch) return;
+  const size_t want = (size_t)atol(e) << 20;
+  if (!want) return;
+  cudaDeviceProp prop{};
+  cudaGetDeviceProperties(&prop, h->device);
+  const size_t lim = std::min<size_t>(want, (size_t)prop.persistingL2CacheMaxSize);
+  cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, lim);
+  cudaStreamAttrValue a{};
+  a.accessPolicyWindow.base_ptr = h->rmatch;
+  a.accessPolicyWindow.num_bytes = std::min<size_t>(std::min<size_t>(want, sizeof(int) * (size_t)h->nr),
+                                                    (size_t)prop.accessPolicyMaxWindowSize);
+  a.accessPolicyWindow.hitRatio = 1.0f;
+  a.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+  a.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+  cudaStreamSetAttribute(h->stream, cudaStreamAttributeAccessPolicyWindow, &a);
+  static bool said = false;
+  if (!said) {
+    said = true;
+    fprintf(stderr, "[bm] persisting L2 window: %zu MB (max persisting %d MB, max window %d MB)\n",
+            (size_t)a.accessPolicyWindow.num_bytes >> 20, prop.persistingL2CacheMaxSize >> 20,
+            prop.accessPolicyMaxWindowSize >> 20);
+  }
+}
+
 bm_status launch(bm_handle* h, int v, Params& p, float* ms) {
+  apply_persist(h);
   const int G = grid_for(h, v);
   void* args[] = {&p};
   BM_CUDA(cudaEventRecord(h->ev0, h->stream));
@@ -1247,8 +1380,8 @@ Params make_params(bm_handle* h, const bm_match_opts& o) {
   p.cmatch = h->cmatch;
   p.pred = h->pred;
   p.bfs = h->bfs;
-  p.vis = h->vis;
-  p.nvis_words = h->nvis_words;
+  p.dead = h->dead;
+  p.ndead_words = h->ndead_words;
   p.F0 = h->F[0];
   p.F1 = h->F[1];
   p.gidx0 = h->gidx[0];
@@ -1259,6 +1392,7 @@ Params make_params(bm_handle* h, const bm_match_opts& o) {
   p.trace = 0;
   p.claim_mode = o.claim_policy;
   p.ep_one = (o.bfs_kernel == BM_BFS_WR && o.endpoint_policy != BM_EP_EVERY) ? 1 : 0;
+  p.solo_edges = kSoloEdges;
   p.tl = h->tl;
   p.tl_cap = h->tl_cap;
   p.ctl = h->ctl;
@@ -1368,7 +1502,6 @@ bm_status drive(bm_handle* h, const bm_match_opts& o, bool fresh, int64_t* cardi
   }
   h->resumable = !done;
   h->run_opts = o;
-  h->clean = true;  // every completed phase leaves pred == -1 and vis == 0
   if (cardinality) *cardinality = ctl.card;
   if (done_out) *done_out = done ? 1 : 0;
   if (counters) {
@@ -1478,10 +1611,10 @@ bm_status bm_destroy(bm_handle* h) {
   dfree(h->rmatch0);
   dfree(h->cmatch0);
   dfree(h->EP);
+  dfree(h->dead);
   dfree(h->gidx[0]);
   dfree(h->gidx[1]);
   dfree(h->wlog);
-  dfree(h->vis);
   dfree(h->F[0]);
   dfree(h->F[1]);
   dfree(h->ctl);
@@ -1507,6 +1640,7 @@ bm_status bm_upload_csc(bm_handle* h, int32_t nc, int32_t nr, const int64_t* cxa
   bm_status s = check_handle(h, false);
   if (s != BM_OK) return s;
   if (nc < 0 || nr < 0) return fail(BM_ERR_INVALID_ARG, "negative vertex count");
+  if (nc >= kVisBit) return fail(BM_ERR_INVALID_ARG, "nc must be < 2^30 in this build (visited flag in rmatch bit 30)");
   if (!cxadj) return fail(BM_ERR_INVALID_ARG, "null cxadj");
   const long long E = cxadj[nc];
   if (E < 0) return fail(BM_ERR_INVALID_ARG, "cxadj[nc] is negative");
@@ -1528,13 +1662,13 @@ bm_status bm_upload_csc(bm_handle* h, int32_t nc, int32_t nr, const int64_t* cxa
   BM_CUDA(dalloc(h->caps, h->rmatch0, nr));
   BM_CUDA(dalloc(h->caps, h->cmatch0, nc));
   BM_CUDA(dalloc(h->caps, h->EP, nr));
+  h->ndead_words = (nc + 31) / 32;
+  BM_CUDA(dalloc(h->caps, h->dead, h->ndead_words));
   const size_t ngran = (size_t)(E / kGran) + 2;
   BM_CUDA(dalloc(h->caps, h->gidx[0], ngran));
   BM_CUDA(dalloc(h->caps, h->gidx[1], ngran));
   h->log_cap = (unsigned)std::min<long long>((long long)nr + nc + 1024, 0xffffffffll);
   BM_CUDA(dalloc(h->caps, h->wlog, h->log_cap));
-  h->nvis_words = (nc + 31) / 32;
-  BM_CUDA(dalloc(h->caps, h->vis, h->nvis_words));
   BM_CUDA(dalloc(h->caps, h->F[0], nc));
   BM_CUDA(dalloc(h->caps, h->F[1], nc));
   // offsets: int64 staged in F[1] (16 B per column >= 8 B per offset), narrowed to u32
@@ -1560,9 +1694,7 @@ bm_status bm_upload_csc(bm_handle* h, int32_t nc, int32_t nr, const int64_t* cxa
   }
   h->sorted = bad[2] == 0;
   BM_CUDA(cudaMemsetAsync(h->pred, 0xff, sizeof(int) * std::max(nr, 1), h->stream));
-  BM_CUDA(cudaMemsetAsync(h->vis, 0, sizeof(unsigned) * std::max(h->nvis_words, 1), h->stream));
   BM_CUDA(cudaStreamSynchronize(h->stream));
-  h->clean = true;
   h->nc = nc;
   h->nr = nr;
   h->E = E;
@@ -1717,7 +1849,6 @@ bm_status bm_bfs_phase(bm_handle* h, int32_t driver, int32_t bfs_kernel, int32_t
   s = launch(h, v, p, &ms);
   if (s != BM_OK) return s;
   h->resumable = false;
-  h->clean = false;
   Ctrl ctl{};
   BM_CUDA(cudaMemcpy(&ctl, h->ctl, sizeof(Ctrl), cudaMemcpyDeviceToHost));
   if (ctl.error) return ctl_error_status(ctl.error);
@@ -1764,7 +1895,6 @@ bm_status bm_verify(bm_handle* h, const int32_t* rmatch, const int32_t* cmatch, 
   float ms = 0.f;
   s = launch(h, 0, p, &ms);
   if (s != BM_OK) return s;
-  h->clean = false;
   Ctrl ctl{};
   BM_CUDA(cudaMemcpy(&ctl, h->ctl, sizeof(Ctrl), cudaMemcpyDeviceToHost));
   if (ctl.error) return ctl_error_status(ctl.error);
