@@ -24,9 +24,17 @@ ORACLE    := oracle/liboracle.so
 
 REF_ROOT  ?= /root/reference/proj
 REF_SRCS  := algorithms baselines csr_graph gpu_match kernel_grid matching matrix_market
+# bench.cpp (run_suite) needs nlohmann/json, which the reference vendors but does not ship;
+# the image has a copy inside cudnn_frontend. Without it the suite runner is left out.
+NLOHMANN  ?= $(firstword $(wildcard /opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty/nlohmann))
+ifneq ($(NLOHMANN),)
+REF_SRCS  += bench
+REF_INC   := -I$(NLOHMANN)
+endif
 REF_LIB   := oracle/_ref/libbmatch_ref.so
+SHIM_TEST := oracle/_ref/shim_test
 
-.PHONY: all ref clean
+.PHONY: all ref shimtest clean
 all: $(LIB) $(ORACLE)
 
 $(BUILD):
@@ -48,8 +56,17 @@ ref: $(REF_LIB)
 
 $(REF_LIB): oracle/ref_capi.cpp $(foreach s,$(REF_SRCS),$(REF_ROOT)/src/$(s).cpp)
 	mkdir -p oracle/_ref
-	$(CXX) -std=c++20 -O3 -DNDEBUG -fPIC -shared -pthread -I$(REF_ROOT)/include \
+	$(CXX) -std=c++20 -O3 -DNDEBUG -fPIC -shared -pthread -I$(REF_ROOT)/include $(REF_INC) \
 	    -o $@ oracle/ref_capi.cpp $(foreach s,$(REF_SRCS),$(REF_ROOT)/src/$(s).cpp)
+
+# The C++ drop-in test: the reference's registry/driver/suite API calling the
+# engine through include/bmatch_b200.hpp (needs the reference headers to build).
+shimtest: $(SHIM_TEST)
+
+$(SHIM_TEST): tests/cpp/shim_test.cpp include/bmatch_b200.hpp include/bmatch_b200.h $(REF_LIB) $(LIB)
+	$(CXX) -std=c++20 -O2 -Wall -Wextra -pthread -I$(REF_ROOT)/include $(REF_INC) -Iinclude \
+	    -o $@ tests/cpp/shim_test.cpp $(REF_LIB) $(LIB) \
+	    -Wl,-rpath,'$$ORIGIN' -Wl,-rpath,'$$ORIGIN/../../paper_1303_1379_b200'
 
 clean:
 	rm -rf $(BUILD) $(LIB) $(ORACLE)
