@@ -183,8 +183,9 @@ bm_status   bm_last_kernel_time(bm_handle* h, double* ms, int32_t* launches);
 
 /* Stage timeline of the last bm_run/bm_resume/bm_match: `n` records of two
  * uint64 each, (tag, device %globaltimer in ns). tag = (kind << 32) | arg with
- * kind 0 start, 1 init pass, 2 setup, 3 BFS level (arg = level index),
- * 4 ALTERNATE, 5 FIX rows, 6 FIX columns, 7 roots of the next phase, 8 end.
+ * kind 0 start, 1 init pass, 2 setup, 3 BFS level (arg = frontier entries),
+ * 4 ALTERNATE, 5 FIX rows, 6 FIX columns, 7 roots of the next phase, 8 end,
+ * 9 the preceding level's frontier edges (arg; same timestamp).
  * Written by one thread after each grid barrier (a few ns per stage). */
 bm_status   bm_timeline(bm_handle* h, uint64_t* out, int64_t cap, int64_t* n);
 

@@ -79,6 +79,9 @@ constexpr unsigned kWBuf = kGran * kMaxTileGran;
 #ifndef BM_BATCH
 #define BM_BATCH 1  // issue all of a thread's claim atomics before consuming any
 #endif
+#ifndef BM_INTERLEAVE
+#define BM_INTERLEAVE 1
+#endif
 #ifndef BM_SOLO_EDGES
 #define BM_SOLO_EDGES 4096
 #endif
@@ -181,7 +184,7 @@ struct Params {
   int nc, nr;
   const unsigned* offs;  // nc + 1
   const int* adj;        // E
-  int* rmatch;
+  int* rm;          // row state: BM_INTERLEAVE ? {mate, pred} pairs : mates (pred in `pred`)
   int* cmatch;
   int* pred;
   int* bfs;
@@ -357,6 +360,16 @@ __device__ __forceinline__ void put_entry(int4* F, unsigned out_base, unsigned* 
   for (unsigned m = (pre + kGran - 1) / kGran; m <= m1; ++m) st_plain(reinterpret_cast<int*>(gidx) + m, (int)local);
 }
 
+// Row state layout. With BM_INTERLEAVE (default) a row's mate (rmatch) and
+// its BFS predecessor share one 8-byte slot: the claim is an atomicOr on the
+// mate word and the predecessor store that follows it lands in the same L2
+// sector, which the atomic has just brought in and dirtied, instead of a
+// second random sector (with a DRAM read-for-fill of a partial write).
+__device__ __forceinline__ int* RM(const Params& p, long long r) { return p.rm + (BM_INTERLEAVE ? 2 * r : r); }
+__device__ __forceinline__ int* PR(const Params& p, long long r) {
+  return BM_INTERLEAVE ? p.rm + 2 * r + 1 : p.pred + r;
+}
+
 // WR early-exit test (gpu_match.cpp:106-108) against the dead-root bitmap:
 // nc/8 bytes that stay in L2, instead of a bfs_array[root] gather per entry.
 // bfs_array[root] still carries the reference's mark (and the endpoint for
@@ -499,7 +512,7 @@ __device__ __forceinline__ void expand_level(const Params& p, Smem& sm, int4* F,
         }
 #pragma unroll
         for (int k = 0; k < kItems; ++k)
-          cm[k] = row[k] >= 0 ? (BM_KEEP >= 1 ? ld_rlx_hint(p.rmatch + row[k], keep) : ld_rlx(p.rmatch + row[k]))
+          cm[k] = row[k] >= 0 ? (BM_KEEP >= 1 ? ld_rlx_hint(RM(p, row[k]), keep) : ld_rlx(RM(p, row[k])))
                               : -3;
         unsigned wins = 0, eps = 0;
         // Column claims: issue every item's atomic before consuming any result
@@ -511,7 +524,7 @@ __device__ __forceinline__ void expand_level(const Params& p, Smem& sm, int4* F,
           old[k] = kVisBit;
           if (BM_BATCH && c >= 0 && !(c & kVisBit) &&
               (!WR || p.claim_mode == 0 || !root_dead(p, sm.root[sl[k]])))
-            old[k] = atomicOr(p.rmatch + row[k], kVisBit);
+            old[k] = atomicOr(RM(p, row[k]), kVisBit);
         }
 #pragma unroll
         for (int k = 0; k < kItems; ++k) {
@@ -520,23 +533,23 @@ __device__ __forceinline__ void expand_level(const Params& p, Smem& sm, int4* F,
           const int root = WR ? sm.root[sl[k]] : col;
           if (c >= 0) {
             if (!BM_BATCH && !(c & kVisBit) && (!WR || p.claim_mode == 0 || !root_dead(p, root)))
-              old[k] = atomicOr(p.rmatch + row[k], kVisBit);
+              old[k] = atomicOr(RM(p, row[k]), kVisBit);
             if (!(old[k] & kVisBit)) {
               wins |= 1u << k;
               if (BM_PF == 2) prefetch_l2(p.offs + c);  // the flush reads offs[c], offs[c+1]
               if (BM_PF == 1) asm volatile("prefetch.global.L2 [%0];" ::"l"(p.offs + c));
-              st_stream(p.pred + row[k], col, pol);
+              st_stream(PR(p, row[k]), col, pol);
               if (p.trace) st_plain(p.bfs + c, level + 1);
             }
           } else if (c == -1) {
             // ONE_PER_TREE: a tree that already holds an endpoint leaves the row alone
             const bool one = WR && p.ep_one;
-            if ((!one || !root_dead(p, root)) && atomicCAS(p.rmatch + row[k], -1, -2) == -1) {
+            if ((!one || !root_dead(p, root)) && atomicCAS(RM(p, row[k]), -1, -2) == -1) {
               bool mine = true;
               if (one) {
                 // the root's mark is the tree's endpoint slot: first CAS wins, a loser releases the row
                 mine = atomicCAS(p.bfs + root, kStartLevel, IMP ? -row[k] : kFoundMark) == kStartLevel;
-                if (!mine) st_rlx(p.rmatch + row[k], -1);
+                if (!mine) st_rlx(RM(p, row[k]), -1);
                 else mark_dead(p, root);
               } else if (WR) {
                 st_rlx(p.bfs + root, IMP ? -row[k] : kFoundMark);  // gpu_match.cpp:122-123
@@ -544,7 +557,7 @@ __device__ __forceinline__ void expand_level(const Params& p, Smem& sm, int4* F,
               }
               if (mine) {
                 eps |= 1u << k;
-                st_plain(p.pred + row[k], col);
+                st_plain(PR(p, row[k]), col);
                 if (ld_rlx(path_flag) == 0u) st_rlx(path_flag, 1u);
               }
             }
@@ -654,15 +667,15 @@ __device__ __forceinline__ void log_write(const Params& p, int row, int col) {
 __device__ __forceinline__ void alternate_walk(const Params& p, unsigned& walks, unsigned& nsteps, int row) {
   long long steps = 0;
   while (row != -1) {
-    const int col = ld_cg(p.pred + row);
+    const int col = ld_cg(PR(p, row));
     if (col < 0) break;
     const int mr = ld_rlx(p.cmatch + col);
-    if (mr >= 0 && ld_cg(p.pred + mr) == col) {
+    if (mr >= 0 && ld_cg(PR(p, mr)) == col) {
       if (steps > 0) log_write(p, row, -1);  // left dangling: its column now belongs to another row
       break;
     }
     st_rlx(p.cmatch + col, row);
-    st_rlx(p.rmatch + row, col);
+    st_rlx(RM(p, row), col);
     log_write(p, row, col);
     row = mr;
     if (++steps > p.nc) {
@@ -677,11 +690,11 @@ __device__ __forceinline__ void alternate_walk(const Params& p, unsigned& walks,
 // FIX rules 1 and 2 for one row (gpu_match.cpp:221-237). The CAS keeps the
 // reset count exact when a row is listed more than once.
 __device__ __forceinline__ void fix_row(const Params& p, unsigned& resets, int r) {
-  const int v = ld_rlx(p.rmatch + r);
+  const int v = ld_rlx(RM(p, r));
   if (v == -2) {
-    if (atomicCAS(p.rmatch + r, -2, -1) == -2) resets++;
+    if (atomicCAS(RM(p, r), -2, -1) == -2) resets++;
   } else if (v >= 0 && ld_rlx(p.cmatch + v) != r) {
-    if (atomicCAS(p.rmatch + r, v, -1) == v) resets++;
+    if (atomicCAS(RM(p, r), v, -1) == v) resets++;
   }
 }
 
@@ -689,7 +702,7 @@ __device__ __forceinline__ void fix_row(const Params& p, unsigned& resets, int r
 // column is unmatched afterwards.
 __device__ __forceinline__ bool fix_col(const Params& p, unsigned& resets, int c) {
   const int r = ld_rlx(p.cmatch + c);
-  if (r >= 0 && ld_rlx(p.rmatch + r) != c) {
+  if (r >= 0 && ld_rlx(RM(p, r)) != c) {
     if (atomicCAS(p.cmatch + c, r, -1) == r) resets++;
     return true;
   }
@@ -698,20 +711,23 @@ __device__ __forceinline__ bool fix_col(const Params& p, unsigned& resets, int c
 
 // Clears the visited bits the BFS left in rmatch (one streaming pass, int4).
 __device__ __forceinline__ void sweep_visited(const Params& p) {
-  int4* r4 = reinterpret_cast<int4*>(p.rmatch);
-  const unsigned long long n4 = (unsigned long long)p.nr / 4;
+  // mates are every BM_INTERLEAVE ? 2nd : 1st int; one int4 covers 4 / (1 + BM_INTERLEAVE) rows
+  constexpr int kRowsPer4 = BM_INTERLEAVE ? 2 : 4;
+  int4* r4 = reinterpret_cast<int4*>(p.rm);
+  const unsigned long long n4 = (unsigned long long)p.nr / kRowsPer4;
+  auto clr = [](int& v) { if (v >= 0) v &= ~kVisBit; };
   for (unsigned long long k = global_thread(); k < n4; k += global_threads()) {
     int4 v = ld_cg(r4 + k);
     const int4 o = v;
-    if (v.x >= 0) v.x &= ~kVisBit;
-    if (v.y >= 0) v.y &= ~kVisBit;
-    if (v.z >= 0) v.z &= ~kVisBit;
-    if (v.w >= 0) v.w &= ~kVisBit;
+    clr(v.x);
+    if (!BM_INTERLEAVE) clr(v.y);
+    clr(v.z);
+    if (!BM_INTERLEAVE) clr(v.w);
     if (v.x != o.x || v.y != o.y || v.z != o.z || v.w != o.w) st_plain(r4 + k, v);
   }
-  for (unsigned long long r = n4 * 4 + global_thread(); r < (unsigned long long)p.nr; r += global_threads()) {
-    const int v = ld_cg(p.rmatch + r);
-    if (v >= 0 && (v & kVisBit)) st_plain(p.rmatch + r, v & ~kVisBit);
+  for (unsigned long long r = n4 * kRowsPer4 + global_thread(); r < (unsigned long long)p.nr; r += global_threads()) {
+    const int v = ld_cg(RM(p, r));
+    if (v >= 0 && (v & kVisBit)) st_plain(RM(p, r), v & ~kVisBit);
   }
 }
 
@@ -961,7 +977,7 @@ __global__ void __launch_bounds__(kThreads, BM_MINB) driver_kernel(Params p) {
           if (pass == 0 && e - b != 1) continue;  // one-sided Karp-Sipser: degree-1 columns first
           for (unsigned j = b; j < e; ++j) {
             const int r = ld_ro(p.adj + j);
-            if (ld_rlx(p.rmatch + r) == -1 && atomicCAS(p.rmatch + r, -1, (int)c) == -1) {
+            if (ld_rlx(RM(p, r)) == -1 && atomicCAS(RM(p, r), -1, (int)c) == -1) {
               st_plain(p.cmatch + c, r);
               break;
             }
@@ -981,7 +997,7 @@ __global__ void __launch_bounds__(kThreads, BM_MINB) driver_kernel(Params p) {
       if (c < (unsigned long long)p.nc) {
         const int r = ld_cg(p.cmatch + c);
         if (r < -1 || r >= p.nr) bad++;
-        else if (r >= 0 && ld_cg(p.rmatch + r) != (int)c) bad++;
+        else if (r >= 0 && ld_cg(RM(p, r)) != (int)c) bad++;
         st_plain(p.bfs + c, r >= 0 ? kUnvisited : kStartLevel);
         if (r < 0) {
           beg = ld_ro(p.offs + c);
@@ -995,7 +1011,7 @@ __global__ void __launch_bounds__(kThreads, BM_MINB) driver_kernel(Params p) {
         put_entry(p.F0, 0u, p.gidx0, slot, (int)c, (int)c, beg, deg);
     }
     for (unsigned long long r = global_thread(); r < (unsigned long long)p.nr; r += global_threads()) {
-      const int v = ld_cg(p.rmatch + r);
+      const int v = ld_cg(RM(p, r));
       if (v < -1 || v >= p.nc) bad++;
       else if (v >= 0 && ld_cg(p.cmatch + v) != (int)r) bad++;
     }
@@ -1176,6 +1192,22 @@ __global__ void validate_kernel(const unsigned* offs, const int* adj, int nc, in
   }
 }
 
+// Row-state (de)interleaving between the caller's plain rmatch / predecessor
+// arrays and the device layout (see RM / PR).
+constexpr int kRowStride = BM_INTERLEAVE ? 2 : 1;
+__global__ void rows_pack_kernel(const int* plain, int* rm, int nr) {
+  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < nr; r += (long long)gridDim.x * blockDim.x)
+    rm[kRowStride * r] = plain[r];
+}
+__global__ void rows_unpack_kernel(const int* rm, int* out, int nr, int off) {
+  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < nr; r += (long long)gridDim.x * blockDim.x)
+    out[r] = rm[kRowStride * r + off];
+}
+__global__ void rows_fill_kernel(int* rm, int nr, int off, int v) {
+  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < nr; r += (long long)gridDim.x * blockDim.x)
+    rm[kRowStride * r + off] = v;
+}
+
 }  // namespace bm
 
 // ===========================================================================
@@ -1250,7 +1282,8 @@ struct bm_handle {
   unsigned* offs = nullptr;
   int* adj = nullptr;
   // state
-  int *rmatch = nullptr, *cmatch = nullptr, *pred = nullptr, *bfs = nullptr;
+  int *rm = nullptr, *cmatch = nullptr, *pred = nullptr, *bfs = nullptr;  // rm: row state (see RM / PR)
+  int* rtmp = nullptr;  // plain nr-int staging for host <-> device row arrays
   int *rmatch0 = nullptr, *cmatch0 = nullptr, *EP = nullptr;
   unsigned* dead = nullptr;
   int ndead_words = 0;
@@ -1280,6 +1313,51 @@ namespace {
 bm_status check_handle(bm_handle* h, bool need_graph) {
   if (!h) return fail(BM_ERR_INVALID_ARG, "null handle");
   if (need_graph && h->nc < 0) return fail(BM_ERR_INVALID_ARG, "no graph uploaded (call bm_upload_csc first)");
+  return BM_OK;
+}
+
+int row_blocks(bm_handle* h) { return std::max(1, std::min(h->sms * 8, (h->nr + 255) / 256)); }
+
+// plain device array (nr ints) -> row-state mates
+bm_status rows_from_plain(bm_handle* h, const int* plain) {
+  if (h->nr <= 0) return BM_OK;
+  rows_pack_kernel<<<row_blocks(h), 256, 0, h->stream>>>(plain, h->rm, h->nr);
+  BM_CUDA(cudaGetLastError());
+  return BM_OK;
+}
+// row-state mates (off 0) or predecessors (off 1) -> plain device array
+bm_status rows_to_plain(bm_handle* h, int* out, int off) {
+  if (h->nr <= 0) return BM_OK;
+  if (!BM_INTERLEAVE && off == 1) {
+    BM_CUDA(cudaMemcpyAsync(out, h->pred, sizeof(int) * h->nr, cudaMemcpyDeviceToDevice, h->stream));
+    return BM_OK;
+  }
+  rows_unpack_kernel<<<row_blocks(h), 256, 0, h->stream>>>(h->rm, out, h->nr, off);
+  BM_CUDA(cudaGetLastError());
+  return BM_OK;
+}
+bm_status rows_fill(bm_handle* h, int off, int v) {
+  if (h->nr <= 0) return BM_OK;
+  if (!BM_INTERLEAVE && off == 1) {
+    rows_fill_kernel<<<row_blocks(h), 256, 0, h->stream>>>(h->pred, h->nr, 0, v);
+  } else {
+    rows_fill_kernel<<<row_blocks(h), 256, 0, h->stream>>>(h->rm, h->nr, off, v);
+  }
+  BM_CUDA(cudaGetLastError());
+  return BM_OK;
+}
+// host rmatch -> row-state mates (through the staging buffer)
+bm_status rows_from_host(bm_handle* h, const int32_t* rmatch) {
+  if (h->nr <= 0) return BM_OK;
+  BM_CUDA(cudaMemcpyAsync(h->rtmp, rmatch, sizeof(int) * h->nr, cudaMemcpyHostToDevice, h->stream));
+  return rows_from_plain(h, h->rtmp);
+}
+bm_status rows_to_host(bm_handle* h, int32_t* out, int off) {
+  if (h->nr <= 0 || !out) return BM_OK;
+  bm_status s = rows_to_plain(h, h->rtmp, off);
+  if (s != BM_OK) return s;
+  BM_CUDA(cudaMemcpyAsync(out, h->rtmp, sizeof(int) * h->nr, cudaMemcpyDeviceToHost, h->stream));
+  BM_CUDA(cudaStreamSynchronize(h->stream));
   return BM_OK;
 }
 
@@ -1324,7 +1402,10 @@ int grid_for(bm_handle* h, int v) {
 // resets predecessors (only for parity probes that report them), and zeroes
 // the control block.
 bm_status prepare_fresh(bm_handle* h, bool reset_pred = false) {
-  if (reset_pred) BM_CUDA(cudaMemsetAsync(h->pred, 0xff, sizeof(int) * std::max(h->nr, 1), h->stream));
+  if (reset_pred) {
+    bm_status s = rows_fill(h, 1, -1);
+    if (s != BM_OK) return s;
+  }
   BM_CUDA(cudaMemsetAsync(h->ctl, 0, sizeof(Ctrl), h->stream));
   BM_CUDA(cudaMemsetAsync(h->dead, 0, sizeof(unsigned) * std::max(h->ndead_words, 1), h->stream));
   return BM_OK;
@@ -1334,7 +1415,7 @@ bm_status prepare_fresh(bm_handle* h, bool reset_pred = false) {
 // persisting L2 access-policy window on the handle's stream.
 void apply_persist(bm_handle* h) {
   const char* e = getenv("BM_PERSIST_MB");
-  if (!e || !h->rmatch) return;
+  if (!e || !h->rm) return;
   const size_t want = (size_t)atol(e) << 20;
   if (!want) return;
   cudaDeviceProp prop{};
@@ -1342,8 +1423,8 @@ void apply_persist(bm_handle* h) {
   const size_t lim = std::min<size_t>(want, (size_t)prop.persistingL2CacheMaxSize);
   cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, lim);
   cudaStreamAttrValue a{};
-  a.accessPolicyWindow.base_ptr = h->rmatch;
-  a.accessPolicyWindow.num_bytes = std::min<size_t>(std::min<size_t>(want, sizeof(int) * (size_t)h->nr),
+  a.accessPolicyWindow.base_ptr = h->rm;
+  a.accessPolicyWindow.num_bytes = std::min<size_t>(std::min<size_t>(want, sizeof(int) * kRowStride * (size_t)h->nr),
                                                     (size_t)prop.accessPolicyMaxWindowSize);
   a.accessPolicyWindow.hitRatio = 1.0f;
   a.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
@@ -1376,7 +1457,7 @@ Params make_params(bm_handle* h, const bm_match_opts& o) {
   p.nr = h->nr;
   p.offs = h->offs;
   p.adj = h->adj;
-  p.rmatch = h->rmatch;
+  p.rm = h->rm;
   p.cmatch = h->cmatch;
   p.pred = h->pred;
   p.bfs = h->bfs;
@@ -1472,7 +1553,10 @@ bm_status drive(bm_handle* h, const bm_match_opts& o, bool fresh, int64_t* cardi
       if (cb) {
         snap_r.resize(h->nr);
         snap_c.resize(h->nc);
-        BM_CUDA(cudaMemcpy(snap_r.data(), h->rmatch, sizeof(int) * h->nr, cudaMemcpyDeviceToHost));
+        {
+          bm_status rs = rows_to_host(h, snap_r.data(), 0);
+          if (rs != BM_OK) return rs;
+        }
         BM_CUDA(cudaMemcpy(snap_c.data(), h->cmatch, sizeof(int) * h->nc, cudaMemcpyDeviceToHost));
         bm_phase_event ev{};
         ev.iteration = (int64_t)h->phase_launches.size();
@@ -1604,7 +1688,8 @@ bm_status bm_destroy(bm_handle* h) {
   if (h->stream) cudaStreamSynchronize(h->stream);
   dfree(h->offs);
   dfree(h->adj);
-  dfree(h->rmatch);
+  dfree(h->rm);
+  dfree(h->rtmp);
   dfree(h->cmatch);
   dfree(h->pred);
   dfree(h->bfs);
@@ -1655,9 +1740,10 @@ bm_status bm_upload_csc(bm_handle* h, int32_t nc, int32_t nr, const int64_t* cxa
   BM_CUDA(dalloc(h->caps, h->offs, (size_t)nc + 1));
   BM_CUDA(dalloc(h->caps, h->adj, (size_t)E));
   // state (sized by the graph)
-  BM_CUDA(dalloc(h->caps, h->rmatch, nr));
+  BM_CUDA(dalloc(h->caps, h->rm, (size_t)kRowStride * std::max(nr, 1)));
+  BM_CUDA(dalloc(h->caps, h->rtmp, nr));
   BM_CUDA(dalloc(h->caps, h->cmatch, nc));
-  BM_CUDA(dalloc(h->caps, h->pred, nr));
+  if (!BM_INTERLEAVE) BM_CUDA(dalloc(h->caps, h->pred, nr));
   BM_CUDA(dalloc(h->caps, h->bfs, nc));
   BM_CUDA(dalloc(h->caps, h->rmatch0, nr));
   BM_CUDA(dalloc(h->caps, h->cmatch0, nc));
@@ -1693,7 +1779,11 @@ bm_status bm_upload_csc(bm_handle* h, int32_t nc, int32_t nr, const int64_t* cxa
     if (bad[1]) return fail(BM_ERR_INVALID_ARG, "row index out of range in cadj");
   }
   h->sorted = bad[2] == 0;
-  BM_CUDA(cudaMemsetAsync(h->pred, 0xff, sizeof(int) * std::max(nr, 1), h->stream));
+  h->nr = nr;
+  {
+    bm_status fs = rows_fill(h, 1, -1);
+    if (fs != BM_OK) return fs;
+  }
   BM_CUDA(cudaStreamSynchronize(h->stream));
   h->nc = nc;
   h->nr = nr;
@@ -1731,10 +1821,12 @@ bm_status bm_run(bm_handle* h, const bm_match_opts* opts, int64_t* cardinality, 
   BM_CUDA(cudaSetDevice(h->device));
   if (opts->init == BM_INIT_GIVEN) {
     if (!h->has_init) return fail(BM_ERR_INVALID_ARG, "no initial matching loaded (bm_load_matching)");
-    BM_CUDA(cudaMemcpyAsync(h->rmatch, h->rmatch0, sizeof(int) * std::max(h->nr, 1), cudaMemcpyDeviceToDevice, h->stream));
+    s = rows_from_plain(h, h->rmatch0);
+    if (s != BM_OK) return s;
     BM_CUDA(cudaMemcpyAsync(h->cmatch, h->cmatch0, sizeof(int) * std::max(h->nc, 1), cudaMemcpyDeviceToDevice, h->stream));
   } else {
-    BM_CUDA(cudaMemsetAsync(h->rmatch, 0xff, sizeof(int) * std::max(h->nr, 1), h->stream));
+    s = rows_fill(h, 0, -1);
+    if (s != BM_OK) return s;
     BM_CUDA(cudaMemsetAsync(h->cmatch, 0xff, sizeof(int) * std::max(h->nc, 1), h->stream));
   }
   s = prepare_fresh(h);
@@ -1761,7 +1853,8 @@ bm_status bm_download_matching(bm_handle* h, int32_t* rmatch, int32_t* cmatch) {
   bm_status s = check_handle(h, true);
   if (s != BM_OK) return s;
   BM_CUDA(cudaSetDevice(h->device));
-  if (rmatch && h->nr > 0) BM_CUDA(cudaMemcpyAsync(rmatch, h->rmatch, sizeof(int) * h->nr, cudaMemcpyDeviceToHost, h->stream));
+  s = rows_to_host(h, rmatch, 0);
+  if (s != BM_OK) return s;
   if (cmatch && h->nc > 0) BM_CUDA(cudaMemcpyAsync(cmatch, h->cmatch, sizeof(int) * h->nc, cudaMemcpyDeviceToHost, h->stream));
   BM_CUDA(cudaStreamSynchronize(h->stream));
   return BM_OK;
@@ -1805,10 +1898,12 @@ bm_status bm_match(bm_handle* h, const bm_match_opts* opts, int32_t* rmatch, int
   if ((!rmatch && h->nr > 0) || (!cmatch && h->nc > 0)) return fail(BM_ERR_INVALID_ARG, "null matching array");
   BM_CUDA(cudaSetDevice(h->device));
   if (opts->init == BM_INIT_GIVEN) {
-    if (h->nr > 0) BM_CUDA(cudaMemcpyAsync(h->rmatch, rmatch, sizeof(int) * h->nr, cudaMemcpyHostToDevice, h->stream));
+    s = rows_from_host(h, rmatch);
+    if (s != BM_OK) return s;
     if (h->nc > 0) BM_CUDA(cudaMemcpyAsync(h->cmatch, cmatch, sizeof(int) * h->nc, cudaMemcpyHostToDevice, h->stream));
   } else {
-    BM_CUDA(cudaMemsetAsync(h->rmatch, 0xff, sizeof(int) * std::max(h->nr, 1), h->stream));
+    s = rows_fill(h, 0, -1);
+    if (s != BM_OK) return s;
     BM_CUDA(cudaMemsetAsync(h->cmatch, 0xff, sizeof(int) * std::max(h->nc, 1), h->stream));
   }
   s = prepare_fresh(h);
@@ -1836,7 +1931,8 @@ bm_status bm_bfs_phase(bm_handle* h, int32_t driver, int32_t bfs_kernel, int32_t
   if (s != BM_OK) return s;
   if ((!rmatch_in && h->nr > 0) || (!cmatch_in && h->nc > 0)) return fail(BM_ERR_INVALID_ARG, "null matching array");
   BM_CUDA(cudaSetDevice(h->device));
-  if (h->nr > 0) BM_CUDA(cudaMemcpyAsync(h->rmatch, rmatch_in, sizeof(int) * h->nr, cudaMemcpyHostToDevice, h->stream));
+  s = rows_from_host(h, rmatch_in);
+  if (s != BM_OK) return s;
   if (h->nc > 0) BM_CUDA(cudaMemcpyAsync(h->cmatch, cmatch_in, sizeof(int) * h->nc, cudaMemcpyHostToDevice, h->stream));
   s = prepare_fresh(h, true);
   if (s != BM_OK) return s;
@@ -1853,8 +1949,10 @@ bm_status bm_bfs_phase(bm_handle* h, int32_t driver, int32_t bfs_kernel, int32_t
   BM_CUDA(cudaMemcpy(&ctl, h->ctl, sizeof(Ctrl), cudaMemcpyDeviceToHost));
   if (ctl.error) return ctl_error_status(ctl.error);
   if (bfs_array && h->nc > 0) BM_CUDA(cudaMemcpy(bfs_array, h->bfs, sizeof(int) * h->nc, cudaMemcpyDeviceToHost));
-  if (predecessor && h->nr > 0) BM_CUDA(cudaMemcpy(predecessor, h->pred, sizeof(int) * h->nr, cudaMemcpyDeviceToHost));
-  if (rmatch_out && h->nr > 0) BM_CUDA(cudaMemcpy(rmatch_out, h->rmatch, sizeof(int) * h->nr, cudaMemcpyDeviceToHost));
+  s = rows_to_host(h, predecessor, 1);
+  if (s != BM_OK) return s;
+  s = rows_to_host(h, rmatch_out, 0);
+  if (s != BM_OK) return s;
   if (launches) *launches = ctl.bfs_levels_last;
   if (path_found) *path_found = ctl.path_found_last;
   return BM_OK;
@@ -1866,11 +1964,12 @@ bm_status bm_verify(bm_handle* h, const int32_t* rmatch, const int32_t* cmatch, 
   if (s != BM_OK) return s;
   if ((!rmatch && h->nr > 0) || (!cmatch && h->nc > 0)) return fail(BM_ERR_INVALID_ARG, "null matching array");
   BM_CUDA(cudaSetDevice(h->device));
-  if (h->nr > 0) BM_CUDA(cudaMemcpyAsync(h->rmatch, rmatch, sizeof(int) * h->nr, cudaMemcpyHostToDevice, h->stream));
+  s = rows_from_host(h, rmatch);  // leaves the plain copy in rtmp for validate_kernel
+  if (s != BM_OK) return s;
   if (h->nc > 0) BM_CUDA(cudaMemcpyAsync(h->cmatch, cmatch, sizeof(int) * h->nc, cudaMemcpyHostToDevice, h->stream));
   BM_CUDA(cudaMemsetAsync(h->scratch, 0, sizeof(unsigned long long) * 4, h->stream));
   const int blocks = std::max(1, std::min(h->sms * 8, (std::max(h->nc, h->nr) + 255) / 256));
-  validate_kernel<<<blocks, 256, 0, h->stream>>>(h->offs, h->adj, h->nc, h->nr, h->sorted, h->rmatch,
+  validate_kernel<<<blocks, 256, 0, h->stream>>>(h->offs, h->adj, h->nc, h->nr, h->sorted, h->rtmp,
                                                  h->cmatch, h->scratch, h->scratch + 1);
   BM_CUDA(cudaGetLastError());
   unsigned long long res[2] = {0, 0};

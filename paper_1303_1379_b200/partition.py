@@ -230,9 +230,20 @@ class PartitionedMatcher:
     """The host loop of the partitioned driver (run_driver, gpu_match.cpp:306-359)."""
 
     def __init__(self, backend, exchange: Exchange):
+        import os
         self.b = backend
         self.x = exchange
         self.rank, self.world = exchange.rank, exchange.world
+        self.timing = os.environ.get("BM_PART_TIMING") == "1"  # host wall time per stage (profiling)
+        self.t = {}
+
+    def _tick(self, key, t0):
+        import time
+        if self.timing:
+            t1 = time.perf_counter()
+            self.t[key] = self.t.get(key, 0.0) + (t1 - t0)
+            return t1
+        return t0
 
     def upload(self, g: BipartiteCsr):
         lo, hi = column_range(g.nc, self.rank, self.world)
@@ -264,26 +275,35 @@ class PartitionedMatcher:
             res.phases += 1
             if res.phases > bound:
                 raise RuntimeError("termination bound exceeded: more than nc + 1 phases")
+            import time
+            t0 = time.perf_counter()
             b.begin_phase(int(kernel), endpoint_policy)
+            t0 = self._tick("begin", t0)
             found = False
             levels = 0
             while True:
                 claims, eps, nc_l, ne_l = b.expand()
+                t0 = self._tick("expand", t0)
                 counts = self.x.allgather_counts([nc_l, ne_l])
+                t0 = self._tick("counts", t0)
                 call, cstride = self._gather(claims, nc_l, counts[:, 0])
                 eall, estride = self._gather(eps, ne_l, counts[:, 1])
+                t0 = self._tick("gather", t0)
                 res.records_exchanged += int(counts.sum())
                 n_next, found = b.merge(call, counts[:, 0], cstride, eall, counts[:, 1], estride)
+                t0 = self._tick("merge", t0)
                 levels += 1
                 if (shortest and found) or n_next == 0:
                     break
             b.end_bfs()
             if self.rank == 0:
                 b.augment(serial)
+            t0 = self._tick("augment", t0)
             rm, cm = b.state()
             self.x.broadcast_(rm, 0)
             self.x.broadcast_(cm, 0)
             after = b.cardinality()
+            t0 = self._tick("broadcast", t0)
             res.levels += levels
             res.launches_per_phase.append(levels)
             if found and after <= before and not serial:

@@ -37,6 +37,9 @@ def main():
     cur_phase = defaultdict(float)
     prev_t = tl[0][2]
     for kind, arg, t in tl[1:]:
+        if kind == "level_edges":  # metadata of the level just recorded: its frontier edges
+            levels[-1] = levels[-1] + (arg,)
+            continue
         dt = (t - prev_t) / 1e3  # us
         prev_t = t
         per_kind[kind] += dt
@@ -54,6 +57,7 @@ def main():
         "per_phase_us": [{k: round(v, 1) for k, v in ph.items()} for ph in phases],
         "slowest_levels_us": sorted(levels, key=lambda x: -x[2])[:12],
         "levels_us": [round(x[2], 1) for x in levels],
+        "levels_detail": [(x[0], x[1], x[3] if len(x) > 3 else None, round(x[2], 1)) for x in levels],
         "counters": {k: getattr(ct, k) for k in ["outer_iterations", "columns_scanned", "edges_traversed",
                                                  "columns_visited", "walk_steps", "alternations_attempted",
                                                  "fix_resets", "frontier_entries"]},
