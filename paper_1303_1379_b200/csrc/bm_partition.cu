@@ -80,33 +80,110 @@ __global__ void part_roots_kernel(PartDev d, int2* F, int* nF) {
   }
 }
 
-// One level over the local frontier: a warp per entry, lanes stride over its
-// rows. Local claims are deduplicated with the rmatch visited bit and the
-// -1 -> -2 CAS; the merge decides the global winners.
-__global__ void part_expand_kernel(PartDev d, const int2* F, int n, int4* claims, int* n_claims, int4* eps,
-                                   int* n_eps, unsigned long long* stats) {
+// One level over the local frontier. Each 8-lane group of a warp takes one
+// entry and strides over its rows; entries of degree >= kBig are done by the
+// whole warp afterwards (degree skew, e.g. R-MAT hubs). Local claims are
+// deduplicated with the rmatch visited bit and the -1 -> -2 CAS; the merge
+// decides the global winners.
+constexpr int kGroup = 8;
+constexpr unsigned long long kBig = 256;
+
+// Records are staged in shared memory and reserved with one global atomic per
+// CTA batch (a warp-level atomic per record batch on a single counter
+// serialises in L2); a full stage falls back to a warp-aggregated global append.
+constexpr int kStageC = 1024, kStageE = 256;
+struct PartSmem {
+  int4 c[kStageC];
+  int4 e[kStageE];
+  int nc, ne, bc, be;
+};
+
+__device__ __forceinline__ void stage(int4* buf, int* n, int cap, int4* out, int* count, int4 rec) {
+  const unsigned m = __activemask();
+  const int leader = __ffs(m) - 1;
+  const int rank = __popc(m & ((1u << lane_id()) - 1));
+  int base = 0;
+  if ((int)lane_id() == leader) base = atomicAdd(n, __popc(m));
+  base = __shfl_sync(m, base, leader) + rank;
+  if (base < cap) buf[base] = rec;
+  else append(out, count, rec);
+}
+
+__device__ __forceinline__ void part_edge(const PartDev& d, PartSmem& sm, int row, int c, int root, int4* claims,
+                                          int* n_claims, int4* eps, int* n_eps) {
+  const int cm = ld_rlx(d.rmatch + row);
+  if (cm >= 0) {
+    if (!(cm & kVis) && !(atomicOr(d.rmatch + row, kVis) & kVis))
+      stage(sm.c, &sm.nc, kStageC, claims, n_claims, make_int4(cm, c, root, row));
+  } else if (cm == -1) {
+    if (d.ep_one && dead_root(d, root)) return;
+    if (atomicCAS(d.rmatch + row, -1, -2) == -1) stage(sm.e, &sm.ne, kStageE, eps, n_eps, make_int4(row, c, root, 0));
+  }
+}
+
+// Copies the CTA's staged records to the global record arrays (CTA-uniform call).
+__device__ __forceinline__ void flush_stage(PartSmem& sm, int4* claims, int* n_claims, int4* eps, int* n_eps) {
+  __syncthreads();
+  const int nc = min(sm.nc, kStageC), ne = min(sm.ne, kStageE);
+  if (threadIdx.x == 0) {
+    sm.bc = nc ? atomicAdd(n_claims, nc) : 0;
+    sm.be = ne ? atomicAdd(n_eps, ne) : 0;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < nc; i += blockDim.x) claims[sm.bc + i] = sm.c[i];
+  for (int i = threadIdx.x; i < ne; i += blockDim.x) eps[sm.be + i] = sm.e[i];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    sm.nc = 0;
+    sm.ne = 0;
+  }
+}
+
+__global__ void __launch_bounds__(kThr) part_expand_kernel(PartDev d, const int2* F, int n, int4* claims,
+                                                           int* n_claims, int4* eps, int* n_eps,
+                                                           unsigned long long* stats) {
+  __shared__ PartSmem sm;
+  if (threadIdx.x == 0) {
+    sm.nc = 0;
+    sm.ne = 0;
+  }
+  __syncthreads();
   const int lane = lane_id();
-  const long long warps = (long long)gridDim.x * blockDim.x / 32;
+  const int grp = lane / kGroup, g = lane % kGroup;
+  constexpr int kPerCta = kThr / kGroup;  // entries per CTA batch
   unsigned long long trav = 0, cexp = 0;
-  for (long long w = (blockIdx.x * (long long)blockDim.x + threadIdx.x) / 32; w < n; w += warps) {
-    const int2 ent = F[w];
-    const int c = ent.x, root = ent.y;
-    if (d.wr && dead_root(d, root)) continue;  // gpu_match.cpp:106-108
-    const unsigned long long b = d.offs[c - d.col_lo], e = d.offs[c - d.col_lo + 1];
-    if (lane == 0) {
+  for (long long cbase = (long long)blockIdx.x * kPerCta; cbase < n; cbase += (long long)gridDim.x * kPerCta) {
+    const long long w = cbase + threadIdx.x / kGroup;
+    int c = 0, root = 0;
+    unsigned long long b = 0, e = 0;
+    if (w < n) {
+      const int2 ent = F[w];
+      c = ent.x;
+      root = ent.y;
+      if (!(d.wr && dead_root(d, root))) {  // gpu_match.cpp:106-108
+        b = d.offs[c - d.col_lo];
+        e = d.offs[c - d.col_lo + 1];
+      }
+    }
+    const bool big = e - b >= kBig;
+    if (g == 0 && e > b) {
       cexp++;
       trav += e - b;
     }
-    for (unsigned long long j = b + lane; j < e; j += 32) {
-      const int row = d.adj[j];
-      const int cm = ld_rlx(d.rmatch + row);
-      if (cm >= 0) {
-        if (!(cm & kVis) && !(atomicOr(d.rmatch + row, kVis) & kVis)) append(claims, n_claims, make_int4(cm, c, root, row));
-      } else if (cm == -1) {
-        if (d.ep_one && dead_root(d, root)) continue;
-        if (atomicCAS(d.rmatch + row, -1, -2) == -1) append(eps, n_eps, make_int4(row, c, root, 0));
-      }
+    if (!big)
+      for (unsigned long long j = b + g; j < e; j += kGroup)
+        part_edge(d, sm, d.adj[j], c, root, claims, n_claims, eps, n_eps);
+    unsigned bigm = __ballot_sync(kFull, big && g == 0);
+    while (bigm) {  // whole warp on each high-degree entry of this batch
+      const int src = __ffs(bigm) - 1;
+      bigm &= bigm - 1;
+      const int bc = __shfl_sync(kFull, c, src), br = __shfl_sync(kFull, root, src);
+      const unsigned long long bb = __shfl_sync(kFull, b, src), be = __shfl_sync(kFull, e, src);
+      for (unsigned long long j = bb + lane; j < be; j += 32)
+        part_edge(d, sm, d.adj[j], bc, br, claims, n_claims, eps, n_eps);
     }
+    (void)grp;
+    flush_stage(sm, claims, n_claims, eps, n_eps);
   }
   trav = warp_sum(trav);
   cexp = warp_sum(cexp);
@@ -532,7 +609,7 @@ bm_status bm_part_expand(bm_part* pt, void* claims_out, void* endpoints_out, int
   PCUDA(cudaSetDevice(pt->device));
   PCUDA(cudaMemsetAsync(pt->cnt + 2, 0, sizeof(int) * 2, pt->stream));
   if (pt->n_cur > 0)
-    part_expand_kernel<<<blocks_for(pt, (long long)pt->n_cur * 32), kThr, 0, pt->stream>>>(
+    part_expand_kernel<<<blocks_for(pt, (long long)pt->n_cur * kGroup), kThr, 0, pt->stream>>>(
         dev_of(pt), pt->F[pt->cur], pt->n_cur, static_cast<int4*>(claims_out), pt->cnt + 2,
         static_cast<int4*>(endpoints_out), pt->cnt + 3, pt->stats);
   PCUDA(cudaGetLastError());
