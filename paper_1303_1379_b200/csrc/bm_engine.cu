@@ -79,8 +79,8 @@ constexpr unsigned kWBuf = kGran * kMaxTileGran;
 #ifndef BM_BATCH
 #define BM_BATCH 1  // issue all of a thread's claim atomics before consuming any
 #endif
-#ifndef BM_INTERLEAVE
-#define BM_INTERLEAVE 1
+#ifndef BM_INTERLEAVE_MB
+#define BM_INTERLEAVE_MB 72  // interleave {mate, pred} when the plain rmatch exceeds this many MB
 #endif
 #ifndef BM_SOLO_EDGES
 #define BM_SOLO_EDGES 4096
@@ -184,7 +184,8 @@ struct Params {
   int nc, nr;
   const unsigned* offs;  // nc + 1
   const int* adj;        // E
-  int* rm;          // row state: BM_INTERLEAVE ? {mate, pred} pairs : mates (pred in `pred`)
+  int* rm;          // row state: mates at rm[rs * r]
+  int rs;           // row stride: 2 = interleaved {mate, pred}, 1 = plain (pred in `pred`)
   int* cmatch;
   int* pred;
   int* bfs;
@@ -360,15 +361,15 @@ __device__ __forceinline__ void put_entry(int4* F, unsigned out_base, unsigned* 
   for (unsigned m = (pre + kGran - 1) / kGran; m <= m1; ++m) st_plain(reinterpret_cast<int*>(gidx) + m, (int)local);
 }
 
-// Row state layout. With BM_INTERLEAVE (default) a row's mate (rmatch) and
+// Row state layout (chosen per graph at upload). Interleaved: a row's mate (rmatch) and
 // its BFS predecessor share one 8-byte slot: the claim is an atomicOr on the
 // mate word and the predecessor store that follows it lands in the same L2
 // sector, which the atomic has just brought in and dirtied, instead of a
 // second random sector (with a DRAM read-for-fill of a partial write).
-__device__ __forceinline__ int* RM(const Params& p, long long r) { return p.rm + (BM_INTERLEAVE ? 2 * r : r); }
-__device__ __forceinline__ int* PR(const Params& p, long long r) {
-  return BM_INTERLEAVE ? p.rm + 2 * r + 1 : p.pred + r;
-}
+// That wins once rmatch is far larger than L2 (C4, C5); while rmatch fits in
+// L2 the plain layout keeps the gathered array half as large (C2, C3).
+__device__ __forceinline__ int* RM(const Params& p, long long r) { return p.rm + p.rs * r; }
+__device__ __forceinline__ int* PR(const Params& p, long long r) { return p.pred + p.rs * r; }
 
 // WR early-exit test (gpu_match.cpp:106-108) against the dead-root bitmap:
 // nc/8 bytes that stay in L2, instead of a bfs_array[root] gather per entry.
@@ -711,8 +712,9 @@ __device__ __forceinline__ bool fix_col(const Params& p, unsigned& resets, int c
 
 // Clears the visited bits the BFS left in rmatch (one streaming pass, int4).
 __device__ __forceinline__ void sweep_visited(const Params& p) {
-  // mates are every BM_INTERLEAVE ? 2nd : 1st int; one int4 covers 4 / (1 + BM_INTERLEAVE) rows
-  constexpr int kRowsPer4 = BM_INTERLEAVE ? 2 : 4;
+  // one int4 covers 2 interleaved rows or 4 plain ones
+  const bool il = p.rs == 2;
+  const int kRowsPer4 = il ? 2 : 4;
   int4* r4 = reinterpret_cast<int4*>(p.rm);
   const unsigned long long n4 = (unsigned long long)p.nr / kRowsPer4;
   auto clr = [](int& v) { if (v >= 0) v &= ~kVisBit; };
@@ -720,9 +722,9 @@ __device__ __forceinline__ void sweep_visited(const Params& p) {
     int4 v = ld_cg(r4 + k);
     const int4 o = v;
     clr(v.x);
-    if (!BM_INTERLEAVE) clr(v.y);
+    if (!il) clr(v.y);
     clr(v.z);
-    if (!BM_INTERLEAVE) clr(v.w);
+    if (!il) clr(v.w);
     if (v.x != o.x || v.y != o.y || v.z != o.z || v.w != o.w) st_plain(r4 + k, v);
   }
   for (unsigned long long r = n4 * kRowsPer4 + global_thread(); r < (unsigned long long)p.nr; r += global_threads()) {
@@ -1194,18 +1196,17 @@ __global__ void validate_kernel(const unsigned* offs, const int* adj, int nc, in
 
 // Row-state (de)interleaving between the caller's plain rmatch / predecessor
 // arrays and the device layout (see RM / PR).
-constexpr int kRowStride = BM_INTERLEAVE ? 2 : 1;
-__global__ void rows_pack_kernel(const int* plain, int* rm, int nr) {
+__global__ void rows_pack_kernel(const int* plain, int* rm, int nr, int rs) {
   for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < nr; r += (long long)gridDim.x * blockDim.x)
-    rm[kRowStride * r] = plain[r];
+    rm[rs * r] = plain[r];
 }
-__global__ void rows_unpack_kernel(const int* rm, int* out, int nr, int off) {
+__global__ void rows_unpack_kernel(const int* a, int* out, int nr, int rs) {
   for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < nr; r += (long long)gridDim.x * blockDim.x)
-    out[r] = rm[kRowStride * r + off];
+    out[r] = a[rs * r];
 }
-__global__ void rows_fill_kernel(int* rm, int nr, int off, int v) {
+__global__ void rows_fill_kernel(int* a, int nr, int rs, int v) {
   for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < nr; r += (long long)gridDim.x * blockDim.x)
-    rm[kRowStride * r + off] = v;
+    a[rs * r] = v;
 }
 
 }  // namespace bm
@@ -1283,6 +1284,8 @@ struct bm_handle {
   int* adj = nullptr;
   // state
   int *rm = nullptr, *cmatch = nullptr, *pred = nullptr, *bfs = nullptr;  // rm: row state (see RM / PR)
+  int* pred_plain = nullptr;  // separate predecessors for the plain layout (pred aliases rm + 1 otherwise)
+  int rs = 1;                 // row stride of rm / pred
   int* rtmp = nullptr;  // plain nr-int staging for host <-> device row arrays
   int *rmatch0 = nullptr, *cmatch0 = nullptr, *EP = nullptr;
   unsigned* dead = nullptr;
@@ -1321,28 +1324,20 @@ int row_blocks(bm_handle* h) { return std::max(1, std::min(h->sms * 8, (h->nr + 
 // plain device array (nr ints) -> row-state mates
 bm_status rows_from_plain(bm_handle* h, const int* plain) {
   if (h->nr <= 0) return BM_OK;
-  rows_pack_kernel<<<row_blocks(h), 256, 0, h->stream>>>(plain, h->rm, h->nr);
+  rows_pack_kernel<<<row_blocks(h), 256, 0, h->stream>>>(plain, h->rm, h->nr, h->rs);
   BM_CUDA(cudaGetLastError());
   return BM_OK;
 }
 // row-state mates (off 0) or predecessors (off 1) -> plain device array
 bm_status rows_to_plain(bm_handle* h, int* out, int off) {
   if (h->nr <= 0) return BM_OK;
-  if (!BM_INTERLEAVE && off == 1) {
-    BM_CUDA(cudaMemcpyAsync(out, h->pred, sizeof(int) * h->nr, cudaMemcpyDeviceToDevice, h->stream));
-    return BM_OK;
-  }
-  rows_unpack_kernel<<<row_blocks(h), 256, 0, h->stream>>>(h->rm, out, h->nr, off);
+  rows_unpack_kernel<<<row_blocks(h), 256, 0, h->stream>>>(off ? h->pred : h->rm, out, h->nr, h->rs);
   BM_CUDA(cudaGetLastError());
   return BM_OK;
 }
 bm_status rows_fill(bm_handle* h, int off, int v) {
   if (h->nr <= 0) return BM_OK;
-  if (!BM_INTERLEAVE && off == 1) {
-    rows_fill_kernel<<<row_blocks(h), 256, 0, h->stream>>>(h->pred, h->nr, 0, v);
-  } else {
-    rows_fill_kernel<<<row_blocks(h), 256, 0, h->stream>>>(h->rm, h->nr, off, v);
-  }
+  rows_fill_kernel<<<row_blocks(h), 256, 0, h->stream>>>(off ? h->pred : h->rm, h->nr, h->rs, v);
   BM_CUDA(cudaGetLastError());
   return BM_OK;
 }
@@ -1424,7 +1419,7 @@ void apply_persist(bm_handle* h) {
   cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, lim);
   cudaStreamAttrValue a{};
   a.accessPolicyWindow.base_ptr = h->rm;
-  a.accessPolicyWindow.num_bytes = std::min<size_t>(std::min<size_t>(want, sizeof(int) * kRowStride * (size_t)h->nr),
+  a.accessPolicyWindow.num_bytes = std::min<size_t>(std::min<size_t>(want, sizeof(int) * h->rs * (size_t)h->nr),
                                                     (size_t)prop.accessPolicyMaxWindowSize);
   a.accessPolicyWindow.hitRatio = 1.0f;
   a.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
@@ -1458,6 +1453,7 @@ Params make_params(bm_handle* h, const bm_match_opts& o) {
   p.offs = h->offs;
   p.adj = h->adj;
   p.rm = h->rm;
+  p.rs = h->rs;
   p.cmatch = h->cmatch;
   p.pred = h->pred;
   p.bfs = h->bfs;
@@ -1691,7 +1687,8 @@ bm_status bm_destroy(bm_handle* h) {
   dfree(h->rm);
   dfree(h->rtmp);
   dfree(h->cmatch);
-  dfree(h->pred);
+  dfree(h->pred_plain);
+  h->pred = nullptr;
   dfree(h->bfs);
   dfree(h->rmatch0);
   dfree(h->cmatch0);
@@ -1740,10 +1737,19 @@ bm_status bm_upload_csc(bm_handle* h, int32_t nc, int32_t nr, const int64_t* cxa
   BM_CUDA(dalloc(h->caps, h->offs, (size_t)nc + 1));
   BM_CUDA(dalloc(h->caps, h->adj, (size_t)E));
   // state (sized by the graph)
-  BM_CUDA(dalloc(h->caps, h->rm, (size_t)kRowStride * std::max(nr, 1)));
+  // row layout: interleave {mate, pred} once rmatch alone is far larger than L2
+  {
+    const char* lay = getenv("BM_ROW_LAYOUT");  // tuning override: "plain" | "interleave"
+    bool il = (size_t)nr * sizeof(int) > ((size_t)BM_INTERLEAVE_MB << 20);
+    if (lay && !strcmp(lay, "plain")) il = false;
+    if (lay && !strcmp(lay, "interleave")) il = true;
+    h->rs = il ? 2 : 1;
+  }
+  BM_CUDA(dalloc(h->caps, h->rm, (size_t)2 * std::max(nr, 1)));
   BM_CUDA(dalloc(h->caps, h->rtmp, nr));
   BM_CUDA(dalloc(h->caps, h->cmatch, nc));
-  if (!BM_INTERLEAVE) BM_CUDA(dalloc(h->caps, h->pred, nr));
+  BM_CUDA(dalloc(h->caps, h->pred_plain, nr));
+  h->pred = h->rs == 2 ? h->rm + 1 : h->pred_plain;
   BM_CUDA(dalloc(h->caps, h->bfs, nc));
   BM_CUDA(dalloc(h->caps, h->rmatch0, nr));
   BM_CUDA(dalloc(h->caps, h->cmatch0, nc));
