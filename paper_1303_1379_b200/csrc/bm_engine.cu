@@ -371,6 +371,15 @@ __device__ __forceinline__ void put_entry(int4* F, unsigned out_base, unsigned* 
 __device__ __forceinline__ int* RM(const Params& p, long long r) { return p.rm + p.rs * r; }
 __device__ __forceinline__ int* PR(const Params& p, long long r) { return p.pred + p.rs * r; }
 
+// Offsets of a claimed column: read once per claim, no reuse worth keeping in
+// L2 (BM_OFFS_EF: evict_first, so they do not displace the gathered rmatch).
+#ifndef BM_OFFS_EF
+#define BM_OFFS_EF 0
+#endif
+__device__ __forceinline__ unsigned ld_offs(const unsigned* a, unsigned long long pol) {
+  return BM_OFFS_EF ? ld_ro_hint(a, pol) : ld_ro(a);
+}
+
 // WR early-exit test (gpu_match.cpp:106-108) against the dead-root bitmap:
 // nc/8 bytes that stay in L2, instead of a bfs_array[root] gather per entry.
 // bfs_array[root] still carries the reference's mark (and the endpoint for
@@ -609,8 +618,8 @@ __device__ __forceinline__ void expand_level(const Params& p, Smem& sm, int4* F,
           unsigned b0 = 0, d0 = 0;
           if (has) {
             cr = sm.wbuf[tid];
-            b0 = ld_ro(p.offs + cr.x);
-            d0 = ld_ro(p.offs + cr.x + 1) - b0;
+            b0 = ld_offs(p.offs + cr.x, pol);
+            d0 = ld_offs(p.offs + cr.x + 1, pol) - b0;
           }
           cta_reserve(sm, has ? 1u : 0u, d0, 0u, out, &p.ctl->n_ep, slot, unused);
           if (has) put_entry(F, out_base, gout, slot, cr.x, cr.y, b0, d0, pol);
@@ -618,14 +627,14 @@ __device__ __forceinline__ void expand_level(const Params& p, Smem& sm, int4* F,
           unsigned cnt = 0, deg = 0;
           for (unsigned j = tid; j < nw; j += kThreads) {
             const int c = sm.wbuf[j].x;
-            deg += ld_ro(p.offs + c + 1) - ld_ro(p.offs + c);
+            deg += ld_offs(p.offs + c + 1, pol) - ld_offs(p.offs + c, pol);
             cnt++;
           }
           cta_reserve(sm, cnt, deg, 0u, out, &p.ctl->n_ep, slot, unused);
           for (unsigned j = tid; j < nw; j += kThreads) {
             const int2 cr = sm.wbuf[j];
-            const unsigned b0 = ld_ro(p.offs + cr.x);
-            const unsigned d0 = ld_ro(p.offs + cr.x + 1) - b0;
+            const unsigned b0 = ld_offs(p.offs + cr.x, pol);
+            const unsigned d0 = ld_offs(p.offs + cr.x + 1, pol) - b0;
             put_entry(F, out_base, gout, slot, cr.x, cr.y, b0, d0, pol);
             slot += (1ull << 33) + d0;
           }
