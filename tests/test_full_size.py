@@ -1,0 +1,44 @@
+"""Full-size parity (BASELINE configs C2-C4 at their real sizes, -m gpu).
+
+The expected maxima come from the reference itself (tests/golden/
+make_large_answers.py runs /root/reference's apfb-wr-ct on the same graphs and
+records a digest of each graph); C2's maximum is also n by construction (a
+planted perfect matching) and C4's is the number of live rows. Every GPU
+result must additionally pass the GPU Berge certificate (valid matching, no
+augmenting path)."""
+import json
+import os
+
+import pytest
+
+import bench
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+KNOWN = json.load(open(os.path.join(ROOT, "tests", "golden", "known_answers.json")))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cfg", ["C2", "C3", "C4"])
+def test_full_size_configs(engine, cfg):
+    import paper_1303_1379_b200 as bm
+    g, known = bench.build_graph(cfg, 1)
+    full = KNOWN.get(f"{cfg}/full")
+    if full is not None:  # the generator still builds the graph the reference solved
+        assert str(bm.csc_digest(g)) == full["digest"]
+        assert g.num_edges() == full["edges"]
+        want = full["maximum"]
+    else:
+        want = known
+    assert want is not None, f"no known answer for {cfg}"
+    if known is not None:
+        assert want == known
+    init = bm.cheap_matching(g)
+    engine.upload(g, force=True)
+    engine.load_matching(init)
+    for algo in ["apfb-wr", "apsb-wr", "apfb-gpubfs"]:
+        shortest, kernel, improved = bench.ALGOS[algo]
+        card, ct, done = engine.run(shortest=shortest, kernel=bm.BfsKernel(kernel), improved=improved)
+        assert done and card == want, (cfg, algo, card, want)
+        m = engine.download()
+        viol, ismax, vcard = engine.verify(g, m)
+        assert viol == 0 and ismax and vcard == want, (cfg, algo, viol, ismax, vcard)
