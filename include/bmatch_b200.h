@@ -213,6 +213,16 @@ bm_status   bm_bfs_phase(bm_handle* h, int32_t driver, int32_t bfs_kernel, int32
 bm_status   bm_verify(bm_handle* h, const int32_t* rmatch, const int32_t* cmatch,
                       int64_t* violations, int32_t* is_max, int64_t* cardinality);
 
+/* ---- random relabelling on the device (permute_random, csr_graph.cpp:80-90) ----
+ * Relabels the uploaded graph: column c becomes cperm[c], row r becomes
+ * rperm[r], and each column's rows are re-sorted (the RCP experiments,
+ * PAPER.md:444-445). With the permutations of bm_permutation_pair(seed) the
+ * result is bit-identical to the reference's permute_random(g, seed). Any
+ * loaded initial matching is dropped. bm_download_csc returns the resident
+ * graph (cxadj[nc+1], cadj[E]). */
+bm_status   bm_permute_random(bm_handle* h, const int32_t* cperm, const int32_t* rperm);
+bm_status   bm_download_csc(bm_handle* h, int64_t* cxadj, int32_t* cadj);
+
 /* ---- 1-D column partition over several GPUs --------------
  * The reference has no multi-device path (its only parallelism is the
  * emulated grid, kernel_grid.hpp:161-222). One bm_part per rank (process,

@@ -54,6 +54,10 @@ bm_status bm_gen_banded(int32_t n, int32_t band, double delete_frac, uint64_t se
                         int32_t threads, int64_t* cxadj, int32_t* cadj, int64_t* nedges,
                         int64_t* live_rows);
 
+/* The column and row permutations of the reference's permute_random(g, seed)
+ * (csr_graph.cpp:68-90): one mt19937_64, columns drawn first. */
+bm_status bm_permutation_pair(int32_t nc, int32_t nr, uint64_t seed, int32_t* cperm, int32_t* rperm);
+
 /* Structural check of a CSC (check_csr, csr_graph.cpp:45-64): returns BM_OK or
  * BM_ERR_INVALID_ARG with the first violation in bm_last_error(). */
 bm_status bm_check_csc(int32_t nc, int32_t nr, const int64_t* cxadj, const int32_t* cadj);

@@ -112,6 +112,9 @@ _PROTOS = {
     "bm_bfs_phase": (C.c_int, [_vp, C.c_int32, C.c_int32, C.c_int32, _i32p, _i32p, _i32p, _i32p, _i32p,
                                _i64p, _i32p]),
     "bm_verify": (C.c_int, [_vp, _i32p, _i32p, _i64p, _i32p, _i64p]),
+    "bm_permute_random": (C.c_int, [_vp, _i32p, _i32p]),
+    "bm_download_csc": (C.c_int, [_vp, _i64p, _i32p]),
+    "bm_permutation_pair": (C.c_int, [C.c_int32, C.c_int32, C.c_uint64, _i32p, _i32p]),
     "bm_host_cheap_matching": (C.c_int, [C.c_int32, C.c_int32, _i64p, _i32p, _i32p, _i32p]),
     "bm_gen_uniform_capacity": (C.c_int64, [C.c_int32, C.c_double]),
     "bm_gen_uniform": (C.c_int, [C.c_int32, C.c_int32, C.c_double, C.c_uint64, C.c_int32, _i64p, _i32p, _i64p]),

@@ -34,6 +34,7 @@ __all__ = [
     "AlgorithmResult", "Engine", "apfb", "apsb", "cheap_matching", "cardinality", "check_csr",
     "csc_digest", "algorithm_ids", "make_algorithm", "register_algorithm", "generate_random_bipartite",
     "generate_planted", "generate_rmat", "generate_banded", "LogicError", "CudaError", "INIT_MODES",
+    "permutation_pair",
 ]
 
 INIT_MODES = {"given": _lib.BM_INIT_GIVEN, "gpu_greedy": _lib.BM_INIT_GPU_GREEDY, "gpu_ks": _lib.BM_INIT_GPU_KS}
@@ -351,6 +352,21 @@ class Engine:
                                C.byref(launches), C.byref(found)))
         return bfs, pred, rm, int(launches.value), bool(found.value)
 
+    def permute_random(self, seed: int):
+        """Relabel the resident graph on the device exactly as the reference's
+        permute_random(g, seed) (csr_graph.cpp:80-90)."""
+        gnc, gnr, _ = self.graph_info()
+        cp, rp = permutation_pair(gnc, gnr, seed)
+        check(lib.bm_permute_random(self._h, i32p(cp), i32p(rp)))
+        self._graph = None
+
+    def download_graph(self, name: str = "") -> BipartiteCsr:
+        gnc, gnr, ne = self.graph_info()
+        cx = np.zeros(gnc + 1, np.int64)
+        adj = np.zeros(max(ne, 0), np.int32)
+        check(lib.bm_download_csc(self._h, i64p(cx), i32p(adj)))
+        return BipartiteCsr(gnc, gnr, cx, adj, name)
+
     def verify(self, g: BipartiteCsr, m: MatchingState):
         """GPU Berge certificate: (violations, is_maximum, cardinality)."""
         self.upload(g)
@@ -385,6 +401,14 @@ def apsb(g: BipartiteCsr, init: MatchingState, grid=None, schedule=None, kernel=
         raise LogicError("the endpoint-encoded alternation requires the with-root kernel")
     return default_engine(device).match(g, init, shortest=True, kernel=BfsKernel(kernel),
                                         improved=improved_alternate, init_mode=init_mode, observer=observer)
+
+
+def permutation_pair(nc: int, nr: int, seed: int):
+    """(cperm, rperm) of the reference's permute_random(g, seed) (csr_graph.cpp:68-90)."""
+    cp = np.zeros(max(nc, 0), np.int32)
+    rp = np.zeros(max(nr, 0), np.int32)
+    check(lib.bm_permutation_pair(nc, nr, seed, i32p(cp), i32p(rp)))
+    return cp, rp
 
 
 def cheap_matching(g: BipartiteCsr) -> MatchingState:

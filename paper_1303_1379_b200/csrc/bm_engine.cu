@@ -53,6 +53,8 @@
 #include <vector>
 
 #include <cooperative_groups.h>
+#include <cub/device/device_scan.cuh>
+#include <cub/device/device_segmented_sort.cuh>
 #include <cuda_runtime.h>
 
 #include "bm_device.cuh"
@@ -1218,6 +1220,21 @@ __global__ void rows_fill_kernel(int* a, int nr, int rs, int v) {
     a[rs * r] = v;
 }
 
+// permute_random on the device (csr_graph.cpp:80-90): column c becomes
+// cperm[c], row r becomes rperm[r], each column's rows re-sorted.
+__global__ void perm_degrees_kernel(const unsigned* offs, const int* cperm, unsigned* deg, int nc) {
+  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < nc; c += (long long)gridDim.x * blockDim.x)
+    deg[cperm[c]] = offs[c + 1] - offs[c];
+}
+__global__ void perm_scatter_kernel(const unsigned* offs, const int* adj, const int* cperm, const int* rperm,
+                                    const unsigned* noffs, int* nadj, int nc) {
+  const long long warps = (long long)gridDim.x * blockDim.x / 32;
+  for (long long c = (blockIdx.x * (long long)blockDim.x + threadIdx.x) / 32; c < nc; c += warps) {
+    const unsigned b = offs[c], e = offs[c + 1], d = noffs[cperm[c]];
+    for (unsigned j = b + lane_id(); j < e; j += 32) nadj[d + (j - b)] = rperm[adj[j]];
+  }
+}
+
 }  // namespace bm
 
 // ===========================================================================
@@ -1970,6 +1987,86 @@ bm_status bm_bfs_phase(bm_handle* h, int32_t driver, int32_t bfs_kernel, int32_t
   if (s != BM_OK) return s;
   if (launches) *launches = ctl.bfs_levels_last;
   if (path_found) *path_found = ctl.path_found_last;
+  return BM_OK;
+}
+
+bm_status bm_permute_random(bm_handle* h, const int32_t* cperm, const int32_t* rperm) {
+  bm_status s = check_handle(h, true);
+  if (s != BM_OK) return s;
+  if ((h->nc > 0 && !cperm) || (h->nr > 0 && !rperm)) return fail(BM_ERR_INVALID_ARG, "null permutation");
+  if (h->E > 0x7fffffffll) return fail(BM_ERR_INVALID_ARG, "bm_permute_random supports E < 2^31 (segmented sort)");
+  {  // a permutation, not just any map (the device scatter relies on it)
+    std::vector<char> seen((size_t)std::max(h->nc, h->nr), 0);
+    for (int i = 0; i < h->nc; ++i) {
+      if (cperm[i] < 0 || cperm[i] >= h->nc || seen[cperm[i]]) return fail(BM_ERR_INVALID_ARG, "cperm is not a permutation");
+      seen[cperm[i]] = 1;
+    }
+    std::fill(seen.begin(), seen.end(), 0);
+    for (int i = 0; i < h->nr; ++i) {
+      if (rperm[i] < 0 || rperm[i] >= h->nr || seen[rperm[i]]) return fail(BM_ERR_INVALID_ARG, "rperm is not a permutation");
+      seen[rperm[i]] = 1;
+    }
+  }
+  BM_CUDA(cudaSetDevice(h->device));
+  const int nc = h->nc, nr = h->nr;
+  const long long E = h->E;
+  int *dcp = nullptr, *drp = nullptr, *nadj = nullptr, *sadj = nullptr;
+  unsigned *deg = nullptr, *noffs = nullptr;
+  void* tmp = nullptr;
+  size_t tmp_scan = 0, tmp_sort = 0;
+  auto cleanup = [&]() {
+    cudaFree(dcp); cudaFree(drp); cudaFree(nadj); cudaFree(sadj); cudaFree(deg); cudaFree(tmp);
+  };
+  cudaError_t e = cudaMalloc(&dcp, sizeof(int) * std::max(nc, 1));
+  if (e == cudaSuccess) e = cudaMalloc(&drp, sizeof(int) * std::max(nr, 1));
+  if (e == cudaSuccess) e = cudaMalloc(&deg, sizeof(unsigned) * ((size_t)nc + 1));
+  if (e == cudaSuccess) e = cudaMalloc(&nadj, sizeof(int) * std::max<long long>(E, 1));
+  if (e == cudaSuccess) e = cudaMalloc(&sadj, sizeof(int) * std::max<long long>(E, 1));
+  if (e != cudaSuccess) {
+    cleanup();
+    return cuda_fail(e, "bm_permute_random");
+  }
+  noffs = deg;  // scanned in place: deg[nc] = 0 -> offsets
+  const int blocks = std::max(1, std::min(h->sms * 8, (nc + 255) / 256));
+  cudaMemcpyAsync(dcp, cperm, sizeof(int) * nc, cudaMemcpyHostToDevice, h->stream);
+  cudaMemcpyAsync(drp, rperm, sizeof(int) * nr, cudaMemcpyHostToDevice, h->stream);
+  cudaMemsetAsync(deg, 0, sizeof(unsigned) * ((size_t)nc + 1), h->stream);
+  if (nc > 0) perm_degrees_kernel<<<blocks, 256, 0, h->stream>>>(h->offs, dcp, deg, nc);
+  cub::DeviceScan::ExclusiveSum(nullptr, tmp_scan, deg, noffs, nc + 1, h->stream);
+  cub::DeviceSegmentedSort::SortKeys(nullptr, tmp_sort, nadj, sadj, (int64_t)E, nc, noffs, noffs + 1, h->stream);
+  e = cudaMalloc(&tmp, std::max<size_t>(std::max(tmp_scan, tmp_sort), 1));
+  if (e != cudaSuccess) {
+    cleanup();
+    return cuda_fail(e, "bm_permute_random temp");
+  }
+  cub::DeviceScan::ExclusiveSum(tmp, tmp_scan, deg, noffs, nc + 1, h->stream);
+  if (nc > 0) {
+    const int wb = std::max(1, std::min(h->sms * 16, (int)(((long long)nc * 32 + 255) / 256)));
+    perm_scatter_kernel<<<wb, 256, 0, h->stream>>>(h->offs, h->adj, dcp, drp, noffs, nadj, nc);
+    cub::DeviceSegmentedSort::SortKeys(tmp, tmp_sort, nadj, sadj, (int64_t)E, nc, noffs, noffs + 1, h->stream);
+  }
+  e = cudaGetLastError();
+  if (e == cudaSuccess && E > 0) e = cudaMemcpyAsync(h->adj, sadj, sizeof(int) * E, cudaMemcpyDeviceToDevice, h->stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(h->offs, noffs, sizeof(unsigned) * ((size_t)nc + 1), cudaMemcpyDeviceToDevice, h->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+  cleanup();
+  if (e != cudaSuccess) return cuda_fail(e, "bm_permute_random");
+  h->sorted = 1;
+  h->has_init = false;  // an initial matching of the old labelling no longer applies
+  h->resumable = false;
+  return BM_OK;
+}
+
+bm_status bm_download_csc(bm_handle* h, int64_t* cxadj, int32_t* cadj) {
+  bm_status s = check_handle(h, true);
+  if (s != BM_OK) return s;
+  BM_CUDA(cudaSetDevice(h->device));
+  if (cxadj) {
+    std::vector<unsigned> o((size_t)h->nc + 1);
+    BM_CUDA(cudaMemcpy(o.data(), h->offs, sizeof(unsigned) * o.size(), cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < o.size(); ++i) cxadj[i] = o[i];
+  }
+  if (cadj && h->E > 0) BM_CUDA(cudaMemcpy(cadj, h->adj, sizeof(int) * h->E, cudaMemcpyDeviceToHost));
   return BM_OK;
 }
 

@@ -384,3 +384,23 @@ bm_status bm_host_cheap_matching(int32_t nc, int32_t nr, const int64_t* cxadj, c
 }
 
 }  // extern "C"
+
+extern "C" bm_status bm_permutation_pair(int32_t nc, int32_t nr, uint64_t seed, int32_t* cperm, int32_t* rperm) {
+  // random_permutation + permute_random's draw order (csr_graph.cpp:68-90): columns
+  // first, then rows, from one mt19937_64 seeded with `seed`; Fisher-Yates from
+  // the top with uniform_int_distribution<int>(0, i) (libstdc++, as the reference).
+  if (nc < 0 || nr < 0) return hfail(BM_ERR_INVALID_ARG, "negative size");
+  if ((nc > 0 && !cperm) || (nr > 0 && !rperm)) return hfail(BM_ERR_INVALID_ARG, "null permutation buffer");
+  std::mt19937_64 rng(seed);
+  auto fill = [&rng](int32_t n, int32_t* perm) {
+    for (int32_t i = 0; i < n; ++i) perm[i] = i;
+    for (int32_t i = n - 1; i > 0; --i) {
+      std::uniform_int_distribution<int> pick(0, i);
+      std::swap(perm[i], perm[pick(rng)]);
+    }
+  };
+  fill(nc, cperm);
+  fill(nr, rperm);
+  return BM_OK;
+}
+
