@@ -141,10 +141,13 @@ enum Stat : int {
   kNumStats
 };
 
+constexpr int kBarSub = 16;  // grid barrier fan-in groups
+
 struct alignas(128) Ctrl {
   unsigned bar_count;
   unsigned bar_gen;
   unsigned pad0[30];
+  unsigned bar_sub[kBarSub][32];  // one 128-byte line per group counter
   Slot lvl[3];
   Slot roots;
   unsigned n_ep;
@@ -206,6 +209,7 @@ struct Params {
   int apsb;
   int init_mode;
   int fresh;
+  int init_checked;  // the given initial matching was validated when it was loaded (bm_load_matching)
   int max_phases;
   int stop_after_bfs;
   int trace;        // write bfs_array level labels (parity probes)
@@ -267,10 +271,22 @@ __device__ __forceinline__ void flush_count(Smem& sm, int idx, unsigned v) {
 __device__ __noinline__ void grid_sync(Ctrl* ctl) {
   __syncthreads();
   if (threadIdx.x == 0) {
+    // Two-level arrival: CTAs count in kBarSub group counters (separate L2
+    // lines, so their atomics proceed in parallel); each group's last arriver
+    // counts at the top; the last of those resets and releases everyone.
     const unsigned gen = ld_acq(&ctl->bar_gen);
     __threadfence();
-    const unsigned arrived = atomicAdd(&ctl->bar_count, 1u);
-    if (arrived == gridDim.x - 1) {
+    const unsigned G = gridDim.x;
+    const unsigned grp = blockIdx.x % kBarSub;
+    const unsigned ngrp = G < (unsigned)kBarSub ? G : (unsigned)kBarSub;
+    const unsigned in_grp = G / kBarSub + (grp < G % kBarSub ? 1u : 0u);
+    bool last = false;
+    if (atomicAdd(&ctl->bar_sub[grp][0], 1u) == in_grp - 1) {
+      st_rlx(&ctl->bar_sub[grp][0], 0u);
+      __threadfence();  // the reset is visible before this group can be released
+      last = atomicAdd(&ctl->bar_count, 1u) == ngrp - 1;
+    }
+    if (last) {
       st_rlx(&ctl->bar_count, 0u);
       __threadfence();
       atomicAdd(&ctl->bar_gen, 1u);
@@ -1009,8 +1025,10 @@ __global__ void __launch_bounds__(kThreads, BM_MINB) driver_kernel(Params p) {
       unsigned beg = 0, deg = 0;
       if (c < (unsigned long long)p.nc) {
         const int r = ld_cg(p.cmatch + c);
-        if (r < -1 || r >= p.nr) bad++;
-        else if (r >= 0 && ld_cg(RM(p, r)) != (int)c) bad++;
+        if (!p.init_checked) {
+          if (r < -1 || r >= p.nr) bad++;
+          else if (r >= 0 && ld_cg(RM(p, r)) != (int)c) bad++;
+        }
         st_plain(p.bfs + c, r >= 0 ? kUnvisited : kStartLevel);
         if (r < 0) {
           beg = ld_ro(p.offs + c);
@@ -1023,11 +1041,12 @@ __global__ void __launch_bounds__(kThreads, BM_MINB) driver_kernel(Params p) {
       if (cta_reserve(sm, root ? 1u : 0u, root ? deg : 0u, 0u, &ctl->roots, &ctl->n_ep, slot, unused) && root)
         put_entry(p.F0, 0u, p.gidx0, slot, (int)c, (int)c, beg, deg);
     }
-    for (unsigned long long r = global_thread(); r < (unsigned long long)p.nr; r += global_threads()) {
-      const int v = ld_cg(RM(p, r));
-      if (v < -1 || v >= p.nc) bad++;
-      else if (v >= 0 && ld_cg(p.cmatch + v) != (int)r) bad++;
-    }
+    if (!p.init_checked)
+      for (unsigned long long r = global_thread(); r < (unsigned long long)p.nr; r += global_threads()) {
+        const int v = ld_cg(RM(p, r));
+        if (v < -1 || v >= p.nc) bad++;
+        else if (v >= 0 && ld_cg(p.cmatch + v) != (int)r) bad++;
+      }
     bad = warp_sum(bad);
     iso = warp_sum(iso);
     if (lane_id() == 0) {
@@ -1235,6 +1254,24 @@ __global__ void perm_scatter_kernel(const unsigned* offs, const int* adj, const 
   }
 }
 
+// Validity of a resident initial matching (plain arrays), checked once at load.
+__global__ void init_check_kernel(const int* rmatch, const int* cmatch, int nc, int nr, unsigned long long* bad) {
+  unsigned long long b = 0;
+  const long long tot = (long long)gridDim.x * blockDim.x;
+  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < nc; c += tot) {
+    const int r = cmatch[c];
+    if (r < -1 || r >= nr) b++;
+    else if (r >= 0 && rmatch[r] != (int)c) b++;
+  }
+  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < nr; r += tot) {
+    const int v = rmatch[r];
+    if (v < -1 || v >= nc) b++;
+    else if (v >= 0 && cmatch[v] != (int)r) b++;
+  }
+  b = warp_sum(b);
+  if (lane_id() == 0 && b) atomicAdd(bad, b);
+}
+
 }  // namespace bm
 
 // ===========================================================================
@@ -1324,6 +1361,7 @@ struct bm_handle {
   PhaseRec* recs = nullptr;
   int rec_cap = 4096;
   bool has_init = false;
+  bool init_valid = false;  // the loaded initial matching passed init_check_kernel
   bool resumable = false;
   bm_match_opts run_opts{};
   std::vector<long long> phase_launches;  // per outer iteration, current run
@@ -1529,10 +1567,11 @@ bm_status ctl_error_status(int err) {
 // budget is spent, or the observer aborts.
 bm_status drive(bm_handle* h, const bm_match_opts& o, bool fresh, int64_t* cardinality,
                 bm_counters* counters, int64_t* per_iter, int64_t cap, bm_phase_cb cb, void* user,
-                int32_t* done_out) {
+                int32_t* done_out, bool init_checked = false) {
   const int v = variant_of(o.bfs_kernel == BM_BFS_WR, o.improved);
   Params p = make_params(h, o);
   p.fresh = fresh ? 1 : 0;
+  p.init_checked = init_checked ? 1 : 0;
   if (fresh) {
     h->timeline.clear();
     h->phase_launches.clear();
@@ -1839,8 +1878,15 @@ bm_status bm_load_matching(bm_handle* h, const int32_t* rmatch, const int32_t* c
   BM_CUDA(cudaSetDevice(h->device));
   if (h->nr > 0) BM_CUDA(cudaMemcpyAsync(h->rmatch0, rmatch, sizeof(int) * h->nr, cudaMemcpyHostToDevice, h->stream));
   if (h->nc > 0) BM_CUDA(cudaMemcpyAsync(h->cmatch0, cmatch, sizeof(int) * h->nc, cudaMemcpyHostToDevice, h->stream));
+  BM_CUDA(cudaMemsetAsync(h->scratch, 0, sizeof(unsigned long long), h->stream));
+  const int blocks = std::max(1, std::min(h->sms * 8, (std::max(h->nc, h->nr) + 255) / 256));
+  init_check_kernel<<<blocks, 256, 0, h->stream>>>(h->rmatch0, h->cmatch0, h->nc, h->nr, h->scratch);
+  BM_CUDA(cudaGetLastError());
+  unsigned long long bad = 0;
+  BM_CUDA(cudaMemcpyAsync(&bad, h->scratch, sizeof(bad), cudaMemcpyDeviceToHost, h->stream));
   BM_CUDA(cudaStreamSynchronize(h->stream));
   h->has_init = true;
+  h->init_valid = bad == 0;
   return BM_OK;
 }
 
@@ -1853,6 +1899,9 @@ bm_status bm_run(bm_handle* h, const bm_match_opts* opts, int64_t* cardinality, 
   BM_CUDA(cudaSetDevice(h->device));
   if (opts->init == BM_INIT_GIVEN) {
     if (!h->has_init) return fail(BM_ERR_INVALID_ARG, "no initial matching loaded (bm_load_matching)");
+    if (!h->init_valid)
+      return fail(BM_ERR_INVALID_ARG,
+                  "initial matching is not a clean valid matching (pending -2, out of range or asymmetric)");
     s = rows_from_plain(h, h->rmatch0);
     if (s != BM_OK) return s;
     BM_CUDA(cudaMemcpyAsync(h->cmatch, h->cmatch0, sizeof(int) * std::max(h->nc, 1), cudaMemcpyDeviceToDevice, h->stream));
@@ -1863,7 +1912,8 @@ bm_status bm_run(bm_handle* h, const bm_match_opts* opts, int64_t* cardinality, 
   }
   s = prepare_fresh(h);
   if (s != BM_OK) return s;
-  return drive(h, *opts, true, cardinality, counters, per_iter, cap, cb, user, done);
+  return drive(h, *opts, true, cardinality, counters, per_iter, cap, cb, user, done,
+               opts->init == BM_INIT_GIVEN);
 }
 
 bm_status bm_resume(bm_handle* h, const bm_match_opts* opts, int64_t* cardinality, bm_counters* counters,
