@@ -1161,27 +1161,34 @@ __global__ void convert_offsets_kernel(const long long* in, unsigned* out, int n
   }
 }
 
-// One warp per column: row range and strict ascending order (sortedness is
-// recorded, not required — the verifier falls back to a linear scan).
-__global__ void check_adj_kernel(const unsigned* offs, const int* adj, int nc, int nr,
-                                 unsigned long long* bad_range, unsigned long long* unsorted) {
-  const long long warps = (long long)gridDim.x * blockDim.x / 32;
-  const int lane = threadIdx.x & 31;
-  for (long long c = (blockIdx.x * (long long)blockDim.x + threadIdx.x) / 32; c < nc; c += warps) {
-    const unsigned b = offs[c], e = offs[c + 1];
-    unsigned long long br = 0, us = 0;
-    for (unsigned j = b + lane; j < e; j += 32) {
-      const int r = adj[j];
-      if (r < 0 || r >= nr) br++;
-      if (j > b && adj[j - 1] >= r) us++;
-    }
-    br = warp_sum(br);
-    us = warp_sum(us);
-    if (lane == 0) {
-      if (br) atomicAdd(bad_range, br);
-      if (us) atomicAdd(unsorted, us);
-    }
+// Flat adjacency check over [j0, j1) (one pass, vector loads): rows out of
+// range, and descending neighbour pairs (j-1, j) anywhere — pairs that straddle
+// a column start are subtracted by col_start_pairs_kernel. Runs per uploaded
+// chunk, overlapped with the copy of the next chunk.
+__global__ void check_adj_flat_kernel(const int* adj, long long j0, long long j1, int nr,
+                                      unsigned long long* bad_range, unsigned long long* desc) {
+  unsigned long long br = 0, ds = 0;
+  const long long tot = (long long)gridDim.x * blockDim.x;
+  for (long long j = j0 + blockIdx.x * (long long)blockDim.x + threadIdx.x; j < j1; j += tot) {
+    const int r = adj[j];
+    if (r < 0 || r >= nr) br++;
+    if (j > 0 && adj[j - 1] >= r) ds++;
   }
+  br = warp_sum(br);
+  ds = warp_sum(ds);
+  if (lane_id() == 0) {
+    if (br) atomicAdd(bad_range, br);
+    if (ds) atomicAdd(desc, ds);
+  }
+}
+__global__ void col_start_pairs_kernel(const unsigned* offs, const int* adj, int nc, unsigned long long* desc_fix) {
+  unsigned long long f = 0;
+  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < nc; c += (long long)gridDim.x * blockDim.x) {
+    const unsigned b = offs[c];
+    if (b > 0 && offs[c + 1] > b && adj[b - 1] >= adj[b]) f++;
+  }
+  f = warp_sum(f);
+  if (lane_id() == 0 && f) atomicAdd(desc_fix, f);
 }
 
 // Validity half of the Berge certificate (validate, matching.cpp:70-104).
@@ -1366,7 +1373,8 @@ struct bm_handle {
   bm_match_opts run_opts{};
   std::vector<long long> phase_launches;  // per outer iteration, current run
   unsigned long long *scratch = nullptr;  // small device counters
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev_up = nullptr;
+  cudaStream_t aux = nullptr;  // upload-time checks overlapped with the copies
   double last_ms = 0.0;
   int last_launches = 0;
   CapMap caps;
@@ -1730,6 +1738,8 @@ bm_status bm_create(int32_t device, bm_handle** out) {
   e = cudaStreamCreateWithFlags(&h->own, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaEventCreate(&h->ev0);
   if (e == cudaSuccess) e = cudaEventCreate(&h->ev1);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_up, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->aux, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void**>(&h->ctl), sizeof(Ctrl));
   if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void**>(&h->recs), sizeof(PhaseRec) * h->rec_cap);
   if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void**>(&h->scratch), sizeof(unsigned long long) * 4);
@@ -1747,6 +1757,7 @@ bm_status bm_destroy(bm_handle* h) {
   if (!h) return BM_OK;
   cudaSetDevice(h->device);
   if (h->stream) cudaStreamSynchronize(h->stream);
+  if (h->aux) cudaStreamSynchronize(h->aux);
   dfree(h->offs);
   dfree(h->adj);
   dfree(h->rm);
@@ -1770,6 +1781,8 @@ bm_status bm_destroy(bm_handle* h) {
   dfree(h->scratch);
   if (h->ev0) cudaEventDestroy(h->ev0);
   if (h->ev1) cudaEventDestroy(h->ev1);
+  if (h->ev_up) cudaEventDestroy(h->ev_up);
+  if (h->aux) cudaStreamDestroy(h->aux);
   if (h->own) cudaStreamDestroy(h->own);
   delete h;
   return BM_OK;
@@ -1831,24 +1844,33 @@ bm_status bm_upload_csc(bm_handle* h, int32_t nc, int32_t nr, const int64_t* cxa
   // offsets: int64 staged in F[1] (16 B per column >= 8 B per offset), narrowed to u32
   long long* staged = reinterpret_cast<long long*>(h->F[1]);
   BM_CUDA(cudaMemcpyAsync(staged, cxadj, sizeof(long long) * ((size_t)nc + 1), cudaMemcpyHostToDevice, h->stream));
-  if (E > 0)
-    BM_CUDA(cudaMemcpyAsync(h->adj, cadj, sizeof(int) * (size_t)E, cudaMemcpyHostToDevice, h->stream));
   BM_CUDA(cudaMemsetAsync(h->scratch, 0, sizeof(unsigned long long) * 4, h->stream));
   const int blocks = std::max(1, std::min(h->sms * 8, (nc + 256) / 256));
   convert_offsets_kernel<<<blocks, 256, 0, h->stream>>>(staged, h->offs, nc, E, h->scratch);
   BM_CUDA(cudaGetLastError());
-  unsigned long long bad[3] = {0, 0, 0};
+  BM_CUDA(cudaEventRecord(h->ev_up, h->stream));
+  BM_CUDA(cudaStreamWaitEvent(h->aux, h->ev_up, 0));
+  // adjacency in chunks: the check of chunk k runs on the aux stream while
+  // chunk k+1 is still being copied
+  const long long chunk = 32ll << 20;  // elements (128 MB)
+  for (long long j0 = 0; j0 < E; j0 += chunk) {
+    const long long j1 = std::min(E, j0 + chunk);
+    BM_CUDA(cudaMemcpyAsync(h->adj + j0, cadj + j0, sizeof(int) * (size_t)(j1 - j0), cudaMemcpyHostToDevice, h->stream));
+    BM_CUDA(cudaEventRecord(h->ev_up, h->stream));
+    BM_CUDA(cudaStreamWaitEvent(h->aux, h->ev_up, 0));
+    const int cb = (int)std::max<long long>(1, std::min<long long>((long long)h->sms * 8, (j1 - j0 + 255) / 256));
+    check_adj_flat_kernel<<<cb, 256, 0, h->aux>>>(h->adj, j0, j1, nr, h->scratch + 1, h->scratch + 2);
+  }
+  if (nc > 0) col_start_pairs_kernel<<<blocks, 256, 0, h->aux>>>(h->offs, h->adj, nc, h->scratch + 3);
+  BM_CUDA(cudaGetLastError());
+  BM_CUDA(cudaEventRecord(h->ev_up, h->aux));
+  BM_CUDA(cudaStreamWaitEvent(h->stream, h->ev_up, 0));
+  unsigned long long bad[4] = {0, 0, 0, 0};
   BM_CUDA(cudaMemcpyAsync(bad, h->scratch, sizeof(bad), cudaMemcpyDeviceToHost, h->stream));
   BM_CUDA(cudaStreamSynchronize(h->stream));
   if (bad[0]) return fail(BM_ERR_INVALID_ARG, "cxadj is not a valid offset array (cxadj[0]=0, non-decreasing, cxadj[nc]=E)");
-  if (nc > 0) {
-    const int wb = std::max(1, std::min(h->sms * 16, (int)(((long long)nc * 32 + 255) / 256)));
-    check_adj_kernel<<<wb, 256, 0, h->stream>>>(h->offs, h->adj, nc, nr, h->scratch + 1, h->scratch + 2);
-    BM_CUDA(cudaGetLastError());
-    BM_CUDA(cudaMemcpyAsync(bad, h->scratch, sizeof(bad), cudaMemcpyDeviceToHost, h->stream));
-    BM_CUDA(cudaStreamSynchronize(h->stream));
-    if (bad[1]) return fail(BM_ERR_INVALID_ARG, "row index out of range in cadj");
-  }
+  if (bad[1]) return fail(BM_ERR_INVALID_ARG, "row index out of range in cadj");
+  bad[2] -= bad[3];  // descending pairs inside columns
   h->sorted = bad[2] == 0;
   h->nr = nr;
   {

@@ -249,3 +249,29 @@ def test_verify_matches_oracle(engine, oracle):
     bad.rmatch[r] = -2
     v, _, _ = engine.verify(g, bad)
     assert v == oracle.validate(g, bad.rmatch, bad.cmatch) > 0
+
+
+def test_unsorted_columns_and_upload_checks(engine, oracle):
+    """check_csr semantics at upload (csr_graph.cpp:45-64): rows out of range are
+    rejected; unsorted columns are accepted (the kernels do not rely on order) and
+    the verifier falls back to a linear scan."""
+    g = bm.generate_random_bipartite(20000, 15000, 5.0, 77)
+    rng = np.random.default_rng(5)
+    adj = g.cadj.copy()
+    for c in range(0, g.nc, 3):  # reverse every third column
+        a, b = g.cxadj[c], g.cxadj[c + 1]
+        adj[a:b] = adj[a:b][::-1]
+    ug = bm.BipartiteCsr(g.nc, g.nr, g.cxadj.copy(), adj)
+    init = bm.cheap_matching(ug)
+    res = engine.match(ug, init)
+    want = oracle.maximum(g)
+    assert bm.cardinality(res.matching) == want
+    viol, ismax, card = engine.verify(ug, res.matching)
+    assert viol == 0 and ismax and card == want
+    bad = g.cadj.copy()
+    bad[int(rng.integers(0, len(bad)))] = g.nr  # one row id out of range
+    with pytest.raises(ValueError):
+        engine.upload(bm.BipartiteCsr(g.nc, g.nr, g.cxadj.copy(), bad), force=True)
+    engine.upload(g, force=True)
+    res = engine.match(g, bm.cheap_matching(g))
+    assert bm.cardinality(res.matching) == want
