@@ -178,7 +178,8 @@ bm_status   bm_resume(bm_handle* h, const bm_match_opts* opts, int64_t* cardinal
                       int64_t cap, bm_phase_cb cb, void* user, int32_t* done);
 bm_status   bm_download_matching(bm_handle* h, int32_t* rmatch, int32_t* cmatch);
 /* Device time (ms, CUDA events on the handle's stream) of the driver kernel
- * launches of the last bm_run/bm_resume/bm_match, and how many launches. */
+ * launches of the last bm_run/bm_resume/bm_match, and how many kernels that
+ * run launched (driver launches plus the initial-state copy kernel). */
 bm_status   bm_last_kernel_time(bm_handle* h, double* ms, int32_t* launches);
 
 /* Stage timeline of the last bm_run/bm_resume/bm_match: `n` records of two

@@ -150,6 +150,8 @@ def _load():
             "There is no CPU fallback.")
     lib = C.CDLL(LIB_PATH)
     for name, (res, args) in _PROTOS.items():
+        if os.environ.get("BM_LIB") and not hasattr(lib, name):
+            continue  # an older tuning build (BM_LIB) may lack newer entry points
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args

@@ -1485,6 +1485,7 @@ struct bm_handle {
   int *rm = nullptr, *cmatch = nullptr, *pred = nullptr, *bfs = nullptr;  // rm: row state (see RM / PR)
   int* pred_plain = nullptr;  // separate predecessors for the plain layout (pred aliases rm + 1 otherwise)
   int rs = 1;                 // row stride of rm / pred
+  int pending_launches = 0;   // helper kernels launched for the next run (counted in last_launches)
   int* rtmp = nullptr;  // plain nr-int staging for host <-> device row arrays
   int *rmatch0 = nullptr, *cmatch0 = nullptr, *EP = nullptr;
   unsigned* dead = nullptr;
@@ -1526,6 +1527,7 @@ int row_blocks(bm_handle* h) { return std::max(1, std::min(h->sms * 8, (h->nr + 
 bm_status rows_from_plain(bm_handle* h, const int* plain) {
   if (h->nr <= 0) return BM_OK;
   rows_pack_kernel<<<row_blocks(h), 256, 0, h->stream>>>(plain, h->rm, h->nr, h->rs);
+  h->pending_launches++;
   BM_CUDA(cudaGetLastError());
   return BM_OK;
 }
@@ -1539,6 +1541,7 @@ bm_status rows_to_plain(bm_handle* h, int* out, int off) {
 bm_status rows_fill(bm_handle* h, int off, int v) {
   if (h->nr <= 0) return BM_OK;
   rows_fill_kernel<<<row_blocks(h), 256, 0, h->stream>>>(off ? h->pred : h->rm, h->nr, h->rs, v);
+  h->pending_launches++;
   BM_CUDA(cudaGetLastError());
   return BM_OK;
 }
@@ -1713,8 +1716,9 @@ bm_status drive(bm_handle* h, const bm_match_opts& o, bool fresh, int64_t* cardi
     h->timeline.clear();
     h->phase_launches.clear();
     h->last_ms = 0.0;
-    h->last_launches = 0;
+    h->last_launches = h->pending_launches;  // the initial-state kernels of this run
   }
+  h->pending_launches = 0;
   long long budget = o.max_phases > 0 ? o.max_phases : -1;
   std::vector<PhaseRec> recs;
   std::vector<int> snap_r, snap_c;
