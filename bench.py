@@ -361,8 +361,8 @@ def run_b200(args):
     eng.load_matching(init)
     flush = torch.empty(args.flush_mb << 20, dtype=torch.uint8, device=dev)
 
-    def one_step():
-        return eng.run(shortest=shortest, kernel=kernel, improved=improved)
+    def one_step(bottom_up=args.bottom_up):
+        return eng.run(shortest=shortest, kernel=kernel, improved=improved, bottom_up=bottom_up)
 
     # correctness of the measured configuration (GPU Berge certificate)
     card, ct, done = one_step()
@@ -406,6 +406,28 @@ def run_b200(args):
         t = torch.tensor([t_ms, k_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         t_ms, k_ms = float(t[0]), float(t[1])
+
+    # ---- the other traversal direction, measured the same way (reported, not the headline) ----
+    alt = None
+    if world == 1 and not args.no_alt:
+        t_idx = time.perf_counter()
+        one_step(not args.bottom_up)  # builds the row index on first use
+        torch.cuda.synchronize(dev)
+        t_idx = time.perf_counter() - t_idx
+        a_ms, a_ph = [], []
+        for _ in range(max(3, args.steps // 2)):
+            flush.fill_(1)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            acard, act, adone = one_step(not args.bottom_up)
+            e1.record(stream)
+            e1.synchronize()
+            a_ms.append(e0.elapsed_time(e1))
+            a_ph.append(act.outer_iterations)
+            parity_ok = parity_ok and adone and (known is None or acard == known)
+        alt = {"bottom_up": not args.bottom_up, "ms_per_step": statistics.mean(a_ms),
+               "phases": a_ph, "first_call_s": t_idx}
 
     # ---- end to end through the public API, pinned host buffers ----
     e2e = None
@@ -485,6 +507,8 @@ def run_b200(args):
                          "algorithmic_bytes_per_launch": b_units, "survey_formula_bytes": b_survey},
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "bottom_up": bool(args.bottom_up),
+            "alternative": alt,
             "gpu_launches": launches,
             "clocks": sampler.summary(),
             "time_to_max_matching_ms": t_ms,
@@ -519,6 +543,9 @@ def main():
     ap.add_argument("--flush-mb", type=int, default=512)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-alt", action="store_true", help="skip the other-direction measurement")
+    ap.add_argument("--bottom-up", action="store_true",
+                    help="pull the dense BFS levels (direction-optimised; builds a row index once per graph)")
     ap.add_argument("--mode", choices=["auto", "single", "partition", "replicas"], default="auto",
                     help="auto: single GPU at N=1, column partition at N>1")
     ap.add_argument("--exchange", choices=["nccl", "gloo"], default="nccl",

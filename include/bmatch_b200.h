@@ -72,7 +72,9 @@ typedef struct bm_match_opts {
                                 outer iterations and return with *done = 0 (resumable) */
   int32_t claim_policy;      /* bm_claim_policy (WR only): which trees may claim a column */
   int32_t endpoint_policy;   /* bm_endpoint_policy (WR only): how many free rows a tree may hold */
-  int32_t reserved;          /* must be 0 */
+  int32_t bottom_up;         /* 1: levels whose frontier holds >= 45% of the edges are pulled
+                                (direction-optimised); needs a row index of
+                                the graph, built on the first such run (E ints). 0: push only */
 } bm_match_opts;
 
 /* Column claims under GPUBFS-WR. REFERENCE: a tree whose root already found a

@@ -44,7 +44,7 @@ class bm_match_opts(C.Structure):
         ("max_phases", C.c_int32),
         ("claim_policy", C.c_int32),
         ("endpoint_policy", C.c_int32),
-        ("reserved", C.c_int32),
+        ("bottom_up", C.c_int32),
     ]
 
 

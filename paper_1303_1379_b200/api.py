@@ -144,10 +144,11 @@ class AlgorithmResult:
 
 
 def _opts(shortest: bool, kernel: BfsKernel, improved: bool, init_mode: str, max_phases: int = 0,
-          claim_mode: int = 0, endpoint_policy: int = 0):
+          claim_mode: int = 0, endpoint_policy: int = 0, bottom_up: bool = False):
     o = _lib.bm_match_opts()
     o.claim_policy = claim_mode
     o.endpoint_policy = endpoint_policy
+    o.bottom_up = 1 if bottom_up else 0
     o.driver = _lib.BM_DRIVER_APSB if shortest else _lib.BM_DRIVER_APFB
     o.bfs_kernel = int(kernel)
     o.improved = 1 if improved else 0
@@ -188,6 +189,7 @@ class Engine:
         self._h = h
         self.device = device
         self._graph = None
+        self.bottom_up = False  # bm_match_opts.bottom_up default for match()/run()
 
     # -- lifecycle
     def close(self):
@@ -235,7 +237,7 @@ class Engine:
 
     def _match(self, g, m, shortest, kernel, improved, init_mode, observer, want_launches=True):
         self.upload(g)
-        o = _opts(shortest, kernel, improved, init_mode)
+        o = _opts(shortest, kernel, improved, init_mode, bottom_up=self.bottom_up)
         if len(m.rmatch) != g.nr or len(m.cmatch) != g.nc:
             raise ValueError("matching arrays do not fit the graph")
         ct = _lib.bm_counters()
@@ -277,10 +279,11 @@ class Engine:
         check(lib.bm_load_matching(self._h, i32p(m.rmatch), i32p(m.cmatch)))
 
     def run(self, *, shortest=False, kernel=BfsKernel.GpubfsWr, improved=False, init_mode="given",
-            max_phases=0, observer=None, resume=False, claim_mode=0, endpoint_policy=0):
+            max_phases=0, observer=None, resume=False, claim_mode=0, endpoint_policy=0, bottom_up=None):
         """Device-resident run (bm_run / bm_resume). Returns (cardinality, counters, done).
         claim_mode / endpoint_policy: bm_claim_policy / bm_endpoint_policy (WR tuning knobs)."""
-        o = _opts(shortest, kernel, improved, init_mode, max_phases, claim_mode, endpoint_policy)
+        o = _opts(shortest, kernel, improved, init_mode, max_phases, claim_mode, endpoint_policy,
+                  self.bottom_up if bottom_up is None else bottom_up)
         ct = _lib.bm_counters()
         nc = self._nc()
         cap = nc + 2

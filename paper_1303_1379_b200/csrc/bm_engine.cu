@@ -219,6 +219,13 @@ struct Params {
   int claim_mode;   // WR claim check at discovery: 0 none (reference), 1 coherent root-mark check
   int ep_one;       // WR endpoint policy: 1 = one free row per tree (root-mark CAS), 0 = every row (reference)
   unsigned solo_edges;  // levels with at most this many frontier edges run on block 0 alone (0 = never)
+  // bottom-up levels (see bu_sweep); roffs == nullptr disables them
+  const unsigned* roffs;   // nr + 1, transposed adjacency (rows -> columns)
+  const int* radj;
+  unsigned* fbit[2];       // frontier bitmaps (nc bits each), alternating by level
+  int* croot;              // root of each frontier column (bottom-up levels)
+  int nfbit_words;
+  unsigned long long bu_min_edges;  // a level with at least this many frontier edges goes bottom-up
   long long phase_bound;
   unsigned long long* tl;  // stage timeline: (tag, %globaltimer ns) pairs written by the leader
   unsigned tl_cap;
@@ -257,6 +264,8 @@ struct Smem {
   unsigned blk_ep;
   unsigned nw;                          // winners staged in wbuf for the current window
   int2 wbuf[kWBuf];                     // (column, root) claimed in the current window
+  int bcand[2 * kThreads];              // bottom-up: candidate rows of a sweep step ...
+  int bcandv[2 * kThreads];             // ... and their rmatch values
 #if BM_ASYNC
   int srow[kWBuf];                      // live edge -> adjacency row (cp.async)
   int scm[kWBuf];                       // live edge -> rmatch of that row (cp.async)
@@ -425,6 +434,201 @@ __device__ __forceinline__ bool root_dead(const Params& p, int root) {
 }
 __device__ __forceinline__ void mark_dead(const Params& p, int root) {
   atomicOr(p.dead + (root >> 5), 1u << (root & 31));
+}
+
+// Pushes the winners staged in sm.wbuf as next-level frontier entries: one
+// CTA reservation (slots + edge prefix) for all of them. CTA-uniform call.
+__device__ __forceinline__ void flush_winners(const Params& p, Smem& sm, int4* F, unsigned out_base, unsigned* gout,
+                                              Slot* out, unsigned long long pol) {
+  const unsigned tid = threadIdx.x;
+  const unsigned nw = sm.nw;
+  if (!nw) return;
+  unsigned long long slot;
+  unsigned unused;
+  if (nw <= (unsigned)kThreads) {  // one winner per thread: a single pass
+    const bool has = tid < nw;
+    int2 cr = make_int2(0, 0);
+    unsigned b0 = 0, d0 = 0;
+    if (has) {
+      cr = sm.wbuf[tid];
+      b0 = ld_offs(p.offs + cr.x, pol);
+      d0 = ld_offs(p.offs + cr.x + 1, pol) - b0;
+    }
+    cta_reserve(sm, has ? 1u : 0u, d0, 0u, out, &p.ctl->n_ep, slot, unused);
+    if (has) put_entry(F, out_base, gout, slot, cr.x, cr.y, b0, d0, pol);
+  } else {
+    unsigned cnt = 0, deg = 0;
+    for (unsigned j = tid; j < nw; j += kThreads) {
+      const int c = sm.wbuf[j].x;
+      deg += ld_offs(p.offs + c + 1, pol) - ld_offs(p.offs + c, pol);
+      cnt++;
+    }
+    cta_reserve(sm, cnt, deg, 0u, out, &p.ctl->n_ep, slot, unused);
+    for (unsigned j = tid; j < nw; j += kThreads) {
+      const int2 cr = sm.wbuf[j];
+      const unsigned b0 = ld_offs(p.offs + cr.x, pol);
+      const unsigned d0 = ld_offs(p.offs + cr.x + 1, pol) - b0;
+      put_entry(F, out_base, gout, slot, cr.x, cr.y, b0, d0, pol);
+      slot += (1ull << 33) + d0;
+    }
+  }
+  __syncthreads();
+  if (tid == 0) sm.nw = 0;  // callers barrier before staging again
+}
+
+// Stages one winner per thread (or none) in sm.wbuf: one shared atomic per warp.
+__device__ __forceinline__ void stage_winner(Smem& sm, bool win, int col, int root) {
+  const unsigned mine = win ? 1u : 0u;
+  const unsigned incl = warp_incl_scan(mine);
+  const unsigned tot = __shfl_sync(kFull, incl, 31);
+  unsigned wb = 0;
+  if (lane_id() == 31 && tot) wb = atomicAdd(&sm.nw, tot);
+  wb = __shfl_sync(kFull, wb, 31) + incl - mine;
+  if (win) sm.wbuf[wb] = make_int2(col, root);
+}
+
+// ---------------------------------------------------------------------------
+// Direction-optimised (bottom-up) level for dense frontiers. The same level of
+// the same BFS as expand_level (gpubfs / gpubfs_wr, gpu_match.cpp:42-70,
+// 99-133), pulled instead of pushed: every unvisited matched row scans its own
+// columns (the transposed adjacency) for one in the frontier and is claimed by
+// the first it finds; every free row likewise becomes an endpoint of the first
+// live tree it touches. Any frontier neighbour is a valid discoverer (the
+// reference's races pick one arbitrarily too), so levels, roots and the
+// augmenting paths keep their meaning; a row stops at its first hit, which is
+// what saves the work when most columns are already in the frontier.
+//
+// bu_prep: the frontier of level lv as a bitmap (+ the root of each member).
+// The bitmap is clean: a bottom-up level clears its own right after the grid
+// barrier that ends it (bu_clear; the next level uses the other bitmap).
+__device__ __forceinline__ void bu_clear(const Params& p, int lv) {
+  unsigned* fb = p.fbit[lv & 1];
+  for (unsigned long long k = global_thread(); k < (unsigned long long)p.nfbit_words; k += global_threads())
+    st_plain(reinterpret_cast<int*>(fb) + k, 0);
+}
+template <bool WR>
+__device__ __forceinline__ void bu_prep(const Params& p, const int4* F, unsigned ls, unsigned n, int lv) {
+  unsigned* fb = p.fbit[lv & 1];
+  for (unsigned long long k = global_thread(); k < n; k += global_threads()) {
+    const int4 ent = ld_cg(F + ls + k);
+    if (WR && root_dead(p, ent.y)) continue;
+    atomicOr(fb + (ent.x >> 5), 1u << (ent.x & 31));
+    st_plain(p.croot + ent.x, WR ? ent.y : ent.x);
+  }
+}
+
+template <bool WR, bool IMP>
+__device__ __forceinline__ void bu_sweep(const Params& p, Smem& sm, int4* F, unsigned out_base, unsigned* gout,
+                                         Slot* out, int lv, int pf) {
+  // Per CTA iteration: (1) kBuRows rows per thread are screened with
+  // independent loads and the candidates (unvisited matched rows and free rows)
+  // are compacted into shared memory; (2) each candidate scans its columns
+  // until the first frontier member; (3) winners are flushed as frontier
+  // entries. Candidates reuse the window arrays of Smem (col/root/beg/pre).
+  constexpr int kBuRows = 8;
+  const unsigned* fb = p.fbit[lv & 1];
+  const unsigned long long pol = policy_evict_first();
+  unsigned* const path_flag = &p.ctl->path_found[pf];
+  unsigned c_trav = 0, c_nvis = 0, c_rows = 0;
+  unsigned& ncand = sm.wtot[0];
+  if (threadIdx.x == 0) {
+    sm.nw = 0;
+    ncand = 0;
+  }
+  __syncthreads();
+  const unsigned long long chunk = (unsigned long long)kThreads * kBuRows;
+  for (unsigned long long b = (unsigned long long)blockIdx.x * chunk; b < (unsigned long long)p.nr;
+       b += (unsigned long long)gridDim.x * chunk) {
+    // (1) screen kBuRows rows per thread (independent loads)
+    int v[kBuRows];
+#pragma unroll
+    for (int k = 0; k < kBuRows; ++k) {
+      const unsigned long long r = b + (unsigned long long)k * kThreads + threadIdx.x;
+      v[k] = r < (unsigned long long)p.nr ? ld_cg(RM(p, r)) : -3;
+    }
+#pragma unroll
+    for (int k = 0; k < kBuRows; ++k) {
+      // stage this step's candidates: at most kThreads per step, the stage holds 2 * kThreads
+      const unsigned long long r = b + (unsigned long long)k * kThreads + threadIdx.x;
+      const bool is_cand = (v[k] >= 0 && !(v[k] & kVisBit)) || v[k] == -1;
+      const unsigned m = __ballot_sync(kFull, is_cand);
+      unsigned base = 0;
+      if (lane_id() == 0 && m) base = atomicAdd(&ncand, (unsigned)__popc(m));
+      base = __shfl_sync(kFull, base, 0);
+      if (is_cand) {
+        const unsigned slot = base + __popc(m & ((1u << lane_id()) - 1));
+        sm.bcand[slot] = (int)r;
+        sm.bcandv[slot] = v[k];
+      }
+      __syncthreads();
+      const unsigned nc_ = ncand;
+      __syncthreads();  // everyone has read ncand before the next step adds to it
+      // (2) resolve once kThreads candidates are staged (and at the end of the chunk)
+      if (nc_ < (unsigned)kThreads && k != kBuRows - 1) continue;
+      for (unsigned t0 = 0; t0 < nc_; t0 += kThreads) {
+        bool win = false, ep = false;
+        int cw = 0, rootw = 0, rr = 0;
+        if (t0 + threadIdx.x < nc_) {
+          rr = sm.bcand[t0 + threadIdx.x];
+          const int vv = sm.bcandv[t0 + threadIdx.x];
+          const unsigned j0 = ld_ro(p.roffs + rr), j1 = ld_ro(p.roffs + rr + 1);
+          c_rows++;
+          for (unsigned j = j0; j < j1; ++j) {
+            const int c = ld_stream(p.radj + j, pol);
+            c_trav++;
+            if (!((ld_ca(reinterpret_cast<const int*>(fb) + (c >> 5)) >> (c & 31)) & 1)) continue;
+            const int root = ld_cg(p.croot + c);
+            if (vv >= 0) {  // matched row: its column joins the frontier below c's tree
+              st_plain(RM(p, rr), vv | kVisBit);
+              st_plain(PR(p, rr), c);
+              win = true;
+              cw = vv;
+              rootw = root;
+              break;
+            }
+            // free row: an endpoint of c's tree
+            const bool one = WR && p.ep_one;
+            if (one && root_dead(p, root)) continue;
+            bool mine = true;
+            if (one) mine = atomicCAS(p.bfs + root, kStartLevel, IMP ? -rr : kFoundMark) == kStartLevel;
+            else if (WR) st_rlx(p.bfs + root, IMP ? -rr : kFoundMark);
+            if (!mine) continue;  // that tree already holds an endpoint: try another neighbour
+            if (WR) mark_dead(p, root);
+            st_rlx(RM(p, rr), -2);
+            st_plain(PR(p, rr), c);
+            ep = true;
+            if (ld_rlx(path_flag) == 0u) st_rlx(path_flag, 1u);
+            break;
+          }
+        }
+        c_nvis += win ? 1u : 0u;
+        stage_winner(sm, win, cw, rootw);
+        {  // endpoints: rare, warp-aggregated global append
+          const unsigned mine = ep ? 1u : 0u;
+          const unsigned incl = warp_incl_scan(mine);
+          const unsigned tot = __shfl_sync(kFull, incl, 31);
+          if (tot) {
+            unsigned eb = 0;
+            if (lane_id() == 31) eb = atomicAdd(&p.ctl->n_ep, tot);
+            eb = __shfl_sync(kFull, eb, 31) + incl - mine;
+            if (ep) st_plain(p.EP + eb, rr);
+          }
+        }
+        __syncthreads();
+        if (sm.nw > kWBuf - kThreads) {
+          flush_winners(p, sm, F, out_base, gout, out, pol);
+          __syncthreads();  // the reset of sm.nw lands before the next stage_winner
+        }
+      }
+      if (threadIdx.x == 0) ncand = 0;
+      __syncthreads();
+    }
+  }
+  __syncthreads();
+  flush_winners(p, sm, F, out_base, gout, out, pol);
+  flush_count(sm, kStTrav, c_trav);
+  flush_count(sm, kStNvis, c_nvis);
+  flush_count(sm, kStCexp, c_rows);
 }
 
 // ---------------------------------------------------------------------------
@@ -755,40 +959,7 @@ __device__ __forceinline__ void expand_level(const Params& p, Smem& sm, int4* F,
         t_a = t;
       }
       // Flush the window's winners: one CTA reservation for all of them.
-      const unsigned nw = sm.nw;
-      if (nw) {
-        unsigned long long slot;
-        unsigned unused;
-        if (nw <= (unsigned)kThreads) {  // one winner per thread: a single pass
-          const bool has = tid < nw;
-          int2 cr = make_int2(0, 0);
-          unsigned b0 = 0, d0 = 0;
-          if (has) {
-            cr = sm.wbuf[tid];
-            b0 = ld_offs(p.offs + cr.x, pol);
-            d0 = ld_offs(p.offs + cr.x + 1, pol) - b0;
-          }
-          cta_reserve(sm, has ? 1u : 0u, d0, 0u, out, &p.ctl->n_ep, slot, unused);
-          if (has) put_entry(F, out_base, gout, slot, cr.x, cr.y, b0, d0, pol);
-        } else {
-          unsigned cnt = 0, deg = 0;
-          for (unsigned j = tid; j < nw; j += kThreads) {
-            const int c = sm.wbuf[j].x;
-            deg += ld_offs(p.offs + c + 1, pol) - ld_offs(p.offs + c, pol);
-            cnt++;
-          }
-          cta_reserve(sm, cnt, deg, 0u, out, &p.ctl->n_ep, slot, unused);
-          for (unsigned j = tid; j < nw; j += kThreads) {
-            const int2 cr = sm.wbuf[j];
-            const unsigned b0 = ld_offs(p.offs + cr.x, pol);
-            const unsigned d0 = ld_offs(p.offs + cr.x + 1, pol) - b0;
-            put_entry(F, out_base, gout, slot, cr.x, cr.y, b0, d0, pol);
-            slot += (1ull << 33) + d0;
-          }
-        }
-        __syncthreads();
-        if (tid == 0) sm.nw = 0;
-      }
+      flush_winners(p, sm, F, out_base, gout, out, pol);
       e = wend;
       i += kThreads;
       __syncthreads();
@@ -937,14 +1108,23 @@ __device__ PhaseOut run_phase(const Params& p, Smem& sm, int cur, int parity, bo
       z->tile = 0;
     }
     if (solo) __syncthreads();
-    expand_level<WR, IMP>(p, sm, F, ls, n, T, (lv & 1) ? p.gidx1 : p.gidx0, (lv & 1) ? p.gidx0 : p.gidx1,
-                          in, outs, kStartLevel + lv, parity);
+    const bool bu = !solo && p.roffs && !p.trace && (unsigned long long)T >= p.bu_min_edges;
+    if (bu) {
+      bu_prep<WR>(p, F, ls, n, lv);
+      grid_sync(ctl);
+      bu_sweep<WR, IMP>(p, sm, F, ls + n, (lv & 1) ? p.gidx0 : p.gidx1, outs, lv, parity);
+    } else {
+      expand_level<WR, IMP>(p, sm, F, ls, n, T, (lv & 1) ? p.gidx1 : p.gidx0, (lv & 1) ? p.gidx0 : p.gidx1,
+                            in, outs, kStartLevel + lv, parity);
+    }
+
     const long long tb = clk();
     if (solo) {
       __threadfence_block();
       __syncthreads();
     } else {
       grid_sync(ctl);
+      if (bu) bu_clear(p, lv);  // read by nobody from here on; the next level uses the other bitmap
     }
     if (threadIdx.x == 0) sm.cnt[kStCycBarrier] += clk() - tb;
     tl_mark(p, kTlLevel, n);
@@ -1031,6 +1211,7 @@ __device__ PhaseOut run_phase(const Params& p, Smem& sm, int cur, int parity, bo
   if (WR)
     for (unsigned long long k = global_thread(); k < (unsigned long long)p.ndead_words; k += global_threads())
       st_plain(reinterpret_cast<int*>(p.dead) + k, 0);
+
   if (is_leader()) {
     for (int s = 0; s < 3; ++s) {
       ctl->lvl[s].packed = 0;
@@ -1408,6 +1589,20 @@ __global__ void init_check_kernel(const int* rmatch, const int* cmatch, int nc, 
   if (lane_id() == 0 && b) atomicAdd(bad, b);
 }
 
+// Transposed adjacency (rows -> columns) for bottom-up levels: count,
+// exclusive scan (CUB), scatter. Row lists come out unsorted (not needed).
+__global__ void row_count_kernel(const int* adj, long long E, unsigned* rdeg) {
+  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < E; j += (long long)gridDim.x * blockDim.x)
+    atomicAdd(rdeg + adj[j], 1u);
+}
+__global__ void transpose_scatter_kernel(const unsigned* offs, const int* adj, int nc, unsigned* cursor, int* radj) {
+  const long long warps = (long long)gridDim.x * blockDim.x / 32;
+  for (long long c = (blockIdx.x * (long long)blockDim.x + threadIdx.x) / 32; c < nc; c += warps) {
+    const unsigned b = offs[c], e = offs[c + 1];
+    for (unsigned j = b + lane_id(); j < e; j += 32) radj[atomicAdd(cursor + adj[j], 1u)] = (int)c;
+  }
+}
+
 }  // namespace bm
 
 // ===========================================================================
@@ -1486,6 +1681,16 @@ struct bm_handle {
   int* pred_plain = nullptr;  // separate predecessors for the plain layout (pred aliases rm + 1 otherwise)
   int rs = 1;                 // row stride of rm / pred
   int pending_launches = 0;   // helper kernels launched for the next run (counted in last_launches)
+  // bottom-up levels: transposed adjacency, frontier bitmaps, frontier roots
+  bool bu_enabled = false;    // the row index exists for the resident graph
+  bool bu_built = false;
+  double bu_frac = 0.45;      // a level goes bottom-up when its frontier edges >= bu_frac * E
+  unsigned* roffs = nullptr;
+  int* radj = nullptr;
+  unsigned* rcursor = nullptr;
+  unsigned* fbit = nullptr;   // 2 * nfbit_words
+  int nfbit_words = 0;
+  int* croot = nullptr;
   int* rtmp = nullptr;  // plain nr-int staging for host <-> device row arrays
   int *rmatch0 = nullptr, *cmatch0 = nullptr, *EP = nullptr;
   unsigned* dead = nullptr;
@@ -1560,6 +1765,41 @@ bm_status rows_to_host(bm_handle* h, int32_t* out, int off) {
   return BM_OK;
 }
 
+// Transposed adjacency for bottom-up levels (BM_BOTTOM_UP=0 disables them;
+// BM_BU_FRAC tunes the switch). Called after every change of the graph.
+bm_status build_transpose(bm_handle* h, int nc, int nr, long long E) {
+  {
+    h->bu_enabled = nr > 0 && nc > 0 && E > 0;
+    const char* fr = getenv("BM_BU_FRAC");
+    if (fr) h->bu_frac = atof(fr);
+  }
+  if (h->bu_enabled) {
+    BM_CUDA(dalloc(h->caps, h->roffs, (size_t)nr + 1));
+    BM_CUDA(dalloc(h->caps, h->rcursor, (size_t)nr + 1));
+    BM_CUDA(dalloc(h->caps, h->radj, (size_t)E));
+    h->nfbit_words = (nc + 31) / 32;
+    BM_CUDA(dalloc(h->caps, h->fbit, (size_t)2 * h->nfbit_words));
+    BM_CUDA(dalloc(h->caps, h->croot, (size_t)nc));
+    BM_CUDA(cudaMemsetAsync(h->rcursor, 0, sizeof(unsigned) * ((size_t)nr + 1), h->stream));
+    BM_CUDA(cudaMemsetAsync(h->fbit, 0, sizeof(unsigned) * 2 * h->nfbit_words, h->stream));
+    const int eb = (int)std::max<long long>(1, std::min<long long>((long long)h->sms * 8, (E + 255) / 256));
+    row_count_kernel<<<eb, 256, 0, h->stream>>>(h->adj, E, h->rcursor);
+    size_t tmp_bytes = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, h->rcursor, h->roffs, nr + 1, h->stream);
+    void* tmp = nullptr;
+    BM_CUDA(cudaMallocAsync(&tmp, std::max<size_t>(tmp_bytes, 1), h->stream));
+    cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, h->rcursor, h->roffs, nr + 1, h->stream);
+    BM_CUDA(cudaFreeAsync(tmp, h->stream));
+    BM_CUDA(cudaMemcpyAsync(h->rcursor, h->roffs, sizeof(unsigned) * ((size_t)nr + 1), cudaMemcpyDeviceToDevice,
+                            h->stream));
+    const int wb = std::max(1, std::min(h->sms * 16, (int)(((long long)nc * 32 + 255) / 256)));
+    transpose_scatter_kernel<<<wb, 256, 0, h->stream>>>(h->offs, h->adj, nc, h->rcursor, h->radj);
+    BM_CUDA(cudaGetLastError());
+  }
+  h->bu_built = true;
+  return BM_OK;
+}
+
 bm_status check_opts(const bm_match_opts* o) {
   if (!o) return fail(BM_ERR_INVALID_ARG, "null options");
   if (o->driver != BM_DRIVER_APFB && o->driver != BM_DRIVER_APSB)
@@ -1573,7 +1813,7 @@ bm_status check_opts(const bm_match_opts* o) {
     return fail(BM_ERR_INVALID_ARG, "unknown claim policy");
   if (o->endpoint_policy < BM_EP_AUTO || o->endpoint_policy > BM_EP_ONE_PER_TREE)
     return fail(BM_ERR_INVALID_ARG, "unknown endpoint policy");
-  if (o->reserved) return fail(BM_ERR_INVALID_ARG, "reserved option field must be 0");
+  if (o->bottom_up < 0 || o->bottom_up > 1) return fail(BM_ERR_INVALID_ARG, "bottom_up must be 0 or 1");
   // gpu_match.cpp:272-274
   if (o->improved && o->bfs_kernel != BM_BFS_WR)
     return fail(BM_ERR_LOGIC, "the endpoint-encoded alternation requires the with-root kernel");
@@ -1607,6 +1847,7 @@ bm_status prepare_fresh(bm_handle* h, bool reset_pred = false) {
   }
   BM_CUDA(cudaMemsetAsync(h->ctl, 0, sizeof(Ctrl), h->stream));
   BM_CUDA(cudaMemsetAsync(h->dead, 0, sizeof(unsigned) * std::max(h->ndead_words, 1), h->stream));
+  if (h->fbit) BM_CUDA(cudaMemsetAsync(h->fbit, 0, sizeof(unsigned) * 2 * std::max(h->nfbit_words, 1), h->stream));
   return BM_OK;
 }
 
@@ -1662,6 +1903,13 @@ Params make_params(bm_handle* h, const bm_match_opts& o) {
   p.pred = h->pred;
   p.bfs = h->bfs;
   p.dead = h->dead;
+  p.roffs = (o.bottom_up && h->bu_enabled && h->bu_built) ? h->roffs : nullptr;
+  p.radj = h->radj;
+  p.fbit[0] = h->fbit;
+  p.fbit[1] = h->fbit ? h->fbit + h->nfbit_words : nullptr;
+  p.croot = h->croot;
+  p.nfbit_words = h->nfbit_words;
+  p.bu_min_edges = (unsigned long long)std::max(1.0, h->bu_frac * (double)h->E);
   p.ndead_words = h->ndead_words;
   p.F0 = h->F[0];
   p.F1 = h->F[1];
@@ -1674,6 +1922,7 @@ Params make_params(bm_handle* h, const bm_match_opts& o) {
   p.claim_mode = o.claim_policy;
   p.ep_one = (o.bfs_kernel == BM_BFS_WR && o.endpoint_policy != BM_EP_EVERY) ? 1 : 0;
   p.solo_edges = kSoloEdges;
+  if (const char* se = getenv("BM_SOLO_EDGES")) p.solo_edges = (unsigned)atol(se);  // tuning / tests
   p.tl = h->tl;
   p.tl_cap = h->tl_cap;
   p.ctl = h->ctl;
@@ -1709,6 +1958,11 @@ bm_status drive(bm_handle* h, const bm_match_opts& o, bool fresh, int64_t* cardi
                 bm_counters* counters, int64_t* per_iter, int64_t cap, bm_phase_cb cb, void* user,
                 int32_t* done_out, bool init_checked = false) {
   const int v = variant_of(o.bfs_kernel == BM_BFS_WR, o.improved);
+  if (o.bottom_up && !h->bu_built) {  // one-time per resident graph
+    bm_status ts = build_transpose(h, h->nc, h->nr, h->E);
+    if (ts != BM_OK) return ts;
+    BM_CUDA(cudaStreamSynchronize(h->stream));
+  }
   Params p = make_params(h, o);
   p.fresh = fresh ? 1 : 0;
   p.init_checked = init_checked ? 1 : 0;
@@ -1903,6 +2157,11 @@ bm_status bm_destroy(bm_handle* h) {
   dfree(h->cmatch0);
   dfree(h->EP);
   dfree(h->dead);
+  dfree(h->roffs);
+  dfree(h->radj);
+  dfree(h->rcursor);
+  dfree(h->fbit);
+  dfree(h->croot);
   dfree(h->gidx[0]);
   dfree(h->gidx[1]);
   dfree(h->wlog);
@@ -2005,6 +2264,7 @@ bm_status bm_upload_csc(bm_handle* h, int32_t nc, int32_t nr, const int64_t* cxa
   if (bad[1]) return fail(BM_ERR_INVALID_ARG, "row index out of range in cadj");
   bad[2] -= bad[3];  // descending pairs inside columns
   h->sorted = bad[2] == 0;
+  h->bu_built = false;  // the row index is built on the first bottom-up run
   h->nr = nr;
   {
     bm_status fs = rows_fill(h, 1, -1);
@@ -2257,6 +2517,7 @@ bm_status bm_permute_random(bm_handle* h, const int32_t* cperm, const int32_t* r
   cleanup();
   if (e != cudaSuccess) return cuda_fail(e, "bm_permute_random");
   h->sorted = 1;
+  h->bu_built = false;
   h->has_init = false;  // an initial matching of the old labelling no longer applies
   h->resumable = false;
   return BM_OK;

@@ -275,3 +275,26 @@ def test_unsorted_columns_and_upload_checks(engine, oracle):
     engine.upload(g, force=True)
     res = engine.match(g, bm.cheap_matching(g))
     assert bm.cardinality(res.matching) == want
+
+
+def test_bottom_up_levels_parity(oracle, corpus, monkeypatch):
+    """Every level bottom-up (BM_BU_FRAC=0, no single-CTA levels): the pulled
+    levels must give the same maxima as the oracle on the corpus and on larger
+    graphs, under every driver/kernel combination."""
+    monkeypatch.setenv("BM_BU_FRAC", "0")
+    monkeypatch.setenv("BM_SOLO_EDGES", "0")
+    eng = bm.Engine(0)
+    eng.bottom_up = True
+    graphs = [g for g, _ in corpus[:120] + corpus[-4:]] + [
+        bm.generate_random_bipartite(20000, 20000, 4.0, 3), bm.generate_planted(30000, 8.0, 4), bm.generate_rmat(13, 8.0, 2)]
+    for g in graphs:
+        init = bm.cheap_matching(g)
+        want = oracle.maximum(g)
+        for shortest, kernel, improved in [(False, bm.BfsKernel.GpubfsWr, False), (True, bm.BfsKernel.GpubfsWr, True),
+                                           (False, bm.BfsKernel.Gpubfs, False), (True, bm.BfsKernel.Gpubfs, False)]:
+            res = eng.match(g, init, shortest=shortest, kernel=kernel, improved=improved)
+            m = res.matching
+            assert bm.cardinality(m) == want, (g.name, shortest, kernel)
+            assert oracle.validate(g, m.rmatch, m.cmatch) == 0
+            assert oracle.is_maximum(g, m.rmatch, m.cmatch) == 1
+    eng.close()
