@@ -86,7 +86,8 @@ __global__ void part_roots_kernel(PartDev d, int2* F, int* nF) {
 // deduplicated with the rmatch visited bit and the -1 -> -2 CAS; the merge
 // decides the global winners.
 constexpr int kGroup = 8;
-constexpr unsigned long long kBig = 256;
+constexpr unsigned long long kBig = 256;     // whole warp per entry
+constexpr unsigned long long kHuge = 16384;  // whole grid per entry (part_expand_huge_kernel)
 
 // Records are staged in shared memory and reserved with one global atomic per
 // CTA batch (a warp-level atomic per record batch on a single counter
@@ -141,7 +142,7 @@ __device__ __forceinline__ void flush_stage(PartSmem& sm, int4* claims, int* n_c
 
 __global__ void __launch_bounds__(kThr) part_expand_kernel(PartDev d, const int2* F, int n, int4* claims,
                                                            int* n_claims, int4* eps, int* n_eps,
-                                                           unsigned long long* stats) {
+                                                           unsigned long long* stats, int2* huge, int* n_huge) {
   __shared__ PartSmem sm;
   if (threadIdx.x == 0) {
     sm.nc = 0;
@@ -164,6 +165,10 @@ __global__ void __launch_bounds__(kThr) part_expand_kernel(PartDev d, const int2
         b = d.offs[c - d.col_lo];
         e = d.offs[c - d.col_lo + 1];
       }
+    }
+    if (e - b >= kHuge) {  // hubs (R-MAT): deferred to the grid-wide pass
+      if (g == 0) huge[atomicAdd(n_huge, 1)] = make_int2((int)w, 0);
+      b = e = 0;
     }
     const bool big = e - b >= kBig;
     if (g == 0 && e > b) {
@@ -188,6 +193,43 @@ __global__ void __launch_bounds__(kThr) part_expand_kernel(PartDev d, const int2
   trav = warp_sum(trav);
   cexp = warp_sum(cexp);
   if (lane == 0 && (trav | cexp)) {
+    atomicAdd(stats + 0, trav);
+    atomicAdd(stats + 1, cexp);
+  }
+}
+
+// The hub entries of this level: every warp of the grid strides over each
+// hub's rows in turn (a hub can hold a sizeable share of the level's edges).
+__global__ void __launch_bounds__(kThr) part_expand_huge_kernel(PartDev d, const int2* F, const int2* huge,
+                                                                const int* n_huge, int4* claims, int* n_claims,
+                                                                int4* eps, int* n_eps, unsigned long long* stats) {
+  __shared__ PartSmem sm;
+  if (threadIdx.x == 0) {
+    sm.nc = 0;
+    sm.ne = 0;
+  }
+  __syncthreads();
+  const int nh = *n_huge;
+  unsigned long long trav = 0, cexp = 0;
+  const long long gt = (long long)gridDim.x * blockDim.x;
+  for (int h = 0; h < nh; ++h) {
+    const int2 ent = F[huge[h].x];
+    const int c = ent.x, root = ent.y;
+    const unsigned long long b = d.offs[c - d.col_lo], e = d.offs[c - d.col_lo + 1];
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      cexp++;
+      trav += e - b;
+    }
+    // CTA-uniform trip count so flush_stage's barriers line up
+    for (unsigned long long base = b + (unsigned long long)blockIdx.x * blockDim.x; base < e; base += gt) {
+      const unsigned long long j = base + threadIdx.x;
+      if (j < e) part_edge(d, sm, d.adj[j], c, root, claims, n_claims, eps, n_eps);
+      flush_stage(sm, claims, n_claims, eps, n_eps);
+    }
+  }
+  trav = warp_sum(trav);
+  cexp = warp_sum(cexp);
+  if (lane_id() == 0 && (trav | cexp)) {
     atomicAdd(stats + 0, trav);
     atomicAdd(stats + 1, cexp);
   }
@@ -388,6 +430,7 @@ struct bm_part {
   int *pred = nullptr, *winC = nullptr, *winR = nullptr, *winE = nullptr, *ep_list = nullptr;
   unsigned* dead = nullptr;
   int2* F[2] = {nullptr, nullptr};
+  int2* huge = nullptr;  // hub entries of the current level
   int cur = 0;
   int* cnt = nullptr;                     // [0] nF cur, [1] nF next, [2] claims, [3] eps, [4] n_ep list, [5] found, [6..] gathered counts
   unsigned long long* stats = nullptr;    // trav, cexp, walks, steps, resets, live, matched
@@ -496,6 +539,7 @@ bm_status bm_part_destroy(bm_part* pt) {
   pfree(pt->dead);
   pfree(pt->F[0]);
   pfree(pt->F[1]);
+  pfree(pt->huge);
   pfree(pt->cnt);
   pfree(pt->stats);
   if (pt->own) cudaStreamDestroy(pt->own);
@@ -534,6 +578,7 @@ bm_status bm_part_upload(bm_part* pt, int32_t nc, int32_t nr, int32_t col_lo, in
   pfree(pt->dead);
   pfree(pt->F[0]);
   pfree(pt->F[1]);
+  pfree(pt->huge);
   pt->nc = -1;
   PCUDA(cudaMalloc(&pt->offs, sizeof(unsigned long long) * (ncl + 1)));
   PCUDA(cudaMalloc(&pt->adj, sizeof(int) * std::max<long long>(E, 1)));
@@ -545,6 +590,7 @@ bm_status bm_part_upload(bm_part* pt, int32_t nc, int32_t nr, int32_t col_lo, in
   PCUDA(cudaMalloc(&pt->dead, sizeof(unsigned) * ((nc + 31) / 32 + 1)));
   PCUDA(cudaMalloc(&pt->F[0], sizeof(int2) * std::max(ncl, 1)));
   PCUDA(cudaMalloc(&pt->F[1], sizeof(int2) * std::max(ncl, 1)));
+  PCUDA(cudaMalloc(&pt->huge, sizeof(int2) * std::max(ncl, 1)));
   PCUDA(cudaMemcpyAsync(pt->offs, cxadj_slice, sizeof(long long) * (ncl + 1), cudaMemcpyHostToDevice, pt->stream));
   if (E > 0) PCUDA(cudaMemcpyAsync(pt->adj, cadj_slice, sizeof(int) * E, cudaMemcpyHostToDevice, pt->stream));
   fill_kernel<<<64, kThr, 0, pt->stream>>>(pt->winC, std::max(nc, 1), INT_MAX);
@@ -608,10 +654,15 @@ bm_status bm_part_expand(bm_part* pt, void* claims_out, void* endpoints_out, int
   if (!claims_out || !endpoints_out) return pfail(BM_ERR_INVALID_ARG, "null record buffer");
   PCUDA(cudaSetDevice(pt->device));
   PCUDA(cudaMemsetAsync(pt->cnt + 2, 0, sizeof(int) * 2, pt->stream));
-  if (pt->n_cur > 0)
+  PCUDA(cudaMemsetAsync(pt->cnt + 63, 0, sizeof(int), pt->stream));  // hub count
+  if (pt->n_cur > 0) {
     part_expand_kernel<<<blocks_for(pt, (long long)pt->n_cur * kGroup), kThr, 0, pt->stream>>>(
         dev_of(pt), pt->F[pt->cur], pt->n_cur, static_cast<int4*>(claims_out), pt->cnt + 2,
+        static_cast<int4*>(endpoints_out), pt->cnt + 3, pt->stats, pt->huge, pt->cnt + 63);
+    part_expand_huge_kernel<<<pt->sms * 4, kThr, 0, pt->stream>>>(
+        dev_of(pt), pt->F[pt->cur], pt->huge, pt->cnt + 63, static_cast<int4*>(claims_out), pt->cnt + 2,
         static_cast<int4*>(endpoints_out), pt->cnt + 3, pt->stats);
+  }
   PCUDA(cudaGetLastError());
   int c[2] = {0, 0};
   PCUDA(cudaMemcpyAsync(c, pt->cnt + 2, sizeof(c), cudaMemcpyDeviceToHost, pt->stream));
@@ -634,7 +685,7 @@ bm_status bm_part_merge(bm_part* pt, const void* claims_all, const int32_t* clai
       return pfail(BM_ERR_INVALID_ARG, "record count exceeds its stride");
   PCUDA(cudaSetDevice(pt->device));
   // counts to the device: [6, 6+world) claims, [6+world, 6+2*world) endpoints
-  if (2 * pt->world + 6 > 64) return pfail(BM_ERR_INVALID_ARG, "world too large");
+  if (2 * pt->world + 6 > 63) return pfail(BM_ERR_INVALID_ARG, "world too large");  // cnt[63]: hub count
   PCUDA(cudaMemcpyAsync(pt->cnt + 6, claim_counts, sizeof(int) * pt->world, cudaMemcpyHostToDevice, pt->stream));
   PCUDA(cudaMemcpyAsync(pt->cnt + 6 + pt->world, endpoint_counts, sizeof(int) * pt->world, cudaMemcpyHostToDevice,
                         pt->stream));
