@@ -44,11 +44,18 @@ struct PartDev {
   int* cmatch;
   int* pred;
   unsigned* dead;
-  int* winC;  // nc, INT_MAX when free
-  int* winR;  // nc (roots)
-  int* winE;  // nr
+  // per-level winner keys, ((~stamp) << 32) | record index: a lower key wins,
+  // keys of earlier levels are larger, so the arrays never need a reset pass
+  unsigned long long* winC;  // nc
+  unsigned long long* winR;  // nc (roots)
+  unsigned long long* winE;  // nr
+  unsigned stamp;            // merge counter of this handle
   int ep_one, wr;
 };
+
+__device__ __forceinline__ unsigned long long win_key(const PartDev& d, long long i) {
+  return ((unsigned long long)(0xffffffffu - d.stamp) << 32) | (unsigned long long)(unsigned)i;
+}
 
 __device__ __forceinline__ bool dead_root(const PartDev& d, int root) {
   return (ld_rlx(d.dead + (root >> 5)) >> (root & 31)) & 1u;
@@ -258,7 +265,7 @@ __global__ void part_ep_root_kernel(PartDev d, Gathered g) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < tot; i += (long long)gridDim.x * blockDim.x) {
     int4 r;
     if (!rec_at(g, i, r)) continue;
-    if (d.ep_one && !dead_root(d, r.z)) atomicMin(d.winR + r.z, (int)i);
+    if (d.ep_one && !dead_root(d, r.z)) atomicMin(d.winR + r.z, win_key(d, i));
   }
 }
 // Step 2: lowest surviving record per row.
@@ -267,7 +274,7 @@ __global__ void part_ep_row_kernel(PartDev d, Gathered g) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < tot; i += (long long)gridDim.x * blockDim.x) {
     int4 r;
     if (!rec_at(g, i, r)) continue;
-    if (d.ep_one ? (d.winR[r.z] == (int)i) : true) atomicMin(d.winE + r.x, (int)i);
+    if (d.ep_one ? (d.winR[r.z] == win_key(d, i)) : true) atomicMin(d.winE + r.x, win_key(d, i));
   }
 }
 // Step 3: winners become endpoints everywhere; a row no record won goes back to -1.
@@ -276,28 +283,18 @@ __global__ void part_ep_apply_kernel(PartDev d, Gathered g, int* ep_list, int* n
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < tot; i += (long long)gridDim.x * blockDim.x) {
     int4 r;
     if (!rec_at(g, i, r)) continue;
-    const int w = d.winE[r.x];
-    if (w == (int)i) {
+    const unsigned long long w = d.winE[r.x];
+    if (w == win_key(d, i)) {
       d.rmatch[r.x] = -2;
       d.pred[r.x] = r.y;
       if (d.wr) atomicOr(d.dead + (r.z >> 5), 1u << (r.z & 31));
       if (keep_list) ep_list[atomicAdd(n_ep, 1)] = r.x;
       *found = 1;
-    } else if (w == INT_MAX) {
-      d.rmatch[r.x] = -1;  // flagged by a rank, won by nobody: free again
+    } else if ((w >> 32) != (0xffffffffu - d.stamp)) {
+      d.rmatch[r.x] = -1;  // flagged by a rank, won by nobody this level: free again
     }
   }
 }
-__global__ void part_ep_reset_kernel(PartDev d, Gathered g) {
-  const long long tot = (long long)g.world * g.stride;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < tot; i += (long long)gridDim.x * blockDim.x) {
-    int4 r;
-    if (!rec_at(g, i, r)) continue;
-    d.winR[r.z] = INT_MAX;
-    d.winE[r.x] = INT_MAX;
-  }
-}
-
 // Claims: lowest record per column wins; the winner's discoverer becomes
 // pred[row] on every rank, and the owner of the column queues it (unless its
 // tree found a path at this level).
@@ -306,7 +303,7 @@ __global__ void part_claim_min_kernel(PartDev d, Gathered g) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < tot; i += (long long)gridDim.x * blockDim.x) {
     int4 r;
     if (!rec_at(g, i, r)) continue;
-    atomicMin(d.winC + r.x, (int)i);
+    atomicMin(d.winC + r.x, win_key(d, i));
   }
 }
 __global__ void part_claim_apply_kernel(PartDev d, Gathered g, int2* Fn, int* nFn, unsigned long long* n_live) {
@@ -315,7 +312,7 @@ __global__ void part_claim_apply_kernel(PartDev d, Gathered g, int2* Fn, int* nF
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < tot; i += (long long)gridDim.x * blockDim.x) {
     int4 r;
     if (!rec_at(g, i, r)) continue;
-    if (d.winC[r.x] != (int)i) continue;
+    if (d.winC[r.x] != win_key(d, i)) continue;
     d.rmatch[r.w] = r.x | kVis;
     d.pred[r.w] = r.y;
     if (d.wr && dead_root(d, r.z)) continue;
@@ -325,15 +322,6 @@ __global__ void part_claim_apply_kernel(PartDev d, Gathered g, int2* Fn, int* nF
   live = warp_sum(live);
   if (lane_id() == 0 && live) atomicAdd(n_live, live);
 }
-__global__ void part_claim_reset_kernel(PartDev d, Gathered g) {
-  const long long tot = (long long)g.world * g.stride;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < tot; i += (long long)gridDim.x * blockDim.x) {
-    int4 r;
-    if (!rec_at(g, i, r)) continue;
-    d.winC[r.x] = INT_MAX;
-  }
-}
-
 __global__ void part_sweep_kernel(int* rmatch, int nr) {
   for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < nr; r += (long long)gridDim.x * blockDim.x) {
     const int v = rmatch[r];
@@ -427,7 +415,9 @@ struct bm_part {
   int* adj = nullptr;
   int* rmatch = nullptr;  // caller-owned (bm_part_bind_state)
   int* cmatch = nullptr;
-  int *pred = nullptr, *winC = nullptr, *winR = nullptr, *winE = nullptr, *ep_list = nullptr;
+  int *pred = nullptr, *ep_list = nullptr;
+  unsigned long long *winC = nullptr, *winR = nullptr, *winE = nullptr;
+  unsigned stamp = 0;
   unsigned* dead = nullptr;
   int2* F[2] = {nullptr, nullptr};
   int2* huge = nullptr;  // hub entries of the current level
@@ -474,6 +464,7 @@ PartDev dev_of(const bm_part* pt) {
   d.winC = pt->winC;
   d.winR = pt->winR;
   d.winE = pt->winE;
+  d.stamp = pt->stamp;
   d.ep_one = pt->ep_one;
   d.wr = pt->wr;
   return d;
@@ -583,9 +574,9 @@ bm_status bm_part_upload(bm_part* pt, int32_t nc, int32_t nr, int32_t col_lo, in
   PCUDA(cudaMalloc(&pt->offs, sizeof(unsigned long long) * (ncl + 1)));
   PCUDA(cudaMalloc(&pt->adj, sizeof(int) * std::max<long long>(E, 1)));
   PCUDA(cudaMalloc(&pt->pred, sizeof(int) * std::max(nr, 1)));
-  PCUDA(cudaMalloc(&pt->winC, sizeof(int) * std::max(nc, 1)));
-  PCUDA(cudaMalloc(&pt->winR, sizeof(int) * std::max(nc, 1)));
-  PCUDA(cudaMalloc(&pt->winE, sizeof(int) * std::max(nr, 1)));
+  PCUDA(cudaMalloc(&pt->winC, sizeof(unsigned long long) * std::max(nc, 1)));
+  PCUDA(cudaMalloc(&pt->winR, sizeof(unsigned long long) * std::max(nc, 1)));
+  PCUDA(cudaMalloc(&pt->winE, sizeof(unsigned long long) * std::max(nr, 1)));
   PCUDA(cudaMalloc(&pt->ep_list, sizeof(int) * std::max(nr, 1)));
   PCUDA(cudaMalloc(&pt->dead, sizeof(unsigned) * ((nc + 31) / 32 + 1)));
   PCUDA(cudaMalloc(&pt->F[0], sizeof(int2) * std::max(ncl, 1)));
@@ -593,9 +584,10 @@ bm_status bm_part_upload(bm_part* pt, int32_t nc, int32_t nr, int32_t col_lo, in
   PCUDA(cudaMalloc(&pt->huge, sizeof(int2) * std::max(ncl, 1)));
   PCUDA(cudaMemcpyAsync(pt->offs, cxadj_slice, sizeof(long long) * (ncl + 1), cudaMemcpyHostToDevice, pt->stream));
   if (E > 0) PCUDA(cudaMemcpyAsync(pt->adj, cadj_slice, sizeof(int) * E, cudaMemcpyHostToDevice, pt->stream));
-  fill_kernel<<<64, kThr, 0, pt->stream>>>(pt->winC, std::max(nc, 1), INT_MAX);
-  fill_kernel<<<64, kThr, 0, pt->stream>>>(pt->winR, std::max(nc, 1), INT_MAX);
-  fill_kernel<<<64, kThr, 0, pt->stream>>>(pt->winE, std::max(nr, 1), INT_MAX);
+  PCUDA(cudaMemsetAsync(pt->winC, 0xff, sizeof(unsigned long long) * std::max(nc, 1), pt->stream));
+  PCUDA(cudaMemsetAsync(pt->winR, 0xff, sizeof(unsigned long long) * std::max(nc, 1), pt->stream));
+  PCUDA(cudaMemsetAsync(pt->winE, 0xff, sizeof(unsigned long long) * std::max(nr, 1), pt->stream));
+  pt->stamp = 0;
   fill_kernel<<<64, kThr, 0, pt->stream>>>(pt->pred, std::max(nr, 1), -1);
   PCUDA(cudaGetLastError());
   PCUDA(cudaStreamSynchronize(pt->stream));
@@ -691,6 +683,7 @@ bm_status bm_part_merge(bm_part* pt, const void* claims_all, const int32_t* clai
                         pt->stream));
   PCUDA(cudaMemsetAsync(pt->stats + 5, 0, sizeof(unsigned long long), pt->stream));
   PCUDA(cudaMemsetAsync(pt->cnt + 1, 0, sizeof(int), pt->stream));
+  pt->stamp++;  // a fresh key space: every earlier level's winner key loses
   const PartDev d = dev_of(pt);
   const Gathered ge{static_cast<const int4*>(endpoints_all), pt->cnt + 6 + pt->world, endpoint_stride, pt->world};
   const Gathered gc{static_cast<const int4*>(claims_all), pt->cnt + 6, claim_stride, pt->world};
@@ -700,13 +693,11 @@ bm_status bm_part_merge(bm_part* pt, const void* claims_all, const int32_t* clai
     part_ep_root_kernel<<<b, kThr, 0, pt->stream>>>(d, ge);
     part_ep_row_kernel<<<b, kThr, 0, pt->stream>>>(d, ge);
     part_ep_apply_kernel<<<b, kThr, 0, pt->stream>>>(d, ge, pt->ep_list, pt->cnt + 4, pt->rank == 0, pt->cnt + 5);
-    part_ep_reset_kernel<<<b, kThr, 0, pt->stream>>>(d, ge);
   }
   if (tc > 0) {
     const int b = blocks_for(pt, tc);
     part_claim_min_kernel<<<b, kThr, 0, pt->stream>>>(d, gc);
     part_claim_apply_kernel<<<b, kThr, 0, pt->stream>>>(d, gc, pt->F[pt->cur ^ 1], pt->cnt + 1, pt->stats + 5);
-    part_claim_reset_kernel<<<b, kThr, 0, pt->stream>>>(d, gc);
   }
   PCUDA(cudaGetLastError());
   int nxt[5] = {0, 0, 0, 0, 0};
