@@ -250,10 +250,18 @@ __device__ __forceinline__ void tl_mark(const Params& p, unsigned kind, unsigned
 }
 
 struct Smem {
-  unsigned pre[kThreads + 1];   // window: raw edge prefix of each entry, then the live-edge prefix
-  int col[kThreads];
-  int root[kThreads];
-  unsigned beg[kThreads];       // first live adjacency index of each entry in this window
+  union {  // a top-down window, or a bottom-up candidate stage (never both at once)
+    struct {
+      unsigned pre[kThreads + 1];  // window: raw edge prefix of each entry, then the live-edge prefix
+      int col[kThreads];
+      int root[kThreads];
+      unsigned beg[kThreads];      // first live adjacency index of each entry in this window
+    };
+    struct {
+      int bcand[2 * kThreads];     // bottom-up: candidate rows of a sweep step ...
+      int bcandv[2 * kThreads];    // ... and their rmatch values
+    };
+  };
   unsigned wtot[kThreads / 32];
   unsigned short cgr[kWBuf / 32 + 2];  // entry holding live edge 32*q (coarse index for the search)
   unsigned tile;
@@ -264,8 +272,6 @@ struct Smem {
   unsigned blk_ep;
   unsigned nw;                          // winners staged in wbuf for the current window
   int2 wbuf[kWBuf];                     // (column, root) claimed in the current window
-  int bcand[2 * kThreads];              // bottom-up: candidate rows of a sweep step ...
-  int bcandv[2 * kThreads];             // ... and their rmatch values
 #if BM_ASYNC
   int srow[kWBuf];                      // live edge -> adjacency row (cp.async)
   int scm[kWBuf];                       // live edge -> rmatch of that row (cp.async)
@@ -1067,7 +1073,7 @@ struct PhaseOut {
 };
 
 // One phase = run_phase (gpu_match.cpp:268-302) from the roots in F[cur].
-template <bool WR, bool IMP>
+template <bool WR, bool IMP, bool BU>
 __device__ PhaseOut run_phase(const Params& p, Smem& sm, int cur, int parity, bool serial_alt,
                               long long isolated) {
   Ctrl* ctl = p.ctl;
@@ -1108,7 +1114,9 @@ __device__ PhaseOut run_phase(const Params& p, Smem& sm, int cur, int parity, bo
       z->tile = 0;
     }
     if (solo) __syncthreads();
-    const bool bu = !solo && p.roffs && !p.trace && (unsigned long long)T >= p.bu_min_edges;
+    // BU: compiled only into the bottom-up kernel instances, so the push-only
+    // kernel keeps its register allocation
+    const bool bu = BU && !solo && p.roffs && !p.trace && (unsigned long long)T >= p.bu_min_edges;
     if (bu) {
       bu_prep<WR>(p, F, ls, n, lv);
       grid_sync(ctl);
@@ -1294,7 +1302,7 @@ __device__ PhaseOut run_phase(const Params& p, Smem& sm, int cur, int parity, bo
 }
 
 // ---------------------------------------------------------------------------
-template <bool WR, bool IMP>
+template <bool WR, bool IMP, bool BU>
 __global__ void __launch_bounds__(kThreads, BM_MINB) driver_kernel(Params p) {
   __shared__ Smem sm;
   Ctrl* ctl = p.ctl;
@@ -1395,7 +1403,7 @@ __global__ void __launch_bounds__(kThreads, BM_MINB) driver_kernel(Params p) {
     }
     ++outer;
     const long long before = card;
-    PhaseOut ph = run_phase<WR, IMP>(p, sm, cur, parity, false, isolated);
+    PhaseOut ph = run_phase<WR, IMP, BU>(p, sm, cur, parity, false, isolated);
     if (p.stop_after_bfs) {
       if (is_leader()) {
         ctl->bfs_levels_last = ph.launches;
@@ -1410,7 +1418,7 @@ __global__ void __launch_bounds__(kThreads, BM_MINB) driver_kernel(Params p) {
     long long after = ph.after;
     bool retried = false;
     if (ph.found && after <= before) {
-      PhaseOut rt = run_phase<WR, IMP>(p, sm, cur, parity, true, isolated);
+      PhaseOut rt = run_phase<WR, IMP, BU>(p, sm, cur, parity, true, isolated);
       cur ^= 1;
       parity ^= 1;
       launches += rt.launches;
@@ -1669,7 +1677,7 @@ struct bm_handle {
   cudaStream_t own = nullptr;
   cudaStream_t stream = nullptr;
   int sms = 0;
-  int bps[3] = {0, 0, 0};  // co-resident CTAs per SM, per kernel variant
+  int bps[6] = {0, 0, 0, 0, 0, 0};  // co-resident CTAs per SM, per kernel variant
   // graph
   int nc = -1, nr = -1;
   long long E = 0;
@@ -1820,13 +1828,16 @@ bm_status check_opts(const bm_match_opts* o) {
   return BM_OK;
 }
 
-int variant_of(int wr, int imp) { return wr ? (imp ? 2 : 1) : 0; }
+int variant_of(int wr, int imp, int bu = 0) { return (wr ? (imp ? 2 : 1) : 0) + (bu ? 3 : 0); }
 
 const void* kernel_ptr(int v) {
   switch (v) {
-    case 0: return reinterpret_cast<const void*>(&driver_kernel<false, false>);
-    case 1: return reinterpret_cast<const void*>(&driver_kernel<true, false>);
-    default: return reinterpret_cast<const void*>(&driver_kernel<true, true>);
+    case 0: return reinterpret_cast<const void*>(&driver_kernel<false, false, false>);
+    case 1: return reinterpret_cast<const void*>(&driver_kernel<true, false, false>);
+    case 2: return reinterpret_cast<const void*>(&driver_kernel<true, true, false>);
+    case 3: return reinterpret_cast<const void*>(&driver_kernel<false, false, true>);
+    case 4: return reinterpret_cast<const void*>(&driver_kernel<true, false, true>);
+    default: return reinterpret_cast<const void*>(&driver_kernel<true, true, true>);
   }
 }
 
@@ -1957,7 +1968,7 @@ bm_status ctl_error_status(int err) {
 bm_status drive(bm_handle* h, const bm_match_opts& o, bool fresh, int64_t* cardinality,
                 bm_counters* counters, int64_t* per_iter, int64_t cap, bm_phase_cb cb, void* user,
                 int32_t* done_out, bool init_checked = false) {
-  const int v = variant_of(o.bfs_kernel == BM_BFS_WR, o.improved);
+  const int v = variant_of(o.bfs_kernel == BM_BFS_WR, o.improved, o.bottom_up);
   if (o.bottom_up && !h->bu_built) {  // one-time per resident graph
     bm_status ts = build_transpose(h, h->nc, h->nr, h->E);
     if (ts != BM_OK) return ts;
@@ -2115,7 +2126,7 @@ bm_status bm_create(int32_t device, bm_handle** out) {
   auto* h = new bm_handle();
   h->device = device;
   h->sms = prop.multiProcessorCount;
-  for (int v = 0; v < 3; ++v) {
+  for (int v = 0; v < 6; ++v) {
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&h->bps[v], kernel_ptr(v), kThreads, 0);
     if (e != cudaSuccess || h->bps[v] < 1) {
       delete h;
