@@ -76,14 +76,8 @@ constexpr int kThreads = BM_THREADS;  // threads per CTA (1024 / kThreads CTAs p
 #endif
 constexpr int kItems = BM_ITEMS;      // edges per thread per round (memory-level parallelism)
 constexpr unsigned kGran = 512;       // edges per granule-index entry; tiles are whole granules
-#ifndef BM_ASYNC
-#define BM_ASYNC 0  // stage a window's adjacency rows and mates in shared memory with cp.async
-#endif
-constexpr unsigned kMaxTileGran = BM_ASYNC ? 4 : 8;  // edges per tile (= the winner / staging buffers)
+constexpr unsigned kMaxTileGran = 8;  // <= 4096 edges per tile (= the winner buffer)
 constexpr unsigned kWBuf = kGran * kMaxTileGran;
-#ifndef BM_BATCH
-#define BM_BATCH 1  // issue all of a thread's claim atomics before consuming any
-#endif
 #ifndef BM_INTERLEAVE_MB
 #define BM_INTERLEAVE_MB 72  // interleave {mate, pred} when the plain rmatch exceeds this many MB
 #endif
@@ -272,10 +266,6 @@ struct Smem {
   unsigned blk_ep;
   unsigned nw;                          // winners staged in wbuf for the current window
   int2 wbuf[kWBuf];                     // (column, root) claimed in the current window
-#if BM_ASYNC
-  int srow[kWBuf];                      // live edge -> adjacency row (cp.async)
-  int scm[kWBuf];                       // live edge -> rmatch of that row (cp.async)
-#endif
 };
 
 // Warp-reduce a per-thread count and add it to the CTA's shared counter. Must
@@ -411,25 +401,8 @@ __device__ __forceinline__ void put_entry(int4* F, unsigned out_base, unsigned* 
 __device__ __forceinline__ int* RM(const Params& p, long long r) { return p.rm + p.rs * r; }
 __device__ __forceinline__ int* PR(const Params& p, long long r) { return p.pred + p.rs * r; }
 
-// Offsets of a claimed column: read once per claim, no reuse worth keeping in
-// L2 (BM_OFFS_EF: evict_first, so they do not displace the gathered rmatch).
-#ifndef BM_OFFS_EF
-#define BM_OFFS_EF 0
-#endif
-__device__ __forceinline__ unsigned ld_offs(const unsigned* a, unsigned long long pol) {
-  return BM_OFFS_EF ? ld_ro_hint(a, pol) : ld_ro(a);
-}
-
-// 4-byte asynchronous global -> shared copies (LDGSTS): a thread can have
-// many in flight without holding a register for each.
-__device__ __forceinline__ void cp_async4(void* smem, const void* gmem, unsigned long long pol) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 4, %2;" ::"r"(s), "l"(gmem), "l"(pol)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() {
-  asm volatile("cp.async.commit_group;\ncp.async.wait_all;" ::: "memory");
-}
+// Offsets of a claimed column (read-only path).
+__device__ __forceinline__ unsigned ld_offs(const unsigned* a, unsigned long long) { return ld_ro(a); }
 
 // WR early-exit test (gpu_match.cpp:106-108) against the dead-root bitmap:
 // nc/8 bytes that stay in L2, instead of a bfs_array[root] gather per entry.
@@ -743,116 +716,6 @@ __device__ __forceinline__ void expand_level(const Params& p, Smem& sm, int4* F,
       if (wend < e1 && i + kThreads + tid < n)
         prefetch_l2(F + ls + i + kThreads + tid);
 
-#if BM_ASYNC
-      // The window's live edges in three bulk steps, each one memory round trip
-      // for the whole window: (A) adjacency rows -> smem, (B) their rmatch
-      // entries -> smem, both with cp.async (no register per outstanding load);
-      // (C) claims in rounds of kItems per thread, atomics issued before use.
-      auto slot_of = [&](unsigned ee) -> int {  // entry holding live edge ee (coarse index, 1-2 steps)
-        const unsigned q = ee >> 5;
-        int a = sm.cgr[q];
-        int b = (q + 1 < nq) ? (int)sm.cgr[q + 1] + 1 : kThreads;
-        while (b - a > 1) {
-          const int mid = (a + b) >> 1;
-          if (sm.pre[mid] <= ee) a = mid; else b = mid;
-        }
-        return a;
-      };
-      for (unsigned ee = tid; ee < live; ee += kThreads) {
-        const int a = slot_of(ee);
-        cp_async4(&sm.srow[ee], p.adj + sm.beg[a] + (ee - sm.pre[a]), pol);
-      }
-      cp_async_wait_all();
-      __syncthreads();
-      for (unsigned ee = tid; ee < live; ee += kThreads) cp_async4(&sm.scm[ee], RM(p, sm.srow[ee]), keep);
-      c_trav += live > tid ? (live - tid + kThreads - 1) / kThreads : 0u;
-      cp_async_wait_all();
-      __syncthreads();
-      for (unsigned base = 0; base < live; base += kThreads * kItems) {
-        int row[kItems], cm[kItems];
-#pragma unroll
-        for (int k = 0; k < kItems; ++k) {
-          const unsigned ee = base + k * kThreads + tid;
-          row[k] = ee < live ? sm.srow[ee] : -1;
-          cm[k] = ee < live ? sm.scm[ee] : -3;
-        }
-        unsigned wins = 0, eps = 0;
-        int old[kItems];
-#pragma unroll
-        for (int k = 0; k < kItems; ++k) {
-          const int c = cm[k];  // mate of the row; kVisBit set = its column was claimed this phase
-          old[k] = kVisBit;
-          if (c >= 0 && !(c & kVisBit) &&
-              (!WR || p.claim_mode == 0 || !root_dead(p, sm.root[slot_of(base + k * kThreads + tid)])))
-            old[k] = atomicOr(RM(p, row[k]), kVisBit);
-        }
-        int wroot[kItems];
-#pragma unroll
-        for (int k = 0; k < kItems; ++k) {
-          const int c = cm[k];
-          wroot[k] = 0;
-          if (c >= 0 ? !(old[k] & kVisBit) : c == -1) {
-            const int sl = slot_of(base + k * kThreads + tid);
-            const int col = sm.col[sl];
-            const int root = WR ? sm.root[sl] : col;
-            wroot[k] = root;
-            if (c >= 0) {
-              wins |= 1u << k;
-              if (BM_PF == 2) prefetch_l2(p.offs + c);  // the flush reads offs[c], offs[c+1]
-              st_stream(PR(p, row[k]), col, pol);
-              if (p.trace) st_plain(p.bfs + c, level + 1);
-            } else {
-              // ONE_PER_TREE: a tree that already holds an endpoint leaves the row alone
-              const bool one = WR && p.ep_one;
-              if ((!one || !root_dead(p, root)) && atomicCAS(RM(p, row[k]), -1, -2) == -1) {
-                bool mine = true;
-                if (one) {
-                  // the root's mark is the tree's endpoint slot: first CAS wins, a loser releases the row
-                  mine = atomicCAS(p.bfs + root, kStartLevel, IMP ? -row[k] : kFoundMark) == kStartLevel;
-                  if (!mine) st_rlx(RM(p, row[k]), -1);
-                  else mark_dead(p, root);
-                } else if (WR) {
-                  st_rlx(p.bfs + root, IMP ? -row[k] : kFoundMark);  // gpu_match.cpp:122-123
-                  mark_dead(p, root);
-                }
-                if (mine) {
-                  eps |= 1u << k;
-                  st_plain(PR(p, row[k]), col);
-                  if (ld_rlx(path_flag) == 0u) st_rlx(path_flag, 1u);
-                }
-              }
-            }
-          }
-        }
-        // stage winners (one shared-memory atomic per warp)
-        {
-          const unsigned mine = __popc(wins);
-          const unsigned incl = warp_incl_scan(mine);
-          const unsigned tot = __shfl_sync(kFull, incl, 31);
-          unsigned wb = 0;
-          if (lane_id() == 31 && tot) wb = atomicAdd(&sm.nw, tot);
-          wb = __shfl_sync(kFull, wb, 31) + incl - mine;
-#pragma unroll
-          for (int k = 0; k < kItems; ++k)
-            if (wins & (1u << k)) sm.wbuf[wb++] = make_int2(cm[k], wroot[k]);
-          c_nvis += mine;
-        }
-        // endpoints are rare: warp-aggregated global append
-        {
-          const unsigned mine = __popc(eps);
-          const unsigned incl = warp_incl_scan(mine);
-          const unsigned tot = __shfl_sync(kFull, incl, 31);
-          if (tot) {
-            unsigned eb = 0;
-            if (lane_id() == 31) eb = atomicAdd(&p.ctl->n_ep, tot);
-            eb = __shfl_sync(kFull, eb, 31) + incl - mine;
-#pragma unroll
-            for (int k = 0; k < kItems; ++k)
-              if (eps & (1u << k)) st_plain(p.EP + eb++, row[k]);
-          }
-        }
-      }
-#else
       // Rounds over the live edges: no CTA-wide barrier inside; winners are
       // staged in sm.wbuf.
       for (unsigned base = 0; base < live; base += kThreads * kItems) {
@@ -888,8 +751,7 @@ __device__ __forceinline__ void expand_level(const Params& p, Smem& sm, int4* F,
         for (int k = 0; k < kItems; ++k) {
           const int c = cm[k];  // mate of the row; kVisBit set = its column was claimed this phase
           old[k] = kVisBit;
-          if (BM_BATCH && c >= 0 && !(c & kVisBit) &&
-              (!WR || p.claim_mode == 0 || !root_dead(p, sm.root[sl[k]])))
+          if (c >= 0 && !(c & kVisBit) && (!WR || p.claim_mode == 0 || !root_dead(p, sm.root[sl[k]])))
             old[k] = atomicOr(RM(p, row[k]), kVisBit);
         }
 #pragma unroll
@@ -898,8 +760,6 @@ __device__ __forceinline__ void expand_level(const Params& p, Smem& sm, int4* F,
           const int col = sm.col[sl[k]];
           const int root = WR ? sm.root[sl[k]] : col;
           if (c >= 0) {
-            if (!BM_BATCH && !(c & kVisBit) && (!WR || p.claim_mode == 0 || !root_dead(p, root)))
-              old[k] = atomicOr(RM(p, row[k]), kVisBit);
             if (!(old[k] & kVisBit)) {
               wins |= 1u << k;
               if (BM_PF == 2) prefetch_l2(p.offs + c);  // the flush reads offs[c], offs[c+1]
@@ -957,7 +817,6 @@ __device__ __forceinline__ void expand_level(const Params& p, Smem& sm, int4* F,
           }
         }
       }
-#endif
       __syncthreads();
       if (tid == 0) {
         const long long t = clk();
