@@ -36,6 +36,9 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+# NCCL's "NCCL version ..." banner goes to stdout; the contract is one JSON line there
+if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
+    os.environ["NCCL_DEBUG"] = "WARN"
 
 METRIC = "time-to-maximum-matching (ms) and traversed edges/sec; % of HBM roofline"
 
@@ -262,6 +265,7 @@ def run_partitioned(args):
     dist.barrier()
     torch.cuda.synchronize(dev)
     ms, cards = [], []
+    launches = 0
     sampler = ClockSampler(local)
     with sampler:
         for _ in range(args.steps):
@@ -273,6 +277,7 @@ def run_partitioned(args):
             e1.synchronize()
             ms.append(e0.elapsed_time(e1))
             cards.append(r.cardinality)
+            launches += r.stats.get("launches", 0)
             parity_ok = parity_ok and (known is None or r.cardinality == known)
     torch.cuda.synchronize(dev)
     dist.barrier()
@@ -312,7 +317,7 @@ def run_partitioned(args):
                          "kernel": "bm_part_* level kernels + exchange (whole step)",
                          "algorithmic_bytes_per_launch": b_units},
             "cpu_baseline": None, "e2e": None,
-            "gpu_launches": None,
+            "gpu_launches": launches,
             "clocks": sampler.summary(),
             "time_to_max_matching_ms": t_ms, "cardinality": cards[-1] if cards else res.cardinality,
             "phases": res.phases, "bfs_levels": res.levels, "records_exchanged": res.records_exchanged,

@@ -267,6 +267,7 @@ bm_status   bm_part_cardinality(bm_part* pt, int64_t* cardinality);
 bm_status   bm_part_stats(bm_part* pt, int64_t* edges_traversed, int64_t* columns_scanned, int64_t* walks,
                           int64_t* walk_steps, int64_t* fix_resets);
 bm_status   bm_part_reset_stats(bm_part* pt);
+bm_status   bm_part_launch_count(bm_part* pt, int64_t* launches);  /* kernels since the last reset */
 
 /* ---- host utilities (not on the hot path) -------------------------------- */
 /* First-fit greedy in ascending column order; restates matching.cpp:13-26. */

@@ -43,8 +43,10 @@ class CpuPartition:
         self.st[:] = 0
 
     def stats(self):
-        return dict(zip(["edges_traversed", "columns_scanned", "walks", "walk_steps", "fix_resets"],
-                        (int(x) for x in self.st)))
+        d = dict(zip(["edges_traversed", "columns_scanned", "walks", "walk_steps", "fix_resets"],
+                     (int(x) for x in self.st)))
+        d["launches"] = 0  # no device kernels in the CPU restatement
+        return d
 
     def state(self):
         return self.rmatch, self.cmatch

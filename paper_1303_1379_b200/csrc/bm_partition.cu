@@ -426,6 +426,7 @@ struct bm_part {
   unsigned long long* stats = nullptr;    // trav, cexp, walks, steps, resets, live, matched
   int ep_one = 1, wr = 1;
   int n_cur = 0;
+  long long launches = 0;  // kernels launched since the last bm_part_reset_stats
   long long cap_claims = 0;
 };
 
@@ -630,7 +631,10 @@ bm_status bm_part_begin_phase(bm_part* pt, int32_t bfs_kernel, int32_t endpoint_
   PCUDA(cudaMemsetAsync(pt->cnt, 0, sizeof(int) * 64, pt->stream));
   PCUDA(cudaMemsetAsync(pt->dead, 0, sizeof(unsigned) * ((pt->nc + 31) / 32 + 1), pt->stream));
   const int ncl = pt->col_hi - pt->col_lo;
-  if (ncl > 0) part_roots_kernel<<<blocks_for(pt, ncl), kThr, 0, pt->stream>>>(dev_of(pt), pt->F[0], pt->cnt);
+  if (ncl > 0) {
+    part_roots_kernel<<<blocks_for(pt, ncl), kThr, 0, pt->stream>>>(dev_of(pt), pt->F[0], pt->cnt);
+    pt->launches++;
+  }
   PCUDA(cudaGetLastError());
   int n = 0;
   PCUDA(cudaMemcpyAsync(&n, pt->cnt, sizeof(int), cudaMemcpyDeviceToHost, pt->stream));
@@ -651,9 +655,11 @@ bm_status bm_part_expand(bm_part* pt, void* claims_out, void* endpoints_out, int
     part_expand_kernel<<<blocks_for(pt, (long long)pt->n_cur * kGroup), kThr, 0, pt->stream>>>(
         dev_of(pt), pt->F[pt->cur], pt->n_cur, static_cast<int4*>(claims_out), pt->cnt + 2,
         static_cast<int4*>(endpoints_out), pt->cnt + 3, pt->stats, pt->huge, pt->cnt + 63);
+    pt->launches++;
     part_expand_huge_kernel<<<pt->sms * 4, kThr, 0, pt->stream>>>(
         dev_of(pt), pt->F[pt->cur], pt->huge, pt->cnt + 63, static_cast<int4*>(claims_out), pt->cnt + 2,
         static_cast<int4*>(endpoints_out), pt->cnt + 3, pt->stats);
+    pt->launches++;
   }
   PCUDA(cudaGetLastError());
   int c[2] = {0, 0};
@@ -691,13 +697,18 @@ bm_status bm_part_merge(bm_part* pt, const void* claims_all, const int32_t* clai
   if (te > 0) {
     const int b = blocks_for(pt, te);
     part_ep_root_kernel<<<b, kThr, 0, pt->stream>>>(d, ge);
+    pt->launches++;
     part_ep_row_kernel<<<b, kThr, 0, pt->stream>>>(d, ge);
+    pt->launches++;
     part_ep_apply_kernel<<<b, kThr, 0, pt->stream>>>(d, ge, pt->ep_list, pt->cnt + 4, pt->rank == 0, pt->cnt + 5);
+    pt->launches++;
   }
   if (tc > 0) {
     const int b = blocks_for(pt, tc);
     part_claim_min_kernel<<<b, kThr, 0, pt->stream>>>(d, gc);
+    pt->launches++;
     part_claim_apply_kernel<<<b, kThr, 0, pt->stream>>>(d, gc, pt->F[pt->cur ^ 1], pt->cnt + 1, pt->stats + 5);
+    pt->launches++;
   }
   PCUDA(cudaGetLastError());
   int nxt[5] = {0, 0, 0, 0, 0};
@@ -717,6 +728,7 @@ bm_status bm_part_end_bfs(bm_part* pt) {
   if (s != BM_OK) return s;
   PCUDA(cudaSetDevice(pt->device));
   part_sweep_kernel<<<blocks_for(pt, pt->nr), kThr, 0, pt->stream>>>(pt->rmatch, pt->nr);
+  pt->launches++;
   PCUDA(cudaGetLastError());
   PCUDA(cudaStreamSynchronize(pt->stream));
   return BM_OK;
@@ -734,9 +746,12 @@ bm_status bm_part_augment(bm_part* pt, int32_t serial, int64_t* cardinality) {
   if (n_ep > 0)
     part_alternate_kernel<<<serial ? 1 : blocks_for(pt, n_ep), serial ? 32 : kThr, 0, pt->stream>>>(
         d, pt->ep_list, n_ep, serial, pt->stats);
+    pt->launches++;
   part_fix_rows_kernel<<<blocks_for(pt, pt->nr), kThr, 0, pt->stream>>>(d, pt->stats);
+  pt->launches++;
   PCUDA(cudaMemsetAsync(pt->stats + 6, 0, sizeof(unsigned long long), pt->stream));
   part_fix_cols_kernel<<<blocks_for(pt, pt->nc), kThr, 0, pt->stream>>>(d, pt->stats, pt->stats + 6);
+  pt->launches++;
   PCUDA(cudaGetLastError());
   unsigned long long m = 0;
   PCUDA(cudaMemcpyAsync(&m, pt->stats + 6, sizeof(m), cudaMemcpyDeviceToHost, pt->stream));
@@ -751,6 +766,7 @@ bm_status bm_part_cardinality(bm_part* pt, int64_t* cardinality) {
   PCUDA(cudaSetDevice(pt->device));
   PCUDA(cudaMemsetAsync(pt->stats + 7, 0, sizeof(unsigned long long), pt->stream));
   part_count_kernel<<<blocks_for(pt, pt->nr), kThr, 0, pt->stream>>>(pt->rmatch, pt->nr, pt->stats + 7);
+  pt->launches++;
   PCUDA(cudaGetLastError());
   unsigned long long m = 0;
   PCUDA(cudaMemcpyAsync(&m, pt->stats + 7, sizeof(m), cudaMemcpyDeviceToHost, pt->stream));
@@ -774,8 +790,15 @@ bm_status bm_part_stats(bm_part* pt, int64_t* edges_traversed, int64_t* columns_
   return BM_OK;
 }
 
+bm_status bm_part_launch_count(bm_part* pt, int64_t* launches) {
+  if (!pt) return pfail(BM_ERR_INVALID_ARG, "null partition handle");
+  if (launches) *launches = pt->launches;
+  return BM_OK;
+}
+
 bm_status bm_part_reset_stats(bm_part* pt) {
   if (!pt) return pfail(BM_ERR_INVALID_ARG, "null partition handle");
+  pt->launches = 0;
   PCUDA(cudaSetDevice(pt->device));
   PCUDA(cudaMemsetAsync(pt->stats, 0, sizeof(unsigned long long) * 8, pt->stream));
   return BM_OK;

@@ -52,6 +52,7 @@ _PART_PROTOS = {
     "bm_part_cardinality": (C.c_int, [_vp, _i64p]),
     "bm_part_stats": (C.c_int, [_vp, _i64p, _i64p, _i64p, _i64p, _i64p]),
     "bm_part_reset_stats": (C.c_int, [_vp]),
+    "bm_part_launch_count": (C.c_int, [_vp, _i64p]),
 }
 for _name, (_res, _args) in _PART_PROTOS.items():
     _fn = getattr(lib, _name)
@@ -205,7 +206,11 @@ class GpuPartition:
         v = [C.c_int64() for _ in range(5)]
         check(lib.bm_part_stats(self._h, *[C.byref(x) for x in v]))
         keys = ["edges_traversed", "columns_scanned", "walks", "walk_steps", "fix_resets"]
-        return {k: x.value for k, x in zip(keys, v)}
+        out = {k: x.value for k, x in zip(keys, v)}
+        n = C.c_int64()
+        check(lib.bm_part_launch_count(self._h, C.byref(n)))
+        out["launches"] = n.value
+        return out
 
     def reset_stats(self):
         check(lib.bm_part_reset_stats(self._h))
