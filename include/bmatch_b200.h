@@ -27,6 +27,13 @@
  * The message of the last failure on the calling thread is bm_last_error().
  * There is no CPU fallback: without a usable sm_100 device every compute
  * entry point fails with BM_ERR_CUDA.
+ *
+ * Tuning environment variables (read at upload / launch; defaults are the
+ * measured best): BM_ROW_LAYOUT=plain|interleave (row-state
+ * layout, default by rmatch size), BM_BU_FRAC (share of the edges a frontier
+ * must hold to be pulled when bottom_up is set, default 0.45), BM_SOLO_EDGES
+ * (widest level run by one CTA, default 4096), BM_PERSIST_MB (L2 persisting
+ * window on the row state, default off).
  */
 #ifndef BMATCH_B200_H
 #define BMATCH_B200_H

@@ -42,6 +42,11 @@ def test_no_cpu_fallback_without_gpu():
     assert b"no CUDA device" in _lib.lib.bm_last_error()
     with pytest.raises(bm.CudaError):
         bm.Engine(0)
+    # the multi-GPU partition handle refuses as well
+    from paper_1303_1379_b200 import partition
+    st = partition.lib.bm_part_create(0, 0, 2, C.byref(h))
+    assert st == _lib.BM_ERR_CUDA
+    assert partition.lib.bm_part_create(0, 3, 2, C.byref(h)) == _lib.BM_ERR_INVALID_ARG  # rank out of range
 
 
 def test_null_handle_errors():
