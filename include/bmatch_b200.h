@@ -32,7 +32,7 @@
  * measured best): BM_ROW_LAYOUT=plain|interleave (row-state
  * layout, default by rmatch size), BM_BU_FRAC (share of the edges a frontier
  * must hold to be pulled when bottom_up is set, default 0.45), BM_SOLO_EDGES
- * (widest level run by one CTA, default 4096), BM_PERSIST_MB (L2 persisting
+ * (widest level run by one CTA, default 1024), BM_PERSIST_MB (L2 persisting
  * window on the row state, default off).
  */
 #ifndef BMATCH_B200_H

@@ -76,13 +76,16 @@ constexpr int kThreads = BM_THREADS;  // threads per CTA (1024 / kThreads CTAs p
 #endif
 constexpr int kItems = BM_ITEMS;      // edges per thread per round (memory-level parallelism)
 constexpr unsigned kGran = 512;       // edges per granule-index entry; tiles are whole granules
-constexpr unsigned kMaxTileGran = 8;  // <= 4096 edges per tile (= the winner buffer)
+#ifndef BM_TILE_GRAN
+#define BM_TILE_GRAN 8
+#endif
+constexpr unsigned kMaxTileGran = BM_TILE_GRAN;  // <= 4096 edges per tile (= the winner buffer)
 constexpr unsigned kWBuf = kGran * kMaxTileGran;
 #ifndef BM_INTERLEAVE_MB
 #define BM_INTERLEAVE_MB 72  // interleave {mate, pred} when the plain rmatch exceeds this many MB
 #endif
 #ifndef BM_SOLO_EDGES
-#define BM_SOLO_EDGES 4096
+#define BM_SOLO_EDGES 1024
 #endif
 constexpr unsigned kSoloEdges = BM_SOLO_EDGES;  // widest level block 0 expands alone
 constexpr int kStartLevel = 2;        // L0 (gpu_match.cpp:275)
