@@ -33,8 +33,9 @@ REF_INC   := -I$(NLOHMANN)
 endif
 REF_LIB   := oracle/_ref/libbmatch_ref.so
 SHIM_TEST := oracle/_ref/shim_test
+SUITE     := oracle/_ref/b200_suite
 
-.PHONY: all ref shimtest clean
+.PHONY: all ref shimtest suite clean
 all: $(LIB) $(ORACLE)
 
 $(BUILD):
@@ -69,6 +70,14 @@ shimtest: $(SHIM_TEST)
 $(SHIM_TEST): tests/cpp/shim_test.cpp include/bmatch_b200.hpp include/bmatch_b200.h $(REF_LIB) $(LIB)
 	$(CXX) -std=c++20 -O2 -Wall -Wextra -pthread -I$(REF_ROOT)/include $(REF_INC) -Iinclude \
 	    -o $@ tests/cpp/shim_test.cpp $(REF_LIB) $(LIB) \
+	    -Wl,-rpath,'$$ORIGIN' -Wl,-rpath,'$$ORIGIN/../../paper_1303_1379_b200'
+
+# The paper's evaluation artefacts through the reference's run_suite (tools/b200_suite.cpp).
+suite: $(SUITE)
+
+$(SUITE): tools/b200_suite.cpp include/bmatch_b200.hpp include/bmatch_b200.h include/bmatch_b200_gen.h $(REF_LIB) $(LIB)
+	$(CXX) -std=c++20 -O2 -Wall -Wextra -pthread -I$(REF_ROOT)/include $(REF_INC) -Iinclude \
+	    -o $@ tools/b200_suite.cpp $(REF_LIB) $(LIB) \
 	    -Wl,-rpath,'$$ORIGIN' -Wl,-rpath,'$$ORIGIN/../../paper_1303_1379_b200'
 
 clean:
