@@ -20,18 +20,24 @@
 // B200 design (not a translation of the reference's host loops):
 //   * Frontier queues instead of an O(nc) level test per launch
 //     (gpu_match.cpp:48/105). A level is a run of 16-byte entries
-//     {col, root, adj_begin, edge_prefix}; one packed 64-bit atomicAdd per warp
-//     ((count<<33)|edges) hands out slots AND the level-local edge prefix, so
-//     the next level is cut into equal *edge* tiles whatever the degree skew.
+//     {col, root, adj_begin, edge_prefix}; one packed 64-bit atomicAdd per CTA
+//     flush ((count<<33)|edges) hands out slots AND the level-local edge
+//     prefix, so the next level is cut into equal *edge* tiles whatever the
+//     degree skew.
 //     While pushing, each entry also records itself in a granule index (one
 //     u32 per kGran edges), so a tile finds its first entry with one load.
 //   * "Unvisited" is one bit (bit 30) of the column's mate entry in rmatch,
 //     claimed with atomicOr: the rmatch[row] gather every traversed edge makes
 //     anyway also answers the visited test, instead of a bfs_array gather.
-//   * WR: a tree whose root already found a path stops claiming columns at
-//     discovery time, not only at expansion (gpu_match.cpp:106-108), leaving
-//     them to live trees. Correctness never depends on it (ALTERNATE's claim
-//     check + FIX do).
+//   * WR: the early-exit test (gpu_match.cpp:106-108) reads a 1-bit-per-root
+//     "dead" bitmap (L2-resident) instead of bfs_array[root]; a tree holds at
+//     most one free row (bm_endpoint_policy ONE_PER_TREE, CAS on its root
+//     mark), which leaves the other free rows to other trees. Correctness
+//     never depends on either (ALTERNATE's claim check + FIX do).
+//   * Row state: the mate and the visited bit share a word; above 72 MB the
+//     predecessor joins them in one 8-byte slot (see RM / PR).
+//   * Optional pulled (bottom-up) dense levels: bu_prep / bu_sweep, compiled
+//     into separate kernel instances (driver_kernel<..., BU=true>).
 //   * FIXMATCHING touches only what ALTERNATE wrote. Every walk step writes
 //     rmatch[row] = pred[row] and cmatch[pred[row]] = row, and logs the pair;
 //     the only other entries that can become inconsistent are the pending
@@ -43,7 +49,8 @@
 //     mate of a claimed column, or a row a walk wrote this phase), all of which
 //     were written in this phase's BFS.
 //   * The next phase's roots come from this phase's roots plus columns FIX
-//     unmatched; nothing is O(nc) per phase except the 1-bit bitmap clear.
+//     unmatched; nothing is O(nc) per phase except the dead-root bitmap clear
+//     and the visited-bit sweep over rmatch.
 #include <algorithm>
 #include <cstdlib>
 #include <cstdint>
