@@ -383,6 +383,7 @@ def run_b200(args):
     torch.cuda.synchronize(dev)
     step_ms, kern_ms, launches, cards = [], [], 0, []
     counters = None
+    step_counters = []  # per timed step: the roofline uses the mean work over the same steps as the mean time
     sampler = ClockSampler(local)
     wall0 = time.perf_counter()
     with sampler:
@@ -395,6 +396,7 @@ def run_b200(args):
             e1.record(stream)
             e1.synchronize()
             step_ms.append(e0.elapsed_time(e1))
+            step_counters.append(counters)
             kms, nl = eng.last_kernel_time()
             kern_ms.append(kms)
             launches += nl
@@ -474,9 +476,14 @@ def run_b200(args):
     # ---- roofline of the driver kernel (SURVEY.md §8d per-unit bytes) ----
     wr = 1 if kernel == bm.BfsKernel.GpubfsWr else 0
     c = counters
-    b_units = (12 * c.edges_traversed + (20 + 8 * wr) * c.columns_scanned + (8 + 4 * wr) * c.columns_visited
-               + 20 * c.walk_steps)
-    b_survey = b_units + c.outer_iterations * (12 * g.nc + 4 * g.nr + 4 * g.nr + 8 * g.nr + 8 * g.nc)
+    nst = max(1, len(step_counters))
+
+    def mean_of(attr):  # mean over the timed steps (phase counts differ from run to run)
+        return sum(getattr(x, attr) for x in step_counters) / nst
+
+    b_units = (12 * mean_of("edges_traversed") + (20 + 8 * wr) * mean_of("columns_scanned")
+               + (8 + 4 * wr) * mean_of("columns_visited") + 20 * mean_of("walk_steps"))
+    b_survey = b_units + mean_of("outer_iterations") * (12 * g.nc + 4 * g.nr + 4 * g.nr + 8 * g.nr + 8 * g.nc)
     peak, peak_src = measured_peak()
     achieved = b_units / (k_ms / 1e3) / 1e9
     traffic = None
@@ -517,10 +524,12 @@ def run_b200(args):
             "clocks": sampler.summary(),
             "time_to_max_matching_ms": t_ms,
             "kernel_ms": k_ms,
-            "teps": c.edges_traversed / (k_ms / 1e3),
+            "teps": mean_of("edges_traversed") / (k_ms / 1e3),
             "cardinality": cards[-1],
             "parity": {"known_answer": known, "gpu_verify_violations": viol, "gpu_is_maximum": ismax,
                        "ok": bool(parity_ok)},
+            "counters_mean": {k: mean_of(k) for k in ["outer_iterations", "columns_scanned", "edges_traversed",
+                                                       "columns_visited", "walk_steps"]},
             "counters": {"outer_iterations": c.outer_iterations, "bfs_levels": c.bfs_launches_total(),
                          "columns_scanned": c.columns_scanned, "edges_traversed": c.edges_traversed,
                          "columns_visited": c.columns_visited, "walks": c.alternations_attempted,
