@@ -163,8 +163,25 @@ def dist_env():
     return world, rank, local
 
 
+_JSON_FD = None  # set while library banners (NCCL) are diverted away from stdout
+
+
 def emit(obj):
-    print(json.dumps(obj), flush=True)
+    line = json.dumps(obj) + "\n"
+    if _JSON_FD is not None:
+        os.write(_JSON_FD, line.encode())
+    else:
+        print(line, end="", flush=True)
+
+
+def divert_stdout():
+    """Route fd 1 to stderr for the rest of the run (NCCL prints its version banner
+    on stdout when its communicator is created); emit() keeps the real stdout."""
+    global _JSON_FD
+    if _JSON_FD is None:
+        sys.stdout.flush()
+        _JSON_FD = os.dup(1)
+        os.dup2(2, 1)
 
 
 _REF_CACHE = {}
@@ -232,10 +249,11 @@ def run_partitioned(args):
     from paper_1303_1379_b200.partition import Exchange, GpuPartition, PartitionedMatcher
 
     world, rank, local = dist_env()
+    divert_stdout()
     local = local % max(1, torch.cuda.device_count())  # gloo tests run several ranks on one GPU
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    backend = "nccl" if args.exchange == "nccl" else "gloo"
+    backend = "gloo" if args.exchange == "gloo" else "nccl"
     if not dist.is_initialized():
         if world == 1:
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
@@ -251,7 +269,16 @@ def run_partitioned(args):
     shortest, kernel, improved = ALGOS[args.algo]
     be = GpuPartition(local, rank, world)
     pm = PartitionedMatcher(be, Exchange())
-    pm.upload(g)
+    exchange = args.exchange
+    if exchange == "p2p":  # fused exchange over peer memory; fall back to the NCCL all-gather if unavailable
+        try:
+            pm.upload(g, p2p=True)
+        except Exception as ex:  # e.g. no CUDA IPC in this container
+            print(f"P2P exchange unavailable ({ex}); using the NCCL all-gather", file=sys.stderr)
+            exchange = "nccl"
+            pm.upload(g)
+    else:
+        pm.upload(g)
     stream = torch.cuda.current_stream(dev)
 
     def step():
@@ -309,7 +336,9 @@ def run_partitioned(args):
                                    (f" (1/{args.scale_div} scale)" if args.scale_div != 1 else ""),
                        "algorithm": f"{args.algo}-b200-partitioned", "nc": g.nc, "nr": g.nr, "edges": E,
                        "init": "first-fit cheap_matching (host, not timed)",
-                       "parallelism": f"column-partition x{world}, per-level record all-gather ({backend})",
+                       "parallelism": f"column-partition x{world}, per-level record exchange: "
+                                      + ("fused P2P stores into every rank's receive slabs (CUDA IPC / NVLink)"
+                                         if exchange == "p2p" else f"all-gather ({backend})"),
                        "l2": "per-step working set exceeds L2 at C2+ scale; no explicit flush"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": None, "peak_source": peak_src,
@@ -336,6 +365,7 @@ def run_b200(args):
     world, rank, local = dist_env()
     if world > 1:
         import torch.distributed as dist
+        divert_stdout()
         torch.cuda.set_device(local)
         dist.init_process_group("nccl")
     else:
@@ -561,8 +591,9 @@ def main():
                     help="pull the dense BFS levels (direction-optimised; builds a row index once per graph)")
     ap.add_argument("--mode", choices=["auto", "single", "partition", "replicas"], default="auto",
                     help="auto: single GPU at N=1, column partition at N>1")
-    ap.add_argument("--exchange", choices=["nccl", "gloo"], default="nccl",
-                    help="partition mode: record exchange backend (gloo: host-staged, for 1-GPU tests)")
+    ap.add_argument("--exchange", choices=["p2p", "nccl", "gloo"], default="p2p",
+                    help="partition mode: p2p = the expand kernel writes every rank's receive slab over peer "
+                         "memory (falls back to nccl if IPC is unavailable); nccl = all-gather; gloo = host-staged")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "b200":
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)

@@ -276,6 +276,23 @@ bm_status   bm_part_stats(bm_part* pt, int64_t* edges_traversed, int64_t* column
 bm_status   bm_part_reset_stats(bm_part* pt);
 bm_status   bm_part_launch_count(bm_part* pt, int64_t* launches);  /* kernels since the last reset */
 
+/* Fused exchange over peer memory (NVLink, CUDA IPC) instead of the caller's
+ * all-gather: the expand kernel itself writes each record into every rank's
+ * receive slab and a signal kernel publishes the counts and bumps every rank's
+ * arrival counter; the merge waits for the arrivals on the device. No
+ * collective library call and no host synchronisation inside the exchange.
+ * Setup: bm_part_p2p_export (allocates the slabs: 2 level parities x world x
+ * cap records; cap >= any rank's records per level, e.g. min(nc, max rank E)
+ * for claims and min(nr, max rank E) for endpoints) returns 4 IPC handles
+ * (4 x 64 bytes); the caller all-gathers them (rank-major) and passes them
+ * to bm_part_p2p_import. Per level: bm_part_expand_p2p(parity = level & 1),
+ * then bm_part_merge_p2p(parity, arrivals = world * levels so far). */
+bm_status   bm_part_p2p_export(bm_part* pt, int64_t claims_cap, int64_t endpoints_cap, void* handles);
+bm_status   bm_part_p2p_import(bm_part* pt, const void* all_handles);
+bm_status   bm_part_expand_p2p(bm_part* pt, int32_t parity);
+bm_status   bm_part_merge_p2p(bm_part* pt, int32_t parity, uint32_t arrivals, int64_t* n_next_total,
+                              int32_t* found);
+
 /* ---- host utilities (not on the hot path) -------------------------------- */
 /* First-fit greedy in ascending column order; restates matching.cpp:13-26. */
 bm_status   bm_host_cheap_matching(int32_t nc, int32_t nr, const int64_t* cxadj,

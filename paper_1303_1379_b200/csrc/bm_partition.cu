@@ -34,6 +34,7 @@ namespace bmp {
 using namespace bm;
 
 constexpr int kVis = 1 << 30;  // visited flag in the mate's rmatch entry (as bm_engine.cu)
+constexpr int kMaxWorld = 8;   // ranks of one NVLink domain (P2P exchange)
 constexpr int kThr = 256;
 
 struct PartDev {
@@ -51,6 +52,12 @@ struct PartDev {
   unsigned long long* winE;  // nr
   unsigned stamp;            // merge counter of this handle
   int ep_one, wr;
+  // P2P exchange: records go straight into every rank's receive slabs (peer
+  // memory over NVLink, CUDA IPC); record k of sender s at [s * cap + k]
+  int p2p, rank, world;
+  long long ccap, ecap;
+  int4* peer_claims[kMaxWorld];
+  int4* peer_eps[kMaxWorld];
 };
 
 __device__ __forceinline__ unsigned long long win_key(const PartDev& d, long long i) {
@@ -106,15 +113,30 @@ struct PartSmem {
   int nc, ne, bc, be;
 };
 
-__device__ __forceinline__ void stage(int4* buf, int* n, int cap, int4* out, int* count, int4 rec) {
+__device__ __forceinline__ void stage(const PartDev& d, bool is_claim, int4* buf, int* n, int cap, int4* out,
+                                      int* count, int4 rec) {
   const unsigned m = __activemask();
   const int leader = __ffs(m) - 1;
   const int rank = __popc(m & ((1u << lane_id()) - 1));
   int base = 0;
   if ((int)lane_id() == leader) base = atomicAdd(n, __popc(m));
   base = __shfl_sync(m, base, leader) + rank;
-  if (base < cap) buf[base] = rec;
-  else append(out, count, rec);
+  if (base < cap) {
+    buf[base] = rec;
+  } else if (!d.p2p) {
+    append(out, count, rec);
+  } else {  // stage full: reserve in the rank's record list and write every rank's slab directly
+    const unsigned m2 = __activemask();
+    const int l2 = __ffs(m2) - 1;
+    const int r2 = __popc(m2 & ((1u << lane_id()) - 1));
+    int b2 = 0;
+    if ((int)lane_id() == l2) b2 = atomicAdd(count, __popc(m2));
+    b2 = __shfl_sync(m2, b2, l2) + r2;
+    for (int r = 0; r < d.world; ++r) {
+      if (is_claim) d.peer_claims[r][(long long)d.rank * d.ccap + b2] = rec;
+      else d.peer_eps[r][(long long)d.rank * d.ecap + b2] = rec;
+    }
+  }
 }
 
 __device__ __forceinline__ void part_edge(const PartDev& d, PartSmem& sm, int row, int c, int root, int4* claims,
@@ -122,15 +144,17 @@ __device__ __forceinline__ void part_edge(const PartDev& d, PartSmem& sm, int ro
   const int cm = ld_rlx(d.rmatch + row);
   if (cm >= 0) {
     if (!(cm & kVis) && !(atomicOr(d.rmatch + row, kVis) & kVis))
-      stage(sm.c, &sm.nc, kStageC, claims, n_claims, make_int4(cm, c, root, row));
+      stage(d, true, sm.c, &sm.nc, kStageC, claims, n_claims, make_int4(cm, c, root, row));
   } else if (cm == -1) {
     if (d.ep_one && dead_root(d, root)) return;
-    if (atomicCAS(d.rmatch + row, -1, -2) == -1) stage(sm.e, &sm.ne, kStageE, eps, n_eps, make_int4(row, c, root, 0));
+    if (atomicCAS(d.rmatch + row, -1, -2) == -1)
+      stage(d, false, sm.e, &sm.ne, kStageE, eps, n_eps, make_int4(row, c, root, 0));
   }
 }
 
 // Copies the CTA's staged records to the global record arrays (CTA-uniform call).
-__device__ __forceinline__ void flush_stage(PartSmem& sm, int4* claims, int* n_claims, int4* eps, int* n_eps) {
+__device__ __forceinline__ void flush_stage(const PartDev& d, PartSmem& sm, int4* claims, int* n_claims, int4* eps,
+                                            int* n_eps) {
   __syncthreads();
   const int nc = min(sm.nc, kStageC), ne = min(sm.ne, kStageE);
   if (threadIdx.x == 0) {
@@ -138,8 +162,17 @@ __device__ __forceinline__ void flush_stage(PartSmem& sm, int4* claims, int* n_c
     sm.be = ne ? atomicAdd(n_eps, ne) : 0;
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < nc; i += blockDim.x) claims[sm.bc + i] = sm.c[i];
-  for (int i = threadIdx.x; i < ne; i += blockDim.x) eps[sm.be + i] = sm.e[i];
+  if (d.p2p) {  // the fused exchange: every rank's slab for this sender, over NVLink
+    for (int r = 0; r < d.world; ++r) {
+      int4* pc = d.peer_claims[r] + (long long)d.rank * d.ccap + sm.bc;
+      int4* pe = d.peer_eps[r] + (long long)d.rank * d.ecap + sm.be;
+      for (int i = threadIdx.x; i < nc; i += blockDim.x) pc[i] = sm.c[i];
+      for (int i = threadIdx.x; i < ne; i += blockDim.x) pe[i] = sm.e[i];
+    }
+  } else {
+    for (int i = threadIdx.x; i < nc; i += blockDim.x) claims[sm.bc + i] = sm.c[i];
+    for (int i = threadIdx.x; i < ne; i += blockDim.x) eps[sm.be + i] = sm.e[i];
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
     sm.nc = 0;
@@ -195,7 +228,7 @@ __global__ void __launch_bounds__(kThr) part_expand_kernel(PartDev d, const int2
         part_edge(d, sm, d.adj[j], bc, br, claims, n_claims, eps, n_eps);
     }
     (void)grp;
-    flush_stage(sm, claims, n_claims, eps, n_eps);
+    flush_stage(d, sm, claims, n_claims, eps, n_eps);
   }
   trav = warp_sum(trav);
   cexp = warp_sum(cexp);
@@ -231,7 +264,7 @@ __global__ void __launch_bounds__(kThr) part_expand_huge_kernel(PartDev d, const
     for (unsigned long long base = b + (unsigned long long)blockIdx.x * blockDim.x; base < e; base += gt) {
       const unsigned long long j = base + threadIdx.x;
       if (j < e) part_edge(d, sm, d.adj[j], c, root, claims, n_claims, eps, n_eps);
-      flush_stage(sm, claims, n_claims, eps, n_eps);
+      flush_stage(d, sm, claims, n_claims, eps, n_eps);
     }
   }
   trav = warp_sum(trav);
@@ -246,43 +279,58 @@ __global__ void __launch_bounds__(kThr) part_expand_huge_kernel(PartDev d, const
 // and has the global key r*stride + k (its order). Lower key wins.
 struct Gathered {
   const int4* rec;
-  const int* counts;  // device copy of the per-rank counts
+  const int* counts;  // device per-rank counts
   long long stride;
   int world;
 };
 
-__device__ __forceinline__ bool rec_at(const Gathered& g, long long i, int4& r) {
-  const int rank = (int)(i / g.stride);
-  const long long k = i - (long long)rank * g.stride;
-  if (rank >= g.world || k >= g.counts[rank]) return false;
-  r = g.rec[i];
-  return true;
+// The t-th valid record (ranks in order, k < counts[rank]) -> its global key
+// i = rank * stride + k and the record; false past the last one.
+__device__ __forceinline__ bool rec_at(const Gathered& g, long long t, long long& i, int4& r) {
+  for (int rank = 0; rank < g.world; ++rank) {
+    const long long c = g.counts[rank];
+    if (t < c) {
+      i = (long long)rank * g.stride + t;
+      r = g.rec[i];
+      return true;
+    }
+    t -= c;
+  }
+  return false;
+}
+__device__ __forceinline__ long long rec_total(const Gathered& g) {
+  long long s = 0;
+  for (int rank = 0; rank < g.world; ++rank) s += g.counts[rank];
+  return s;
 }
 
 // Endpoints, step 1 (ONE_PER_TREE): lowest record per live root.
 __global__ void part_ep_root_kernel(PartDev d, Gathered g) {
-  const long long tot = (long long)g.world * g.stride;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < tot; i += (long long)gridDim.x * blockDim.x) {
+  const long long tot = rec_total(g);
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < tot; t += (long long)gridDim.x * blockDim.x) {
     int4 r;
-    if (!rec_at(g, i, r)) continue;
+    long long i;
+    if (!rec_at(g, t, i, r)) continue;
     if (d.ep_one && !dead_root(d, r.z)) atomicMin(d.winR + r.z, win_key(d, i));
   }
 }
 // Step 2: lowest surviving record per row.
 __global__ void part_ep_row_kernel(PartDev d, Gathered g) {
-  const long long tot = (long long)g.world * g.stride;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < tot; i += (long long)gridDim.x * blockDim.x) {
+  const long long tot = rec_total(g);
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < tot; t += (long long)gridDim.x * blockDim.x) {
     int4 r;
-    if (!rec_at(g, i, r)) continue;
+    long long i;
+    if (!rec_at(g, t, i, r)) continue;
     if (d.ep_one ? (d.winR[r.z] == win_key(d, i)) : true) atomicMin(d.winE + r.x, win_key(d, i));
   }
 }
 // Step 3: winners become endpoints everywhere; a row no record won goes back to -1.
 __global__ void part_ep_apply_kernel(PartDev d, Gathered g, int* ep_list, int* n_ep, int keep_list, int* found) {
-  const long long tot = (long long)g.world * g.stride;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < tot; i += (long long)gridDim.x * blockDim.x) {
+  const long long tot = rec_total(g);
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < tot; t += (long long)gridDim.x * blockDim.x) {
     int4 r;
-    if (!rec_at(g, i, r)) continue;
+    long long i;
+    if (!rec_at(g, t, i, r)) continue;
     const unsigned long long w = d.winE[r.x];
     if (w == win_key(d, i)) {
       d.rmatch[r.x] = -2;
@@ -299,19 +347,21 @@ __global__ void part_ep_apply_kernel(PartDev d, Gathered g, int* ep_list, int* n
 // pred[row] on every rank, and the owner of the column queues it (unless its
 // tree found a path at this level).
 __global__ void part_claim_min_kernel(PartDev d, Gathered g) {
-  const long long tot = (long long)g.world * g.stride;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < tot; i += (long long)gridDim.x * blockDim.x) {
+  const long long tot = rec_total(g);
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < tot; t += (long long)gridDim.x * blockDim.x) {
     int4 r;
-    if (!rec_at(g, i, r)) continue;
+    long long i;
+    if (!rec_at(g, t, i, r)) continue;
     atomicMin(d.winC + r.x, win_key(d, i));
   }
 }
 __global__ void part_claim_apply_kernel(PartDev d, Gathered g, int2* Fn, int* nFn, unsigned long long* n_live) {
-  const long long tot = (long long)g.world * g.stride;
+  const long long tot = rec_total(g);
   unsigned long long live = 0;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < tot; i += (long long)gridDim.x * blockDim.x) {
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < tot; t += (long long)gridDim.x * blockDim.x) {
     int4 r;
-    if (!rec_at(g, i, r)) continue;
+    long long i;
+    if (!rec_at(g, t, i, r)) continue;
     if (d.winC[r.x] != win_key(d, i)) continue;
     d.rmatch[r.w] = r.x | kVis;
     d.pred[r.w] = r.y;
@@ -322,6 +372,37 @@ __global__ void part_claim_apply_kernel(PartDev d, Gathered g, int2* Fn, int* nF
   live = warp_sum(live);
   if (lane_id() == 0 && live) atomicAdd(n_live, live);
 }
+// P2P exchange: after this rank's expand, publish its record counts in every
+// rank's count table and bump every rank's arrival counter (system-scope
+// release: the records and counts are visible before the arrival).
+__global__ void part_signal_kernel(const int* n_claims, const int* n_eps, int* const* peer_counts,
+                                   unsigned* const* peer_flags, int rank, int world, int parity) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const int c = *n_claims, e = *n_eps;
+  for (int r = 0; r < world; ++r) {
+    peer_counts[r][parity * 2 * kMaxWorld + rank] = c;
+    peer_counts[r][parity * 2 * kMaxWorld + kMaxWorld + rank] = e;
+  }
+  __threadfence_system();
+  for (int r = 0; r < world; ++r) atomicAdd_system(peer_flags[r], 1u);
+}
+// Waits until every rank has signalled this level (arrivals >= target).
+__global__ void part_wait_kernel(const unsigned* flag, unsigned target, int* timeout) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const long long t0 = clock64();
+  for (;;) {
+    unsigned v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+    if ((int)(v - target) >= 0) break;
+    __nanosleep(256);
+    if (clock64() - t0 > (1ll << 38)) {  // ~140 s: a peer is gone
+      *timeout = 1;
+      break;
+    }
+  }
+  __threadfence_system();
+}
+
 __global__ void part_sweep_kernel(int* rmatch, int nr) {
   for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < nr; r += (long long)gridDim.x * blockDim.x) {
     const int v = rmatch[r];
@@ -428,6 +509,19 @@ struct bm_part {
   int n_cur = 0;
   long long launches = 0;  // kernels launched since the last bm_part_reset_stats
   long long cap_claims = 0;
+  // P2P exchange (bm_part_p2p_*): receive slabs by level parity, count table, arrival counter
+  bool p2p = false;
+  long long ccap = 0, ecap = 0;
+  int4* recv_claims = nullptr;  // 2 parities x world x ccap
+  int4* recv_eps = nullptr;     // 2 parities x world x ecap
+  int* recv_counts = nullptr;   // [parity][claims | eps][kMaxWorld]
+  unsigned* flag = nullptr;     // arrivals of every rank's signal
+  int* timeout = nullptr;
+  int4* peer_claims[kMaxWorld] = {};
+  int4* peer_eps[kMaxWorld] = {};
+  int** dpeer_counts = nullptr;       // device copies of the peers' count tables / counters
+  unsigned** dpeer_flags = nullptr;
+  void* opened[kMaxWorld][4] = {};    // IPC mappings to close
 };
 
 namespace {
@@ -450,8 +544,19 @@ void pfree(T*& p) {
   p = nullptr;
 }
 
-PartDev dev_of(const bm_part* pt) {
+PartDev dev_of(const bm_part* pt, int parity = -1) {
   PartDev d{};
+  if (parity >= 0 && pt->p2p) {
+    d.p2p = 1;
+    d.rank = pt->rank;
+    d.world = pt->world;
+    d.ccap = pt->ccap;
+    d.ecap = pt->ecap;
+    for (int r = 0; r < pt->world; ++r) {
+      d.peer_claims[r] = pt->peer_claims[r] + (long long)parity * pt->world * pt->ccap;
+      d.peer_eps[r] = pt->peer_eps[r] + (long long)parity * pt->world * pt->ecap;
+    }
+  }
   d.nc = pt->nc;
   d.nr = pt->nr;
   d.col_lo = pt->col_lo;
@@ -534,6 +639,16 @@ bm_status bm_part_destroy(bm_part* pt) {
   pfree(pt->huge);
   pfree(pt->cnt);
   pfree(pt->stats);
+  for (int r = 0; r < kMaxWorld; ++r)
+    for (int k = 0; k < 4; ++k)
+      if (pt->opened[r][k]) cudaIpcCloseMemHandle(pt->opened[r][k]);
+  pfree(pt->recv_claims);
+  pfree(pt->recv_eps);
+  pfree(pt->recv_counts);
+  pfree(pt->flag);
+  pfree(pt->timeout);
+  pfree(pt->dpeer_counts);
+  pfree(pt->dpeer_flags);
   if (pt->own) cudaStreamDestroy(pt->own);
   delete pt;
   return BM_OK;
@@ -787,6 +902,143 @@ bm_status bm_part_stats(bm_part* pt, int64_t* edges_traversed, int64_t* columns_
   if (walks) *walks = (int64_t)st[2];
   if (walk_steps) *walk_steps = (int64_t)st[3];
   if (fix_resets) *fix_resets = (int64_t)st[4];
+  return BM_OK;
+}
+
+bm_status bm_part_p2p_export(bm_part* pt, int64_t ccap, int64_t ecap, void* handles) {
+  bm_status s = ready(pt, true);
+  if (s != BM_OK) return s;
+  if (pt->world > kMaxWorld) return pfail(BM_ERR_INVALID_ARG, "P2P exchange supports up to 8 ranks");
+  if (ccap < 1 || ecap < 1 || !handles) return pfail(BM_ERR_INVALID_ARG, "bad P2P capacities");
+  PCUDA(cudaSetDevice(pt->device));
+  for (int r = 0; r < kMaxWorld; ++r)
+    for (int k = 0; k < 4; ++k)
+      if (pt->opened[r][k]) {
+        cudaIpcCloseMemHandle(pt->opened[r][k]);
+        pt->opened[r][k] = nullptr;
+      }
+  pt->p2p = false;
+  pfree(pt->recv_claims);
+  pfree(pt->recv_eps);
+  pfree(pt->recv_counts);
+  pfree(pt->flag);
+  pfree(pt->timeout);
+  pt->ccap = ccap;
+  pt->ecap = ecap;
+  PCUDA(cudaMalloc(&pt->recv_claims, sizeof(int4) * 2 * pt->world * ccap));
+  PCUDA(cudaMalloc(&pt->recv_eps, sizeof(int4) * 2 * pt->world * ecap));
+  PCUDA(cudaMalloc(&pt->recv_counts, sizeof(int) * 4 * kMaxWorld));
+  PCUDA(cudaMalloc(&pt->flag, sizeof(unsigned)));
+  PCUDA(cudaMalloc(&pt->timeout, sizeof(int)));
+  PCUDA(cudaMemset(pt->recv_counts, 0, sizeof(int) * 4 * kMaxWorld));
+  PCUDA(cudaMemset(pt->flag, 0, sizeof(unsigned)));
+  PCUDA(cudaMemset(pt->timeout, 0, sizeof(int)));
+  cudaIpcMemHandle_t* h = static_cast<cudaIpcMemHandle_t*>(handles);
+  PCUDA(cudaIpcGetMemHandle(&h[0], pt->recv_claims));
+  PCUDA(cudaIpcGetMemHandle(&h[1], pt->recv_eps));
+  PCUDA(cudaIpcGetMemHandle(&h[2], pt->recv_counts));
+  PCUDA(cudaIpcGetMemHandle(&h[3], pt->flag));
+  return BM_OK;
+}
+
+bm_status bm_part_p2p_import(bm_part* pt, const void* all_handles) {
+  bm_status s = ready(pt, true);
+  if (s != BM_OK) return s;
+  if (!pt->recv_claims || !all_handles) return pfail(BM_ERR_INVALID_ARG, "call bm_part_p2p_export first");
+  PCUDA(cudaSetDevice(pt->device));
+  for (int r = 0; r < kMaxWorld; ++r)  // mappings of an earlier setup (e.g. a previous graph)
+    for (int k = 0; k < 4; ++k)
+      if (pt->opened[r][k]) {
+        cudaIpcCloseMemHandle(pt->opened[r][k]);
+        pt->opened[r][k] = nullptr;
+      }
+  const cudaIpcMemHandle_t* h = static_cast<const cudaIpcMemHandle_t*>(all_handles);
+  int* counts[kMaxWorld] = {};
+  unsigned* flags[kMaxWorld] = {};
+  for (int r = 0; r < pt->world; ++r) {
+    if (r == pt->rank) {
+      pt->peer_claims[r] = pt->recv_claims;
+      pt->peer_eps[r] = pt->recv_eps;
+      counts[r] = pt->recv_counts;
+      flags[r] = pt->flag;
+      continue;
+    }
+    void* ptrs[4];
+    for (int k = 0; k < 4; ++k) {
+      PCUDA(cudaIpcOpenMemHandle(&ptrs[k], h[4 * r + k], cudaIpcMemLazyEnablePeerAccess));
+      pt->opened[r][k] = ptrs[k];
+    }
+    pt->peer_claims[r] = static_cast<int4*>(ptrs[0]);
+    pt->peer_eps[r] = static_cast<int4*>(ptrs[1]);
+    counts[r] = static_cast<int*>(ptrs[2]);
+    flags[r] = static_cast<unsigned*>(ptrs[3]);
+  }
+  pfree(pt->dpeer_counts);
+  pfree(pt->dpeer_flags);
+  PCUDA(cudaMalloc(&pt->dpeer_counts, sizeof(int*) * kMaxWorld));
+  PCUDA(cudaMalloc(&pt->dpeer_flags, sizeof(unsigned*) * kMaxWorld));
+  PCUDA(cudaMemcpy(pt->dpeer_counts, counts, sizeof(int*) * kMaxWorld, cudaMemcpyHostToDevice));
+  PCUDA(cudaMemcpy(pt->dpeer_flags, flags, sizeof(unsigned*) * kMaxWorld, cudaMemcpyHostToDevice));
+  pt->p2p = true;
+  return BM_OK;
+}
+
+bm_status bm_part_expand_p2p(bm_part* pt, int32_t parity) {
+  bm_status s = ready(pt, true);
+  if (s != BM_OK) return s;
+  if (!pt->p2p) return pfail(BM_ERR_INVALID_ARG, "P2P exchange not set up (bm_part_p2p_import)");
+  PCUDA(cudaSetDevice(pt->device));
+  parity &= 1;
+  PCUDA(cudaMemsetAsync(pt->cnt + 2, 0, sizeof(int) * 2, pt->stream));
+  PCUDA(cudaMemsetAsync(pt->cnt + 63, 0, sizeof(int), pt->stream));
+  const PartDev d = dev_of(pt, parity);
+  if (pt->n_cur > 0) {
+    part_expand_kernel<<<blocks_for(pt, (long long)pt->n_cur * kGroup), kThr, 0, pt->stream>>>(
+        d, pt->F[pt->cur], pt->n_cur, nullptr, pt->cnt + 2, nullptr, pt->cnt + 3, pt->stats, pt->huge, pt->cnt + 63);
+    part_expand_huge_kernel<<<pt->sms * 4, kThr, 0, pt->stream>>>(d, pt->F[pt->cur], pt->huge, pt->cnt + 63, nullptr,
+                                                                  pt->cnt + 2, nullptr, pt->cnt + 3, pt->stats);
+    pt->launches += 2;
+  }
+  part_signal_kernel<<<1, 32, 0, pt->stream>>>(pt->cnt + 2, pt->cnt + 3, pt->dpeer_counts, pt->dpeer_flags, pt->rank,
+                                               pt->world, parity);
+  pt->launches++;
+  PCUDA(cudaGetLastError());
+  return BM_OK;
+}
+
+bm_status bm_part_merge_p2p(bm_part* pt, int32_t parity, uint32_t arrivals, int64_t* n_next_total, int32_t* found) {
+  bm_status s = ready(pt, true);
+  if (s != BM_OK) return s;
+  if (!pt->p2p) return pfail(BM_ERR_INVALID_ARG, "P2P exchange not set up (bm_part_p2p_import)");
+  PCUDA(cudaSetDevice(pt->device));
+  parity &= 1;
+  part_wait_kernel<<<1, 32, 0, pt->stream>>>(pt->flag, arrivals, pt->timeout);
+  PCUDA(cudaMemsetAsync(pt->stats + 5, 0, sizeof(unsigned long long), pt->stream));
+  PCUDA(cudaMemsetAsync(pt->cnt + 1, 0, sizeof(int), pt->stream));
+  pt->stamp++;
+  const PartDev d = dev_of(pt);
+  const int* counts = pt->recv_counts + parity * 2 * kMaxWorld;
+  const Gathered gc{pt->recv_claims + (long long)parity * pt->world * pt->ccap, counts, pt->ccap, pt->world};
+  const Gathered ge{pt->recv_eps + (long long)parity * pt->world * pt->ecap, counts + kMaxWorld, pt->ecap, pt->world};
+  const int b = pt->sms * 8;
+  part_ep_root_kernel<<<b, kThr, 0, pt->stream>>>(d, ge);
+  part_ep_row_kernel<<<b, kThr, 0, pt->stream>>>(d, ge);
+  part_ep_apply_kernel<<<b, kThr, 0, pt->stream>>>(d, ge, pt->ep_list, pt->cnt + 4, pt->rank == 0, pt->cnt + 5);
+  part_claim_min_kernel<<<b, kThr, 0, pt->stream>>>(d, gc);
+  part_claim_apply_kernel<<<b, kThr, 0, pt->stream>>>(d, gc, pt->F[pt->cur ^ 1], pt->cnt + 1, pt->stats + 5);
+  pt->launches += 6;
+  PCUDA(cudaGetLastError());
+  int nxt[5] = {0, 0, 0, 0, 0}, to = 0;
+  unsigned long long live = 0;
+  PCUDA(cudaMemcpyAsync(nxt, pt->cnt + 1, sizeof(nxt), cudaMemcpyDeviceToHost, pt->stream));
+  PCUDA(cudaMemcpyAsync(&live, pt->stats + 5, sizeof(live), cudaMemcpyDeviceToHost, pt->stream));
+  PCUDA(cudaMemcpyAsync(&to, pt->timeout, sizeof(int), cudaMemcpyDeviceToHost, pt->stream));
+  PCUDA(cudaStreamSynchronize(pt->stream));
+  if (to) return pfail(BM_ERR_NCCL, "P2P exchange timed out waiting for a peer");
+  pt->cur ^= 1;
+  pt->n_cur = nxt[0];
+  if (n_next_total) *n_next_total = (int64_t)live;
+  if (found) *found = nxt[4] != 0;
   return BM_OK;
 }
 

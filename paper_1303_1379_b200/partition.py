@@ -53,6 +53,10 @@ _PART_PROTOS = {
     "bm_part_stats": (C.c_int, [_vp, _i64p, _i64p, _i64p, _i64p, _i64p]),
     "bm_part_reset_stats": (C.c_int, [_vp]),
     "bm_part_launch_count": (C.c_int, [_vp, _i64p]),
+    "bm_part_p2p_export": (C.c_int, [_vp, C.c_int64, C.c_int64, _vp]),
+    "bm_part_p2p_import": (C.c_int, [_vp, _vp]),
+    "bm_part_expand_p2p": (C.c_int, [_vp, C.c_int32]),
+    "bm_part_merge_p2p": (C.c_int, [_vp, C.c_int32, C.c_uint32, _i64p, _i32p]),
 }
 for _name, (_res, _args) in _PART_PROTOS.items():
     _fn = getattr(lib, _name)
@@ -104,6 +108,14 @@ class Exchange:
         parts = [torch.empty_like(host) for _ in range(self.world)]
         self.dist.all_gather(parts, host, group=self.group)
         return torch.cat(parts).to(local.device)
+
+    def barrier(self):
+        self.dist.barrier(group=self.group)
+
+    def allgather_bytes(self, data: bytes) -> list:
+        out = [None] * self.world
+        self.dist.all_gather_object(out, data, group=self.group)
+        return out
 
     def broadcast_(self, t, src: int = 0):
         if self.nccl or t.device.type == "cpu":
@@ -185,6 +197,25 @@ class GpuPartition:
                                 C.byref(nxt), C.byref(found)))
         return nxt.value, bool(found.value)
 
+    # -- fused P2P exchange (peer memory over NVLink, CUDA IPC)
+    def p2p_export(self, claims_cap: int, endpoints_cap: int) -> bytes:
+        buf = C.create_string_buffer(4 * 64)
+        check(lib.bm_part_p2p_export(self._h, claims_cap, endpoints_cap, C.cast(buf, _vp)))
+        return buf.raw
+
+    def p2p_import(self, handles: bytes):
+        buf = C.create_string_buffer(handles, len(handles))
+        check(lib.bm_part_p2p_import(self._h, C.cast(buf, _vp)))
+
+    def expand_p2p(self, parity: int):
+        self.torch.cuda.current_stream(self.device).synchronize()
+        check(lib.bm_part_expand_p2p(self._h, parity))
+
+    def merge_p2p(self, parity: int, arrivals: int):
+        nxt, found = C.c_int64(), C.c_int32()
+        check(lib.bm_part_merge_p2p(self._h, parity, arrivals & 0xFFFFFFFF, C.byref(nxt), C.byref(found)))
+        return nxt.value, bool(found.value)
+
     def end_bfs(self):
         check(lib.bm_part_end_bfs(self._h))
 
@@ -250,11 +281,24 @@ class PartitionedMatcher:
             return t1
         return t0
 
-    def upload(self, g: BipartiteCsr):
+    def upload(self, g: BipartiteCsr, p2p: bool = False):
+        """Uploads this rank's slice. p2p: set up the fused exchange (records written
+        straight into every rank's receive slabs over peer memory) instead of the
+        all-gather through torch.distributed."""
         lo, hi = column_range(g.nc, self.rank, self.world)
         cxs, adjs = slice_csc(g, lo, hi)
         self.b.upload(g.nc, g.nr, lo, hi, cxs, adjs)
         self.nc, self.nr = g.nc, g.nr
+        self.p2p = False
+        if p2p:
+            max_e = max(int(g.cxadj[column_range(g.nc, r, self.world)[1]] - g.cxadj[column_range(g.nc, r, self.world)[0]])
+                        for r in range(self.world))
+            self.x.barrier()  # no rank still maps a slab about to be replaced
+            h = self.b.p2p_export(max(1, min(g.nc, max_e)), max(1, min(g.nr, max_e)))
+            allh = self.x.allgather_bytes(h)
+            self.b.p2p_import(b"".join(allh))
+            self.p2p = True
+            self.arrivals = 0
 
     def _gather(self, local, n_local: int, counts):
         """All-gather this rank's records, padded to the largest count."""
@@ -287,16 +331,24 @@ class PartitionedMatcher:
             found = False
             levels = 0
             while True:
-                claims, eps, nc_l, ne_l = b.expand()
-                t0 = self._tick("expand", t0)
-                counts = self.x.allgather_counts([nc_l, ne_l])
-                t0 = self._tick("counts", t0)
-                call, cstride = self._gather(claims, nc_l, counts[:, 0])
-                eall, estride = self._gather(eps, ne_l, counts[:, 1])
-                t0 = self._tick("gather", t0)
-                res.records_exchanged += int(counts.sum())
-                n_next, found = b.merge(call, counts[:, 0], cstride, eall, counts[:, 1], estride)
-                t0 = self._tick("merge", t0)
+                if self.p2p:  # fused exchange: no collective call, arrivals counted on the device
+                    parity = (self.arrivals // self.world) & 1  # alternates every level, across phases too
+                    b.expand_p2p(parity)
+                    t0 = self._tick("expand", t0)
+                    self.arrivals += self.world
+                    n_next, found = b.merge_p2p(parity, self.arrivals)
+                    t0 = self._tick("merge", t0)
+                else:
+                    claims, eps, nc_l, ne_l = b.expand()
+                    t0 = self._tick("expand", t0)
+                    counts = self.x.allgather_counts([nc_l, ne_l])
+                    t0 = self._tick("counts", t0)
+                    call, cstride = self._gather(claims, nc_l, counts[:, 0])
+                    eall, estride = self._gather(eps, ne_l, counts[:, 1])
+                    t0 = self._tick("gather", t0)
+                    res.records_exchanged += int(counts.sum())
+                    n_next, found = b.merge(call, counts[:, 0], cstride, eall, counts[:, 1], estride)
+                    t0 = self._tick("merge", t0)
                 levels += 1
                 if (shortest and found) or n_next == 0:
                     break

@@ -12,7 +12,7 @@ torch.cuda.set_device(0)
 g, known = bench.build_graph(sys.argv[1] if len(sys.argv) > 1 else "C2", 1)
 init = bm.cheap_matching(g)
 pm = PartitionedMatcher(GpuPartition(0, 0, 1), Exchange())
-pm.upload(g)
+pm.upload(g, p2p=os.environ.get("BM_P2P") == "1")
 pm.match(init)
 pm.t = {}
 t = time.perf_counter(); r = pm.match(init); t = time.perf_counter() - t

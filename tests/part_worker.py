@@ -30,6 +30,8 @@ def run(rank, world, port, backend, out_dir, device_mode):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("nccl" if device_mode == "nccl" else "gloo", rank=rank, world_size=world)
+    # "p2p": the fused exchange through CUDA IPC peer memory (gloo only carries the setup and the
+    # per-phase broadcast); with several ranks on one GPU the "peers" are the same device
     import paper_1303_1379_b200 as bm
     from paper_1303_1379_b200.partition import Exchange, GpuPartition, PartitionedMatcher
     if backend == "cpu":
@@ -43,7 +45,7 @@ def run(rank, world, port, backend, out_dir, device_mode):
     results = []
     for gi, g in enumerate(graphs()):
         init = bm.cheap_matching(g)
-        pm.upload(g)
+        pm.upload(g, p2p=(device_mode == "p2p"))
         for shortest, kernel in [(False, bm.BfsKernel.GpubfsWr), (True, bm.BfsKernel.GpubfsWr),
                                  (False, bm.BfsKernel.Gpubfs)]:
             res = pm.match(init, shortest=shortest, kernel=kernel)

@@ -58,6 +58,13 @@ def test_partition_kernels_two_ranks_one_gpu(tmp_path, oracle):
     _check(_run(2, "gpu", tmp_path), oracle)
 
 
+@pytest.mark.gpu
+def test_partition_fused_p2p_exchange_two_ranks(tmp_path, oracle):
+    """The fused exchange: records written by the expand kernel straight into
+    both ranks' receive slabs (CUDA IPC), device-side arrival counting."""
+    _check(_run(2, "gpu", tmp_path, device_mode="p2p"), oracle)
+
+
 def test_column_range_and_slice():
     import paper_1303_1379_b200 as bm
     from paper_1303_1379_b200.partition import column_range, slice_csc
