@@ -253,7 +253,8 @@ def run_partitioned(args):
     local = local % max(1, torch.cuda.device_count())  # gloo tests run several ranks on one GPU
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    backend = "gloo" if args.exchange == "gloo" else "nccl"
+    # the process group is the control plane (setup, per-phase broadcast); NCCL needs one GPU per rank
+    backend = "nccl" if args.exchange != "gloo" and world <= torch.cuda.device_count() else "gloo"
     if not dist.is_initialized():
         if world == 1:
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
