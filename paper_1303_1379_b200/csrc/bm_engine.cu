@@ -82,7 +82,10 @@ constexpr int kThreads = BM_THREADS;  // threads per CTA (1024 / kThreads CTAs p
 #define BM_MINB (1024 / BM_THREADS)
 #endif
 constexpr int kItems = BM_ITEMS;      // edges per thread per round (memory-level parallelism)
-constexpr unsigned kGran = 512;       // edges per granule-index entry; tiles are whole granules
+#ifndef BM_GRAN
+#define BM_GRAN 512
+#endif
+constexpr unsigned kGran = BM_GRAN;   // edges per granule-index entry; tiles are whole granules
 #ifndef BM_TILE_GRAN
 #define BM_TILE_GRAN 8
 #endif
