@@ -59,8 +59,14 @@ ALGOS = {  # id -> (shortest, kernel, improved)  algorithms.cpp:19-27
 }
 
 
+GRAPH_FILE = None  # --graph: a user matrix instead of a synthetic config
+
+
 def build_graph(name: str, scale_div: int = 1):
     import paper_1303_1379_b200 as bm
+    if name == "file":  # maximum unknown up front: the GPU certificate and the reference arm check it
+        path = GRAPH_FILE
+        return (bm.load_csc(path) if path.endswith(".bcsc") else bm.load_matrix_market(path)), None
     if name == "C1":
         return bm.generate_random_bipartite(100_000, 100_000, 8.0, 1), 99_961
     if name == "C2":
@@ -75,6 +81,10 @@ def build_graph(name: str, scale_div: int = 1):
         n = 100_000_000 // scale_div
         return bm.generate_random_bipartite(n, n, 16.0, 5), (99_999_986 if scale_div == 1 else None)
     raise SystemExit(f"unknown config {name}")
+
+
+def data_kind() -> str:
+    return f"file {os.path.basename(GRAPH_FILE)}" if GRAPH_FILE else "synthetic"
 
 
 def known_answers():
@@ -229,7 +239,7 @@ def run_reference_arm(args):
     emit({
         "impl": "reference", "metric": METRIC, "value": value, "unit": "edges/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+        "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": data_kind(),
         "config": {"workload": f"{args.config}: {CONFIGS[args.config]}", "algorithm": "apfb-wr-ct (reference CPU)",
                    "nc": g.nc, "nr": g.nr, "edges": E, "init": "first-fit cheap_matching (not timed)"},
         "cpu_baseline": {"value": value, "unit": "edges/s", "cores": cores, "kind": kind, "sample": sample},
@@ -332,7 +342,7 @@ def run_partitioned(args):
         emit({
             "metric": METRIC, "value": E / (t_ms / 1e3), "unit": "edges/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_ms, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+            "scaling": "strong", "vs_baseline": None, "dtype": "int32", "data": data_kind(),
             "config": {"workload": f"{args.config}: {CONFIGS[args.config]}" +
                                    (f" (1/{args.scale_div} scale)" if args.scale_div != 1 else ""),
                        "algorithm": f"{args.algo}-b200-partitioned", "nc": g.nc, "nr": g.nr, "edges": E,
@@ -536,7 +546,7 @@ def run_b200(args):
         out = {
             "metric": METRIC, "value": world * E / (t_ms / 1e3), "unit": "edges/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_ms, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+            "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": data_kind(),
             "config": {"workload": f"{args.config}: {CONFIGS[args.config]}" +
                                    (f" (1/{args.scale_div} scale)" if args.scale_div != 1 else ""),
                        "algorithm": f"{args.algo}-b200", "nc": g.nc, "nr": g.nr, "edges": E,
@@ -595,7 +605,14 @@ def main():
     ap.add_argument("--exchange", choices=["p2p", "nccl", "gloo"], default="p2p",
                     help="partition mode: p2p = the expand kernel writes every rank's receive slab over peer "
                          "memory (falls back to nccl if IPC is unavailable); nccl = all-gather; gloo = host-staged")
+    ap.add_argument("--graph", default=None,
+                    help="a Matrix Market (.mtx) or binary CSC (.bcsc) file to use instead of --config")
     args = ap.parse_args()
+    if args.graph:
+        global GRAPH_FILE
+        GRAPH_FILE = os.path.abspath(args.graph)
+        CONFIGS["file"] = f"{os.path.basename(args.graph)} (read by the parallel file reader, bmatch_b200_io.h)"
+        args.config = "file"
     if args.warmup < 3 and args.impl == "b200":
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)
     if args.impl == "reference":

@@ -24,6 +24,8 @@
  *   std::invalid_argument  -> BM_ERR_INVALID_ARG  (e.g. matching.cpp:71-73)
  *   std::logic_error       -> BM_ERR_LOGIC        (gpu_match.cpp:77-80, 272-274)
  *   std::runtime_error     -> BM_ERR_BOUND_EXCEEDED (nc+1 phase bound, gpu_match.cpp:317-320)
+ *   ParseError{line}       -> BM_ERR_PARSE        (matrix_market.cpp:29-99; bmatch_b200_io.h)
+ *   "cannot open" etc.     -> BM_ERR_IO           (matrix_market.cpp:103-104)
  * The message of the last failure on the calling thread is bm_last_error().
  * There is no CPU fallback: without a usable sm_100 device every compute
  * entry point fails with BM_ERR_CUDA.
@@ -53,7 +55,9 @@ typedef enum bm_status {
   BM_ERR_BOUND_EXCEEDED = 3,
   BM_ERR_CUDA = 4,
   BM_ERR_OOM = 5,
-  BM_ERR_NCCL = 6
+  BM_ERR_NCCL = 6,
+  BM_ERR_PARSE = 7,  /* malformed input file: the reference's ParseError (parse_error.hpp:9-14) */
+  BM_ERR_IO = 8      /* a file cannot be opened, read or written */
 } bm_status;
 
 /* Driver: APFB = augment along every path found per phase (gpu_match.hpp:131-135);

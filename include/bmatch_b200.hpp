@@ -16,6 +16,11 @@
 //        the CLI's `match --algo` (src/cli.cpp:59-76) reach the B200 engine
 //        with no other change. With shadow_reference_ids = true it also
 //        replaces the reference's own ids apfb-wr-ct, apsb-wr-ct, ... .
+//   load_matrix_market(path), read_matrix_market(text), write_matrix_market(g, path)
+//        replace the reference's Matrix Market I/O (include/bmatch/matrix_market.hpp:
+//        14-24) with the parallel reader/writer of bmatch_b200_io.h; same graph,
+//        same bytes, same ParseError{line}
+//   load_csc(path), save_csc(g, path)                         binary CSC files
 //
 // Behaviour the reference's callers rely on is kept:
 //   * same parameter lists; GridConfig and Schedule are accepted and ignored
@@ -47,7 +52,9 @@
 #include "bmatch/gpu_match.hpp"
 #include "bmatch/kernel_grid.hpp"
 #include "bmatch/matching.hpp"
+#include "bmatch/parse_error.hpp"
 #include "bmatch_b200.h"
+#include "bmatch_b200_io.h"
 
 namespace bmatch::b200 {
 
@@ -192,6 +199,84 @@ inline void register_algorithms(int device = 0, bool shadow_reference_ids = fals
       register_algorithm(a.base, fn);
     }
   }
+}
+
+namespace detail {
+
+// Runs a bm_mm_* reader; rethrows BM_ERR_PARSE as the reference's ParseError.
+template <typename Info, typename Load>
+BipartiteCsr read_mm(Info&& info, Load&& load) {
+  auto check = [](bm_status s, int64_t line) {
+    if (s != BM_ERR_PARSE) return throw_on(s);
+    std::string msg = bm_last_error();  // "line N: message", as ParseError::what()
+    const std::string head = "line " + std::to_string(line) + ": ";
+    if (msg.compare(0, head.size(), head) == 0) msg = msg.substr(head.size());
+    throw ParseError(line, msg);
+  };
+  bm_mm_header h{};
+  int64_t line = 0;
+  bm_status s = info(&h, &line);  // (the status must be taken before `line` is read)
+  check(s, line);
+  BipartiteCsr g;
+  g.nc = h.ncols;
+  g.nr = h.nrows;
+  g.cxadj.assign((size_t)h.ncols + 1, 0);
+  g.cadj.assign((size_t)h.capacity, 0);
+  int64_t ne = 0;
+  s = load(h.capacity, g.cxadj.data(), g.cadj.data(), &ne, &line);
+  check(s, line);
+  g.cadj.resize((size_t)ne);
+  g.cadj.shrink_to_fit();
+  return g;
+}
+
+inline std::string stem(const std::string& path) {
+  const size_t slash = path.find_last_of('/');
+  std::string base = slash == std::string::npos ? path : path.substr(slash + 1);
+  const size_t dot = base.find_last_of('.');
+  return dot == std::string::npos || dot == 0 ? base : base.substr(0, dot);
+}
+
+}  // namespace detail
+
+// read_matrix_market on an in-memory text (matrix_market.cpp:29-99).
+inline BipartiteCsr read_matrix_market(const std::string& text, int threads = 0) {
+  return detail::read_mm(
+      [&](bm_mm_header* h, int64_t* line) { return bm_mm_parse_info(text.data(), (int64_t)text.size(), h, line); },
+      [&](int64_t cap, int64_t* cx, int32_t* adj, int64_t* ne, int64_t* line) {
+        return bm_mm_parse(text.data(), (int64_t)text.size(), threads, cap, cx, adj, ne, line);
+      });
+}
+
+// load_matrix_market (matrix_market.cpp:101-108): memory-mapped, parsed on every core.
+inline BipartiteCsr load_matrix_market(const std::string& path, int threads = 0) {
+  BipartiteCsr g = detail::read_mm(
+      [&](bm_mm_header* h, int64_t* line) { return bm_mm_info(path.c_str(), h, line); },
+      [&](int64_t cap, int64_t* cx, int32_t* adj, int64_t* ne, int64_t* line) {
+        return bm_mm_load(path.c_str(), threads, cap, cx, adj, ne, line);
+      });
+  g.name = detail::stem(path);
+  return g;
+}
+
+// write_matrix_market (matrix_market.cpp:111-118) to a file, byte for byte.
+inline void write_matrix_market(const BipartiteCsr& g, const std::string& path, int threads = 0) {
+  throw_on(bm_mm_write(path.c_str(), g.nc, g.nr, g.cxadj.data(), g.cadj.data(), threads));
+}
+
+inline void save_csc(const BipartiteCsr& g, const std::string& path, int threads = 0) {
+  throw_on(bm_csc_write(path.c_str(), g.nc, g.nr, g.cxadj.data(), g.cadj.data(), threads));
+}
+
+inline BipartiteCsr load_csc(const std::string& path, int threads = 0) {
+  BipartiteCsr g;
+  int64_t ne = 0;
+  throw_on(bm_csc_info(path.c_str(), &g.nc, &g.nr, &ne));
+  g.cxadj.assign((size_t)g.nc + 1, 0);
+  g.cadj.assign((size_t)ne, 0);
+  throw_on(bm_csc_read(path.c_str(), threads, ne, g.cxadj.data(), g.cadj.data()));
+  g.name = detail::stem(path);
+  return g;
 }
 
 }  // namespace bmatch::b200

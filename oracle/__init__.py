@@ -142,6 +142,10 @@ class Reference:
     def __init__(self, path: str = REF_PATH):
         if not os.path.exists(path):
             raise ImportError(f"{path} missing: run `make ref` where /root/reference exists")
+        # The reference's iostream-based Matrix Market reader needs the shared
+        # libstdc++'s locale machinery visible globally (this toolchain links a
+        # static copy into the .so; without the preload its streams crash).
+        C.CDLL("libstdc++.so.6", mode=C.RTLD_GLOBAL)
         L = self.lib = C.CDLL(path)
         vp = C.c_void_p
         sig = {
@@ -164,6 +168,8 @@ class Reference:
                                        _i32p, _i32p]),
             "ref_alternate": (C.c_int64, [vp, C.c_int32, C.c_int32, _i32p, _i32p, _i32p, _i32p]),
             "ref_fix_matching": (C.c_int64, [C.c_int32, C.c_int32, _i32p, _i32p]),
+            "ref_read_matrix_market": (vp, [C.c_char_p, C.c_int64, _i32p, _i64p]),
+            "ref_write_matrix_market": (C.c_int64, [vp, C.c_char_p, C.c_int64]),
         }
         for k, (r, a) in sig.items():
             f = getattr(L, k)
@@ -182,6 +188,21 @@ class Reference:
 
     def generate_random_bipartite(self, nc, nr, deg, seed):
         return RefGraph(self, self.lib.ref_generate_random_bipartite(nc, nr, deg, seed))
+
+    def read_matrix_market(self, text: bytes):
+        """-> ("ok", nc, nr, cxadj, cadj) | ("parse", line, message) | ("error", message)."""
+        kind, line = C.c_int32(), C.c_int64()
+        h = self.lib.ref_read_matrix_market(text, len(text), C.byref(kind), C.byref(line))
+        if not h:
+            return ("parse", line.value, self.error()) if kind.value == 1 else ("error", self.error())
+        return ("ok",) + RefGraph(self, h).arrays()
+
+    def write_matrix_market(self, g) -> bytes:
+        rg = self.from_csc(g)
+        n = self.lib.ref_write_matrix_market(rg.h, None, 0)
+        buf = C.create_string_buffer(max(n, 1))
+        self.lib.ref_write_matrix_market(rg.h, buf, n)
+        return buf.raw[:n]
 
     def fix_matching(self, rmatch, cmatch):
         r, c = rmatch.copy(), cmatch.copy()

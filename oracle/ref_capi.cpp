@@ -7,6 +7,7 @@
 #include <chrono>
 #include <cstdint>
 #include <cstring>
+#include <sstream>
 #include <string>
 #include <thread>
 #include <vector>
@@ -17,6 +18,7 @@
 #include "bmatch/gpu_match.hpp"
 #include "bmatch/kernel_grid.hpp"
 #include "bmatch/matching.hpp"
+#include "bmatch/matrix_market.hpp"
 
 using namespace bmatch;
 
@@ -71,6 +73,37 @@ void ref_graph_copy(void* h, int64_t* cxadj, int32_t* cadj) {
   auto* g = static_cast<BipartiteCsr*>(h);
   std::memcpy(cxadj, g->cxadj.data(), sizeof(int64_t) * g->cxadj.size());
   if (!g->cadj.empty()) std::memcpy(cadj, g->cadj.data(), sizeof(int32_t) * g->cadj.size());
+}
+
+// read_matrix_market on an in-memory stream (matrix_market.cpp:29-99). Returns
+// a graph handle, or null with *err_kind = 1 (ParseError; *err_line set) or 2
+// (another exception, e.g. from_edge_list's out_of_range); message in
+// ref_last_error().
+void* ref_read_matrix_market(const char* text, int64_t len, int32_t* err_kind, int64_t* err_line) {
+  *err_kind = 0;
+  *err_line = 0;
+  try {
+    std::istringstream in(std::string(text, (size_t)len));
+    return new BipartiteCsr(read_matrix_market(in));
+  } catch (const ParseError& e) {
+    *err_kind = 1;
+    *err_line = e.line;
+    g_ref_err = e.what();
+  } catch (const std::exception& e) {
+    *err_kind = 2;
+    g_ref_err = e.what();
+  }
+  return nullptr;
+}
+
+// write_matrix_market (matrix_market.cpp:111-118) into a caller buffer;
+// returns the byte length (copies only when cap is large enough).
+int64_t ref_write_matrix_market(void* h, char* out, int64_t cap) {
+  std::ostringstream os;
+  write_matrix_market(*static_cast<BipartiteCsr*>(h), os);
+  const std::string s = os.str();
+  if (out && cap >= (int64_t)s.size()) std::memcpy(out, s.data(), s.size());
+  return (int64_t)s.size();
 }
 
 void ref_graph_free(void* h) { delete static_cast<BipartiteCsr*>(h); }

@@ -18,6 +18,7 @@ LIB_PATH = os.environ.get("BM_LIB") or os.path.join(_HERE, "libbmatch_b200.so") 
 HEADERS = [
     os.path.join(os.path.dirname(_HERE), "include", "bmatch_b200.h"),
     os.path.join(os.path.dirname(_HERE), "include", "bmatch_b200_gen.h"),
+    os.path.join(os.path.dirname(_HERE), "include", "bmatch_b200_io.h"),
 ]
 
 BM_OK = 0
@@ -27,6 +28,8 @@ BM_ERR_BOUND_EXCEEDED = 3
 BM_ERR_CUDA = 4
 BM_ERR_OOM = 5
 BM_ERR_NCCL = 6
+BM_ERR_PARSE = 7
+BM_ERR_IO = 8
 
 BM_DRIVER_APFB, BM_DRIVER_APSB = 0, 1
 BM_BFS_GPUBFS, BM_BFS_WR = 0, 1
@@ -82,6 +85,17 @@ class bm_phase_event(C.Structure):
     ]
 
 
+class bm_mm_header(C.Structure):
+    _fields_ = [
+        ("nrows", C.c_int32),
+        ("ncols", C.c_int32),
+        ("entries", C.c_int64),
+        ("symmetric", C.c_int32),
+        ("field", C.c_int32),
+        ("capacity", C.c_int64),
+    ]
+
+
 PHASE_CB = C.CFUNCTYPE(C.c_int, C.POINTER(bm_phase_event), C.c_void_p)
 
 _i32p = C.POINTER(C.c_int32)
@@ -128,6 +142,14 @@ _PROTOS = {
                                 _i32p, _i64p, _i64p]),
     "bm_check_csc": (C.c_int, [C.c_int32, C.c_int32, _i64p, _i32p]),
     "bm_csc_digest": (C.c_uint64, [C.c_int32, C.c_int32, _i64p, _i32p]),
+    "bm_mm_info": (C.c_int, [C.c_char_p, C.POINTER(bm_mm_header), _i64p]),
+    "bm_mm_load": (C.c_int, [C.c_char_p, C.c_int32, C.c_int64, _i64p, _i32p, _i64p, _i64p]),
+    "bm_mm_parse_info": (C.c_int, [C.c_char_p, C.c_int64, C.POINTER(bm_mm_header), _i64p]),
+    "bm_mm_parse": (C.c_int, [C.c_char_p, C.c_int64, C.c_int32, C.c_int64, _i64p, _i32p, _i64p, _i64p]),
+    "bm_mm_write": (C.c_int, [C.c_char_p, C.c_int32, C.c_int32, _i64p, _i32p, C.c_int32]),
+    "bm_csc_write": (C.c_int, [C.c_char_p, C.c_int32, C.c_int32, _i64p, _i32p, C.c_int32]),
+    "bm_csc_info": (C.c_int, [C.c_char_p, _i32p, _i32p, _i64p]),
+    "bm_csc_read": (C.c_int, [C.c_char_p, C.c_int32, C.c_int64, _i64p, _i32p]),
 }
 
 
@@ -165,16 +187,29 @@ class LogicError(Exception):
     """Mirror of std::logic_error (gpu_match.cpp:77-80, 272-274)."""
 
 
+class ParseError(ValueError):
+    """Mirror of bmatch::ParseError (parse_error.hpp:9-14): a malformed input
+    file, tagged with the 1-based line number."""
+
+    def __init__(self, line: int, message: str):
+        super().__init__(message)
+        self.line = line
+
+
 class CudaError(RuntimeError):
     """The device path failed (no GPU, launch error, out of memory)."""
 
 
-def check(status: int) -> None:
+def check(status: int, line: int = 0) -> None:
     if status == BM_OK:
         return
     msg = (lib.bm_last_error() or b"").decode(errors="replace")
     name = (lib.bm_status_string(status) or b"").decode()
     text = f"{name}: {msg}"
+    if status == BM_ERR_PARSE:
+        raise ParseError(line, msg)
+    if status == BM_ERR_IO:
+        raise OSError(msg)
     if status == BM_ERR_INVALID_ARG:
         raise ValueError(text)
     if status == BM_ERR_LOGIC:

@@ -10,6 +10,8 @@ Names, argument meaning and error behaviour follow the reference
   DriverResult, apfb, apsb                include/bmatch/gpu_match.hpp:13-144
   AlgorithmResult, algorithm_ids,
   make_algorithm, register_algorithm      include/bmatch/algorithms.hpp:15-42
+  ParseError, read_matrix_market,
+  load_matrix_market, write_matrix_market include/bmatch/matrix_market.hpp:10-24
 
 Every matching call goes through the C ABI (libbmatch_b200.so) to the sm_100a
 engine; `grid` and `schedule` are accepted for signature compatibility and
@@ -27,14 +29,15 @@ from typing import Callable, Optional
 import numpy as np
 
 from . import _lib
-from ._lib import CudaError, LogicError, check, i32p, i64p, lib
+from ._lib import CudaError, LogicError, ParseError, check, i32p, i64p, lib
 
 __all__ = [
     "BfsKernel", "BipartiteCsr", "MatchingState", "PhaseCounters", "PhaseEvent", "DriverResult",
     "AlgorithmResult", "Engine", "apfb", "apsb", "cheap_matching", "cardinality", "check_csr",
     "csc_digest", "algorithm_ids", "make_algorithm", "register_algorithm", "generate_random_bipartite",
     "generate_planted", "generate_rmat", "generate_banded", "LogicError", "CudaError", "INIT_MODES",
-    "permutation_pair",
+    "permutation_pair", "ParseError", "read_matrix_market", "load_matrix_market", "write_matrix_market",
+    "save_csc", "load_csc",
 ]
 
 INIT_MODES = {"given": _lib.BM_INIT_GIVEN, "gpu_greedy": _lib.BM_INIT_GPU_GREEDY, "gpu_ks": _lib.BM_INIT_GPU_KS}
@@ -513,3 +516,66 @@ def generate_banded(n: int, band: int, delete_frac: float, seed: int, permute=Tr
     g = _gen(n, n, cap, lambda cx, adj, ne: lib.bm_gen_banded(n, band, delete_frac, seed, 1 if permute else 0,
                                                                threads, cx, adj, ne, C.byref(live)))
     return g, int(live.value)
+
+
+# ---- graph files (include/bmatch_b200_io.h) -------------------------------
+def _mm_build(info, load) -> BipartiteCsr:
+    hdr = _lib.bm_mm_header()
+    line = C.c_int64(0)
+    check(info(C.byref(hdr), C.byref(line)), line.value)
+    nc, nr = hdr.ncols, hdr.nrows
+    return _gen(nc, nr, int(hdr.capacity),
+                lambda cx, adj, ne: _status_line(load, int(hdr.capacity), cx, adj, ne))
+
+
+def _status_line(load, cap, cx, adj, ne):
+    line = C.c_int64(0)
+    st = load(cap, cx, adj, ne, C.byref(line))
+    if st:
+        check(st, line.value)
+    return st
+
+
+def read_matrix_market(text) -> BipartiteCsr:
+    """read_matrix_market (matrix_market.cpp:29-99) on an in-memory stream
+    (str or bytes); raises ParseError with the reference's line number."""
+    data = text.encode() if isinstance(text, str) else bytes(text)
+    return _mm_build(lambda h, ln: lib.bm_mm_parse_info(data, len(data), h, ln),
+                     lambda cap, cx, adj, ne, ln: lib.bm_mm_parse(data, len(data), 0, cap, cx, adj, ne, ln))
+
+
+def load_matrix_market(path: str, threads: int = 0) -> BipartiteCsr:
+    """load_matrix_market (matrix_market.cpp:101-108), parsed on every host
+    core; the graph name is the file stem."""
+    import os
+    bp = os.fsencode(path)
+    g = _mm_build(lambda h, ln: lib.bm_mm_info(bp, h, ln),
+                  lambda cap, cx, adj, ne, ln: lib.bm_mm_load(bp, threads, cap, cx, adj, ne, ln))
+    g.name = os.path.splitext(os.path.basename(path))[0]
+    return g
+
+
+def write_matrix_market(g: BipartiteCsr, path: str, threads: int = 0) -> None:
+    """The bytes of write_matrix_market (matrix_market.cpp:111-118)."""
+    import os
+    check(lib.bm_mm_write(os.fsencode(path), g.nc, g.nr, i64p(g.cxadj), i32p(g.cadj), threads))
+
+
+def save_csc(g: BipartiteCsr, path: str, threads: int = 0) -> None:
+    """Binary CSC container BMCSC001 (include/bmatch_b200_io.h)."""
+    import os
+    check(lib.bm_csc_write(os.fsencode(path), g.nc, g.nr, i64p(g.cxadj), i32p(g.cadj), threads))
+
+
+def load_csc(path: str, threads: int = 0) -> BipartiteCsr:
+    """Reads a BMCSC001 file; verifies its checksum and the CSC invariants."""
+    import os
+    bp = os.fsencode(path)
+    nc, nr, ne = C.c_int32(), C.c_int32(), C.c_int64()
+    check(lib.bm_csc_info(bp, C.byref(nc), C.byref(nr), C.byref(ne)))
+    cx = np.zeros(nc.value + 1, np.int64)
+    adj = np.zeros(max(ne.value, 1), np.int32)
+    check(lib.bm_csc_read(bp, threads, ne.value, i64p(cx), i32p(adj)))
+    g = BipartiteCsr(nc.value, nr.value, cx, adj[: ne.value])
+    g.name = os.path.splitext(os.path.basename(path))[0]
+    return g

@@ -1969,6 +1969,8 @@ const char* bm_status_string(int32_t s) {
     case BM_ERR_CUDA: return "cuda error";
     case BM_ERR_OOM: return "out of device memory";
     case BM_ERR_NCCL: return "nccl error";
+    case BM_ERR_PARSE: return "parse error";
+    case BM_ERR_IO: return "i/o error";
     default: return "unknown status";
   }
 }

@@ -80,6 +80,38 @@ int main(int argc, char** argv) {
   for (const char* id : {"apfb-wr-b200", "apfb-gpubfs-b200", "apsb-wr-b200", "apsb-gpubfs-b200"})
     CHECK(make_algorithm(id).has_value());
 
+  // 0. file I/O drop-ins (host only, so they run with or without a GPU):
+  //    the parallel reader must rebuild exactly what the reference wrote and
+  //    read, and raise the reference's ParseError with its line number.
+  {
+    namespace fs = std::filesystem;
+    const fs::path p = fs::temp_directory_path() / "bmatch_b200_shim_io.mtx";
+    const BipartiteCsr g = generate_random_bipartite(5000, 4000, 3.0, 8);
+    {
+      std::ofstream out(p);
+      write_matrix_market(g, out);
+    }
+    const BipartiteCsr mine = b200::load_matrix_market(p.string(), 4);
+    const BipartiteCsr theirs = load_matrix_market(p.string());
+    CHECK(mine.nc == theirs.nc && mine.nr == theirs.nr && mine.name == theirs.name);
+    CHECK(mine.cxadj == theirs.cxadj && mine.cadj == theirs.cadj);
+    b200::write_matrix_market(g, p.string());
+    CHECK(load_matrix_market(p.string()).cadj == g.cadj);
+    b200::save_csc(g, p.string() + ".bcsc");
+    CHECK(b200::load_csc(p.string() + ".bcsc").cadj == g.cadj);
+    fs::remove(p);
+    fs::remove(p.string() + ".bcsc");
+    long long line = 0;
+    std::string what;
+    try {
+      b200::read_matrix_market("%%MatrixMarket matrix coordinate pattern general\n2 2 1\n3 1\n");
+    } catch (const ParseError& e) {
+      line = e.line;
+      what = e.what();
+    }
+    CHECK(line == 3 && what == "line 3: row index 3 outside [1, 2]");
+  }
+
   if (no_gpu) {  // the product path must fail loudly, never fall back to the CPU
     const BipartiteCsr g = fork_graph();
     bool threw = false;
