@@ -240,7 +240,7 @@ struct Params {
 
 enum TlTag : unsigned {
   kTlStart = 0, kTlInit = 1, kTlSetup = 2, kTlLevel = 3, kTlAlt = 4, kTlFixRows = 5, kTlFixCols = 6,
-  kTlRoots = 7, kTlEnd = 8
+  kTlRoots = 7, kTlEnd = 8, kTlLevelEdges = 9
 };
 
 __device__ __forceinline__ void tl_mark(const Params& p, unsigned kind, unsigned arg) {
@@ -1008,6 +1008,7 @@ __device__ PhaseOut run_phase(const Params& p, Smem& sm, int cur, int parity, bo
     }
     if (threadIdx.x == 0) sm.cnt[kStCycBarrier] += clk() - tb;
     tl_mark(p, kTlLevel, n);
+    tl_mark(p, kTlLevelEdges, (T & 0x7fffffffu) | (bu ? 0x80000000u : 0u));  // frontier edges; top bit: pulled
     out.launches++;
     const unsigned long long op = ld_rlx(&outs->packed);
     const unsigned n_next = (unsigned)(op >> 33);
