@@ -406,7 +406,21 @@ def run_b200(args):
     eng.load_matching(init)
     flush = torch.empty(args.flush_mb << 20, dtype=torch.uint8, device=dev)
 
-    def one_step(bottom_up=args.bottom_up):
+    # the traversal direction this run measures: auto resolves per graph at upload; a
+    # qualifying graph gets its row index with the upload (graph preparation, like the
+    # CSC upload itself outside `value`; timed and reported as row_index_ms)
+    auto_level = eng.bottom_up_auto()
+    pulled = args.bottom_up == "on" or (args.bottom_up == "auto" and auto_level > 0)
+    row_index_ms = []
+
+    def prepare():
+        if pulled:
+            t = time.perf_counter()
+            eng.prepare_row_index()
+            row_index_ms.append(1e3 * (time.perf_counter() - t))
+    prepare()
+
+    def one_step(bottom_up=pulled):
         return eng.run(shortest=shortest, kernel=kernel, improved=improved, bottom_up=bottom_up)
 
     # correctness of the measured configuration (GPU Berge certificate)
@@ -416,6 +430,7 @@ def run_b200(args):
     parity_ok = bool(done and viol == 0 and ismax and vcard == card and (known is None or card == known))
     eng.upload(g, force=True)
     eng.load_matching(init)
+    prepare()
 
     for _ in range(args.warmup):
         one_step()
@@ -458,7 +473,7 @@ def run_b200(args):
     alt = None
     if world == 1 and not args.no_alt:
         t_idx = time.perf_counter()
-        one_step(not args.bottom_up)  # builds the row index on first use
+        one_step(not pulled)  # builds the row index on first use
         torch.cuda.synchronize(dev)
         t_idx = time.perf_counter() - t_idx
         a_ms, a_ph = [], []
@@ -467,13 +482,13 @@ def run_b200(args):
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            acard, act, adone = one_step(not args.bottom_up)
+            acard, act, adone = one_step(not pulled)
             e1.record(stream)
             e1.synchronize()
             a_ms.append(e0.elapsed_time(e1))
             a_ph.append(act.outer_iterations)
             parity_ok = parity_ok and adone and (known is None or acard == known)
-        alt = {"bottom_up": not args.bottom_up, "ms_per_step": statistics.mean(a_ms),
+        alt = {"bottom_up": not pulled, "ms_per_step": statistics.mean(a_ms),
                "phases": a_ph, "first_call_s": t_idx}
 
     # ---- end to end through the public API, pinned host buffers ----
@@ -487,6 +502,7 @@ def run_b200(args):
         ms_list = []
         eng2 = bm.Engine(local)
         eng2.set_stream(stream.cuda_stream)
+        eng2.bottom_up = {"auto": "auto", "on": True, "off": False}[args.bottom_up]
         for i in range(args.warmup + args.steps):
             r_p.numpy()[:] = init.rmatch
             c_p.numpy()[:] = init.cmatch
@@ -511,7 +527,9 @@ def run_b200(args):
         h2d = 8 * (g.nc + 1) + 4 * E + 4 * (g.nr + g.nc)
         d2h = 4 * (g.nr + g.nc)
         e2e = {"value": world * E / (e_ms / 1e3), "unit": "edges/s", "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": d2h, "ms_per_step": e_ms}
+               "d2h_bytes_per_step": d2h, "ms_per_step": e_ms,
+               # one-shot (upload + match per step): auto pulls only where one run repays the row index
+               "pulled_dense_levels": args.bottom_up == "on" or (args.bottom_up == "auto" and auto_level == 2)}
         del eng2
 
     # ---- roofline of the driver kernel (SURVEY.md §8d per-unit bytes) ----
@@ -559,7 +577,8 @@ def run_b200(args):
                          "algorithmic_bytes_per_launch": b_units, "survey_formula_bytes": b_survey},
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "bottom_up": bool(args.bottom_up),
+            "bottom_up": {"mode": args.bottom_up, "pulled_dense_levels": bool(pulled),
+                          "row_index_ms": row_index_ms[-1] if row_index_ms else None},
             "alternative": alt,
             "gpu_launches": launches,
             "clocks": sampler.summary(),
@@ -598,8 +617,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-alt", action="store_true", help="skip the other-direction measurement")
-    ap.add_argument("--bottom-up", action="store_true",
-                    help="pull the dense BFS levels (direction-optimised; builds a row index once per graph)")
+    ap.add_argument("--bottom-up", choices=["auto", "on", "off"], default="auto",
+                    help="pull the dense BFS levels (direction-optimised; needs a row index, built on the first "
+                         "run after an upload): auto = the engine decides per graph (BM_BU_AUTO)")
     ap.add_argument("--mode", choices=["auto", "single", "partition", "replicas"], default="auto",
                     help="auto: single GPU at N=1, column partition at N>1")
     ap.add_argument("--exchange", choices=["p2p", "nccl", "gloo"], default="p2p",

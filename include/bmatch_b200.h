@@ -33,7 +33,8 @@
  * Tuning environment variables (read at upload / launch; defaults are the
  * measured best): BM_ROW_LAYOUT=plain|interleave (row-state
  * layout, default by rmatch size), BM_BU_FRAC (share of the edges a frontier
- * must hold to be pulled when bottom_up is set, default 0.45), BM_SOLO_EDGES
+ * must hold to be pulled when bottom_up is set, default 0.45), BM_BU_AUTO
+ * (0|1: overrides the AUTO decision), BM_SOLO_EDGES
  * (widest level run by one CTA, default 1024), BM_PERSIST_MB (L2 persisting
  * window on the row state, default off).
  */
@@ -83,10 +84,21 @@ typedef struct bm_match_opts {
                                 outer iterations and return with *done = 0 (resumable) */
   int32_t claim_policy;      /* bm_claim_policy (WR only): which trees may claim a column */
   int32_t endpoint_policy;   /* bm_endpoint_policy (WR only): how many free rows a tree may hold */
-  int32_t bottom_up;         /* 1: levels whose frontier holds >= 45% of the edges are pulled
-                                (direction-optimised); needs a row index of
-                                the graph, built on the first such run (E ints). 0: push only */
+  int32_t bottom_up;         /* bm_bottom_up: whether levels whose frontier holds >= 45% of
+                                the edges are pulled (direction-optimised); they
+                                need a row index of the graph (E ints), built on the first such
+                                run after an upload */
 } bm_match_opts;
+
+/* OFF: push every level. ON: pull dense levels (builds the row index on the
+ * first run after an upload). AUTO: pull them on graphs of the kind where that
+ * pays (bm_bottom_up_auto: >= 2M rows, so the row state outgrows what L2 keeps
+ * close; >= 75% non-empty columns; average degree >= 8 over those, i.e. a BFS
+ * whose middle levels cover most columns), once the row index exists
+ * (bm_prepare_row_index) or right away at >= 2^26 rows, where one run repays
+ * building it. Measured on B200: -20% per run on C2, -45% on C5; C1, C3 and
+ * C4 do not qualify. BM_BU_AUTO=0|1 overrides the graph test. */
+typedef enum bm_bottom_up { BM_BU_OFF = 0, BM_BU_ON = 1, BM_BU_AUTO = 2 } bm_bottom_up;
 
 /* Column claims under GPUBFS-WR. REFERENCE: a tree whose root already found a
  * path keeps claiming columns at discovery; they are skipped at expansion
@@ -164,6 +176,14 @@ bm_status   bm_set_stream(bm_handle* h, void* stream);
 bm_status   bm_upload_csc(bm_handle* h, int32_t nc, int32_t nr,
                           const int64_t* cxadj, const int32_t* cadj);
 bm_status   bm_graph_info(bm_handle* h, int32_t* nc, int32_t* nr, int64_t* nedges);
+/* BM_BU_AUTO for the resident graph: 0 = pushes; 1 = pulls its dense levels
+ * once the row index is prepared; 2 = pulls them from the first run. */
+bm_status   bm_bottom_up_auto(bm_handle* h, int32_t* enabled);
+/* Builds the row index the pulled levels read (4E + 8E bytes of device
+ * memory; about 6 ms for 1.6e8 edges), so that BM_BU_AUTO pulls from the next
+ * run on. Call it once per upload when the same graph is matched repeatedly;
+ * a single match of a graph below 2^26 rows does not repay it and pushes. */
+bm_status   bm_prepare_row_index(bm_handle* h);
 
 /* ---- matching: the reference-shaped one-call entry ----------------------
  * Replaces apfb()/apsb() (gpu_match.hpp:133-144): rmatch[nr]/cmatch[nc] are

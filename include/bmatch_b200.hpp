@@ -133,6 +133,7 @@ inline DriverResult run(const BipartiteCsr& g, MatchingState init, bool shortest
   o.bfs_kernel = kernel == BfsKernel::GpubfsWr ? BM_BFS_WR : BM_BFS_GPUBFS;
   o.improved = improved ? 1 : 0;
   o.init = BM_INIT_GIVEN;
+  o.bottom_up = BM_BU_AUTO;  // pull dense levels where the engine judges it pays
   bm_counters ct{};
   std::vector<int64_t> launches((size_t)g.nc + 2);
   int64_t card = 0;

@@ -36,6 +36,7 @@ BM_BFS_GPUBFS, BM_BFS_WR = 0, 1
 BM_INIT_GIVEN, BM_INIT_GPU_GREEDY, BM_INIT_GPU_KS = 0, 1, 2
 BM_CLAIM_REFERENCE, BM_CLAIM_AT_DISCOVERY = 0, 1
 BM_EP_AUTO, BM_EP_EVERY, BM_EP_ONE_PER_TREE = 0, 1, 2
+BM_BU_OFF, BM_BU_ON, BM_BU_AUTO = 0, 1, 2
 
 
 class bm_match_opts(C.Structure):
@@ -112,6 +113,8 @@ _PROTOS = {
     "bm_set_stream": (C.c_int, [_vp, _vp]),
     "bm_upload_csc": (C.c_int, [_vp, C.c_int32, C.c_int32, _i64p, _i32p]),
     "bm_graph_info": (C.c_int, [_vp, _i32p, _i32p, _i64p]),
+    "bm_bottom_up_auto": (C.c_int, [_vp, _i32p]),
+    "bm_prepare_row_index": (C.c_int, [_vp]),
     "bm_match": (C.c_int, [_vp, C.POINTER(bm_match_opts), _i32p, _i32p, _i64p, C.POINTER(bm_counters),
                            _i64p, C.c_int64, PHASE_CB, _vp]),
     "bm_load_matching": (C.c_int, [_vp, _i32p, _i32p]),

@@ -146,12 +146,21 @@ class AlgorithmResult:
     counters: Optional[PhaseCounters] = None
 
 
+def _bu_mode(bottom_up) -> int:
+    """bm_bottom_up from True / False / "auto" (or the int itself)."""
+    if isinstance(bottom_up, str):
+        return {"auto": _lib.BM_BU_AUTO, "on": _lib.BM_BU_ON, "off": _lib.BM_BU_OFF}[bottom_up]
+    if isinstance(bottom_up, bool):
+        return _lib.BM_BU_ON if bottom_up else _lib.BM_BU_OFF
+    return int(bottom_up)
+
+
 def _opts(shortest: bool, kernel: BfsKernel, improved: bool, init_mode: str, max_phases: int = 0,
-          claim_mode: int = 0, endpoint_policy: int = 0, bottom_up: bool = False):
+          claim_mode: int = 0, endpoint_policy: int = 0, bottom_up="auto"):
     o = _lib.bm_match_opts()
     o.claim_policy = claim_mode
     o.endpoint_policy = endpoint_policy
-    o.bottom_up = 1 if bottom_up else 0
+    o.bottom_up = _bu_mode(bottom_up)
     o.driver = _lib.BM_DRIVER_APSB if shortest else _lib.BM_DRIVER_APFB
     o.bfs_kernel = int(kernel)
     o.improved = 1 if improved else 0
@@ -192,7 +201,7 @@ class Engine:
         self._h = h
         self.device = device
         self._graph = None
-        self.bottom_up = False  # bm_match_opts.bottom_up default for match()/run()
+        self.bottom_up = "auto"  # bm_match_opts.bottom_up default for match()/run(): True, False or "auto"
 
     # -- lifecycle
     def close(self):
@@ -306,6 +315,17 @@ class Engine:
         m = MatchingState.unmatched(gnc, gnr)
         check(lib.bm_download_matching(self._h, i32p(m.rmatch), i32p(m.cmatch)))
         return m
+
+    def bottom_up_auto(self) -> int:
+        """BM_BU_AUTO for the resident graph (bmatch_b200.h): 0 pushes, 1 pulls dense
+        levels once the row index is prepared, 2 pulls them from the first run."""
+        v = C.c_int32()
+        check(lib.bm_bottom_up_auto(self._h, C.byref(v)))
+        return int(v.value)
+
+    def prepare_row_index(self):
+        """Build the row index now (bm_prepare_row_index), so "auto" pulls from the next run."""
+        check(lib.bm_prepare_row_index(self._h))
 
     def graph_info(self):
         nc, nr, ne = C.c_int32(), C.c_int32(), C.c_int64()

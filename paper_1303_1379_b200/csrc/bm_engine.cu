@@ -1339,7 +1339,7 @@ __global__ void __launch_bounds__(kThreads, BM_MINB) driver_kernel(Params p) {
 // ---------------------------------------------------------------------------
 // Upload-time validation (check_csr, csr_graph.cpp:45-64) and offset narrowing.
 __global__ void convert_offsets_kernel(const long long* in, unsigned* out, int nc, long long E,
-                                       unsigned long long* bad) {
+                                       unsigned long long* bad, unsigned long long* empty) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i <= nc;
        i += (long long)gridDim.x * blockDim.x) {
     const long long v = in[i];
@@ -1348,6 +1348,8 @@ __global__ void convert_offsets_kernel(const long long* in, unsigned* out, int n
     if (i == nc && v != E) ok = false;
     if (i > 0 && in[i - 1] > v) ok = false;
     if (!ok) atomicAdd(bad, 1ull);
+    const unsigned e = __ballot_sync(__activemask(), i > 0 && in[i - 1] == v);  // column i-1 is empty
+    if (e && (threadIdx.x & 31) == __ffs(__activemask()) - 1) atomicAdd(empty, (unsigned long long)__popc(e));
     out[i] = (unsigned)v;
   }
 }
@@ -1476,11 +1478,83 @@ __global__ void row_count_kernel(const int* adj, long long E, unsigned* rdeg) {
   for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < E; j += (long long)gridDim.x * blockDim.x)
     atomicAdd(rdeg + adj[j], 1u);
 }
-__global__ void transpose_scatter_kernel(const unsigned* offs, const int* adj, int nc, unsigned* cursor, int* radj) {
-  const long long warps = (long long)gridDim.x * blockDim.x / 32;
-  for (long long c = (blockIdx.x * (long long)blockDim.x + threadIdx.x) / 32; c < nc; c += warps) {
-    const unsigned b = offs[c], e = offs[c + 1];
-    for (unsigned j = b + lane_id(); j < e; j += 32) radj[atomicAdd(cursor + adj[j], 1u)] = (int)c;
+// Row index (transpose) for the pulled levels, built in two passes so that
+// the scattered writes stay inside L2. A one-pass scatter (one atomic cursor
+// bump and one 4-byte store per edge at a random place in the 4E-byte row
+// index) makes every store a partial-sector DRAM read-modify-write: 8.7 ms at
+// C2. Instead:
+//   pass A (bucket_partition_kernel) streams the CSC once and appends every
+//     edge as a (row, col) pair to the bucket of its row range; rows are
+//     bucketed so that one bucket's slice of the row index is <= 32 MB;
+//   pass B (bucket_scatter_kernel) streams the pairs bucket by bucket; the
+//     grid works on one or two buckets at a time, so the cursor bumps and the
+//     scattered stores hit one L2-resident window and leave it as full sectors.
+constexpr int kTpChunk = 2048;  // edges per CTA step of pass A (8 per thread)
+
+__global__ void bucket_base_kernel(const unsigned* roffs, int nr, int shift, int nb, unsigned* pcur) {
+  for (int b = blockIdx.x * blockDim.x + threadIdx.x; b <= nb; b += gridDim.x * blockDim.x) {
+    const long long r = min((long long)b << shift, (long long)nr);
+    pcur[b] = roffs[r];
+  }
+}
+
+// First column whose range [offs[c], offs[c+1]) holds edge j (offs ascending, offs[0] = 0).
+__device__ __forceinline__ int column_of(const unsigned* offs, int lo, int hi, unsigned j) {
+  while (hi - lo > 1) {  // invariant: offs[lo] <= j < offs[hi]
+    const int mid = (lo + hi) >> 1;
+    if (ld_ro(offs + mid) <= j) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+__global__ void __launch_bounds__(256) bucket_partition_kernel(const unsigned* offs, const int* adj, int nc,
+                                                                unsigned E, int shift, int nb, unsigned* pcur,
+                                                                int2* pairs) {
+  __shared__ unsigned hist[512];
+  __shared__ unsigned base[512];
+  __shared__ int span[2];
+  constexpr int kPer = kTpChunk / 256;
+  const unsigned nchunks = (E + kTpChunk - 1) / kTpChunk;
+  for (unsigned ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+    const unsigned j0 = ch * kTpChunk, j1 = min(E, j0 + kTpChunk);
+    for (int b = threadIdx.x; b < nb; b += blockDim.x) hist[b] = 0;
+    if (threadIdx.x < 2) span[threadIdx.x] = column_of(offs, 0, nc, threadIdx.x ? j1 - 1 : j0) + threadIdx.x;
+    __syncthreads();
+    // this thread's kPer consecutive edges [jb, je)
+    const unsigned jb = j0 + threadIdx.x * kPer, je = min(j1, jb + kPer);
+    int row[kPer];
+    unsigned short rank[kPer];
+    int col = jb < je ? column_of(offs, span[0], span[1], jb) : 0;
+    unsigned next = jb < je ? ld_ro(offs + col + 1) : 0;
+    int cols[kPer];
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const unsigned j = jb + k;
+      row[k] = -1;
+      if (j < je) {
+        while (j >= next) next = ld_ro(offs + (++col) + 1);  // empty columns are skipped
+        row[k] = ld_ro(adj + j);
+        cols[k] = col;
+        rank[k] = (unsigned short)atomicAdd(&hist[row[k] >> shift], 1u);
+      }
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < nb; b += blockDim.x)
+      if (hist[b]) base[b] = atomicAdd(pcur + b, hist[b]);
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kPer; ++k)
+      if (row[k] >= 0) pairs[base[row[k] >> shift] + rank[k]] = make_int2(row[k], cols[k]);
+    __syncthreads();
+  }
+}
+
+__global__ void bucket_scatter_kernel(const int2* pairs, unsigned E, unsigned* cursor, int* radj) {
+  // consecutive blocks take consecutive slices: the grid sweeps the buckets in order
+  for (unsigned long long j = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; j < E;
+       j += (unsigned long long)gridDim.x * blockDim.x) {
+    const int2 rc = pairs[j];
+    radj[atomicAdd(cursor + rc.x, 1u)] = rc.y;
   }
 }
 
@@ -1565,6 +1639,10 @@ struct bm_handle {
   // bottom-up levels: transposed adjacency, frontier bitmaps, frontier roots
   bool bu_enabled = false;    // the row index exists for the resident graph
   bool bu_built = false;
+  bool bu_auto = false;       // BM_BU_AUTO: the graph is of the kind whose dense levels pay to pull (upload)
+  bool bu_huge = false;       // ... and so large that one run repays building the row index
+  unsigned* tp_pcur = nullptr;  // row-index build scratch (bucket cursors, bucketed pairs)
+  int2* tp_pairs = nullptr;
   double bu_frac = 0.45;      // a level goes bottom-up when its frontier edges >= bu_frac * E
   unsigned* roffs = nullptr;
   int* radj = nullptr;
@@ -1673,8 +1751,24 @@ bm_status build_transpose(bm_handle* h, int nc, int nr, long long E) {
     BM_CUDA(cudaFreeAsync(tmp, h->stream));
     BM_CUDA(cudaMemcpyAsync(h->rcursor, h->roffs, sizeof(unsigned) * ((size_t)nr + 1), cudaMemcpyDeviceToDevice,
                             h->stream));
-    const int wb = std::max(1, std::min(h->sms * 16, (int)(((long long)nc * 32 + 255) / 256)));
-    transpose_scatter_kernel<<<wb, 256, 0, h->stream>>>(h->offs, h->adj, nc, h->rcursor, h->radj);
+    // rows bucketed so that one bucket's slice of radj is at most 32 MB
+    int shift = 0;
+    {
+      const long long nb_min = std::max<long long>(1, (E * (long long)sizeof(int) + (32ll << 20) - 1) >> 25);
+      while (shift < 31 && ((long long)nr + (1ll << shift) - 1) >> shift > nb_min) ++shift;
+    }
+    const int nb = (int)(((long long)nr + (1ll << shift) - 1) >> shift);
+    if (nb > 512) return fail(BM_ERR_INVALID_ARG, "row index: too many buckets");
+    // (the pair buffer is kept with the handle: a fresh allocation of 8E bytes per build
+    // costs more than the build itself)
+    BM_CUDA(dalloc(h->caps, h->tp_pcur, (size_t)nb + 1));
+    BM_CUDA(dalloc(h->caps, h->tp_pairs, (size_t)E));
+    unsigned* pcur = h->tp_pcur;
+    int2* pairs = h->tp_pairs;
+    bucket_base_kernel<<<(nb + 256) / 256, 256, 0, h->stream>>>(h->roffs, nr, shift, nb, pcur);
+    const int pa = (int)std::max<long long>(1, std::min<long long>((long long)h->sms * 8, (E + kTpChunk - 1) / kTpChunk));
+    bucket_partition_kernel<<<pa, 256, 0, h->stream>>>(h->offs, h->adj, nc, (unsigned)E, shift, nb, pcur, pairs);
+    bucket_scatter_kernel<<<h->sms * 8, 256, 0, h->stream>>>(pairs, (unsigned)E, h->rcursor, h->radj);
     BM_CUDA(cudaGetLastError());
   }
   h->bu_built = true;
@@ -1694,7 +1788,7 @@ bm_status check_opts(const bm_match_opts* o) {
     return fail(BM_ERR_INVALID_ARG, "unknown claim policy");
   if (o->endpoint_policy < BM_EP_AUTO || o->endpoint_policy > BM_EP_ONE_PER_TREE)
     return fail(BM_ERR_INVALID_ARG, "unknown endpoint policy");
-  if (o->bottom_up < 0 || o->bottom_up > 1) return fail(BM_ERR_INVALID_ARG, "bottom_up must be 0 or 1");
+  if (o->bottom_up < BM_BU_OFF || o->bottom_up > BM_BU_AUTO) return fail(BM_ERR_INVALID_ARG, "unknown bottom_up mode");
   // gpu_match.cpp:272-274
   if (o->improved && o->bfs_kernel != BM_BFS_WR)
     return fail(BM_ERR_LOGIC, "the endpoint-encoded alternation requires the with-root kernel");
@@ -1775,6 +1869,14 @@ bm_status launch(bm_handle* h, int v, Params& p, float* ms) {
   return BM_OK;
 }
 
+// Whether this run pulls dense levels (bm_bottom_up).
+// AUTO pulls on a qualifying graph once its row index exists (bm_prepare_row_index,
+// or an earlier ON run), or right away when the graph is so large that the
+// first run already repays the build.
+bool pulls(const bm_handle* h, const bm_match_opts& o) {
+  return o.bottom_up == BM_BU_ON || (o.bottom_up == BM_BU_AUTO && h->bu_auto && (h->bu_built || h->bu_huge));
+}
+
 Params make_params(bm_handle* h, const bm_match_opts& o) {
   Params p{};
   p.nc = h->nc;
@@ -1787,7 +1889,7 @@ Params make_params(bm_handle* h, const bm_match_opts& o) {
   p.pred = h->pred;
   p.bfs = h->bfs;
   p.dead = h->dead;
-  p.roffs = (o.bottom_up && h->bu_enabled && h->bu_built) ? h->roffs : nullptr;
+  p.roffs = (pulls(h, o) && h->bu_enabled && h->bu_built) ? h->roffs : nullptr;
   p.radj = h->radj;
   p.fbit[0] = h->fbit;
   p.fbit[1] = h->fbit ? h->fbit + h->nfbit_words : nullptr;
@@ -1841,8 +1943,9 @@ bm_status ctl_error_status(int err) {
 bm_status drive(bm_handle* h, const bm_match_opts& o, bool fresh, int64_t* cardinality,
                 bm_counters* counters, int64_t* per_iter, int64_t cap, bm_phase_cb cb, void* user,
                 int32_t* done_out, bool init_checked = false) {
-  const int v = variant_of(o.bfs_kernel == BM_BFS_WR, o.improved, o.bottom_up);
-  if (o.bottom_up && !h->bu_built) {  // one-time per resident graph
+  const bool bu = pulls(h, o);
+  const int v = variant_of(o.bfs_kernel == BM_BFS_WR, o.improved, bu);
+  if (bu && !h->bu_built) {  // one-time per resident graph
     bm_status ts = build_transpose(h, h->nc, h->nr, h->E);
     if (ts != BM_OK) return ts;
     BM_CUDA(cudaStreamSynchronize(h->stream));
@@ -2015,7 +2118,7 @@ bm_status bm_create(int32_t device, bm_handle** out) {
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->aux, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void**>(&h->ctl), sizeof(Ctrl));
   if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void**>(&h->recs), sizeof(PhaseRec) * h->rec_cap);
-  if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void**>(&h->scratch), sizeof(unsigned long long) * 4);
+  if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void**>(&h->scratch), sizeof(unsigned long long) * 8);
   if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void**>(&h->tl), sizeof(unsigned long long) * 2 * h->tl_cap);
   if (e != cudaSuccess) {
     bm_destroy(h);
@@ -2045,6 +2148,8 @@ bm_status bm_destroy(bm_handle* h) {
   dfree(h->dead);
   dfree(h->roffs);
   dfree(h->radj);
+  dfree(h->tp_pcur);
+  dfree(h->tp_pairs);
   dfree(h->rcursor);
   dfree(h->fbit);
   dfree(h->croot);
@@ -2122,9 +2227,9 @@ bm_status bm_upload_csc(bm_handle* h, int32_t nc, int32_t nr, const int64_t* cxa
   // offsets: int64 staged in F[1] (16 B per column >= 8 B per offset), narrowed to u32
   long long* staged = reinterpret_cast<long long*>(h->F[1]);
   BM_CUDA(cudaMemcpyAsync(staged, cxadj, sizeof(long long) * ((size_t)nc + 1), cudaMemcpyHostToDevice, h->stream));
-  BM_CUDA(cudaMemsetAsync(h->scratch, 0, sizeof(unsigned long long) * 4, h->stream));
+  BM_CUDA(cudaMemsetAsync(h->scratch, 0, sizeof(unsigned long long) * 5, h->stream));
   const int blocks = std::max(1, std::min(h->sms * 8, (nc + 256) / 256));
-  convert_offsets_kernel<<<blocks, 256, 0, h->stream>>>(staged, h->offs, nc, E, h->scratch);
+  convert_offsets_kernel<<<blocks, 256, 0, h->stream>>>(staged, h->offs, nc, E, h->scratch, h->scratch + 4);
   BM_CUDA(cudaGetLastError());
   BM_CUDA(cudaEventRecord(h->ev_up, h->stream));
   BM_CUDA(cudaStreamWaitEvent(h->aux, h->ev_up, 0));
@@ -2143,9 +2248,16 @@ bm_status bm_upload_csc(bm_handle* h, int32_t nc, int32_t nr, const int64_t* cxa
   BM_CUDA(cudaGetLastError());
   BM_CUDA(cudaEventRecord(h->ev_up, h->aux));
   BM_CUDA(cudaStreamWaitEvent(h->stream, h->ev_up, 0));
-  unsigned long long bad[4] = {0, 0, 0, 0};
+  unsigned long long bad[5] = {0, 0, 0, 0, 0};
   BM_CUDA(cudaMemcpyAsync(bad, h->scratch, sizeof(bad), cudaMemcpyDeviceToHost, h->stream));
   BM_CUDA(cudaStreamSynchronize(h->stream));
+  {  // BM_BU_AUTO (bmatch_b200.h): large, few empty columns, average degree >= 8 over the rest
+    const long long nonempty = (long long)nc - (long long)bad[4];
+    h->bu_auto = nr >= (1 << 21) && nonempty * 4 >= 3ll * nc && E >= 8 * nonempty;
+    h->bu_huge = nr >= (1 << 26);  // rmatch >= 256 MB: pushed dense levels pay DRAM sectors per gather
+    const char* fa = getenv("BM_BU_AUTO");
+    if (fa && *fa) h->bu_auto = h->bu_huge = atoi(fa) != 0;
+  }
   if (bad[0]) return fail(BM_ERR_INVALID_ARG, "cxadj is not a valid offset array (cxadj[0]=0, non-decreasing, cxadj[nc]=E)");
   if (bad[1]) return fail(BM_ERR_INVALID_ARG, "row index out of range in cadj");
   bad[2] -= bad[3];  // descending pairs inside columns
@@ -2160,6 +2272,25 @@ bm_status bm_upload_csc(bm_handle* h, int32_t nc, int32_t nr, const int64_t* cxa
   h->nc = nc;
   h->nr = nr;
   h->E = E;
+  return BM_OK;
+}
+
+bm_status bm_prepare_row_index(bm_handle* h) {
+  bm_status s = check_handle(h, true);
+  if (s != BM_OK) return s;
+  BM_CUDA(cudaSetDevice(h->device));
+  if (!h->bu_built) {
+    s = build_transpose(h, h->nc, h->nr, h->E);
+    if (s != BM_OK) return s;
+  }
+  BM_CUDA(cudaStreamSynchronize(h->stream));
+  return BM_OK;
+}
+
+bm_status bm_bottom_up_auto(bm_handle* h, int32_t* enabled) {
+  bm_status s = check_handle(h, true);
+  if (s != BM_OK) return s;
+  if (enabled) *enabled = h->bu_auto ? (h->bu_huge ? 2 : 1) : 0;
   return BM_OK;
 }
 

@@ -298,3 +298,38 @@ def test_bottom_up_levels_parity(oracle, corpus, monkeypatch):
             assert oracle.validate(g, m.rmatch, m.cmatch) == 0
             assert oracle.is_maximum(g, m.rmatch, m.cmatch) == 1
     eng.close()
+
+
+def test_bottom_up_auto_decision_and_row_index(oracle, monkeypatch):
+    """BM_BU_AUTO: small graphs push; a large, even-degree graph pulls its dense
+    levels. The row index the pulled levels read is built by the bucketed
+    two-pass transpose; forcing AUTO on for small graphs (so the index is
+    built for graphs of every shape, including empty columns and rows) must
+    keep every maximum."""
+    eng = bm.Engine(0)
+    small = bm.generate_random_bipartite(20000, 20000, 8.0, 1)
+    eng.upload(small)
+    assert not eng.bottom_up_auto()
+    big = bm.generate_random_bipartite(1 << 21, 1 << 21, 9.0, 2)
+    eng.upload(big, force=True)
+    assert eng.bottom_up_auto() == 1  # qualifies; pulls once the row index is prepared
+    eng.prepare_row_index()
+    init = bm.cheap_matching(big)
+    res = eng.match(big, init)  # default "auto": pulled levels
+    eng.bottom_up = False
+    push = eng.match(big, init)
+    assert bm.cardinality(res.matching) == bm.cardinality(push.matching)
+    viol, ismax, _ = eng.verify(big, res.matching)
+    assert viol == 0 and ismax
+    eng.bottom_up = "auto"
+    monkeypatch.setenv("BM_BU_AUTO", "1")
+    monkeypatch.setenv("BM_BU_FRAC", "0")
+    monkeypatch.setenv("BM_SOLO_EDGES", "0")
+    for g in [small, bm.generate_rmat(14, 8.0, 5), bm.generate_banded(30000, 3, 0.1, 6)[0],
+              bm.BipartiteCsr.from_edge_list(5, 4, [(1, 0), (1, 3), (4, 3)])]:
+        eng.upload(g, force=True)
+        assert eng.bottom_up_auto() == 2
+        m = eng.match(g, bm.cheap_matching(g)).matching
+        assert bm.cardinality(m) == oracle.maximum(g)
+        assert oracle.validate(g, m.rmatch, m.cmatch) == 0
+    eng.close()
