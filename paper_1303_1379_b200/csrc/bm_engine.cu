@@ -1474,27 +1474,46 @@ __global__ void init_check_kernel(const int* rmatch, const int* cmatch, int nc, 
 
 // Transposed adjacency (rows -> columns) for bottom-up levels: count,
 // exclusive scan (CUB), scatter. Row lists come out unsorted (not needed).
-__global__ void row_count_kernel(const int* adj, long long E, unsigned* rdeg) {
-  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < E; j += (long long)gridDim.x * blockDim.x)
-    atomicAdd(rdeg + adj[j], 1u);
-}
-// Row index (transpose) for the pulled levels, built in two passes so that
-// the scattered writes stay inside L2. A one-pass scatter (one atomic cursor
-// bump and one 4-byte store per edge at a random place in the 4E-byte row
-// index) makes every store a partial-sector DRAM read-modify-write: 8.7 ms at
-// C2. Instead:
-//   pass A (bucket_partition_kernel) streams the CSC once and appends every
-//     edge as a (row, col) pair to the bucket of its row range; rows are
-//     bucketed so that one bucket's slice of the row index is <= 32 MB;
-//   pass B (bucket_scatter_kernel) streams the pairs bucket by bucket; the
-//     grid works on one or two buckets at a time, so the cursor bumps and the
-//     scattered stores hit one L2-resident window and leave it as full sectors.
-constexpr int kTpChunk = 2048;  // edges per CTA step of pass A (8 per thread)
+// Row index (transpose) for the pulled levels. A one-pass scatter (an atomic
+// cursor bump and a 4-byte store per edge at a random place of the 4E-byte
+// index, after an atomic degree count into nr counters) turns every access
+// into a partial-sector DRAM read-modify-write once the arrays outgrow L2:
+// 9.6 ms at C2, ~300 ms at C5. Instead the edges are first bucketed by row
+// range, so that everything after that works inside one L2-sized window:
+//   bucket_hist   bucket sizes (NB <= 512 counters, CTA-aggregated)
+//   bucket_partition  streams the CSC once and appends every edge as a
+//                 (row, col) pair to its bucket (CTA-staged runs)
+//   pair_count    row degrees, streaming the pairs bucket by bucket
+//   (CUB scan)    row offsets
+//   pair_scatter  the row index, streaming the pairs bucket by bucket
+// The last two hand out chunks in order from a global counter, so the whole
+// grid stays within one or two buckets: each bucket's counters (<= 2 MB) and
+// slice of the index (<= 32 MB) stay in L2 and leave it as full sectors.
+constexpr int kTpChunk = 2048;   // edges per CTA step of bucket_partition (8 per thread)
+constexpr int kPairChunk = 4096; // pairs per CTA step of the ordered passes (16 per thread)
+constexpr int kMaxBuckets = 512;
 
-__global__ void bucket_base_kernel(const unsigned* roffs, int nr, int shift, int nb, unsigned* pcur) {
-  for (int b = blockIdx.x * blockDim.x + threadIdx.x; b <= nb; b += gridDim.x * blockDim.x) {
-    const long long r = min((long long)b << shift, (long long)nr);
-    pcur[b] = roffs[r];
+__global__ void __launch_bounds__(256) bucket_hist_kernel(const int* adj, unsigned E, int shift, int nb,
+                                                          unsigned* bcount) {
+  __shared__ unsigned hist[kMaxBuckets];
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) hist[b] = 0;
+  __syncthreads();
+  for (unsigned long long j = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; j < E;
+       j += (unsigned long long)gridDim.x * blockDim.x)
+    atomicAdd(&hist[ld_ro(adj + j) >> shift], 1u);
+  __syncthreads();
+  for (int b = threadIdx.x; b < nb; b += blockDim.x)
+    if (hist[b]) atomicAdd(bcount + b, hist[b]);
+}
+
+// pcur[b] = first pair slot of bucket b (exclusive scan of nb <= 512 counts).
+__global__ void bucket_base_kernel(const unsigned* bcount, int nb, unsigned* pcur) {
+  if (threadIdx.x == 0) {
+    unsigned run = 0;
+    for (int b = 0; b < nb; ++b) {
+      pcur[b] = run;
+      run += bcount[b];
+    }
   }
 }
 
@@ -1510,8 +1529,12 @@ __device__ __forceinline__ int column_of(const unsigned* offs, int lo, int hi, u
 __global__ void __launch_bounds__(256) bucket_partition_kernel(const unsigned* offs, const int* adj, int nc,
                                                                 unsigned E, int shift, int nb, unsigned* pcur,
                                                                 int2* pairs) {
-  __shared__ unsigned hist[512];
-  __shared__ unsigned base[512];
+  __shared__ unsigned hist[kMaxBuckets];
+  __shared__ unsigned base[kMaxBuckets];   // global slot of this chunk's run of each bucket
+  __shared__ unsigned lbase[kMaxBuckets];  // its slot in the stage
+  __shared__ unsigned wsum[8];
+  __shared__ int2 stage[kTpChunk];
+  __shared__ unsigned short sbk[kTpChunk];
   __shared__ int span[2];
   constexpr int kPer = kTpChunk / 256;
   const unsigned nchunks = (E + kTpChunk - 1) / kTpChunk;
@@ -1539,22 +1562,70 @@ __global__ void __launch_bounds__(256) bucket_partition_kernel(const unsigned* o
       }
     }
     __syncthreads();
-    for (int b = threadIdx.x; b < nb; b += blockDim.x)
-      if (hist[b]) base[b] = atomicAdd(pcur + b, hist[b]);
+    // CTA-local bucket-major order: exclusive scan of the (<= 512) bucket counts,
+    // two per thread; then one global reservation per non-empty bucket
+    {
+      const int b0 = 2 * threadIdx.x;
+      const unsigned c0 = b0 < nb ? hist[b0] : 0u, c1 = b0 + 1 < nb ? hist[b0 + 1] : 0u;
+      const unsigned incl = warp_incl_scan(c0 + c1);
+      if (lane_id() == 31) wsum[threadIdx.x >> 5] = incl;
+      __syncthreads();
+      unsigned wb = 0;
+      for (int w = 0; w < (int)(threadIdx.x >> 5); ++w) wb += wsum[w];
+      const unsigned ex = wb + incl - (c0 + c1);
+      if (b0 < nb) {
+        lbase[b0] = ex;
+        if (c0) base[b0] = atomicAdd(pcur + b0, c0);
+      }
+      if (b0 + 1 < nb) {
+        lbase[b0 + 1] = ex + c0;
+        if (c1) base[b0 + 1] = atomicAdd(pcur + b0 + 1, c1);
+      }
+    }
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < kPer; ++k)
-      if (row[k] >= 0) pairs[base[row[k] >> shift] + rank[k]] = make_int2(row[k], cols[k]);
+      if (row[k] >= 0) {
+        const unsigned b = (unsigned)row[k] >> shift;
+        const unsigned slot = lbase[b] + rank[k];
+        stage[slot] = make_int2(row[k], cols[k]);
+        sbk[slot] = (unsigned short)b;
+      }
+    __syncthreads();
+    // runs of one bucket are contiguous in the stage and in the output: coalesced stores
+    for (unsigned i = threadIdx.x; i < j1 - j0; i += blockDim.x) {
+      const unsigned b = sbk[i];
+      pairs[base[b] + (i - lbase[b])] = stage[i];
+    }
     __syncthreads();
   }
 }
 
-__global__ void bucket_scatter_kernel(const int2* pairs, unsigned E, unsigned* cursor, int* radj) {
-  // consecutive blocks take consecutive slices: the grid sweeps the buckets in order
-  for (unsigned long long j = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; j < E;
-       j += (unsigned long long)gridDim.x * blockDim.x) {
-    const int2 rc = pairs[j];
-    radj[atomicAdd(cursor + rc.x, 1u)] = rc.y;
+// Ordered passes over the bucketed pairs: chunks are handed out in order, so
+// the grid's working set is one or two buckets wide.
+template <bool kScatter>
+__global__ void __launch_bounds__(256) pair_pass_kernel(const int2* pairs, unsigned E, unsigned* ticket,
+                                                        unsigned* cursor, int* radj) {
+  __shared__ unsigned chunk;
+  constexpr int kPer = kPairChunk / 256;
+  for (;;) {
+    if (threadIdx.x == 0) chunk = atomicAdd(ticket, 1u);
+    __syncthreads();
+    const unsigned long long j0 = (unsigned long long)chunk * kPairChunk;
+    __syncthreads();
+    if (j0 >= E) break;
+    int2 rc[kPer];
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const unsigned long long j = j0 + k * 256 + threadIdx.x;
+      rc[k] = j < E ? pairs[j] : make_int2(-1, 0);
+    }
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      if (rc[k].x < 0) continue;
+      if (kScatter) radj[atomicAdd(cursor + rc[k].x, 1u)] = rc[k].y;
+      else atomicAdd(cursor + rc[k].x, 1u);
+    }
   }
 }
 
@@ -1739,10 +1810,31 @@ bm_status build_transpose(bm_handle* h, int nc, int nr, long long E) {
     h->nfbit_words = (nc + 31) / 32;
     BM_CUDA(dalloc(h->caps, h->fbit, (size_t)2 * h->nfbit_words));
     BM_CUDA(dalloc(h->caps, h->croot, (size_t)nc));
+    // rows bucketed so that one bucket's slice of radj is at most 32 MB
+    int shift = 0;
+    {
+      const long long nb_min = std::max<long long>(1, (E * (long long)sizeof(int) + (32ll << 20) - 1) >> 25);
+      while (shift < 31 && ((long long)nr + (1ll << shift) - 1) >> shift > nb_min) ++shift;
+    }
+    const int nb = (int)(((long long)nr + (1ll << shift) - 1) >> shift);
+    if (nb > kMaxBuckets) return fail(BM_ERR_INVALID_ARG, "row index: too many buckets");
+    // scratch kept with the handle (a fresh 8E-byte allocation per build costs more than the build):
+    // [0, nb) bucket cursors, [kMaxBuckets, +nb) bucket counts, [2 kMaxBuckets, +2) tickets
+    BM_CUDA(dalloc(h->caps, h->tp_pcur, (size_t)2 * kMaxBuckets + 2));
+    BM_CUDA(dalloc(h->caps, h->tp_pairs, (size_t)E));
+    unsigned* pcur = h->tp_pcur;
+    unsigned* bcount = h->tp_pcur + kMaxBuckets;
+    unsigned* tickets = h->tp_pcur + 2 * kMaxBuckets;
+    int2* pairs = h->tp_pairs;
+    BM_CUDA(cudaMemsetAsync(h->tp_pcur, 0, sizeof(unsigned) * (2 * kMaxBuckets + 2), h->stream));
     BM_CUDA(cudaMemsetAsync(h->rcursor, 0, sizeof(unsigned) * ((size_t)nr + 1), h->stream));
     BM_CUDA(cudaMemsetAsync(h->fbit, 0, sizeof(unsigned) * 2 * h->nfbit_words, h->stream));
-    const int eb = (int)std::max<long long>(1, std::min<long long>((long long)h->sms * 8, (E + 255) / 256));
-    row_count_kernel<<<eb, 256, 0, h->stream>>>(h->adj, E, h->rcursor);
+    const int grid = h->sms * 8;
+    bucket_hist_kernel<<<grid, 256, 0, h->stream>>>(h->adj, (unsigned)E, shift, nb, bcount);
+    bucket_base_kernel<<<1, 32, 0, h->stream>>>(bcount, nb, pcur);
+    const int pa = (int)std::max<long long>(1, std::min<long long>((long long)grid, (E + kTpChunk - 1) / kTpChunk));
+    bucket_partition_kernel<<<pa, 256, 0, h->stream>>>(h->offs, h->adj, nc, (unsigned)E, shift, nb, pcur, pairs);
+    pair_pass_kernel<false><<<grid, 256, 0, h->stream>>>(pairs, (unsigned)E, tickets, h->rcursor, nullptr);
     size_t tmp_bytes = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, h->rcursor, h->roffs, nr + 1, h->stream);
     void* tmp = nullptr;
@@ -1751,24 +1843,7 @@ bm_status build_transpose(bm_handle* h, int nc, int nr, long long E) {
     BM_CUDA(cudaFreeAsync(tmp, h->stream));
     BM_CUDA(cudaMemcpyAsync(h->rcursor, h->roffs, sizeof(unsigned) * ((size_t)nr + 1), cudaMemcpyDeviceToDevice,
                             h->stream));
-    // rows bucketed so that one bucket's slice of radj is at most 32 MB
-    int shift = 0;
-    {
-      const long long nb_min = std::max<long long>(1, (E * (long long)sizeof(int) + (32ll << 20) - 1) >> 25);
-      while (shift < 31 && ((long long)nr + (1ll << shift) - 1) >> shift > nb_min) ++shift;
-    }
-    const int nb = (int)(((long long)nr + (1ll << shift) - 1) >> shift);
-    if (nb > 512) return fail(BM_ERR_INVALID_ARG, "row index: too many buckets");
-    // (the pair buffer is kept with the handle: a fresh allocation of 8E bytes per build
-    // costs more than the build itself)
-    BM_CUDA(dalloc(h->caps, h->tp_pcur, (size_t)nb + 1));
-    BM_CUDA(dalloc(h->caps, h->tp_pairs, (size_t)E));
-    unsigned* pcur = h->tp_pcur;
-    int2* pairs = h->tp_pairs;
-    bucket_base_kernel<<<(nb + 256) / 256, 256, 0, h->stream>>>(h->roffs, nr, shift, nb, pcur);
-    const int pa = (int)std::max<long long>(1, std::min<long long>((long long)h->sms * 8, (E + kTpChunk - 1) / kTpChunk));
-    bucket_partition_kernel<<<pa, 256, 0, h->stream>>>(h->offs, h->adj, nc, (unsigned)E, shift, nb, pcur, pairs);
-    bucket_scatter_kernel<<<h->sms * 8, 256, 0, h->stream>>>(pairs, (unsigned)E, h->rcursor, h->radj);
+    pair_pass_kernel<true><<<grid, 256, 0, h->stream>>>(pairs, (unsigned)E, tickets + 1, h->rcursor, h->radj);
     BM_CUDA(cudaGetLastError());
   }
   h->bu_built = true;
