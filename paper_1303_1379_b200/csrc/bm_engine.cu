@@ -82,6 +82,11 @@ constexpr int kThreads = BM_THREADS;  // threads per CTA (1024 / kThreads CTAs p
 #define BM_MINB (1024 / BM_THREADS)
 #endif
 constexpr int kItems = BM_ITEMS;      // edges per thread per round (memory-level parallelism)
+#ifndef BM_EPT
+#define BM_EPT 1
+#endif
+constexpr int kEPT = BM_EPT;          // frontier entries per thread in a push window
+constexpr int kWin = kThreads * kEPT; // entries per push window
 #ifndef BM_GRAN
 #define BM_GRAN 512
 #endif
@@ -259,10 +264,10 @@ __device__ __forceinline__ void tl_mark(const Params& p, unsigned kind, unsigned
 struct Smem {
   union {  // a top-down window, or a bottom-up candidate stage (never both at once)
     struct {
-      unsigned pre[kThreads + 1];  // window: raw edge prefix of each entry, then the live-edge prefix
-      int col[kThreads];
-      int root[kThreads];
-      unsigned beg[kThreads];      // first live adjacency index of each entry in this window
+      unsigned pre[kWin + 1];      // window: raw edge prefix of each entry, then the live-edge prefix
+      int col[kWin];
+      int root[kWin];
+      unsigned beg[kWin];          // first live adjacency index of each entry in this window
     };
     struct {
       int bcand[2 * kThreads];     // bottom-up: candidate rows of a sweep step ...
@@ -669,36 +674,46 @@ __device__ __forceinline__ void expand_level(const Params& p, Smem& sm, int4* F,
     unsigned i = (unsigned)ld_cg(reinterpret_cast<const int*>(gin) + e0 / kGran);  // entry holding edge e0
     unsigned e = e0;
     while (e < e1) {
-      // Window of up to kThreads entries starting at i.
-      const unsigned wi = i + tid;
-      if (wi < n) {
-        const int4 ent = ld_cg_stream(F + ls + wi, pol);
-        bool skip = false;
-        if (WR) skip = root_dead(p, ent.y);  // early exit (gpu_match.cpp:106-108)
-        sm.col[tid] = ent.x;
-        sm.root[tid] = skip ? -1 : ent.y;
-        sm.beg[tid] = (unsigned)ent.z;
-        sm.pre[tid] = (unsigned)ent.w;
-        if ((unsigned)ent.w >= e0 && (unsigned)ent.w < e1) {
-          c_entries++;
-          if (!skip) c_cexp++;
+      // Window of up to kWin entries starting at i (thread t holds entries t*kEPT ..).
+#pragma unroll
+      for (int k = 0; k < kEPT; ++k) {
+        const unsigned sl0 = tid * kEPT + k;
+        const unsigned wi = i + sl0;
+        if (wi < n) {
+          const int4 ent = ld_cg_stream(F + ls + wi, pol);
+          bool skip = false;
+          if (WR) skip = root_dead(p, ent.y);  // early exit (gpu_match.cpp:106-108)
+          sm.col[sl0] = ent.x;
+          sm.root[sl0] = skip ? -1 : ent.y;
+          sm.beg[sl0] = (unsigned)ent.z;
+          sm.pre[sl0] = (unsigned)ent.w;
+          if ((unsigned)ent.w >= e0 && (unsigned)ent.w < e1) {
+            c_entries++;
+            if (!skip) c_cexp++;
+          }
+        } else {
+          sm.pre[sl0] = T;
+          sm.root[sl0] = -1;
         }
-      } else {
-        sm.pre[tid] = T;
-        sm.root[tid] = -1;
       }
-      if (tid == 0) sm.pre[kThreads] = (i + kThreads < n) ? ld_cg_u(F + ls + i + kThreads) : T;
+      if (tid == 0) sm.pre[kWin] = (i + kWin < n) ? ld_cg_u(F + ls + i + kWin) : T;
       __syncthreads();
-      const unsigned wend = min(e1, sm.pre[kThreads]);
+      const unsigned wend = min(e1, sm.pre[kWin]);
       // Compact the window to its live edges: entries of trees that already
       // found a path (WR) and edge ranges outside [e, wend) contribute none.
       unsigned live;
       {
-        const unsigned lo = max(sm.pre[tid], e);
-        const unsigned hi = min(sm.pre[tid + 1], wend);
-        const unsigned len = (sm.root[tid] >= 0 && hi > lo) ? hi - lo : 0u;
-        const unsigned nb = sm.beg[tid] + (lo - sm.pre[tid]);
-        const unsigned incl = warp_incl_scan(len);
+        unsigned len[kEPT], nb[kEPT], tsum = 0;
+#pragma unroll
+        for (int k = 0; k < kEPT; ++k) {
+          const unsigned sl0 = tid * kEPT + k;
+          const unsigned lo = max(sm.pre[sl0], e);
+          const unsigned hi = min(sm.pre[sl0 + 1], wend);
+          len[k] = (sm.root[sl0] >= 0 && hi > lo) ? hi - lo : 0u;
+          nb[k] = sm.beg[sl0] + (lo - sm.pre[sl0]);
+          tsum += len[k];
+        }
+        const unsigned incl = warp_incl_scan(tsum);
         if (lane_id() == 31) sm.wtot[tid >> 5] = incl;
         __syncthreads();
         unsigned wbase = 0, tot = 0;
@@ -709,14 +724,19 @@ __device__ __forceinline__ void expand_level(const Params& p, Smem& sm, int4* F,
           tot += t;
         }
         live = tot;
-        const unsigned vp = wbase + incl - len;
-        sm.beg[tid] = nb;
-        sm.pre[tid] = vp;  // live-edge prefix (ties resolve to the last entry)
-        if (tid == 0) sm.pre[kThreads] = tot;
-        if (len) {  // coarse index: this entry holds live edges 32q for q in [ceil(vp/32), (vp+len-1)/32]
-          const unsigned q1 = (vp + len - 1) >> 5;
-          for (unsigned q = (vp + 31) >> 5; q <= q1; ++q) sm.cgr[q] = (unsigned short)tid;
+        unsigned vp = wbase + incl - tsum;
+#pragma unroll
+        for (int k = 0; k < kEPT; ++k) {
+          const unsigned sl0 = tid * kEPT + k;
+          sm.beg[sl0] = nb[k];
+          sm.pre[sl0] = vp;  // live-edge prefix (ties resolve to the last entry)
+          if (len[k]) {  // coarse index: this entry holds live edges 32q for q in [ceil(vp/32), (vp+len-1)/32]
+            const unsigned q1 = (vp + len[k] - 1) >> 5;
+            for (unsigned q = (vp + 31) >> 5; q <= q1; ++q) sm.cgr[q] = (unsigned short)sl0;
+          }
+          vp += len[k];
         }
+        if (tid == 0) sm.pre[kWin] = tot;
         __syncthreads();
       }
       const unsigned nq = (live + 31) >> 5;
@@ -726,8 +746,9 @@ __device__ __forceinline__ void expand_level(const Params& p, Smem& sm, int4* F,
         t_a = t;
       }
       // Prefetch the next window's entries while this window's rounds run.
-      if (wend < e1 && i + kThreads + tid < n)
-        prefetch_l2(F + ls + i + kThreads + tid);
+#pragma unroll
+      for (int k = 0; k < kEPT; ++k)
+        if (wend < e1 && i + kWin + k * kThreads + tid < n) prefetch_l2(F + ls + i + kWin + k * kThreads + tid);
 
       // Rounds over the live edges: no CTA-wide barrier inside; winners are
       // staged in sm.wbuf.
@@ -742,7 +763,7 @@ __device__ __forceinline__ void expand_level(const Params& p, Smem& sm, int4* F,
             // the entry holding ee lies in [cgr[q], cgr[q+1]] (1-2 steps for typical degrees)
             const unsigned q = ee >> 5;
             int a = sm.cgr[q];
-            int b = (q + 1 < nq) ? (int)sm.cgr[q + 1] + 1 : kThreads;
+            int b = (q + 1 < nq) ? (int)sm.cgr[q + 1] + 1 : kWin;
             while (b - a > 1) {
               const int mid = (a + b) >> 1;
               if (sm.pre[mid] <= ee) a = mid; else b = mid;
@@ -839,7 +860,7 @@ __device__ __forceinline__ void expand_level(const Params& p, Smem& sm, int4* F,
       // Flush the window's winners: one CTA reservation for all of them.
       flush_winners(p, sm, F, out_base, gout, out, pol);
       e = wend;
-      i += kThreads;
+      i += kWin;
       __syncthreads();
       if (tid == 0) {
         const long long t = clk();
