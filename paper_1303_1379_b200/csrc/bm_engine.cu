@@ -523,6 +523,10 @@ __device__ __forceinline__ void bu_sweep(const Params& p, Smem& sm, int4* F, uns
   // until the first frontier member; (3) winners are flushed as frontier
   // entries. Candidates reuse the window arrays of Smem (col/root/beg/pre).
   constexpr int kBuRows = 8;
+#ifndef BM_BU_PROBE
+#define BM_BU_PROBE 4
+#endif
+  constexpr int kBuProbe = BM_BU_PROBE;
   const unsigned* fb = p.fbit[lv & 1];
   const unsigned long long pol = policy_evict_first();
   unsigned* const path_flag = &p.ctl->path_found[pf];
@@ -570,32 +574,47 @@ __device__ __forceinline__ void bu_sweep(const Params& p, Smem& sm, int4* F, uns
           const int vv = sm.bcandv[t0 + threadIdx.x];
           const unsigned j0 = ld_ro(p.roffs + rr), j1 = ld_ro(p.roffs + rr + 1);
           c_rows++;
-          for (unsigned j = j0; j < j1; ++j) {
-            const int c = ld_stream(p.radj + j, pol);
-            c_trav++;
-            if (!((ld_ca(reinterpret_cast<const int*>(fb) + (c >> 5)) >> (c & 31)) & 1)) continue;
-            const int root = ld_cg(p.croot + c);
-            if (vv >= 0) {  // matched row: its column joins the frontier below c's tree
-              st_plain(RM(p, rr), vv | kVisBit);
+          // kBuProbe neighbours per step: their index loads and frontier-bit loads
+          // are independent, so a row that scans far waits kBuProbe x fewer round trips
+          bool done = false;
+          for (unsigned jb = j0; jb < j1 && !done; jb += kBuProbe) {
+            int cs[kBuProbe];
+            unsigned wd[kBuProbe];
+#pragma unroll
+            for (int k = 0; k < kBuProbe; ++k) cs[k] = jb + k < j1 ? ld_stream(p.radj + jb + k, pol) : -1;
+#pragma unroll
+            for (int k = 0; k < kBuProbe; ++k)
+              wd[k] = cs[k] >= 0 ? ld_ca(reinterpret_cast<const int*>(fb) + (cs[k] >> 5)) : 0u;
+#pragma unroll
+            for (int k = 0; k < kBuProbe; ++k) {
+              const int c = cs[k];
+              if (done || c < 0) continue;
+              c_trav++;
+              if (!((wd[k] >> (c & 31)) & 1)) continue;
+              const int root = ld_cg(p.croot + c);
+              if (vv >= 0) {  // matched row: its column joins the frontier below c's tree
+                st_plain(RM(p, rr), vv | kVisBit);
+                st_plain(PR(p, rr), c);
+                win = true;
+                cw = vv;
+                rootw = root;
+                done = true;
+                continue;
+              }
+              // free row: an endpoint of c's tree
+              const bool one = WR && p.ep_one;
+              if (one && root_dead(p, root)) continue;
+              bool mine = true;
+              if (one) mine = atomicCAS(p.bfs + root, kStartLevel, IMP ? -rr : kFoundMark) == kStartLevel;
+              else if (WR) st_rlx(p.bfs + root, IMP ? -rr : kFoundMark);
+              if (!mine) continue;  // that tree already holds an endpoint: try another neighbour
+              if (WR) mark_dead(p, root);
+              st_rlx(RM(p, rr), -2);
               st_plain(PR(p, rr), c);
-              win = true;
-              cw = vv;
-              rootw = root;
-              break;
+              ep = true;
+              if (ld_rlx(path_flag) == 0u) st_rlx(path_flag, 1u);
+              done = true;
             }
-            // free row: an endpoint of c's tree
-            const bool one = WR && p.ep_one;
-            if (one && root_dead(p, root)) continue;
-            bool mine = true;
-            if (one) mine = atomicCAS(p.bfs + root, kStartLevel, IMP ? -rr : kFoundMark) == kStartLevel;
-            else if (WR) st_rlx(p.bfs + root, IMP ? -rr : kFoundMark);
-            if (!mine) continue;  // that tree already holds an endpoint: try another neighbour
-            if (WR) mark_dead(p, root);
-            st_rlx(RM(p, rr), -2);
-            st_plain(PR(p, rr), c);
-            ep = true;
-            if (ld_rlx(path_flag) == 0u) st_rlx(path_flag, 1u);
-            break;
           }
         }
         c_nvis += win ? 1u : 0u;

@@ -9,6 +9,9 @@ for cfg in cfgs:
     g, known = bench.build_graph(cfg, 1)
     init = bm.cheap_matching(g)
     eng = bm.Engine(0); eng.upload(g); eng.load_matching(init)
+    if os.environ.get("PERF_BU") == "1":  # pulled dense levels (AUTO with a prepared row index)
+        eng.prepare_row_index()
+        eng.bottom_up = True
     eng.run()
     ms, ph, lv, ok = [], [], [], True
     for _ in range(5):
