@@ -33,7 +33,8 @@
  * Tuning environment variables (read at upload / launch; defaults are the
  * measured best): BM_ROW_LAYOUT=plain|interleave (row-state
  * layout, default by rmatch size), BM_BU_FRAC (share of the edges a frontier
- * must hold to be pulled when bottom_up is set, default 0.45), BM_BU_AUTO
+ * must hold to be pulled: default 0.45, or 0.2 once the row state is
+ * interleaved, i.e. far beyond L2), BM_BU_AUTO
  * (0|1: overrides the AUTO decision), BM_SOLO_EDGES
  * (widest level run by one CTA, default 1024), BM_PERSIST_MB (L2 persisting
  * window on the row state, default off).

@@ -1754,6 +1754,7 @@ struct bm_handle {
   bool bu_huge = false;       // ... and so large that one run repays building the row index
   unsigned* tp_pcur = nullptr;  // row-index build scratch (bucket cursors, bucketed pairs)
   int2* tp_pairs = nullptr;
+  unsigned char* tp_tmp = nullptr;  // CUB scan scratch
   double bu_frac = 0.45;      // a level goes bottom-up when its frontier edges >= bu_frac * E
   unsigned* roffs = nullptr;
   int* radj = nullptr;
@@ -1840,6 +1841,11 @@ bm_status rows_to_host(bm_handle* h, int32_t* out, int off) {
 bm_status build_transpose(bm_handle* h, int nc, int nr, long long E) {
   {
     h->bu_enabled = nr > 0 && nc > 0 && E > 0;
+    // Pull threshold (share of the edges in the frontier). Once the row state is
+    // far beyond L2 (the interleaved layout) every pushed gather pays DRAM
+    // sectors, so pulling pays from sparser frontiers: measured optimum 0.15-0.25
+    // on C5 against 0.45-0.6 on C2 (profiles/README.md).
+    h->bu_frac = h->rs == 2 ? 0.2 : 0.45;
     const char* fr = getenv("BM_BU_FRAC");
     if (fr) h->bu_frac = atof(fr);
   }
@@ -1877,10 +1883,10 @@ bm_status build_transpose(bm_handle* h, int nc, int nr, long long E) {
     pair_pass_kernel<false><<<grid, 256, 0, h->stream>>>(pairs, (unsigned)E, tickets, h->rcursor, nullptr);
     size_t tmp_bytes = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, h->rcursor, h->roffs, nr + 1, h->stream);
-    void* tmp = nullptr;
-    BM_CUDA(cudaMallocAsync(&tmp, std::max<size_t>(tmp_bytes, 1), h->stream));
-    cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, h->rcursor, h->roffs, nr + 1, h->stream);
-    BM_CUDA(cudaFreeAsync(tmp, h->stream));
+    // kept with the handle too: a stream-ordered allocation here cost 3-115 ms per build
+    // (the default pool hands its memory back at every synchronisation)
+    BM_CUDA(dalloc(h->caps, h->tp_tmp, tmp_bytes));
+    cub::DeviceScan::ExclusiveSum(h->tp_tmp, tmp_bytes, h->rcursor, h->roffs, nr + 1, h->stream);
     BM_CUDA(cudaMemcpyAsync(h->rcursor, h->roffs, sizeof(unsigned) * ((size_t)nr + 1), cudaMemcpyDeviceToDevice,
                             h->stream));
     pair_pass_kernel<true><<<grid, 256, 0, h->stream>>>(pairs, (unsigned)E, tickets + 1, h->rcursor, h->radj);
@@ -2265,6 +2271,7 @@ bm_status bm_destroy(bm_handle* h) {
   dfree(h->radj);
   dfree(h->tp_pcur);
   dfree(h->tp_pairs);
+  dfree(h->tp_tmp);
   dfree(h->rcursor);
   dfree(h->fbit);
   dfree(h->croot);
