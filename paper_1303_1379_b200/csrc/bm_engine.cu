@@ -270,8 +270,8 @@ struct Smem {
       unsigned beg[kWin];          // first live adjacency index of each entry in this window
     };
     struct {
-      int bcand[2 * kThreads];     // bottom-up: candidate rows of a sweep step ...
-      int bcandv[2 * kThreads];    // ... and their rmatch values
+      int bcand[4 * kThreads];     // bottom-up: candidate rows of a sweep step (per warp) ...
+      int bcandv[4 * kThreads];    // ... and their rmatch values
     };
   };
   unsigned wtot[kThreads / 32];
@@ -517,12 +517,14 @@ __device__ __forceinline__ void bu_prep(const Params& p, const int4* F, unsigned
 template <bool WR, bool IMP>
 __device__ __forceinline__ void bu_sweep(const Params& p, Smem& sm, int4* F, unsigned out_base, unsigned* gout,
                                          Slot* out, int lv, int pf) {
-  // Per CTA iteration: (1) kBuRows rows per thread are screened with
-  // independent loads and the candidates (unvisited matched rows and free rows)
-  // are compacted into shared memory; (2) each candidate scans its columns
-  // until the first frontier member; (3) winners are flushed as frontier
-  // entries. Candidates reuse the window arrays of Smem (col/root/beg/pre).
-  constexpr int kBuRows = 8;
+  // Warp-synchronous: per CTA step every warp (1) screens kBuRows rows per lane
+  // with independent loads and compacts its candidates (unvisited matched rows
+  // and free rows) into a warp-private stage; (2) each candidate scans its
+  // columns until the first frontier member. Winners go to the CTA's wbuf and
+  // are flushed (3) between steps; that is the only CTA-wide synchronisation.
+  constexpr int kBuRows = 4;
+  constexpr int kWarpRows = 32 * kBuRows;              // rows a warp screens per step
+  constexpr int kStepRows = kThreads * kBuRows;        // rows a CTA screens per step
 #ifndef BM_BU_PROBE
 #define BM_BU_PROBE 4
 #endif
@@ -531,113 +533,106 @@ __device__ __forceinline__ void bu_sweep(const Params& p, Smem& sm, int4* F, uns
   const unsigned long long pol = policy_evict_first();
   unsigned* const path_flag = &p.ctl->path_found[pf];
   unsigned c_trav = 0, c_nvis = 0, c_rows = 0;
-  unsigned& ncand = sm.wtot[0];
-  if (threadIdx.x == 0) {
-    sm.nw = 0;
-    ncand = 0;
-  }
+  const unsigned warp = threadIdx.x >> 5, lane = lane_id();
+  int* const wrow = sm.bcand + warp * kWarpRows;   // this warp's stage
+  int* const wval = sm.bcandv + warp * kWarpRows;
+  if (threadIdx.x == 0) sm.nw = 0;
   __syncthreads();
-  const unsigned long long chunk = (unsigned long long)kThreads * kBuRows;
-  for (unsigned long long b = (unsigned long long)blockIdx.x * chunk; b < (unsigned long long)p.nr;
-       b += (unsigned long long)gridDim.x * chunk) {
-    // (1) screen kBuRows rows per thread (independent loads)
+  for (unsigned long long b = (unsigned long long)blockIdx.x * kStepRows; b < (unsigned long long)p.nr;
+       b += (unsigned long long)gridDim.x * kStepRows) {
+    // (1) screen and compact (warp-private)
+    const unsigned long long wb = b + (unsigned long long)warp * kWarpRows;
     int v[kBuRows];
 #pragma unroll
     for (int k = 0; k < kBuRows; ++k) {
-      const unsigned long long r = b + (unsigned long long)k * kThreads + threadIdx.x;
+      const unsigned long long r = wb + (unsigned long long)k * 32 + lane;
       v[k] = r < (unsigned long long)p.nr ? ld_cg(RM(p, r)) : -3;
     }
+    unsigned ncand = 0;
 #pragma unroll
     for (int k = 0; k < kBuRows; ++k) {
-      // stage this step's candidates: at most kThreads per step, the stage holds 2 * kThreads
-      const unsigned long long r = b + (unsigned long long)k * kThreads + threadIdx.x;
       const bool is_cand = (v[k] >= 0 && !(v[k] & kVisBit)) || v[k] == -1;
       const unsigned m = __ballot_sync(kFull, is_cand);
-      unsigned base = 0;
-      if (lane_id() == 0 && m) base = atomicAdd(&ncand, (unsigned)__popc(m));
-      base = __shfl_sync(kFull, base, 0);
       if (is_cand) {
-        const unsigned slot = base + __popc(m & ((1u << lane_id()) - 1));
-        sm.bcand[slot] = (int)r;
-        sm.bcandv[slot] = v[k];
+        const unsigned slot = ncand + __popc(m & ((1u << lane) - 1));
+        wrow[slot] = (int)(wb + (unsigned long long)k * 32 + lane);
+        wval[slot] = v[k];
       }
-      __syncthreads();
-      const unsigned nc_ = ncand;
-      __syncthreads();  // everyone has read ncand before the next step adds to it
-      // (2) resolve once kThreads candidates are staged (and at the end of the chunk)
-      if (nc_ < (unsigned)kThreads && k != kBuRows - 1) continue;
-      for (unsigned t0 = 0; t0 < nc_; t0 += kThreads) {
-        bool win = false, ep = false;
-        int cw = 0, rootw = 0, rr = 0;
-        if (t0 + threadIdx.x < nc_) {
-          rr = sm.bcand[t0 + threadIdx.x];
-          const int vv = sm.bcandv[t0 + threadIdx.x];
-          const unsigned j0 = ld_ro(p.roffs + rr), j1 = ld_ro(p.roffs + rr + 1);
-          c_rows++;
-          // kBuProbe neighbours per step: their index loads and frontier-bit loads
-          // are independent, so a row that scans far waits kBuProbe x fewer round trips
-          bool done = false;
-          for (unsigned jb = j0; jb < j1 && !done; jb += kBuProbe) {
-            int cs[kBuProbe];
-            unsigned wd[kBuProbe];
+      ncand += __popc(m);
+    }
+    __syncwarp();
+    // (2) resolve the warp's candidates, 32 at a time
+    for (unsigned t0 = 0; t0 < ncand; t0 += 32) {
+      bool win = false, ep = false;
+      int cw = 0, rootw = 0, rr = 0;
+      if (t0 + lane < ncand) {
+        rr = wrow[t0 + lane];
+        const int vv = wval[t0 + lane];
+        const unsigned j0 = ld_ro(p.roffs + rr), j1 = ld_ro(p.roffs + rr + 1);
+        c_rows++;
+        // kBuProbe neighbours per step: their index loads and frontier-bit loads
+        // are independent, so a row that scans far waits kBuProbe x fewer round trips
+        bool done = false;
+        for (unsigned jb = j0; jb < j1 && !done; jb += kBuProbe) {
+          int cs[kBuProbe];
+          unsigned wd[kBuProbe];
 #pragma unroll
-            for (int k = 0; k < kBuProbe; ++k) cs[k] = jb + k < j1 ? ld_stream(p.radj + jb + k, pol) : -1;
+          for (int k = 0; k < kBuProbe; ++k) cs[k] = jb + k < j1 ? ld_stream(p.radj + jb + k, pol) : -1;
 #pragma unroll
-            for (int k = 0; k < kBuProbe; ++k)
-              wd[k] = cs[k] >= 0 ? ld_ca(reinterpret_cast<const int*>(fb) + (cs[k] >> 5)) : 0u;
+          for (int k = 0; k < kBuProbe; ++k)
+            wd[k] = cs[k] >= 0 ? ld_ca(reinterpret_cast<const int*>(fb) + (cs[k] >> 5)) : 0u;
 #pragma unroll
-            for (int k = 0; k < kBuProbe; ++k) {
-              const int c = cs[k];
-              if (done || c < 0) continue;
-              c_trav++;
-              if (!((wd[k] >> (c & 31)) & 1)) continue;
-              const int root = ld_cg(p.croot + c);
-              if (vv >= 0) {  // matched row: its column joins the frontier below c's tree
-                st_plain(RM(p, rr), vv | kVisBit);
-                st_plain(PR(p, rr), c);
-                win = true;
-                cw = vv;
-                rootw = root;
-                done = true;
-                continue;
-              }
-              // free row: an endpoint of c's tree
-              const bool one = WR && p.ep_one;
-              if (one && root_dead(p, root)) continue;
-              bool mine = true;
-              if (one) mine = atomicCAS(p.bfs + root, kStartLevel, IMP ? -rr : kFoundMark) == kStartLevel;
-              else if (WR) st_rlx(p.bfs + root, IMP ? -rr : kFoundMark);
-              if (!mine) continue;  // that tree already holds an endpoint: try another neighbour
-              if (WR) mark_dead(p, root);
-              st_rlx(RM(p, rr), -2);
+          for (int k = 0; k < kBuProbe; ++k) {
+            const int c = cs[k];
+            if (done || c < 0) continue;
+            c_trav++;
+            if (!((wd[k] >> (c & 31)) & 1)) continue;
+            const int root = ld_cg(p.croot + c);
+            if (vv >= 0) {  // matched row: its column joins the frontier below c's tree
+              st_plain(RM(p, rr), vv | kVisBit);
               st_plain(PR(p, rr), c);
-              ep = true;
-              if (ld_rlx(path_flag) == 0u) st_rlx(path_flag, 1u);
+              win = true;
+              cw = vv;
+              rootw = root;
               done = true;
+              continue;
             }
+            // free row: an endpoint of c's tree
+            const bool one = WR && p.ep_one;
+            if (one && root_dead(p, root)) continue;
+            bool mine = true;
+            if (one) mine = atomicCAS(p.bfs + root, kStartLevel, IMP ? -rr : kFoundMark) == kStartLevel;
+            else if (WR) st_rlx(p.bfs + root, IMP ? -rr : kFoundMark);
+            if (!mine) continue;  // that tree already holds an endpoint: try another neighbour
+            if (WR) mark_dead(p, root);
+            st_rlx(RM(p, rr), -2);
+            st_plain(PR(p, rr), c);
+            ep = true;
+            if (ld_rlx(path_flag) == 0u) st_rlx(path_flag, 1u);
+            done = true;
           }
-        }
-        c_nvis += win ? 1u : 0u;
-        stage_winner(sm, win, cw, rootw);
-        {  // endpoints: rare, warp-aggregated global append
-          const unsigned mine = ep ? 1u : 0u;
-          const unsigned incl = warp_incl_scan(mine);
-          const unsigned tot = __shfl_sync(kFull, incl, 31);
-          if (tot) {
-            unsigned eb = 0;
-            if (lane_id() == 31) eb = atomicAdd(&p.ctl->n_ep, tot);
-            eb = __shfl_sync(kFull, eb, 31) + incl - mine;
-            if (ep) st_plain(p.EP + eb, rr);
-          }
-        }
-        __syncthreads();
-        if (sm.nw > kWBuf - kThreads) {
-          flush_winners(p, sm, F, out_base, gout, out, pol);
-          __syncthreads();  // the reset of sm.nw lands before the next stage_winner
         }
       }
-      if (threadIdx.x == 0) ncand = 0;
-      __syncthreads();
+      c_nvis += win ? 1u : 0u;
+      stage_winner(sm, win, cw, rootw);  // one shared atomic per warp
+      {  // endpoints: rare, warp-aggregated global append
+        const unsigned mine = ep ? 1u : 0u;
+        const unsigned incl = warp_incl_scan(mine);
+        const unsigned tot = __shfl_sync(kFull, incl, 31);
+        if (tot) {
+          unsigned eb = 0;
+          if (lane == 31) eb = atomicAdd(&p.ctl->n_ep, tot);
+          eb = __shfl_sync(kFull, eb, 31) + incl - mine;
+          if (ep) st_plain(p.EP + eb, rr);
+        }
+      }
+    }
+    __syncwarp();  // the stage is reused by the next step
+    // (3) the next step adds at most kStepRows winners: flush when they might not fit
+    __syncthreads();
+    if (sm.nw > kWBuf - kStepRows) {
+      flush_winners(p, sm, F, out_base, gout, out, pol);
+      __syncthreads();  // the reset of sm.nw lands before the next stage_winner
     }
   }
   __syncthreads();
