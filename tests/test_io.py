@@ -182,3 +182,19 @@ def test_parallel_check_csc_matches_serial_messages():
     bad.cadj[int(bad.cxadj[90000])] = 5000  # an earlier column with an out-of-range row wins
     with pytest.raises(ValueError, match="row index out of range in column 90000"):
         bm.check_csr(bad)
+
+
+@pytest.mark.gpu
+def test_files_to_maximum_matching_on_gpu(tmp_path):
+    """File in, matching out: a Matrix Market file and its BMCSC001 copy load to
+    the same graph, and the engine finds the reference's known maximum on it
+    (C1: generate_random_bipartite(100000, 100000, 8.0, 1) -> 99,961)."""
+    g = bm.generate_random_bipartite(100000, 100000, 8.0, 1)
+    mtx, bcsc = tmp_path / "c1.mtx", tmp_path / "c1.bcsc"
+    bm.write_matrix_market(g, str(mtx))
+    h = bm.load_matrix_market(str(mtx))
+    bm.save_csc(h, str(bcsc))
+    for gg in (h, bm.load_csc(str(bcsc))):
+        assert np.array_equal(gg.cadj, g.cadj)
+        res = bm.apfb(gg, bm.cheap_matching(gg), None, None, bm.BfsKernel.GpubfsWr)
+        assert bm.cardinality(res.matching) == 99961
