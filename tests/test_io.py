@@ -1,4 +1,5 @@
-"""Graph files on the host (include/bmatch_b200_io.h), CPU only.
+"""Graph files on the host (include/bmatch_b200_io.h): CPU tests, plus one GPU
+test that runs a file through to the maximum matching.
 
 Matrix Market ingest must reproduce read_matrix_market (matrix_market.cpp:
 29-99) exactly: the same CSC for every accepted text, the same ParseError
