@@ -275,7 +275,10 @@ bm_status   bm_download_csc(bm_handle* h, int64_t* cxadj, int32_t* cadj);
  * {row, discoverer, root, 0}; buffers are device memory, caller-owned, sized
  * by bm_part_record_capacity. After the level loop: bm_part_end_bfs on every
  * rank, bm_part_augment (ALTERNATE + FIX, gpu_match.cpp:144-245) on rank 0,
- * then the caller broadcasts rmatch/cmatch from rank 0. */
+ * then the caller broadcasts rmatch/cmatch from rank 0.
+ * This replaces the single-process bm_create_multi(devs, n) sketched in
+ * one process per GPU (torch.distributed / NCCL for the
+ * plumbing) is the deployment model, so a handle never spans devices. */
 typedef struct bm_part bm_part;
 bm_status   bm_part_create(int32_t device, int32_t rank, int32_t world, bm_part** out);
 bm_status   bm_part_destroy(bm_part* pt);
