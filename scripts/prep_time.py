@@ -1,3 +1,4 @@
+"""Time bm_prepare_row_index (the row index of the pulled levels) across repeated uploads of C2."""
 import sys, time
 sys.path.insert(0, '/root/repo')
 import torch, bench
