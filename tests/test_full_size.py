@@ -35,10 +35,16 @@ def test_full_size_configs(engine, cfg):
     init = bm.cheap_matching(g)
     engine.upload(g, force=True)
     engine.load_matching(init)
-    for algo in ["apfb-wr", "apsb-wr", "apfb-gpubfs"]:
-        shortest, kernel, improved = bench.ALGOS[algo]
-        card, ct, done = engine.run(shortest=shortest, kernel=bm.BfsKernel(kernel), improved=improved)
-        assert done and card == want, (cfg, algo, card, want)
-        m = engine.download()
-        viol, ismax, vcard = engine.verify(g, m)
-        assert viol == 0 and ismax and vcard == want, (cfg, algo, viol, ismax, vcard)
+    # pushed levels, then pulled dense levels (the bench default for C2; forced on
+    # for C3/C4, which AUTO leaves pushed) over the prepared row index
+    for bottom_up in (False, True):
+        if bottom_up:
+            engine.prepare_row_index()
+        for algo in ["apfb-wr", "apsb-wr", "apfb-gpubfs"]:
+            shortest, kernel, improved = bench.ALGOS[algo]
+            card, ct, done = engine.run(shortest=shortest, kernel=bm.BfsKernel(kernel), improved=improved,
+                                        bottom_up=bottom_up)
+            assert done and card == want, (cfg, algo, bottom_up, card, want)
+            m = engine.download()
+            viol, ismax, vcard = engine.verify(g, m)
+            assert viol == 0 and ismax and vcard == want, (cfg, algo, bottom_up, viol, ismax, vcard)
