@@ -333,3 +333,23 @@ def test_bottom_up_auto_decision_and_row_index(oracle, monkeypatch):
         assert bm.cardinality(m) == oracle.maximum(g)
         assert oracle.validate(g, m.rmatch, m.cmatch) == 0
     eng.close()
+
+
+def test_mixed_pushed_and_pulled_levels_parity(oracle, corpus, monkeypatch):
+    """AUTO forced on (BM_BU_AUTO=1) with the default pull threshold: levels
+    switch between pushed and pulled as the frontier grows and shrinks, and
+    every driver/kernel combination must still reach the oracle's maximum."""
+    monkeypatch.setenv("BM_BU_AUTO", "1")
+    eng = bm.Engine(0)
+    graphs = [g for g, _ in corpus[::5]] + [bm.generate_random_bipartite(30000, 30000, 8.0, 7),
+                                             bm.generate_planted(40000, 12.0, 8)]
+    for g in graphs:
+        eng.upload(g, force=True)
+        init = bm.cheap_matching(g)
+        want = oracle.maximum(g)
+        for shortest, kernel, improved in [(False, bm.BfsKernel.GpubfsWr, False), (True, bm.BfsKernel.GpubfsWr, True),
+                                           (False, bm.BfsKernel.Gpubfs, False)]:
+            m = eng.match(g, init, shortest=shortest, kernel=kernel, improved=improved).matching
+            assert bm.cardinality(m) == want, (g.name, shortest, kernel)
+            assert oracle.validate(g, m.rmatch, m.cmatch) == 0
+    eng.close()
