@@ -86,9 +86,10 @@ typedef struct bm_match_opts {
   int32_t claim_policy;      /* bm_claim_policy (WR only): which trees may claim a column */
   int32_t endpoint_policy;   /* bm_endpoint_policy (WR only): how many free rows a tree may hold */
   int32_t bottom_up;         /* bm_bottom_up: whether levels whose frontier holds >= 45% of
-                                the edges are pulled (direction-optimised); they
-                                need a row index of the graph (E ints), built on the first such
-                                run after an upload */
+                                the edges (20% once the row state is interleaved) are pulled
+                                (direction-optimised); they need a row index
+                                of the graph (E ints), built by bm_prepare_row_index or the
+                                first such run after an upload */
 } bm_match_opts;
 
 /* OFF: push every level. ON: pull dense levels (builds the row index on the
