@@ -538,6 +538,7 @@ __device__ __forceinline__ void bu_sweep(const Params& p, Smem& sm, int4* F, uns
   int* const wval = sm.bcandv + warp * kWarpRows;
   if (threadIdx.x == 0) sm.nw = 0;
   __syncthreads();
+  unsigned step = 0;
   for (unsigned long long b = (unsigned long long)blockIdx.x * kStepRows; b < (unsigned long long)p.nr;
        b += (unsigned long long)gridDim.x * kStepRows) {
     // (1) screen and compact (warp-private)
@@ -628,11 +629,19 @@ __device__ __forceinline__ void bu_sweep(const Params& p, Smem& sm, int4* F, uns
       }
     }
     __syncwarp();  // the stage is reused by the next step
-    // (3) the next step adds at most kStepRows winners: flush when they might not fit
-    __syncthreads();
-    if (sm.nw > kWBuf - kStepRows) {
-      flush_winners(p, sm, F, out_base, gout, out, pol);
-      __syncthreads();  // the reset of sm.nw lands before the next stage_winner
+    // (3) every kFlushSteps steps (at most kFlushSteps * kStepRows winners in between,
+    // which wbuf holds): flush when the next kFlushSteps steps might not fit
+#ifndef BM_BU_FLUSH_STEPS
+#define BM_BU_FLUSH_STEPS 4
+#endif
+    constexpr unsigned kFlushSteps = BM_BU_FLUSH_STEPS;
+    static_assert(kFlushSteps * kStepRows <= kWBuf, "wbuf must hold the winners between flush checks");
+    if (++step % kFlushSteps == 0) {
+      __syncthreads();
+      if (sm.nw > kWBuf - kFlushSteps * kStepRows) {
+        flush_winners(p, sm, F, out_base, gout, out, pol);
+        __syncthreads();  // the reset of sm.nw lands before the next stage_winner
+      }
     }
   }
   __syncthreads();
