@@ -21,6 +21,7 @@ CSRC      := $(PKG)/csrc
 BUILD     := build
 LIB       := $(PKG)/libbmatch_b200.so
 ORACLE    := oracle/liboracle.so
+GENORACLE := oracle/libgen_oracle.so
 
 REF_ROOT  ?= /root/reference/proj
 REF_SRCS  := algorithms baselines csr_graph gpu_match kernel_grid matching matrix_market
@@ -36,7 +37,7 @@ SHIM_TEST := oracle/_ref/shim_test
 SUITE     := oracle/_ref/b200_suite
 
 .PHONY: all ref shimtest suite clean
-all: $(LIB) $(ORACLE)
+all: $(LIB) $(ORACLE) $(GENORACLE)
 
 $(BUILD):
 	mkdir -p $(BUILD)
@@ -58,6 +59,10 @@ $(LIB): $(BUILD)/bm_engine.o $(BUILD)/bm_partition.o $(BUILD)/bm_host.o $(BUILD)
 
 $(ORACLE): oracle/bm_oracle.c oracle/bm_oracle.h
 	$(CC) $(CFLAGS) -shared -o $@ oracle/bm_oracle.c
+
+# the synthetic configs restated for the reference arm (no product library mapped)
+$(GENORACLE): oracle/gen_oracle.cpp
+	$(CXX) $(CXXFLAGS) -shared -o $@ $<
 
 ref: $(REF_LIB)
 
@@ -84,4 +89,4 @@ $(SUITE): tools/b200_suite.cpp include/bmatch_b200.hpp include/bmatch_b200.h inc
 	    -Wl,-rpath,'$$ORIGIN' -Wl,-rpath,'$$ORIGIN/../../paper_1303_1379_b200'
 
 clean:
-	rm -rf $(BUILD) $(LIB) $(ORACLE)
+	rm -rf $(BUILD) $(LIB) $(ORACLE) $(GENORACLE)

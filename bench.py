@@ -1,12 +1,13 @@
 #!/usr/bin/env python
 """Benchmark: time-to-maximum-matching on B200 (BASELINE.json metric).
 
-Default workload (N=1): C2 = configs[1] of BASELINE.json — 10M x 10M random
-bipartite graph with a planted perfect matching, average degree 16
-(~1.6e8 edges), APFB-GPUBFS-WR from the reference's first-fit initial
-matching (the reference methodology: cheap_matching outside the timed
-region, bench.cpp:52-63). One *step* = one complete run to the maximum
-matching from the same initial matching, inputs resident in HBM.
+Default workload (N=1): C5 = the largest synthetic graph of BASELINE.json
+(configs[4]; north_star puts the 1-GPU targets on it): the reference's own
+generate_random_bipartite(1e8, 1e8, 16.0, seed 5), 1.6e9 edges, APFB-GPUBFS-WR
+from the reference's first-fit initial matching (the reference methodology:
+cheap_matching outside the timed region, bench.cpp:52-63). One *step* = one
+complete run to the maximum matching from the same initial matching, inputs
+resident in HBM.
 
   value     = graph edges / time-to-maximum-matching   (edges/s, higher is better)
   e2e       = same metric through the public C-ABI call with pinned host
@@ -17,10 +18,16 @@ matching from the same initial matching, inputs resident in HBM.
               (oracle/_ref: /root/reference sources compiled unmodified),
               apfb-wr-ct under Schedule::parallel(all host cores)
 
+The reference arm builds its input with oracle/gen_oracle.cpp (a restatement
+of the same generators) and never loads the product library. Each of its steps
+is one full run of the same workload; at C5 one run takes about a minute on 16
+cores, so it times as many steps as fit its --ref-budget-s (reported as
+`steps`, with `steps_requested`).
+
 Multi-GPU (torchrun, N>1): by default the workload is 1-D partitioned by
 column across the ranks (strong scaling, paper_1303_1379_b200/partition.py):
 each rank expands its own columns and the per-level frontier records are
-all-gathered over NCCL; ALTERNATE/FIX run on rank 0 and the matching is
+exchanged over peer memory; ALTERNATE/FIX run on rank 0 and the matching is
 broadcast. --mode replicas instead solves one independent replica per rank
 (weak scaling, no collective). Timing is the max over ranks.
 """
@@ -81,6 +88,43 @@ def build_graph(name: str, scale_div: int = 1):
         n = 100_000_000 // scale_div
         return bm.generate_random_bipartite(n, n, 16.0, 5), (99_999_986 if scale_div == 1 else None)
     raise SystemExit(f"unknown config {name}")
+
+
+def build_graph_oracle(name: str, scale_div: int = 1):
+    """The same graphs as build_graph, built by oracle/gen_oracle.cpp (the
+    reference arm must not map the product library)."""
+    from oracle import Generators, Reference, OGraph
+    gen = Generators()
+    if name == "file":  # the reference's own reader (matrix_market.cpp) through oracle/_ref
+        if GRAPH_FILE.endswith(".bcsc"):
+            raise SystemExit("--impl reference reads Matrix Market files only")
+        with open(GRAPH_FILE, "rb") as f:
+            st = Reference().read_matrix_market(f.read())
+        if st[0] != "ok":
+            raise SystemExit(f"reference reader failed: {st}")
+        return OGraph(st[1], st[2], st[3], st[4], os.path.basename(GRAPH_FILE)), None
+    if name == "C1":
+        return gen.uniform(100_000, 100_000, 8.0, 1), 99_961
+    if name == "C2":
+        n = 10_000_000 // scale_div
+        return gen.planted(n, 16.0, 2024), n
+    if name == "C3":
+        return gen.rmat(24, 16.0, 2024), None
+    if name == "C4":
+        return gen.banded(20_000_000 // scale_div, 3, 0.05, 12345)
+    if name == "C5":
+        n = 100_000_000 // scale_div
+        return gen.uniform(n, n, 16.0, 5), (99_999_986 if scale_div == 1 else None)
+    raise SystemExit(f"unknown config {name}")
+
+
+def workload_config(args, g) -> dict:
+    """The `config` object, identical in both arms (impl-specific keys live outside it)."""
+    return {"workload": f"{args.config}: {CONFIGS[args.config]}" +
+                        (f" (1/{args.scale_div} scale)" if args.scale_div != 1 else ""),
+            "nc": g.nc, "nr": g.nr, "edges": g.num_edges(),
+            "init": "first-fit cheap_matching (matching.cpp:13-26), computed before timing",
+            "l2": f"GPU arm flushes L2 between steps ({args.flush_mb} MiB write)"}
 
 
 def data_kind() -> str:
@@ -219,33 +263,59 @@ def cpu_reference_run(g, init, threads_label="parallel"):
 
 
 def run_reference_arm(args):
+    """--impl reference: the reference's own CPU implementation (oracle/_ref,
+    apfb-wr-ct under Schedule::parallel(all host threads), kernel_grid.cpp:127-131,
+    timed as bench.cpp:52-63) on the same workload. Nothing from the product
+    package is imported or loaded here."""
     world, rank, local = dist_env()
     if rank != 0:
         return 0
-    import paper_1303_1379_b200 as bm
-    g, known = build_graph(args.config, args.scale_div)
-    init = bm.cheap_matching(g)
+    from oracle import Generators, have_reference
+    t_gen = time.perf_counter()
+    g, known = build_graph_oracle(args.config, args.scale_div)
+    if known is None:
+        known = known_answers().get(f"{args.config}/div{args.scale_div}")
+    r0, c0 = Generators().first_fit(g)
+
+    class _Init:
+        rmatch, cmatch = r0, c0
+    t_gen = time.perf_counter() - t_gen
     E = g.num_edges()
-    times, cards, kind, cores = [], [], None, None
-    for i in range(args.warmup + args.steps):
-        res = cpu_reference_run(g, init)
-        if i >= args.warmup:
-            times.append(res["seconds"])
-            cards.append(res["cardinality"])
-        kind, cores = res["kind"], res["cores"]
+    budget = args.ref_budget_s
+    wall0 = time.perf_counter()
+    probe = cpu_reference_run(g, _Init)  # first run: warm-up, and the per-step cost estimate
+    t1 = probe["seconds"]
+    cards = [probe["cardinality"]]
+    warm = min(args.warmup, 1)
+    if t1 * (args.warmup - 1 + args.steps) <= budget:
+        for _ in range(max(0, args.warmup - 1)):
+            cards.append(cpu_reference_run(g, _Init)["cardinality"])
+        warm = max(args.warmup, 1)
+        steps = args.steps
+    else:  # one step is a full run; time as many as fit the budget
+        steps = max(1, min(args.steps, int(budget // max(t1, 1e-9))))
+    times = []
+    for _ in range(steps):
+        res = cpu_reference_run(g, _Init)
+        times.append(res["seconds"])
+        cards.append(res["cardinality"])
+    kind, cores = res["kind"], res["cores"]
     t = statistics.mean(times)
     value = E / t
-    sample = f"full {args.config} workload per step: {g.nc}x{g.nr}, {E} edges, apfb-wr-ct parallel:{cores}"
+    sample = (f"{steps} full {args.config} run(s) ({g.nc}x{g.nr}, {E} edges) of apfb-wr-ct parallel:{cores} "
+              f"from first-fit; {warm} untimed warm-up run(s)")
     emit({
         "impl": "reference", "metric": METRIC, "value": value, "unit": "edges/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "steps": steps, "steps_requested": args.steps, "warmup": warm, "warmup_requested": args.warmup,
+        "ms_per_step": t * 1e3, "ms_per_step_min": min(times) * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": data_kind(),
-        "config": {"workload": f"{args.config}: {CONFIGS[args.config]}", "algorithm": "apfb-wr-ct (reference CPU)",
-                   "nc": g.nc, "nr": g.nr, "edges": E, "init": "first-fit cheap_matching (not timed)"},
+        "config": workload_config(args, g),
+        "algorithm": "apfb-wr-ct (reference CPU, oracle/_ref)" if have_reference() else "apfb-wr (C port, serial)",
         "cpu_baseline": {"value": value, "unit": "edges/s", "cores": cores, "kind": kind, "sample": sample},
         "e2e": {"value": value, "unit": "edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "time_to_max_matching_ms": t * 1e3, "cardinality": cards[-1] if cards else None,
+        "time_to_max_matching_ms": t * 1e3, "cardinality": cards[-1],
         "parity": {"known_answer": known, "ok": (known is None or all(c == known for c in cards))},
+        "generation_s": t_gen, "wall_s": time.perf_counter() - wall0,
     })
     return 0
 
@@ -343,14 +413,11 @@ def run_partitioned(args):
             "metric": METRIC, "value": E / (t_ms / 1e3), "unit": "edges/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_ms, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "int32", "data": data_kind(),
-            "config": {"workload": f"{args.config}: {CONFIGS[args.config]}" +
-                                   (f" (1/{args.scale_div} scale)" if args.scale_div != 1 else ""),
-                       "algorithm": f"{args.algo}-b200-partitioned", "nc": g.nc, "nr": g.nr, "edges": E,
-                       "init": "first-fit cheap_matching (host, not timed)",
-                       "parallelism": f"column-partition x{world}, per-level record exchange: "
-                                      + ("fused P2P stores into every rank's receive slabs (CUDA IPC / NVLink)"
-                                         if exchange == "p2p" else f"all-gather ({backend})"),
-                       "l2": "per-step working set exceeds L2 at C2+ scale; no explicit flush"},
+            "config": workload_config(args, g),
+            "algorithm": f"{args.algo}-b200-partitioned",
+            "parallelism": f"column-partition x{world}, per-level record exchange: "
+                           + ("fused P2P stores into every rank's receive slabs (CUDA IPC / NVLink)"
+                              if exchange == "p2p" else f"all-gather ({backend})"),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": None, "peak_source": peak_src,
                          "kernel": "bm_part_* level kernels + exchange (whole step)",
@@ -565,12 +632,9 @@ def run_b200(args):
             "metric": METRIC, "value": world * E / (t_ms / 1e3), "unit": "edges/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": data_kind(),
-            "config": {"workload": f"{args.config}: {CONFIGS[args.config]}" +
-                                   (f" (1/{args.scale_div} scale)" if args.scale_div != 1 else ""),
-                       "algorithm": f"{args.algo}-b200", "nc": g.nc, "nr": g.nr, "edges": E,
-                       "init": "first-fit cheap_matching, resident in HBM (not timed)",
-                       "l2": f"flushed between steps ({args.flush_mb} MiB write)",
-                       "parallelism": "replicas" if world > 1 else "single-gpu"},
+            "config": workload_config(args, g),
+            "algorithm": f"{args.algo}-b200",
+            "parallelism": "replicas" if world > 1 else "single-gpu",
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                          "kernel": "bm::driver_kernel (persistent, whole run)",
@@ -610,10 +674,12 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
-    ap.add_argument("--config", choices=sorted(CONFIGS), default="C2")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="C5")
     ap.add_argument("--algo", choices=sorted(ALGOS), default="apfb-wr")
     ap.add_argument("--scale-div", type=int, default=1, help="shrink C2/C4/C5 by this factor (testing only)")
     ap.add_argument("--flush-mb", type=int, default=512)
+    ap.add_argument("--ref-budget-s", type=float, default=180.0,
+                    help="reference arm: wall budget for its timed full runs (a C5 run is ~1 min on 16 cores)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-alt", action="store_true", help="skip the other-direction measurement")

@@ -217,6 +217,16 @@ bm_status   bm_download_matching(bm_handle* h, int32_t* rmatch, int32_t* cmatch)
  * run launched (driver launches plus the initial-state copy kernel). */
 bm_status   bm_last_kernel_time(bm_handle* h, double* ms, int32_t* launches);
 
+/* Fault injection for the failure-path tests (no reference counterpart; every
+ * key defaults to off). PHASE_BOUND: replaces the nc+1 termination bound of
+ * run_driver (gpu_match.cpp:313-320) by `value` phases (0 = nc+1), so a run
+ * that needs more phases fails with BM_ERR_BOUND_EXCEEDED. SKIP_ALTERNATE_PHASE:
+ * outer iteration `value` (1-based; 0 = none) runs its raced ALTERNATE as a
+ * no-op, i.e. finds paths but augments none, which forces the serial retry of
+ * gpu_match.cpp:328-343 (serial_retries = 1). */
+typedef enum bm_debug_key { BM_DEBUG_PHASE_BOUND = 1, BM_DEBUG_SKIP_ALTERNATE_PHASE = 2 } bm_debug_key;
+bm_status   bm_debug_set(bm_handle* h, int32_t key, int64_t value);
+
 /* Stage timeline of the last bm_run/bm_resume/bm_match: `n` records of two
  * uint64 each, (tag, device %globaltimer in ns). tag = (kind << 32) | arg with
  * kind 0 start, 1 init pass, 2 setup, 3 BFS level (arg = frontier entries),

@@ -271,3 +271,76 @@ class RefGraph:
 
 def have_reference() -> bool:
     return os.path.exists(REF_PATH)
+
+
+GEN_PATH = os.path.join(_HERE, "libgen_oracle.so")
+
+
+class OGraph:
+    """A CSC in numpy arrays, shaped like paper_1303_1379_b200.BipartiteCsr
+    (nc, nr, cxadj int64, cadj int32) but built without the product library."""
+
+    def __init__(self, nc, nr, cxadj, cadj, name=""):
+        self.nc, self.nr, self.cxadj, self.cadj, self.name = nc, nr, cxadj, cadj, name
+
+    def num_edges(self) -> int:
+        return int(self.cxadj[-1])
+
+
+class Generators:
+    """gen_oracle.cpp: the bench configs' synthetic graphs restated for the
+    reference arm / CPU baseline (the product's generators live in libbmatch_b200.so)."""
+
+    def __init__(self, path: str = GEN_PATH, threads: int = 0):
+        if not os.path.exists(path):
+            raise ImportError(f"{path} missing: run `make`")
+        L = self.lib = C.CDLL(path)
+        self.threads = threads
+        i32, i64, dbl, u64 = C.c_int32, C.c_int64, C.c_double, C.c_uint64
+        sig = {
+            "go_uniform": [i32, i32, dbl, u64, i32, _i64p, _i32p],
+            "go_planted": [i32, dbl, u64, i32, _i64p, _i32p],
+            "go_rmat": [i32, dbl, dbl, dbl, dbl, u64, i32, i32, _i64p, _i32p],
+            "go_banded": [i32, i32, dbl, u64, i32, i32, _i64p, _i32p, _i64p],
+        }
+        for k, a in sig.items():
+            getattr(L, k).restype = C.c_int64
+            getattr(L, k).argtypes = a
+        L.go_first_fit.restype = None
+        L.go_first_fit.argtypes = [i32, i32, _i64p, _i32p, _i32p, _i32p]
+
+    @staticmethod
+    def _alloc(nc, cap):
+        return np.empty(nc + 1, np.int64), np.empty(max(int(cap), 1), np.int32)
+
+    def _done(self, nc, nr, cx, adj, ne, name):
+        return OGraph(nc, nr, cx, adj[:ne], name)
+
+    def uniform(self, nc, nr, deg, seed):
+        cx, adj = self._alloc(nc, round(nc * deg))
+        ne = self.lib.go_uniform(nc, nr, deg, seed, self.threads, _p64(cx), _p32(adj))
+        return self._done(nc, nr, cx, adj, ne, f"uniform/{nc}/{deg}/{seed}")
+
+    def planted(self, n, deg, seed):
+        cx, adj = self._alloc(n, n + max(0, round((deg - 1.0) * n)))
+        ne = self.lib.go_planted(n, deg, seed, self.threads, _p64(cx), _p32(adj))
+        return self._done(n, n, cx, adj, ne, f"planted/{n}/{deg}/{seed}")
+
+    def rmat(self, scale, ef, seed, a=0.57, b=0.19, c=0.19, permute=True):
+        n = 1 << scale
+        cx, adj = self._alloc(n, round(ef * n))
+        ne = self.lib.go_rmat(scale, ef, a, b, c, seed, 1 if permute else 0, self.threads, _p64(cx), _p32(adj))
+        return self._done(n, n, cx, adj, ne, f"rmat/{scale}/{ef}/{seed}")
+
+    def banded(self, n, band, frac, seed, permute=True):
+        cx, adj = self._alloc(n, n * band)
+        live = C.c_int64()
+        ne = self.lib.go_banded(n, band, frac, seed, 1 if permute else 0, self.threads, _p64(cx), _p32(adj),
+                                C.byref(live))
+        return self._done(n, n, cx, adj, ne, f"banded/{n}/{band}/{frac}/{seed}"), int(live.value)
+
+    def first_fit(self, g):
+        r = np.empty(g.nr, np.int32)
+        c = np.empty(g.nc, np.int32)
+        self.lib.go_first_fit(g.nc, g.nr, _p64(g.cxadj), _p32(g.cadj), _p32(r), _p32(c))
+        return r, c

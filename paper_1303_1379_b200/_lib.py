@@ -124,6 +124,7 @@ _PROTOS = {
                             PHASE_CB, _vp, _i32p]),
     "bm_download_matching": (C.c_int, [_vp, _i32p, _i32p]),
     "bm_last_kernel_time": (C.c_int, [_vp, C.POINTER(C.c_double), _i32p]),
+    "bm_debug_set": (C.c_int, [_vp, C.c_int32, C.c_int64]),
     "bm_timeline": (C.c_int, [_vp, C.POINTER(C.c_uint64), C.c_int64, _i64p]),
     "bm_debug_stats": (C.c_int, [_vp, C.POINTER(C.c_uint64), C.c_int64, _i64p]),
     "bm_bfs_phase": (C.c_int, [_vp, C.c_int32, C.c_int32, C.c_int32, _i32p, _i32p, _i32p, _i32p, _i32p,

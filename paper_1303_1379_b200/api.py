@@ -335,6 +335,13 @@ class Engine:
     def _nc(self) -> int:
         return self.graph_info()[0]
 
+    DEBUG_PHASE_BOUND = 1
+    DEBUG_SKIP_ALTERNATE_PHASE = 2
+
+    def debug_set(self, key: int, value: int):
+        """Fault injection for the failure-path tests (bm_debug_set)."""
+        check(lib.bm_debug_set(self._h, key, value))
+
     def last_kernel_time(self):
         ms, n = C.c_double(), C.c_int32()
         check(lib.bm_last_kernel_time(self._h, C.byref(ms), C.byref(n)))

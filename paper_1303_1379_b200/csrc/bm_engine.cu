@@ -225,6 +225,8 @@ struct Params {
   int init_mode;
   int fresh;
   int init_checked;  // the given initial matching was validated when it was loaded (bm_load_matching)
+  int sorted;        // every column's rows ascend (binary-searchable adjacency)
+  int dbg_skip_alt_phase;  // fault injection (bm_debug_set): this phase's raced ALTERNATE does nothing
   int max_phases;
   int stop_after_bfs;
   int trace;        // write bfs_array level labels (parity probes)
@@ -397,6 +399,24 @@ __device__ __forceinline__ bool cta_reserve(Smem& sm, unsigned cnt, unsigned deg
   return true;
 }
 
+// Whether row r is in column c's adjacency [b, e) (binary search over a sorted
+// CSC, else a scan): a matched pair of an initial matching must be an edge
+// (validate, matching.cpp:70-104).
+__device__ __forceinline__ bool has_edge(const int* adj, unsigned b, unsigned e, int r, bool sorted) {
+  if (sorted) {
+    while (b < e) {
+      const unsigned mid = b + ((e - b) >> 1);
+      const int v = ld_ro(adj + mid);
+      if (v == r) return true;
+      if (v < r) b = mid + 1; else e = mid;
+    }
+    return false;
+  }
+  for (unsigned j = b; j < e; ++j)
+    if (ld_ro(adj + j) == r) return true;
+  return false;
+}
+
 // Writes one reserved frontier entry and its granule-index records.
 __device__ __forceinline__ void put_entry(int4* F, unsigned out_base, unsigned* gidx, unsigned long long slot,
                                           int col, int root, unsigned beg, unsigned deg,
@@ -405,6 +425,7 @@ __device__ __forceinline__ void put_entry(int4* F, unsigned out_base, unsigned* 
   const unsigned pre = (unsigned)(slot & kEdgeMask);
   if (pol) st_stream(F + out_base + local, make_int4(col, root, (int)beg, (int)pre), pol);
   else st_plain(F + out_base + local, make_int4(col, root, (int)beg, (int)pre));
+  if (deg == 0) return;  // holds no edge: no granule starts inside it
   const unsigned m1 = (pre + deg - 1) / kGran;
   for (unsigned m = (pre + kGran - 1) / kGran; m <= m1; ++m) st_plain(reinterpret_cast<int*>(gidx) + m, (int)local);
 }
@@ -991,7 +1012,7 @@ struct PhaseOut {
 // One phase = run_phase (gpu_match.cpp:268-302) from the roots in F[cur].
 template <bool WR, bool IMP, bool BU>
 __device__ PhaseOut run_phase(const Params& p, Smem& sm, int cur, int parity, bool serial_alt,
-                              long long isolated) {
+                              long long isolated, bool skip_alt) {
   Ctrl* ctl = p.ctl;
   int4* F = cur ? p.F1 : p.F0;
   int4* Fn = cur ? p.F0 : p.F1;
@@ -1091,7 +1112,10 @@ __device__ PhaseOut run_phase(const Params& p, Smem& sm, int cur, int parity, bo
   if (is_leader()) ctl->path_found[parity ^ 1] = 0u;  // flag of the next phase
   const unsigned n_ep = ld_rlx(&ctl->n_ep);
   unsigned walks = 0, steps = 0, resets = 0;
-  if (!serial_alt) {
+  if (skip_alt) {
+    // fault injection: a raced ALTERNATE that augmented nothing, so the driver
+    // must take the serial retry (gpu_match.cpp:328-343)
+  } else if (!serial_alt) {
     if (!IMP) {
       for (unsigned long long k = global_thread(); k < n_ep; k += global_threads())
         alternate_walk(p, walks, steps, ld_cg(p.EP + k));
@@ -1263,6 +1287,7 @@ __global__ void __launch_bounds__(kThreads, BM_MINB) driver_kernel(Params p) {
         if (!p.init_checked) {
           if (r < -1 || r >= p.nr) bad++;
           else if (r >= 0 && ld_cg(RM(p, r)) != (int)c) bad++;
+          else if (r >= 0 && !has_edge(p.adj, ld_ro(p.offs + c), ld_ro(p.offs + c + 1), r, p.sorted)) bad++;
         }
         st_plain(p.bfs + c, r >= 0 ? kUnvisited : kStartLevel);
         if (r < 0) {
@@ -1320,7 +1345,7 @@ __global__ void __launch_bounds__(kThreads, BM_MINB) driver_kernel(Params p) {
     }
     ++outer;
     const long long before = card;
-    PhaseOut ph = run_phase<WR, IMP, BU>(p, sm, cur, parity, false, isolated);
+    PhaseOut ph = run_phase<WR, IMP, BU>(p, sm, cur, parity, false, isolated, outer == p.dbg_skip_alt_phase);
     if (p.stop_after_bfs) {
       if (is_leader()) {
         ctl->bfs_levels_last = ph.launches;
@@ -1335,7 +1360,7 @@ __global__ void __launch_bounds__(kThreads, BM_MINB) driver_kernel(Params p) {
     long long after = ph.after;
     bool retried = false;
     if (ph.found && after <= before) {
-      PhaseOut rt = run_phase<WR, IMP, BU>(p, sm, cur, parity, true, isolated);
+      PhaseOut rt = run_phase<WR, IMP, BU>(p, sm, cur, parity, true, isolated, false);
       cur ^= 1;
       parity ^= 1;
       launches += rt.launches;
@@ -1468,6 +1493,37 @@ __global__ void validate_kernel(const unsigned* offs, const int* adj, int nc, in
   }
 }
 
+// Maximality half of the certificate (is_maximum, matching.cpp:106-131) as a
+// plain queue BFS that shares nothing with driver_kernel: alternating levels
+// from every free non-isolated column over the plain rmatch, a visited bitmap
+// of its own, one warp per frontier column, one launch per level. A free row
+// reached from a free column is an augmenting path.
+__global__ void verify_roots_kernel(const unsigned* offs, const int* cmatch, int nc, unsigned* vis, int* q,
+                                    unsigned* qn) {
+  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < nc; c += (long long)gridDim.x * blockDim.x) {
+    if (cmatch[c] != -1 || offs[c + 1] == offs[c]) continue;
+    atomicOr(vis + (c >> 5), 1u << (c & 31));
+    q[atomicAdd(qn, 1u)] = (int)c;
+  }
+}
+__global__ void verify_level_kernel(const unsigned* offs, const int* adj, const int* rmatch, const int* q,
+                                    unsigned n, unsigned* vis, int* qnext, unsigned* qn, unsigned* found) {
+  const long long warps = (long long)gridDim.x * blockDim.x / 32;
+  for (long long i = (blockIdx.x * (long long)blockDim.x + threadIdx.x) / 32; i < n; i += warps) {
+    if (*(volatile unsigned*)found) return;
+    const int c = q[i];
+    for (unsigned j = offs[c] + lane_id(); j < offs[c + 1]; j += 32) {
+      const int m = rmatch[adj[j]];
+      if (m == -1) {
+        *found = 1u;
+      } else if (m >= 0) {
+        const unsigned bit = 1u << (m & 31);
+        if (!(atomicOr(vis + (m >> 5), bit) & bit)) qnext[atomicAdd(qn, 1u)] = m;
+      }
+    }
+  }
+}
+
 // Row-state (de)interleaving between the caller's plain rmatch / predecessor
 // arrays and the device layout (see RM / PR).
 __global__ void rows_pack_kernel(const int* plain, int* rm, int nr, int rs) {
@@ -1499,13 +1555,15 @@ __global__ void perm_scatter_kernel(const unsigned* offs, const int* adj, const 
 }
 
 // Validity of a resident initial matching (plain arrays), checked once at load.
-__global__ void init_check_kernel(const int* rmatch, const int* cmatch, int nc, int nr, unsigned long long* bad) {
+__global__ void init_check_kernel(const unsigned* offs, const int* adj, int sorted, const int* rmatch,
+                                  const int* cmatch, int nc, int nr, unsigned long long* bad) {
   unsigned long long b = 0;
   const long long tot = (long long)gridDim.x * blockDim.x;
   for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < nc; c += tot) {
     const int r = cmatch[c];
     if (r < -1 || r >= nr) b++;
     else if (r >= 0 && rmatch[r] != (int)c) b++;
+    else if (r >= 0 && !has_edge(adj, offs[c], offs[c + 1], r, sorted != 0)) b++;  // a pair must be an edge
   }
   for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < nr; r += tot) {
     const int v = rmatch[r];
@@ -1791,6 +1849,9 @@ struct bm_handle {
   unsigned long long* tl = nullptr;
   unsigned tl_cap = 1u << 16;
   std::vector<unsigned long long> timeline;  // host copy for the last run
+  // fault injection for the failure-path tests (bm_debug_set)
+  long long dbg_phase_bound = 0;
+  int dbg_skip_alt_phase = 0;
 };
 
 namespace {
@@ -2045,6 +2106,9 @@ Params make_params(bm_handle* h, const bm_match_opts& o) {
   p.max_phases = h->rec_cap;
   p.stop_after_bfs = 0;
   p.phase_bound = (long long)h->nc + 1;
+  if (h->dbg_phase_bound > 0) p.phase_bound = h->dbg_phase_bound;
+  p.sorted = h->sorted;
+  p.dbg_skip_alt_phase = h->dbg_skip_alt_phase;
   return p;
 }
 
@@ -2438,7 +2502,8 @@ bm_status bm_load_matching(bm_handle* h, const int32_t* rmatch, const int32_t* c
   if (h->nc > 0) BM_CUDA(cudaMemcpyAsync(h->cmatch0, cmatch, sizeof(int) * h->nc, cudaMemcpyHostToDevice, h->stream));
   BM_CUDA(cudaMemsetAsync(h->scratch, 0, sizeof(unsigned long long), h->stream));
   const int blocks = std::max(1, std::min(h->sms * 8, (std::max(h->nc, h->nr) + 255) / 256));
-  init_check_kernel<<<blocks, 256, 0, h->stream>>>(h->rmatch0, h->cmatch0, h->nc, h->nr, h->scratch);
+  init_check_kernel<<<blocks, 256, 0, h->stream>>>(h->offs, h->adj, h->sorted, h->rmatch0, h->cmatch0, h->nc,
+                                                   h->nr, h->scratch);
   BM_CUDA(cudaGetLastError());
   unsigned long long bad = 0;
   BM_CUDA(cudaMemcpyAsync(&bad, h->scratch, sizeof(bad), cudaMemcpyDeviceToHost, h->stream));
@@ -2498,6 +2563,16 @@ bm_status bm_download_matching(bm_handle* h, int32_t* rmatch, int32_t* cmatch) {
   if (cmatch && h->nc > 0) BM_CUDA(cudaMemcpyAsync(cmatch, h->cmatch, sizeof(int) * h->nc, cudaMemcpyDeviceToHost, h->stream));
   BM_CUDA(cudaStreamSynchronize(h->stream));
   return BM_OK;
+}
+
+bm_status bm_debug_set(bm_handle* h, int32_t key, int64_t value) {
+  bm_status s = check_handle(h, false);
+  if (s != BM_OK) return s;
+  switch (key) {
+    case BM_DEBUG_PHASE_BOUND: h->dbg_phase_bound = value; return BM_OK;
+    case BM_DEBUG_SKIP_ALTERNATE_PHASE: h->dbg_skip_alt_phase = (int)value; return BM_OK;
+    default: return fail(BM_ERR_INVALID_ARG, "unknown debug key");
+  }
 }
 
 bm_status bm_last_kernel_time(bm_handle* h, double* ms, int32_t* launches) {
@@ -2701,24 +2776,33 @@ bm_status bm_verify(bm_handle* h, const int32_t* rmatch, const int32_t* cmatch, 
   if (cardinality) *cardinality = (int64_t)res[1];
   if (is_max) *is_max = 0;
   if (res[0] != 0) return BM_OK;
-  // Maximality half (is_maximum, matching.cpp:106-131): one full GPUBFS
-  // phase from every unmatched column; a reached unmatched row is an
-  // augmenting path.
-  s = prepare_fresh(h);
-  if (s != BM_OK) return s;
-  bm_match_opts o{};
-  o.driver = BM_DRIVER_APFB;
-  o.bfs_kernel = BM_BFS_GPUBFS;
-  Params p = make_params(h, o);
-  p.stop_after_bfs = 1;
-  p.max_phases = 1;
-  float ms = 0.f;
-  s = launch(h, 0, p, &ms);
-  if (s != BM_OK) return s;
-  Ctrl ctl{};
-  BM_CUDA(cudaMemcpy(&ctl, h->ctl, sizeof(Ctrl), cudaMemcpyDeviceToHost));
-  if (ctl.error) return ctl_error_status(ctl.error);
-  if (is_max) *is_max = ctl.path_found_last ? 0 : 1;
+  // Maximality half (is_maximum, matching.cpp:106-131): a queue BFS of its own
+  // (verify_*_kernel), not the engine's driver kernel, so a BFS bug in the
+  // engine cannot both stop a run early and certify its result.
+  unsigned* vis = h->dead;  // nc bits; free outside a run
+  int* qa = reinterpret_cast<int*>(h->F[0]);
+  int* qb = reinterpret_cast<int*>(h->F[1]);
+  unsigned* cnt = reinterpret_cast<unsigned*>(h->scratch + 4);  // [0] queue length, [1] found
+  BM_CUDA(cudaMemsetAsync(vis, 0, sizeof(unsigned) * std::max(h->ndead_words, 1), h->stream));
+  BM_CUDA(cudaMemsetAsync(cnt, 0, sizeof(unsigned) * 2, h->stream));
+  const int cblocks = std::max(1, std::min(h->sms * 8, (h->nc + 255) / 256));
+  if (h->nc > 0) verify_roots_kernel<<<cblocks, 256, 0, h->stream>>>(h->offs, h->cmatch, h->nc, vis, qa, cnt);
+  BM_CUDA(cudaGetLastError());
+  unsigned st[2] = {0, 0};
+  BM_CUDA(cudaMemcpyAsync(st, cnt, sizeof(st), cudaMemcpyDeviceToHost, h->stream));
+  BM_CUDA(cudaStreamSynchronize(h->stream));
+  for (long long lv = 0; st[0] > 0 && !st[1]; ++lv) {
+    if (lv > (long long)h->nc + 1) return fail(BM_ERR_CUDA, "verify BFS exceeded nc + 1 levels");
+    const unsigned n = st[0];
+    BM_CUDA(cudaMemsetAsync(cnt, 0, sizeof(unsigned), h->stream));
+    const int vb = (int)std::max<long long>(1, std::min<long long>((long long)h->sms * 16, ((long long)n * 32 + 255) / 256));
+    verify_level_kernel<<<vb, 256, 0, h->stream>>>(h->offs, h->adj, h->rtmp, qa, n, vis, qb, cnt, cnt + 1);
+    BM_CUDA(cudaGetLastError());
+    BM_CUDA(cudaMemcpyAsync(st, cnt, sizeof(st), cudaMemcpyDeviceToHost, h->stream));
+    BM_CUDA(cudaStreamSynchronize(h->stream));
+    std::swap(qa, qb);
+  }
+  if (is_max) *is_max = st[1] ? 0 : 1;
   return BM_OK;
 }
 

@@ -188,6 +188,26 @@ int main(int argc, char** argv) {
       invalid = true;
     }
     CHECK(invalid);
+    // the nc + 1 phase bound (gpu_match.cpp:313-320) -> std::runtime_error; the
+    // bound is lowered through the engine's fault-injection hook
+    const BipartiteCsr gr = generate_random_bipartite(50000, 50000, 6.0, 9);
+    const MatchingState gi = cheap_matching(gr);
+    bm_handle* h = b200::thread_engine(0).get();
+    CHECK(bm_debug_set(h, BM_DEBUG_PHASE_BOUND, 1) == BM_OK);
+    bool bound = false;
+    try {
+      b200::apfb(gr, gi, GridConfig{}, Schedule::serial(), BfsKernel::GpubfsWr);
+    } catch (const std::runtime_error& e) {
+      bound = std::string(e.what()).find("bound") != std::string::npos;
+    }
+    CHECK(bound);
+    CHECK(bm_debug_set(h, BM_DEBUG_PHASE_BOUND, 0) == BM_OK);
+    // a raced phase with no progress takes the serial retry (gpu_match.cpp:328-343)
+    CHECK(bm_debug_set(h, BM_DEBUG_SKIP_ALTERNATE_PHASE, 1) == BM_OK);
+    const DriverResult rr = b200::apfb(gr, gi, GridConfig{}, Schedule::serial(), BfsKernel::GpubfsWr);
+    CHECK(rr.counters.serial_retries == 1);
+    CHECK(bm_debug_set(h, BM_DEBUG_SKIP_ALTERNATE_PHASE, 0) == BM_OK);
+    check_result(gr, rr.matching, cardinality(hopcroft_karp(gr, gi)));
   }
 
   // 4. the reference's suite runner with its cardinality-mismatch gate

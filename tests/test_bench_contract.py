@@ -37,6 +37,23 @@ def test_reference_arm_contract():
     assert "workload" in d["config"]
 
 
+def test_reference_arm_does_not_load_the_product():
+    """The reference arm builds its graph with oracle/gen_oracle.cpp: neither the
+    product package nor libbmatch_b200.so may be loaded in that process."""
+    if not os.path.exists(os.path.join(ROOT, "oracle", "_ref", "libbmatch_ref.so")):
+        pytest.skip("oracle/_ref not built")
+    code = ("import sys; sys.argv = ['bench.py', '--impl', 'reference', '--config', 'C1', '--steps', '1', "
+            "'--warmup', '0']; import bench; bench.main(); "
+            "maps = open('/proc/self/maps').read(); "
+            "assert 'libbmatch_b200' not in maps, 'product library mapped'; "
+            "assert not any(m.startswith('paper_1303_1379_b200') for m in sys.modules), 'product imported'; "
+            "print('CLEAN', file=sys.stderr)")
+    out = subprocess.run([sys.executable, "-c", code], cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0 and "CLEAN" in out.stderr, out.stderr[-2000:]
+    d = json.loads([l for l in out.stdout.splitlines() if l.strip()][-1])
+    assert d["cardinality"] == 99961 and d["parity"]["ok"]
+
+
 @pytest.mark.gpu
 def test_b200_arm_contract():
     d = _run(["--config", "C1", "--steps", "3", "--warmup", "3", "--no-cpu-baseline"])

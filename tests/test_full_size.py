@@ -48,3 +48,31 @@ def test_full_size_configs(engine, cfg):
             m = engine.download()
             viol, ismax, vcard = engine.verify(g, m)
             assert viol == 0 and ismax and vcard == want, (cfg, algo, bottom_up, viol, ismax, vcard)
+
+
+@pytest.mark.gpu
+@pytest.mark.slow
+def test_full_size_c5(engine):
+    """C5 (configs[4], 1.6e9 edges) on one B200: the maximum the reference
+    computed (apfb-wr-ct parallel, tests/golden/make_large_answers.py C5) on the
+    same graph (digest), by the bench's configuration (AUTO: pulled dense
+    levels), by pushed levels, and by APsB-WR; every result passes the GPU
+    certificate (valid, and no augmenting path by the independent queue BFS)."""
+    import paper_1303_1379_b200 as bm
+    full = KNOWN["C5/full"]
+    g, known = bench.build_graph("C5", 1)
+    assert g.num_edges() == full["edges"] and str(bm.csc_digest(g)) == full["digest"]
+    assert known == full["maximum"]
+    init = bm.cheap_matching(g)
+    assert bm.cardinality(init) == full["first_fit"]
+    engine.upload(g, force=True)
+    engine.load_matching(init)
+    for algo, bottom_up in [("apfb-wr", "auto"), ("apfb-wr", False), ("apsb-wr", "auto")]:
+        shortest, kernel, improved = bench.ALGOS[algo]
+        card, ct, done = engine.run(shortest=shortest, kernel=bm.BfsKernel(kernel), improved=improved,
+                                    bottom_up=bottom_up)
+        assert done and card == full["maximum"], (algo, bottom_up, card)
+        m = engine.download()
+        viol, ismax, vcard = engine.verify(g, m)
+        assert viol == 0 and ismax and vcard == full["maximum"], (algo, bottom_up, viol, ismax, vcard)
+        engine.load_matching(init)

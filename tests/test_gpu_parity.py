@@ -353,3 +353,95 @@ def test_mixed_pushed_and_pulled_levels_parity(oracle, corpus, monkeypatch):
             assert bm.cardinality(m) == want, (g.name, shortest, kernel)
             assert oracle.validate(g, m.rmatch, m.cmatch) == 0
     eng.close()
+
+
+# ---- failure paths of run_driver (fault injection through bm_debug_set) ----
+
+@pytest.mark.parametrize("cfg", CONFIGS, ids=[c[0] for c in CONFIGS])
+@pytest.mark.parametrize("bottom_up", [False, True])
+def test_serial_retry_after_no_progress_phase(oracle, cfg, bottom_up, monkeypatch):
+    """A raced phase that found paths but augmented none is rerun with a serial
+    ALTERNATE (gpu_match.cpp:328-343): phase 1's parallel ALTERNATE is made a
+    no-op, so the device must take the retry, count it, and still reach the
+    maximum."""
+    if bottom_up:
+        monkeypatch.setenv("BM_BU_FRAC", "0")  # every wide level pulled
+    _, shortest, kernel, improved = cfg
+    eng = bm.Engine(0)
+    g = bm.generate_random_bipartite(20000, 20000, 6.0, 3)
+    init = bm.cheap_matching(g)
+    want = oracle.maximum(g)
+    eng.debug_set(bm.Engine.DEBUG_SKIP_ALTERNATE_PHASE, 1)
+    eng.upload(g)
+    eng.load_matching(init)
+    card, ct, done = eng.run(shortest=shortest, kernel=kernel, improved=improved, bottom_up=bottom_up)
+    assert done and card == want
+    assert ct.serial_retries == 1
+    m = eng.download()
+    assert oracle.validate(g, m.rmatch, m.cmatch) == 0 and oracle.is_maximum(g, m.rmatch, m.cmatch) == 1
+    # the retried phase is one outer iteration (its launches include both BFS passes)
+    res = eng.match(g, init, shortest=shortest, kernel=kernel, improved=improved)
+    _check(oracle, g, res, want)
+    assert res.counters.serial_retries == 1
+    events = []
+    eng.match(g, init, shortest=shortest, kernel=kernel, improved=improved, observer=events.append)
+    assert events[0].serial_retry and events[0].cardinality_after > events[0].cardinality_before
+    assert not any(e.serial_retry for e in events[1:])
+    eng.debug_set(bm.Engine.DEBUG_SKIP_ALTERNATE_PHASE, 0)
+    res = eng.match(g, init, shortest=shortest, kernel=kernel, improved=improved)
+    assert res.counters.serial_retries == 0
+
+
+def test_phase_bound_exceeded_raises(engine, oracle):
+    """More than the bound's phases -> runtime_error (gpu_match.cpp:313-320),
+    BM_ERR_BOUND_EXCEEDED at the C ABI; the handle stays usable."""
+    g = bm.generate_random_bipartite(50000, 50000, 6.0, 9)
+    init = bm.cheap_matching(g)
+    want = oracle.maximum(g)
+    res = engine.match(g, init)
+    assert res.counters.outer_iterations >= 3
+    engine.debug_set(bm.Engine.DEBUG_PHASE_BOUND, 2)
+    try:
+        with pytest.raises(RuntimeError, match="bound"):
+            engine.match(g, init)
+        engine.upload(g)
+        engine.load_matching(init)
+        with pytest.raises(RuntimeError, match="bound"):
+            engine.run()
+        # a bound the run fits under is not an error
+        engine.debug_set(bm.Engine.DEBUG_PHASE_BOUND, res.counters.outer_iterations + 8)
+        _check(oracle, g, engine.match(g, init), want)
+    finally:
+        engine.debug_set(bm.Engine.DEBUG_PHASE_BOUND, 0)
+    _check(oracle, g, engine.match(g, init), want)
+
+
+def test_initial_matching_pair_must_be_an_edge(engine):
+    """validate (matching.cpp:70-104): a matched (row, col) pair that is not an
+    edge makes the initial matching invalid — including a column with no edges
+    at all — on both the host-init path (bm_match) and the resident path."""
+    # c0 = {r0}, c1 = {} (degree 0), c2 = {r1, r2}
+    g = bm.BipartiteCsr(3, 3, np.array([0, 1, 1, 3], np.int64), np.array([0, 1, 2], np.int32))
+    cases = [
+        bm.MatchingState(np.array([1, -1, -1], np.int32), np.array([-1, 0, -1], np.int32)),  # c1-r0, deg(c1)=0
+        bm.MatchingState(np.array([-1, -1, -1], np.int32), np.array([-1, -1, -1], np.int32)),
+        bm.MatchingState(np.array([2, -1, -1], np.int32), np.array([-1, -1, 0], np.int32)),  # c2-r0 not an edge
+    ]
+    for i, m in enumerate(cases):
+        if i == 1:
+            assert bm.cardinality(engine.match(g, m).matching) == 2
+            continue
+        with pytest.raises(ValueError):
+            engine.match(g, m)
+        engine.upload(g, force=True)
+        engine.load_matching(m)
+        with pytest.raises(ValueError):
+            engine.run()
+    gu = bm.BipartiteCsr(2, 3, np.array([0, 2, 4], np.int64), np.array([2, 0, 1, 2], np.int32))  # unsorted c0
+    ok = bm.MatchingState(np.array([0, -1, -1], np.int32), np.array([0, -1], np.int32))
+    assert bm.cardinality(engine.match(gu, ok).matching) == 2
+    bad = bm.MatchingState(np.array([-1, 0, -1], np.int32), np.array([1, -1], np.int32))  # c0-r1 not an edge
+    with pytest.raises(ValueError):
+        engine.match(gu, bad)
+    r = engine.match(g, bm.cheap_matching(g))  # still usable
+    assert bm.cardinality(r.matching) == 2

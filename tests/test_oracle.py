@@ -226,3 +226,31 @@ def test_known_answers_oracle(oracle):
     g = bm.generate_rmat(18, 16.0, 2024)
     k = ka["rmat/18/16/2024"]
     assert bm.csc_digest(g) == int(k["digest"]) and oracle.maximum(g) == k["maximum"]
+
+
+def test_generator_restatement_matches(oracle):
+    """oracle/gen_oracle.cpp (the reference arm's input builder, which must not
+    load the product library) produces the same CSC as the product generators,
+    and its uniform generator is the reference's generate_random_bipartite
+    (csr_graph.cpp:92-112; digest of the 100K C1 graph from known_answers.json)."""
+    from oracle import Generators
+    gen = Generators(threads=4)
+    pairs = [
+        (gen.uniform(100_000, 100_000, 8.0, 1), bm.generate_random_bipartite(100_000, 100_000, 8.0, 1)),
+        (gen.uniform(3_001, 2_000, 5.5, 77), bm.generate_random_bipartite(3_001, 2_000, 5.5, 77)),
+        (gen.planted(200_000, 16.0, 2024), bm.generate_planted(200_000, 16.0, 2024)),
+        (gen.rmat(14, 16.0, 2024), bm.generate_rmat(14, 16.0, 2024)),
+        (gen.banded(300_000, 3, 0.05, 12345)[0], bm.generate_banded(300_000, 3, 0.05, 12345)[0]),
+    ]
+    for og, pg in pairs:
+        assert (og.nc, og.nr) == (pg.nc, pg.nr)
+        assert np.array_equal(og.cxadj, pg.cxadj), og.name
+        assert np.array_equal(og.cadj, pg.cadj), og.name
+    assert gen.banded(300_000, 3, 0.05, 12345)[1] == bm.generate_banded(300_000, 3, 0.05, 12345)[1]
+    ka = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "known_answers.json")))
+    g1 = pairs[0][0]
+    assert str(bm.csc_digest(g1)) == ka["uniform/100000/8.0/1"]["digest"]
+    r, c = gen.first_fit(g1)
+    assert int((r >= 0).sum()) == ka["uniform/100000/8.0/1"]["first_fit"]
+    r2, c2 = oracle.cheap_matching(g1)
+    assert np.array_equal(r, r2) and np.array_equal(c, c2)
