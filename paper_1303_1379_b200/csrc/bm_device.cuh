@@ -51,6 +51,11 @@ __device__ __forceinline__ int4 ld_cg(const int4* p) {
                : "l"(p));
   return v;
 }
+__device__ __forceinline__ int2 ld_cg(const int2* p) {
+  int2 v;
+  asm volatile("ld.global.cg.v2.b32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
+  return v;
+}
 __device__ __forceinline__ unsigned ld_cg_u(const int4* p) {  // .w field only
   unsigned v;
   asm volatile("ld.global.cg.b32 %0, [%1];" : "=r"(v) : "l"(reinterpret_cast<const char*>(p) + 12));
@@ -138,6 +143,10 @@ __device__ __forceinline__ int4 ld_cg_stream(const int4* p, unsigned long long p
 }
 __device__ __forceinline__ void st_stream(int* p, int v, unsigned long long pol) {
   asm volatile("st.global.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(p), "r"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void st_stream(int2* p, int2 v, unsigned long long pol) {
+  asm volatile("st.global.L2::cache_hint.v2.b32 [%0], {%1,%2}, %3;" ::"l"(p), "r"(v.x), "r"(v.y), "l"(pol)
+               : "memory");
 }
 __device__ __forceinline__ void st_stream(int4* p, int4 v, unsigned long long pol) {
   asm volatile("st.global.L2::cache_hint.v4.b32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),

@@ -120,6 +120,8 @@ enum CtlError : int {
   kErrBarrier = 3,      // grid barrier watchdog fired
   kErrWalk = 4,         // an ALTERNATE walk exceeded nc steps (cannot happen on valid state)
   kErrLevels = 5,       // more BFS levels than columns (cannot happen)
+  kErrWindow = 6,       // a push window's live edges exceed its tile (inconsistent frontier entries)
+  kErrCheck = 7,        // BM_CHECK=1 self-check of a level's entries failed (dbg holds the details)
 };
 
 struct alignas(128) Slot {
@@ -153,6 +155,9 @@ enum Stat : int {
   kStCycFlush,
   kStCycBarrier,
   kStCycOther,
+  kStRowsPulled,  // rows a pulled level screened in as candidates (scanned their own columns)
+  kStPulledLevels,
+  kStMaterialized,  // frontier entries turned from (col, root) pairs into edge-tiled entries
   kNumStats
 };
 
@@ -165,6 +170,8 @@ struct alignas(128) Ctrl {
   unsigned bar_sub[kBarSub][32];  // one 128-byte line per group counter
   Slot lvl[3];
   Slot roots;
+  Slot mat[2];  // materialize reservations, by level parity (never the level's own slot: slow CTAs
+                // may still be reading its count when the next level starts)
   unsigned n_ep;
   unsigned pad1[31];
   unsigned n_log;
@@ -198,6 +205,7 @@ struct alignas(128) Ctrl {
   int n_recs;
   int path_found_last;
   int phase_parity;
+  long long dbg[8];  // details of the first kErrWindow (ls, n, T, i, e, wend, live, level)
 };
 
 struct Params {
@@ -227,6 +235,7 @@ struct Params {
   int init_checked;  // the given initial matching was validated when it was loaded (bm_load_matching)
   int sorted;        // every column's rows ascend (binary-searchable adjacency)
   int dbg_skip_alt_phase;  // fault injection (bm_debug_set): this phase's raced ALTERNATE does nothing
+  int check;               // BM_CHECK=1: verify every pushed level's entries before expanding it (debugging)
   int max_phases;
   int stop_after_bfs;
   int trace;        // write bfs_array level labels (parity probes)
@@ -239,7 +248,18 @@ struct Params {
   unsigned* fbit[2];       // frontier bitmaps (nc bits each), alternating by level
   int* croot;              // root of each frontier column (bottom-up levels)
   int nfbit_words;
-  unsigned long long bu_min_edges;  // a level with at least this many frontier edges goes bottom-up
+  unsigned long long bu_min_edges;  // bu_rule 0: a level with at least this many frontier edges goes bottom-up
+  int bu_rule;             // 0: bu_min_edges threshold; 1: frontier edges vs unexplored edges (below)
+  float bu_alpha;          // bu_rule 1: pull when alpha * frontier edges >= edges of the unvisited rows ...
+  unsigned bu_min_n;       // ... and the frontier holds at least this many columns
+  double deg_col;          // E / nc: frontier edges of a level held as pairs are estimated from its size
+  double deg_row;          // E / nr
+  // Lazy frontier (pulled-capable kernels only): a wide level pushes its winners
+  // as (col, root) pairs; the next level either pulls straight from them or,
+  // when it is pushed, first turns them into edge-tiled entries (materialize).
+  // Winners of a pulled level never need their offsets gathered.
+  int2* P;                 // pairs, indexed like F (level entries [ls, ls + n))
+  unsigned long long pairs_min_edges;  // a pushed level this wide emits pairs
   long long phase_bound;
   unsigned long long* tl;  // stage timeline: (tag, %globaltimer ns) pairs written by the leader
   unsigned tl_cap;
@@ -505,6 +525,68 @@ __device__ __forceinline__ void stage_winner(Smem& sm, bool win, int col, int ro
   if (win) sm.wbuf[wb] = make_int2(col, root);
 }
 
+// Pushes the winners staged in sm.wbuf as (col, root) pairs: one slot
+// reservation per CTA, coalesced stores, no offsets gathered. CTA-uniform call.
+__device__ __forceinline__ void flush_pairs(const Params& p, Smem& sm, unsigned out_base, Slot* out,
+                                            unsigned long long pol) {
+  const unsigned nw = sm.nw;
+  if (!nw) return;
+  if (threadIdx.x == 0) sm.blk_base = atomicAdd(&out->packed, (unsigned long long)nw << 33);
+  __syncthreads();
+  const unsigned base = out_base + (unsigned)(sm.blk_base >> 33);
+  for (unsigned j = threadIdx.x; j < nw; j += kThreads) st_stream(p.P + base + j, sm.wbuf[j], pol);
+  __syncthreads();
+  if (threadIdx.x == 0) sm.nw = 0;
+}
+
+// Turns the n pairs of a level, P[ls, ls + n), into edge-tiled frontier entries
+// F[ls, ls + n) plus their granule index, for a level that is pushed.
+// Reservations go to `in`, a zeroed slot, whose low bits end as the level's
+// edge total. Every CTA of the caller's set must call it (a grid barrier must
+// follow before the entries are read).
+constexpr int kMatItems = 4;
+__device__ __forceinline__ void materialize(const Params& p, Smem& sm, int4* F, unsigned ls, unsigned n,
+                                            unsigned* gin, Slot* in, unsigned long long pol, bool solo) {
+  const unsigned long long G = solo ? 1ull : gridDim.x;
+  const unsigned long long B0 = solo ? 0ull : blockIdx.x;
+  unsigned done = 0;
+  for (unsigned long long b = B0 * kThreads * kMatItems; b < n; b += G * kThreads * kMatItems) {
+    int2 pr[kMatItems];
+    unsigned beg[kMatItems], deg[kMatItems];
+    unsigned cnt = 0, sum = 0;
+#pragma unroll
+    for (int k = 0; k < kMatItems; ++k) {
+      const unsigned long long i = b + (unsigned long long)k * kThreads + threadIdx.x;
+      pr[k] = i < n ? ld_cg(p.P + ls + i) : make_int2(-1, 0);
+    }
+#pragma unroll
+    for (int k = 0; k < kMatItems; ++k) {
+      beg[k] = pr[k].x >= 0 ? ld_ro(p.offs + pr[k].x) : 0u;
+      deg[k] = pr[k].x >= 0 ? ld_ro(p.offs + pr[k].x + 1) : 0u;
+    }
+#pragma unroll
+    for (int k = 0; k < kMatItems; ++k) {
+      deg[k] -= beg[k];
+      if (pr[k].x >= 0) {
+        cnt++;
+        sum += deg[k];
+      }
+    }
+    unsigned long long slot;
+    unsigned unused;
+    if (cta_reserve(sm, cnt, sum, 0u, in, &p.ctl->n_ep, slot, unused)) {
+#pragma unroll
+      for (int k = 0; k < kMatItems; ++k)
+        if (pr[k].x >= 0) {
+          put_entry(F, ls, gin, slot, pr[k].x, pr[k].y, beg[k], deg[k], pol);
+          slot += (1ull << 33) + deg[k];
+        }
+    }
+    done += cnt;
+  }
+  flush_count(sm, kStMaterialized, done);
+}
+
 // ---------------------------------------------------------------------------
 // Direction-optimised (bottom-up) level for dense frontiers. The same level of
 // the same BFS as expand_level (gpubfs / gpubfs_wr, gpu_match.cpp:42-70,
@@ -524,20 +606,50 @@ __device__ __forceinline__ void bu_clear(const Params& p, int lv) {
   for (unsigned long long k = global_thread(); k < (unsigned long long)p.nfbit_words; k += global_threads())
     st_plain(reinterpret_cast<int*>(fb) + k, 0);
 }
+// The frontier comes as (col, root) pairs (levels >= 1 of a pulled-capable
+// run) or as entries (level 0). Counts the live entries as columns expanded.
 template <bool WR>
-__device__ __forceinline__ void bu_prep(const Params& p, const int4* F, unsigned ls, unsigned n, int lv) {
+__device__ __forceinline__ void bu_prep(const Params& p, Smem& sm, const int4* F, bool pairs, unsigned ls,
+                                        unsigned n, int lv) {
   unsigned* fb = p.fbit[lv & 1];
-  for (unsigned long long k = global_thread(); k < n; k += global_threads()) {
-    const int4 ent = ld_cg(F + ls + k);
-    if (WR && root_dead(p, ent.y)) continue;
-    atomicOr(fb + (ent.x >> 5), 1u << (ent.x & 31));
-    st_plain(p.croot + ent.x, WR ? ent.y : ent.x);
+  unsigned live = 0;
+  constexpr int K = 8;  // entries per thread in flight (the loop is latency-bound otherwise)
+  const unsigned long long GT = global_threads();
+  for (unsigned long long k0 = global_thread(); k0 < n; k0 += K * GT) {
+    int col[K], root[K];
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      const unsigned long long k = k0 + i * GT;
+      col[i] = -1;
+      root[i] = 0;
+      if (k < n) {
+        if (pairs) {
+          const int2 pr = ld_cg(p.P + ls + k);
+          col[i] = pr.x;
+          root[i] = pr.y;
+        } else {
+          const int4 ent = ld_cg(F + ls + k);
+          col[i] = ent.x;
+          root[i] = ent.y;
+        }
+      }
+    }
+    bool on[K];
+#pragma unroll
+    for (int i = 0; i < K; ++i) on[i] = col[i] >= 0 && !(WR && root_dead(p, root[i]));
+#pragma unroll
+    for (int i = 0; i < K; ++i)
+      if (on[i]) {
+        live++;
+        atomicOr(fb + (col[i] >> 5), 1u << (col[i] & 31));
+        st_plain(p.croot + col[i], WR ? root[i] : col[i]);
+      }
   }
+  flush_count(sm, kStCexp, live);
 }
 
 template <bool WR, bool IMP>
-__device__ __forceinline__ void bu_sweep(const Params& p, Smem& sm, int4* F, unsigned out_base, unsigned* gout,
-                                         Slot* out, int lv, int pf) {
+__device__ __forceinline__ void bu_sweep(const Params& p, Smem& sm, unsigned out_base, Slot* out, int lv, int pf) {
   // Warp-synchronous: per CTA step every warp (1) screens kBuRows rows per lane
   // with independent loads and compacts its candidates (unvisited matched rows
   // and free rows) into a warp-private stage; (2) each candidate scans its
@@ -660,24 +772,25 @@ __device__ __forceinline__ void bu_sweep(const Params& p, Smem& sm, int4* F, uns
     if (++step % kFlushSteps == 0) {
       __syncthreads();
       if (sm.nw > kWBuf - kFlushSteps * kStepRows) {
-        flush_winners(p, sm, F, out_base, gout, out, pol);
+        flush_pairs(p, sm, out_base, out, pol);
         __syncthreads();  // the reset of sm.nw lands before the next stage_winner
       }
     }
   }
   __syncthreads();
-  flush_winners(p, sm, F, out_base, gout, out, pol);
+  flush_pairs(p, sm, out_base, out, pol);
   flush_count(sm, kStTrav, c_trav);
   flush_count(sm, kStNvis, c_nvis);
-  flush_count(sm, kStCexp, c_rows);
+  flush_count(sm, kStRowsPulled, c_rows);
 }
 
 // ---------------------------------------------------------------------------
 // One BFS level (GPUBFS, Alg. 2, gpu_match.cpp:42-70; GPUBFS-WR, Alg. 4,
 // gpu_match.cpp:99-133) over the frontier F[ls, ls+n) holding T edges.
-template <bool WR, bool IMP>
+template <bool WR, bool IMP, bool BU>
 __device__ __forceinline__ void expand_level(const Params& p, Smem& sm, int4* F, unsigned ls, unsigned n, unsigned T,
-                             const unsigned* gin, unsigned* gout, Slot* in, Slot* out, int level, int pf) {
+                             const unsigned* gin, unsigned* gout, Slot* in, Slot* out, int level, int pf,
+                             bool pairs_out) {
   if (T == 0) return;
   const unsigned tid = threadIdx.x;
   unsigned c_trav = 0, c_cexp = 0, c_nvis = 0, c_entries = 0;
@@ -768,6 +881,14 @@ __device__ __forceinline__ void expand_level(const Params& p, Smem& sm, int4* F,
           tot += t;
         }
         live = tot;
+        if (tot > kWBuf) {  // cannot happen on consistent entries: skip the window, report, stop the run
+          if (tid == 0 && atomicCAS(&p.ctl->error, 0, (int)kErrWindow) == 0) {
+            long long* d = p.ctl->dbg;
+            d[0] = ls; d[1] = n; d[2] = T; d[3] = i; d[4] = e; d[5] = wend; d[6] = tot; d[7] = level;
+          }
+          live = 0;
+          for (int k = 0; k < kEPT; ++k) len[k] = 0;
+        }
         unsigned vp = wbase + incl - tsum;
 #pragma unroll
         for (int k = 0; k < kEPT; ++k) {
@@ -902,7 +1023,8 @@ __device__ __forceinline__ void expand_level(const Params& p, Smem& sm, int4* F,
         t_a = t;
       }
       // Flush the window's winners: one CTA reservation for all of them.
-      flush_winners(p, sm, F, out_base, gout, out, pol);
+      if (BU && pairs_out) flush_pairs(p, sm, out_base, out, pol);
+      else flush_winners(p, sm, F, out_base, gout, out, pol);
       e = wend;
       i += kWin;
       __syncthreads();
@@ -988,18 +1110,67 @@ __device__ __forceinline__ void sweep_visited(const Params& p) {
   int4* r4 = reinterpret_cast<int4*>(p.rm);
   const unsigned long long n4 = (unsigned long long)p.nr / kRowsPer4;
   auto clr = [](int& v) { if (v >= 0) v &= ~kVisBit; };
-  for (unsigned long long k = global_thread(); k < n4; k += global_threads()) {
-    int4 v = ld_cg(r4 + k);
-    const int4 o = v;
-    clr(v.x);
-    if (!il) clr(v.y);
-    clr(v.z);
-    if (!il) clr(v.w);
-    if (v.x != o.x || v.y != o.y || v.z != o.z || v.w != o.w) st_plain(r4 + k, v);
+  constexpr int K = 4;  // int4s per thread in flight
+  const unsigned long long GT = global_threads();
+  for (unsigned long long k0 = global_thread(); k0 < n4; k0 += K * GT) {
+    int4 v[K];
+#pragma unroll
+    for (int i = 0; i < K; ++i)
+      if (k0 + i * GT < n4) v[i] = ld_cg(r4 + k0 + i * GT);
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      if (k0 + i * GT >= n4) continue;
+      const int4 o = v[i];
+      clr(v[i].x);
+      if (!il) clr(v[i].y);
+      clr(v[i].z);
+      if (!il) clr(v[i].w);
+      if (v[i].x != o.x || v[i].y != o.y || v[i].z != o.z || v[i].w != o.w) st_plain(r4 + k0 + i * GT, v[i]);
+    }
   }
   for (unsigned long long r = n4 * kRowsPer4 + global_thread(); r < (unsigned long long)p.nr; r += global_threads()) {
     const int v = ld_cg(RM(p, r));
     if (v >= 0 && (v & kVisBit)) st_plain(RM(p, r), v & ~kVisBit);
+  }
+}
+
+// Whether a level of T frontier edges over n columns is pulled (bu_rule 1:
+// direction-optimising BFS — pull once the frontier's edges are a large enough
+// share of the edges still to explore, i.e. of the rows not yet visited).
+__device__ __forceinline__ bool want_pull(const Params& p, unsigned long long T, unsigned n, unsigned ls) {
+  if (p.bu_rule == 0) return T >= p.bu_min_edges;
+  const long long unv = (long long)p.nr - (long long)ls - (long long)n;
+  const double mu = (unv > 0 ? (double)unv : 0.0) * p.deg_row;
+  return n >= p.bu_min_n && (double)T * (double)p.bu_alpha >= mu;
+}
+
+__device__ __forceinline__ void check_fail(const Params& p, long long a, long long b, long long c, long long d,
+                                           long long e, long long f, long long g, long long h) {
+  if (atomicCAS(&p.ctl->error, 0, (int)kErrCheck) == 0) {
+    long long* x = p.ctl->dbg;
+    x[0] = a; x[1] = b; x[2] = c; x[3] = d; x[4] = e; x[5] = f; x[6] = g; x[7] = h;
+  }
+}
+// BM_CHECK: the n entries of a pushed level are consecutive edge ranges
+// (pre[k] + deg[k] == pre[k+1], the last ending at T) and the granule index
+// points at the entry holding each granule's first edge.
+__device__ void check_level(const Params& p, const int4* F, unsigned ls, unsigned n, unsigned T, const unsigned* gin,
+                            int lv, int tag) {
+  for (unsigned long long k = global_thread(); k < n; k += global_threads()) {
+    const int4 a = ld_cg(F + ls + k);
+    if (a.x < 0 || a.x >= p.nc) {
+      check_fail(p, tag + 20, lv, ls, n, T, k, a.x, a.w);
+      continue;
+    }
+    const unsigned deg = ld_ro(p.offs + a.x + 1) - ld_ro(p.offs + a.x);
+    const unsigned nxt = k + 1 < n ? (unsigned)ld_cg(F + ls + k + 1).w : T;
+    if (a.x < 0 || a.x >= p.nc || (unsigned)a.w + deg != nxt || (unsigned)a.z != ld_ro(p.offs + a.x))
+      check_fail(p, tag, lv, ls, n, T, k, a.w, nxt);
+    if (deg) {
+      const unsigned m1 = ((unsigned)a.w + deg - 1) / kGran;
+      for (unsigned m = ((unsigned)a.w + kGran - 1) / kGran; m <= m1; ++m)
+        if ((unsigned)ld_cg(reinterpret_cast<const int*>(gin) + m) != k) check_fail(p, tag + 10, lv, ls, n, T, k, m, 0);
+    }
   }
 }
 
@@ -1026,12 +1197,39 @@ __device__ PhaseOut run_phase(const Params& p, Smem& sm, int cur, int parity, bo
   unsigned ls = 0;
   int lv = 0;
   bool found = false;
+  bool in_pairs = false;  // this level's entries are (col, root) pairs in P (pulled-capable kernels)
+  const unsigned long long pol_mat = policy_evict_first();
   // Narrow levels (at most solo_edges frontier edges) run on block 0 alone,
   // back to back with CTA barriers only — a grid barrier costs more than such
   // a level's work. The other CTAs wait at one grid barrier and take over
   // when the frontier widens again or the BFS ends.
   for (;;) {
-    const bool solo = T <= p.solo_edges;
+    Slot* in = lv == 0 ? &ctl->roots : &ctl->lvl[lv % 3];
+    // BU: compiled only into the bottom-up kernel instances, so the push-only
+    // kernel keeps its register allocation
+    const bool bu = BU && p.roffs && !p.trace && T > p.solo_edges && want_pull(p, T, n, ls);
+    const bool mat = BU && in_pairs && !bu;
+    if (p.check && BU && in_pairs) {
+      for (unsigned long long k = global_thread(); k < n; k += global_threads()) {
+        const int2 pr = ld_cg(p.P + ls + k);
+        if (pr.x < 0 || pr.x >= p.nc || pr.y < 0 || pr.y >= p.nc) check_fail(p, 40, lv, ls, n, T, k, pr.x, pr.y);
+      }
+      grid_sync(ctl);
+    }
+    if (mat) {  // pushed after all: build its edge-tiled entries first
+      Slot* ms = &ctl->mat[lv & 1];
+      materialize(p, sm, F, ls, n, (lv & 1) ? p.gidx1 : p.gidx0, ms, pol_mat, false);
+      grid_sync(ctl);
+      const unsigned long long mp = ld_rlx(&ms->packed);
+      T = (unsigned)(mp & kEdgeMask);
+      in_pairs = false;
+      if (p.check && is_leader() && (mp >> 33) != n) check_fail(p, 30, lv, ls, n, T, (long long)(mp >> 33), 0, 0);
+    }
+    if (p.check && !bu && T > p.solo_edges) {  // (block 0's solo levels are not checked)
+      check_level(p, F, ls, n, T, (lv & 1) ? p.gidx1 : p.gidx0, lv, mat ? 2 : 1);
+      grid_sync(ctl);
+    }
+    const bool solo = !bu && T <= p.solo_edges;
     if (solo && blockIdx.x != 0) {
       grid_sync(ctl);  // block 0's hand-over
       lv = ld_rlx(&ctl->solo_lv);
@@ -1040,27 +1238,28 @@ __device__ PhaseOut run_phase(const Params& p, Smem& sm, int cur, int parity, bo
       T = (unsigned)ld_rlx(&ctl->solo_T);
       found = ld_rlx(&ctl->solo_found) != 0;
       out.launches = (long long)ld_rlx((const unsigned long long*)&ctl->solo_launches);
+      in_pairs = false;  // solo levels push entries
       if (ld_rlx(&ctl->solo_stop)) break;
       continue;
     }
-    Slot* in = lv == 0 ? &ctl->roots : &ctl->lvl[lv % 3];
     Slot* outs = &ctl->lvl[(lv + 1) % 3];
     if (is_leader() && lv >= 1) {
       Slot* z = &ctl->lvl[(lv + 2) % 3];
       z->packed = 0;
       z->tile = 0;
     }
+    if (BU && is_leader()) ctl->mat[(lv + 1) & 1].packed = 0;  // last read before this level's barrier
     if (solo) __syncthreads();
-    // BU: compiled only into the bottom-up kernel instances, so the push-only
-    // kernel keeps its register allocation
-    const bool bu = BU && !solo && p.roffs && !p.trace && (unsigned long long)T >= p.bu_min_edges;
+    // a wide level hands its winners on as pairs (see Params::P)
+    const bool pairs_out = BU && p.roffs && !p.trace && !solo && (bu || (unsigned long long)T >= p.pairs_min_edges);
     if (bu) {
-      bu_prep<WR>(p, F, ls, n, lv);
+      bu_prep<WR>(p, sm, F, in_pairs, ls, n, lv);
       grid_sync(ctl);
-      bu_sweep<WR, IMP>(p, sm, F, ls + n, (lv & 1) ? p.gidx0 : p.gidx1, outs, lv, parity);
+      bu_sweep<WR, IMP>(p, sm, ls + n, outs, lv, parity);
+      if (threadIdx.x == 0) sm.cnt[kStPulledLevels] += is_leader() ? 1 : 0;
     } else {
-      expand_level<WR, IMP>(p, sm, F, ls, n, T, (lv & 1) ? p.gidx1 : p.gidx0, (lv & 1) ? p.gidx0 : p.gidx1,
-                            in, outs, kStartLevel + lv, parity);
+      expand_level<WR, IMP, BU>(p, sm, F, ls, n, T, (lv & 1) ? p.gidx1 : p.gidx0, (lv & 1) ? p.gidx0 : p.gidx1,
+                                in, outs, kStartLevel + lv, parity, pairs_out);
     }
 
     const long long tb = clk();
@@ -1083,6 +1282,8 @@ __device__ PhaseOut run_phase(const Params& p, Smem& sm, int cur, int parity, bo
       ls += n;
       n = n_next;
       T = (unsigned)(op & kEdgeMask);
+      in_pairs = pairs_out;
+      if (pairs_out) T = (unsigned)fmin((double)n * p.deg_col, 4294967295.0);  // an estimate until materialized
       ++lv;
       if (lv > p.nc + 2) {
         if (is_leader()) ctl->error = kErrLevels;
@@ -1168,6 +1369,8 @@ __device__ PhaseOut run_phase(const Params& p, Smem& sm, int cur, int parity, bo
     }
     ctl->roots.packed = 0;
     ctl->roots.tile = 0;
+    ctl->mat[0].packed = 0;
+    ctl->mat[1].packed = 0;
   }
   grid_sync(ctl);
   tl_mark(p, kTlFixRows, dense ? 1u : 0u);
@@ -1817,7 +2020,12 @@ struct bm_handle {
   unsigned* tp_pcur = nullptr;  // row-index build scratch (bucket cursors, bucketed pairs)
   int2* tp_pairs = nullptr;
   unsigned char* tp_tmp = nullptr;  // CUB scan scratch
-  double bu_frac = 0.45;      // a level goes bottom-up when its frontier edges >= bu_frac * E
+  double bu_frac = 0.45;      // BM_BU_FRAC (bu_rule 0): a level goes bottom-up when its frontier edges >= bu_frac * E
+  int bu_rule = 1;            // 1: want_pull's direction-optimising test (default); 0: the bu_frac threshold
+  float bu_alpha = 14.f;      // want_pull: pull when alpha * frontier edges >= edges of the unvisited rows
+  double bu_beta = 24.0;      // ... and the frontier holds >= nc / beta columns
+  long long nonempty = 0;     // columns with at least one edge (upload)
+  int2* P = nullptr;          // lazy-frontier pairs (nc), pulled-capable runs only
   unsigned* roffs = nullptr;
   int* radj = nullptr;
   unsigned* rcursor = nullptr;
@@ -1910,9 +2118,7 @@ bm_status build_transpose(bm_handle* h, int nc, int nr, long long E) {
     // far beyond L2 (the interleaved layout) every pushed gather pays DRAM
     // sectors, so pulling pays from sparser frontiers: measured optimum 0.15-0.25
     // on C5 against 0.45-0.6 on C2 (profiles/README.md).
-    h->bu_frac = h->rs == 2 ? 0.2 : 0.45;
-    const char* fr = getenv("BM_BU_FRAC");
-    if (fr) h->bu_frac = atof(fr);
+
   }
   if (h->bu_enabled) {
     BM_CUDA(dalloc(h->caps, h->roffs, (size_t)nr + 1));
@@ -1921,6 +2127,7 @@ bm_status build_transpose(bm_handle* h, int nc, int nr, long long E) {
     h->nfbit_words = (nc + 31) / 32;
     BM_CUDA(dalloc(h->caps, h->fbit, (size_t)2 * h->nfbit_words));
     BM_CUDA(dalloc(h->caps, h->croot, (size_t)nc));
+    BM_CUDA(dalloc(h->caps, h->P, (size_t)nc));
     // rows bucketed so that one bucket's slice of radj is at most 32 MB
     int shift = 0;
     {
@@ -2081,7 +2288,27 @@ Params make_params(bm_handle* h, const bm_match_opts& o) {
   p.fbit[1] = h->fbit ? h->fbit + h->nfbit_words : nullptr;
   p.croot = h->croot;
   p.nfbit_words = h->nfbit_words;
+  // pull rule (tuning knobs read per run): BM_BU_FRAC selects the plain edge-share
+  // threshold; otherwise want_pull's test with BM_BU_ALPHA / BM_BU_BETA
+  h->bu_frac = h->rs == 2 ? 0.2 : 0.45;
+  h->bu_rule = 1;
+  if (const char* fr = getenv("BM_BU_FRAC")) {
+    h->bu_frac = atof(fr);
+    h->bu_rule = 0;
+  }
+  h->bu_alpha = h->rs == 2 ? 14.f : 4.f;
+  if (const char* a = getenv("BM_BU_ALPHA")) h->bu_alpha = (float)atof(a);
+  h->bu_beta = 24.0;
+  if (const char* b = getenv("BM_BU_BETA")) h->bu_beta = atof(b);
   p.bu_min_edges = (unsigned long long)std::max(1.0, h->bu_frac * (double)h->E);
+  p.bu_rule = h->bu_rule;
+  p.bu_alpha = h->bu_alpha;
+  p.bu_min_n = (unsigned)std::min<double>(4e9, (double)h->nc / std::max(1e-9, h->bu_beta));
+  p.deg_col = (double)h->E / (double)std::max<long long>(1, h->nonempty);
+  p.deg_row = (double)h->E / (double)std::max(1, h->nr);
+  p.P = h->P;
+  p.pairs_min_edges = std::max<unsigned long long>(1ull << 20, (unsigned long long)h->E / 128);
+  if (const char* pm = getenv("BM_PAIRS_MIN_EDGES")) p.pairs_min_edges = (unsigned long long)atoll(pm);
   p.ndead_words = h->ndead_words;
   p.F0 = h->F[0];
   p.F1 = h->F[1];
@@ -2108,6 +2335,7 @@ Params make_params(bm_handle* h, const bm_match_opts& o) {
   p.phase_bound = (long long)h->nc + 1;
   if (h->dbg_phase_bound > 0) p.phase_bound = h->dbg_phase_bound;
   p.sorted = h->sorted;
+  p.check = getenv("BM_CHECK") ? atoi(getenv("BM_CHECK")) : 0;
   p.dbg_skip_alt_phase = h->dbg_skip_alt_phase;
   return p;
 }
@@ -2123,6 +2351,7 @@ bm_status ctl_error_status(int err) {
     case kErrBarrier: return fail(BM_ERR_CUDA, "grid barrier watchdog fired");
     case kErrWalk: return fail(BM_ERR_CUDA, "ALTERNATE walk exceeded nc steps");
     case kErrLevels: return fail(BM_ERR_CUDA, "BFS exceeded nc + 2 levels");
+    case kErrWindow: return fail(BM_ERR_CUDA, "inconsistent frontier entries (push window wider than its tile)");
     default: return fail(BM_ERR_CUDA, "unknown device error " + std::to_string(err));
   }
 }
@@ -2175,6 +2404,11 @@ bm_status drive(bm_handle* h, const bm_match_opts& o, bool fresh, int64_t* cardi
     }
     if (ctl.error) {
       h->resumable = false;
+      if (ctl.error == kErrWindow || ctl.error == kErrCheck) {
+        std::string d;
+        for (int i = 0; i < 8; ++i) d += (i ? "," : "") + std::to_string(ctl.dbg[i]);
+        return fail(BM_ERR_CUDA, "inconsistent frontier entries (push window wider than its tile): ls,n,T,i,e,wend,live,level=" + d);
+      }
       return ctl_error_status(ctl.error);
     }
     recs.resize(ctl.n_recs);
@@ -2343,6 +2577,7 @@ bm_status bm_destroy(bm_handle* h) {
   dfree(h->rcursor);
   dfree(h->fbit);
   dfree(h->croot);
+  dfree(h->P);
   dfree(h->gidx[0]);
   dfree(h->gidx[1]);
   dfree(h->wlog);
@@ -2443,6 +2678,7 @@ bm_status bm_upload_csc(bm_handle* h, int32_t nc, int32_t nr, const int64_t* cxa
   BM_CUDA(cudaStreamSynchronize(h->stream));
   {  // BM_BU_AUTO (bmatch_b200.h): large, few empty columns, average degree >= 8 over the rest
     const long long nonempty = (long long)nc - (long long)bad[4];
+    h->nonempty = nonempty;
     h->bu_auto = nr >= (1 << 21) && nonempty * 4 >= 3ll * nc && E >= 8 * nonempty;
     h->bu_huge = nr >= (1 << 26);  // rmatch >= 256 MB: pushed dense levels pay DRAM sectors per gather
     const char* fa = getenv("BM_BU_AUTO");

@@ -445,3 +445,29 @@ def test_initial_matching_pair_must_be_an_edge(engine):
         engine.match(gu, bad)
     r = engine.match(g, bm.cheap_matching(g))  # still usable
     assert bm.cardinality(r.matching) == 2
+
+
+@pytest.mark.parametrize("spec", [{}, {"BM_BU_FRAC": "1.0"}, {"BM_BU_ALPHA": "100", "BM_SOLO_EDGES": "0"}])
+def test_lazy_frontier_self_check(oracle, monkeypatch, spec):
+    """Pulled-capable runs hand wide levels on as (col, root) pairs and build
+    edge-tiled entries only for levels that are pushed (materialize). BM_CHECK=1
+    makes the kernel verify every pushed level's entries and granule index
+    before expanding it (a failed check is a CudaError). Skewed graph, repeated
+    runs: the check once caught a race between a level's count and the next
+    level's reservations."""
+    monkeypatch.setenv("BM_CHECK", "1")
+    for k, v in spec.items():
+        monkeypatch.setenv(k, v)
+    g = bm.generate_rmat(20, 16.0, 7)
+    want = oracle.maximum(g)
+    init = bm.cheap_matching(g)
+    eng = bm.Engine(0)
+    eng.upload(g)
+    eng.load_matching(init)
+    eng.prepare_row_index()
+    for _ in range(4):
+        for _, shortest, kernel, improved in CONFIGS:
+            card, ct, done = eng.run(shortest=shortest, kernel=kernel, improved=improved, bottom_up=True)
+            assert done and card == want
+    m = eng.download()
+    assert oracle.validate(g, m.rmatch, m.cmatch) == 0 and oracle.is_maximum(g, m.rmatch, m.cmatch) == 1
