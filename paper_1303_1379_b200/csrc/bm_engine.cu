@@ -103,6 +103,11 @@ constexpr unsigned kWBuf = kGran * kMaxTileGran;
 #define BM_SOLO_EDGES 1024
 #endif
 constexpr unsigned kSoloEdges = BM_SOLO_EDGES;  // widest level block 0 expands alone
+#ifdef BM_CLAIM_STORE
+constexpr size_t kFSlack(long long nc) { return (size_t)(nc / 4 + 4096); }
+#else
+constexpr size_t kFSlack(long long) { return 0; }
+#endif
 constexpr int kStartLevel = 2;        // L0 (gpu_match.cpp:275)
 constexpr int kUnvisited = kStartLevel - 1;
 constexpr int kFoundMark = kStartLevel - 2;
@@ -282,6 +287,15 @@ __device__ __forceinline__ void tl_mark(const Params& p, unsigned kind, unsigned
     p.ctl->n_tl = n + 1;
   }
 }
+
+// A pulled-level candidate row: its row-state value and its column range in the row index.
+struct BuCand {
+  int row;
+  int val;
+  unsigned j0;
+  unsigned j1;
+};
+constexpr int kCandCap = 160;  // per-warp queue: < 32 left over + one screened chunk of 128 rows
 
 struct Smem {
   union {  // a top-down window, or a bottom-up candidate stage (never both at once)
@@ -784,6 +798,183 @@ __device__ __forceinline__ void bu_sweep(const Params& p, Smem& sm, unsigned out
   flush_count(sm, kStRowsPulled, c_rows);
 }
 
+// Warp-autonomous pulled level. Every warp owns chunks of 128 consecutive rows
+// (grid-stride over the warps of the grid) and keeps a queue of candidate rows
+// in shared memory: screening a chunk reads the rows' state and their row-index
+// offsets in one coalesced round and appends the candidates (unvisited matched
+// rows, free rows) with their column ranges. Lanes then probe independently:
+// a lane whose row is resolved (hit, or its columns exhausted) takes the next
+// queued candidate in the following round, so a warp never waits for its
+// slowest row, and no CTA-wide barrier is needed — winners are staged per warp
+// in its slice of wbuf and flushed with one reservation per warp.
+template <bool WR, bool IMP>
+__device__ __forceinline__ void bu_sweep_q(const Params& p, Smem& sm, unsigned out_base, Slot* out, int lv, int pf) {
+  constexpr int kWarps = kThreads / 32;
+  constexpr unsigned kChunk = 128;
+  constexpr unsigned kWStage = 128;  // winners staged per warp
+  // wbuf is free during a pulled level: it holds the warps' candidate queues, then their winner stages
+  static_assert(sizeof(BuCand) * kCandCap * kWarps + sizeof(int2) * kWStage * kWarps <= sizeof(int2) * kWBuf,
+                "candidate queues and winner stages must fit in wbuf");
+  constexpr int kBuProbe = BM_BU_PROBE;
+  const unsigned* fb = p.fbit[lv & 1];
+  const unsigned long long pol = policy_evict_first();
+  unsigned* const path_flag = &p.ctl->path_found[pf];
+  unsigned c_trav = 0, c_nvis = 0, c_rows = 0;
+  const unsigned warp = threadIdx.x >> 5, lane = lane_id();
+  BuCand* const q = reinterpret_cast<BuCand*>(sm.wbuf) + warp * kCandCap;
+  int2* const wst = reinterpret_cast<int2*>(reinterpret_cast<BuCand*>(sm.wbuf) + kWarps * kCandCap) + warp * kWStage;
+  const unsigned long long nchunks = ((unsigned long long)p.nr + kChunk - 1) / kChunk;
+  const unsigned long long W = (unsigned long long)gridDim.x * kWarps;
+  unsigned long long chunk = (unsigned long long)blockIdx.x * kWarps + warp;
+  unsigned qh = 0, qt = 0;  // queued candidates q[qh, qt) (warp-uniform)
+  unsigned nwin = 0;        // winners staged in wst (warp-uniform)
+  int rr = -1, vv = 0;      // this lane's current candidate
+  unsigned j = 0, j1 = 0;
+  for (;;) {
+    // refill: the idle lanes would drain the queue and rows remain
+    const unsigned idle = __ballot_sync(kFull, rr < 0);
+    while (qt - qh < (unsigned)__popc(idle) && chunk < nchunks) {  // (a chunk may hold no candidate)
+      // move the leftovers (< 32) to the front, then screen one chunk
+      const unsigned left = qt - qh;
+      BuCand keep;
+      if (lane < left) keep = q[qh + lane];
+      __syncwarp();
+      if (lane < left) q[lane] = keep;
+      qh = 0;
+      qt = left;
+      const unsigned long long r0 = chunk * kChunk;
+      chunk += W;
+      int v[4];
+      unsigned o[4], onext;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const unsigned long long r = r0 + (unsigned long long)k * 32 + lane;
+        v[k] = r < (unsigned long long)p.nr ? ld_cg(RM(p, r)) : -3;
+        o[k] = r <= (unsigned long long)p.nr ? ld_ro(p.roffs + r) : 0u;  // roffs[nr] ends the last row
+      }
+      {
+        const unsigned long long r = r0 + 4 * 32;
+        onext = (lane == 0 && r <= (unsigned long long)p.nr) ? ld_ro(p.roffs + r) : 0u;
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        // end of this row's columns = start of the next row's
+        unsigned e = __shfl_down_sync(kFull, o[k], 1);
+        const unsigned nxt0 = __shfl_sync(kFull, k < 3 ? o[(k + 1) & 3] : onext, 0);
+        if (lane == 31) e = nxt0;
+        const bool is_cand = (v[k] >= 0 && !(v[k] & kVisBit)) || v[k] == -1;
+        const unsigned m = __ballot_sync(kFull, is_cand && e > o[k]);
+        if (is_cand && e > o[k]) {
+          BuCand c;
+          c.row = (int)(r0 + (unsigned long long)k * 32 + lane);
+          c.val = v[k];
+          c.j0 = o[k];
+          c.j1 = e;
+          q[qt + __popc(m & ((1u << lane) - 1))] = c;
+        }
+        qt += __popc(m);
+      }
+      __syncwarp();
+    }
+    // idle lanes take queued candidates in lane order
+    {
+      const unsigned avail = qt - qh;
+      const unsigned rank = __popc(idle & ((1u << lane) - 1));
+      if (rr < 0 && rank < avail) {
+        const BuCand c = q[qh + rank];
+        rr = c.row;
+        vv = c.val;
+        j = c.j0;
+        j1 = c.j1;
+        c_rows++;
+      }
+      qh += min((unsigned)__popc(idle), avail);
+    }
+    if (!__any_sync(kFull, rr >= 0)) break;  // queue empty and every chunk screened
+    // one probe round
+    bool win = false, ep = false;
+    int cw = 0, rootw = 0;
+    const int myrow = rr;
+    if (rr >= 0) {
+      int cs[kBuProbe];
+      unsigned wd[kBuProbe];
+#pragma unroll
+      for (int k = 0; k < kBuProbe; ++k) cs[k] = j + k < j1 ? ld_stream(p.radj + j + k, pol) : -1;
+#pragma unroll
+      for (int k = 0; k < kBuProbe; ++k)
+        wd[k] = cs[k] >= 0 ? ld_ca(reinterpret_cast<const int*>(fb) + (cs[k] >> 5)) : 0u;
+      bool done = false;
+#pragma unroll
+      for (int k = 0; k < kBuProbe; ++k) {
+        const int c = cs[k];
+        if (done || c < 0) continue;
+        c_trav++;
+        if (!((wd[k] >> (c & 31)) & 1)) continue;
+        const int root = ld_cg(p.croot + c);
+        if (vv >= 0) {  // matched row: its column joins the frontier below c's tree
+          st_plain(RM(p, rr), vv | kVisBit);
+          st_plain(PR(p, rr), c);
+          win = true;
+          cw = vv;
+          rootw = root;
+          done = true;
+          continue;
+        }
+        // free row: an endpoint of c's tree
+        const bool one = WR && p.ep_one;
+        if (one && root_dead(p, root)) continue;
+        bool mine = true;
+        if (one) mine = atomicCAS(p.bfs + root, kStartLevel, IMP ? -rr : kFoundMark) == kStartLevel;
+        else if (WR) st_rlx(p.bfs + root, IMP ? -rr : kFoundMark);
+        if (!mine) continue;  // that tree already holds an endpoint: try another neighbour
+        if (WR) mark_dead(p, root);
+        st_rlx(RM(p, rr), -2);
+        st_plain(PR(p, rr), c);
+        ep = true;
+        if (ld_rlx(path_flag) == 0u) st_rlx(path_flag, 1u);
+        done = true;
+      }
+      j += kBuProbe;
+      if (done || j >= j1) rr = -1;
+    }
+    // stage winners in this warp's slice of wbuf; flush it when the next round might not fit
+    {
+      const unsigned m = __ballot_sync(kFull, win);
+      if (win) wst[nwin + __popc(m & ((1u << lane) - 1))] = make_int2(cw, rootw);
+      nwin += __popc(m);
+      c_nvis += win ? 1u : 0u;
+      if (nwin > kWStage - 32) {
+        __syncwarp();
+        unsigned base = 0;
+        if (lane == 0) base = (unsigned)(atomicAdd(&out->packed, (unsigned long long)nwin << 33) >> 33);
+        base = __shfl_sync(kFull, base, 0) + out_base;
+        for (unsigned i = lane; i < nwin; i += 32) st_stream(p.P + base + i, wst[i], pol);
+        __syncwarp();
+        nwin = 0;
+      }
+    }
+    {  // endpoints: rare, warp-aggregated global append
+      const unsigned m = __ballot_sync(kFull, ep);
+      if (m) {
+        unsigned eb = 0;
+        if (lane == 0) eb = atomicAdd(&p.ctl->n_ep, (unsigned)__popc(m));
+        eb = __shfl_sync(kFull, eb, 0) + __popc(m & ((1u << lane) - 1));
+        if (ep) st_plain(p.EP + eb, myrow);
+      }
+    }
+  }
+  if (nwin) {
+    __syncwarp();
+    unsigned base = 0;
+    if (lane == 0) base = (unsigned)(atomicAdd(&out->packed, (unsigned long long)nwin << 33) >> 33);
+    base = __shfl_sync(kFull, base, 0) + out_base;
+    for (unsigned i = lane; i < nwin; i += 32) st_stream(p.P + base + i, wst[i], pol);
+  }
+  flush_count(sm, kStTrav, c_trav);
+  flush_count(sm, kStNvis, c_nvis);
+  flush_count(sm, kStRowsPulled, c_rows);
+}
+
 // ---------------------------------------------------------------------------
 // One BFS level (GPUBFS, Alg. 2, gpu_match.cpp:42-70; GPUBFS-WR, Alg. 4,
 // gpu_match.cpp:99-133) over the frontier F[ls, ls+n) holding T edges.
@@ -950,8 +1141,14 @@ __device__ __forceinline__ void expand_level(const Params& p, Smem& sm, int4* F,
         for (int k = 0; k < kItems; ++k) {
           const int c = cm[k];  // mate of the row; kVisBit set = its column was claimed this phase
           old[k] = kVisBit;
-          if (c >= 0 && !(c & kVisBit) && (!WR || p.claim_mode == 0 || !root_dead(p, sm.root[sl[k]])))
+          if (c >= 0 && !(c & kVisBit) && (!WR || p.claim_mode == 0 || !root_dead(p, sm.root[sl[k]]))) {
+#ifdef BM_CLAIM_STORE
+            st_plain(RM(p, row[k]), c | kVisBit);  // racy claim: a rare duplicate discoverer pushes the column twice
+            old[k] = c;
+#else
             old[k] = atomicOr(RM(p, row[k]), kVisBit);
+#endif
+          }
         }
 #pragma unroll
         for (int k = 0; k < kItems; ++k) {
@@ -1255,7 +1452,11 @@ __device__ PhaseOut run_phase(const Params& p, Smem& sm, int cur, int parity, bo
     if (bu) {
       bu_prep<WR>(p, sm, F, in_pairs, ls, n, lv);
       grid_sync(ctl);
+#ifdef BM_SWEEP_OLD
       bu_sweep<WR, IMP>(p, sm, ls + n, outs, lv, parity);
+#else
+      bu_sweep_q<WR, IMP>(p, sm, ls + n, outs, lv, parity);
+#endif
       if (threadIdx.x == 0) sm.cnt[kStPulledLevels] += is_leader() ? 1 : 0;
     } else {
       expand_level<WR, IMP, BU>(p, sm, F, ls, n, T, (lv & 1) ? p.gidx1 : p.gidx0, (lv & 1) ? p.gidx0 : p.gidx1,
@@ -1448,7 +1649,8 @@ __device__ PhaseOut run_phase(const Params& p, Smem& sm, int cur, int parity, bo
 // ---------------------------------------------------------------------------
 template <bool WR, bool IMP, bool BU>
 __global__ void __launch_bounds__(kThreads, BM_MINB) driver_kernel(Params p) {
-  __shared__ Smem sm;
+  extern __shared__ __align__(16) unsigned char smem_raw[];  // sizeof(Smem) > 48 KB: dynamic shared memory
+  Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
   Ctrl* ctl = p.ctl;
   if (threadIdx.x < kNumStats) sm.cnt[threadIdx.x] = 0;
   __syncthreads();
@@ -2127,7 +2329,7 @@ bm_status build_transpose(bm_handle* h, int nc, int nr, long long E) {
     h->nfbit_words = (nc + 31) / 32;
     BM_CUDA(dalloc(h->caps, h->fbit, (size_t)2 * h->nfbit_words));
     BM_CUDA(dalloc(h->caps, h->croot, (size_t)nc));
-    BM_CUDA(dalloc(h->caps, h->P, (size_t)nc));
+    BM_CUDA(dalloc(h->caps, h->P, (size_t)nc + kFSlack(nc)));
     // rows bucketed so that one bucket's slice of radj is at most 32 MB
     int shift = 0;
     {
@@ -2255,7 +2457,7 @@ bm_status launch(bm_handle* h, int v, Params& p, float* ms) {
   const int G = grid_for(h, v);
   void* args[] = {&p};
   BM_CUDA(cudaEventRecord(h->ev0, h->stream));
-  BM_CUDA(cudaLaunchCooperativeKernel(kernel_ptr(v), dim3(G), dim3(kThreads), args, 0, h->stream));
+  BM_CUDA(cudaLaunchCooperativeKernel(kernel_ptr(v), dim3(G), dim3(kThreads), args, sizeof(Smem), h->stream));
   BM_CUDA(cudaEventRecord(h->ev1, h->stream));
   BM_CUDA(cudaStreamSynchronize(h->stream));
   BM_CUDA(cudaEventElapsedTime(ms, h->ev0, h->ev1));
@@ -2528,7 +2730,9 @@ bm_status bm_create(int32_t device, bm_handle** out) {
   h->device = device;
   h->sms = prop.multiProcessorCount;
   for (int v = 0; v < 6; ++v) {
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&h->bps[v], kernel_ptr(v), kThreads, 0);
+    e = cudaFuncSetAttribute(kernel_ptr(v), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem));
+    if (e == cudaSuccess)
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&h->bps[v], kernel_ptr(v), kThreads, sizeof(Smem));
     if (e != cudaSuccess || h->bps[v] < 1) {
       delete h;
       return fail(BM_ERR_CUDA, std::string("occupancy query failed: ") + cudaGetErrorString(e));
@@ -2647,8 +2851,8 @@ bm_status bm_upload_csc(bm_handle* h, int32_t nc, int32_t nr, const int64_t* cxa
   BM_CUDA(dalloc(h->caps, h->gidx[1], ngran));
   h->log_cap = (unsigned)std::min<long long>((long long)nr + nc + 1024, 0xffffffffll);
   BM_CUDA(dalloc(h->caps, h->wlog, h->log_cap));
-  BM_CUDA(dalloc(h->caps, h->F[0], nc));
-  BM_CUDA(dalloc(h->caps, h->F[1], nc));
+  BM_CUDA(dalloc(h->caps, h->F[0], (size_t)nc + kFSlack(nc)));
+  BM_CUDA(dalloc(h->caps, h->F[1], (size_t)nc + kFSlack(nc)));
   // offsets: int64 staged in F[1] (16 B per column >= 8 B per offset), narrowed to u32
   long long* staged = reinterpret_cast<long long*>(h->F[1]);
   BM_CUDA(cudaMemcpyAsync(staged, cxadj, sizeof(long long) * ((size_t)nc + 1), cudaMemcpyHostToDevice, h->stream));

@@ -26,9 +26,10 @@ def line_map(cubin, fn):
             continue
         if not in_fn:
             continue
-        mm = re.search(r'//## File ".*?", line (\d+)', ln)
+        mm = re.search(r'//## File "(.*?)", line (\d+)', ln)
         if mm:
-            cur_line = int(mm.group(1))
+            f = mm.group(1).rsplit("/", 1)[-1]
+            cur_line = int(mm.group(2)) if f == "bm_engine.cu" else (f, int(mm.group(2)))
             continue
         mi = re.match(r"\s*/\*([0-9a-f]{4,})\*/", ln)
         if mi and cur_line is not None:
@@ -60,17 +61,18 @@ def main():
         for k in stalls:
             a[k] += float(r[idx[k]] or 0)
     src = {}
-    try:
-        for i, t in enumerate(open("paper_1303_1379_b200/csrc/bm_engine.cu").read().splitlines(), 1):
-            src[i] = t.strip()
-    except OSError:
-        pass
+    for fname in ("bm_engine.cu", "bm_device.cuh"):
+        try:
+            for i, t in enumerate(open("paper_1303_1379_b200/csrc/" + fname).read().splitlines(), 1):
+                src[i if fname == "bm_engine.cu" else (fname, i)] = t.strip()
+        except OSError:
+            pass
     tot_i = sum(a["inst"] for a in agg.values())
     tot_s = sum(a["samples"] for a in agg.values())
     print(f"total warp-inst {tot_i:.3e}  samples {tot_s:.0f}")
     for line, a in sorted(agg.items(), key=lambda kv: -kv[1]["samples"])[:top]:
         st = max(stalls, key=lambda k: a[k]) if stalls else ""
-        print(f"{line:5d} inst {100 * a['inst'] / tot_i:5.1f}%  samp {100 * a['samples'] / tot_s:5.1f}%  "
+        print(f"{str(line):>22s} inst {100 * a['inst'] / tot_i:5.1f}%  samp {100 * a['samples'] / tot_s:5.1f}%  "
               f"{st[6:]:14s} {src.get(line, '')[:80]}")
 
 

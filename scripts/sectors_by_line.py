@@ -23,7 +23,8 @@ for r in data:
     a["req"] += f(r[idx["L1 Tag Requests Global"]])
     a["op"] = r[idx["Access Operation"]] or a.get("op", "")
 src = {i: t.strip() for i, t in enumerate(open("paper_1303_1379_b200/csrc/bm_engine.cu").read().splitlines(), 1)}
+src.update({("bm_device.cuh", i): t.strip() for i, t in enumerate(open("paper_1303_1379_b200/csrc/bm_device.cuh").read().splitlines(), 1)})
 tot = sum(a["sect"] for a in agg.values())
 print(f"total L2 theoretical global sectors {tot:.3e}")
 for line, a in sorted(agg.items(), key=lambda kv: -kv[1]["sect"])[:top]:
-    print(f"{line:5d} {100*a['sect']/tot:5.1f}%  sect {a['sect']:.3e} ideal {a['ideal']:.3e} req {a['req']:.3e}  {src.get(line,'')[:90]}")
+    print(f"{str(line):>22s} {100*a['sect']/tot:5.1f}%  sect {a['sect']:.3e} ideal {a['ideal']:.3e} req {a['req']:.3e}  {src.get(line,'')[:90]}")
