@@ -42,7 +42,7 @@ all: $(LIB) $(ORACLE) $(GENORACLE)
 $(BUILD):
 	mkdir -p $(BUILD)
 
-$(BUILD)/bm_engine.o: $(CSRC)/bm_engine.cu $(CSRC)/bm_device.cuh include/bmatch_b200.h | $(BUILD)
+$(BUILD)/bm_engine.o: $(CSRC)/bm_engine.cu $(CSRC)/bm_kernels.cuh $(CSRC)/bm_device.cuh include/bmatch_b200.h | $(BUILD)
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(BUILD)/ptxas.log || (cat $(BUILD)/ptxas.log; false)
 
 $(BUILD)/bm_partition.o: $(CSRC)/bm_partition.cu $(CSRC)/bm_device.cuh include/bmatch_b200.h | $(BUILD)

@@ -1,0 +1,2211 @@
+// bm_kernels.cuh — the device side of the engine: the persistent driver kernel
+// and its stages, plus the upload / verify / row-index kernels.
+//
+// Included twice, inside a namespace, with no includes of its own:
+//   * bm_engine.cu:  namespace bm   — the single-GPU engine (BM_MG undefined);
+//   * bm_mg.cu:      namespace bmg  — the multi-GPU engine (BM_MG = 1): the same
+//     stages, with the row state, cmatch, root marks and frontier roots of other
+//     ranks reached through peer pointers (see the BM_MG blocks).
+// The includer provides <cooperative_groups.h> (as cg), CUB, bm_device.cuh and
+// bmatch_b200.h.
+
+#ifndef BM_THREADS
+#define BM_THREADS 256
+#endif
+constexpr int kThreads = BM_THREADS;  // threads per CTA (1024 / kThreads CTAs per SM at <= 64 registers)
+#ifndef BM_ITEMS
+#define BM_ITEMS 4
+#endif
+#ifndef BM_MINB
+#define BM_MINB (768 / BM_THREADS)  // 80 registers: fewer spills than 4 CTAs at 64 (A/B: -3..-11 % per phase on C2-C5)
+#endif
+constexpr int kItems = BM_ITEMS;      // edges per thread per round (memory-level parallelism)
+#ifndef BM_EPT
+#define BM_EPT 1
+#endif
+constexpr int kEPT = BM_EPT;          // frontier entries per thread in a push window
+constexpr int kWin = kThreads * kEPT; // entries per push window
+#ifndef BM_GRAN
+#define BM_GRAN 512
+#endif
+constexpr unsigned kGran = BM_GRAN;   // edges per granule-index entry; tiles are whole granules
+#ifndef BM_TILE_GRAN
+#define BM_TILE_GRAN 8
+#endif
+constexpr unsigned kMaxTileGran = BM_TILE_GRAN;  // <= 4096 edges per tile (= the winner buffer)
+constexpr unsigned kWBuf = kGran * kMaxTileGran;
+#ifndef BM_INTERLEAVE_MB
+#define BM_INTERLEAVE_MB 72  // interleave {mate, pred} when the plain rmatch exceeds this many MB
+#endif
+#ifndef BM_SOLO_EDGES
+#define BM_SOLO_EDGES 1024
+#endif
+constexpr unsigned kSoloEdges = BM_SOLO_EDGES;  // widest level block 0 expands alone
+// Frontier capacity per phase beyond nc: room for the duplicate entries that
+// store claims can create (see expand_level). A level claims by store only when
+// even one entry per frontier edge would fit, so the capacity can never overflow.
+constexpr size_t kFSlack(long long nc) { return (size_t)(nc / 4 + 4096); }
+constexpr int kStartLevel = 2;        // L0 (gpu_match.cpp:275)
+constexpr int kUnvisited = kStartLevel - 1;
+constexpr int kFoundMark = kStartLevel - 2;
+constexpr unsigned long long kEdgeMask = (1ull << 33) - 1;
+// "Column visited this phase" lives in bit 30 of its mate's rmatch entry: the
+// gather rmatch[row] that finds a row's column also says whether that column
+// was claimed, so a traversed edge costs one random access, not two. Needs
+// nc < 2^30; cleared by sweep_visited() when the BFS ends.
+constexpr int kVisBit = 1 << 30;
+
+enum CtlError : int {
+  kErrNone = 0,
+  kErrBound = 1,        // more than nc + 1 phases (gpu_match.cpp:317-320)
+  kErrInvalidInit = 2,  // initial matching is not a clean valid matching
+  kErrBarrier = 3,      // grid barrier watchdog fired
+  kErrWalk = 4,         // an ALTERNATE walk exceeded nc steps (cannot happen on valid state)
+  kErrLevels = 5,       // more BFS levels than columns (cannot happen)
+  kErrWindow = 6,       // a push window's live edges exceed its tile (inconsistent frontier entries)
+  kErrCheck = 7,        // BM_CHECK=1 self-check of a level's entries failed (dbg holds the details)
+};
+
+struct alignas(128) Slot {
+  unsigned long long packed;  // (entries << 33) | edges, pushed by the previous level
+  unsigned tile;              // dynamic edge-tile counter while this level is expanded
+  unsigned pad[29];
+};
+
+struct PhaseRec {
+  long long launches;
+  long long before;
+  long long after;
+  int found;
+  int retry;
+};
+
+enum Stat : int {
+  kStTrav = 0,
+  kStCexp,
+  kStNvis,
+  kStEntries,
+  kStWalks,
+  kStSteps,
+  kStResets,
+  kStLevels,
+  kStRetries,
+  kStDenseFix,
+  kStCycTile,     // CTA cycles (thread 0's view) per part of expand_level and in grid barriers
+  kStCycWindow,
+  kStCycRounds,
+  kStCycFlush,
+  kStCycBarrier,
+  kStCycOther,
+  kStRowsPulled,  // rows a pulled level screened in as candidates (scanned their own columns)
+  kStPulledLevels,
+  kStMaterialized,  // frontier entries turned from (col, root) pairs into edge-tiled entries
+  kNumStats
+};
+
+constexpr int kBarSub = 16;  // grid barrier fan-in groups
+
+struct alignas(128) Ctrl {
+  unsigned bar_count;
+  unsigned bar_gen;
+  unsigned pad0[30];
+  unsigned bar_sub[kBarSub][32];  // one 128-byte line per group counter
+  Slot lvl[3];
+  Slot roots;
+  Slot mat[2];  // materialize reservations, by level parity (never the level's own slot: slow CTAs
+                // may still be reading its count when the next level starts)
+  unsigned n_ep;
+  unsigned pad1[31];
+  unsigned n_log;
+  unsigned log_overflow;
+  unsigned n_tl;
+  unsigned pad1b[29];
+  unsigned path_found[2];
+  unsigned pad2[30];
+  // hand-over from a solo run of narrow levels (block 0 alone) to the grid
+  int solo_lv;
+  int solo_stop;
+  unsigned solo_ls;
+  unsigned solo_n;
+  unsigned solo_T;
+  int solo_found;
+  long long solo_launches;
+  unsigned pad2b[24];
+  unsigned long long invalid;
+  unsigned long long isolated;
+  unsigned long long pad3[14];
+  unsigned long long stats[kNumStats];
+  // run state carried between launches (written by block 0 / thread 0 on exit)
+  long long outer;
+  long long card;
+  long long isolated_cols;
+  long long init_card;
+  long long bfs_levels_last;
+  int cur;
+  int done;
+  int error;
+  int n_recs;
+  int path_found_last;
+  int phase_parity;
+  long long dbg[8];  // details of the first kErrWindow (ls, n, T, i, e, wend, live, level)
+};
+
+#ifndef BM_MG
+#define BM_MG 0
+#endif
+constexpr int kMaxRanks = 8;
+
+#if BM_MG
+// One rank's state as every rank addresses it (multi-GPU engine, bm_mg.cu).
+// Bases are pre-offset so that they take GLOBAL ids: row r of the owner's row
+// range is rm + rs * r, column c of its column range is cmatch + c, etc. Peers
+// are reached through CUDA IPC mappings (NVLink), or are other allocations on
+// the same device when several ranks share one GPU.
+struct PeerPtrs {
+  int* rm;          // row state {mate, pred} (interleaved) or mates (plain)
+  int* pred;
+  int* cmatch;
+  int* bfs;         // root marks
+  int* croot;       // root of each frontier column (pulled levels)
+  unsigned* dead;   // the rank's replica of the dead-root bitmap (all nc bits)
+  unsigned* fbit;   // the rank's replicas of the two frontier bitmaps (2 x all nc bits)
+  int2* P;          // pair inbox: (column, root) winners routed to the column's owner
+  int* EP;          // endpoint rows found by the rank
+  int4* F0;
+  int4* F1;
+  struct Ctrl* ctl;
+};
+// Cross-rank barrier and the flags every rank reads (rank 0's memory).
+struct alignas(128) MgTeam {
+  unsigned count;
+  unsigned gen;
+  unsigned pad0[30];
+  unsigned path_found[2];
+  unsigned pad1[30];
+};
+#endif
+
+struct Params {
+  int nc, nr;
+  const unsigned* offs;  // nc + 1
+  const int* adj;        // E
+  int* rm;          // row state: mates at rm[rs * r]
+  int rs;           // row stride: 2 = interleaved {mate, pred}, 1 = plain (pred in `pred`)
+  int* cmatch;
+  int* pred;
+  int* bfs;
+  unsigned* dead;   // WR: 1 bit per column, set when the tree rooted there holds an endpoint
+  int ndead_words;
+  int4* F0;
+  int4* F1;
+  unsigned* gidx0;  // granule index, ping-pong by level parity
+  unsigned* gidx1;
+  int* EP;
+  int2* wlog;       // ALTERNATE write log: (row, col) per step, (row, -1) for a dangling row
+  unsigned log_cap;
+  Ctrl* ctl;
+  PhaseRec* recs;
+  int rec_cap;
+  int apsb;
+  int init_mode;
+  int fresh;
+  int init_checked;  // the given initial matching was validated when it was loaded (bm_load_matching)
+  int sorted;        // every column's rows ascend (binary-searchable adjacency)
+  int dbg_skip_alt_phase;  // fault injection (bm_debug_set): this phase's raced ALTERNATE does nothing
+  int check;               // BM_CHECK=1: verify every pushed level's entries before expanding it (debugging)
+  int max_phases;
+  int stop_after_bfs;
+  int trace;        // write bfs_array level labels (parity probes)
+  int claim_mode;   // WR claim check at discovery: 0 none (reference), 1 coherent root-mark check
+  int ep_one;       // WR endpoint policy: 1 = one free row per tree (root-mark CAS), 0 = every row (reference)
+  unsigned solo_edges;  // levels with at most this many frontier edges run on block 0 alone (0 = never)
+  // bottom-up levels (see bu_sweep); roffs == nullptr disables them
+  const unsigned* roffs;   // nr + 1, transposed adjacency (rows -> columns)
+  const int* radj;
+  unsigned* fbit[2];       // frontier bitmaps (nc bits each), alternating by level
+  int* croot;              // root of each frontier column (bottom-up levels)
+  int nfbit_words;
+  unsigned long long bu_min_edges;  // bu_rule 0: a level with at least this many frontier edges goes bottom-up
+  int bu_rule;             // 0: bu_min_edges threshold; 1: frontier edges vs unexplored edges (below)
+  float bu_alpha;          // bu_rule 1: pull when alpha * frontier edges >= edges of the unvisited rows ...
+  unsigned bu_min_n;       // ... and the frontier holds at least this many columns
+  double deg_col;          // E / nc: frontier edges of a level held as pairs are estimated from its size
+  double deg_row;          // E / nr
+  // Lazy frontier (pulled-capable kernels only): a wide level pushes its winners
+  // as (col, root) pairs; the next level either pulls straight from them or,
+  // when it is pushed, first turns them into edge-tiled entries (materialize).
+  // Winners of a pulled level never need their offsets gathered.
+  int2* P;                 // pairs, indexed like F (level entries [ls, ls + n))
+  unsigned long long pairs_min_edges;  // a pushed level this wide emits pairs
+  long long phase_bound;
+  unsigned long long fcap;  // frontier entries a phase may append (F0/F1 and P hold nc + kFSlack)
+  int claim_store;          // pushed levels may claim by plain store (BM_CLAIM_STORE=0 disables)
+  unsigned long long* tl;  // stage timeline: (tag, %globaltimer ns) pairs written by the leader
+  unsigned tl_cap;
+#if BM_MG
+  int world, rank;
+  int col_lo, col_hi, row_lo, row_hi;  // this rank's columns and rows
+  int cb[kMaxRanks - 1];               // column ownership: owner(c) = #{i : c >= cb[i]} (cb[i] = INT_MAX past world - 1)
+  int rb[kMaxRanks - 1];               // row ownership, likewise
+  int world_solo;                      // world == 1: narrow levels may still run on block 0 alone
+  MgTeam* team;
+  PeerPtrs peer[kMaxRanks];
+#endif
+};
+
+enum TlTag : unsigned {
+  kTlStart = 0, kTlInit = 1, kTlSetup = 2, kTlLevel = 3, kTlAlt = 4, kTlFixRows = 5, kTlFixCols = 6,
+  kTlRoots = 7, kTlEnd = 8, kTlLevelEdges = 9
+};
+
+__device__ __forceinline__ void tl_mark(const Params& p, unsigned kind, unsigned arg) {
+  if (blockIdx.x == 0 && threadIdx.x == 0 && p.tl) {
+    const unsigned n = p.ctl->n_tl;
+    if (n < p.tl_cap) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      p.tl[2 * n] = ((unsigned long long)kind << 32) | arg;
+      p.tl[2 * n + 1] = t;
+    }
+    p.ctl->n_tl = n + 1;
+  }
+}
+
+// A pulled-level candidate row: its row-state value and its column range in the row index.
+struct BuCand {
+  int row;
+  int val;
+  unsigned j0;
+  unsigned j1;
+};
+constexpr int kCandCap = 160;  // per-warp queue: < 32 left over + one screened chunk of 128 rows
+
+struct Smem {
+  union {  // a top-down window, or a bottom-up candidate stage (never both at once)
+    struct {
+      unsigned pre[kWin + 1];      // window: raw edge prefix of each entry, then the live-edge prefix
+      int col[kWin];
+      int root[kWin];
+      unsigned beg[kWin];          // first live adjacency index of each entry in this window
+    };
+    struct {
+      int bcand[4 * kThreads];     // bottom-up: candidate rows of a sweep step (per warp) ...
+      int bcandv[4 * kThreads];    // ... and their rmatch values
+    };
+  };
+  unsigned wtot[kThreads / 32];
+  unsigned short cgr[kWBuf / 32 + 2];  // entry holding live edge 32*q (coarse index for the search)
+  unsigned tile;
+  unsigned long long cnt[kNumStats];  // per-CTA work counters, flushed to Ctrl at exit
+  unsigned long long wsum[kThreads / 32];  // CTA-aggregated pushes: per-warp totals
+  unsigned wep[kThreads / 32];
+  unsigned long long blk_base;
+  unsigned blk_ep;
+  unsigned nw;                          // winners staged in wbuf for the current window
+  int2 wbuf[kWBuf];                     // (column, root) claimed in the current window
+};
+
+// Warp-reduce a per-thread count and add it to the CTA's shared counter. Must
+// be called by every lane of the warp.
+__device__ __forceinline__ void flush_count(Smem& sm, int idx, unsigned v) {
+  v = warp_sum(v);
+  if (lane_id() == 0 && v) atomicAdd(&sm.cnt[idx], (unsigned long long)v);
+}
+
+// ---------------------------------------------------------------------------
+// Grid barrier. All CTAs are co-resident (cooperative launch). Thread 0 of
+// each CTA arrives with one atomic; the last arriver resets the count and
+// bumps the generation. __threadfence() on both sides orders every write of
+// the stage before every read of the next (and invalidates this SM's L1).
+//
+// Multi-GPU (BM_MG): the barrier spans the team. The last CTA of each rank to
+// arrive does the cross-rank arrival on rank 0's team block (system-scope
+// atomics, NVLink) and releases its own grid only when every rank has arrived;
+// system-scope fences make each CTA's stores to peer memory visible first.
+#if BM_MG
+#define BM_FENCE() __threadfence_system()
+#else
+#define BM_FENCE() __threadfence()
+#endif
+__device__ __forceinline__ unsigned ld_acq_sys(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.sys.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __noinline__ void grid_sync(const Params& p) {
+  Ctrl* ctl = p.ctl;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    // Two-level arrival: CTAs count in kBarSub group counters (separate L2
+    // lines, so their atomics proceed in parallel); each group's last arriver
+    // counts at the top; the last of those resets and releases everyone.
+    const unsigned gen = ld_acq(&ctl->bar_gen);
+    BM_FENCE();
+    const unsigned G = gridDim.x;
+    const unsigned grp = blockIdx.x % kBarSub;
+    const unsigned ngrp = G < (unsigned)kBarSub ? G : (unsigned)kBarSub;
+    const unsigned in_grp = G / kBarSub + (grp < G % kBarSub ? 1u : 0u);
+    bool last = false;
+    if (atomicAdd(&ctl->bar_sub[grp][0], 1u) == in_grp - 1) {
+      st_rlx(&ctl->bar_sub[grp][0], 0u);
+      __threadfence();  // the reset is visible before this group can be released
+      last = atomicAdd(&ctl->bar_count, 1u) == ngrp - 1;
+    }
+    if (last) {
+      st_rlx(&ctl->bar_count, 0u);
+#if BM_MG
+      if (p.world > 1) {  // every rank's grid has arrived before any is released
+        MgTeam* t = p.team;
+        const unsigned tgen = ld_acq_sys(&t->gen);
+        __threadfence_system();
+        if (atomicAdd_system(&t->count, 1u) == (unsigned)p.world - 1) {
+          atomicExch_system(&t->count, 0u);
+          __threadfence_system();
+          atomicAdd_system(&t->gen, 1u);
+        } else {
+          const long long t0 = clock64();
+          unsigned spins = 0;
+          while (ld_acq_sys(&t->gen) == tgen) {
+            __nanosleep(64);
+            if (((++spins) & 0xfffu) == 0 && clock64() - t0 > (1ll << 37)) {
+              ctl->error = kErrBarrier;
+              __threadfence_system();
+              __trap();
+            }
+          }
+        }
+      }
+#endif
+      BM_FENCE();
+      atomicAdd(&ctl->bar_gen, 1u);
+    } else {
+      const long long t0 = clock64();
+      unsigned spins = 0;
+      while (ld_acq(&ctl->bar_gen) == gen) {
+        __nanosleep(32);
+        if (((++spins) & 0xfffu) == 0 && clock64() - t0 > (1ll << 37)) {  // ~70 s watchdog
+          ctl->error = kErrBarrier;
+          __threadfence_system();
+          __trap();
+        }
+      }
+    }
+    BM_FENCE();
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ bool is_leader() { return blockIdx.x == 0 && threadIdx.x == 0; }
+
+__device__ __forceinline__ long long clk() { return clock64(); }
+
+__device__ __forceinline__ unsigned long long global_thread() {
+  return (unsigned long long)blockIdx.x * kThreads + threadIdx.x;
+}
+__device__ __forceinline__ unsigned long long global_threads() {
+  return (unsigned long long)gridDim.x * kThreads;
+}
+
+__device__ __forceinline__ unsigned long long warp_incl_scan64(unsigned long long v) {
+  const unsigned lane = lane_id();
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long t = __shfl_up_sync(kFull, v, o);
+    if (lane >= (unsigned)o) v += t;
+  }
+  return v;
+}
+
+// CTA-wide reservation of frontier slots/edge prefix and endpoint slots: one
+// atomic per CTA instead of one per warp (every warp of the GPU pushes into
+// the same two counters, so per-warp atomics serialise in L2). `cnt`/`deg`
+// are this thread's winners and their total degree, `epc` its endpoints.
+// Returns this thread's first packed (slot << 33 | prefix) and endpoint slot.
+// Must be called by every thread of the CTA; returns false (no work) for all
+// threads when the CTA pushes nothing.
+__device__ __forceinline__ bool cta_reserve(Smem& sm, unsigned cnt, unsigned deg, unsigned epc, Slot* out,
+                                            unsigned* n_ep, unsigned long long& tbase, unsigned& tep) {
+  const unsigned long long v = ((unsigned long long)cnt << 33) | deg;
+  const unsigned long long incl = warp_incl_scan64(v);
+  const unsigned ep_incl = warp_incl_scan(epc);
+  const unsigned warp = threadIdx.x >> 5;
+  if (lane_id() == 31) {
+    sm.wsum[warp] = incl;
+    sm.wep[warp] = ep_incl;
+  }
+  if (!__syncthreads_or((cnt | epc) != 0u)) return false;
+  if (threadIdx.x == 0) {
+    unsigned long long run = 0;
+    unsigned er = 0;
+#pragma unroll
+    for (int w = 0; w < kThreads / 32; ++w) {
+      const unsigned long long t = sm.wsum[w];
+      sm.wsum[w] = run;
+      run += t;
+      const unsigned te = sm.wep[w];
+      sm.wep[w] = er;
+      er += te;
+    }
+    sm.blk_base = run ? atomicAdd(&out->packed, run) : 0ull;
+    sm.blk_ep = er ? atomicAdd(n_ep, er) : 0u;
+  }
+  __syncthreads();
+  tbase = sm.blk_base + sm.wsum[warp] + (incl - v);
+  tep = sm.blk_ep + sm.wep[warp] + (ep_incl - epc);
+  return true;
+}
+
+// Whether row r is in column c's adjacency [b, e) (binary search over a sorted
+// CSC, else a scan): a matched pair of an initial matching must be an edge
+// (validate, matching.cpp:70-104).
+__device__ __forceinline__ bool has_edge(const int* adj, unsigned b, unsigned e, int r, bool sorted) {
+  if (sorted) {
+    while (b < e) {
+      const unsigned mid = b + ((e - b) >> 1);
+      const int v = ld_ro(adj + mid);
+      if (v == r) return true;
+      if (v < r) b = mid + 1; else e = mid;
+    }
+    return false;
+  }
+  for (unsigned j = b; j < e; ++j)
+    if (ld_ro(adj + j) == r) return true;
+  return false;
+}
+
+// Writes one reserved frontier entry and its granule-index records.
+__device__ __forceinline__ void put_entry(int4* F, unsigned out_base, unsigned* gidx, unsigned long long slot,
+                                          int col, int root, unsigned beg, unsigned deg,
+                                          unsigned long long pol = 0) {
+  const unsigned local = (unsigned)(slot >> 33);
+  const unsigned pre = (unsigned)(slot & kEdgeMask);
+  if (pol) st_stream(F + out_base + local, make_int4(col, root, (int)beg, (int)pre), pol);
+  else st_plain(F + out_base + local, make_int4(col, root, (int)beg, (int)pre));
+  if (deg == 0) return;  // holds no edge: no granule starts inside it
+  const unsigned m1 = (pre + deg - 1) / kGran;
+  for (unsigned m = (pre + kGran - 1) / kGran; m <= m1; ++m) st_plain(reinterpret_cast<int*>(gidx) + m, (int)local);
+}
+
+// Row state layout (chosen per graph at upload). Interleaved: a row's mate (rmatch) and
+// its BFS predecessor share one 8-byte slot: the claim is an atomicOr on the
+// mate word and the predecessor store that follows it lands in the same L2
+// sector, which the atomic has just brought in and dirtied, instead of a
+// second random sector (with a DRAM read-for-fill of a partial write).
+// That wins once rmatch is far larger than L2 (C4, C5); while rmatch fits in
+// L2 the plain layout keeps the gathered array half as large (C2, C3).
+#if BM_MG
+__device__ __forceinline__ int owner_col(const Params& p, long long c) {
+  int q = 0;
+#pragma unroll
+  for (int i = 0; i < kMaxRanks - 1; ++i) q += c >= p.cb[i] ? 1 : 0;
+  return q;
+}
+__device__ __forceinline__ int owner_row(const Params& p, long long r) {
+  int q = 0;
+#pragma unroll
+  for (int i = 0; i < kMaxRanks - 1; ++i) q += r >= p.rb[i] ? 1 : 0;
+  return q;
+}
+// any row / column, wherever it lives
+__device__ __forceinline__ int* RM(const Params& p, long long r) { return p.peer[owner_row(p, r)].rm + p.rs * r; }
+__device__ __forceinline__ int* PR(const Params& p, long long r) { return p.peer[owner_row(p, r)].pred + p.rs * r; }
+__device__ __forceinline__ int* CM(const Params& p, long long c) { return p.peer[owner_col(p, c)].cmatch + c; }
+__device__ __forceinline__ int* BF(const Params& p, long long c) { return p.peer[owner_col(p, c)].bfs + c; }
+__device__ __forceinline__ int* CR(const Params& p, long long c) { return p.peer[owner_col(p, c)].croot + c; }
+#else
+__device__ __forceinline__ int* RM(const Params& p, long long r) { return p.rm + p.rs * r; }
+__device__ __forceinline__ int* PR(const Params& p, long long r) { return p.pred + p.rs * r; }
+__device__ __forceinline__ int* CM(const Params& p, long long c) { return p.cmatch + c; }
+__device__ __forceinline__ int* BF(const Params& p, long long c) { return p.bfs + c; }
+__device__ __forceinline__ int* CR(const Params& p, long long c) { return p.croot + c; }
+#endif
+// this rank's own rows / columns (the whole graph on one GPU): no ownership lookup
+__device__ __forceinline__ int* RML(const Params& p, long long r) { return p.rm + p.rs * r; }
+__device__ __forceinline__ int* PRL(const Params& p, long long r) { return p.pred + p.rs * r; }
+
+// State atomics: system scope when the location may live on another GPU.
+#if BM_MG
+__device__ __forceinline__ int at_or(int* a, int v) { return atomicOr_system(a, v); }
+__device__ __forceinline__ unsigned at_or(unsigned* a, unsigned v) { return atomicOr_system(a, v); }
+__device__ __forceinline__ int at_cas(int* a, int c, int v) { return atomicCAS_system(a, c, v); }
+__device__ __forceinline__ unsigned at_cas(unsigned* a, unsigned c, unsigned v) { return atomicCAS_system(a, c, v); }
+__device__ __forceinline__ unsigned long long at_add(unsigned long long* a, unsigned long long v) {
+  return atomicAdd_system(a, v);
+}
+#else
+__device__ __forceinline__ int at_or(int* a, int v) { return atomicOr(a, v); }
+__device__ __forceinline__ unsigned at_or(unsigned* a, unsigned v) { return atomicOr(a, v); }
+__device__ __forceinline__ int at_cas(int* a, int c, int v) { return atomicCAS(a, c, v); }
+__device__ __forceinline__ unsigned at_cas(unsigned* a, unsigned c, unsigned v) { return atomicCAS(a, c, v); }
+__device__ __forceinline__ unsigned long long at_add(unsigned long long* a, unsigned long long v) {
+  return atomicAdd(a, v);
+}
+#endif
+
+// Offsets of a claimed column (read-only path).
+__device__ __forceinline__ unsigned ld_offs(const unsigned* a, unsigned long long) { return ld_ro(a); }
+
+// WR early-exit test (gpu_match.cpp:106-108) against the dead-root bitmap:
+// nc/8 bytes that stay in L2, instead of a bfs_array[root] gather per entry.
+// bfs_array[root] still carries the reference's mark (and the endpoint for
+// the improved walk); the bit only mirrors "marked".
+__device__ __forceinline__ bool root_dead(const Params& p, int root) {
+  return (ld_rlx(p.dead + (root >> 5)) >> (root & 31)) & 1u;
+}
+__device__ __forceinline__ void mark_dead(const Params& p, int root) {
+  atomicOr(p.dead + (root >> 5), 1u << (root & 31));
+}
+
+// Pushes the winners staged in sm.wbuf as next-level frontier entries: one
+// CTA reservation (slots + edge prefix) for all of them. CTA-uniform call.
+__device__ __forceinline__ void flush_winners(const Params& p, Smem& sm, int4* F, unsigned out_base, unsigned* gout,
+                                              Slot* out, unsigned long long pol) {
+  const unsigned tid = threadIdx.x;
+  const unsigned nw = sm.nw;
+  if (!nw) return;
+  unsigned long long slot;
+  unsigned unused;
+  if (nw <= (unsigned)kThreads) {  // one winner per thread: a single pass
+    const bool has = tid < nw;
+    int2 cr = make_int2(0, 0);
+    unsigned b0 = 0, d0 = 0;
+    if (has) {
+      cr = sm.wbuf[tid];
+      b0 = ld_offs(p.offs + cr.x, pol);
+      d0 = ld_offs(p.offs + cr.x + 1, pol) - b0;
+    }
+    cta_reserve(sm, has ? 1u : 0u, d0, 0u, out, &p.ctl->n_ep, slot, unused);
+    if (has) put_entry(F, out_base, gout, slot, cr.x, cr.y, b0, d0, pol);
+  } else {
+    unsigned cnt = 0, deg = 0;
+    for (unsigned j = tid; j < nw; j += kThreads) {
+      const int c = sm.wbuf[j].x;
+      deg += ld_offs(p.offs + c + 1, pol) - ld_offs(p.offs + c, pol);
+      cnt++;
+    }
+    cta_reserve(sm, cnt, deg, 0u, out, &p.ctl->n_ep, slot, unused);
+    for (unsigned j = tid; j < nw; j += kThreads) {
+      const int2 cr = sm.wbuf[j];
+      const unsigned b0 = ld_offs(p.offs + cr.x, pol);
+      const unsigned d0 = ld_offs(p.offs + cr.x + 1, pol) - b0;
+      put_entry(F, out_base, gout, slot, cr.x, cr.y, b0, d0, pol);
+      slot += (1ull << 33) + d0;
+    }
+  }
+  __syncthreads();
+  if (tid == 0) sm.nw = 0;  // callers barrier before staging again
+}
+
+// Stages one winner per thread (or none) in sm.wbuf: one shared atomic per warp.
+__device__ __forceinline__ void stage_winner(Smem& sm, bool win, int col, int root) {
+  const unsigned mine = win ? 1u : 0u;
+  const unsigned incl = warp_incl_scan(mine);
+  const unsigned tot = __shfl_sync(kFull, incl, 31);
+  unsigned wb = 0;
+  if (lane_id() == 31 && tot) wb = atomicAdd(&sm.nw, tot);
+  wb = __shfl_sync(kFull, wb, 31) + incl - mine;
+  if (win) sm.wbuf[wb] = make_int2(col, root);
+}
+
+// Pushes the winners staged in sm.wbuf as (col, root) pairs: one slot
+// reservation per CTA, coalesced stores, no offsets gathered. CTA-uniform call.
+__device__ __forceinline__ void flush_pairs(const Params& p, Smem& sm, unsigned out_base, Slot* out,
+                                            unsigned long long pol) {
+  const unsigned nw = sm.nw;
+  if (!nw) return;
+  if (threadIdx.x == 0) sm.blk_base = atomicAdd(&out->packed, (unsigned long long)nw << 33);
+  __syncthreads();
+  const unsigned base = out_base + (unsigned)(sm.blk_base >> 33);
+  for (unsigned j = threadIdx.x; j < nw; j += kThreads) st_stream(p.P + base + j, sm.wbuf[j], pol);
+  __syncthreads();
+  if (threadIdx.x == 0) sm.nw = 0;
+}
+
+// Turns the n pairs of a level, P[ls, ls + n), into edge-tiled frontier entries
+// F[ls, ls + n) plus their granule index, for a level that is pushed.
+// Reservations go to `in`, a zeroed slot, whose low bits end as the level's
+// edge total. Every CTA of the caller's set must call it (a grid barrier must
+// follow before the entries are read).
+constexpr int kMatItems = 4;
+__device__ __forceinline__ void materialize(const Params& p, Smem& sm, int4* F, unsigned ls, unsigned n,
+                                            unsigned* gin, Slot* in, unsigned long long pol, bool solo) {
+  const unsigned long long G = solo ? 1ull : gridDim.x;
+  const unsigned long long B0 = solo ? 0ull : blockIdx.x;
+  unsigned done = 0;
+  for (unsigned long long b = B0 * kThreads * kMatItems; b < n; b += G * kThreads * kMatItems) {
+    int2 pr[kMatItems];
+    unsigned beg[kMatItems], deg[kMatItems];
+    unsigned cnt = 0, sum = 0;
+#pragma unroll
+    for (int k = 0; k < kMatItems; ++k) {
+      const unsigned long long i = b + (unsigned long long)k * kThreads + threadIdx.x;
+      pr[k] = i < n ? ld_cg(p.P + ls + i) : make_int2(-1, 0);
+    }
+#pragma unroll
+    for (int k = 0; k < kMatItems; ++k) {
+      beg[k] = pr[k].x >= 0 ? ld_ro(p.offs + pr[k].x) : 0u;
+      deg[k] = pr[k].x >= 0 ? ld_ro(p.offs + pr[k].x + 1) : 0u;
+    }
+#pragma unroll
+    for (int k = 0; k < kMatItems; ++k) {
+      deg[k] -= beg[k];
+      if (pr[k].x >= 0) {
+        cnt++;
+        sum += deg[k];
+      }
+    }
+    unsigned long long slot;
+    unsigned unused;
+    if (cta_reserve(sm, cnt, sum, 0u, in, &p.ctl->n_ep, slot, unused)) {
+#pragma unroll
+      for (int k = 0; k < kMatItems; ++k)
+        if (pr[k].x >= 0) {
+          put_entry(F, ls, gin, slot, pr[k].x, pr[k].y, beg[k], deg[k], pol);
+          slot += (1ull << 33) + deg[k];
+        }
+    }
+    done += cnt;
+  }
+  flush_count(sm, kStMaterialized, done);
+}
+
+// ---------------------------------------------------------------------------
+// Direction-optimised (bottom-up) level for dense frontiers. The same level of
+// the same BFS as expand_level (gpubfs / gpubfs_wr, gpu_match.cpp:42-70,
+// 99-133), pulled instead of pushed: every unvisited matched row scans its own
+// columns (the transposed adjacency) for one in the frontier and is claimed by
+// the first it finds; every free row likewise becomes an endpoint of the first
+// live tree it touches. Any frontier neighbour is a valid discoverer (the
+// reference's races pick one arbitrarily too), so levels, roots and the
+// augmenting paths keep their meaning; a row stops at its first hit, which is
+// what saves the work when most columns are already in the frontier.
+//
+// bu_prep: the frontier of level lv as a bitmap (+ the root of each member).
+// The bitmap is clean: a bottom-up level clears its own right after the grid
+// barrier that ends it (bu_clear; the next level uses the other bitmap).
+__device__ __forceinline__ void bu_clear(const Params& p, int lv) {
+  unsigned* fb = p.fbit[lv & 1];
+  for (unsigned long long k = global_thread(); k < (unsigned long long)p.nfbit_words; k += global_threads())
+    st_plain(reinterpret_cast<int*>(fb) + k, 0);
+}
+// The frontier comes as (col, root) pairs (levels >= 1 of a pulled-capable
+// run) or as entries (level 0). Counts the live entries as columns expanded.
+template <bool WR>
+__device__ __forceinline__ void bu_prep(const Params& p, Smem& sm, const int4* F, bool pairs, unsigned ls,
+                                        unsigned n, int lv) {
+  unsigned* fb = p.fbit[lv & 1];
+  unsigned live = 0;
+  constexpr int K = 8;  // entries per thread in flight (the loop is latency-bound otherwise)
+  const unsigned long long GT = global_threads();
+  for (unsigned long long k0 = global_thread(); k0 < n; k0 += K * GT) {
+    int col[K], root[K];
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      const unsigned long long k = k0 + i * GT;
+      col[i] = -1;
+      root[i] = 0;
+      if (k < n) {
+        if (pairs) {
+          const int2 pr = ld_cg(p.P + ls + k);
+          col[i] = pr.x;
+          root[i] = pr.y;
+        } else {
+          const int4 ent = ld_cg(F + ls + k);
+          col[i] = ent.x;
+          root[i] = ent.y;
+        }
+      }
+    }
+    bool on[K];
+#pragma unroll
+    for (int i = 0; i < K; ++i) on[i] = col[i] >= 0 && !(WR && root_dead(p, root[i]));
+#pragma unroll
+    for (int i = 0; i < K; ++i)
+      if (on[i]) {
+        live++;
+        atomicOr(fb + (col[i] >> 5), 1u << (col[i] & 31));
+        st_plain(p.croot + col[i], WR ? root[i] : col[i]);
+      }
+  }
+  flush_count(sm, kStCexp, live);
+}
+
+template <bool WR, bool IMP>
+__device__ __forceinline__ void bu_sweep(const Params& p, Smem& sm, unsigned out_base, Slot* out, int lv, int pf) {
+  // Warp-synchronous: per CTA step every warp (1) screens kBuRows rows per lane
+  // with independent loads and compacts its candidates (unvisited matched rows
+  // and free rows) into a warp-private stage; (2) each candidate scans its
+  // columns until the first frontier member. Winners go to the CTA's wbuf and
+  // are flushed (3) between steps; that is the only CTA-wide synchronisation.
+  constexpr int kBuRows = 4;
+  constexpr int kWarpRows = 32 * kBuRows;              // rows a warp screens per step
+  constexpr int kStepRows = kThreads * kBuRows;        // rows a CTA screens per step
+#ifndef BM_BU_PROBE
+#define BM_BU_PROBE 4
+#endif
+  constexpr int kBuProbe = BM_BU_PROBE;
+  const unsigned* fb = p.fbit[lv & 1];
+  const unsigned long long pol = policy_evict_first();
+  unsigned* const path_flag = &p.ctl->path_found[pf];
+  unsigned c_trav = 0, c_nvis = 0, c_rows = 0;
+  const unsigned warp = threadIdx.x >> 5, lane = lane_id();
+  int* const wrow = sm.bcand + warp * kWarpRows;   // this warp's stage
+  int* const wval = sm.bcandv + warp * kWarpRows;
+  if (threadIdx.x == 0) sm.nw = 0;
+  __syncthreads();
+  unsigned step = 0;
+  for (unsigned long long b = (unsigned long long)blockIdx.x * kStepRows; b < (unsigned long long)p.nr;
+       b += (unsigned long long)gridDim.x * kStepRows) {
+    // (1) screen and compact (warp-private)
+    const unsigned long long wb = b + (unsigned long long)warp * kWarpRows;
+    int v[kBuRows];
+#pragma unroll
+    for (int k = 0; k < kBuRows; ++k) {
+      const unsigned long long r = wb + (unsigned long long)k * 32 + lane;
+      v[k] = r < (unsigned long long)p.nr ? ld_cg(RM(p, r)) : -3;
+    }
+    unsigned ncand = 0;
+#pragma unroll
+    for (int k = 0; k < kBuRows; ++k) {
+      const bool is_cand = (v[k] >= 0 && !(v[k] & kVisBit)) || v[k] == -1;
+      const unsigned m = __ballot_sync(kFull, is_cand);
+      if (is_cand) {
+        const unsigned slot = ncand + __popc(m & ((1u << lane) - 1));
+        wrow[slot] = (int)(wb + (unsigned long long)k * 32 + lane);
+        wval[slot] = v[k];
+      }
+      ncand += __popc(m);
+    }
+    __syncwarp();
+    // (2) resolve the warp's candidates, 32 at a time
+    for (unsigned t0 = 0; t0 < ncand; t0 += 32) {
+      bool win = false, ep = false;
+      int cw = 0, rootw = 0, rr = 0;
+      if (t0 + lane < ncand) {
+        rr = wrow[t0 + lane];
+        const int vv = wval[t0 + lane];
+        const unsigned j0 = ld_ro(p.roffs + rr), j1 = ld_ro(p.roffs + rr + 1);
+        c_rows++;
+        // kBuProbe neighbours per step: their index loads and frontier-bit loads
+        // are independent, so a row that scans far waits kBuProbe x fewer round trips
+        bool done = false;
+        for (unsigned jb = j0; jb < j1 && !done; jb += kBuProbe) {
+          int cs[kBuProbe];
+          unsigned wd[kBuProbe];
+#pragma unroll
+          for (int k = 0; k < kBuProbe; ++k) cs[k] = jb + k < j1 ? ld_stream(p.radj + jb + k, pol) : -1;
+#pragma unroll
+          for (int k = 0; k < kBuProbe; ++k)
+            wd[k] = cs[k] >= 0 ? ld_ca(reinterpret_cast<const int*>(fb) + (cs[k] >> 5)) : 0u;
+#pragma unroll
+          for (int k = 0; k < kBuProbe; ++k) {
+            const int c = cs[k];
+            if (done || c < 0) continue;
+            c_trav++;
+            if (!((wd[k] >> (c & 31)) & 1)) continue;
+            const int root = ld_cg(p.croot + c);
+            if (vv >= 0) {  // matched row: its column joins the frontier below c's tree
+              st_plain(RM(p, rr), vv | kVisBit);
+              st_plain(PR(p, rr), c);
+              win = true;
+              cw = vv;
+              rootw = root;
+              done = true;
+              continue;
+            }
+            // free row: an endpoint of c's tree
+            const bool one = WR && p.ep_one;
+            if (one && root_dead(p, root)) continue;
+            bool mine = true;
+            if (one) mine = atomicCAS(p.bfs + root, kStartLevel, IMP ? -rr : kFoundMark) == kStartLevel;
+            else if (WR) st_rlx(p.bfs + root, IMP ? -rr : kFoundMark);
+            if (!mine) continue;  // that tree already holds an endpoint: try another neighbour
+            if (WR) mark_dead(p, root);
+            st_rlx(RM(p, rr), -2);
+            st_plain(PR(p, rr), c);
+            ep = true;
+            if (ld_rlx(path_flag) == 0u) st_rlx(path_flag, 1u);
+            done = true;
+          }
+        }
+      }
+      c_nvis += win ? 1u : 0u;
+      stage_winner(sm, win, cw, rootw);  // one shared atomic per warp
+      {  // endpoints: rare, warp-aggregated global append
+        const unsigned mine = ep ? 1u : 0u;
+        const unsigned incl = warp_incl_scan(mine);
+        const unsigned tot = __shfl_sync(kFull, incl, 31);
+        if (tot) {
+          unsigned eb = 0;
+          if (lane == 31) eb = atomicAdd(&p.ctl->n_ep, tot);
+          eb = __shfl_sync(kFull, eb, 31) + incl - mine;
+          if (ep) st_plain(p.EP + eb, rr);
+        }
+      }
+    }
+    __syncwarp();  // the stage is reused by the next step
+    // (3) every kFlushSteps steps (at most kFlushSteps * kStepRows winners in between,
+    // which wbuf holds): flush when the next kFlushSteps steps might not fit
+#ifndef BM_BU_FLUSH_STEPS
+#define BM_BU_FLUSH_STEPS 4
+#endif
+    constexpr unsigned kFlushSteps = BM_BU_FLUSH_STEPS;
+    static_assert(kFlushSteps * kStepRows <= kWBuf, "wbuf must hold the winners between flush checks");
+    if (++step % kFlushSteps == 0) {
+      __syncthreads();
+      if (sm.nw > kWBuf - kFlushSteps * kStepRows) {
+        flush_pairs(p, sm, out_base, out, pol);
+        __syncthreads();  // the reset of sm.nw lands before the next stage_winner
+      }
+    }
+  }
+  __syncthreads();
+  flush_pairs(p, sm, out_base, out, pol);
+  flush_count(sm, kStTrav, c_trav);
+  flush_count(sm, kStNvis, c_nvis);
+  flush_count(sm, kStRowsPulled, c_rows);
+}
+
+// Warp-autonomous pulled level. Every warp owns chunks of 128 consecutive rows
+// (grid-stride over the warps of the grid) and keeps a queue of candidate rows
+// in shared memory: screening a chunk reads the rows' state and their row-index
+// offsets in one coalesced round and appends the candidates (unvisited matched
+// rows, free rows) with their column ranges. Lanes then probe independently:
+// a lane whose row is resolved (hit, or its columns exhausted) takes the next
+// queued candidate in the following round, so a warp never waits for its
+// slowest row, and no CTA-wide barrier is needed — winners are staged per warp
+// in its slice of wbuf and flushed with one reservation per warp.
+template <bool WR, bool IMP>
+__device__ __forceinline__ void bu_sweep_q(const Params& p, Smem& sm, unsigned out_base, Slot* out, int lv, int pf) {
+  constexpr int kWarps = kThreads / 32;
+  constexpr unsigned kChunk = 128;
+  constexpr unsigned kWStage = 128;  // winners staged per warp
+  // wbuf is free during a pulled level: it holds the warps' candidate queues, then their winner stages
+  static_assert(sizeof(BuCand) * kCandCap * kWarps + sizeof(int2) * kWStage * kWarps <= sizeof(int2) * kWBuf,
+                "candidate queues and winner stages must fit in wbuf");
+  constexpr int kBuProbe = BM_BU_PROBE;
+  const unsigned* fb = p.fbit[lv & 1];
+  const unsigned long long pol = policy_evict_first();
+  unsigned* const path_flag = &p.ctl->path_found[pf];
+  unsigned c_trav = 0, c_nvis = 0, c_rows = 0;
+  const unsigned warp = threadIdx.x >> 5, lane = lane_id();
+  BuCand* const q = reinterpret_cast<BuCand*>(sm.wbuf) + warp * kCandCap;
+  int2* const wst = reinterpret_cast<int2*>(reinterpret_cast<BuCand*>(sm.wbuf) + kWarps * kCandCap) + warp * kWStage;
+  const unsigned long long nchunks = ((unsigned long long)p.nr + kChunk - 1) / kChunk;
+  const unsigned long long W = (unsigned long long)gridDim.x * kWarps;
+  unsigned long long chunk = (unsigned long long)blockIdx.x * kWarps + warp;
+  unsigned qh = 0, qt = 0;  // queued candidates q[qh, qt) (warp-uniform)
+  unsigned nwin = 0;        // winners staged in wst (warp-uniform)
+  int rr = -1, vv = 0;      // this lane's current candidate
+  unsigned j = 0, j1 = 0;
+  for (;;) {
+    // refill: the idle lanes would drain the queue and rows remain
+    const unsigned idle = __ballot_sync(kFull, rr < 0);
+    while (qt - qh < (unsigned)__popc(idle) && chunk < nchunks) {  // (a chunk may hold no candidate)
+      // move the leftovers (< 32) to the front, then screen one chunk
+      const unsigned left = qt - qh;
+      BuCand keep;
+      if (lane < left) keep = q[qh + lane];
+      __syncwarp();
+      if (lane < left) q[lane] = keep;
+      qh = 0;
+      qt = left;
+      const unsigned long long r0 = chunk * kChunk;
+      chunk += W;
+      int v[4];
+      unsigned o[4], onext;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const unsigned long long r = r0 + (unsigned long long)k * 32 + lane;
+        v[k] = r < (unsigned long long)p.nr ? ld_cg(RM(p, r)) : -3;
+        o[k] = r <= (unsigned long long)p.nr ? ld_ro(p.roffs + r) : 0u;  // roffs[nr] ends the last row
+      }
+      {
+        const unsigned long long r = r0 + 4 * 32;
+        onext = (lane == 0 && r <= (unsigned long long)p.nr) ? ld_ro(p.roffs + r) : 0u;
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        // end of this row's columns = start of the next row's
+        unsigned e = __shfl_down_sync(kFull, o[k], 1);
+        const unsigned nxt0 = __shfl_sync(kFull, k < 3 ? o[(k + 1) & 3] : onext, 0);
+        if (lane == 31) e = nxt0;
+        const bool is_cand = (v[k] >= 0 && !(v[k] & kVisBit)) || v[k] == -1;
+        const unsigned m = __ballot_sync(kFull, is_cand && e > o[k]);
+        if (is_cand && e > o[k]) {
+          BuCand c;
+          c.row = (int)(r0 + (unsigned long long)k * 32 + lane);
+          c.val = v[k];
+          c.j0 = o[k];
+          c.j1 = e;
+          q[qt + __popc(m & ((1u << lane) - 1))] = c;
+        }
+        qt += __popc(m);
+      }
+      __syncwarp();
+    }
+    // idle lanes take queued candidates in lane order
+    {
+      const unsigned avail = qt - qh;
+      const unsigned rank = __popc(idle & ((1u << lane) - 1));
+      if (rr < 0 && rank < avail) {
+        const BuCand c = q[qh + rank];
+        rr = c.row;
+        vv = c.val;
+        j = c.j0;
+        j1 = c.j1;
+        c_rows++;
+      }
+      qh += min((unsigned)__popc(idle), avail);
+    }
+    if (!__any_sync(kFull, rr >= 0)) break;  // queue empty and every chunk screened
+    // one probe round
+    bool win = false, ep = false;
+    int cw = 0, rootw = 0;
+    const int myrow = rr;
+    if (rr >= 0) {
+      int cs[kBuProbe];
+      unsigned wd[kBuProbe];
+#pragma unroll
+      for (int k = 0; k < kBuProbe; ++k) cs[k] = j + k < j1 ? ld_stream(p.radj + j + k, pol) : -1;
+#pragma unroll
+      for (int k = 0; k < kBuProbe; ++k)
+        wd[k] = cs[k] >= 0 ? ld_ca(reinterpret_cast<const int*>(fb) + (cs[k] >> 5)) : 0u;
+      bool done = false;
+#pragma unroll
+      for (int k = 0; k < kBuProbe; ++k) {
+        const int c = cs[k];
+        if (done || c < 0) continue;
+        c_trav++;
+        if (!((wd[k] >> (c & 31)) & 1)) continue;
+        const int root = ld_cg(p.croot + c);
+        if (vv >= 0) {  // matched row: its column joins the frontier below c's tree
+          st_plain(RM(p, rr), vv | kVisBit);
+          st_plain(PR(p, rr), c);
+          win = true;
+          cw = vv;
+          rootw = root;
+          done = true;
+          continue;
+        }
+        // free row: an endpoint of c's tree
+        const bool one = WR && p.ep_one;
+        if (one && root_dead(p, root)) continue;
+        bool mine = true;
+        if (one) mine = atomicCAS(p.bfs + root, kStartLevel, IMP ? -rr : kFoundMark) == kStartLevel;
+        else if (WR) st_rlx(p.bfs + root, IMP ? -rr : kFoundMark);
+        if (!mine) continue;  // that tree already holds an endpoint: try another neighbour
+        if (WR) mark_dead(p, root);
+        st_rlx(RM(p, rr), -2);
+        st_plain(PR(p, rr), c);
+        ep = true;
+        if (ld_rlx(path_flag) == 0u) st_rlx(path_flag, 1u);
+        done = true;
+      }
+      j += kBuProbe;
+      if (done || j >= j1) rr = -1;
+    }
+    // stage winners in this warp's slice of wbuf; flush it when the next round might not fit
+    {
+      const unsigned m = __ballot_sync(kFull, win);
+      if (win) wst[nwin + __popc(m & ((1u << lane) - 1))] = make_int2(cw, rootw);
+      nwin += __popc(m);
+      c_nvis += win ? 1u : 0u;
+      if (nwin > kWStage - 32) {
+        __syncwarp();
+        unsigned base = 0;
+        if (lane == 0) base = (unsigned)(atomicAdd(&out->packed, (unsigned long long)nwin << 33) >> 33);
+        base = __shfl_sync(kFull, base, 0) + out_base;
+        for (unsigned i = lane; i < nwin; i += 32) st_stream(p.P + base + i, wst[i], pol);
+        __syncwarp();
+        nwin = 0;
+      }
+    }
+    {  // endpoints: rare, warp-aggregated global append
+      const unsigned m = __ballot_sync(kFull, ep);
+      if (m) {
+        unsigned eb = 0;
+        if (lane == 0) eb = atomicAdd(&p.ctl->n_ep, (unsigned)__popc(m));
+        eb = __shfl_sync(kFull, eb, 0) + __popc(m & ((1u << lane) - 1));
+        if (ep) st_plain(p.EP + eb, myrow);
+      }
+    }
+  }
+  if (nwin) {
+    __syncwarp();
+    unsigned base = 0;
+    if (lane == 0) base = (unsigned)(atomicAdd(&out->packed, (unsigned long long)nwin << 33) >> 33);
+    base = __shfl_sync(kFull, base, 0) + out_base;
+    for (unsigned i = lane; i < nwin; i += 32) st_stream(p.P + base + i, wst[i], pol);
+  }
+  flush_count(sm, kStTrav, c_trav);
+  flush_count(sm, kStNvis, c_nvis);
+  flush_count(sm, kStRowsPulled, c_rows);
+}
+
+// ---------------------------------------------------------------------------
+// One BFS level (GPUBFS, Alg. 2, gpu_match.cpp:42-70; GPUBFS-WR, Alg. 4,
+// gpu_match.cpp:99-133) over the frontier F[ls, ls+n) holding T edges.
+template <bool WR, bool IMP, bool BU>
+__device__ __forceinline__ void expand_level(const Params& p, Smem& sm, int4* F, unsigned ls, unsigned n, unsigned T,
+                             const unsigned* gin, unsigned* gout, Slot* in, Slot* out, int level, int pf,
+                             bool pairs_out, bool claim_store) {
+  if (T == 0) return;
+  const unsigned tid = threadIdx.x;
+  unsigned c_trav = 0, c_cexp = 0, c_nvis = 0, c_entries = 0;
+  const unsigned long long G = gridDim.x;
+  unsigned long long per = (T + 2 * G - 1) / (2 * G);
+  per = ((per + kGran - 1) / kGran) * kGran;
+  if (per > (unsigned long long)kGran * kMaxTileGran) per = (unsigned long long)kGran * kMaxTileGran;
+  const unsigned ET = (unsigned)per;
+  const unsigned ntiles = (unsigned)((T + (unsigned long long)ET - 1) / ET);
+  const unsigned out_base = ls + n;
+  unsigned* const path_flag = &p.ctl->path_found[pf];
+
+  const unsigned long long pol = policy_evict_first();
+#ifndef BM_PF
+#define BM_PF 2
+#endif
+#ifndef BM_KEEP
+#define BM_KEEP 1
+#endif
+  // BM_KEEP: 0 default priority for the gathered state; 1 rmatch evict_last;
+  // 2 rmatch + visited bitmap + offsets evict_last.
+  const unsigned long long keep = policy_evict_last();
+  if (tid == 0) sm.nw = 0;
+  long long t_a = clk();
+  for (;;) {
+    if (tid == 0) sm.tile = atomicAdd(&in->tile, 1u);
+    __syncthreads();
+    const unsigned tile = sm.tile;
+    __syncthreads();
+    if (tid == 0) {
+      const long long t = clk();
+      sm.cnt[kStCycTile] += t - t_a;
+      t_a = t;
+    }
+    if (tile >= ntiles) break;
+    const unsigned e0 = tile * ET;
+    const unsigned e1 = (T - e0 < ET) ? T : e0 + ET;
+    unsigned i = (unsigned)ld_cg(reinterpret_cast<const int*>(gin) + e0 / kGran);  // entry holding edge e0
+    unsigned e = e0;
+    while (e < e1) {
+      // Window of up to kWin entries starting at i (thread t holds entries t*kEPT ..).
+#pragma unroll
+      for (int k = 0; k < kEPT; ++k) {
+        const unsigned sl0 = tid * kEPT + k;
+        const unsigned wi = i + sl0;
+        if (wi < n) {
+          const int4 ent = ld_cg_stream(F + ls + wi, pol);
+          bool skip = false;
+          if (WR) skip = root_dead(p, ent.y);  // early exit (gpu_match.cpp:106-108)
+          sm.col[sl0] = ent.x;
+          sm.root[sl0] = skip ? -1 : ent.y;
+          sm.beg[sl0] = (unsigned)ent.z;
+          sm.pre[sl0] = (unsigned)ent.w;
+          if ((unsigned)ent.w >= e0 && (unsigned)ent.w < e1) {
+            c_entries++;
+            if (!skip) c_cexp++;
+          }
+        } else {
+          sm.pre[sl0] = T;
+          sm.root[sl0] = -1;
+        }
+      }
+      if (tid == 0) sm.pre[kWin] = (i + kWin < n) ? ld_cg_u(F + ls + i + kWin) : T;
+      __syncthreads();
+      const unsigned wend = min(e1, sm.pre[kWin]);
+      // Compact the window to its live edges: entries of trees that already
+      // found a path (WR) and edge ranges outside [e, wend) contribute none.
+      unsigned live;
+      {
+        unsigned len[kEPT], nb[kEPT], tsum = 0;
+#pragma unroll
+        for (int k = 0; k < kEPT; ++k) {
+          const unsigned sl0 = tid * kEPT + k;
+          const unsigned lo = max(sm.pre[sl0], e);
+          const unsigned hi = min(sm.pre[sl0 + 1], wend);
+          len[k] = (sm.root[sl0] >= 0 && hi > lo) ? hi - lo : 0u;
+          nb[k] = sm.beg[sl0] + (lo - sm.pre[sl0]);
+          tsum += len[k];
+        }
+        const unsigned incl = warp_incl_scan(tsum);
+        if (lane_id() == 31) sm.wtot[tid >> 5] = incl;
+        __syncthreads();
+        unsigned wbase = 0, tot = 0;
+#pragma unroll
+        for (int w = 0; w < kThreads / 32; ++w) {
+          const unsigned t = sm.wtot[w];
+          wbase += (w < (int)(tid >> 5)) ? t : 0u;
+          tot += t;
+        }
+        live = tot;
+        if (tot > kWBuf) {  // cannot happen on consistent entries: skip the window, report, stop the run
+          if (tid == 0 && atomicCAS(&p.ctl->error, 0, (int)kErrWindow) == 0) {
+            long long* d = p.ctl->dbg;
+            d[0] = ls; d[1] = n; d[2] = T; d[3] = i; d[4] = e; d[5] = wend; d[6] = tot; d[7] = level;
+          }
+          live = 0;
+          for (int k = 0; k < kEPT; ++k) len[k] = 0;
+        }
+        unsigned vp = wbase + incl - tsum;
+#pragma unroll
+        for (int k = 0; k < kEPT; ++k) {
+          const unsigned sl0 = tid * kEPT + k;
+          sm.beg[sl0] = nb[k];
+          sm.pre[sl0] = vp;  // live-edge prefix (ties resolve to the last entry)
+          if (len[k]) {  // coarse index: this entry holds live edges 32q for q in [ceil(vp/32), (vp+len-1)/32]
+            const unsigned q1 = (vp + len[k] - 1) >> 5;
+            for (unsigned q = (vp + 31) >> 5; q <= q1; ++q) sm.cgr[q] = (unsigned short)sl0;
+          }
+          vp += len[k];
+        }
+        if (tid == 0) sm.pre[kWin] = tot;
+        __syncthreads();
+      }
+      const unsigned nq = (live + 31) >> 5;
+      if (tid == 0) {
+        const long long t = clk();
+        sm.cnt[kStCycWindow] += t - t_a;
+        t_a = t;
+      }
+      // Prefetch the next window's entries while this window's rounds run.
+#pragma unroll
+      for (int k = 0; k < kEPT; ++k)
+        if (wend < e1 && i + kWin + k * kThreads + tid < n) prefetch_l2(F + ls + i + kWin + k * kThreads + tid);
+
+      // Rounds over the live edges: no CTA-wide barrier inside; winners are
+      // staged in sm.wbuf.
+      for (unsigned base = 0; base < live; base += kThreads * kItems) {
+        int row[kItems], cm[kItems], sl[kItems];
+#pragma unroll
+        for (int k = 0; k < kItems; ++k) {
+          const unsigned ee = base + k * kThreads + tid;
+          row[k] = -1;
+          sl[k] = 0;
+          if (ee < live) {
+            // the entry holding ee lies in [cgr[q], cgr[q+1]] (1-2 steps for typical degrees)
+            const unsigned q = ee >> 5;
+            int a = sm.cgr[q];
+            int b = (q + 1 < nq) ? (int)sm.cgr[q + 1] + 1 : kWin;
+            while (b - a > 1) {
+              const int mid = (a + b) >> 1;
+              if (sm.pre[mid] <= ee) a = mid; else b = mid;
+            }
+            sl[k] = a;
+            row[k] = ld_stream(p.adj + sm.beg[a] + (ee - sm.pre[a]), pol);
+            c_trav++;
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < kItems; ++k)
+          cm[k] = row[k] >= 0 ? (BM_KEEP >= 1 ? ld_rlx_hint(RM(p, row[k]), keep) : ld_rlx(RM(p, row[k])))
+                              : -3;
+        unsigned wins = 0, eps = 0;
+        // Column claims: issue every item's atomic before consuming any result
+        // (kItems claims in flight per thread instead of one).
+        int old[kItems];
+#pragma unroll
+        for (int k = 0; k < kItems; ++k) {
+          const int c = cm[k];  // mate of the row; kVisBit set = its column was claimed this phase
+          old[k] = kVisBit;
+          if (c >= 0 && !(c & kVisBit) && (!WR || p.claim_mode == 0 || !root_dead(p, sm.root[sl[k]]))) {
+            if (claim_store) {  // racy claim: a rare concurrent discoverer pushes the column twice
+              st_plain(RM(p, row[k]), c | kVisBit);
+              old[k] = c;
+            } else {
+              old[k] = atomicOr(RM(p, row[k]), kVisBit);
+            }
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < kItems; ++k) {
+          const int c = cm[k];
+          const int col = sm.col[sl[k]];
+          const int root = WR ? sm.root[sl[k]] : col;
+          if (c >= 0) {
+            if (!(old[k] & kVisBit)) {
+              wins |= 1u << k;
+              if (BM_PF == 2) prefetch_l2(p.offs + c);  // the flush reads offs[c], offs[c+1]
+              if (BM_PF == 1) asm volatile("prefetch.global.L2 [%0];" ::"l"(p.offs + c));
+              st_stream(PR(p, row[k]), col, pol);
+              if (p.trace) st_plain(p.bfs + c, level + 1);
+            }
+          } else if (c == -1) {
+            // ONE_PER_TREE: a tree that already holds an endpoint leaves the row alone
+            const bool one = WR && p.ep_one;
+            if ((!one || !root_dead(p, root)) && atomicCAS(RM(p, row[k]), -1, -2) == -1) {
+              bool mine = true;
+              if (one) {
+                // the root's mark is the tree's endpoint slot: first CAS wins, a loser releases the row
+                mine = atomicCAS(p.bfs + root, kStartLevel, IMP ? -row[k] : kFoundMark) == kStartLevel;
+                if (!mine) st_rlx(RM(p, row[k]), -1);
+                else mark_dead(p, root);
+              } else if (WR) {
+                st_rlx(p.bfs + root, IMP ? -row[k] : kFoundMark);  // gpu_match.cpp:122-123
+                mark_dead(p, root);
+              }
+              if (mine) {
+                eps |= 1u << k;
+                st_plain(PR(p, row[k]), col);
+                if (ld_rlx(path_flag) == 0u) st_rlx(path_flag, 1u);
+              }
+            }
+          }
+        }
+        // stage winners (one shared-memory atomic per warp)
+        {
+          const unsigned mine = __popc(wins);
+          const unsigned incl = warp_incl_scan(mine);
+          const unsigned tot = __shfl_sync(kFull, incl, 31);
+          unsigned wb = 0;
+          if (lane_id() == 31 && tot) wb = atomicAdd(&sm.nw, tot);
+          wb = __shfl_sync(kFull, wb, 31) + incl - mine;
+#pragma unroll
+          for (int k = 0; k < kItems; ++k)
+            if (wins & (1u << k)) sm.wbuf[wb++] = make_int2(cm[k], WR ? sm.root[sl[k]] : sm.col[sl[k]]);
+          c_nvis += mine;
+        }
+        // endpoints are rare: warp-aggregated global append
+        {
+          const unsigned mine = __popc(eps);
+          const unsigned incl = warp_incl_scan(mine);
+          const unsigned tot = __shfl_sync(kFull, incl, 31);
+          if (tot) {
+            unsigned eb = 0;
+            if (lane_id() == 31) eb = atomicAdd(&p.ctl->n_ep, tot);
+            eb = __shfl_sync(kFull, eb, 31) + incl - mine;
+#pragma unroll
+            for (int k = 0; k < kItems; ++k)
+              if (eps & (1u << k)) st_plain(p.EP + eb++, row[k]);
+          }
+        }
+      }
+      __syncthreads();
+      if (tid == 0) {
+        const long long t = clk();
+        sm.cnt[kStCycRounds] += t - t_a;
+        t_a = t;
+      }
+      // Flush the window's winners: one CTA reservation for all of them.
+      if (BU && pairs_out) flush_pairs(p, sm, out_base, out, pol);
+      else flush_winners(p, sm, F, out_base, gout, out, pol);
+      e = wend;
+      i += kWin;
+      __syncthreads();
+      if (tid == 0) {
+        const long long t = clk();
+        sm.cnt[kStCycFlush] += t - t_a;
+        t_a = t;
+      }
+    }
+  }
+  flush_count(sm, kStTrav, c_trav);
+  flush_count(sm, kStCexp, c_cexp);
+  flush_count(sm, kStNvis, c_nvis);
+  flush_count(sm, kStEntries, c_entries);
+}
+
+// Appends one (row, col) record to the ALTERNATE write log; lanes that reach
+// this point together share one atomic.
+__device__ __forceinline__ void log_write(const Params& p, int row, int col) {
+  cg::coalesced_group g = cg::coalesced_threads();
+  unsigned base = 0;
+  if (g.thread_rank() == 0) base = atomicAdd(&p.ctl->n_log, g.size());
+  base = g.shfl(base, 0) + g.thread_rank();
+  if (base < p.log_cap) {
+    asm volatile("st.global.v2.b32 [%0], {%1,%2};" ::"l"(p.wlog + base), "r"(row), "r"(col) : "memory");
+  } else {
+    st_rlx(&p.ctl->log_overflow, 1u);
+  }
+}
+
+// ALTERNATE walk (gpu_match.cpp:144-154): swap pairs toward the root, break
+// on a column another walk already claimed this phase.
+__device__ __forceinline__ void alternate_walk(const Params& p, unsigned& walks, unsigned& nsteps, int row) {
+  long long steps = 0;
+  while (row != -1) {
+    const int col = ld_cg(PR(p, row));
+    if (col < 0) break;
+    const int mr = ld_rlx(p.cmatch + col);
+    if (mr >= 0 && ld_cg(PR(p, mr)) == col) {
+      if (steps > 0) log_write(p, row, -1);  // left dangling: its column now belongs to another row
+      break;
+    }
+    st_rlx(p.cmatch + col, row);
+    st_rlx(RM(p, row), col);
+    log_write(p, row, col);
+    row = mr;
+    if (++steps > p.nc) {
+      p.ctl->error = kErrWalk;
+      break;
+    }
+  }
+  nsteps += (unsigned)steps;
+  walks++;
+}
+
+// FIX rules 1 and 2 for one row (gpu_match.cpp:221-237). The CAS keeps the
+// reset count exact when a row is listed more than once.
+__device__ __forceinline__ void fix_row(const Params& p, unsigned& resets, int r) {
+  const int v = ld_rlx(RM(p, r));
+  if (v == -2) {
+    if (atomicCAS(RM(p, r), -2, -1) == -2) resets++;
+  } else if (v >= 0 && ld_rlx(p.cmatch + v) != r) {
+    if (atomicCAS(RM(p, r), v, -1) == v) resets++;
+  }
+}
+
+// FIX rule 3 for one column (gpu_match.cpp:238-243); returns true if the
+// column is unmatched afterwards.
+__device__ __forceinline__ bool fix_col(const Params& p, unsigned& resets, int c) {
+  const int r = ld_rlx(p.cmatch + c);
+  if (r >= 0 && ld_rlx(RM(p, r)) != c) {
+    if (atomicCAS(p.cmatch + c, r, -1) == r) resets++;
+    return true;
+  }
+  return r < 0;
+}
+
+// Clears the visited bits the BFS left in rmatch (one streaming pass, int4).
+__device__ __forceinline__ void sweep_visited(const Params& p) {
+  // one int4 covers 2 interleaved rows or 4 plain ones
+  const bool il = p.rs == 2;
+  const int kRowsPer4 = il ? 2 : 4;
+  int4* r4 = reinterpret_cast<int4*>(p.rm);
+  const unsigned long long n4 = (unsigned long long)p.nr / kRowsPer4;
+  auto clr = [](int& v) { if (v >= 0) v &= ~kVisBit; };
+  constexpr int K = 4;  // int4s per thread in flight
+  const unsigned long long GT = global_threads();
+  for (unsigned long long k0 = global_thread(); k0 < n4; k0 += K * GT) {
+    int4 v[K];
+#pragma unroll
+    for (int i = 0; i < K; ++i)
+      if (k0 + i * GT < n4) v[i] = ld_cg(r4 + k0 + i * GT);
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      if (k0 + i * GT >= n4) continue;
+      const int4 o = v[i];
+      clr(v[i].x);
+      if (!il) clr(v[i].y);
+      clr(v[i].z);
+      if (!il) clr(v[i].w);
+      if (v[i].x != o.x || v[i].y != o.y || v[i].z != o.z || v[i].w != o.w) st_plain(r4 + k0 + i * GT, v[i]);
+    }
+  }
+  for (unsigned long long r = n4 * kRowsPer4 + global_thread(); r < (unsigned long long)p.nr; r += global_threads()) {
+    const int v = ld_cg(RM(p, r));
+    if (v >= 0 && (v & kVisBit)) st_plain(RM(p, r), v & ~kVisBit);
+  }
+}
+
+// Whether a level of T frontier edges over n columns is pulled (bu_rule 1:
+// direction-optimising BFS — pull once the frontier's edges are a large enough
+// share of the edges still to explore, i.e. of the rows not yet visited).
+__device__ __forceinline__ bool want_pull(const Params& p, unsigned long long T, unsigned n, unsigned ls) {
+  if (p.bu_rule == 0) return T >= p.bu_min_edges;
+  const long long unv = (long long)p.nr - (long long)ls - (long long)n;
+  const double mu = (unv > 0 ? (double)unv : 0.0) * p.deg_row;
+  return n >= p.bu_min_n && (double)T * (double)p.bu_alpha >= mu;
+}
+
+__device__ __forceinline__ void check_fail(const Params& p, long long a, long long b, long long c, long long d,
+                                           long long e, long long f, long long g, long long h) {
+  if (atomicCAS(&p.ctl->error, 0, (int)kErrCheck) == 0) {
+    long long* x = p.ctl->dbg;
+    x[0] = a; x[1] = b; x[2] = c; x[3] = d; x[4] = e; x[5] = f; x[6] = g; x[7] = h;
+  }
+}
+// BM_CHECK: the n entries of a pushed level are consecutive edge ranges
+// (pre[k] + deg[k] == pre[k+1], the last ending at T) and the granule index
+// points at the entry holding each granule's first edge.
+__device__ void check_level(const Params& p, const int4* F, unsigned ls, unsigned n, unsigned T, const unsigned* gin,
+                            int lv, int tag) {
+  for (unsigned long long k = global_thread(); k < n; k += global_threads()) {
+    const int4 a = ld_cg(F + ls + k);
+    if (a.x < 0 || a.x >= p.nc) {
+      check_fail(p, tag + 20, lv, ls, n, T, k, a.x, a.w);
+      continue;
+    }
+    const unsigned deg = ld_ro(p.offs + a.x + 1) - ld_ro(p.offs + a.x);
+    const unsigned nxt = k + 1 < n ? (unsigned)ld_cg(F + ls + k + 1).w : T;
+    if (a.x < 0 || a.x >= p.nc || (unsigned)a.w + deg != nxt || (unsigned)a.z != ld_ro(p.offs + a.x))
+      check_fail(p, tag, lv, ls, n, T, k, a.w, nxt);
+    if (deg) {
+      const unsigned m1 = ((unsigned)a.w + deg - 1) / kGran;
+      for (unsigned m = ((unsigned)a.w + kGran - 1) / kGran; m <= m1; ++m)
+        if ((unsigned)ld_cg(reinterpret_cast<const int*>(gin) + m) != k) check_fail(p, tag + 10, lv, ls, n, T, k, m, 0);
+    }
+  }
+}
+
+struct PhaseOut {
+  bool found;
+  long long launches;
+  long long after;
+};
+
+// One phase = run_phase (gpu_match.cpp:268-302) from the roots in F[cur].
+template <bool WR, bool IMP, bool BU>
+__device__ PhaseOut run_phase(const Params& p, Smem& sm, int cur, int parity, bool serial_alt,
+                              long long isolated, bool skip_alt) {
+  Ctrl* ctl = p.ctl;
+  int4* F = cur ? p.F1 : p.F0;
+  int4* Fn = cur ? p.F0 : p.F1;
+  PhaseOut out{false, 0, 0};
+
+  // ---- BFS level loop (expand_bfs, gpu_match.cpp:247-266) ----
+  const unsigned long long rp = ld_rlx(&ctl->roots.packed);
+  const unsigned n0 = (unsigned)(rp >> 33);
+  unsigned n = n0;
+  unsigned T = (unsigned)(rp & kEdgeMask);
+  unsigned ls = 0;
+  int lv = 0;
+  bool found = false;
+  bool in_pairs = false;  // this level's entries are (col, root) pairs in P (pulled-capable kernels)
+  const unsigned long long pol_mat = policy_evict_first();
+  // Narrow levels (at most solo_edges frontier edges) run on block 0 alone,
+  // back to back with CTA barriers only — a grid barrier costs more than such
+  // a level's work. The other CTAs wait at one grid barrier and take over
+  // when the frontier widens again or the BFS ends.
+  for (;;) {
+    Slot* in = lv == 0 ? &ctl->roots : &ctl->lvl[lv % 3];
+    // BU: compiled only into the bottom-up kernel instances, so the push-only
+    // kernel keeps its register allocation
+    const bool bu = BU && p.roffs && !p.trace && T > p.solo_edges && want_pull(p, T, n, ls);
+    const bool mat = BU && in_pairs && !bu;
+    if (p.check && BU && in_pairs) {
+      for (unsigned long long k = global_thread(); k < n; k += global_threads()) {
+        const int2 pr = ld_cg(p.P + ls + k);
+        if (pr.x < 0 || pr.x >= p.nc || pr.y < 0 || pr.y >= p.nc) check_fail(p, 40, lv, ls, n, T, k, pr.x, pr.y);
+      }
+      grid_sync(p);
+    }
+    if (mat) {  // pushed after all: build its edge-tiled entries first
+      Slot* ms = &ctl->mat[lv & 1];
+      materialize(p, sm, F, ls, n, (lv & 1) ? p.gidx1 : p.gidx0, ms, pol_mat, false);
+      grid_sync(p);
+      const unsigned long long mp = ld_rlx(&ms->packed);
+      T = (unsigned)(mp & kEdgeMask);
+      in_pairs = false;
+      if (p.check && is_leader() && (mp >> 33) != n) check_fail(p, 30, lv, ls, n, T, (long long)(mp >> 33), 0, 0);
+    }
+    if (p.check && !bu && T > p.solo_edges) {  // (block 0's solo levels are not checked)
+      check_level(p, F, ls, n, T, (lv & 1) ? p.gidx1 : p.gidx0, lv, mat ? 2 : 1);
+      grid_sync(p);
+    }
+    const bool solo = !bu && T <= p.solo_edges;
+    if (solo && blockIdx.x != 0) {
+      grid_sync(p);  // block 0's hand-over
+      lv = ld_rlx(&ctl->solo_lv);
+      ls = (unsigned)ld_rlx(&ctl->solo_ls);
+      n = (unsigned)ld_rlx(&ctl->solo_n);
+      T = (unsigned)ld_rlx(&ctl->solo_T);
+      found = ld_rlx(&ctl->solo_found) != 0;
+      out.launches = (long long)ld_rlx((const unsigned long long*)&ctl->solo_launches);
+      in_pairs = false;  // solo levels push entries
+      if (ld_rlx(&ctl->solo_stop)) break;
+      continue;
+    }
+    Slot* outs = &ctl->lvl[(lv + 1) % 3];
+    if (is_leader() && lv >= 1) {
+      Slot* z = &ctl->lvl[(lv + 2) % 3];
+      z->packed = 0;
+      z->tile = 0;
+    }
+    if (BU && is_leader()) ctl->mat[(lv + 1) & 1].packed = 0;  // last read before this level's barrier
+    if (solo) __syncthreads();
+    // a wide level hands its winners on as pairs (see Params::P)
+    const bool pairs_out = BU && p.roffs && !p.trace && !solo && (bu || (unsigned long long)T >= p.pairs_min_edges);
+    if (bu) {
+      bu_prep<WR>(p, sm, F, in_pairs, ls, n, lv);
+      grid_sync(p);
+#ifdef BM_SWEEP_OLD
+      bu_sweep<WR, IMP>(p, sm, ls + n, outs, lv, parity);
+#else
+      bu_sweep_q<WR, IMP>(p, sm, ls + n, outs, lv, parity);
+#endif
+      if (threadIdx.x == 0) sm.cnt[kStPulledLevels] += is_leader() ? 1 : 0;
+    } else {
+      // Claims by plain store (no atomic round trip; two discoverers racing on one
+      // row both push its column, which the reference's plain stores allow too)
+      // when one output entry per frontier edge still fits the phase's frontier
+      // capacity; otherwise by atomicOr, which pushes every column once.
+      const bool claim_store = p.claim_store && (unsigned long long)ls + n + T <= p.fcap;
+      expand_level<WR, IMP, BU>(p, sm, F, ls, n, T, (lv & 1) ? p.gidx1 : p.gidx0, (lv & 1) ? p.gidx0 : p.gidx1,
+                                in, outs, kStartLevel + lv, parity, pairs_out, claim_store);
+    }
+
+    const long long tb = clk();
+    if (solo) {
+      __threadfence_block();
+      __syncthreads();
+    } else {
+      grid_sync(p);
+      if (bu) bu_clear(p, lv);  // read by nobody from here on; the next level uses the other bitmap
+    }
+    if (threadIdx.x == 0) sm.cnt[kStCycBarrier] += clk() - tb;
+    tl_mark(p, kTlLevel, n);
+    tl_mark(p, kTlLevelEdges, (T & 0x7fffffffu) | (bu ? 0x80000000u : 0u));  // frontier edges; top bit: pulled
+    out.launches++;
+    const unsigned long long op = ld_rlx(&outs->packed);
+    const unsigned n_next = (unsigned)(op >> 33);
+    found = ld_rlx(&ctl->path_found[parity]) != 0u;
+    bool stop = (p.apsb && found) || n_next == 0;
+    if (!stop) {
+      ls += n;
+      n = n_next;
+      T = (unsigned)(op & kEdgeMask);
+      in_pairs = pairs_out;
+      if (pairs_out) T = (unsigned)fmin((double)n * p.deg_col, 4294967295.0);  // an estimate until materialized
+      ++lv;
+      if (lv > p.nc + 2) {
+        if (is_leader()) ctl->error = kErrLevels;
+        stop = true;
+      }
+    }
+    if (solo && (stop || T > p.solo_edges)) {  // block 0 hands the BFS back to the grid
+      if (threadIdx.x == 0) {
+        ctl->solo_lv = lv;
+        ctl->solo_stop = stop ? 1 : 0;
+        ctl->solo_ls = ls;
+        ctl->solo_n = n;
+        ctl->solo_T = T;
+        ctl->solo_found = found ? 1 : 0;
+        ctl->solo_launches = out.launches;
+      }
+      grid_sync(p);
+    }
+    if (stop) break;
+  }
+  out.found = found;
+  sweep_visited(p);
+  grid_sync(p);
+  if (p.stop_after_bfs) return out;
+
+  // ---- ALTERNATE (gpu_match.cpp:158-218) ----
+  if (is_leader()) ctl->path_found[parity ^ 1] = 0u;  // flag of the next phase
+  const unsigned n_ep = ld_rlx(&ctl->n_ep);
+  unsigned walks = 0, steps = 0, resets = 0;
+  if (skip_alt) {
+    // fault injection: a raced ALTERNATE that augmented nothing, so the driver
+    // must take the serial retry (gpu_match.cpp:328-343)
+  } else if (!serial_alt) {
+    if (!IMP) {
+      for (unsigned long long k = global_thread(); k < n_ep; k += global_threads())
+        alternate_walk(p, walks, steps, ld_cg(p.EP + k));
+    } else {
+      for (unsigned long long k = global_thread(); k < n0; k += global_threads()) {
+        const int c = ld_cg(reinterpret_cast<const int*>(F + k));
+        const int mark = ld_rlx(p.bfs + c);
+        if (mark <= 0) alternate_walk(p, walks, steps, -mark);  // live levels are >= 1 (L0 = 2)
+      }
+    }
+  } else if (is_leader()) {
+    // Serial retry (gpu_match.cpp:328-343): one thread walks every endpoint
+    // in turn; the first walk cannot meet a claimed column, so the phase
+    // always augments when a path exists.
+    if (!IMP) {
+      for (unsigned k = 0; k < n_ep; ++k) alternate_walk(p, walks, steps, ld_cg(p.EP + k));
+    } else {
+      for (unsigned k = 0; k < n0; ++k) {
+        const int c = ld_cg(reinterpret_cast<const int*>(F + k));
+        const int mark = ld_rlx(p.bfs + c);
+        if (mark <= 0) alternate_walk(p, walks, steps, -mark);
+      }
+    }
+  }
+  flush_count(sm, kStWalks, walks);
+  flush_count(sm, kStSteps, steps);
+  grid_sync(p);
+  tl_mark(p, kTlAlt, 0);
+
+  // ---- FIXMATCHING rules 1+2 over the rows ALTERNATE wrote or left behind ----
+  const bool dense = ld_rlx(&ctl->log_overflow) != 0u;
+  const unsigned n_log = dense ? 0u : min(ld_rlx(&ctl->n_log), p.log_cap);
+  if (!dense) {
+    for (unsigned long long k = global_thread(); k < n_log; k += global_threads())
+      fix_row(p, resets, ld_cg(reinterpret_cast<const int*>(p.wlog + k)));
+    for (unsigned long long k = global_thread(); k < n_ep; k += global_threads())
+      fix_row(p, resets, ld_cg(p.EP + k));
+  } else {  // log overflow: the reference's full pass
+    for (unsigned long long r = global_thread(); r < (unsigned long long)p.nr; r += global_threads())
+      fix_row(p, resets, (int)r);
+  }
+  if (WR)
+    for (unsigned long long k = global_thread(); k < (unsigned long long)p.ndead_words; k += global_threads())
+      st_plain(reinterpret_cast<int*>(p.dead) + k, 0);
+
+  if (is_leader()) {
+    for (int s = 0; s < 3; ++s) {
+      ctl->lvl[s].packed = 0;
+      ctl->lvl[s].tile = 0;
+    }
+    ctl->roots.packed = 0;
+    ctl->roots.tile = 0;
+    ctl->mat[0].packed = 0;
+    ctl->mat[1].packed = 0;
+  }
+  grid_sync(p);
+  tl_mark(p, kTlFixRows, dense ? 1u : 0u);
+
+  // ---- FIXMATCHING rule 3 over the columns ALTERNATE wrote; a non-root column
+  //      it unmatches becomes a root of the next phase ----
+  const unsigned long long ncheck = dense ? (unsigned long long)p.nc : n_log;
+  for (unsigned long long b = (unsigned long long)blockIdx.x * kThreads; b < ncheck; b += global_threads()) {
+    const unsigned long long k = b + threadIdx.x;
+    bool push = false;
+    int c = -1;
+    unsigned beg = 0, deg = 0;
+    if (k < ncheck) {
+      c = dense ? (int)k : ld_cg(reinterpret_cast<const int*>(p.wlog + k) + 1);
+      if (c >= 0 && fix_col(p, resets, c)) {
+        // roots of this phase are handled below; others enter the root set once
+        if (dense) {
+          push = ld_rlx(p.bfs + c) == kUnvisited;
+          if (push) st_rlx(p.bfs + c, kStartLevel);
+        } else {
+          push = atomicCAS(p.bfs + c, kUnvisited, kStartLevel) == kUnvisited;
+        }
+        if (push) {
+          beg = ld_ro(p.offs + c);
+          deg = ld_ro(p.offs + c + 1) - beg;
+          push = deg > 0;
+        }
+      }
+    }
+    unsigned long long slot;
+    unsigned unused;
+    if (cta_reserve(sm, push ? 1u : 0u, push ? deg : 0u, 0u, &ctl->roots, &ctl->n_ep, slot, unused) && push)
+      put_entry(Fn, 0u, p.gidx0, slot, c, c, beg, deg);
+  }
+  if (is_leader()) {
+    ctl->n_ep = 0u;
+    ctl->n_log = 0u;
+    ctl->log_overflow = 0u;
+  }
+  grid_sync(p);
+  tl_mark(p, kTlFixCols, n_log);
+
+  // ---- this phase's roots: still unmatched -> root again; matched -> bfs 1 ----
+  for (unsigned long long b = (unsigned long long)blockIdx.x * kThreads; b < n0; b += global_threads()) {
+    const unsigned long long k = b + threadIdx.x;
+    bool push = false;
+    int c = -1;
+    unsigned beg = 0, deg = 0;
+    if (k < n0) {
+      const int4 ent = ld_cg(F + k);
+      c = ent.x;
+      if (ld_rlx(p.cmatch + c) < 0) {
+        push = true;
+        beg = (unsigned)ent.z;
+        const unsigned nxt = (k + 1 < n0) ? ld_cg_u(F + k + 1) : (unsigned)(rp & kEdgeMask);
+        deg = nxt - (unsigned)ent.w;
+        st_plain(p.bfs + c, kStartLevel);
+      } else {
+        st_plain(p.bfs + c, kUnvisited);
+      }
+    }
+    unsigned long long slot;
+    unsigned unused;
+    if (cta_reserve(sm, push ? 1u : 0u, push ? deg : 0u, 0u, &ctl->roots, &ctl->n_ep, slot, unused) && push)
+      put_entry(Fn, 0u, p.gidx0, slot, c, c, beg, deg);
+  }
+  flush_count(sm, kStResets, resets);
+  grid_sync(p);
+  const unsigned long long np = ld_rlx(&ctl->roots.packed);
+  tl_mark(p, kTlRoots, (unsigned)(np >> 33));
+  out.after = (long long)p.nc - isolated - (long long)(np >> 33);
+  return out;
+}
+
+// ---------------------------------------------------------------------------
+template <bool WR, bool IMP, bool BU>
+__global__ void __launch_bounds__(kThreads, BM_MINB) driver_kernel(Params p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];  // sizeof(Smem) > 48 KB: dynamic shared memory
+  Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
+  Ctrl* ctl = p.ctl;
+  if (threadIdx.x < kNumStats) sm.cnt[threadIdx.x] = 0;
+  __syncthreads();
+  tl_mark(p, kTlStart, p.fresh);
+
+  int cur;
+  long long card, outer, isolated;
+  int recs = 0;
+
+  if (p.fresh) {
+    // ---- optional GPU initial matching (parallel first-fit with CAS) ----
+    if (p.init_mode != BM_INIT_GIVEN) {
+      for (int pass = (p.init_mode == BM_INIT_GPU_KS ? 0 : 1); pass < 2; ++pass) {
+        for (unsigned long long c = global_thread(); c < (unsigned long long)p.nc; c += global_threads()) {
+          if (ld_cg(p.cmatch + c) != -1) continue;
+          const unsigned b = ld_ro(p.offs + c), e = ld_ro(p.offs + c + 1);
+          if (pass == 0 && e - b != 1) continue;  // one-sided Karp-Sipser: degree-1 columns first
+          for (unsigned j = b; j < e; ++j) {
+            const int r = ld_ro(p.adj + j);
+            if (ld_rlx(RM(p, r)) == -1 && atomicCAS(RM(p, r), -1, (int)c) == -1) {
+              st_plain(p.cmatch + c, r);
+              break;
+            }
+          }
+        }
+        grid_sync(p);
+        tl_mark(p, kTlInit, pass);
+      }
+    }
+    // ---- setup: validate init, bfs_array init, roots of phase 1 ----
+    unsigned long long bad = 0, iso = 0;
+    for (unsigned long long b = (unsigned long long)blockIdx.x * kThreads; b < (unsigned long long)p.nc;
+         b += global_threads()) {
+      const unsigned long long c = b + threadIdx.x;
+      bool root = false;
+      unsigned beg = 0, deg = 0;
+      if (c < (unsigned long long)p.nc) {
+        const int r = ld_cg(p.cmatch + c);
+        if (!p.init_checked) {
+          if (r < -1 || r >= p.nr) bad++;
+          else if (r >= 0 && ld_cg(RM(p, r)) != (int)c) bad++;
+          else if (r >= 0 && !has_edge(p.adj, ld_ro(p.offs + c), ld_ro(p.offs + c + 1), r, p.sorted)) bad++;
+        }
+        st_plain(p.bfs + c, r >= 0 ? kUnvisited : kStartLevel);
+        if (r < 0) {
+          beg = ld_ro(p.offs + c);
+          deg = ld_ro(p.offs + c + 1) - beg;
+          if (deg > 0) root = true; else iso++;
+        }
+      }
+      unsigned long long slot;
+      unsigned unused;
+      if (cta_reserve(sm, root ? 1u : 0u, root ? deg : 0u, 0u, &ctl->roots, &ctl->n_ep, slot, unused) && root)
+        put_entry(p.F0, 0u, p.gidx0, slot, (int)c, (int)c, beg, deg);
+    }
+    if (!p.init_checked)
+      for (unsigned long long r = global_thread(); r < (unsigned long long)p.nr; r += global_threads()) {
+        const int v = ld_cg(RM(p, r));
+        if (v < -1 || v >= p.nc) bad++;
+        else if (v >= 0 && ld_cg(p.cmatch + v) != (int)r) bad++;
+      }
+    bad = warp_sum(bad);
+    iso = warp_sum(iso);
+    if (lane_id() == 0) {
+      if (bad) atomicAdd(&ctl->invalid, bad);
+      if (iso) atomicAdd(&ctl->isolated, iso);
+    }
+    grid_sync(p);
+    tl_mark(p, kTlSetup, 0);
+    if (ld_rlx(&ctl->invalid) != 0ull) {
+      if (is_leader()) ctl->error = kErrInvalidInit;
+      return;
+    }
+    isolated = (long long)ld_rlx(&ctl->isolated);
+    cur = 0;
+    card = (long long)p.nc - isolated - (long long)(ld_rlx(&ctl->roots.packed) >> 33);
+    outer = 0;
+    if (is_leader()) {
+      ctl->init_card = card;
+      ctl->isolated_cols = isolated;
+    }
+  } else {
+    cur = ctl->cur;
+    card = ctl->card;
+    outer = ctl->outer;
+    isolated = ctl->isolated_cols;
+  }
+  int parity = ctl->phase_parity;
+  if (p.fresh) parity = 0;
+
+  // ---- driver loop (run_driver, gpu_match.cpp:306-359) ----
+  bool done = false;
+  for (;;) {
+    if (outer + 1 > p.phase_bound) {
+      if (is_leader()) ctl->error = kErrBound;
+      break;
+    }
+    ++outer;
+    const long long before = card;
+    PhaseOut ph = run_phase<WR, IMP, BU>(p, sm, cur, parity, false, isolated, outer == p.dbg_skip_alt_phase);
+    if (p.stop_after_bfs) {
+      if (is_leader()) {
+        ctl->bfs_levels_last = ph.launches;
+        ctl->path_found_last = ph.found ? 1 : 0;
+      }
+      done = true;
+      break;
+    }
+    cur ^= 1;
+    parity ^= 1;
+    long long launches = ph.launches;
+    long long after = ph.after;
+    bool retried = false;
+    if (ph.found && after <= before) {
+      PhaseOut rt = run_phase<WR, IMP, BU>(p, sm, cur, parity, true, isolated, false);
+      cur ^= 1;
+      parity ^= 1;
+      launches += rt.launches;
+      after = rt.after;
+      ph.found = rt.found;
+      retried = true;
+    }
+    if (is_leader()) {
+      if (recs < p.rec_cap) {
+        PhaseRec r;
+        r.launches = launches;
+        r.before = before;
+        r.after = after;
+        r.found = ph.found ? 1 : 0;
+        r.retry = retried ? 1 : 0;
+        p.recs[recs] = r;
+      }
+      sm.cnt[kStLevels] += (unsigned long long)launches;
+      if (retried) sm.cnt[kStRetries]++;
+    }
+    ++recs;
+    card = after;
+    if (!ph.found) {
+      done = true;
+      break;
+    }
+    if (ld_rlx((const unsigned*)&ctl->error) != 0u) break;
+    if (recs >= p.max_phases || recs >= p.rec_cap) break;
+  }
+
+  // ---- flush counters and run state ----
+  tl_mark(p, kTlEnd, 0);
+  __syncthreads();
+  if (threadIdx.x < kNumStats && sm.cnt[threadIdx.x]) atomicAdd(&ctl->stats[threadIdx.x], sm.cnt[threadIdx.x]);
+  if (is_leader()) {
+    ctl->cur = cur;
+    ctl->card = card;
+    ctl->outer = outer;
+    ctl->done = done ? 1 : 0;
+    ctl->n_recs = recs < p.rec_cap ? recs : p.rec_cap;
+    ctl->phase_parity = parity;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Upload-time validation (check_csr, csr_graph.cpp:45-64) and offset narrowing.
+__global__ void convert_offsets_kernel(const long long* in, unsigned* out, int nc, long long E,
+                                       unsigned long long* bad, unsigned long long* empty) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i <= nc;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long v = in[i];
+    bool ok = v >= 0 && v <= E;
+    if (i == 0 && v != 0) ok = false;
+    if (i == nc && v != E) ok = false;
+    if (i > 0 && in[i - 1] > v) ok = false;
+    if (!ok) atomicAdd(bad, 1ull);
+    const unsigned e = __ballot_sync(__activemask(), i > 0 && in[i - 1] == v);  // column i-1 is empty
+    if (e && (threadIdx.x & 31) == __ffs(__activemask()) - 1) atomicAdd(empty, (unsigned long long)__popc(e));
+    out[i] = (unsigned)v;
+  }
+}
+
+// Flat adjacency check over [j0, j1) (one pass, vector loads): rows out of
+// range, and descending neighbour pairs (j-1, j) anywhere — pairs that straddle
+// a column start are subtracted by col_start_pairs_kernel. Runs per uploaded
+// chunk, overlapped with the copy of the next chunk.
+__global__ void check_adj_flat_kernel(const int* adj, long long j0, long long j1, int nr,
+                                      unsigned long long* bad_range, unsigned long long* desc) {
+  unsigned long long br = 0, ds = 0;
+  const long long tot = (long long)gridDim.x * blockDim.x;
+  for (long long j = j0 + blockIdx.x * (long long)blockDim.x + threadIdx.x; j < j1; j += tot) {
+    const int r = adj[j];
+    if (r < 0 || r >= nr) br++;
+    if (j > 0 && adj[j - 1] >= r) ds++;
+  }
+  br = warp_sum(br);
+  ds = warp_sum(ds);
+  if (lane_id() == 0) {
+    if (br) atomicAdd(bad_range, br);
+    if (ds) atomicAdd(desc, ds);
+  }
+}
+__global__ void col_start_pairs_kernel(const unsigned* offs, const int* adj, int nc, unsigned long long* desc_fix) {
+  unsigned long long f = 0;
+  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < nc; c += (long long)gridDim.x * blockDim.x) {
+    const unsigned b = offs[c];
+    if (b > 0 && offs[c + 1] > b && adj[b - 1] >= adj[b]) f++;
+  }
+  f = warp_sum(f);
+  if (lane_id() == 0 && f) atomicAdd(desc_fix, f);
+}
+
+// Validity half of the Berge certificate (validate, matching.cpp:70-104).
+__global__ void validate_kernel(const unsigned* offs, const int* adj, int nc, int nr, int sorted,
+                                const int* rmatch, const int* cmatch,
+                                unsigned long long* violations, unsigned long long* matched) {
+  const long long tot = (long long)gridDim.x * blockDim.x;
+  unsigned long long bad = 0, m = 0;
+  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < nr; r += tot) {
+    const int c = rmatch[r];
+    if (c == -1) continue;
+    if (c < 0 || c >= nc) { bad++; continue; }  // -2 pending flag or out of range
+    if (cmatch[c] != (int)r) { bad++; continue; }
+    const unsigned b = offs[c], e = offs[c + 1];
+    bool has = false;
+    if (sorted) {
+      unsigned lo = b, hi = e;
+      while (lo < hi) {
+        const unsigned mid = lo + ((hi - lo) >> 1);
+        const int v = adj[mid];
+        if (v == (int)r) { has = true; break; }
+        if (v < (int)r) lo = mid + 1; else hi = mid;
+      }
+    } else {
+      for (unsigned j = b; j < e && !has; ++j) has = adj[j] == (int)r;
+    }
+    if (!has) bad++; else m++;
+  }
+  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < nc; c += tot) {
+    const int r = cmatch[c];
+    if (r == -1) continue;
+    if (r < 0 || r >= nr) { bad++; continue; }
+    if (rmatch[r] != (int)c) bad++;
+  }
+  bad = warp_sum(bad);
+  m = warp_sum(m);
+  if ((threadIdx.x & 31) == 0) {
+    if (bad) atomicAdd(violations, bad);
+    if (m) atomicAdd(matched, m);
+  }
+}
+
+// Maximality half of the certificate (is_maximum, matching.cpp:106-131) as a
+// plain queue BFS that shares nothing with driver_kernel: alternating levels
+// from every free non-isolated column over the plain rmatch, a visited bitmap
+// of its own, one warp per frontier column, one launch per level. A free row
+// reached from a free column is an augmenting path.
+__global__ void verify_roots_kernel(const unsigned* offs, const int* cmatch, int nc, unsigned* vis, int* q,
+                                    unsigned* qn) {
+  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < nc; c += (long long)gridDim.x * blockDim.x) {
+    if (cmatch[c] != -1 || offs[c + 1] == offs[c]) continue;
+    atomicOr(vis + (c >> 5), 1u << (c & 31));
+    q[atomicAdd(qn, 1u)] = (int)c;
+  }
+}
+__global__ void verify_level_kernel(const unsigned* offs, const int* adj, const int* rmatch, const int* q,
+                                    unsigned n, unsigned* vis, int* qnext, unsigned* qn, unsigned* found) {
+  const long long warps = (long long)gridDim.x * blockDim.x / 32;
+  for (long long i = (blockIdx.x * (long long)blockDim.x + threadIdx.x) / 32; i < n; i += warps) {
+    if (*(volatile unsigned*)found) return;
+    const int c = q[i];
+    for (unsigned j = offs[c] + lane_id(); j < offs[c + 1]; j += 32) {
+      const int m = rmatch[adj[j]];
+      if (m == -1) {
+        *found = 1u;
+      } else if (m >= 0) {
+        const unsigned bit = 1u << (m & 31);
+        if (!(atomicOr(vis + (m >> 5), bit) & bit)) qnext[atomicAdd(qn, 1u)] = m;
+      }
+    }
+  }
+}
+
+// Row-state (de)interleaving between the caller's plain rmatch / predecessor
+// arrays and the device layout (see RM / PR).
+__global__ void rows_pack_kernel(const int* plain, int* rm, int nr, int rs) {
+  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < nr; r += (long long)gridDim.x * blockDim.x)
+    rm[rs * r] = plain[r];
+}
+__global__ void rows_unpack_kernel(const int* a, int* out, int nr, int rs) {
+  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < nr; r += (long long)gridDim.x * blockDim.x)
+    out[r] = a[rs * r];
+}
+__global__ void rows_fill_kernel(int* a, int nr, int rs, int v) {
+  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < nr; r += (long long)gridDim.x * blockDim.x)
+    a[rs * r] = v;
+}
+
+// permute_random on the device (csr_graph.cpp:80-90): column c becomes
+// cperm[c], row r becomes rperm[r], each column's rows re-sorted.
+__global__ void perm_degrees_kernel(const unsigned* offs, const int* cperm, unsigned* deg, int nc) {
+  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < nc; c += (long long)gridDim.x * blockDim.x)
+    deg[cperm[c]] = offs[c + 1] - offs[c];
+}
+__global__ void perm_scatter_kernel(const unsigned* offs, const int* adj, const int* cperm, const int* rperm,
+                                    const unsigned* noffs, int* nadj, int nc) {
+  const long long warps = (long long)gridDim.x * blockDim.x / 32;
+  for (long long c = (blockIdx.x * (long long)blockDim.x + threadIdx.x) / 32; c < nc; c += warps) {
+    const unsigned b = offs[c], e = offs[c + 1], d = noffs[cperm[c]];
+    for (unsigned j = b + lane_id(); j < e; j += 32) nadj[d + (j - b)] = rperm[adj[j]];
+  }
+}
+
+// Validity of a resident initial matching (plain arrays), checked once at load.
+__global__ void init_check_kernel(const unsigned* offs, const int* adj, int sorted, const int* rmatch,
+                                  const int* cmatch, int nc, int nr, unsigned long long* bad) {
+  unsigned long long b = 0;
+  const long long tot = (long long)gridDim.x * blockDim.x;
+  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < nc; c += tot) {
+    const int r = cmatch[c];
+    if (r < -1 || r >= nr) b++;
+    else if (r >= 0 && rmatch[r] != (int)c) b++;
+    else if (r >= 0 && !has_edge(adj, offs[c], offs[c + 1], r, sorted != 0)) b++;  // a pair must be an edge
+  }
+  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < nr; r += tot) {
+    const int v = rmatch[r];
+    if (v < -1 || v >= nc) b++;
+    else if (v >= 0 && cmatch[v] != (int)r) b++;
+  }
+  b = warp_sum(b);
+  if (lane_id() == 0 && b) atomicAdd(bad, b);
+}
+
+// Transposed adjacency (rows -> columns) for bottom-up levels: count,
+// exclusive scan (CUB), scatter. Row lists come out unsorted (not needed).
+// Row index (transpose) for the pulled levels. A one-pass scatter (an atomic
+// cursor bump and a 4-byte store per edge at a random place of the 4E-byte
+// index, after an atomic degree count into nr counters) turns every access
+// into a partial-sector DRAM read-modify-write once the arrays outgrow L2:
+// 9.6 ms at C2, ~300 ms at C5. Instead the edges are first bucketed by row
+// range, so that everything after that works inside one L2-sized window:
+//   bucket_hist   bucket sizes (NB <= 512 counters, CTA-aggregated)
+//   bucket_partition  streams the CSC once and appends every edge as a
+//                 (row, col) pair to its bucket (CTA-staged runs)
+//   pair_count    row degrees, streaming the pairs bucket by bucket
+//   (CUB scan)    row offsets
+//   pair_scatter  the row index, streaming the pairs bucket by bucket
+// The last two hand out chunks in order from a global counter, so the whole
+// grid stays within one or two buckets: each bucket's counters (<= 2 MB) and
+// slice of the index (<= 32 MB) stay in L2 and leave it as full sectors.
+constexpr int kTpChunk = 2048;   // edges per CTA step of bucket_partition (8 per thread)
+constexpr int kPairChunk = 4096; // pairs per CTA step of the ordered passes (16 per thread)
+constexpr int kMaxBuckets = 512;
+
+__global__ void __launch_bounds__(256) bucket_hist_kernel(const int* adj, unsigned E, int shift, int nb,
+                                                          unsigned* bcount) {
+  __shared__ unsigned hist[kMaxBuckets];
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) hist[b] = 0;
+  __syncthreads();
+  for (unsigned long long j = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; j < E;
+       j += (unsigned long long)gridDim.x * blockDim.x)
+    atomicAdd(&hist[ld_ro(adj + j) >> shift], 1u);
+  __syncthreads();
+  for (int b = threadIdx.x; b < nb; b += blockDim.x)
+    if (hist[b]) atomicAdd(bcount + b, hist[b]);
+}
+
+// pcur[b] = first pair slot of bucket b (exclusive scan of nb <= 512 counts).
+__global__ void bucket_base_kernel(const unsigned* bcount, int nb, unsigned* pcur) {
+  if (threadIdx.x == 0) {
+    unsigned run = 0;
+    for (int b = 0; b < nb; ++b) {
+      pcur[b] = run;
+      run += bcount[b];
+    }
+  }
+}
+
+// First column whose range [offs[c], offs[c+1]) holds edge j (offs ascending, offs[0] = 0).
+__device__ __forceinline__ int column_of(const unsigned* offs, int lo, int hi, unsigned j) {
+  while (hi - lo > 1) {  // invariant: offs[lo] <= j < offs[hi]
+    const int mid = (lo + hi) >> 1;
+    if (ld_ro(offs + mid) <= j) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+__global__ void __launch_bounds__(256) bucket_partition_kernel(const unsigned* offs, const int* adj, int nc,
+                                                                unsigned E, int shift, int nb, unsigned* pcur,
+                                                                int2* pairs) {
+  __shared__ unsigned hist[kMaxBuckets];
+  __shared__ unsigned base[kMaxBuckets];   // global slot of this chunk's run of each bucket
+  __shared__ unsigned lbase[kMaxBuckets];  // its slot in the stage
+  __shared__ unsigned wsum[8];
+  __shared__ int2 stage[kTpChunk];
+  __shared__ unsigned short sbk[kTpChunk];
+  __shared__ int span[2];
+  constexpr int kPer = kTpChunk / 256;
+  const unsigned nchunks = (E + kTpChunk - 1) / kTpChunk;
+  for (unsigned ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+    const unsigned j0 = ch * kTpChunk, j1 = min(E, j0 + kTpChunk);
+    for (int b = threadIdx.x; b < nb; b += blockDim.x) hist[b] = 0;
+    if (threadIdx.x < 2) span[threadIdx.x] = column_of(offs, 0, nc, threadIdx.x ? j1 - 1 : j0) + threadIdx.x;
+    __syncthreads();
+    // this thread's kPer consecutive edges [jb, je)
+    const unsigned jb = j0 + threadIdx.x * kPer, je = min(j1, jb + kPer);
+    int row[kPer];
+    unsigned short rank[kPer];
+    int col = jb < je ? column_of(offs, span[0], span[1], jb) : 0;
+    unsigned next = jb < je ? ld_ro(offs + col + 1) : 0;
+    int cols[kPer];
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const unsigned j = jb + k;
+      row[k] = -1;
+      if (j < je) {
+        while (j >= next) next = ld_ro(offs + (++col) + 1);  // empty columns are skipped
+        row[k] = ld_ro(adj + j);
+        cols[k] = col;
+        rank[k] = (unsigned short)atomicAdd(&hist[row[k] >> shift], 1u);
+      }
+    }
+    __syncthreads();
+    // CTA-local bucket-major order: exclusive scan of the (<= 512) bucket counts,
+    // two per thread; then one global reservation per non-empty bucket
+    {
+      const int b0 = 2 * threadIdx.x;
+      const unsigned c0 = b0 < nb ? hist[b0] : 0u, c1 = b0 + 1 < nb ? hist[b0 + 1] : 0u;
+      const unsigned incl = warp_incl_scan(c0 + c1);
+      if (lane_id() == 31) wsum[threadIdx.x >> 5] = incl;
+      __syncthreads();
+      unsigned wb = 0;
+      for (int w = 0; w < (int)(threadIdx.x >> 5); ++w) wb += wsum[w];
+      const unsigned ex = wb + incl - (c0 + c1);
+      if (b0 < nb) {
+        lbase[b0] = ex;
+        if (c0) base[b0] = atomicAdd(pcur + b0, c0);
+      }
+      if (b0 + 1 < nb) {
+        lbase[b0 + 1] = ex + c0;
+        if (c1) base[b0 + 1] = atomicAdd(pcur + b0 + 1, c1);
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kPer; ++k)
+      if (row[k] >= 0) {
+        const unsigned b = (unsigned)row[k] >> shift;
+        const unsigned slot = lbase[b] + rank[k];
+        stage[slot] = make_int2(row[k], cols[k]);
+        sbk[slot] = (unsigned short)b;
+      }
+    __syncthreads();
+    // runs of one bucket are contiguous in the stage and in the output: coalesced stores
+    for (unsigned i = threadIdx.x; i < j1 - j0; i += blockDim.x) {
+      const unsigned b = sbk[i];
+      pairs[base[b] + (i - lbase[b])] = stage[i];
+    }
+    __syncthreads();
+  }
+}
+
+// Ordered passes over the bucketed pairs: chunks are handed out in order, so
+// the grid's working set is one or two buckets wide.
+template <bool kScatter>
+__global__ void __launch_bounds__(256) pair_pass_kernel(const int2* pairs, unsigned E, unsigned* ticket,
+                                                        unsigned* cursor, int* radj) {
+  __shared__ unsigned chunk;
+  constexpr int kPer = kPairChunk / 256;
+  for (;;) {
+    if (threadIdx.x == 0) chunk = atomicAdd(ticket, 1u);
+    __syncthreads();
+    const unsigned long long j0 = (unsigned long long)chunk * kPairChunk;
+    __syncthreads();
+    if (j0 >= E) break;
+    int2 rc[kPer];
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const unsigned long long j = j0 + k * 256 + threadIdx.x;
+      rc[k] = j < E ? pairs[j] : make_int2(-1, 0);
+    }
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      if (rc[k].x < 0) continue;
+      if (kScatter) radj[atomicAdd(cursor + rc[k].x, 1u)] = rc[k].y;
+      else atomicAdd(cursor + rc[k].x, 1u);
+    }
+  }
+}
+
