@@ -26,10 +26,11 @@ cores, so it times as many steps as fit its --ref-budget-s (reported as
 
 Multi-GPU (torchrun, N>1): by default the workload is 1-D partitioned by
 column across the ranks (strong scaling, paper_1303_1379_b200/partition.py):
-each rank expands its own columns and the per-level frontier records are
-exchanged over peer memory; ALTERNATE/FIX run on rank 0 and the matching is
-broadcast. --mode replicas instead solves one independent replica per rank
-(weak scaling, no collective). Timing is the max over ranks.
+the multi-GPU engine runs the whole driver as one persistent launch per rank,
+claims resolved at the row's owner and winner columns stored into their
+owner's inbox over peer memory (CUDA IPC / NVLink), the level barrier
+spanning the team. --mode replicas instead solves one independent replica per
+rank (weak scaling, no collective). Timing is the max over ranks.
 """
 from __future__ import annotations
 
@@ -321,25 +322,26 @@ def run_reference_arm(args):
 
 
 def run_partitioned(args):
-    """N ranks, one column slice each; value = graph edges / time."""
+    """N ranks, one GPU each (torchrun), one column slice each:
+    the multi-GPU engine (csrc/bm_mg.cu) runs the whole driver as one launch
+    per rank over peer memory. value = graph edges / time (max over ranks)."""
     import numpy as np
     import torch
     import torch.distributed as dist
     import paper_1303_1379_b200 as bm
-    from paper_1303_1379_b200.partition import Exchange, GpuPartition, PartitionedMatcher
+    from paper_1303_1379_b200.partition import DistTransport, GpuRank, PartitionedMatcher
 
     world, rank, local = dist_env()
     divert_stdout()
-    local = local % max(1, torch.cuda.device_count())  # gloo tests run several ranks on one GPU
+    ndev = max(1, torch.cuda.device_count())
+    local = local % ndev
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    # the process group is the control plane (setup, per-phase broadcast); NCCL needs one GPU per rank
-    backend = "nccl" if args.exchange != "gloo" and world <= torch.cuda.device_count() else "gloo"
     if not dist.is_initialized():
         if world == 1:
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
             os.environ.setdefault("MASTER_PORT", "29533")
-        dist.init_process_group(backend, rank=rank, world_size=world)
+        dist.init_process_group("gloo", rank=rank, world_size=world)  # setup messages only (no data path)
     t_gen = time.perf_counter()
     g, known = build_graph(args.config, args.scale_div)
     if known is None:
@@ -348,65 +350,85 @@ def run_partitioned(args):
     t_gen = time.perf_counter() - t_gen
     E = g.num_edges()
     shortest, kernel, improved = ALGOS[args.algo]
-    be = GpuPartition(local, rank, world)
-    pm = PartitionedMatcher(be, Exchange())
-    exchange = args.exchange
-    if exchange == "p2p":  # fused exchange over peer memory; fall back to the NCCL all-gather if unavailable
-        try:
-            pm.upload(g, p2p=True)
-        except Exception as ex:  # e.g. no CUDA IPC in this container
-            print(f"P2P exchange unavailable ({ex}); using the NCCL all-gather", file=sys.stderr)
-            exchange = "nccl"
-            pm.upload(g)
-    else:
-        pm.upload(g)
+    kernel = bm.BfsKernel(kernel)
+    # ranks sharing a device (more ranks than GPUs) cannot co-run their persistent kernels across processes
+    if world > ndev:
+        raise SystemExit(f"{world} ranks on {ndev} GPU(s): the multi-GPU engine needs one GPU per rank")
+    x = DistTransport()
+    rk = GpuRank(local, rank, world)
     stream = torch.cuda.current_stream(dev)
+    rk.set_stream(stream.cuda_stream)
+    pm = PartitionedMatcher(rk, x)
+    pulled = args.bottom_up != "off"
+    t_up = time.perf_counter()
+    pm.upload(g, row_index=pulled)
+    t_up = time.perf_counter() - t_up
+    bu = {"auto": "auto", "on": "on", "off": "off"}[args.bottom_up]
 
     def step():
-        return pm.match(init, shortest=shortest, kernel=bm.BfsKernel(kernel))
+        return pm.match(init, shortest=shortest, kernel=kernel, improved=improved, bottom_up=bu)
 
     res = step()
+    m = pm.gather()
     parity_ok = known is None or res.cardinality == known
     for _ in range(args.warmup):
         step()
-    torch.cuda.synchronize(dev)
-    dist.barrier()
-    torch.cuda.synchronize(dev)
-    ms, cards = [], []
-    launches = 0
+    x.barrier()
+    kms, cards, ph = [], [], []
     sampler = ClockSampler(local)
     with sampler:
         for _ in range(args.steps):
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            r = step()
-            e1.record(stream)
-            e1.synchronize()
-            ms.append(e0.elapsed_time(e1))
+            r = step()  # load + barrier + launch + finish; the kernel time is the run
+            kms.append(r.kernel_ms)
             cards.append(r.cardinality)
-            launches += r.stats.get("launches", 0)
+            ph.append(r.phases)
             parity_ok = parity_ok and (known is None or r.cardinality == known)
-    torch.cuda.synchronize(dev)
-    dist.barrier()
-    t = torch.tensor([statistics.mean(ms)], dtype=torch.float64, device=dev if backend == "nccl" else "cpu")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    t_ms = float(t[0])
-    st = be.stats()
-    tot = torch.tensor([st["edges_traversed"], st["columns_scanned"]], dtype=torch.int64,
-                       device=dev if backend == "nccl" else "cpu")
-    dist.all_reduce(tot)
+    t_ms = x.allreduce_max(statistics.mean(kms))
+    trav = x.allreduce_sum(sum(c.edges_traversed for c in r.counters))
+    cexp = x.allreduce_sum(sum(c.columns_scanned for c in r.counters))
+    nvis = x.allreduce_sum(sum(c.columns_visited for c in r.counters))
+    steps_walk = x.allreduce_sum(sum(c.walk_steps for c in r.counters))
+
+    # end to end through the public API: each rank uploads its slice from pinned host memory,
+    # matches, and reads its rows and columns back
+    e2e = None
+    if not args.no_e2e:
+        lo, hi = pm.cb[rank], pm.cb[rank + 1]
+        cx = torch.from_numpy(np.ascontiguousarray(g.cxadj[lo:hi + 1] - g.cxadj[lo])).pin_memory()
+        adj = torch.from_numpy(np.ascontiguousarray(g.cadj[int(g.cxadj[lo]):int(g.cxadj[hi])])).pin_memory()
+        e_ms = []
+        for i in range(args.warmup + args.steps):
+            x.barrier()
+            t0 = time.perf_counter()
+            pm.upload(g, row_index=pulled, slices=(cx.numpy(), adj.numpy()))
+            pm.match(init, shortest=shortest, kernel=kernel, improved=improved, bottom_up=bu)
+            rs, cs = rk.download()
+            t1 = time.perf_counter()
+            if i >= args.warmup:
+                e_ms.append(1e3 * (t1 - t0))
+        e_max = x.allreduce_max(statistics.mean(e_ms))
+        h2d = x.allreduce_sum(int(cx.numel()) * 8 + int(adj.numel()) * 4 + 4 * ((pm.rb[rank + 1] - pm.rb[rank]) +
+                                                                             (hi - lo)))
+        d2h = 4 * (g.nr + g.nc)
+        e2e = {"value": E / (e_max / 1e3), "unit": "edges/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "ms_per_step": e_max, "note": "wall clock per rank (max over ranks): slice upload from host, "
+                                             "row index, initial matching, the run, result download"}
     if rank == 0:
-        m = be.download()
-        eng = bm.Engine(local)  # GPU Berge certificate of the partitioned result
+        eng = bm.Engine(local)  # GPU Berge certificate of the gathered result
         eng.upload(g)
         viol, ismax, vcard = eng.verify(g, m)
         g_ok = bool(viol == 0 and ismax and vcard == res.cardinality)
         del eng
-        parity_ok = parity_ok and bool(g_ok)
-        trav = int(tot[0])  # stats cover the last run (match() resets them)
-        cexp = int(tot[1])
-        b_units = 12 * trav + 28 * cexp
+        parity_ok = parity_ok and g_ok
+        cpu = None
+        if not args.no_cpu_baseline:
+            cr = cpu_reference_run(g, init)
+            cpu = {"value": E / cr["seconds"], "unit": "edges/s", "cores": cr["cores"], "kind": cr["kind"],
+                   "sample": f"one full {args.config} run ({E} edges) of apfb-wr-ct on the host",
+                   "seconds": cr["seconds"], "cardinality": cr["cardinality"]}
+            parity_ok = parity_ok and cr["cardinality"] == res.cardinality
+        wr = 1 if kernel == bm.BfsKernel.GpubfsWr else 0
+        b_units = 12 * trav + (20 + 8 * wr) * cexp + (8 + 4 * wr) * nvis + 20 * steps_walk
         peak, peak_src = measured_peak()
         achieved = b_units / (t_ms / 1e3) / 1e9
         emit({
@@ -414,23 +436,22 @@ def run_partitioned(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_ms, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "int32", "data": data_kind(),
             "config": workload_config(args, g),
-            "algorithm": f"{args.algo}-b200-partitioned",
-            "parallelism": f"column-partition x{world}, per-level record exchange: "
-                           + ("fused P2P stores into every rank's receive slabs (CUDA IPC / NVLink)"
-                              if exchange == "p2p" else f"all-gather ({backend})"),
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": None, "peak_source": peak_src,
-                         "kernel": "bm_part_* level kernels + exchange (whole step)",
+            "algorithm": f"{args.algo}-b200-multigpu",
+            "parallelism": f"1-D column partition x{world}: one persistent launch per rank, claims at the row's "
+                           "owner and winners into the column's owner over peer memory (CUDA IPC / NVLink)",
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak * world, "unit": "GB/s",
+                         "frac": achieved / (peak * world), "traffic": None, "peak_source": peak_src + f" x {world}",
+                         "kernel": "bmg::driver_kernel (persistent, whole run, every rank)",
                          "algorithmic_bytes_per_launch": b_units},
-            "cpu_baseline": None, "e2e": None,
-            "gpu_launches": launches,
+            "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": args.steps * world,
             "clocks": sampler.summary(),
             "time_to_max_matching_ms": t_ms, "cardinality": cards[-1] if cards else res.cardinality,
-            "phases": res.phases, "bfs_levels": res.levels, "records_exchanged": res.records_exchanged,
+            "phases": ph, "bfs_levels": res.levels,
             "parity": {"known_answer": known, "gpu_verify": g_ok, "ok": bool(parity_ok)},
-            "generation_s": t_gen,
+            "generation_s": t_gen, "upload_s": t_up,
         })
-    dist.barrier()
+    x.barrier()
     dist.destroy_process_group()
     return 0
 
@@ -688,9 +709,6 @@ def main():
                          "run after an upload): auto = the engine decides per graph (BM_BU_AUTO)")
     ap.add_argument("--mode", choices=["auto", "single", "partition", "replicas"], default="auto",
                     help="auto: single GPU at N=1, column partition at N>1")
-    ap.add_argument("--exchange", choices=["p2p", "nccl", "gloo"], default="p2p",
-                    help="partition mode: p2p = the expand kernel writes every rank's receive slab over peer "
-                         "memory (falls back to nccl if IPC is unavailable); nccl = all-gather; gloo = host-staged")
     ap.add_argument("--graph", default=None,
                     help="a Matrix Market (.mtx) or binary CSC (.bcsc) file to use instead of --config")
     args = ap.parse_args()

@@ -269,6 +269,48 @@ bm_status   bm_verify(bm_handle* h, const int32_t* rmatch, const int32_t* cmatch
 bm_status   bm_permute_random(bm_handle* h, const int32_t* cperm, const int32_t* rperm);
 bm_status   bm_download_csc(bm_handle* h, int64_t* cxadj, int32_t* cadj);
 
+/* ---- multi-GPU engine: one persistent kernel per rank over peer memory ----
+ * (the reference has no multi-device path, its only
+ * parallelism is the emulated grid, kernel_grid.hpp:161-222.)
+ * 1-D partition: rank q owns columns [cb[q], cb[q+1]) with their CSC slice,
+ * cmatch and root marks, and rows [rb[q], rb[q+1]) with their row state and
+ * (pulled levels) their slice of the row index. The whole APFB/APsB driver
+ * (run_driver, gpu_match.cpp:306-376) runs as ONE cooperative launch per rank:
+ * claims are system-scope atomics at the row's owner, winner columns are
+ * stored into their owner's inbox, and the level barrier spans the team,
+ * all over peer memory (CUDA IPC / NVLink; plain pointers for ranks of one
+ * process). No host round trip per level, no collective on the data path.
+ * Protocol (every rank):
+ *   bm_mg_create(device, rank, world, share)   share = ranks on this device
+ *   bm_mg_upload(slice)                        bounds from bm_mg_partition
+ *   bm_mg_export(blob) -> all-gather blobs -> bm_mg_import(all blobs)
+ *   [bm_mg_row_index_begin, host barrier, bm_mg_row_index_end]  pulled levels
+ *   bm_mg_load_matching(own rows, own columns), host barrier
+ *   bm_mg_launch (every rank) then bm_mg_finish  (= bm_mg_run)
+ *   bm_mg_download(own rows, own columns)
+ * Status codes as for the single-GPU engine; BM_ERR_BOUND_EXCEEDED for the
+ * nc + 1 bound (gpu_match.cpp:313-320). */
+typedef struct bm_mg bm_mg;
+bm_status   bm_mg_partition(int32_t n, int32_t world, int32_t* bounds /* world + 1 */);
+bm_status   bm_mg_create(int32_t device, int32_t rank, int32_t world, int32_t share, bm_mg** out);
+bm_status   bm_mg_destroy(bm_mg* h);
+bm_status   bm_mg_set_stream(bm_mg* h, void* stream);
+/* cxadj[cb[rank+1]-cb[rank]+1] rebased to 0, cadj its rows (global ids) */
+bm_status   bm_mg_upload(bm_mg* h, int32_t nc, int32_t nr, int64_t e_total, const int32_t* cb,
+                         const int32_t* rb, const int64_t* cxadj, const int32_t* cadj);
+bm_status   bm_mg_blob_size(int64_t* bytes);
+bm_status   bm_mg_export(bm_mg* h, void* blob);
+bm_status   bm_mg_import(bm_mg* h, const void* blobs /* world blobs, rank order */);
+bm_status   bm_mg_row_index_begin(bm_mg* h);
+bm_status   bm_mg_row_index_end(bm_mg* h);
+bm_status   bm_mg_load_matching(bm_mg* h, const int32_t* rmatch_slice, const int32_t* cmatch_slice);
+bm_status   bm_mg_launch(bm_mg* h, const bm_match_opts* opts);
+bm_status   bm_mg_finish(bm_mg* h, int64_t* cardinality, bm_counters* counters /* this rank's work */);
+bm_status   bm_mg_run(bm_mg* h, const bm_match_opts* opts, int64_t* cardinality, bm_counters* counters);
+bm_status   bm_mg_download(bm_mg* h, int32_t* rmatch_slice, int32_t* cmatch_slice);
+bm_status   bm_mg_kernel_time(bm_mg* h, double* ms);
+bm_status   bm_mg_info(bm_mg* h, int64_t* local_edges, int64_t* row_index_edges, int32_t* pulled_capable);
+
 /* ---- 1-D column partition over several GPUs --------------
  * The reference has no multi-device path (its only parallelism is the
  * emulated grid, kernel_grid.hpp:161-222). One bm_part per rank (process,

@@ -93,6 +93,9 @@ __device__ __forceinline__ void st_rlx(unsigned* p, unsigned v) {
 __device__ __forceinline__ void st_plain(int* p, int v) {
   asm volatile("st.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+__device__ __forceinline__ void st_plain(int2* p, int2 v) {
+  asm volatile("st.global.v2.b32 [%0], {%1,%2};" ::"l"(p), "r"(v.x), "r"(v.y) : "memory");
+}
 __device__ __forceinline__ void st_plain(int4* p, int4 v) {
   asm volatile("st.global.v4.b32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
                "r"(v.w)

@@ -288,8 +288,8 @@ bm_status build_transpose(bm_handle* h, int nc, int nr, long long E) {
     bucket_hist_kernel<<<grid, 256, 0, h->stream>>>(h->adj, (unsigned)E, shift, nb, bcount);
     bucket_base_kernel<<<1, 32, 0, h->stream>>>(bcount, nb, pcur);
     const int pa = (int)std::max<long long>(1, std::min<long long>((long long)grid, (E + kTpChunk - 1) / kTpChunk));
-    bucket_partition_kernel<<<pa, 256, 0, h->stream>>>(h->offs, h->adj, nc, (unsigned)E, shift, nb, pcur, pairs);
-    pair_pass_kernel<false><<<grid, 256, 0, h->stream>>>(pairs, (unsigned)E, tickets, h->rcursor, nullptr);
+    bucket_partition_kernel<<<pa, 256, 0, h->stream>>>(h->offs, h->adj, 0, nc, (unsigned)E, shift, nb, pcur, pairs);
+    pair_pass_kernel<false><<<grid, 256, 0, h->stream>>>(pairs, (unsigned)E, tickets, h->rcursor, nullptr, 0, nr);
     size_t tmp_bytes = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, h->rcursor, h->roffs, nr + 1, h->stream);
     // kept with the handle too: a stream-ordered allocation here cost 3-115 ms per build
@@ -298,7 +298,7 @@ bm_status build_transpose(bm_handle* h, int nc, int nr, long long E) {
     cub::DeviceScan::ExclusiveSum(h->tp_tmp, tmp_bytes, h->rcursor, h->roffs, nr + 1, h->stream);
     BM_CUDA(cudaMemcpyAsync(h->rcursor, h->roffs, sizeof(unsigned) * ((size_t)nr + 1), cudaMemcpyDeviceToDevice,
                             h->stream));
-    pair_pass_kernel<true><<<grid, 256, 0, h->stream>>>(pairs, (unsigned)E, tickets + 1, h->rcursor, h->radj);
+    pair_pass_kernel<true><<<grid, 256, 0, h->stream>>>(pairs, (unsigned)E, tickets + 1, h->rcursor, h->radj, 0, nr);
     BM_CUDA(cudaGetLastError());
   }
   h->bu_built = true;

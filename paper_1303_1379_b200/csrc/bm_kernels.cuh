@@ -114,6 +114,7 @@ struct alignas(128) Ctrl {
   Slot roots;
   Slot mat[2];  // materialize reservations, by level parity (never the level's own slot: slow CTAs
                 // may still be reading its count when the next level starts)
+  Slot rootp;   // multi-GPU: next-phase roots routed here by other ranks' FIX, as (c, c) pairs in P
   unsigned n_ep;
   unsigned pad1[31];
   unsigned n_log;
@@ -281,16 +282,12 @@ struct BuCand {
 constexpr int kCandCap = 160;  // per-warp queue: < 32 left over + one screened chunk of 128 rows
 
 struct Smem {
-  union {  // a top-down window, or a bottom-up candidate stage (never both at once)
+  union {  // a top-down window (a pulled level keeps its candidate queues in wbuf)
     struct {
       unsigned pre[kWin + 1];      // window: raw edge prefix of each entry, then the live-edge prefix
       int col[kWin];
       int root[kWin];
       unsigned beg[kWin];          // first live adjacency index of each entry in this window
-    };
-    struct {
-      int bcand[4 * kThreads];     // bottom-up: candidate rows of a sweep step (per warp) ...
-      int bcandv[4 * kThreads];    // ... and their rmatch values
     };
   };
   unsigned wtot[kThreads / 32];
@@ -303,6 +300,16 @@ struct Smem {
   unsigned blk_ep;
   unsigned nw;                          // winners staged in wbuf for the current window
   int2 wbuf[kWBuf];                     // (column, root) claimed in the current window
+#if BM_MG
+  // level bookkeeping of every rank (thread 0 refreshes it after each barrier)
+  unsigned mg_ls[kMaxRanks];    // first entry of the current level in the rank's F / P
+  unsigned mg_n[kMaxRanks];     // entries of the current level
+  unsigned mg_nn[kMaxRanks];    // entries of the next level (pushed into the rank's inbox)
+  unsigned mg_cnt[kMaxRanks];   // routed flush: winners per destination ...
+  unsigned mg_base[kMaxRanks];  // ... their slots in the destination's inbox ...
+  unsigned mg_cur[kMaxRanks];   // ... and the cursor within them
+  unsigned long long mg_tot[4];  // team sums (entries, edges, ...) of the last refresh
+#endif
 };
 
 // Warp-reduce a per-thread count and add it to the CTA's shared counter. Must
@@ -323,7 +330,13 @@ __device__ __forceinline__ void flush_count(Smem& sm, int idx, unsigned v) {
 // atomics, NVLink) and releases its own grid only when every rank has arrived;
 // system-scope fences make each CTA's stores to peer memory visible first.
 #if BM_MG
-#define BM_FENCE() __threadfence_system()
+#define BM_FENCE()                      \
+  do {                                  \
+    if (p.world > 1)                    \
+      __threadfence_system();           \
+    else                                \
+      __threadfence();                  \
+  } while (0)
 #else
 #define BM_FENCE() __threadfence()
 #endif
@@ -396,6 +409,24 @@ __device__ __noinline__ void grid_sync(const Params& p) {
 }
 
 __device__ __forceinline__ bool is_leader() { return blockIdx.x == 0 && threadIdx.x == 0; }
+
+// "An augmenting path was found in this phase" (by parity): team-wide in the
+// multi-GPU build (rank 0's team block), per launch otherwise.
+__device__ __forceinline__ unsigned* path_flag_of(const Params& p, int pf) {
+#if BM_MG
+  return &p.team->path_found[pf];
+#else
+  return &p.ctl->path_found[pf];
+#endif
+}
+// Multi-GPU teams of more than one rank route every winner to its owner.
+__device__ __forceinline__ bool routed(const Params& p) {
+#if BM_MG
+  return p.world > 1;
+#else
+  return false;
+#endif
+}
 
 __device__ __forceinline__ long long clk() { return clock64(); }
 
@@ -553,7 +584,11 @@ __device__ __forceinline__ bool root_dead(const Params& p, int root) {
   return (ld_rlx(p.dead + (root >> 5)) >> (root & 31)) & 1u;
 }
 __device__ __forceinline__ void mark_dead(const Params& p, int root) {
+#if BM_MG
+  for (int q = 0; q < p.world; ++q) atomicOr_system(p.peer[q].dead + (root >> 5), 1u << (root & 31));  // every replica
+#else
   atomicOr(p.dead + (root >> 5), 1u << (root & 31));
+#endif
 }
 
 // Pushes the winners staged in sm.wbuf as next-level frontier entries: one
@@ -620,6 +655,68 @@ __device__ __forceinline__ void flush_pairs(const Params& p, Smem& sm, unsigned 
   __syncthreads();
   if (threadIdx.x == 0) sm.nw = 0;
 }
+
+#if BM_MG
+__device__ __forceinline__ unsigned lanemask_lt() { return (1u << lane_id()) - 1u; }
+// Multi-GPU: routes the winners staged in sm.wbuf to their columns' owners —
+// per destination one slot reservation on the owner's level counter, then the
+// pairs are stored straight into the owner's inbox (peer memory, NVLink).
+// CTA-uniform call.
+__device__ __forceinline__ void flush_pairs_mg(const Params& p, Smem& sm, int out_slot, unsigned long long pol) {
+  const unsigned nw = sm.nw;
+  if (!nw) return;
+  if (threadIdx.x < kMaxRanks) {
+    sm.mg_cnt[threadIdx.x] = 0;
+    sm.mg_cur[threadIdx.x] = 0;
+  }
+  __syncthreads();
+  for (unsigned j = threadIdx.x; j < nw; j += kThreads) atomicAdd(&sm.mg_cnt[owner_col(p, sm.wbuf[j].x)], 1u);
+  __syncthreads();
+  if (threadIdx.x < (unsigned)p.world && sm.mg_cnt[threadIdx.x])
+    sm.mg_base[threadIdx.x] = (unsigned)(atomicAdd_system(&p.peer[threadIdx.x].ctl->lvl[out_slot].packed,
+                                                          (unsigned long long)sm.mg_cnt[threadIdx.x] << 33) >> 33);
+  __syncthreads();
+  for (unsigned j = threadIdx.x; j < nw; j += kThreads) {
+    const int2 w = sm.wbuf[j];
+    const int q = owner_col(p, w.x);
+    const unsigned i = atomicAdd(&sm.mg_cur[q], 1u);
+    st_stream(p.peer[q].P + sm.mg_ls[q] + sm.mg_n[q] + sm.mg_base[q] + i, w, pol);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) sm.nw = 0;
+}
+// The same for one warp's stage of nwin winners (pulled levels); warp-uniform call.
+__device__ __forceinline__ void warp_flush_mg(const Params& p, const Smem& sm, const int2* wst, unsigned nwin,
+                                              int out_slot, unsigned long long pol) {
+  const unsigned lane = lane_id();
+  unsigned cnt = 0;  // lane d: winners for destination d
+  for (unsigned i0 = 0; i0 < nwin; i0 += 32) {
+    const unsigned i = i0 + lane;
+    const int q = i < nwin ? owner_col(p, wst[i].x) : -1;
+    for (int d = 0; d < p.world; ++d) {
+      const unsigned m = __ballot_sync(kFull, q == d);
+      if (lane == (unsigned)d) cnt += __popc(m);
+    }
+  }
+  unsigned base = 0;
+  if (lane < (unsigned)p.world && cnt)
+    base = (unsigned)(atomicAdd_system(&p.peer[lane].ctl->lvl[out_slot].packed, (unsigned long long)cnt << 33) >> 33);
+  unsigned run = 0;
+  for (unsigned i0 = 0; i0 < nwin; i0 += 32) {
+    const unsigned i = i0 + lane;
+    const int2 w = i < nwin ? wst[i] : make_int2(-1, 0);
+    const int q = w.x >= 0 ? owner_col(p, w.x) : -1;
+    unsigned pos = 0;
+    for (int d = 0; d < p.world; ++d) {
+      const unsigned m = __ballot_sync(kFull, q == d);
+      const unsigned b = __shfl_sync(kFull, base + run, d);
+      if (q == d) pos = b + __popc(m & lanemask_lt());
+      if (lane == (unsigned)d) run += __popc(m);
+    }
+    if (q >= 0) st_stream(p.peer[q].P + sm.mg_ls[q] + sm.mg_n[q] + pos, w, pol);
+  }
+}
+#endif
 
 // Turns the n pairs of a level, P[ls, ls + n), into edge-tiled frontier entries
 // F[ls, ls + n) plus their granule index, for a level that is pushed.
@@ -730,142 +827,9 @@ __device__ __forceinline__ void bu_prep(const Params& p, Smem& sm, const int4* F
   flush_count(sm, kStCexp, live);
 }
 
-template <bool WR, bool IMP>
-__device__ __forceinline__ void bu_sweep(const Params& p, Smem& sm, unsigned out_base, Slot* out, int lv, int pf) {
-  // Warp-synchronous: per CTA step every warp (1) screens kBuRows rows per lane
-  // with independent loads and compacts its candidates (unvisited matched rows
-  // and free rows) into a warp-private stage; (2) each candidate scans its
-  // columns until the first frontier member. Winners go to the CTA's wbuf and
-  // are flushed (3) between steps; that is the only CTA-wide synchronisation.
-  constexpr int kBuRows = 4;
-  constexpr int kWarpRows = 32 * kBuRows;              // rows a warp screens per step
-  constexpr int kStepRows = kThreads * kBuRows;        // rows a CTA screens per step
 #ifndef BM_BU_PROBE
 #define BM_BU_PROBE 4
 #endif
-  constexpr int kBuProbe = BM_BU_PROBE;
-  const unsigned* fb = p.fbit[lv & 1];
-  const unsigned long long pol = policy_evict_first();
-  unsigned* const path_flag = &p.ctl->path_found[pf];
-  unsigned c_trav = 0, c_nvis = 0, c_rows = 0;
-  const unsigned warp = threadIdx.x >> 5, lane = lane_id();
-  int* const wrow = sm.bcand + warp * kWarpRows;   // this warp's stage
-  int* const wval = sm.bcandv + warp * kWarpRows;
-  if (threadIdx.x == 0) sm.nw = 0;
-  __syncthreads();
-  unsigned step = 0;
-  for (unsigned long long b = (unsigned long long)blockIdx.x * kStepRows; b < (unsigned long long)p.nr;
-       b += (unsigned long long)gridDim.x * kStepRows) {
-    // (1) screen and compact (warp-private)
-    const unsigned long long wb = b + (unsigned long long)warp * kWarpRows;
-    int v[kBuRows];
-#pragma unroll
-    for (int k = 0; k < kBuRows; ++k) {
-      const unsigned long long r = wb + (unsigned long long)k * 32 + lane;
-      v[k] = r < (unsigned long long)p.nr ? ld_cg(RM(p, r)) : -3;
-    }
-    unsigned ncand = 0;
-#pragma unroll
-    for (int k = 0; k < kBuRows; ++k) {
-      const bool is_cand = (v[k] >= 0 && !(v[k] & kVisBit)) || v[k] == -1;
-      const unsigned m = __ballot_sync(kFull, is_cand);
-      if (is_cand) {
-        const unsigned slot = ncand + __popc(m & ((1u << lane) - 1));
-        wrow[slot] = (int)(wb + (unsigned long long)k * 32 + lane);
-        wval[slot] = v[k];
-      }
-      ncand += __popc(m);
-    }
-    __syncwarp();
-    // (2) resolve the warp's candidates, 32 at a time
-    for (unsigned t0 = 0; t0 < ncand; t0 += 32) {
-      bool win = false, ep = false;
-      int cw = 0, rootw = 0, rr = 0;
-      if (t0 + lane < ncand) {
-        rr = wrow[t0 + lane];
-        const int vv = wval[t0 + lane];
-        const unsigned j0 = ld_ro(p.roffs + rr), j1 = ld_ro(p.roffs + rr + 1);
-        c_rows++;
-        // kBuProbe neighbours per step: their index loads and frontier-bit loads
-        // are independent, so a row that scans far waits kBuProbe x fewer round trips
-        bool done = false;
-        for (unsigned jb = j0; jb < j1 && !done; jb += kBuProbe) {
-          int cs[kBuProbe];
-          unsigned wd[kBuProbe];
-#pragma unroll
-          for (int k = 0; k < kBuProbe; ++k) cs[k] = jb + k < j1 ? ld_stream(p.radj + jb + k, pol) : -1;
-#pragma unroll
-          for (int k = 0; k < kBuProbe; ++k)
-            wd[k] = cs[k] >= 0 ? ld_ca(reinterpret_cast<const int*>(fb) + (cs[k] >> 5)) : 0u;
-#pragma unroll
-          for (int k = 0; k < kBuProbe; ++k) {
-            const int c = cs[k];
-            if (done || c < 0) continue;
-            c_trav++;
-            if (!((wd[k] >> (c & 31)) & 1)) continue;
-            const int root = ld_cg(p.croot + c);
-            if (vv >= 0) {  // matched row: its column joins the frontier below c's tree
-              st_plain(RM(p, rr), vv | kVisBit);
-              st_plain(PR(p, rr), c);
-              win = true;
-              cw = vv;
-              rootw = root;
-              done = true;
-              continue;
-            }
-            // free row: an endpoint of c's tree
-            const bool one = WR && p.ep_one;
-            if (one && root_dead(p, root)) continue;
-            bool mine = true;
-            if (one) mine = atomicCAS(p.bfs + root, kStartLevel, IMP ? -rr : kFoundMark) == kStartLevel;
-            else if (WR) st_rlx(p.bfs + root, IMP ? -rr : kFoundMark);
-            if (!mine) continue;  // that tree already holds an endpoint: try another neighbour
-            if (WR) mark_dead(p, root);
-            st_rlx(RM(p, rr), -2);
-            st_plain(PR(p, rr), c);
-            ep = true;
-            if (ld_rlx(path_flag) == 0u) st_rlx(path_flag, 1u);
-            done = true;
-          }
-        }
-      }
-      c_nvis += win ? 1u : 0u;
-      stage_winner(sm, win, cw, rootw);  // one shared atomic per warp
-      {  // endpoints: rare, warp-aggregated global append
-        const unsigned mine = ep ? 1u : 0u;
-        const unsigned incl = warp_incl_scan(mine);
-        const unsigned tot = __shfl_sync(kFull, incl, 31);
-        if (tot) {
-          unsigned eb = 0;
-          if (lane == 31) eb = atomicAdd(&p.ctl->n_ep, tot);
-          eb = __shfl_sync(kFull, eb, 31) + incl - mine;
-          if (ep) st_plain(p.EP + eb, rr);
-        }
-      }
-    }
-    __syncwarp();  // the stage is reused by the next step
-    // (3) every kFlushSteps steps (at most kFlushSteps * kStepRows winners in between,
-    // which wbuf holds): flush when the next kFlushSteps steps might not fit
-#ifndef BM_BU_FLUSH_STEPS
-#define BM_BU_FLUSH_STEPS 4
-#endif
-    constexpr unsigned kFlushSteps = BM_BU_FLUSH_STEPS;
-    static_assert(kFlushSteps * kStepRows <= kWBuf, "wbuf must hold the winners between flush checks");
-    if (++step % kFlushSteps == 0) {
-      __syncthreads();
-      if (sm.nw > kWBuf - kFlushSteps * kStepRows) {
-        flush_pairs(p, sm, out_base, out, pol);
-        __syncthreads();  // the reset of sm.nw lands before the next stage_winner
-      }
-    }
-  }
-  __syncthreads();
-  flush_pairs(p, sm, out_base, out, pol);
-  flush_count(sm, kStTrav, c_trav);
-  flush_count(sm, kStNvis, c_nvis);
-  flush_count(sm, kStRowsPulled, c_rows);
-}
-
 // Warp-autonomous pulled level. Every warp owns chunks of 128 consecutive rows
 // (grid-stride over the warps of the grid) and keeps a queue of candidate rows
 // in shared memory: screening a chunk reads the rows' state and their row-index
@@ -875,8 +839,25 @@ __device__ __forceinline__ void bu_sweep(const Params& p, Smem& sm, unsigned out
 // queued candidate in the following round, so a warp never waits for its
 // slowest row, and no CTA-wide barrier is needed — winners are staged per warp
 // in its slice of wbuf and flushed with one reservation per warp.
+#if BM_MG
+// Multi-GPU: after bu_prep, each rank copies the words of its own columns
+// (column ranges are 32-aligned) into every peer's replica of the bitmap.
+__device__ __forceinline__ void bu_share(const Params& p, int lv) {
+  if (p.col_lo >= p.col_hi) return;  // owns no column (the last word belongs to the rank that ends at nc)
+  const unsigned w0 = (unsigned)p.col_lo >> 5, w1 = ((unsigned)p.col_hi + 31) >> 5;
+  const unsigned* src = p.fbit[lv & 1];
+  const unsigned long long off = (unsigned long long)(lv & 1) * p.nfbit_words;
+  for (unsigned long long k = w0 + global_thread(); k < w1; k += global_threads()) {
+    const unsigned v = (unsigned)ld_cg(reinterpret_cast<const int*>(src) + k);
+    for (int q = 0; q < p.world; ++q)
+      if (q != p.rank) st_plain(reinterpret_cast<int*>(p.peer[q].fbit + off) + k, (int)v);
+  }
+}
+#endif
+
 template <bool WR, bool IMP>
-__device__ __forceinline__ void bu_sweep_q(const Params& p, Smem& sm, unsigned out_base, Slot* out, int lv, int pf) {
+__device__ __forceinline__ void bu_sweep_q(const Params& p, Smem& sm, unsigned out_base, Slot* out, int out_slot,
+                                           int lv, int pf) {
   constexpr int kWarps = kThreads / 32;
   constexpr unsigned kChunk = 128;
   constexpr unsigned kWStage = 128;  // winners staged per warp
@@ -886,12 +867,17 @@ __device__ __forceinline__ void bu_sweep_q(const Params& p, Smem& sm, unsigned o
   constexpr int kBuProbe = BM_BU_PROBE;
   const unsigned* fb = p.fbit[lv & 1];
   const unsigned long long pol = policy_evict_first();
-  unsigned* const path_flag = &p.ctl->path_found[pf];
+  unsigned* const path_flag = path_flag_of(p, pf);
+#if BM_MG
+  const unsigned long long rlo = (unsigned long long)p.row_lo, rhi = (unsigned long long)p.row_hi;  // own rows
+#else
+  const unsigned long long rlo = 0, rhi = (unsigned long long)p.nr;
+#endif
   unsigned c_trav = 0, c_nvis = 0, c_rows = 0;
   const unsigned warp = threadIdx.x >> 5, lane = lane_id();
   BuCand* const q = reinterpret_cast<BuCand*>(sm.wbuf) + warp * kCandCap;
   int2* const wst = reinterpret_cast<int2*>(reinterpret_cast<BuCand*>(sm.wbuf) + kWarps * kCandCap) + warp * kWStage;
-  const unsigned long long nchunks = ((unsigned long long)p.nr + kChunk - 1) / kChunk;
+  const unsigned long long nchunks = (rhi - rlo + kChunk - 1) / kChunk;
   const unsigned long long W = (unsigned long long)gridDim.x * kWarps;
   unsigned long long chunk = (unsigned long long)blockIdx.x * kWarps + warp;
   unsigned qh = 0, qt = 0;  // queued candidates q[qh, qt) (warp-uniform)
@@ -910,19 +896,19 @@ __device__ __forceinline__ void bu_sweep_q(const Params& p, Smem& sm, unsigned o
       if (lane < left) q[lane] = keep;
       qh = 0;
       qt = left;
-      const unsigned long long r0 = chunk * kChunk;
+      const unsigned long long r0 = rlo + chunk * kChunk;
       chunk += W;
       int v[4];
       unsigned o[4], onext;
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         const unsigned long long r = r0 + (unsigned long long)k * 32 + lane;
-        v[k] = r < (unsigned long long)p.nr ? ld_cg(RM(p, r)) : -3;
-        o[k] = r <= (unsigned long long)p.nr ? ld_ro(p.roffs + r) : 0u;  // roffs[nr] ends the last row
+        v[k] = r < rhi ? ld_cg(RML(p, r)) : -3;
+        o[k] = r <= rhi ? ld_ro(p.roffs + r) : 0u;  // roffs[rhi] ends the last row
       }
       {
         const unsigned long long r = r0 + 4 * 32;
-        onext = (lane == 0 && r <= (unsigned long long)p.nr) ? ld_ro(p.roffs + r) : 0u;
+        onext = (lane == 0 && r <= rhi) ? ld_ro(p.roffs + r) : 0u;
       }
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
@@ -978,10 +964,10 @@ __device__ __forceinline__ void bu_sweep_q(const Params& p, Smem& sm, unsigned o
         if (done || c < 0) continue;
         c_trav++;
         if (!((wd[k] >> (c & 31)) & 1)) continue;
-        const int root = ld_cg(p.croot + c);
+        const int root = ld_cg(CR(p, c));
         if (vv >= 0) {  // matched row: its column joins the frontier below c's tree
-          st_plain(RM(p, rr), vv | kVisBit);
-          st_plain(PR(p, rr), c);
+          st_plain(RML(p, rr), vv | kVisBit);
+          st_plain(PRL(p, rr), c);
           win = true;
           cw = vv;
           rootw = root;
@@ -992,12 +978,12 @@ __device__ __forceinline__ void bu_sweep_q(const Params& p, Smem& sm, unsigned o
         const bool one = WR && p.ep_one;
         if (one && root_dead(p, root)) continue;
         bool mine = true;
-        if (one) mine = atomicCAS(p.bfs + root, kStartLevel, IMP ? -rr : kFoundMark) == kStartLevel;
-        else if (WR) st_rlx(p.bfs + root, IMP ? -rr : kFoundMark);
+        if (one) mine = at_cas(BF(p, root), kStartLevel, IMP ? -rr : kFoundMark) == kStartLevel;
+        else if (WR) st_rlx(BF(p, root), IMP ? -rr : kFoundMark);
         if (!mine) continue;  // that tree already holds an endpoint: try another neighbour
         if (WR) mark_dead(p, root);
-        st_rlx(RM(p, rr), -2);
-        st_plain(PR(p, rr), c);
+        st_rlx(RML(p, rr), -2);
+        st_plain(PRL(p, rr), c);
         ep = true;
         if (ld_rlx(path_flag) == 0u) st_rlx(path_flag, 1u);
         done = true;
@@ -1013,10 +999,17 @@ __device__ __forceinline__ void bu_sweep_q(const Params& p, Smem& sm, unsigned o
       c_nvis += win ? 1u : 0u;
       if (nwin > kWStage - 32) {
         __syncwarp();
-        unsigned base = 0;
-        if (lane == 0) base = (unsigned)(atomicAdd(&out->packed, (unsigned long long)nwin << 33) >> 33);
-        base = __shfl_sync(kFull, base, 0) + out_base;
-        for (unsigned i = lane; i < nwin; i += 32) st_stream(p.P + base + i, wst[i], pol);
+#if BM_MG
+        if (routed(p)) {
+          warp_flush_mg(p, sm, wst, nwin, out_slot, pol);
+        } else
+#endif
+        {
+          unsigned base = 0;
+          if (lane == 0) base = (unsigned)(atomicAdd(&out->packed, (unsigned long long)nwin << 33) >> 33);
+          base = __shfl_sync(kFull, base, 0) + out_base;
+          for (unsigned i = lane; i < nwin; i += 32) st_stream(p.P + base + i, wst[i], pol);
+        }
         __syncwarp();
         nwin = 0;
       }
@@ -1033,10 +1026,17 @@ __device__ __forceinline__ void bu_sweep_q(const Params& p, Smem& sm, unsigned o
   }
   if (nwin) {
     __syncwarp();
-    unsigned base = 0;
-    if (lane == 0) base = (unsigned)(atomicAdd(&out->packed, (unsigned long long)nwin << 33) >> 33);
-    base = __shfl_sync(kFull, base, 0) + out_base;
-    for (unsigned i = lane; i < nwin; i += 32) st_stream(p.P + base + i, wst[i], pol);
+#if BM_MG
+    if (routed(p)) {
+      warp_flush_mg(p, sm, wst, nwin, out_slot, pol);
+    } else
+#endif
+    {
+      unsigned base = 0;
+      if (lane == 0) base = (unsigned)(atomicAdd(&out->packed, (unsigned long long)nwin << 33) >> 33);
+      base = __shfl_sync(kFull, base, 0) + out_base;
+      for (unsigned i = lane; i < nwin; i += 32) st_stream(p.P + base + i, wst[i], pol);
+    }
   }
   flush_count(sm, kStTrav, c_trav);
   flush_count(sm, kStNvis, c_nvis);
@@ -1049,7 +1049,7 @@ __device__ __forceinline__ void bu_sweep_q(const Params& p, Smem& sm, unsigned o
 template <bool WR, bool IMP, bool BU>
 __device__ __forceinline__ void expand_level(const Params& p, Smem& sm, int4* F, unsigned ls, unsigned n, unsigned T,
                              const unsigned* gin, unsigned* gout, Slot* in, Slot* out, int level, int pf,
-                             bool pairs_out, bool claim_store) {
+                             bool pairs_out, bool claim_store, int out_slot) {
   if (T == 0) return;
   const unsigned tid = threadIdx.x;
   unsigned c_trav = 0, c_cexp = 0, c_nvis = 0, c_entries = 0;
@@ -1060,7 +1060,7 @@ __device__ __forceinline__ void expand_level(const Params& p, Smem& sm, int4* F,
   const unsigned ET = (unsigned)per;
   const unsigned ntiles = (unsigned)((T + (unsigned long long)ET - 1) / ET);
   const unsigned out_base = ls + n;
-  unsigned* const path_flag = &p.ctl->path_found[pf];
+  unsigned* const path_flag = path_flag_of(p, pf);
 
   const unsigned long long pol = policy_evict_first();
 #ifndef BM_PF
@@ -1214,7 +1214,7 @@ __device__ __forceinline__ void expand_level(const Params& p, Smem& sm, int4* F,
               st_plain(RM(p, row[k]), c | kVisBit);
               old[k] = c;
             } else {
-              old[k] = atomicOr(RM(p, row[k]), kVisBit);
+              old[k] = at_or(RM(p, row[k]), kVisBit);
             }
           }
         }
@@ -1226,23 +1226,25 @@ __device__ __forceinline__ void expand_level(const Params& p, Smem& sm, int4* F,
           if (c >= 0) {
             if (!(old[k] & kVisBit)) {
               wins |= 1u << k;
-              if (BM_PF == 2) prefetch_l2(p.offs + c);  // the flush reads offs[c], offs[c+1]
-              if (BM_PF == 1) asm volatile("prefetch.global.L2 [%0];" ::"l"(p.offs + c));
+              if (!routed(p)) {  // (routed: the owner of c reads its offsets when it materializes the pair)
+                if (BM_PF == 2) prefetch_l2(p.offs + c);  // the flush reads offs[c], offs[c+1]
+                if (BM_PF == 1) asm volatile("prefetch.global.L2 [%0];" ::"l"(p.offs + c));
+              }
               st_stream(PR(p, row[k]), col, pol);
-              if (p.trace) st_plain(p.bfs + c, level + 1);
+              if (p.trace) st_plain(BF(p, c), level + 1);
             }
           } else if (c == -1) {
             // ONE_PER_TREE: a tree that already holds an endpoint leaves the row alone
             const bool one = WR && p.ep_one;
-            if ((!one || !root_dead(p, root)) && atomicCAS(RM(p, row[k]), -1, -2) == -1) {
+            if ((!one || !root_dead(p, root)) && at_cas(RM(p, row[k]), -1, -2) == -1) {
               bool mine = true;
               if (one) {
                 // the root's mark is the tree's endpoint slot: first CAS wins, a loser releases the row
-                mine = atomicCAS(p.bfs + root, kStartLevel, IMP ? -row[k] : kFoundMark) == kStartLevel;
+                mine = at_cas(BF(p, root), kStartLevel, IMP ? -row[k] : kFoundMark) == kStartLevel;
                 if (!mine) st_rlx(RM(p, row[k]), -1);
                 else mark_dead(p, root);
               } else if (WR) {
-                st_rlx(p.bfs + root, IMP ? -row[k] : kFoundMark);  // gpu_match.cpp:122-123
+                st_rlx(BF(p, root), IMP ? -row[k] : kFoundMark);  // gpu_match.cpp:122-123
                 mark_dead(p, root);
               }
               if (mine) {
@@ -1288,6 +1290,10 @@ __device__ __forceinline__ void expand_level(const Params& p, Smem& sm, int4* F,
         t_a = t;
       }
       // Flush the window's winners: one CTA reservation for all of them.
+#if BM_MG
+      if (routed(p)) flush_pairs_mg(p, sm, out_slot, pol);  // every winner goes to its column's owner as a pair
+      else
+#endif
       if (BU && pairs_out) flush_pairs(p, sm, out_base, out, pol);
       else flush_winners(p, sm, F, out_base, gout, out, pol);
       e = wend;
@@ -1327,12 +1333,12 @@ __device__ __forceinline__ void alternate_walk(const Params& p, unsigned& walks,
   while (row != -1) {
     const int col = ld_cg(PR(p, row));
     if (col < 0) break;
-    const int mr = ld_rlx(p.cmatch + col);
+    const int mr = ld_rlx(CM(p, col));
     if (mr >= 0 && ld_cg(PR(p, mr)) == col) {
       if (steps > 0) log_write(p, row, -1);  // left dangling: its column now belongs to another row
       break;
     }
-    st_rlx(p.cmatch + col, row);
+    st_rlx(CM(p, col), row);
     st_rlx(RM(p, row), col);
     log_write(p, row, col);
     row = mr;
@@ -1350,18 +1356,18 @@ __device__ __forceinline__ void alternate_walk(const Params& p, unsigned& walks,
 __device__ __forceinline__ void fix_row(const Params& p, unsigned& resets, int r) {
   const int v = ld_rlx(RM(p, r));
   if (v == -2) {
-    if (atomicCAS(RM(p, r), -2, -1) == -2) resets++;
-  } else if (v >= 0 && ld_rlx(p.cmatch + v) != r) {
-    if (atomicCAS(RM(p, r), v, -1) == v) resets++;
+    if (at_cas(RM(p, r), -2, -1) == -2) resets++;
+  } else if (v >= 0 && ld_rlx(CM(p, v)) != r) {
+    if (at_cas(RM(p, r), v, -1) == v) resets++;
   }
 }
 
 // FIX rule 3 for one column (gpu_match.cpp:238-243); returns true if the
 // column is unmatched afterwards.
 __device__ __forceinline__ bool fix_col(const Params& p, unsigned& resets, int c) {
-  const int r = ld_rlx(p.cmatch + c);
+  const int r = ld_rlx(CM(p, c));
   if (r >= 0 && ld_rlx(RM(p, r)) != c) {
-    if (atomicCAS(p.cmatch + c, r, -1) == r) resets++;
+    if (at_cas(CM(p, c), r, -1) == r) resets++;
     return true;
   }
   return r < 0;
@@ -1372,8 +1378,13 @@ __device__ __forceinline__ void sweep_visited(const Params& p) {
   // one int4 covers 2 interleaved rows or 4 plain ones
   const bool il = p.rs == 2;
   const int kRowsPer4 = il ? 2 : 4;
-  int4* r4 = reinterpret_cast<int4*>(p.rm);
-  const unsigned long long n4 = (unsigned long long)p.nr / kRowsPer4;
+#if BM_MG
+  const long long r_lo = p.row_lo, nrows = (long long)p.row_hi - p.row_lo;  // own rows (32-aligned start)
+#else
+  const long long r_lo = 0, nrows = p.nr;
+#endif
+  int4* r4 = reinterpret_cast<int4*>(RML(p, r_lo));
+  const unsigned long long n4 = (unsigned long long)nrows / kRowsPer4;
   auto clr = [](int& v) { if (v >= 0) v &= ~kVisBit; };
   constexpr int K = 4;  // int4s per thread in flight
   const unsigned long long GT = global_threads();
@@ -1393,9 +1404,9 @@ __device__ __forceinline__ void sweep_visited(const Params& p) {
       if (v[i].x != o.x || v[i].y != o.y || v[i].z != o.z || v[i].w != o.w) st_plain(r4 + k0 + i * GT, v[i]);
     }
   }
-  for (unsigned long long r = n4 * kRowsPer4 + global_thread(); r < (unsigned long long)p.nr; r += global_threads()) {
-    const int v = ld_cg(RM(p, r));
-    if (v >= 0 && (v & kVisBit)) st_plain(RM(p, r), v & ~kVisBit);
+  for (unsigned long long r = n4 * kRowsPer4 + global_thread(); r < (unsigned long long)nrows; r += global_threads()) {
+    const int v = ld_cg(RML(p, r_lo + r));
+    if (v >= 0 && (v & kVisBit)) st_plain(RML(p, r_lo + r), v & ~kVisBit);
   }
 }
 
@@ -1464,6 +1475,113 @@ __device__ PhaseOut run_phase(const Params& p, Smem& sm, int cur, int parity, bo
   bool found = false;
   bool in_pairs = false;  // this level's entries are (col, root) pairs in P (pulled-capable kernels)
   const unsigned long long pol_mat = policy_evict_first();
+#if BM_MG
+  if (routed(p)) {
+  // Multi-GPU level loop: every rank expands its own frontier (columns it
+  // owns); every winner goes to its column's owner as a pair, so each level
+  // after the roots arrives as pairs and is materialized (pushed) or turned
+  // into the bitmap (pulled) by its owner. Decisions (pull, stop) use team
+  // totals read from every rank's counters after the barrier, so all ranks
+  // take the same ones.
+  (void)pol_mat;
+  if (threadIdx.x == 0) {
+    unsigned long long nt = 0, tt = 0, mx = 0;
+    for (int q = 0; q < p.world; ++q) {
+      const unsigned long long v = ld_rlx(&p.peer[q].ctl->roots.packed);
+      sm.mg_ls[q] = 0;
+      sm.mg_n[q] = (unsigned)(v >> 33);
+      nt += v >> 33;
+      tt += v & kEdgeMask;
+      mx = (v >> 33) > mx ? (v >> 33) : mx;
+    }
+    sm.mg_tot[0] = nt;
+    sm.mg_tot[1] = tt;
+    sm.mg_tot[3] = mx;
+  }
+  __syncthreads();
+  unsigned long long n_tot = sm.mg_tot[0], T_tot = sm.mg_tot[1], ls_tot = 0;
+  for (;;) {
+    Slot* in = lv == 0 ? &ctl->roots : &ctl->lvl[lv % 3];
+    const bool bu = BU && p.roffs && !p.trace && want_pull(p, T_tot, (unsigned)n_tot, (unsigned)ls_tot);
+    if (in_pairs && !bu) {  // pushed: this rank's pairs become edge-tiled entries
+      Slot* ms = &ctl->mat[lv & 1];
+      materialize(p, sm, F, ls, n, (lv & 1) ? p.gidx1 : p.gidx0, ms, policy_evict_first(), false);
+      grid_sync(p);
+      T = (unsigned)(ld_rlx(&ms->packed) & kEdgeMask);
+      in_pairs = false;
+    }
+    Slot* outs = &ctl->lvl[(lv + 1) % 3];
+    if (is_leader() && lv >= 1) {
+      Slot* z = &ctl->lvl[(lv + 2) % 3];
+      z->packed = 0;
+      z->tile = 0;
+    }
+    if (is_leader()) ctl->mat[(lv + 1) & 1].packed = 0;
+    if (bu) {
+      bu_prep<WR>(p, sm, F, in_pairs, ls, n, lv);
+      grid_sync(p);
+      if (p.world > 1) {
+        bu_share(p, lv);
+        grid_sync(p);
+      }
+      bu_sweep_q<WR, IMP>(p, sm, ls + n, outs, (lv + 1) % 3, lv, parity);
+      if (threadIdx.x == 0) sm.cnt[kStPulledLevels] += is_leader() ? 1 : 0;
+    } else {
+      // store claims when even one entry per frontier edge of the team fits every inbox
+      const bool claim_store = p.claim_store && sm.mg_tot[3] + T_tot <= p.fcap;
+      expand_level<WR, IMP, BU>(p, sm, F, ls, n, T, (lv & 1) ? p.gidx1 : p.gidx0, (lv & 1) ? p.gidx0 : p.gidx1,
+                                in, outs, kStartLevel + lv, parity, true, claim_store, (lv + 1) % 3);
+    }
+    const long long tb = clk();
+    grid_sync(p);
+    if (bu) bu_clear(p, lv);
+    if (threadIdx.x == 0) sm.cnt[kStCycBarrier] += clk() - tb;
+    tl_mark(p, kTlLevel, n);
+    tl_mark(p, kTlLevelEdges, (T & 0x7fffffffu) | (bu ? 0x80000000u : 0u));
+    out.launches++;
+    if (threadIdx.x == 0) {
+      unsigned long long nt = 0;
+      for (int q = 0; q < p.world; ++q) {
+        const unsigned nn = (unsigned)(ld_rlx(&p.peer[q].ctl->lvl[(lv + 1) % 3].packed) >> 33);
+        sm.mg_nn[q] = nn;
+        nt += nn;
+      }
+      sm.mg_tot[0] = nt;
+    }
+    __syncthreads();
+    const unsigned long long n_next_tot = sm.mg_tot[0];
+    found = ld_rlx(path_flag_of(p, parity)) != 0u;
+    bool stop = (p.apsb && found) || n_next_tot == 0;
+    if (!stop) {
+      ls += n;
+      n = sm.mg_nn[p.rank];
+      in_pairs = true;
+      T = (unsigned)fmin((double)n * p.deg_col, 4294967295.0);  // an estimate until materialized
+      ls_tot += n_tot;
+      n_tot = n_next_tot;
+      T_tot = (unsigned long long)fmin((double)n_tot * p.deg_col, 1.8e19);
+      ++lv;
+      if (lv > p.nc + 2) {
+        if (is_leader()) ctl->error = kErrLevels;
+        stop = true;
+      }
+    }
+    __syncthreads();  // every thread has read mg_nn before thread 0 advances the bookkeeping
+    if (!stop && threadIdx.x == 0) {
+      unsigned long long mx = 0;
+      for (int q = 0; q < p.world; ++q) {
+        sm.mg_ls[q] += sm.mg_n[q];
+        sm.mg_n[q] = sm.mg_nn[q];
+        const unsigned long long e = (unsigned long long)sm.mg_ls[q] + sm.mg_n[q];
+        mx = e > mx ? e : mx;
+      }
+      sm.mg_tot[3] = mx;
+    }
+    __syncthreads();
+    if (stop) break;
+  }
+  } else {  // a team of one: the single-GPU level loop below
+#endif
   // Narrow levels (at most solo_edges frontier edges) run on block 0 alone,
   // back to back with CTA barriers only — a grid barrier costs more than such
   // a level's work. The other CTAs wait at one grid barrier and take over
@@ -1520,11 +1638,7 @@ __device__ PhaseOut run_phase(const Params& p, Smem& sm, int cur, int parity, bo
     if (bu) {
       bu_prep<WR>(p, sm, F, in_pairs, ls, n, lv);
       grid_sync(p);
-#ifdef BM_SWEEP_OLD
-      bu_sweep<WR, IMP>(p, sm, ls + n, outs, lv, parity);
-#else
-      bu_sweep_q<WR, IMP>(p, sm, ls + n, outs, lv, parity);
-#endif
+      bu_sweep_q<WR, IMP>(p, sm, ls + n, outs, (lv + 1) % 3, lv, parity);
       if (threadIdx.x == 0) sm.cnt[kStPulledLevels] += is_leader() ? 1 : 0;
     } else {
       // Claims by plain store (no atomic round trip; two discoverers racing on one
@@ -1533,7 +1647,7 @@ __device__ PhaseOut run_phase(const Params& p, Smem& sm, int cur, int parity, bo
       // capacity; otherwise by atomicOr, which pushes every column once.
       const bool claim_store = p.claim_store && (unsigned long long)ls + n + T <= p.fcap;
       expand_level<WR, IMP, BU>(p, sm, F, ls, n, T, (lv & 1) ? p.gidx1 : p.gidx0, (lv & 1) ? p.gidx0 : p.gidx1,
-                                in, outs, kStartLevel + lv, parity, pairs_out, claim_store);
+                                in, outs, kStartLevel + lv, parity, pairs_out, claim_store, (lv + 1) % 3);
     }
 
     const long long tb = clk();
@@ -1550,7 +1664,7 @@ __device__ PhaseOut run_phase(const Params& p, Smem& sm, int cur, int parity, bo
     out.launches++;
     const unsigned long long op = ld_rlx(&outs->packed);
     const unsigned n_next = (unsigned)(op >> 33);
-    found = ld_rlx(&ctl->path_found[parity]) != 0u;
+    found = ld_rlx(path_flag_of(p, parity)) != 0u;
     bool stop = (p.apsb && found) || n_next == 0;
     if (!stop) {
       ls += n;
@@ -1578,13 +1692,16 @@ __device__ PhaseOut run_phase(const Params& p, Smem& sm, int cur, int parity, bo
     }
     if (stop) break;
   }
+#if BM_MG
+  }
+#endif
   out.found = found;
   sweep_visited(p);
   grid_sync(p);
   if (p.stop_after_bfs) return out;
 
   // ---- ALTERNATE (gpu_match.cpp:158-218) ----
-  if (is_leader()) ctl->path_found[parity ^ 1] = 0u;  // flag of the next phase
+  if (is_leader()) *path_flag_of(p, parity ^ 1) = 0u;  // flag of the next phase
   const unsigned n_ep = ld_rlx(&ctl->n_ep);
   unsigned walks = 0, steps = 0, resets = 0;
   if (skip_alt) {
@@ -1605,6 +1722,23 @@ __device__ PhaseOut run_phase(const Params& p, Smem& sm, int cur, int parity, bo
     // Serial retry (gpu_match.cpp:328-343): one thread walks every endpoint
     // in turn; the first walk cannot meet a claimed column, so the phase
     // always augments when a path exists.
+#if BM_MG
+    if (p.rank == 0)  // rank 0 walks every rank's endpoints (or roots), in rank order
+      for (int q = 0; q < p.world; ++q) {
+        if (!IMP) {
+          const unsigned nq = ld_rlx(&p.peer[q].ctl->n_ep);
+          for (unsigned k = 0; k < nq; ++k) alternate_walk(p, walks, steps, ld_cg(p.peer[q].EP + k));
+        } else {
+          const int4* Fq = cur ? p.peer[q].F1 : p.peer[q].F0;
+          const unsigned nq = (unsigned)(ld_rlx(&p.peer[q].ctl->roots.packed) >> 33);
+          for (unsigned k = 0; k < nq; ++k) {
+            const int c = ld_cg(reinterpret_cast<const int*>(Fq + k));
+            const int mark = ld_rlx(BF(p, c));
+            if (mark <= 0) alternate_walk(p, walks, steps, -mark);
+          }
+        }
+      }
+#else
     if (!IMP) {
       for (unsigned k = 0; k < n_ep; ++k) alternate_walk(p, walks, steps, ld_cg(p.EP + k));
     } else {
@@ -1614,6 +1748,7 @@ __device__ PhaseOut run_phase(const Params& p, Smem& sm, int cur, int parity, bo
         if (mark <= 0) alternate_walk(p, walks, steps, -mark);
       }
     }
+#endif
   }
   flush_count(sm, kStWalks, walks);
   flush_count(sm, kStSteps, steps);
@@ -1621,16 +1756,25 @@ __device__ PhaseOut run_phase(const Params& p, Smem& sm, int cur, int parity, bo
   tl_mark(p, kTlAlt, 0);
 
   // ---- FIXMATCHING rules 1+2 over the rows ALTERNATE wrote or left behind ----
+#if BM_MG
+  bool dense = false;  // team-wide: a rank whose log overflowed lost rows of other ranks too
+  for (int q = 0; q < p.world; ++q) dense = dense || ld_rlx(&p.peer[q].ctl->log_overflow) != 0u;
+#else
   const bool dense = ld_rlx(&ctl->log_overflow) != 0u;
+#endif
   const unsigned n_log = dense ? 0u : min(ld_rlx(&ctl->n_log), p.log_cap);
   if (!dense) {
     for (unsigned long long k = global_thread(); k < n_log; k += global_threads())
       fix_row(p, resets, ld_cg(reinterpret_cast<const int*>(p.wlog + k)));
     for (unsigned long long k = global_thread(); k < n_ep; k += global_threads())
       fix_row(p, resets, ld_cg(p.EP + k));
-  } else {  // log overflow: the reference's full pass
-    for (unsigned long long r = global_thread(); r < (unsigned long long)p.nr; r += global_threads())
-      fix_row(p, resets, (int)r);
+  } else {  // log overflow: the reference's full pass (over this rank's rows)
+#if BM_MG
+    const unsigned long long r_lo = p.row_lo, r_hi = p.row_hi;
+#else
+    const unsigned long long r_lo = 0, r_hi = p.nr;
+#endif
+    for (unsigned long long r = r_lo + global_thread(); r < r_hi; r += global_threads()) fix_row(p, resets, (int)r);
   }
   if (WR)
     for (unsigned long long k = global_thread(); k < (unsigned long long)p.ndead_words; k += global_threads())
@@ -1651,22 +1795,37 @@ __device__ PhaseOut run_phase(const Params& p, Smem& sm, int cur, int parity, bo
 
   // ---- FIXMATCHING rule 3 over the columns ALTERNATE wrote; a non-root column
   //      it unmatches becomes a root of the next phase ----
+#if BM_MG
+  const unsigned long long c_lo = p.col_lo;  // dense: this rank's columns
+  const unsigned long long ncheck = dense ? (unsigned long long)(p.col_hi - p.col_lo) : n_log;
+#else
+  const unsigned long long c_lo = 0;
   const unsigned long long ncheck = dense ? (unsigned long long)p.nc : n_log;
+#endif
   for (unsigned long long b = (unsigned long long)blockIdx.x * kThreads; b < ncheck; b += global_threads()) {
     const unsigned long long k = b + threadIdx.x;
     bool push = false;
     int c = -1;
     unsigned beg = 0, deg = 0;
     if (k < ncheck) {
-      c = dense ? (int)k : ld_cg(reinterpret_cast<const int*>(p.wlog + k) + 1);
+      c = dense ? (int)(c_lo + k) : ld_cg(reinterpret_cast<const int*>(p.wlog + k) + 1);
       if (c >= 0 && fix_col(p, resets, c)) {
         // roots of this phase are handled below; others enter the root set once
         if (dense) {
-          push = ld_rlx(p.bfs + c) == kUnvisited;
-          if (push) st_rlx(p.bfs + c, kStartLevel);
+          push = ld_rlx(BF(p, c)) == kUnvisited;
+          if (push) st_rlx(BF(p, c), kStartLevel);
         } else {
-          push = atomicCAS(p.bfs + c, kUnvisited, kStartLevel) == kUnvisited;
+          push = at_cas(BF(p, c), kUnvisited, kStartLevel) == kUnvisited;
         }
+#if BM_MG
+        if (push && owner_col(p, c) != p.rank) {
+          // another rank's column: route it to its owner's next roots (it was matched, so it has an edge)
+          const int q = owner_col(p, c);
+          const unsigned sl = (unsigned)(atomicAdd_system(&p.peer[q].ctl->rootp.packed, 1ull << 33) >> 33);
+          st_plain(p.peer[q].P + sl, make_int2(c, c));
+          push = false;
+        }
+#endif
         if (push) {
           beg = ld_ro(p.offs + c);
           deg = ld_ro(p.offs + c + 1) - beg;
@@ -1713,15 +1872,35 @@ __device__ PhaseOut run_phase(const Params& p, Smem& sm, int cur, int parity, bo
   }
   flush_count(sm, kStResets, resets);
   grid_sync(p);
+#if BM_MG
+  if (routed(p)) {  // the roots other ranks routed here join this rank's roots
+    const unsigned n_rp = (unsigned)(ld_rlx(&ctl->rootp.packed) >> 33);
+    if (n_rp) materialize(p, sm, Fn, 0u, n_rp, p.gidx0, &ctl->roots, policy_evict_first(), false);
+    grid_sync(p);  // (every rank: the barrier is team-wide)
+    if (is_leader()) ctl->rootp.packed = 0;
+  }
+  long long roots_tot = 0;
+  for (int q = 0; q < p.world; ++q) roots_tot += (long long)(ld_rlx(&p.peer[q].ctl->roots.packed) >> 33);
+  tl_mark(p, kTlRoots, (unsigned)roots_tot);
+  out.after = (long long)p.nc - isolated - roots_tot;
+#else
   const unsigned long long np = ld_rlx(&ctl->roots.packed);
   tl_mark(p, kTlRoots, (unsigned)(np >> 33));
   out.after = (long long)p.nc - isolated - (long long)(np >> 33);
+#endif
   return out;
 }
 
 // ---------------------------------------------------------------------------
 template <bool WR, bool IMP, bool BU>
+#if BM_MG
+__global__ void __launch_bounds__(kThreads, BM_MINB) driver_kernel(const __grid_constant__ Params p) {
+  // (grid constant: the peer table is indexed at run time without a local copy)
+  const unsigned long long c_lo = p.col_lo, c_hi = p.col_hi, r_lo = p.row_lo, r_hi = p.row_hi;
+#else
 __global__ void __launch_bounds__(kThreads, BM_MINB) driver_kernel(Params p) {
+  const unsigned long long c_lo = 0, c_hi = p.nc, r_lo = 0, r_hi = p.nr;
+#endif
   extern __shared__ __align__(16) unsigned char smem_raw[];  // sizeof(Smem) > 48 KB: dynamic shared memory
   Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
   Ctrl* ctl = p.ctl;
@@ -1737,13 +1916,13 @@ __global__ void __launch_bounds__(kThreads, BM_MINB) driver_kernel(Params p) {
     // ---- optional GPU initial matching (parallel first-fit with CAS) ----
     if (p.init_mode != BM_INIT_GIVEN) {
       for (int pass = (p.init_mode == BM_INIT_GPU_KS ? 0 : 1); pass < 2; ++pass) {
-        for (unsigned long long c = global_thread(); c < (unsigned long long)p.nc; c += global_threads()) {
+        for (unsigned long long c = c_lo + global_thread(); c < c_hi; c += global_threads()) {
           if (ld_cg(p.cmatch + c) != -1) continue;
           const unsigned b = ld_ro(p.offs + c), e = ld_ro(p.offs + c + 1);
           if (pass == 0 && e - b != 1) continue;  // one-sided Karp-Sipser: degree-1 columns first
           for (unsigned j = b; j < e; ++j) {
             const int r = ld_ro(p.adj + j);
-            if (ld_rlx(RM(p, r)) == -1 && atomicCAS(RM(p, r), -1, (int)c) == -1) {
+            if (ld_rlx(RM(p, r)) == -1 && at_cas(RM(p, r), -1, (int)c) == -1) {
               st_plain(p.cmatch + c, r);
               break;
             }
@@ -1755,12 +1934,11 @@ __global__ void __launch_bounds__(kThreads, BM_MINB) driver_kernel(Params p) {
     }
     // ---- setup: validate init, bfs_array init, roots of phase 1 ----
     unsigned long long bad = 0, iso = 0;
-    for (unsigned long long b = (unsigned long long)blockIdx.x * kThreads; b < (unsigned long long)p.nc;
-         b += global_threads()) {
+    for (unsigned long long b = c_lo + (unsigned long long)blockIdx.x * kThreads; b < c_hi; b += global_threads()) {
       const unsigned long long c = b + threadIdx.x;
       bool root = false;
       unsigned beg = 0, deg = 0;
-      if (c < (unsigned long long)p.nc) {
+      if (c < c_hi) {
         const int r = ld_cg(p.cmatch + c);
         if (!p.init_checked) {
           if (r < -1 || r >= p.nr) bad++;
@@ -1780,10 +1958,10 @@ __global__ void __launch_bounds__(kThreads, BM_MINB) driver_kernel(Params p) {
         put_entry(p.F0, 0u, p.gidx0, slot, (int)c, (int)c, beg, deg);
     }
     if (!p.init_checked)
-      for (unsigned long long r = global_thread(); r < (unsigned long long)p.nr; r += global_threads()) {
-        const int v = ld_cg(RM(p, r));
+      for (unsigned long long r = r_lo + global_thread(); r < r_hi; r += global_threads()) {
+        const int v = ld_cg(RML(p, r));
         if (v < -1 || v >= p.nc) bad++;
-        else if (v >= 0 && ld_cg(p.cmatch + v) != (int)r) bad++;
+        else if (v >= 0 && ld_cg(CM(p, v)) != (int)r) bad++;
       }
     bad = warp_sum(bad);
     iso = warp_sum(iso);
@@ -1793,13 +1971,24 @@ __global__ void __launch_bounds__(kThreads, BM_MINB) driver_kernel(Params p) {
     }
     grid_sync(p);
     tl_mark(p, kTlSetup, 0);
-    if (ld_rlx(&ctl->invalid) != 0ull) {
+#if BM_MG
+    unsigned long long inv_tot = 0, iso_tot = 0, roots_tot = 0;  // team totals
+    for (int q = 0; q < p.world; ++q) {
+      inv_tot += ld_rlx(&p.peer[q].ctl->invalid);
+      iso_tot += ld_rlx(&p.peer[q].ctl->isolated);
+      roots_tot += ld_rlx(&p.peer[q].ctl->roots.packed) >> 33;
+    }
+#else
+    const unsigned long long inv_tot = ld_rlx(&ctl->invalid), iso_tot = ld_rlx(&ctl->isolated);
+    const unsigned long long roots_tot = ld_rlx(&ctl->roots.packed) >> 33;
+#endif
+    if (inv_tot != 0ull) {
       if (is_leader()) ctl->error = kErrInvalidInit;
       return;
     }
-    isolated = (long long)ld_rlx(&ctl->isolated);
+    isolated = (long long)iso_tot;
     cur = 0;
-    card = (long long)p.nc - isolated - (long long)(ld_rlx(&ctl->roots.packed) >> 33);
+    card = (long long)p.nc - isolated - (long long)roots_tot;
     outer = 0;
     if (is_leader()) {
       ctl->init_card = card;
@@ -1865,7 +2054,13 @@ __global__ void __launch_bounds__(kThreads, BM_MINB) driver_kernel(Params p) {
       done = true;
       break;
     }
+#if BM_MG
+    bool err = false;  // any rank's error stops every rank (they all read it after the same barrier)
+    for (int q = 0; q < p.world; ++q) err = err || ld_rlx((const unsigned*)&p.peer[q].ctl->error) != 0u;
+    if (err) break;
+#else
     if (ld_rlx((const unsigned*)&ctl->error) != 0u) break;
+#endif
     if (recs >= p.max_phases || recs >= p.rec_cap) break;
   }
 
@@ -2106,7 +2301,7 @@ __device__ __forceinline__ int column_of(const unsigned* offs, int lo, int hi, u
   return lo;
 }
 
-__global__ void __launch_bounds__(256) bucket_partition_kernel(const unsigned* offs, const int* adj, int nc,
+__global__ void __launch_bounds__(256) bucket_partition_kernel(const unsigned* offs, const int* adj, int col_base, int nc,
                                                                 unsigned E, int shift, int nb, unsigned* pcur,
                                                                 int2* pairs) {
   __shared__ unsigned hist[kMaxBuckets];
@@ -2119,7 +2314,8 @@ __global__ void __launch_bounds__(256) bucket_partition_kernel(const unsigned* o
   constexpr int kPer = kTpChunk / 256;
   const unsigned nchunks = (E + kTpChunk - 1) / kTpChunk;
   for (unsigned ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
-    const unsigned j0 = ch * kTpChunk, j1 = min(E, j0 + kTpChunk);
+    // (64-bit end: E may be within one chunk of 2^32)
+    const unsigned j0 = ch * kTpChunk, j1 = (unsigned)min((unsigned long long)E, (unsigned long long)j0 + kTpChunk);
     for (int b = threadIdx.x; b < nb; b += blockDim.x) hist[b] = 0;
     if (threadIdx.x < 2) span[threadIdx.x] = column_of(offs, 0, nc, threadIdx.x ? j1 - 1 : j0) + threadIdx.x;
     __syncthreads();
@@ -2137,7 +2333,7 @@ __global__ void __launch_bounds__(256) bucket_partition_kernel(const unsigned* o
       if (j < je) {
         while (j >= next) next = ld_ro(offs + (++col) + 1);  // empty columns are skipped
         row[k] = ld_ro(adj + j);
-        cols[k] = col;
+        cols[k] = col_base + col;  // (global id: a rank's slice starts at col_base)
         rank[k] = (unsigned short)atomicAdd(&hist[row[k] >> shift], 1u);
       }
     }
@@ -2185,7 +2381,8 @@ __global__ void __launch_bounds__(256) bucket_partition_kernel(const unsigned* o
 // the grid's working set is one or two buckets wide.
 template <bool kScatter>
 __global__ void __launch_bounds__(256) pair_pass_kernel(const int2* pairs, unsigned E, unsigned* ticket,
-                                                        unsigned* cursor, int* radj) {
+                                                        unsigned* cursor, int* radj, int row_lo, int row_hi) {
+  // rows outside [row_lo, row_hi) belong to another rank (multi-GPU inbox); cursor is indexed from row_lo
   __shared__ unsigned chunk;
   constexpr int kPer = kPairChunk / 256;
   for (;;) {
@@ -2202,9 +2399,9 @@ __global__ void __launch_bounds__(256) pair_pass_kernel(const int2* pairs, unsig
     }
 #pragma unroll
     for (int k = 0; k < kPer; ++k) {
-      if (rc[k].x < 0) continue;
-      if (kScatter) radj[atomicAdd(cursor + rc[k].x, 1u)] = rc[k].y;
-      else atomicAdd(cursor + rc[k].x, 1u);
+      if (rc[k].x < row_lo || rc[k].x >= row_hi) continue;
+      if (kScatter) radj[atomicAdd(cursor + (rc[k].x - row_lo), 1u)] = rc[k].y;
+      else atomicAdd(cursor + (rc[k].x - row_lo), 1u);
     }
   }
 }
