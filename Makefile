@@ -48,16 +48,13 @@ $(BUILD)/bm_engine.o: $(CSRC)/bm_engine.cu $(CSRC)/bm_kernels.cuh $(CSRC)/bm_dev
 $(BUILD)/bm_mg.o: $(CSRC)/bm_mg.cu $(CSRC)/bm_kernels.cuh $(CSRC)/bm_device.cuh include/bmatch_b200.h | $(BUILD)
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(BUILD)/ptxas_mg.log || (cat $(BUILD)/ptxas_mg.log; false)
 
-$(BUILD)/bm_partition.o: $(CSRC)/bm_partition.cu $(CSRC)/bm_device.cuh include/bmatch_b200.h | $(BUILD)
-	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(BUILD)/ptxas_part.log || (cat $(BUILD)/ptxas_part.log; false)
-
 $(BUILD)/bm_host.o: $(CSRC)/bm_host.cpp $(CSRC)/bm_host_util.hpp include/bmatch_b200.h include/bmatch_b200_gen.h | $(BUILD)
 	$(CXX) $(CXXFLAGS) -c $< -o $@
 
 $(BUILD)/bm_io.o: $(CSRC)/bm_io.cpp $(CSRC)/bm_host_util.hpp include/bmatch_b200.h include/bmatch_b200_io.h | $(BUILD)
 	$(CXX) $(CXXFLAGS) -c $< -o $@
 
-$(LIB): $(BUILD)/bm_engine.o $(BUILD)/bm_mg.o $(BUILD)/bm_partition.o $(BUILD)/bm_host.o $(BUILD)/bm_io.o
+$(LIB): $(BUILD)/bm_engine.o $(BUILD)/bm_mg.o $(BUILD)/bm_host.o $(BUILD)/bm_io.o
 	$(NVCC) $(ARCH) -shared -o $@ $^ -Xcompiler -pthread
 
 $(ORACLE): oracle/bm_oracle.c oracle/bm_oracle.h

@@ -311,74 +311,6 @@ bm_status   bm_mg_download(bm_mg* h, int32_t* rmatch_slice, int32_t* cmatch_slic
 bm_status   bm_mg_kernel_time(bm_mg* h, double* ms);
 bm_status   bm_mg_info(bm_mg* h, int64_t* local_edges, int64_t* row_index_edges, int32_t* pulled_capable);
 
-/* ---- 1-D column partition over several GPUs --------------
- * The reference has no multi-device path (its only parallelism is the
- * emulated grid, kernel_grid.hpp:161-222). One bm_part per rank (process,
- * GPU): rank p owns columns [col_lo, col_hi) and their CSC slice; rmatch,
- * cmatch (caller-owned device buffers, bm_part_bind_state) and pred are
- * replicated. Per BFS level (gpubfs / gpubfs_wr, gpu_match.cpp:23-135):
- *   bm_part_expand   expands the local frontier into this rank's records;
- *   (caller)         all-gathers the records of every rank, rank-major,
- *                    record k of rank r at r*stride + k (NCCL over NVLink);
- *   bm_part_merge    applies ALL records in the same order on every rank:
- *                    per column and per free row the lowest (rank, index)
- *                    wins, so the replicas stay identical; the owner queues
- *                    the won columns as its next frontier.
- * Records are int4: claim {column, discoverer, root, row}, endpoint
- * {row, discoverer, root, 0}; buffers are device memory, caller-owned, sized
- * by bm_part_record_capacity. After the level loop: bm_part_end_bfs on every
- * rank, bm_part_augment (ALTERNATE + FIX, gpu_match.cpp:144-245) on rank 0,
- * then the caller broadcasts rmatch/cmatch from rank 0.
- * This replaces the single-process bm_create_multi(devs, n) sketched in
- * one process per GPU (torch.distributed / NCCL for the
- * plumbing) is the deployment model, so a handle never spans devices. */
-typedef struct bm_part bm_part;
-bm_status   bm_part_create(int32_t device, int32_t rank, int32_t world, bm_part** out);
-bm_status   bm_part_destroy(bm_part* pt);
-bm_status   bm_part_set_stream(bm_part* pt, void* stream);
-/* cxadj_slice[col_hi-col_lo+1] rebased to start at 0; cadj_slice its rows. */
-bm_status   bm_part_upload(bm_part* pt, int32_t nc, int32_t nr, int32_t col_lo, int32_t col_hi,
-                           const int64_t* cxadj_slice, const int32_t* cadj_slice);
-bm_status   bm_part_bind_state(bm_part* pt, void* rmatch_dev, void* cmatch_dev);
-bm_status   bm_part_record_capacity(bm_part* pt, int64_t* claims_cap, int64_t* endpoints_cap);
-bm_status   bm_part_begin_phase(bm_part* pt, int32_t bfs_kernel, int32_t endpoint_policy,
-                                int64_t* n_roots_local);
-bm_status   bm_part_expand(bm_part* pt, void* claims_out, void* endpoints_out,
-                           int32_t* n_claims, int32_t* n_endpoints);
-bm_status   bm_part_merge(bm_part* pt, const void* claims_all, const int32_t* claim_counts,
-                          int64_t claim_stride, const void* endpoints_all,
-                          const int32_t* endpoint_counts, int64_t endpoint_stride,
-                          int64_t* n_next_total, int32_t* found);
-bm_status   bm_part_end_bfs(bm_part* pt);
-bm_status   bm_part_augment(bm_part* pt, int32_t serial, int64_t* cardinality);
-bm_status   bm_part_cardinality(bm_part* pt, int64_t* cardinality);
-bm_status   bm_part_stats(bm_part* pt, int64_t* edges_traversed, int64_t* columns_scanned, int64_t* walks,
-                          int64_t* walk_steps, int64_t* fix_resets);
-bm_status   bm_part_reset_stats(bm_part* pt);
-bm_status   bm_part_launch_count(bm_part* pt, int64_t* launches);  /* kernels since the last reset */
-
-/* Fused exchange over peer memory (NVLink, CUDA IPC) instead of the caller's
- * all-gather: the expand kernel itself writes each record into every rank's
- * receive slab and a signal kernel publishes the counts and bumps every rank's
- * arrival counter; the merge waits for the arrivals on the device. No
- * collective library call and no host synchronisation inside the exchange.
- * Setup: bm_part_p2p_export (allocates the slabs: 2 level parities x world x
- * cap records; cap >= any rank's records per level, e.g. min(nc, max rank E)
- * for claims and min(nr, max rank E) for endpoints) returns 4 IPC handles
- * (4 x 64 bytes); the caller all-gathers them (rank-major) and passes them
- * to bm_part_p2p_import. Per level: bm_part_expand_p2p(parity = level & 1),
- * then bm_part_merge_p2p(parity, arrivals = world * levels so far). */
-bm_status   bm_part_p2p_export(bm_part* pt, int64_t claims_cap, int64_t endpoints_cap, void* handles);
-bm_status   bm_part_p2p_import(bm_part* pt, const void* all_handles);
-bm_status   bm_part_expand_p2p(bm_part* pt, int32_t parity);
-bm_status   bm_part_merge_p2p(bm_part* pt, int32_t parity, uint32_t arrivals, int64_t* n_next_total,
-                              int32_t* found);
-
-/* ---- host utilities (not on the hot path) -------------------------------- */
-/* First-fit greedy in ascending column order; restates matching.cpp:13-26. */
-bm_status   bm_host_cheap_matching(int32_t nc, int32_t nr, const int64_t* cxadj,
-                                   const int32_t* cadj, int32_t* rmatch, int32_t* cmatch);
-
 #ifdef __cplusplus
 }
 #endif

@@ -5,6 +5,6 @@ NV="nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcomp
 $NV $flags -c paper_1303_1379_b200/csrc/bm_engine.cu -o tunelib/$name.o && \
 g++ -O3 -std=c++17 -fPIC -pthread -Iinclude -c paper_1303_1379_b200/csrc/bm_host.cpp -o tunelib/host.o && \
 g++ -O3 -std=c++17 -fPIC -pthread -Iinclude -c paper_1303_1379_b200/csrc/bm_io.cpp -o tunelib/io.o && \
-$NV -c paper_1303_1379_b200/csrc/bm_partition.cu -o tunelib/part.o && \
-nvcc -gencode arch=compute_100a,code=sm_100a -shared -o tunelib/$name.so tunelib/$name.o tunelib/part.o tunelib/host.o tunelib/io.o -Xcompiler -pthread && \
-rm -f tunelib/$name.o
+$NV $flags -c paper_1303_1379_b200/csrc/bm_mg.cu -o tunelib/mg_$name.o && \
+nvcc -gencode arch=compute_100a,code=sm_100a -shared -o tunelib/$name.so tunelib/$name.o tunelib/mg_$name.o tunelib/host.o tunelib/io.o -Xcompiler -pthread && \
+rm -f tunelib/$name.o tunelib/mg_$name.o

@@ -42,11 +42,12 @@ def test_no_cpu_fallback_without_gpu():
     assert b"no CUDA device" in _lib.lib.bm_last_error()
     with pytest.raises(bm.CudaError):
         bm.Engine(0)
-    # the multi-GPU partition handle refuses as well
+    # the multi-GPU engine refuses as well
     from paper_1303_1379_b200 import partition
-    st = partition.lib.bm_part_create(0, 0, 2, C.byref(h))
+    st = partition.lib.bm_mg_create(0, 0, 2, 1, C.byref(h))
     assert st == _lib.BM_ERR_CUDA
-    assert partition.lib.bm_part_create(0, 3, 2, C.byref(h)) == _lib.BM_ERR_INVALID_ARG  # rank out of range
+    assert partition.lib.bm_mg_create(0, 3, 2, 1, C.byref(h)) == _lib.BM_ERR_INVALID_ARG  # rank out of range
+    assert partition.lib.bm_mg_create(0, 0, 9, 1, C.byref(h)) == _lib.BM_ERR_INVALID_ARG  # world > 8
 
 
 def test_null_handle_errors():
