@@ -256,7 +256,7 @@ struct Params {
 
 enum TlTag : unsigned {
   kTlStart = 0, kTlInit = 1, kTlSetup = 2, kTlLevel = 3, kTlAlt = 4, kTlFixRows = 5, kTlFixCols = 6,
-  kTlRoots = 7, kTlEnd = 8, kTlLevelEdges = 9
+  kTlRoots = 7, kTlEnd = 8, kTlLevelEdges = 9, kTlMat = 10, kTlPrep = 11
 };
 
 __device__ __forceinline__ void tl_mark(const Params& p, unsigned kind, unsigned arg) {
@@ -1603,6 +1603,7 @@ __device__ PhaseOut run_phase(const Params& p, Smem& sm, int cur, int parity, bo
       Slot* ms = &ctl->mat[lv & 1];
       materialize(p, sm, F, ls, n, (lv & 1) ? p.gidx1 : p.gidx0, ms, pol_mat, false);
       grid_sync(p);
+      tl_mark(p, kTlMat, n);
       const unsigned long long mp = ld_rlx(&ms->packed);
       T = (unsigned)(mp & kEdgeMask);
       in_pairs = false;
@@ -1638,6 +1639,7 @@ __device__ PhaseOut run_phase(const Params& p, Smem& sm, int cur, int parity, bo
     if (bu) {
       bu_prep<WR>(p, sm, F, in_pairs, ls, n, lv);
       grid_sync(p);
+      tl_mark(p, kTlPrep, n);
       bu_sweep_q<WR, IMP>(p, sm, ls + n, outs, (lv + 1) % 3, lv, parity);
       if (threadIdx.x == 0) sm.cnt[kStPulledLevels] += is_leader() ? 1 : 0;
     } else {
@@ -2312,7 +2314,7 @@ __global__ void __launch_bounds__(256) bucket_partition_kernel(const unsigned* o
   __shared__ unsigned short sbk[kTpChunk];
   __shared__ int span[2];
   constexpr int kPer = kTpChunk / 256;
-  const unsigned nchunks = (E + kTpChunk - 1) / kTpChunk;
+  const unsigned nchunks = (unsigned)(((unsigned long long)E + kTpChunk - 1) / kTpChunk);
   for (unsigned ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
     // (64-bit end: E may be within one chunk of 2^32)
     const unsigned j0 = ch * kTpChunk, j1 = (unsigned)min((unsigned long long)E, (unsigned long long)j0 + kTpChunk);

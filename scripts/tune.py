@@ -23,6 +23,7 @@ def timeline_summary(eng):
     levels, prev = [], tl[0][2]
     phase = 0
     kinds = {}
+    sub = {}
     for kind, arg, t in tl[1:]:
         if kind == "level_edges":
             levels[-1] += [arg & 0x7FFFFFFF, arg >> 31]
@@ -30,8 +31,12 @@ def timeline_summary(eng):
         dt = (t - prev) / 1e3
         prev = t
         kinds[kind] = kinds.get(kind, 0.0) + dt
+        if kind in ("materialize", "pull_prep"):  # parts of the level that follows
+            sub[kind] = round(dt, 1)
+            continue
         if kind == "level":
-            levels.append([phase, arg, round(dt, 1)])
+            levels.append([phase, arg, round(dt + sum(sub.values()), 1), sub])
+            sub = {}
         if kind == "roots":
             phase += 1
     return {"per_kind_us": {k: round(v, 1) for k, v in kinds.items()}, "levels": levels}
