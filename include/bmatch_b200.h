@@ -186,6 +186,17 @@ bm_status   bm_bottom_up_auto(bm_handle* h, int32_t* enabled);
  * run on. Call it once per upload when the same graph is matched repeatedly;
  * a single match of a graph below 2^26 rows does not repay it and pushes. */
 bm_status   bm_prepare_row_index(bm_handle* h);
+/* The row index as the pulled levels read it: roffs[nr + 1] (uint32) and
+ * radj[E] (int32), the columns of row r in radj[roffs[r], roffs[r + 1]) in no
+ * particular order. BM_ERR_INVALID_ARG when it has not been built. Either
+ * pointer may be NULL. (Diagnostics and tests: the one-pass build and the
+ * build that bm_upload_csc overlaps with the copy must agree.)
+ *
+ * bm_upload_csc builds the row index while it copies the adjacency (chunk by
+ * chunk, on a second stream; only the final scatter is left when the copy
+ * ends, and the next run waits for it) on graphs where AUTO pulls from the
+ * first run (>= 2^26 rows and E >= 6 nc). BM_PREBUILD=1|0 forces it on|off. */
+bm_status   bm_download_row_index(bm_handle* h, uint32_t* roffs, int32_t* radj);
 
 /* ---- matching: the reference-shaped one-call entry ----------------------
  * Replaces apfb()/apsb() (gpu_match.hpp:133-144): rmatch[nr]/cmatch[nc] are
@@ -231,7 +242,9 @@ bm_status   bm_debug_set(bm_handle* h, int32_t key, int64_t value);
  * uint64 each, (tag, device %globaltimer in ns). tag = (kind << 32) | arg with
  * kind 0 start, 1 init pass, 2 setup, 3 BFS level (arg = frontier entries),
  * 4 ALTERNATE, 5 FIX rows, 6 FIX columns, 7 roots of the next phase, 8 end,
- * 9 the preceding level's frontier edges (arg; same timestamp).
+ * 9 the preceding level's frontier edges (arg; same timestamp), 10 the
+ * preceding pushed level's pairs turned into entries (materialize), 11 the
+ * preceding pulled level's frontier bitmap built (pull prep).
  * Written by one thread after each grid barrier (a few ns per stage). */
 bm_status   bm_timeline(bm_handle* h, uint64_t* out, int64_t cap, int64_t* n);
 

@@ -327,6 +327,15 @@ class Engine:
         """Build the row index now (bm_prepare_row_index), so "auto" pulls from the next run."""
         check(lib.bm_prepare_row_index(self._h))
 
+    def row_index(self):
+        """The row index the pulled levels read (bm_download_row_index): (roffs[nr+1], radj[E])."""
+        nc, nr, ne = self.graph_info()
+        roffs = np.empty(nr + 1, np.uint32)
+        radj = np.empty(max(ne, 1), np.int32)
+        check(lib.bm_download_row_index(self._h, roffs.ctypes.data_as(C.POINTER(C.c_uint32)),
+                                        radj.ctypes.data_as(C.POINTER(C.c_int32))))
+        return roffs, radj[:ne]
+
     def graph_info(self):
         nc, nr, ne = C.c_int32(), C.c_int32(), C.c_int64()
         check(lib.bm_graph_info(self._h, C.byref(nc), C.byref(nr), C.byref(ne)))

@@ -52,8 +52,10 @@
 //     unmatched; nothing is O(nc) per phase except the dead-root bitmap clear
 //     and the visited-bit sweep over rmatch.
 #include <algorithm>
+#include <climits>
 #include <cstdlib>
 #include <cstdint>
+#include <deque>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -65,6 +67,7 @@
 #include <cuda_runtime.h>
 
 #include "bm_device.cuh"
+#include "bm_host_util.hpp"
 #include "bmatch_b200.h"
 
 namespace cg = cooperative_groups;
@@ -156,6 +159,12 @@ struct bm_handle {
   bool bu_huge = false;       // ... and so large that one run repays building the row index
   unsigned* tp_pcur = nullptr;  // row-index build scratch (bucket cursors, bucketed pairs)
   int2* tp_pairs = nullptr;
+  unsigned* tp_runs = nullptr;  // chunked build (with the upload): run starts, cursors, counts, tile prefix, tickets
+  cudaEvent_t ev_ri = nullptr;  // the row index built with the upload is complete (aux stream)
+  // pageable host buffers: copied through pinned staging buffers (xfer_h2d / xfer_d2h)
+  void* stg_buf[3] = {nullptr, nullptr, nullptr};
+  cudaEvent_t stg_ev[3] = {nullptr, nullptr, nullptr};
+  int stg_next = 0;
   unsigned char* tp_tmp = nullptr;  // CUB scan scratch
   double bu_frac = 0.45;      // BM_BU_FRAC (bu_rule 0): a level goes bottom-up when its frontier edges >= bu_frac * E
   int bu_rule = 1;            // 1: want_pull's direction-optimising test (default); 0: the bu_frac threshold
@@ -209,6 +218,107 @@ bm_status check_handle(bm_handle* h, bool need_graph) {
 
 int row_blocks(bm_handle* h) { return std::max(1, std::min(h->sms * 8, (h->nr + 255) / 256)); }
 
+// ---- host <-> device copies ------------------------------------------------
+// A pageable host buffer (the C++ shim's std::vectors, plain numpy arrays) is
+// copied through a ring of pinned staging buffers: host threads fill (or drain)
+// one buffer while the copy engine moves the previous one, so the copy runs
+// near the pinned PCIe rate instead of the driver's single-threaded bounce
+// path. Pinned (or registered) buffers go straight to cudaMemcpyAsync.
+constexpr int kStgBufs = 3;
+constexpr size_t kStgBytes = 64ull << 20;
+constexpr size_t kStgMin = 8ull << 20;  // smaller copies go direct
+
+bool host_pageable(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return true;
+  }
+  return a.type == cudaMemoryTypeUnregistered;
+}
+
+bm_status stage_init(bm_handle* h) {
+  for (int i = 0; i < kStgBufs; ++i) {
+    if (h->stg_buf[i]) continue;
+    BM_CUDA(cudaHostAlloc(&h->stg_buf[i], kStgBytes, cudaHostAllocDefault));
+    BM_CUDA(cudaEventCreateWithFlags(&h->stg_ev[i], cudaEventDisableTiming));
+  }
+  return BM_OK;
+}
+
+void par_copy(void* dst, const void* src, size_t n) {  // >= 8 MB per thread, at most 8 threads
+  const int t = (int)std::max<size_t>(1, std::min<size_t>((size_t)std::min(8, bm_host::resolve_threads(0)), n >> 23));
+  bm_host::parallel_for((long long)t, t, [&](long long b, long long e, int) {
+    for (long long w = b; w < e; ++w) {
+      const size_t lo = n * (size_t)w / (size_t)t, hi = n * (size_t)(w + 1) / (size_t)t;
+      std::memcpy(static_cast<char*>(dst) + lo, static_cast<const char*>(src) + lo, hi - lo);
+    }
+  });
+}
+
+// Enqueues a host -> device copy on st (returns once the host buffer may be reused).
+bm_status xfer_h2d(bm_handle* h, void* dst, const void* src, size_t n, cudaStream_t st) {
+  if (n == 0) return BM_OK;
+  if (n < kStgMin || !host_pageable(src)) {
+    BM_CUDA(cudaMemcpyAsync(dst, src, n, cudaMemcpyHostToDevice, st));
+    return BM_OK;
+  }
+  bm_status s = stage_init(h);
+  if (s != BM_OK) return s;
+  for (size_t off = 0; off < n; off += kStgBytes) {
+    const size_t len = std::min(kStgBytes, n - off);
+    const int i = h->stg_next;
+    h->stg_next = (i + 1) % kStgBufs;
+    BM_CUDA(cudaEventSynchronize(h->stg_ev[i]));  // the buffer's previous copy is done
+    par_copy(h->stg_buf[i], static_cast<const char*>(src) + off, len);
+    BM_CUDA(cudaMemcpyAsync(static_cast<char*>(dst) + off, h->stg_buf[i], len, cudaMemcpyHostToDevice, st));
+    BM_CUDA(cudaEventRecord(h->stg_ev[i], st));
+  }
+  return BM_OK;
+}
+
+// Device -> host copy, complete on return (stream-ordered after earlier work on st).
+bm_status xfer_d2h(bm_handle* h, void* dst, const void* src, size_t n, cudaStream_t st) {
+  if (n == 0) return BM_OK;
+  if (n < kStgMin || !host_pageable(dst)) {
+    BM_CUDA(cudaMemcpyAsync(dst, src, n, cudaMemcpyDeviceToHost, st));
+    BM_CUDA(cudaStreamSynchronize(st));
+    return BM_OK;
+  }
+  bm_status s = stage_init(h);
+  if (s != BM_OK) return s;
+  struct Piece {
+    int buf;
+    size_t off, len;
+  };
+  std::deque<Piece> q;
+  auto drain = [&]() -> bm_status {
+    const Piece pc = q.front();
+    q.pop_front();
+    BM_CUDA(cudaEventSynchronize(h->stg_ev[pc.buf]));
+    par_copy(static_cast<char*>(dst) + pc.off, h->stg_buf[pc.buf], pc.len);
+    return BM_OK;
+  };
+  for (size_t off = 0; off < n; off += kStgBytes) {
+    const size_t len = std::min(kStgBytes, n - off);
+    if ((int)q.size() == kStgBufs) {  // the oldest piece holds the buffer this one takes
+      s = drain();
+      if (s != BM_OK) return s;
+    }
+    const int i = h->stg_next;
+    h->stg_next = (i + 1) % kStgBufs;
+    BM_CUDA(cudaEventSynchronize(h->stg_ev[i]));
+    BM_CUDA(cudaMemcpyAsync(h->stg_buf[i], static_cast<const char*>(src) + off, len, cudaMemcpyDeviceToHost, st));
+    BM_CUDA(cudaEventRecord(h->stg_ev[i], st));
+    q.push_back({i, off, len});
+  }
+  while (!q.empty()) {
+    s = drain();
+    if (s != BM_OK) return s;
+  }
+  return BM_OK;
+}
+
 // plain device array (nr ints) -> row-state mates
 bm_status rows_from_plain(bm_handle* h, const int* plain) {
   if (h->nr <= 0) return BM_OK;
@@ -234,49 +344,60 @@ bm_status rows_fill(bm_handle* h, int off, int v) {
 // host rmatch -> row-state mates (through the staging buffer)
 bm_status rows_from_host(bm_handle* h, const int32_t* rmatch) {
   if (h->nr <= 0) return BM_OK;
-  BM_CUDA(cudaMemcpyAsync(h->rtmp, rmatch, sizeof(int) * h->nr, cudaMemcpyHostToDevice, h->stream));
+  bm_status s = xfer_h2d(h, h->rtmp, rmatch, sizeof(int) * h->nr, h->stream);
+  if (s != BM_OK) return s;
   return rows_from_plain(h, h->rtmp);
 }
 bm_status rows_to_host(bm_handle* h, int32_t* out, int off) {
   if (h->nr <= 0 || !out) return BM_OK;
   bm_status s = rows_to_plain(h, h->rtmp, off);
   if (s != BM_OK) return s;
-  BM_CUDA(cudaMemcpyAsync(out, h->rtmp, sizeof(int) * h->nr, cudaMemcpyDeviceToHost, h->stream));
-  BM_CUDA(cudaStreamSynchronize(h->stream));
+  return xfer_d2h(h, out, h->rtmp, sizeof(int) * h->nr, h->stream);
+}
+
+// Transposed adjacency (the row index) for pulled levels: allocations and the
+// bucket geometry shared by the one-pass build (build_transpose) and the build
+// that runs chunk by chunk with the upload (chunked_*). Rows are bucketed so
+// that one bucket's slice of radj is at most 32 MB (kernels: bm_kernels.cuh).
+bm_status transpose_alloc(bm_handle* h, int nc, int nr, long long E, int* shift_out, int* nb_out) {
+  h->bu_enabled = nr > 0 && nc > 0 && E > 0;
+  if (!h->bu_enabled) return BM_OK;
+  BM_CUDA(dalloc(h->caps, h->roffs, (size_t)nr + 1));
+  BM_CUDA(dalloc(h->caps, h->rcursor, (size_t)nr + 1));
+  BM_CUDA(dalloc(h->caps, h->radj, (size_t)E));
+  h->nfbit_words = (nc + 31) / 32;
+  BM_CUDA(dalloc(h->caps, h->fbit, (size_t)2 * h->nfbit_words));
+  BM_CUDA(dalloc(h->caps, h->croot, (size_t)nc));
+  BM_CUDA(dalloc(h->caps, h->P, (size_t)nc + kFSlack(nc)));
+  int shift = 0;
+  {
+    const long long nb_min = std::max<long long>(1, (E * (long long)sizeof(int) + (32ll << 20) - 1) >> 25);
+    while (shift < 31 && ((long long)nr + (1ll << shift) - 1) >> shift > nb_min) ++shift;
+  }
+  const int nb = (int)(((long long)nr + (1ll << shift) - 1) >> shift);
+  if (nb > kMaxBuckets) return fail(BM_ERR_INVALID_ARG, "row index: too many buckets");
+  // scratch kept with the handle (a fresh 8E-byte allocation per build costs more than the build):
+  // [0, nb) bucket cursors, [kMaxBuckets, +nb) bucket counts, [2 kMaxBuckets, +2) tickets
+  BM_CUDA(dalloc(h->caps, h->tp_pcur, (size_t)2 * kMaxBuckets + 2));
+  BM_CUDA(dalloc(h->caps, h->tp_pairs, (size_t)E));
+  size_t tmp_bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, h->rcursor, h->roffs, nr + 1, h->stream);
+  // kept with the handle too: a stream-ordered allocation here cost 3-115 ms per build
+  // (the default pool hands its memory back at every synchronisation)
+  BM_CUDA(dalloc(h->caps, h->tp_tmp, tmp_bytes));
+  *shift_out = shift;
+  *nb_out = nb;
   return BM_OK;
 }
 
-// Transposed adjacency for bottom-up levels (BM_BOTTOM_UP=0 disables them;
-// BM_BU_FRAC tunes the switch). Called after every change of the graph.
+// One-pass build over the resident CSC (bm_prepare_row_index, or the first
+// pulling run after an upload that did not build it).
 bm_status build_transpose(bm_handle* h, int nc, int nr, long long E) {
-  {
-    h->bu_enabled = nr > 0 && nc > 0 && E > 0;
-    // Pull threshold (share of the edges in the frontier). Once the row state is
-    // far beyond L2 (the interleaved layout) every pushed gather pays DRAM
-    // sectors, so pulling pays from sparser frontiers: measured optimum 0.15-0.25
-    // on C5 against 0.45-0.6 on C2 (profiles/README.md).
-
-  }
+  BM_CUDA(cudaStreamWaitEvent(h->stream, h->ev_ri, 0));  // (an earlier chunked build's scatter)
+  int shift = 0, nb = 0;
+  bm_status s = transpose_alloc(h, nc, nr, E, &shift, &nb);
+  if (s != BM_OK) return s;
   if (h->bu_enabled) {
-    BM_CUDA(dalloc(h->caps, h->roffs, (size_t)nr + 1));
-    BM_CUDA(dalloc(h->caps, h->rcursor, (size_t)nr + 1));
-    BM_CUDA(dalloc(h->caps, h->radj, (size_t)E));
-    h->nfbit_words = (nc + 31) / 32;
-    BM_CUDA(dalloc(h->caps, h->fbit, (size_t)2 * h->nfbit_words));
-    BM_CUDA(dalloc(h->caps, h->croot, (size_t)nc));
-    BM_CUDA(dalloc(h->caps, h->P, (size_t)nc + kFSlack(nc)));
-    // rows bucketed so that one bucket's slice of radj is at most 32 MB
-    int shift = 0;
-    {
-      const long long nb_min = std::max<long long>(1, (E * (long long)sizeof(int) + (32ll << 20) - 1) >> 25);
-      while (shift < 31 && ((long long)nr + (1ll << shift) - 1) >> shift > nb_min) ++shift;
-    }
-    const int nb = (int)(((long long)nr + (1ll << shift) - 1) >> shift);
-    if (nb > kMaxBuckets) return fail(BM_ERR_INVALID_ARG, "row index: too many buckets");
-    // scratch kept with the handle (a fresh 8E-byte allocation per build costs more than the build):
-    // [0, nb) bucket cursors, [kMaxBuckets, +nb) bucket counts, [2 kMaxBuckets, +2) tickets
-    BM_CUDA(dalloc(h->caps, h->tp_pcur, (size_t)2 * kMaxBuckets + 2));
-    BM_CUDA(dalloc(h->caps, h->tp_pairs, (size_t)E));
     unsigned* pcur = h->tp_pcur;
     unsigned* bcount = h->tp_pcur + kMaxBuckets;
     unsigned* tickets = h->tp_pcur + 2 * kMaxBuckets;
@@ -285,22 +406,76 @@ bm_status build_transpose(bm_handle* h, int nc, int nr, long long E) {
     BM_CUDA(cudaMemsetAsync(h->rcursor, 0, sizeof(unsigned) * ((size_t)nr + 1), h->stream));
     BM_CUDA(cudaMemsetAsync(h->fbit, 0, sizeof(unsigned) * 2 * h->nfbit_words, h->stream));
     const int grid = h->sms * 8;
-    bucket_hist_kernel<<<grid, 256, 0, h->stream>>>(h->adj, (unsigned)E, shift, nb, bcount);
+    bucket_hist_kernel<<<grid, 256, 0, h->stream>>>(h->adj, (unsigned)E, shift, nb, nr, bcount);
     bucket_base_kernel<<<1, 32, 0, h->stream>>>(bcount, nb, pcur);
     const int pa = (int)std::max<long long>(1, std::min<long long>((long long)grid, (E + kTpChunk - 1) / kTpChunk));
     bucket_partition_kernel<<<pa, 256, 0, h->stream>>>(h->offs, h->adj, 0, nc, (unsigned)E, shift, nb, pcur, pairs);
     pair_pass_kernel<false><<<grid, 256, 0, h->stream>>>(pairs, (unsigned)E, tickets, h->rcursor, nullptr, 0, nr);
     size_t tmp_bytes = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, h->rcursor, h->roffs, nr + 1, h->stream);
-    // kept with the handle too: a stream-ordered allocation here cost 3-115 ms per build
-    // (the default pool hands its memory back at every synchronisation)
-    BM_CUDA(dalloc(h->caps, h->tp_tmp, tmp_bytes));
     cub::DeviceScan::ExclusiveSum(h->tp_tmp, tmp_bytes, h->rcursor, h->roffs, nr + 1, h->stream);
     BM_CUDA(cudaMemcpyAsync(h->rcursor, h->roffs, sizeof(unsigned) * ((size_t)nr + 1), cudaMemcpyDeviceToDevice,
                             h->stream));
     pair_pass_kernel<true><<<grid, 256, 0, h->stream>>>(pairs, (unsigned)E, tickets + 1, h->rcursor, h->radj, 0, nr);
     BM_CUDA(cudaGetLastError());
   }
+  h->bu_built = true;
+  return BM_OK;
+}
+
+// The build overlapped with the upload (bm_upload_csc, graphs where AUTO pulls
+// from the first run): every adjacency chunk, as soon as its copy lands, is
+// bucketed into its own slice of the pairs and its rows counted (aux stream);
+// after the last chunk only the scan and the bucket-major scatter remain.
+struct ChunkBuild {
+  bool on = false;
+  int shift = 0, nb = 0, K = 0;
+  unsigned *start = nullptr, *cur = nullptr, *cnt = nullptr, *tpre = nullptr, *tickets = nullptr;
+};
+
+bm_status chunked_begin(bm_handle* h, int nc, int nr, long long E, long long chunk, ChunkBuild& cb) {
+  bm_status s = transpose_alloc(h, nc, nr, E, &cb.shift, &cb.nb);
+  if (s != BM_OK || !h->bu_enabled) return s;
+  cb.K = (int)((E + chunk - 1) / chunk);
+  const size_t kn = (size_t)cb.K * cb.nb;
+  BM_CUDA(dalloc(h->caps, h->tp_runs, 4 * kn + 1 + (size_t)cb.K + 1));
+  cb.start = h->tp_runs;
+  cb.cur = cb.start + kn;
+  cb.cnt = cb.cur + kn;
+  cb.tpre = cb.cnt + kn;
+  cb.tickets = cb.tpre + kn + 1;
+  BM_CUDA(cudaMemsetAsync(cb.cnt, 0, sizeof(unsigned) * kn, h->aux));
+  BM_CUDA(cudaMemsetAsync(cb.tickets, 0, sizeof(unsigned) * ((size_t)cb.K + 1), h->aux));
+  BM_CUDA(cudaMemsetAsync(h->rcursor, 0, sizeof(unsigned) * ((size_t)nr + 1), h->aux));
+  BM_CUDA(cudaMemsetAsync(h->fbit, 0, sizeof(unsigned) * 2 * h->nfbit_words, h->aux));
+  cb.on = true;
+  return BM_OK;
+}
+
+// Chunk k = adjacency [j0, j1), enqueued on aux after its copy.
+void chunked_chunk(bm_handle* h, const ChunkBuild& cb, int k, int nc, int nr, long long j0, long long j1) {
+  const unsigned n = (unsigned)(j1 - j0);
+  const size_t o = (size_t)k * cb.nb;
+  const int grid = (int)std::max<long long>(1, std::min<long long>((long long)h->sms * 8, (n + 255) / 256));
+  bucket_hist_kernel<<<grid, 256, 0, h->aux>>>(h->adj + j0, n, cb.shift, cb.nb, nr, cb.cnt + o);
+  bucket_base_kernel<<<1, 32, 0, h->aux>>>(cb.cnt + o, cb.nb, cb.cur + o, (unsigned)j0, cb.start + o);
+  const int pa = (int)std::max<long long>(1, std::min<long long>((long long)h->sms * 8, (n + kTpChunk - 1) / kTpChunk));
+  bucket_partition_kernel<<<pa, 256, 0, h->aux>>>(h->offs, h->adj, 0, nc, n, cb.shift, cb.nb, cb.cur + o, h->tp_pairs,
+                                                   (unsigned)j0, nr);
+  pair_pass_kernel<false><<<grid, 256, 0, h->aux>>>(h->tp_pairs + j0, n, cb.tickets + k, h->rcursor, nullptr, 0, nr);
+}
+
+// After the last chunk (and the upload's checks): row offsets, then the scatter.
+bm_status chunked_end(bm_handle* h, const ChunkBuild& cb, int nr) {
+  size_t tmp_bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, h->rcursor, h->roffs, nr + 1, h->aux);
+  cub::DeviceScan::ExclusiveSum(h->tp_tmp, tmp_bytes, h->rcursor, h->roffs, nr + 1, h->aux);
+  BM_CUDA(cudaMemcpyAsync(h->rcursor, h->roffs, sizeof(unsigned) * ((size_t)nr + 1), cudaMemcpyDeviceToDevice, h->aux));
+  run_tiles_kernel<<<1, 1024, 0, h->aux>>>(cb.cnt, cb.K, cb.nb, cb.tpre);
+  pair_scatter_runs_kernel<<<h->sms * 8, 256, 0, h->aux>>>(h->tp_pairs, cb.start, cb.cnt, cb.tpre, cb.K, cb.nb,
+                                                          cb.tickets + cb.K, h->rcursor, h->radj, nr);
+  BM_CUDA(cudaGetLastError());
+  BM_CUDA(cudaEventRecord(h->ev_ri, h->aux));  // every run waits for it (launch)
   h->bu_built = true;
   return BM_OK;
 }
@@ -389,6 +564,7 @@ void apply_persist(bm_handle* h) {
 
 bm_status launch(bm_handle* h, int v, Params& p, float* ms) {
   apply_persist(h);
+  BM_CUDA(cudaStreamWaitEvent(h->stream, h->ev_ri, 0));  // a row index still being built with the upload
   const int G = grid_for(h, v);
   void* args[] = {&p};
   BM_CUDA(cudaEventRecord(h->ev0, h->stream));
@@ -680,6 +856,7 @@ bm_status bm_create(int32_t device, bm_handle** out) {
   if (e == cudaSuccess) e = cudaEventCreate(&h->ev0);
   if (e == cudaSuccess) e = cudaEventCreate(&h->ev1);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_up, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_ri, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->aux, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void**>(&h->ctl), sizeof(Ctrl));
   if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void**>(&h->recs), sizeof(PhaseRec) * h->rec_cap);
@@ -716,6 +893,7 @@ bm_status bm_destroy(bm_handle* h) {
   dfree(h->tp_pcur);
   dfree(h->tp_pairs);
   dfree(h->tp_tmp);
+  dfree(h->tp_runs);
   dfree(h->rcursor);
   dfree(h->fbit);
   dfree(h->croot);
@@ -732,6 +910,11 @@ bm_status bm_destroy(bm_handle* h) {
   if (h->ev0) cudaEventDestroy(h->ev0);
   if (h->ev1) cudaEventDestroy(h->ev1);
   if (h->ev_up) cudaEventDestroy(h->ev_up);
+  if (h->ev_ri) cudaEventDestroy(h->ev_ri);
+  for (int i = 0; i < kStgBufs; ++i) {
+    if (h->stg_buf[i]) cudaFreeHost(h->stg_buf[i]);
+    if (h->stg_ev[i]) cudaEventDestroy(h->stg_ev[i]);
+  }
   if (h->aux) cudaStreamDestroy(h->aux);
   if (h->own) cudaStreamDestroy(h->own);
   delete h;
@@ -758,8 +941,10 @@ bm_status bm_upload_csc(bm_handle* h, int32_t nc, int32_t nr, const int64_t* cxa
   if (E > 0 && !cadj) return fail(BM_ERR_INVALID_ARG, "null cadj");
   BM_CUDA(cudaSetDevice(h->device));
   BM_CUDA(cudaStreamSynchronize(h->stream));
+  BM_CUDA(cudaStreamSynchronize(h->aux));  // (a row index build of the previous graph)
   h->nc = -1;
   h->has_init = false;
+  h->bu_built = false;
   h->resumable = false;
   // graph
   BM_CUDA(dalloc(h->caps, h->offs, (size_t)nc + 1));
@@ -793,23 +978,41 @@ bm_status bm_upload_csc(bm_handle* h, int32_t nc, int32_t nr, const int64_t* cxa
   BM_CUDA(dalloc(h->caps, h->F[1], (size_t)nc + kFSlack(nc)));
   // offsets: int64 staged in F[1] (16 B per column >= 8 B per offset), narrowed to u32
   long long* staged = reinterpret_cast<long long*>(h->F[1]);
-  BM_CUDA(cudaMemcpyAsync(staged, cxadj, sizeof(long long) * ((size_t)nc + 1), cudaMemcpyHostToDevice, h->stream));
+  bm_status xs = xfer_h2d(h, staged, cxadj, sizeof(long long) * ((size_t)nc + 1), h->stream);
+  if (xs != BM_OK) return xs;
   BM_CUDA(cudaMemsetAsync(h->scratch, 0, sizeof(unsigned long long) * 5, h->stream));
   const int blocks = std::max(1, std::min(h->sms * 8, (nc + 256) / 256));
   convert_offsets_kernel<<<blocks, 256, 0, h->stream>>>(staged, h->offs, nc, E, h->scratch, h->scratch + 4);
   BM_CUDA(cudaGetLastError());
   BM_CUDA(cudaEventRecord(h->ev_up, h->stream));
   BM_CUDA(cudaStreamWaitEvent(h->aux, h->ev_up, 0));
-  // adjacency in chunks: the check of chunk k runs on the aux stream while
-  // chunk k+1 is still being copied
-  const long long chunk = 32ll << 20;  // elements (128 MB)
+  const char* spb = getenv("BM_PREBUILD");  // build the row index with the upload: 1 always, 0 never
+  // default: graphs on which AUTO pulls from the first run (bu_huge; E >= 6 nc is implied by bu_auto)
+  const bool prebuild = spb && *spb ? atoi(spb) != 0 : (nr >= (1 << 26) && E >= 6ll * nc && E > 0);
+  long long chunk = 32ll << 20;  // adjacency elements per chunk (128 MB)
+  if (const char* ch = getenv("BM_UPLOAD_CHUNK")) chunk = std::max(4096ll, atoll(ch));  // tests: many chunks
+  ChunkBuild cbuild;
+  if (prebuild && E > 0) {
+    // the chunk partition walks the offsets: they must be valid before the first chunk
+    unsigned long long bad0 = 0;
+    BM_CUDA(cudaMemcpyAsync(&bad0, h->scratch, sizeof(bad0), cudaMemcpyDeviceToHost, h->stream));
+    BM_CUDA(cudaStreamSynchronize(h->stream));
+    if (bad0)
+      return fail(BM_ERR_INVALID_ARG, "cxadj is not a valid offset array (cxadj[0]=0, non-decreasing, cxadj[nc]=E)");
+    bm_status bs = chunked_begin(h, nc, nr, E, chunk, cbuild);
+    if (bs != BM_OK) return bs;
+  }
+  // adjacency in chunks: the check of chunk k (and its share of the row index)
+  // runs on the aux stream while chunk k+1 is still being copied
   for (long long j0 = 0; j0 < E; j0 += chunk) {
     const long long j1 = std::min(E, j0 + chunk);
-    BM_CUDA(cudaMemcpyAsync(h->adj + j0, cadj + j0, sizeof(int) * (size_t)(j1 - j0), cudaMemcpyHostToDevice, h->stream));
+    xs = xfer_h2d(h, h->adj + j0, cadj + j0, sizeof(int) * (size_t)(j1 - j0), h->stream);
+    if (xs != BM_OK) return xs;
     BM_CUDA(cudaEventRecord(h->ev_up, h->stream));
     BM_CUDA(cudaStreamWaitEvent(h->aux, h->ev_up, 0));
     const int cb = (int)std::max<long long>(1, std::min<long long>((long long)h->sms * 8, (j1 - j0 + 255) / 256));
     check_adj_flat_kernel<<<cb, 256, 0, h->aux>>>(h->adj, j0, j1, nr, h->scratch + 1, h->scratch + 2);
+    if (cbuild.on) chunked_chunk(h, cbuild, (int)(j0 / chunk), nc, nr, j0, j1);
   }
   if (nc > 0) col_start_pairs_kernel<<<blocks, 256, 0, h->aux>>>(h->offs, h->adj, nc, h->scratch + 3);
   BM_CUDA(cudaGetLastError());
@@ -830,7 +1033,11 @@ bm_status bm_upload_csc(bm_handle* h, int32_t nc, int32_t nr, const int64_t* cxa
   if (bad[1]) return fail(BM_ERR_INVALID_ARG, "row index out of range in cadj");
   bad[2] -= bad[3];  // descending pairs inside columns
   h->sorted = bad[2] == 0;
-  h->bu_built = false;  // the row index is built on the first bottom-up run
+  h->bu_built = false;  // the row index is built on the first bottom-up run ...
+  if (cbuild.on) {      // ... or now, finishing the share the chunks did (the runs wait for it)
+    bm_status bs = chunked_end(h, cbuild, nr);
+    if (bs != BM_OK) return bs;
+  }
   h->nr = nr;
   {
     bm_status fs = rows_fill(h, 1, -1);
@@ -849,6 +1056,24 @@ bm_status bm_prepare_row_index(bm_handle* h) {
   BM_CUDA(cudaSetDevice(h->device));
   if (!h->bu_built) {
     s = build_transpose(h, h->nc, h->nr, h->E);
+    if (s != BM_OK) return s;
+  }
+  BM_CUDA(cudaStreamSynchronize(h->stream));
+  return BM_OK;
+}
+
+bm_status bm_download_row_index(bm_handle* h, uint32_t* roffs, int32_t* radj) {
+  bm_status s = check_handle(h, true);
+  if (s != BM_OK) return s;
+  if (!h->bu_built || !h->bu_enabled) return fail(BM_ERR_INVALID_ARG, "the row index has not been built");
+  BM_CUDA(cudaSetDevice(h->device));
+  BM_CUDA(cudaStreamWaitEvent(h->stream, h->ev_ri, 0));
+  if (roffs) {
+    s = xfer_d2h(h, roffs, h->roffs, sizeof(unsigned) * ((size_t)h->nr + 1), h->stream);
+    if (s != BM_OK) return s;
+  }
+  if (radj) {
+    s = xfer_d2h(h, radj, h->radj, sizeof(int) * (size_t)h->E, h->stream);
     if (s != BM_OK) return s;
   }
   BM_CUDA(cudaStreamSynchronize(h->stream));
@@ -876,8 +1101,14 @@ bm_status bm_load_matching(bm_handle* h, const int32_t* rmatch, const int32_t* c
   if (s != BM_OK) return s;
   if ((!rmatch && h->nr > 0) || (!cmatch && h->nc > 0)) return fail(BM_ERR_INVALID_ARG, "null matching array");
   BM_CUDA(cudaSetDevice(h->device));
-  if (h->nr > 0) BM_CUDA(cudaMemcpyAsync(h->rmatch0, rmatch, sizeof(int) * h->nr, cudaMemcpyHostToDevice, h->stream));
-  if (h->nc > 0) BM_CUDA(cudaMemcpyAsync(h->cmatch0, cmatch, sizeof(int) * h->nc, cudaMemcpyHostToDevice, h->stream));
+  if (h->nr > 0) {
+    s = xfer_h2d(h, h->rmatch0, rmatch, sizeof(int) * h->nr, h->stream);
+    if (s != BM_OK) return s;
+  }
+  if (h->nc > 0) {
+    s = xfer_h2d(h, h->cmatch0, cmatch, sizeof(int) * h->nc, h->stream);
+    if (s != BM_OK) return s;
+  }
   BM_CUDA(cudaMemsetAsync(h->scratch, 0, sizeof(unsigned long long), h->stream));
   const int blocks = std::max(1, std::min(h->sms * 8, (std::max(h->nc, h->nr) + 255) / 256));
   init_check_kernel<<<blocks, 256, 0, h->stream>>>(h->offs, h->adj, h->sorted, h->rmatch0, h->cmatch0, h->nc,
@@ -938,7 +1169,10 @@ bm_status bm_download_matching(bm_handle* h, int32_t* rmatch, int32_t* cmatch) {
   BM_CUDA(cudaSetDevice(h->device));
   s = rows_to_host(h, rmatch, 0);
   if (s != BM_OK) return s;
-  if (cmatch && h->nc > 0) BM_CUDA(cudaMemcpyAsync(cmatch, h->cmatch, sizeof(int) * h->nc, cudaMemcpyDeviceToHost, h->stream));
+  if (cmatch && h->nc > 0) {
+    s = xfer_d2h(h, cmatch, h->cmatch, sizeof(int) * h->nc, h->stream);
+    if (s != BM_OK) return s;
+  }
   BM_CUDA(cudaStreamSynchronize(h->stream));
   return BM_OK;
 }
@@ -993,7 +1227,10 @@ bm_status bm_match(bm_handle* h, const bm_match_opts* opts, int32_t* rmatch, int
   if (opts->init == BM_INIT_GIVEN) {
     s = rows_from_host(h, rmatch);
     if (s != BM_OK) return s;
-    if (h->nc > 0) BM_CUDA(cudaMemcpyAsync(h->cmatch, cmatch, sizeof(int) * h->nc, cudaMemcpyHostToDevice, h->stream));
+    if (h->nc > 0) {
+      s = xfer_h2d(h, h->cmatch, cmatch, sizeof(int) * h->nc, h->stream);
+      if (s != BM_OK) return s;
+    }
   } else {
     s = rows_fill(h, 0, -1);
     if (s != BM_OK) return s;
@@ -1069,6 +1306,7 @@ bm_status bm_permute_random(bm_handle* h, const int32_t* cperm, const int32_t* r
     }
   }
   BM_CUDA(cudaSetDevice(h->device));
+  BM_CUDA(cudaStreamSynchronize(h->aux));  // (a row index still being built with the upload)
   const int nc = h->nc, nr = h->nr;
   const long long E = h->E;
   int *dcp = nullptr, *drp = nullptr, *nadj = nullptr, *sadj = nullptr;
@@ -1140,7 +1378,10 @@ bm_status bm_verify(bm_handle* h, const int32_t* rmatch, const int32_t* cmatch, 
   BM_CUDA(cudaSetDevice(h->device));
   s = rows_from_host(h, rmatch);  // leaves the plain copy in rtmp for validate_kernel
   if (s != BM_OK) return s;
-  if (h->nc > 0) BM_CUDA(cudaMemcpyAsync(h->cmatch, cmatch, sizeof(int) * h->nc, cudaMemcpyHostToDevice, h->stream));
+  if (h->nc > 0) {
+    s = xfer_h2d(h, h->cmatch, cmatch, sizeof(int) * h->nc, h->stream);
+    if (s != BM_OK) return s;
+  }
   BM_CUDA(cudaMemsetAsync(h->scratch, 0, sizeof(unsigned long long) * 4, h->stream));
   const int blocks = std::max(1, std::min(h->sms * 8, (std::max(h->nc, h->nr) + 255) / 256));
   validate_kernel<<<blocks, 256, 0, h->stream>>>(h->offs, h->adj, h->nc, h->nr, h->sorted, h->rtmp,

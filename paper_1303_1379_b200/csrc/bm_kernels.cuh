@@ -2270,25 +2270,32 @@ constexpr int kTpChunk = 2048;   // edges per CTA step of bucket_partition (8 pe
 constexpr int kPairChunk = 4096; // pairs per CTA step of the ordered passes (16 per thread)
 constexpr int kMaxBuckets = 512;
 
-__global__ void __launch_bounds__(256) bucket_hist_kernel(const int* adj, unsigned E, int shift, int nb,
+// Edges [0, E) of adj; rows outside [0, nr) are left out (the partition below
+// skips them too), so a chunk whose range check has not been read yet is safe.
+__global__ void __launch_bounds__(256) bucket_hist_kernel(const int* adj, unsigned E, int shift, int nb, int nr,
                                                           unsigned* bcount) {
   __shared__ unsigned hist[kMaxBuckets];
   for (int b = threadIdx.x; b < nb; b += blockDim.x) hist[b] = 0;
   __syncthreads();
   for (unsigned long long j = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; j < E;
-       j += (unsigned long long)gridDim.x * blockDim.x)
-    atomicAdd(&hist[ld_ro(adj + j) >> shift], 1u);
+       j += (unsigned long long)gridDim.x * blockDim.x) {
+    const unsigned r = (unsigned)ld_ro(adj + j);
+    if (r < (unsigned)nr) atomicAdd(&hist[r >> shift], 1u);
+  }
   __syncthreads();
   for (int b = threadIdx.x; b < nb; b += blockDim.x)
     if (hist[b]) atomicAdd(bcount + b, hist[b]);
 }
 
-// pcur[b] = first pair slot of bucket b (exclusive scan of nb <= 512 counts).
-__global__ void bucket_base_kernel(const unsigned* bcount, int nb, unsigned* pcur) {
+// pcur[b] = first pair slot of bucket b (base + exclusive scan of nb <= 512
+// counts); start, when given, keeps a copy (the run table of a chunked build).
+__global__ void bucket_base_kernel(const unsigned* bcount, int nb, unsigned* pcur, unsigned base = 0,
+                                   unsigned* start = nullptr) {
   if (threadIdx.x == 0) {
-    unsigned run = 0;
+    unsigned run = base;
     for (int b = 0; b < nb; ++b) {
       pcur[b] = run;
+      if (start) start[b] = run;
       run += bcount[b];
     }
   }
@@ -2303,9 +2310,10 @@ __device__ __forceinline__ int column_of(const unsigned* offs, int lo, int hi, u
   return lo;
 }
 
+// Edges [jbase, jbase + E) (global adjacency positions; offs must be valid).
 __global__ void __launch_bounds__(256) bucket_partition_kernel(const unsigned* offs, const int* adj, int col_base, int nc,
                                                                 unsigned E, int shift, int nb, unsigned* pcur,
-                                                                int2* pairs) {
+                                                                int2* pairs, unsigned jbase = 0, int nr = INT_MAX) {
   __shared__ unsigned hist[kMaxBuckets];
   __shared__ unsigned base[kMaxBuckets];   // global slot of this chunk's run of each bucket
   __shared__ unsigned lbase[kMaxBuckets];  // its slot in the stage
@@ -2317,7 +2325,8 @@ __global__ void __launch_bounds__(256) bucket_partition_kernel(const unsigned* o
   const unsigned nchunks = (unsigned)(((unsigned long long)E + kTpChunk - 1) / kTpChunk);
   for (unsigned ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
     // (64-bit end: E may be within one chunk of 2^32)
-    const unsigned j0 = ch * kTpChunk, j1 = (unsigned)min((unsigned long long)E, (unsigned long long)j0 + kTpChunk);
+    const unsigned j0 = jbase + ch * kTpChunk;
+    const unsigned j1 = (unsigned)min((unsigned long long)jbase + E, (unsigned long long)j0 + kTpChunk);
     for (int b = threadIdx.x; b < nb; b += blockDim.x) hist[b] = 0;
     if (threadIdx.x < 2) span[threadIdx.x] = column_of(offs, 0, nc, threadIdx.x ? j1 - 1 : j0) + threadIdx.x;
     __syncthreads();
@@ -2336,7 +2345,8 @@ __global__ void __launch_bounds__(256) bucket_partition_kernel(const unsigned* o
         while (j >= next) next = ld_ro(offs + (++col) + 1);  // empty columns are skipped
         row[k] = ld_ro(adj + j);
         cols[k] = col_base + col;  // (global id: a rank's slice starts at col_base)
-        rank[k] = (unsigned short)atomicAdd(&hist[row[k] >> shift], 1u);
+        if ((unsigned)row[k] < (unsigned)nr) rank[k] = (unsigned short)atomicAdd(&hist[row[k] >> shift], 1u);
+        else row[k] = -1;  // out of range: the upload fails on it; leave it out here
       }
     }
     __syncthreads();
@@ -2371,7 +2381,8 @@ __global__ void __launch_bounds__(256) bucket_partition_kernel(const unsigned* o
       }
     __syncthreads();
     // runs of one bucket are contiguous in the stage and in the output: coalesced stores
-    for (unsigned i = threadIdx.x; i < j1 - j0; i += blockDim.x) {
+    const unsigned nstage = lbase[nb - 1] + hist[nb - 1];  // edges kept (all of them on a valid graph)
+    for (unsigned i = threadIdx.x; i < nstage; i += blockDim.x) {
       const unsigned b = sbk[i];
       pairs[base[b] + (i - lbase[b])] = stage[i];
     }
@@ -2405,6 +2416,71 @@ __global__ void __launch_bounds__(256) pair_pass_kernel(const int2* pairs, unsig
       if (kScatter) radj[atomicAdd(cursor + (rc[k].x - row_lo), 1u)] = rc[k].y;
       else atomicAdd(cursor + (rc[k].x - row_lo), 1u);
     }
+  }
+}
+
+// Chunked build (bm_upload_csc overlaps it with the copy): chunk k of the
+// upload partitions its own edges into its own slice of the pairs, bucket by
+// bucket, so that bucket b of chunk k is the run [start[k nb + b], + cnt[..]).
+// The scatter then takes the runs bucket-major (every chunk's run of bucket 0,
+// then of bucket 1, ...) so that, as in the one-pass build, the grid works
+// inside one bucket's L2-sized slice of the index at a time.
+// tpre = exclusive prefix of the runs' tile counts in bucket-major order.
+__global__ void __launch_bounds__(1024) run_tiles_kernel(const unsigned* cnt, int K, int nb, unsigned* tpre) {
+  __shared__ unsigned wsum[32];
+  const int n = K * nb;
+  const int per = (n + blockDim.x - 1) / blockDim.x;
+  const int i0 = threadIdx.x * per, i1 = min(n, i0 + per);
+  unsigned t = 0;
+  for (int i = i0; i < i1; ++i) {  // i = b K + k (bucket-major)
+    const int b = i / K, k = i % K;
+    t += (cnt[k * nb + b] + kPairChunk - 1) / kPairChunk;
+  }
+  const unsigned incl = warp_incl_scan(t);
+  if (lane_id() == 31) wsum[threadIdx.x >> 5] = incl;
+  __syncthreads();
+  unsigned run = incl - t;
+  for (int w = 0; w < (int)(threadIdx.x >> 5); ++w) run += wsum[w];
+  for (int i = i0; i < i1; ++i) {
+    tpre[i] = run;
+    const int b = i / K, k = i % K;
+    run += (cnt[k * nb + b] + kPairChunk - 1) / kPairChunk;
+  }
+  if (i1 == n && i0 < i1) tpre[n] = run;
+  if (n == 0 && threadIdx.x == 0) tpre[0] = 0;
+}
+
+__global__ void __launch_bounds__(256) pair_scatter_runs_kernel(const int2* pairs, const unsigned* start,
+                                                                const unsigned* cnt, const unsigned* tpre, int K,
+                                                                int nb, unsigned* ticket, unsigned* cursor, int* radj,
+                                                                int nr) {
+  __shared__ unsigned chunk;
+  constexpr int kPer = kPairChunk / 256;
+  const int n = K * nb;
+  const unsigned total = ld_ro(tpre + n);
+  for (;;) {
+    if (threadIdx.x == 0) chunk = atomicAdd(ticket, 1u);
+    __syncthreads();
+    const unsigned t = chunk;
+    __syncthreads();
+    if (t >= total) break;
+    int lo = 0, hi = n;  // the run holding tile t: tpre[lo] <= t < tpre[lo + 1]
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (ld_ro(tpre + mid) <= t) lo = mid; else hi = mid;
+    }
+    const int b = lo / K, k = lo % K;
+    const unsigned s0 = ld_ro(start + k * nb + b), c0 = ld_ro(cnt + k * nb + b);
+    const unsigned j0 = (t - ld_ro(tpre + lo)) * kPairChunk;
+    int2 rc[kPer];
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {
+      const unsigned j = j0 + q * 256 + threadIdx.x;
+      rc[q] = j < c0 ? pairs[(unsigned long long)s0 + j] : make_int2(-1, 0);
+    }
+#pragma unroll
+    for (int q = 0; q < kPer; ++q)
+      if ((unsigned)rc[q].x < (unsigned)nr) radj[atomicAdd(cursor + rc[q].x, 1u)] = rc[q].y;
   }
 }
 

@@ -482,7 +482,7 @@ bm_status bm_mg_row_index_begin(bm_mg* h) {
   BM_CUDA(cudaMemsetAsync(h->out_idx, 0, sizeof(unsigned) * (2 * bmg::kMaxBuckets + 4), h->stream));
   if (h->E > 0) {
     const int grid = h->sms * 8;
-    bmg::bucket_hist_kernel<<<grid, 256, 0, h->stream>>>(h->adj, (unsigned)h->E, h->shift, h->nb, bcount);
+    bmg::bucket_hist_kernel<<<grid, 256, 0, h->stream>>>(h->adj, (unsigned)h->E, h->shift, h->nb, INT_MAX, bcount);
     bmg::bucket_base_kernel<<<1, 32, 0, h->stream>>>(bcount, h->nb, pcur);
     const int pa = (int)std::max<long long>(1, std::min<long long>(grid, (h->E + bmg::kTpChunk - 1) / bmg::kTpChunk));
     bmg::bucket_partition_kernel<<<pa, 256, 0, h->stream>>>(h->offs, h->adj, h->clo, ncl, (unsigned)h->E, h->shift, h->nb,
