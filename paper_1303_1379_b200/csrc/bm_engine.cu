@@ -175,7 +175,7 @@ struct bm_handle {
   unsigned* roffs = nullptr;
   int* radj = nullptr;
   unsigned* rcursor = nullptr;
-  unsigned* fbit = nullptr;   // 2 * nfbit_words
+  unsigned* fbit = nullptr;   // kNumFbit * nfbit_words
   int nfbit_words = 0;
   int* croot = nullptr;
   int* rtmp = nullptr;  // plain nr-int staging for host <-> device row arrays
@@ -364,9 +364,9 @@ bm_status transpose_alloc(bm_handle* h, int nc, int nr, long long E, int* shift_
   if (!h->bu_enabled) return BM_OK;
   BM_CUDA(dalloc(h->caps, h->roffs, (size_t)nr + 1));
   BM_CUDA(dalloc(h->caps, h->rcursor, (size_t)nr + 1));
-  BM_CUDA(dalloc(h->caps, h->radj, (size_t)E));
+  BM_CUDA(dalloc(h->caps, h->radj, (size_t)E + 4));  // (+4: the pulled probes read aligned groups of 4)
   h->nfbit_words = (nc + 31) / 32;
-  BM_CUDA(dalloc(h->caps, h->fbit, (size_t)2 * h->nfbit_words));
+  BM_CUDA(dalloc(h->caps, h->fbit, (size_t)kNumFbit * h->nfbit_words));
   BM_CUDA(dalloc(h->caps, h->croot, (size_t)nc));
   BM_CUDA(dalloc(h->caps, h->P, (size_t)nc + kFSlack(nc)));
   int shift = 0;
@@ -404,7 +404,7 @@ bm_status build_transpose(bm_handle* h, int nc, int nr, long long E) {
     int2* pairs = h->tp_pairs;
     BM_CUDA(cudaMemsetAsync(h->tp_pcur, 0, sizeof(unsigned) * (2 * kMaxBuckets + 2), h->stream));
     BM_CUDA(cudaMemsetAsync(h->rcursor, 0, sizeof(unsigned) * ((size_t)nr + 1), h->stream));
-    BM_CUDA(cudaMemsetAsync(h->fbit, 0, sizeof(unsigned) * 2 * h->nfbit_words, h->stream));
+    BM_CUDA(cudaMemsetAsync(h->fbit, 0, sizeof(unsigned) * kNumFbit * h->nfbit_words, h->stream));
     const int grid = h->sms * 8;
     bucket_hist_kernel<<<grid, 256, 0, h->stream>>>(h->adj, (unsigned)E, shift, nb, nr, bcount);
     bucket_base_kernel<<<1, 32, 0, h->stream>>>(bcount, nb, pcur);
@@ -447,7 +447,7 @@ bm_status chunked_begin(bm_handle* h, int nc, int nr, long long E, long long chu
   BM_CUDA(cudaMemsetAsync(cb.cnt, 0, sizeof(unsigned) * kn, h->aux));
   BM_CUDA(cudaMemsetAsync(cb.tickets, 0, sizeof(unsigned) * ((size_t)cb.K + 1), h->aux));
   BM_CUDA(cudaMemsetAsync(h->rcursor, 0, sizeof(unsigned) * ((size_t)nr + 1), h->aux));
-  BM_CUDA(cudaMemsetAsync(h->fbit, 0, sizeof(unsigned) * 2 * h->nfbit_words, h->aux));
+  BM_CUDA(cudaMemsetAsync(h->fbit, 0, sizeof(unsigned) * kNumFbit * h->nfbit_words, h->aux));
   cb.on = true;
   return BM_OK;
 }
@@ -530,7 +530,7 @@ bm_status prepare_fresh(bm_handle* h, bool reset_pred = false) {
   }
   BM_CUDA(cudaMemsetAsync(h->ctl, 0, sizeof(Ctrl), h->stream));
   BM_CUDA(cudaMemsetAsync(h->dead, 0, sizeof(unsigned) * std::max(h->ndead_words, 1), h->stream));
-  if (h->fbit) BM_CUDA(cudaMemsetAsync(h->fbit, 0, sizeof(unsigned) * 2 * std::max(h->nfbit_words, 1), h->stream));
+  if (h->fbit) BM_CUDA(cudaMemsetAsync(h->fbit, 0, sizeof(unsigned) * kNumFbit * std::max(h->nfbit_words, 1), h->stream));
   return BM_OK;
 }
 
@@ -597,8 +597,7 @@ Params make_params(bm_handle* h, const bm_match_opts& o) {
   p.dead = h->dead;
   p.roffs = (pulls(h, o) && h->bu_enabled && h->bu_built) ? h->roffs : nullptr;
   p.radj = h->radj;
-  p.fbit[0] = h->fbit;
-  p.fbit[1] = h->fbit ? h->fbit + h->nfbit_words : nullptr;
+  for (int b = 0; b < kNumFbit; ++b) p.fbit[b] = h->fbit ? h->fbit + (size_t)b * h->nfbit_words : nullptr;
   p.croot = h->croot;
   p.nfbit_words = h->nfbit_words;
   // pull rule (tuning knobs read per run): BM_BU_FRAC selects the plain edge-share

@@ -169,7 +169,7 @@ struct PeerPtrs {
   int* bfs;         // root marks
   int* croot;       // root of each frontier column (pulled levels)
   unsigned* dead;   // the rank's replica of the dead-root bitmap (all nc bits)
-  unsigned* fbit;   // the rank's replicas of the two frontier bitmaps (2 x all nc bits)
+  unsigned* fbit;   // the rank's replicas of the frontier bitmaps (kNumFbit x all nc bits)
   int2* P;          // pair inbox: (column, root) winners routed to the column's owner
   int* EP;          // endpoint rows found by the rank
   int4* F0;
@@ -185,6 +185,11 @@ struct alignas(128) MgTeam {
   unsigned pad1[30];
 };
 #endif
+
+// Frontier bitmaps of pulled levels, rotating by level (lv % 3): a level reads
+// its own, its winners mark the next one, and the one two levels back is
+// cleared meanwhile (no barrier needed between the clear and the next marks).
+constexpr int kNumFbit = 3;
 
 struct Params {
   int nc, nr;
@@ -223,7 +228,7 @@ struct Params {
   // bottom-up levels (see bu_sweep); roffs == nullptr disables them
   const unsigned* roffs;   // nr + 1, transposed adjacency (rows -> columns)
   const int* radj;
-  unsigned* fbit[2];       // frontier bitmaps (nc bits each), alternating by level
+  unsigned* fbit[kNumFbit];  // frontier bitmaps (nc bits each), rotating by level (lv % kNumFbit)
   int* croot;              // root of each frontier column (bottom-up levels)
   int nfbit_words;
   unsigned long long bu_min_edges;  // bu_rule 0: a level with at least this many frontier edges goes bottom-up
@@ -780,8 +785,8 @@ __device__ __forceinline__ void materialize(const Params& p, Smem& sm, int4* F, 
 // bu_prep: the frontier of level lv as a bitmap (+ the root of each member).
 // The bitmap is clean: a bottom-up level clears its own right after the grid
 // barrier that ends it (bu_clear; the next level uses the other bitmap).
-__device__ __forceinline__ void bu_clear(const Params& p, int lv) {
-  unsigned* fb = p.fbit[lv & 1];
+__device__ __forceinline__ void bu_clear(const Params& p, int b) {
+  unsigned* fb = p.fbit[b];
   for (unsigned long long k = global_thread(); k < (unsigned long long)p.nfbit_words; k += global_threads())
     st_plain(reinterpret_cast<int*>(fb) + k, 0);
 }
@@ -790,7 +795,7 @@ __device__ __forceinline__ void bu_clear(const Params& p, int lv) {
 template <bool WR>
 __device__ __forceinline__ void bu_prep(const Params& p, Smem& sm, const int4* F, bool pairs, unsigned ls,
                                         unsigned n, int lv) {
-  unsigned* fb = p.fbit[lv & 1];
+  unsigned* fb = p.fbit[lv % kNumFbit];
   unsigned live = 0;
   constexpr int K = 8;  // entries per thread in flight (the loop is latency-bound otherwise)
   const unsigned long long GT = global_threads();
@@ -830,6 +835,13 @@ __device__ __forceinline__ void bu_prep(const Params& p, Smem& sm, const int4* F
 #ifndef BM_BU_PROBE
 #define BM_BU_PROBE 4
 #endif
+#ifndef BM_BU_MARK
+#define BM_BU_MARK 1  // wide levels mark the next level's frontier bitmap (0: bu_prep every pulled level)
+#endif
+constexpr bool BU_MARK = BM_BU_MARK != 0;
+#ifndef BM_BU_VEC
+#define BM_BU_VEC 0  // pulled probes: 1 = one aligned int4 load per round, 0 = four scalar loads
+#endif
 // Warp-autonomous pulled level. Every warp owns chunks of 128 consecutive rows
 // (grid-stride over the warps of the grid) and keeps a queue of candidate rows
 // in shared memory: screening a chunk reads the rows' state and their row-index
@@ -845,8 +857,8 @@ __device__ __forceinline__ void bu_prep(const Params& p, Smem& sm, const int4* F
 __device__ __forceinline__ void bu_share(const Params& p, int lv) {
   if (p.col_lo >= p.col_hi) return;  // owns no column (the last word belongs to the rank that ends at nc)
   const unsigned w0 = (unsigned)p.col_lo >> 5, w1 = ((unsigned)p.col_hi + 31) >> 5;
-  const unsigned* src = p.fbit[lv & 1];
-  const unsigned long long off = (unsigned long long)(lv & 1) * p.nfbit_words;
+  const unsigned* src = p.fbit[lv % kNumFbit];
+  const unsigned long long off = (unsigned long long)(lv % kNumFbit) * p.nfbit_words;
   for (unsigned long long k = w0 + global_thread(); k < w1; k += global_threads()) {
     const unsigned v = (unsigned)ld_cg(reinterpret_cast<const int*>(src) + k);
     for (int q = 0; q < p.world; ++q)
@@ -855,9 +867,14 @@ __device__ __forceinline__ void bu_share(const Params& p, int lv) {
 }
 #endif
 
+// fb_next (nullable): the next level's bitmap, marked here for every winner
+// together with its root (croot), so that a pulled successor needs no bu_prep.
+// marked_in: this level's bitmap was marked that way by the level before, so
+// it still holds columns of trees that have found their path since (WR skips
+// them at the hit, as bu_prep would have left them out).
 template <bool WR, bool IMP>
 __device__ __forceinline__ void bu_sweep_q(const Params& p, Smem& sm, unsigned out_base, Slot* out, int out_slot,
-                                           int lv, int pf) {
+                                           int lv, int pf, unsigned* fb_next, bool marked_in) {
   constexpr int kWarps = kThreads / 32;
   constexpr unsigned kChunk = 128;
   constexpr unsigned kWStage = 128;  // winners staged per warp
@@ -865,7 +882,7 @@ __device__ __forceinline__ void bu_sweep_q(const Params& p, Smem& sm, unsigned o
   static_assert(sizeof(BuCand) * kCandCap * kWarps + sizeof(int2) * kWStage * kWarps <= sizeof(int2) * kWBuf,
                 "candidate queues and winner stages must fit in wbuf");
   constexpr int kBuProbe = BM_BU_PROBE;
-  const unsigned* fb = p.fbit[lv & 1];
+  const unsigned* fb = p.fbit[lv % kNumFbit];
   const unsigned long long pol = policy_evict_first();
   unsigned* const path_flag = path_flag_of(p, pf);
 #if BM_MG
@@ -952,8 +969,23 @@ __device__ __forceinline__ void bu_sweep_q(const Params& p, Smem& sm, unsigned o
     if (rr >= 0) {
       int cs[kBuProbe];
       unsigned wd[kBuProbe];
+#if BM_BU_VEC
+      // one aligned 16-byte load per round: the row's entries of that group (one
+      // L2 request instead of four)
+      static_assert(kBuProbe == 4, "BM_BU_VEC probes aligned groups of 4");
+      {
+        const unsigned g0 = j & ~3u;
+        const int4 v = ld_stream4(reinterpret_cast<const int4*>(p.radj + g0), pol);
+        cs[0] = (g0 >= j && g0 < j1) ? v.x : -1;
+        cs[1] = (g0 + 1 >= j && g0 + 1 < j1) ? v.y : -1;
+        cs[2] = (g0 + 2 >= j && g0 + 2 < j1) ? v.z : -1;
+        cs[3] = (g0 + 3 < j1) ? v.w : -1;
+        j = g0;  // (advanced by kBuProbe below)
+      }
+#else
 #pragma unroll
       for (int k = 0; k < kBuProbe; ++k) cs[k] = j + k < j1 ? ld_stream(p.radj + j + k, pol) : -1;
+#endif
 #pragma unroll
       for (int k = 0; k < kBuProbe; ++k)
         wd[k] = cs[k] >= 0 ? ld_ca(reinterpret_cast<const int*>(fb) + (cs[k] >> 5)) : 0u;
@@ -964,10 +996,16 @@ __device__ __forceinline__ void bu_sweep_q(const Params& p, Smem& sm, unsigned o
         if (done || c < 0) continue;
         c_trav++;
         if (!((wd[k] >> (c & 31)) & 1)) continue;
-        const int root = ld_cg(CR(p, c));
+        const int root = WR ? ld_cg(CR(p, c)) : c;
+        // (WR) a tree that found its path after this bitmap was built expands no further
+        if (WR && marked_in && root_dead(p, root)) continue;
         if (vv >= 0) {  // matched row: its column joins the frontier below c's tree
           st_plain(RML(p, rr), vv | kVisBit);
           st_plain(PRL(p, rr), c);
+          if (fb_next) {  // the next level's frontier, ready for a pull
+            atomicOr(fb_next + (vv >> 5), 1u << (vv & 31));
+            if (WR) st_plain(CR(p, vv), root);
+          }
           win = true;
           cw = vv;
           rootw = root;
@@ -1049,7 +1087,7 @@ __device__ __forceinline__ void bu_sweep_q(const Params& p, Smem& sm, unsigned o
 template <bool WR, bool IMP, bool BU>
 __device__ __forceinline__ void expand_level(const Params& p, Smem& sm, int4* F, unsigned ls, unsigned n, unsigned T,
                              const unsigned* gin, unsigned* gout, Slot* in, Slot* out, int level, int pf,
-                             bool pairs_out, bool claim_store, int out_slot) {
+                             bool pairs_out, bool claim_store, int out_slot, unsigned* fb_next = nullptr) {
   if (T == 0) return;
   const unsigned tid = threadIdx.x;
   unsigned c_trav = 0, c_cexp = 0, c_nvis = 0, c_entries = 0;
@@ -1232,6 +1270,10 @@ __device__ __forceinline__ void expand_level(const Params& p, Smem& sm, int4* F,
               }
               st_stream(PR(p, row[k]), col, pol);
               if (p.trace) st_plain(BF(p, c), level + 1);
+              if (BU && fb_next) {  // a wide level marks its successor's bitmap (see bu_sweep_q)
+                atomicOr(fb_next + (c >> 5), 1u << (c & 31));
+                if (WR) st_plain(CR(p, c), root);
+              }
             }
           } else if (c == -1) {
             // ONE_PER_TREE: a tree that already holds an endpoint leaves the row alone
@@ -1474,6 +1516,7 @@ __device__ PhaseOut run_phase(const Params& p, Smem& sm, int cur, int parity, bo
   int lv = 0;
   bool found = false;
   bool in_pairs = false;  // this level's entries are (col, root) pairs in P (pulled-capable kernels)
+  unsigned dirty = 0;     // frontier bitmaps holding marks (bit b: fbit[b]); grid-uniform
   const unsigned long long pol_mat = policy_evict_first();
 #if BM_MG
   if (routed(p)) {
@@ -1524,7 +1567,7 @@ __device__ PhaseOut run_phase(const Params& p, Smem& sm, int cur, int parity, bo
         bu_share(p, lv);
         grid_sync(p);
       }
-      bu_sweep_q<WR, IMP>(p, sm, ls + n, outs, (lv + 1) % 3, lv, parity);
+      bu_sweep_q<WR, IMP>(p, sm, ls + n, outs, (lv + 1) % 3, lv, parity, nullptr, false);
       if (threadIdx.x == 0) sm.cnt[kStPulledLevels] += is_leader() ? 1 : 0;
     } else {
       // store claims when even one entry per frontier edge of the team fits every inbox
@@ -1534,7 +1577,7 @@ __device__ PhaseOut run_phase(const Params& p, Smem& sm, int cur, int parity, bo
     }
     const long long tb = clk();
     grid_sync(p);
-    if (bu) bu_clear(p, lv);
+    if (bu) bu_clear(p, lv % kNumFbit);
     if (threadIdx.x == 0) sm.cnt[kStCycBarrier] += clk() - tb;
     tl_mark(p, kTlLevel, n);
     tl_mark(p, kTlLevelEdges, (T & 0x7fffffffu) | (bu ? 0x80000000u : 0u));
@@ -1603,6 +1646,10 @@ __device__ PhaseOut run_phase(const Params& p, Smem& sm, int cur, int parity, bo
       Slot* ms = &ctl->mat[lv & 1];
       materialize(p, sm, F, ls, n, (lv & 1) ? p.gidx1 : p.gidx0, ms, pol_mat, false);
       grid_sync(p);
+      if (dirty & (1u << (lv % kNumFbit))) {  // the marks the level before left for a pull: unused
+        bu_clear(p, lv % kNumFbit);           // (next written two levels on, after a grid barrier)
+        dirty &= ~(1u << (lv % kNumFbit));
+      }
       tl_mark(p, kTlMat, n);
       const unsigned long long mp = ld_rlx(&ms->packed);
       T = (unsigned)(mp & kEdgeMask);
@@ -1636,11 +1683,21 @@ __device__ PhaseOut run_phase(const Params& p, Smem& sm, int cur, int parity, bo
     if (solo) __syncthreads();
     // a wide level hands its winners on as pairs (see Params::P)
     const bool pairs_out = BU && p.roffs && !p.trace && !solo && (bu || (unsigned long long)T >= p.pairs_min_edges);
+    // A wide level also marks its winners in the next level's bitmap (and their
+    // roots in croot), so that a pulled successor starts at once (no bu_prep pass
+    // of its own: one scattered croot store per column fewer, and one grid barrier).
+    unsigned* const fb_next = pairs_out && BU_MARK ? p.fbit[(lv + 1) % kNumFbit] : nullptr;
     if (bu) {
-      bu_prep<WR>(p, sm, F, in_pairs, ls, n, lv);
-      grid_sync(p);
-      tl_mark(p, kTlPrep, n);
-      bu_sweep_q<WR, IMP>(p, sm, ls + n, outs, (lv + 1) % 3, lv, parity);
+      const bool marked = (dirty >> (lv % kNumFbit)) & 1u;  // the level before marked this one
+      if (!marked) {
+        bu_prep<WR>(p, sm, F, in_pairs, ls, n, lv);
+        grid_sync(p);
+        dirty |= 1u << (lv % kNumFbit);
+        tl_mark(p, kTlPrep, n);
+      } else if (is_leader()) {
+        sm.cnt[kStCexp] += n;  // (entries; bu_prep counts the live ones)
+      }
+      bu_sweep_q<WR, IMP>(p, sm, ls + n, outs, (lv + 1) % 3, lv, parity, fb_next, marked);
       if (threadIdx.x == 0) sm.cnt[kStPulledLevels] += is_leader() ? 1 : 0;
     } else {
       // Claims by plain store (no atomic round trip; two discoverers racing on one
@@ -1649,8 +1706,9 @@ __device__ PhaseOut run_phase(const Params& p, Smem& sm, int cur, int parity, bo
       // capacity; otherwise by atomicOr, which pushes every column once.
       const bool claim_store = p.claim_store && (unsigned long long)ls + n + T <= p.fcap;
       expand_level<WR, IMP, BU>(p, sm, F, ls, n, T, (lv & 1) ? p.gidx1 : p.gidx0, (lv & 1) ? p.gidx0 : p.gidx1,
-                                in, outs, kStartLevel + lv, parity, pairs_out, claim_store, (lv + 1) % 3);
+                                in, outs, kStartLevel + lv, parity, pairs_out, claim_store, (lv + 1) % 3, fb_next);
     }
+    if (fb_next) dirty |= 1u << ((lv + 1) % kNumFbit);
 
     const long long tb = clk();
     if (solo) {
@@ -1658,7 +1716,10 @@ __device__ PhaseOut run_phase(const Params& p, Smem& sm, int cur, int parity, bo
       __syncthreads();
     } else {
       grid_sync(p);
-      if (bu) bu_clear(p, lv);  // read by nobody from here on; the next level uses the other bitmap
+      if (dirty & (1u << (lv % kNumFbit))) {  // read by nobody from here on
+        bu_clear(p, lv % kNumFbit);
+        dirty &= ~(1u << (lv % kNumFbit));
+      }
     }
     if (threadIdx.x == 0) sm.cnt[kStCycBarrier] += clk() - tb;
     tl_mark(p, kTlLevel, n);
@@ -1694,6 +1755,8 @@ __device__ PhaseOut run_phase(const Params& p, Smem& sm, int cur, int parity, bo
     }
     if (stop) break;
   }
+  for (int b = 0; b < kNumFbit; ++b)  // marks the BFS left (its last levels): clean for the next phase
+    if (dirty & (1u << b)) bu_clear(p, b);
 #if BM_MG
   }
 #endif

@@ -51,6 +51,7 @@ using bmg::Params;
 using bmg::PhaseRec;
 using bmg::Smem;
 using bmg::kMaxRanks;
+using bmg::kNumFbit;
 
 bm_status fail(bm_status s, const std::string& msg) {
   bm_internal_set_error(msg);
@@ -343,7 +344,7 @@ bm_status bm_mg_upload(bm_mg* h, int32_t nc, int32_t nr, int64_t e_total, const 
   BM_CUDA(dnew(h->croot, ncl));
   h->ndead_words = h->nfbit_words = (nc + 31) / 32;
   BM_CUDA(dnew(h->dead, h->ndead_words));
-  BM_CUDA(dnew(h->fbit, (size_t)2 * h->nfbit_words));
+  BM_CUDA(dnew(h->fbit, (size_t)kNumFbit * h->nfbit_words));
   BM_CUDA(dnew(h->P, h->fcap));
   BM_CUDA(dnew(h->F[0], h->fcap));
   BM_CUDA(dnew(h->F[1], h->fcap));
@@ -355,7 +356,7 @@ bm_status bm_mg_upload(bm_mg* h, int32_t nc, int32_t nr, int64_t e_total, const 
   BM_CUDA(dnew(h->wlog, h->log_cap));
   BM_CUDA(cudaMemset(h->pred_plain, 0xff, sizeof(int) * std::max(nrl, 1)));
   BM_CUDA(cudaMemset(h->rm, 0xff, sizeof(int) * 2 * std::max(nrl, 1)));  // mates -1, interleaved preds -1
-  BM_CUDA(cudaMemset(h->fbit, 0, sizeof(unsigned) * 2 * h->nfbit_words));
+  BM_CUDA(cudaMemset(h->fbit, 0, sizeof(unsigned) * kNumFbit * h->nfbit_words));
   // row index: bucket the rows so that one bucket's slice of an index is <= 32 MB
   {
     const long long nb_min = std::max<long long>(1, (e_total * 4 + (32ll << 20) - 1) >> 25);
@@ -546,7 +547,7 @@ bm_status bm_mg_row_index_end(bm_mg* h) {
   BM_CUDA(cudaMemcpyAsync(&last, h->roffs + nrl, sizeof(unsigned), cudaMemcpyDeviceToHost, h->stream));
   BM_CUDA(cudaStreamSynchronize(h->stream));
   mine = last;
-  BM_CUDA(dnew(h->radj, mine));
+  BM_CUDA(dnew(h->radj, mine + 4));  // (+4: the pulled probes read aligned groups of 4)
   BM_CUDA(cudaMemcpyAsync(h->rcursor, h->roffs, sizeof(unsigned) * ((size_t)nrl + 1), cudaMemcpyDeviceToDevice,
                           h->stream));
   if (total) bmg::pair_pass_kernel<true><<<grid, 256, 0, h->stream>>>(h->inbox, (unsigned)total, tickets + 1,
@@ -573,7 +574,7 @@ bm_status bm_mg_launch(bm_mg* h, const bm_match_opts* o) {
   const int ncl = h->chi - h->clo, nrl = h->rhi - h->rlo;
   BM_CUDA(cudaMemsetAsync(h->ctl, 0, sizeof(Ctrl), h->stream));
   BM_CUDA(cudaMemsetAsync(h->dead, 0, sizeof(unsigned) * h->ndead_words, h->stream));
-  BM_CUDA(cudaMemsetAsync(h->fbit, 0, sizeof(unsigned) * 2 * h->nfbit_words, h->stream));
+  BM_CUDA(cudaMemsetAsync(h->fbit, 0, sizeof(unsigned) * kNumFbit * h->nfbit_words, h->stream));
   // (the team block is zeroed once, at creation: another rank's kernel may already be
   // arriving at its barrier; a run leaves its count at 0 and its path flags clear)
   const bool pull = h->row_index && o->bottom_up != BM_BU_OFF;
@@ -620,8 +621,7 @@ bm_status bm_mg_launch(bm_mg* h, const bm_match_opts* o) {
   if (const char* se = getenv("BM_SOLO_EDGES")) p.solo_edges = h->world == 1 ? (unsigned)atol(se) : 0;
   p.roffs = pull ? h->roffs - h->rlo : nullptr;
   p.radj = h->radj;
-  p.fbit[0] = h->fbit;
-  p.fbit[1] = h->fbit + h->nfbit_words;
+  for (int b = 0; b < kNumFbit; ++b) p.fbit[b] = h->fbit + (size_t)b * h->nfbit_words;
   p.nfbit_words = h->nfbit_words;
   p.bu_rule = 1;
   p.bu_alpha = h->rs == 2 ? 14.f : 4.f;

@@ -22,8 +22,15 @@ for r in data:
     a["ideal"] += f(r[idx["L2 Theoretical Sectors Global Ideal"]])
     a["req"] += f(r[idx["L1 Tag Requests Global"]])
     a["op"] = r[idx["Access Operation"]] or a.get("op", "")
-src = {i: t.strip() for i, t in enumerate(open("paper_1303_1379_b200/csrc/bm_engine.cu").read().splitlines(), 1)}
-src.update({("bm_device.cuh", i): t.strip() for i, t in enumerate(open("paper_1303_1379_b200/csrc/bm_device.cuh").read().splitlines(), 1)})
+import os
+rev = os.environ.get("SRC_REV")  # the git revision that was profiled (default: the working tree)
+def text(path):
+    if rev:
+        return subprocess.run(["git", "show", f"{rev}:{path}"], capture_output=True, text=True).stdout
+    return open(path).read()
+src = {i: t.strip() for i, t in enumerate(text("paper_1303_1379_b200/csrc/bm_engine.cu").splitlines(), 1)}
+for hf in ("bm_device.cuh", "bm_kernels.cuh"):
+    src.update({(hf, i): t.strip() for i, t in enumerate(text("paper_1303_1379_b200/csrc/" + hf).splitlines(), 1)})
 tot = sum(a["sect"] for a in agg.values())
 print(f"total L2 theoretical global sectors {tot:.3e}")
 for line, a in sorted(agg.items(), key=lambda kv: -kv[1]["sect"])[:top]:
