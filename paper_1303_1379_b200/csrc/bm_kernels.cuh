@@ -836,11 +836,16 @@ __device__ __forceinline__ void bu_prep(const Params& p, Smem& sm, const int4* F
 #define BM_BU_PROBE 4
 #endif
 #ifndef BM_BU_MARK
-#define BM_BU_MARK 1  // wide levels mark the next level's frontier bitmap (0: bu_prep every pulled level)
+#define BM_BU_MARK 0  // 1: wide levels mark the next level's frontier bitmap at claim time instead of a bu_prep
+                      // pass (A/B on B200: +20 % on C5, +29 % on C2 -- the stores in the latency-bound loops cost more)
 #endif
 constexpr bool BU_MARK = BM_BU_MARK != 0;
 #ifndef BM_BU_VEC
 #define BM_BU_VEC 0  // pulled probes: 1 = one aligned int4 load per round, 0 = four scalar loads
+#endif
+#ifndef BM_BU_HINT
+#define BM_BU_HINT 0  // pulled levels: 1 = the streamed row screen, roots and visited sweep evict_first,
+                      // the frontier-bitmap probes evict_last (keep the bitmap in L2)
 #endif
 // Warp-autonomous pulled level. Every warp owns chunks of 128 consecutive rows
 // (grid-stride over the warps of the grid) and keeps a queue of candidate rows
@@ -884,6 +889,8 @@ __device__ __forceinline__ void bu_sweep_q(const Params& p, Smem& sm, unsigned o
   constexpr int kBuProbe = BM_BU_PROBE;
   const unsigned* fb = p.fbit[lv % kNumFbit];
   const unsigned long long pol = policy_evict_first();
+  const unsigned long long keep = policy_evict_last();
+  (void)keep;
   unsigned* const path_flag = path_flag_of(p, pf);
 #if BM_MG
   const unsigned long long rlo = (unsigned long long)p.row_lo, rhi = (unsigned long long)p.row_hi;  // own rows
@@ -920,8 +927,13 @@ __device__ __forceinline__ void bu_sweep_q(const Params& p, Smem& sm, unsigned o
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         const unsigned long long r = r0 + (unsigned long long)k * 32 + lane;
+#if BM_BU_HINT
+        v[k] = r < rhi ? ld_cg_hint(RML(p, r), pol) : -3;
+        o[k] = r <= rhi ? ld_ro_hint(p.roffs + r, pol) : 0u;  // roffs[rhi] ends the last row
+#else
         v[k] = r < rhi ? ld_cg(RML(p, r)) : -3;
         o[k] = r <= rhi ? ld_ro(p.roffs + r) : 0u;  // roffs[rhi] ends the last row
+#endif
       }
       {
         const unsigned long long r = r0 + 4 * 32;
@@ -988,7 +1000,11 @@ __device__ __forceinline__ void bu_sweep_q(const Params& p, Smem& sm, unsigned o
 #endif
 #pragma unroll
       for (int k = 0; k < kBuProbe; ++k)
+#if BM_BU_HINT
+        wd[k] = cs[k] >= 0 ? ld_ca_hint(reinterpret_cast<const int*>(fb) + (cs[k] >> 5), keep) : 0u;
+#else
         wd[k] = cs[k] >= 0 ? ld_ca(reinterpret_cast<const int*>(fb) + (cs[k] >> 5)) : 0u;
+#endif
       bool done = false;
 #pragma unroll
       for (int k = 0; k < kBuProbe; ++k) {
@@ -996,7 +1012,11 @@ __device__ __forceinline__ void bu_sweep_q(const Params& p, Smem& sm, unsigned o
         if (done || c < 0) continue;
         c_trav++;
         if (!((wd[k] >> (c & 31)) & 1)) continue;
+#if BM_BU_HINT
+        const int root = WR ? ld_cg_hint(CR(p, c), pol) : c;
+#else
         const int root = WR ? ld_cg(CR(p, c)) : c;
+#endif
         // (WR) a tree that found its path after this bitmap was built expands no further
         if (WR && marked_in && root_dead(p, root)) continue;
         if (vv >= 0) {  // matched row: its column joins the frontier below c's tree
@@ -1432,9 +1452,16 @@ __device__ __forceinline__ void sweep_visited(const Params& p) {
   const unsigned long long GT = global_threads();
   for (unsigned long long k0 = global_thread(); k0 < n4; k0 += K * GT) {
     int4 v[K];
+#if BM_BU_HINT
+    const unsigned long long pol = policy_evict_first();
+#pragma unroll
+    for (int i = 0; i < K; ++i)
+      if (k0 + i * GT < n4) v[i] = ld_cg_hint(r4 + k0 + i * GT, pol);
+#else
 #pragma unroll
     for (int i = 0; i < K; ++i)
       if (k0 + i * GT < n4) v[i] = ld_cg(r4 + k0 + i * GT);
+#endif
 #pragma unroll
     for (int i = 0; i < K; ++i) {
       if (k0 + i * GT >= n4) continue;

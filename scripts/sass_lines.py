@@ -16,20 +16,25 @@ from collections import defaultdict
 
 
 def line_map(cubin, fn):
-    out = subprocess.run(["nvdisasm", "-g", "-c", cubin], capture_output=True, text=True).stdout
+    """SASS offset -> (file, line) of the engine source that issued it: inlined
+    helpers (bm_device.cuh, CUDA headers) are attributed to their call site."""
+    out = subprocess.run(["nvdisasm", "-gi", "-c", cubin], capture_output=True, text=True).stdout
     m = {}
     cur_line = None
     in_fn = False
+    own = ("bm_kernels.cuh", "bm_engine.cu", "bm_mg.cu")
     for ln in out.splitlines():
         if ln.startswith(".text.") or "--------------------- .text." in ln:
             in_fn = (fn in ln)
             continue
         if not in_fn:
             continue
-        mm = re.search(r'//## File "(.*?)", line (\d+)', ln)
-        if mm:
-            f = mm.group(1).rsplit("/", 1)[-1]
-            cur_line = int(mm.group(2)) if f == "bm_engine.cu" else (f, int(mm.group(2)))
+        if "//## File" in ln:
+            locs = [(a.rsplit("/", 1)[-1], int(b)) for a, b in re.findall(r'"(.*?)", line (\d+)', ln)]
+            # nvdisasm keeps one level of inlining: (innermost, outermost call site)
+            pick = tuple(locs) if len(locs) > 1 else (locs[0] if locs else None)
+            if pick:
+                cur_line = pick
             continue
         mi = re.match(r"\s*/\*([0-9a-f]{4,})\*/", ln)
         if mi and cur_line is not None:
@@ -60,13 +65,15 @@ def main():
         a["samples"] += float(r[idx["# Samples"]] or 0)
         for k in stalls:
             a[k] += float(r[idx[k]] or 0)
+    import os
+    rev = os.environ.get("SRC_REV")  # the git revision that was profiled (default: the working tree)
     src = {}
-    for fname in ("bm_engine.cu", "bm_device.cuh"):
-        try:
-            for i, t in enumerate(open("paper_1303_1379_b200/csrc/" + fname).read().splitlines(), 1):
-                src[i if fname == "bm_engine.cu" else (fname, i)] = t.strip()
-        except OSError:
-            pass
+    for fname in ("bm_engine.cu", "bm_device.cuh", "bm_kernels.cuh", "bm_mg.cu"):
+        path = "paper_1303_1379_b200/csrc/" + fname
+        txt = (subprocess.run(["git", "show", f"{rev}:{path}"], capture_output=True, text=True).stdout if rev
+               else open(path).read())
+        for i, t in enumerate(txt.splitlines(), 1):
+            src[(fname, i)] = t.strip()
     tot_i = sum(a["inst"] for a in agg.values())
     tot_s = sum(a["samples"] for a in agg.values())
     print(f"total warp-inst {tot_i:.3e}  samples {tot_s:.0f}")

@@ -28,10 +28,13 @@ def text(path):
     if rev:
         return subprocess.run(["git", "show", f"{rev}:{path}"], capture_output=True, text=True).stdout
     return open(path).read()
-src = {i: t.strip() for i, t in enumerate(text("paper_1303_1379_b200/csrc/bm_engine.cu").splitlines(), 1)}
-for hf in ("bm_device.cuh", "bm_kernels.cuh"):
+src = {}
+for hf in ("bm_engine.cu", "bm_device.cuh", "bm_kernels.cuh", "bm_mg.cu"):
     src.update({(hf, i): t.strip() for i, t in enumerate(text("paper_1303_1379_b200/csrc/" + hf).splitlines(), 1)})
 tot = sum(a["sect"] for a in agg.values())
 print(f"total L2 theoretical global sectors {tot:.3e}")
 for line, a in sorted(agg.items(), key=lambda kv: -kv[1]["sect"])[:top]:
-    print(f"{str(line):>22s} {100*a['sect']/tot:5.1f}%  sect {a['sect']:.3e} ideal {a['ideal']:.3e} req {a['req']:.3e}  {src.get(line,'')[:90]}")
+    key = line[0] if line and isinstance(line[0], tuple) else line
+    call = line[-1] if line and isinstance(line[0], tuple) else None
+    txt = src.get(key, '')[:60] + (f"  <- {call[0]}:{call[1]} {src.get(call, '')[:60]}" if call else "")
+    print(f"{str(key):>28s} {100*a['sect']/tot:5.1f}%  sect {a['sect']:.3e} ideal {a['ideal']:.3e} req {a['req']:.3e}  {txt}")
