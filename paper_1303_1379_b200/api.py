@@ -374,7 +374,7 @@ class Engine:
     STAT_NAMES = ["edges_traversed", "columns_scanned", "columns_visited", "frontier_entries", "walks",
                   "walk_steps", "fix_resets", "levels", "serial_retries", "dense_fix", "cyc_tile", "cyc_window",
                   "cyc_rounds", "cyc_flush", "cyc_barrier", "cyc_other", "rows_pulled", "pulled_levels",
-                  "materialized"]
+                  "materialized", "cyc_bu_screen", "cyc_bu_probe", "cyc_bu_flush", "bu_rounds"]
 
     def debug_stats(self) -> dict:
         buf = np.zeros(32, np.uint64)

@@ -100,6 +100,10 @@ enum Stat : int {
   kStRowsPulled,  // rows a pulled level screened in as candidates (scanned their own columns)
   kStPulledLevels,
   kStMaterialized,  // frontier entries turned from (col, root) pairs into edge-tiled entries
+  kStCycBuScreen,   // pulled levels, warp cycles (lane 0's view): screening chunks into the candidate queue
+  kStCycBuProbe,    // ... probe rounds
+  kStCycBuFlush,    // ... winner and endpoint flushes
+  kStBuRounds,      // ... probe rounds (warp-level)
   kNumStats
 };
 
@@ -843,6 +847,9 @@ constexpr bool BU_MARK = BM_BU_MARK != 0;
 #ifndef BM_BU_VEC
 #define BM_BU_VEC 0  // pulled probes: 1 = one aligned int4 load per round, 0 = four scalar loads
 #endif
+#ifndef BM_BU_CYC
+#define BM_BU_CYC 0  // 1: per-part warp cycle counters in pulled levels (profiling builds)
+#endif
 #ifndef BM_BU_HINT
 #define BM_BU_HINT 0  // pulled levels: 1 = the streamed row screen, roots and visited sweep evict_first,
                       // the frontier-bitmap probes evict_last (keep the bitmap in L2)
@@ -898,6 +905,7 @@ __device__ __forceinline__ void bu_sweep_q(const Params& p, Smem& sm, unsigned o
   const unsigned long long rlo = 0, rhi = (unsigned long long)p.nr;
 #endif
   unsigned c_trav = 0, c_nvis = 0, c_rows = 0;
+  long long cy_screen = 0, cy_probe = 0, cy_flush = 0, n_rounds = 0;  // BM_BU_CYC
   const unsigned warp = threadIdx.x >> 5, lane = lane_id();
   BuCand* const q = reinterpret_cast<BuCand*>(sm.wbuf) + warp * kCandCap;
   int2* const wst = reinterpret_cast<int2*>(reinterpret_cast<BuCand*>(sm.wbuf) + kWarps * kCandCap) + warp * kWStage;
@@ -910,6 +918,7 @@ __device__ __forceinline__ void bu_sweep_q(const Params& p, Smem& sm, unsigned o
   unsigned j = 0, j1 = 0;
   for (;;) {
     // refill: the idle lanes would drain the queue and rows remain
+    long long t0 = BM_BU_CYC ? clk() : 0;
     const unsigned idle = __ballot_sync(kFull, rr < 0);
     while (qt - qh < (unsigned)__popc(idle) && chunk < nchunks) {  // (a chunk may hold no candidate)
       // move the leftovers (< 32) to the front, then screen one chunk
@@ -972,6 +981,11 @@ __device__ __forceinline__ void bu_sweep_q(const Params& p, Smem& sm, unsigned o
         c_rows++;
       }
       qh += min((unsigned)__popc(idle), avail);
+    }
+    if (BM_BU_CYC) {
+      const long long t = clk();
+      cy_screen += t - t0;
+      t0 = t;
     }
     if (!__any_sync(kFull, rr >= 0)) break;  // queue empty and every chunk screened
     // one probe round
@@ -1049,6 +1063,13 @@ __device__ __forceinline__ void bu_sweep_q(const Params& p, Smem& sm, unsigned o
       j += kBuProbe;
       if (done || j >= j1) rr = -1;
     }
+    if (BM_BU_CYC) {
+      __syncwarp();
+      const long long t = clk();
+      cy_probe += t - t0;
+      t0 = t;
+      n_rounds++;
+    }
     // stage winners in this warp's slice of wbuf; flush it when the next round might not fit
     {
       const unsigned m = __ballot_sync(kFull, win);
@@ -1081,6 +1102,13 @@ __device__ __forceinline__ void bu_sweep_q(const Params& p, Smem& sm, unsigned o
         if (ep) st_plain(p.EP + eb, myrow);
       }
     }
+    if (BM_BU_CYC) cy_flush += clk() - t0;
+  }
+  if (BM_BU_CYC && lane == 0) {
+    atomicAdd(&sm.cnt[kStCycBuScreen], (unsigned long long)cy_screen);
+    atomicAdd(&sm.cnt[kStCycBuProbe], (unsigned long long)cy_probe);
+    atomicAdd(&sm.cnt[kStCycBuFlush], (unsigned long long)cy_flush);
+    atomicAdd(&sm.cnt[kStBuRounds], (unsigned long long)n_rounds);
   }
   if (nwin) {
     __syncwarp();

@@ -94,7 +94,7 @@ def main():
                "ms_med": round(statistics.median(ms), 2), "ms": [round(x, 2) for x in ms],
                "phases": phases[1:], "levels": levels[1:], "ok": all(c == known for c in cards) if known else None,
                "card": cards[-1], "edges_traversed": ct.edges_traversed, "columns_scanned": ct.columns_scanned,
-               "stats": {k: st.get(k) for k in ("rows_pulled", "pulled_levels", "materialized")}}
+               "stats": {k: st.get(k) for k in ("rows_pulled", "pulled_levels", "materialized", "cyc_bu_screen", "cyc_bu_probe", "cyc_bu_flush", "bu_rounds", "cyc_tile", "cyc_window", "cyc_rounds", "cyc_flush", "cyc_barrier")}}
         if tl:
             out["timeline"] = timeline_summary(eng)
         print(json.dumps(out), flush=True)
