@@ -184,6 +184,9 @@ __device__ __forceinline__ void st_stream(int4* p, int4 v, unsigned long long po
 __device__ __forceinline__ void prefetch_l2(const void* p) {
   asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(p));
 }
+__device__ __forceinline__ void prefetch_l2n(const void* p) {  // normal eviction priority (streamed data)
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
 
 // ---- warp helpers ----------------------------------------------------------
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }

@@ -514,7 +514,9 @@ const void* kernel_ptr(int v) {
 }
 
 int grid_for(bm_handle* h, int v) {
-  const long long maxg = (long long)h->sms * std::max(1, h->bps[v]);
+  long long maxg = (long long)h->sms * std::max(1, h->bps[v]);
+  // sanitizer runs: BM_GRID_CTAS=1 makes every grid barrier a no-op (no cross-CTA spinning)
+  if (const char* gc = getenv("BM_GRID_CTAS")) maxg = std::max(1ll, std::min(maxg, atoll(gc)));
   const long long work = std::max<long long>({(long long)h->nc, (long long)h->nr, h->E / 8, 1});
   const long long want = (work + kThreads - 1) / kThreads;
   return (int)std::max<long long>(1, std::min(maxg, want));

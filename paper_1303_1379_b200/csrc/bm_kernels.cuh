@@ -847,6 +847,9 @@ constexpr bool BU_MARK = BM_BU_MARK != 0;
 #ifndef BM_BU_VEC
 #define BM_BU_VEC 0  // pulled probes: 1 = one aligned int4 load per round, 0 = four scalar loads
 #endif
+#ifndef BM_BU_PF
+#define BM_BU_PF 0  // pulled levels: L2 prefetch of the next chunk's row state/offsets and of each candidate's columns
+#endif
 #ifndef BM_BU_CYC
 #define BM_BU_CYC 0  // 1: per-part warp cycle counters in pulled levels (profiling builds)
 #endif
@@ -931,6 +934,21 @@ __device__ __forceinline__ void bu_sweep_q(const Params& p, Smem& sm, unsigned o
       qt = left;
       const unsigned long long r0 = rlo + chunk * kChunk;
       chunk += W;
+#if BM_BU_PF
+      // L2 prefetch of the warp's next chunk (row state, row offsets): its screen,
+      // a few probe rounds from now, then finds them in L2 instead of waiting on DRAM
+      if (chunk < nchunks) {
+        const unsigned long long rn = rlo + chunk * kChunk;
+        const unsigned long long rend = min(rhi, rn + kChunk);
+        // row state: kChunk rows x 4 B x rs -> one 32-byte sector per lane (rs = 2: 1 KB = 32 sectors)
+        const unsigned long long rr0 = rn + (unsigned long long)lane * (8 / p.rs);
+        if (rr0 < rend) prefetch_l2n(RML(p, rr0));
+        if (lane < 16) {  // offsets: 512 B = 16 sectors
+          const unsigned long long ro = rn + (unsigned long long)lane * 8;
+          if (ro <= rend) prefetch_l2n(p.roffs + ro);
+        }
+      }
+#endif
       int v[4];
       unsigned o[4], onext;
 #pragma unroll
@@ -963,6 +981,9 @@ __device__ __forceinline__ void bu_sweep_q(const Params& p, Smem& sm, unsigned o
           c.j0 = o[k];
           c.j1 = e;
           q[qt + __popc(m & ((1u << lane) - 1))] = c;
+#if BM_BU_PF
+          prefetch_l2n(p.radj + o[k]);  // the candidate's first probe group, a few rounds ahead
+#endif
         }
         qt += __popc(m);
       }

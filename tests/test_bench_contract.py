@@ -64,6 +64,9 @@ def test_b200_arm_contract():
     assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9
     e = d["e2e"]
     assert {"value", "unit", "h2d_bytes_per_step", "d2h_bytes_per_step"} <= set(e) and e["h2d_bytes_per_step"] > 0
+    assert e["pageable"]["ms_per_step"] > 0  # the shim's pageable-buffer path, same calls
+    gi = e["gpu_init"]  # GPU cheap init inside the timed region
+    assert gi["cardinality"] == 99961 and 0 < gi["initial_cardinality"] <= 99961 and gi["ms_per_step"] > 0
     assert d["gpu_launches"] > 0
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
     assert d["parity"]["ok"] and d["cardinality"] == 99961
