@@ -244,7 +244,8 @@ bm_status   bm_debug_set(bm_handle* h, int32_t key, int64_t value);
  * 4 ALTERNATE, 5 FIX rows, 6 FIX columns, 7 roots of the next phase, 8 end,
  * 9 the preceding level's frontier edges (arg; same timestamp), 10 the
  * preceding pushed level's pairs turned into entries (materialize), 11 the
- * preceding pulled level's frontier bitmap built (pull prep).
+ * preceding pulled level's frontier bitmap built (pull prep), 12 the
+ * preceding bucketed pushed level's partition pass done.
  * Written by one thread after each grid barrier (a few ns per stage). */
 bm_status   bm_timeline(bm_handle* h, uint64_t* out, int64_t cap, int64_t* n);
 

@@ -357,7 +357,7 @@ class Engine:
         return ms.value, n.value
 
     TL_KINDS = {0: "start", 1: "init", 2: "setup", 3: "level", 4: "alternate", 5: "fix_rows", 6: "fix_cols",
-                7: "roots", 8: "end", 9: "level_edges", 10: "materialize", 11: "pull_prep"}
+                7: "roots", 8: "end", 9: "level_edges", 10: "materialize", 11: "pull_prep", 12: "bucketed"}
 
     def timeline(self):
         """Stage timeline of the last run: list of (kind, arg, t_ns) from the device clock."""

@@ -172,6 +172,10 @@ struct bm_handle {
   double bu_beta = 24.0;      // ... and the frontier holds >= nc / beta columns
   long long nonempty = 0;     // columns with at least one edge (upload)
   int2* P = nullptr;          // lazy-frontier pairs (nc), pulled-capable runs only
+  int4* tb = nullptr;         // bucketed pushed levels: (row, col, root) triples (ensure_pb)
+  unsigned long long pb_max = 0;
+  int pb_shift = 0, pb_nb = 0;
+  unsigned pb_cap = 0;
   unsigned* roffs = nullptr;
   int* radj = nullptr;
   unsigned* rcursor = nullptr;
@@ -585,6 +589,41 @@ bool pulls(const bm_handle* h, const bm_match_opts& o) {
   return o.bottom_up == BM_BU_ON || (o.bottom_up == BM_BU_AUTO && h->bu_auto && (h->bu_built || h->bu_huge));
 }
 
+// Bucketed pushed levels (push_bucketed, bm_kernels.cuh): on a row state far
+// beyond L2 (interleaved layout), wide pushed levels of pulling runs first
+// group their edges by row range. Buckets hold <= 16-24 MB of row state;
+// every bucket region has room for 1.25x its share of the widest such level,
+// and an overflow region can take a whole level, so any degree skew fits.
+// BM_PB=0 disables; BM_PB_MIN / BM_PB_MAX bound the levels (edges).
+bm_status ensure_pb(bm_handle* h) {
+  const char* e = getenv("BM_PB");
+  if ((e && atoi(e) == 0) || h->rs != 2 || h->nr <= 0 || h->E <= 0) {
+    h->pb_max = 0;
+    return BM_OK;
+  }
+  unsigned long long tmax = std::min<unsigned long long>((unsigned long long)h->E, 1ull << 27);
+  if (const char* m = getenv("BM_PB_MAX")) tmax = std::min<unsigned long long>(tmax, (unsigned long long)atoll(m));
+  const unsigned long long rows_target = (24ull << 20) / (4ull * h->rs);
+  int shift = 0;
+  while ((2ull << shift) <= rows_target) ++shift;
+  while ((((unsigned long long)h->nr - 1) >> shift) + 1 > (unsigned long long)kPbMax) ++shift;
+  const int nb = (int)((((unsigned long long)h->nr - 1) >> shift) + 1);
+  unsigned long long slack = 4096;
+  if (const char* sl = getenv("BM_PB_SLACK")) slack = (unsigned long long)atoll(sl);  // tests: 0 forces overflow
+  const unsigned cap = (unsigned)std::min<unsigned long long>(0xffff0000ull, (tmax * 5 / 4) / nb + slack);
+  const size_t need = (size_t)nb * cap + tmax;
+  if (need * sizeof(int4) >= (1ull << 36)) {  // (> 64 GB: do not)
+    h->pb_max = 0;
+    return BM_OK;
+  }
+  BM_CUDA(dalloc(h->caps, h->tb, need));
+  h->pb_max = tmax;
+  h->pb_shift = shift;
+  h->pb_nb = nb;
+  h->pb_cap = cap;
+  return BM_OK;
+}
+
 Params make_params(bm_handle* h, const bm_match_opts& o) {
   Params p{};
   p.nc = h->nc;
@@ -650,6 +689,13 @@ Params make_params(bm_handle* h, const bm_match_opts& o) {
   p.fcap = (unsigned long long)h->nc + kFSlack(h->nc);
   p.claim_store = 1;
   if (const char* cs = getenv("BM_CLAIM_STORE")) p.claim_store = atoi(cs);
+  p.tb = (h->pb_max && p.roffs) ? h->tb : nullptr;
+  p.pb_min_edges = 1ull << 22;
+  if (const char* pm = getenv("BM_PB_MIN")) p.pb_min_edges = (unsigned long long)atoll(pm);
+  p.pb_max_edges = h->pb_max;
+  p.pb_shift = h->pb_shift;
+  p.pb_nb = h->pb_nb;
+  p.pb_cap = h->pb_cap;
   if (h->dbg_phase_bound > 0) p.phase_bound = h->dbg_phase_bound;
   p.sorted = h->sorted;
   p.check = getenv("BM_CHECK") ? atoi(getenv("BM_CHECK")) : 0;
@@ -684,6 +730,10 @@ bm_status drive(bm_handle* h, const bm_match_opts& o, bool fresh, int64_t* cardi
     bm_status ts = build_transpose(h, h->nc, h->nr, h->E);
     if (ts != BM_OK) return ts;
     BM_CUDA(cudaStreamSynchronize(h->stream));
+  }
+  if (bu) {
+    bm_status ps = ensure_pb(h);
+    if (ps != BM_OK) return ps;
   }
   Params p = make_params(h, o);
   p.fresh = fresh ? 1 : 0;
@@ -899,6 +949,7 @@ bm_status bm_destroy(bm_handle* h) {
   dfree(h->fbit);
   dfree(h->croot);
   dfree(h->P);
+  dfree(h->tb);
   dfree(h->gidx[0]);
   dfree(h->gidx[1]);
   dfree(h->wlog);

@@ -108,6 +108,7 @@ enum Stat : int {
 };
 
 constexpr int kBarSub = 16;  // grid barrier fan-in groups
+constexpr int kPbMax = 64;   // row buckets of a bucketed pushed level
 
 struct alignas(128) Ctrl {
   unsigned bar_count;
@@ -121,6 +122,12 @@ struct alignas(128) Ctrl {
   Slot rootp;   // multi-GPU: next-phase roots routed here by other ranks' FIX, as (c, c) pairs in P
   unsigned n_ep;
   unsigned pad1[31];
+  // bucketed pushed level (push_bucketed), by level parity: per-bucket cursors,
+  // overflow cursor, claim-pass ticket (reset after the level's barrier)
+  unsigned pb_cur[2][64];
+  unsigned pb_ovf[2];
+  unsigned pb_ticket[2];
+  unsigned pad1c[28];
   unsigned n_log;
   unsigned log_overflow;
   unsigned n_tl;
@@ -250,6 +257,15 @@ struct Params {
   long long phase_bound;
   unsigned long long fcap;  // frontier entries a phase may append (F0/F1 and P hold nc + kFSlack)
   int claim_store;          // pushed levels may claim by plain store (BM_CLAIM_STORE=0 disables)
+  // Bucketed pushed levels (push_bucketed): a wide level's live edges are first
+  // written as (row, col, root) triples grouped by row range, then claimed bucket
+  // by bucket, so the row-state gathers and claims of a bucket hit an L2-sized window.
+  int4* tb;                 // triples: pb_nb regions of pb_cap, then an overflow region
+  unsigned long long pb_min_edges;  // a pushed level with at least this many edges (and <= pb_max) goes bucketed
+  unsigned long long pb_max_edges;  // (0: never)
+  int pb_shift;             // bucket of row r = r >> pb_shift
+  int pb_nb;                // buckets (<= kPbMax)
+  unsigned pb_cap;          // triples per bucket region
   unsigned long long* tl;  // stage timeline: (tag, %globaltimer ns) pairs written by the leader
   unsigned tl_cap;
 #if BM_MG
@@ -265,7 +281,7 @@ struct Params {
 
 enum TlTag : unsigned {
   kTlStart = 0, kTlInit = 1, kTlSetup = 2, kTlLevel = 3, kTlAlt = 4, kTlFixRows = 5, kTlFixCols = 6,
-  kTlRoots = 7, kTlEnd = 8, kTlLevelEdges = 9, kTlMat = 10, kTlPrep = 11
+  kTlRoots = 7, kTlEnd = 8, kTlLevelEdges = 9, kTlMat = 10, kTlPrep = 11, kTlBucket = 12
 };
 
 __device__ __forceinline__ void tl_mark(const Params& p, unsigned kind, unsigned arg) {
@@ -310,6 +326,10 @@ struct Smem {
   unsigned wep[kThreads / 32];
   unsigned long long blk_base;
   unsigned blk_ep;
+  unsigned pb_hist[kPbMax];   // bucketed push: this window's triples per bucket ...
+  unsigned pb_base[kPbMax];   // ... their first slot in the bucket's region
+  unsigned pb_obase[kPbMax];  // ... and in the overflow region (the part past the region's end)
+  unsigned pb_pre[kPbMax + 2];  // claim pass: first chunk of each bucket (and of the overflow)
   unsigned nw;                          // winners staged in wbuf for the current window
   int2 wbuf[kWBuf];                     // (column, root) claimed in the current window
 #if BM_MG
@@ -1427,6 +1447,314 @@ __device__ __forceinline__ void expand_level(const Params& p, Smem& sm, int4* F,
   flush_count(sm, kStEntries, c_entries);
 }
 
+// ---------------------------------------------------------------------------
+// Bucketed pushed level: the same level as expand_level (gpubfs / gpubfs_wr,
+// gpu_match.cpp:42-70, 99-133) for wide levels over a row state far beyond L2,
+// in two passes separated by a grid barrier:
+//   1. partition: expand_level's edge-tiled windows, but every live edge is
+//      written as a triple (row, col, root) into the region of its row's bucket
+//      (CTA-staged runs, one reservation per bucket per window); no row state
+//      is touched;
+//   2. claim: the triples bucket by bucket (chunks handed out in order), so the
+//      grid's row-state gathers, claims and predecessor stores stay inside one
+//      or two buckets' slice of the row state (L2-sized) instead of landing
+//      anywhere in it (one random DRAM sector per edge otherwise).
+// Claims, endpoints and winners are expand_level's; only their order differs,
+// which the reference's races leave open too.
+template <bool WR, bool IMP, bool BU>
+__device__ __noinline__ void push_bucketed(const Params& p, Smem& sm, int4* F, unsigned ls, unsigned n, unsigned T,
+                                            const unsigned* gin, unsigned* gout, Slot* in, Slot* out, int level,
+                                            int pf, bool pairs_out, bool claim_store, int par) {
+  const unsigned tid = threadIdx.x;
+  Ctrl* ctl = p.ctl;
+  unsigned c_trav = 0, c_cexp = 0, c_nvis = 0, c_entries = 0;
+  const unsigned long long G = gridDim.x;
+  unsigned long long per = (T + 2 * G - 1) / (2 * G);
+  per = ((per + kGran - 1) / kGran) * kGran;
+  if (per > (unsigned long long)kGran * kMaxTileGran) per = (unsigned long long)kGran * kMaxTileGran;
+  const unsigned ET = (unsigned)per;
+  const unsigned ntiles = (unsigned)((T + (unsigned long long)ET - 1) / ET);
+  const unsigned out_base = ls + n;
+  unsigned* const path_flag = path_flag_of(p, pf);
+  const unsigned long long pol = policy_evict_first();
+  const unsigned long long keep = policy_evict_last();
+  const int nb = p.pb_nb, shift = p.pb_shift;
+  const unsigned cap = p.pb_cap;
+  const unsigned long long ovf0 = (unsigned long long)nb * cap;  // overflow region
+  unsigned* const cur = ctl->pb_cur[par];
+
+  // ---- pass 1: partition the level's live edges by row bucket ----
+  for (;;) {
+    if (tid == 0) sm.tile = atomicAdd(&in->tile, 1u);
+    __syncthreads();
+    const unsigned tile = sm.tile;
+    __syncthreads();
+    if (tile >= ntiles) break;
+    const unsigned e0 = tile * ET;
+    const unsigned e1 = (T - e0 < ET) ? T : e0 + ET;
+    unsigned i = (unsigned)ld_cg(reinterpret_cast<const int*>(gin) + e0 / kGran);
+    unsigned e = e0;
+    while (e < e1) {
+#pragma unroll
+      for (int k = 0; k < kEPT; ++k) {
+        const unsigned sl0 = tid * kEPT + k;
+        const unsigned wi = i + sl0;
+        if (wi < n) {
+          const int4 ent = ld_cg_stream(F + ls + wi, pol);
+          bool skip = false;
+          if (WR) skip = root_dead(p, ent.y);
+          sm.col[sl0] = ent.x;
+          sm.root[sl0] = skip ? -1 : ent.y;
+          sm.beg[sl0] = (unsigned)ent.z;
+          sm.pre[sl0] = (unsigned)ent.w;
+          if ((unsigned)ent.w >= e0 && (unsigned)ent.w < e1) {
+            c_entries++;
+            if (!skip) c_cexp++;
+          }
+        } else {
+          sm.pre[sl0] = T;
+          sm.root[sl0] = -1;
+        }
+      }
+      if (tid == 0) sm.pre[kWin] = (i + kWin < n) ? ld_cg_u(F + ls + i + kWin) : T;
+      for (int b = tid; b < nb; b += kThreads) sm.pb_hist[b] = 0;
+      __syncthreads();
+      const unsigned wend = min(e1, sm.pre[kWin]);
+      unsigned live;
+      {
+        unsigned len[kEPT], nbg[kEPT], tsum = 0;
+#pragma unroll
+        for (int k = 0; k < kEPT; ++k) {
+          const unsigned sl0 = tid * kEPT + k;
+          const unsigned lo = max(sm.pre[sl0], e);
+          const unsigned hi = min(sm.pre[sl0 + 1], wend);
+          len[k] = (sm.root[sl0] >= 0 && hi > lo) ? hi - lo : 0u;
+          nbg[k] = sm.beg[sl0] + (lo - sm.pre[sl0]);
+          tsum += len[k];
+        }
+        const unsigned incl = warp_incl_scan(tsum);
+        if (lane_id() == 31) sm.wtot[tid >> 5] = incl;
+        __syncthreads();
+        unsigned wbase = 0, tot = 0;
+#pragma unroll
+        for (int w = 0; w < kThreads / 32; ++w) {
+          const unsigned t = sm.wtot[w];
+          wbase += (w < (int)(tid >> 5)) ? t : 0u;
+          tot += t;
+        }
+        live = tot;
+        if (tot > kWBuf) {
+          if (tid == 0 && atomicCAS(&p.ctl->error, 0, (int)kErrWindow) == 0) {
+            long long* d = p.ctl->dbg;
+            d[0] = ls; d[1] = n; d[2] = T; d[3] = i; d[4] = e; d[5] = wend; d[6] = tot; d[7] = level;
+          }
+          live = 0;
+          for (int k = 0; k < kEPT; ++k) len[k] = 0;
+        }
+        unsigned vp = wbase + incl - tsum;
+#pragma unroll
+        for (int k = 0; k < kEPT; ++k) {
+          const unsigned sl0 = tid * kEPT + k;
+          sm.beg[sl0] = nbg[k];
+          sm.pre[sl0] = vp;
+          if (len[k]) {
+            const unsigned q1 = (vp + len[k] - 1) >> 5;
+            for (unsigned q = (vp + 31) >> 5; q <= q1; ++q) sm.cgr[q] = (unsigned short)sl0;
+          }
+          vp += len[k];
+        }
+        if (tid == 0) sm.pre[kWin] = tot;
+        __syncthreads();
+      }
+      const unsigned nq = (live + 31) >> 5;
+#pragma unroll
+      for (int k = 0; k < kEPT; ++k)
+        if (wend < e1 && i + kWin + k * kThreads + tid < n) prefetch_l2(F + ls + i + kWin + k * kThreads + tid);
+      // stage every live edge as (row, slot | rank-in-bucket << 8); count per bucket
+      for (unsigned base = 0; base < live; base += kThreads * kItems) {
+        int row[kItems], sl[kItems];
+#pragma unroll
+        for (int k = 0; k < kItems; ++k) {
+          const unsigned ee = base + k * kThreads + tid;
+          row[k] = -1;
+          sl[k] = 0;
+          if (ee < live) {
+            const unsigned q = ee >> 5;
+            int a = sm.cgr[q];
+            int b = (q + 1 < nq) ? (int)sm.cgr[q + 1] + 1 : kWin;
+            while (b - a > 1) {
+              const int mid = (a + b) >> 1;
+              if (sm.pre[mid] <= ee) a = mid; else b = mid;
+            }
+            sl[k] = a;
+            row[k] = ld_stream(p.adj + sm.beg[a] + (ee - sm.pre[a]), pol);
+            c_trav++;
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < kItems; ++k) {
+          const unsigned ee = base + k * kThreads + tid;
+          if (row[k] >= 0) {
+            const unsigned rank = atomicAdd(&sm.pb_hist[row[k] >> shift], 1u);
+            sm.wbuf[ee] = make_int2(row[k], sl[k] | (int)(rank << 8));
+          }
+        }
+      }
+      __syncthreads();
+      // one reservation per bucket; the part of a run past its region's end goes to the overflow region
+      for (int b = tid; b < nb; b += kThreads) {
+        const unsigned h = sm.pb_hist[b];
+        if (h) {
+          const unsigned base = atomicAdd(cur + b, h);
+          sm.pb_base[b] = base;
+          const unsigned fit = base >= cap ? 0u : min(h, cap - base);
+          if (fit < h) sm.pb_obase[b] = atomicAdd(&ctl->pb_ovf[par], h - fit);
+        }
+      }
+      __syncthreads();
+      for (unsigned ee = tid; ee < live; ee += kThreads) {
+        const int2 w = sm.wbuf[ee];
+        const int slw = w.y & 255;
+        const unsigned rank = (unsigned)w.y >> 8;
+        const int b = w.x >> shift;
+        const unsigned pos = sm.pb_base[b] + rank;
+        const unsigned long long idx =
+            pos < cap ? (unsigned long long)b * cap + pos : ovf0 + sm.pb_obase[b] + (pos - max(sm.pb_base[b], cap));
+        st_stream(p.tb + idx, make_int4(w.x, sm.col[slw], WR ? sm.root[slw] : sm.col[slw], 0), pol);
+      }
+      __syncthreads();
+      e = wend;
+      i += kWin;
+    }
+  }
+  flush_count(sm, kStTrav, c_trav);
+  flush_count(sm, kStCexp, c_cexp);
+  flush_count(sm, kStEntries, c_entries);
+  grid_sync(p);
+  tl_mark(p, kTlBucket, n);
+
+  // ---- pass 2: claim bucket by bucket ----
+  constexpr unsigned CH = kThreads * kItems;
+  if (tid == 0) {
+    unsigned acc = 0;
+    for (int b = 0; b < nb; ++b) {
+      sm.pb_pre[b] = acc;
+      acc += (min(ld_rlx(cur + b), cap) + CH - 1) / CH;
+    }
+    sm.pb_pre[nb] = acc;
+    acc += (ld_rlx(&ctl->pb_ovf[par]) + CH - 1) / CH;
+    sm.pb_pre[nb + 1] = acc;
+    sm.nw = 0;
+  }
+  __syncthreads();
+  const unsigned total = sm.pb_pre[nb + 1];
+  for (;;) {
+    if (tid == 0) sm.tile = atomicAdd(&ctl->pb_ticket[par], 1u);
+    __syncthreads();
+    const unsigned t = sm.tile;
+    __syncthreads();
+    if (t >= total) break;
+    int b = 0;
+    while (b < nb && sm.pb_pre[b + 1] <= t) ++b;  // b == nb: the overflow region
+    const unsigned long long r0 = b < nb ? (unsigned long long)b * cap : ovf0;
+    const unsigned m = b < nb ? min(ld_rlx(cur + b), cap) : ld_rlx(&ctl->pb_ovf[par]);
+    const unsigned j0 = (t - sm.pb_pre[b]) * CH;
+    int row[kItems], cm[kItems], colk[kItems], rootk[kItems];
+#pragma unroll
+    for (int k = 0; k < kItems; ++k) {
+      const unsigned jj = j0 + k * kThreads + tid;
+      row[k] = -1;
+      colk[k] = 0;
+      rootk[k] = 0;
+      if (jj < m) {
+        const int4 tr = ld_cg_stream(p.tb + r0 + jj, pol);
+        row[k] = tr.x;
+        colk[k] = tr.y;
+        rootk[k] = tr.z;
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kItems; ++k) cm[k] = row[k] >= 0 ? ld_rlx_hint(RM(p, row[k]), keep) : -3;
+    unsigned wins = 0, eps = 0;
+    int old[kItems];
+#pragma unroll
+    for (int k = 0; k < kItems; ++k) {
+      const int c = cm[k];
+      old[k] = kVisBit;
+      if (c >= 0 && !(c & kVisBit) && (!WR || p.claim_mode == 0 || !root_dead(p, rootk[k]))) {
+        if (claim_store) {
+          st_plain(RM(p, row[k]), c | kVisBit);
+          old[k] = c;
+        } else {
+          old[k] = at_or(RM(p, row[k]), kVisBit);
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kItems; ++k) {
+      const int c = cm[k];
+      const int col = colk[k];
+      const int root = rootk[k];
+      if (c >= 0) {
+        if (!(old[k] & kVisBit)) {
+          wins |= 1u << k;
+          if (!(BU && pairs_out)) prefetch_l2(p.offs + c);  // the flush reads offs[c], offs[c+1]
+          st_stream(PR(p, row[k]), col, pol);
+          if (p.trace) st_plain(BF(p, c), level + 1);
+        }
+      } else if (c == -1) {
+        const bool one = WR && p.ep_one;
+        if ((!one || !root_dead(p, root)) && at_cas(RM(p, row[k]), -1, -2) == -1) {
+          bool mine = true;
+          if (one) {
+            mine = at_cas(BF(p, root), kStartLevel, IMP ? -row[k] : kFoundMark) == kStartLevel;
+            if (!mine) st_rlx(RM(p, row[k]), -1);
+            else mark_dead(p, root);
+          } else if (WR) {
+            st_rlx(BF(p, root), IMP ? -row[k] : kFoundMark);
+            mark_dead(p, root);
+          }
+          if (mine) {
+            eps |= 1u << k;
+            st_plain(PR(p, row[k]), col);
+            if (ld_rlx(path_flag) == 0u) st_rlx(path_flag, 1u);
+          }
+        }
+      }
+    }
+    {
+      const unsigned mine = __popc(wins);
+      const unsigned incl = warp_incl_scan(mine);
+      const unsigned tot = __shfl_sync(kFull, incl, 31);
+      unsigned wb = 0;
+      if (lane_id() == 31 && tot) wb = atomicAdd(&sm.nw, tot);
+      wb = __shfl_sync(kFull, wb, 31) + incl - mine;
+#pragma unroll
+      for (int k = 0; k < kItems; ++k)
+        if (wins & (1u << k)) sm.wbuf[wb++] = make_int2(cm[k], WR ? rootk[k] : colk[k]);
+      c_nvis += mine;
+    }
+    {
+      const unsigned mine = __popc(eps);
+      const unsigned incl = warp_incl_scan(mine);
+      const unsigned tot = __shfl_sync(kFull, incl, 31);
+      if (tot) {
+        unsigned eb = 0;
+        if (lane_id() == 31) eb = atomicAdd(&p.ctl->n_ep, tot);
+        eb = __shfl_sync(kFull, eb, 31) + incl - mine;
+#pragma unroll
+        for (int k = 0; k < kItems; ++k)
+          if (eps & (1u << k)) st_plain(p.EP + eb++, row[k]);
+      }
+    }
+    __syncthreads();
+    if (BU && pairs_out) flush_pairs(p, sm, out_base, out, pol);
+    else flush_winners(p, sm, F, out_base, gout, out, pol);
+    __syncthreads();
+  }
+  flush_count(sm, kStNvis, c_nvis);
+}
+
 // Appends one (row, col) record to the ALTERNATE write log; lanes that reach
 // this point together share one atomic.
 __device__ __forceinline__ void log_write(const Params& p, int row, int col) {
@@ -1767,6 +2095,9 @@ __device__ PhaseOut run_phase(const Params& p, Smem& sm, int cur, int parity, bo
     // roots in croot), so that a pulled successor starts at once (no bu_prep pass
     // of its own: one scattered croot store per column fewer, and one grid barrier).
     unsigned* const fb_next = pairs_out && BU_MARK ? p.fbit[(lv + 1) % kNumFbit] : nullptr;
+    // a wide pushed level over a row state far beyond L2 goes bucketed (push_bucketed)
+    const bool bucketed = BU && !bu && !solo && p.tb && !fb_next && (unsigned long long)T >= p.pb_min_edges &&
+                          (unsigned long long)T <= p.pb_max_edges;
     if (bu) {
       const bool marked = (dirty >> (lv % kNumFbit)) & 1u;  // the level before marked this one
       if (!marked) {
@@ -1785,8 +2116,12 @@ __device__ PhaseOut run_phase(const Params& p, Smem& sm, int cur, int parity, bo
       // when one output entry per frontier edge still fits the phase's frontier
       // capacity; otherwise by atomicOr, which pushes every column once.
       const bool claim_store = p.claim_store && (unsigned long long)ls + n + T <= p.fcap;
-      expand_level<WR, IMP, BU>(p, sm, F, ls, n, T, (lv & 1) ? p.gidx1 : p.gidx0, (lv & 1) ? p.gidx0 : p.gidx1,
-                                in, outs, kStartLevel + lv, parity, pairs_out, claim_store, (lv + 1) % 3, fb_next);
+      if (bucketed)
+        push_bucketed<WR, IMP, BU>(p, sm, F, ls, n, T, (lv & 1) ? p.gidx1 : p.gidx0, (lv & 1) ? p.gidx0 : p.gidx1,
+                                   in, outs, kStartLevel + lv, parity, pairs_out, claim_store, lv & 1);
+      else
+        expand_level<WR, IMP, BU>(p, sm, F, ls, n, T, (lv & 1) ? p.gidx1 : p.gidx0, (lv & 1) ? p.gidx0 : p.gidx1,
+                                  in, outs, kStartLevel + lv, parity, pairs_out, claim_store, (lv + 1) % 3, fb_next);
     }
     if (fb_next) dirty |= 1u << ((lv + 1) % kNumFbit);
 
@@ -1796,6 +2131,11 @@ __device__ PhaseOut run_phase(const Params& p, Smem& sm, int cur, int parity, bo
       __syncthreads();
     } else {
       grid_sync(p);
+      if (bucketed && is_leader()) {  // next used two levels on (after another barrier)
+        for (int b = 0; b < p.pb_nb; ++b) ctl->pb_cur[lv & 1][b] = 0;
+        ctl->pb_ovf[lv & 1] = 0;
+        ctl->pb_ticket[lv & 1] = 0;
+      }
       if (dirty & (1u << (lv % kNumFbit))) {  // read by nobody from here on
         bu_clear(p, lv % kNumFbit);
         dirty &= ~(1u << (lv % kNumFbit));

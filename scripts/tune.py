@@ -31,7 +31,7 @@ def timeline_summary(eng):
         dt = (t - prev) / 1e3
         prev = t
         kinds[kind] = kinds.get(kind, 0.0) + dt
-        if kind in ("materialize", "pull_prep"):  # parts of the level that follows
+        if kind in ("materialize", "pull_prep", "bucketed"):  # parts of the level that follows
             sub[kind] = round(dt, 1)
             continue
         if kind == "level":
