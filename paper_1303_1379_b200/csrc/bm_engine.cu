@@ -55,7 +55,10 @@
 #include <climits>
 #include <cstdlib>
 #include <cstdint>
+#include <condition_variable>
 #include <deque>
+#include <mutex>
+#include <thread>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -250,15 +253,83 @@ bm_status stage_init(bm_handle* h) {
   return BM_OK;
 }
 
-void par_copy(void* dst, const void* src, size_t n) {  // >= 8 MB per thread, at most 8 threads
-  const int t = (int)std::max<size_t>(1, std::min<size_t>((size_t)std::min(8, bm_host::resolve_threads(0)), n >> 23));
-  bm_host::parallel_for((long long)t, t, [&](long long b, long long e, int) {
-    for (long long w = b; w < e; ++w) {
-      const size_t lo = n * (size_t)w / (size_t)t, hi = n * (size_t)(w + 1) / (size_t)t;
-      std::memcpy(static_cast<char*>(dst) + lo, static_cast<const char*>(src) + lo, hi - lo);
+// Host copy threads for the staging ring: a persistent pool (a thread spawn per
+// 64 MB piece cost ~10 % of the copy). Process-wide, created on first use and
+// never torn down (its threads sleep on a condition variable).
+class CopyPool {
+ public:
+  static CopyPool& get() {
+    static CopyPool* pool = new CopyPool();  // (leaked on purpose: no join at exit)
+    return *pool;
+  }
+  // dst <- src, n bytes, split over the pool (the caller takes one part too)
+  void copy(void* dst, const void* src, size_t n) {
+    const int parts = (int)std::max<size_t>(1, std::min<size_t>((size_t)nthreads_ + 1, n >> 22));  // >= 4 MB each
+    if (parts == 1) {
+      std::memcpy(dst, src, n);
+      return;
     }
-  });
-}
+    std::lock_guard<std::mutex> one_job(job_mu_);  // (callers on other threads take turns)
+    std::unique_lock<std::mutex> lk(mu_);
+    dst_ = static_cast<char*>(dst);
+    src_ = static_cast<const char*>(src);
+    n_ = n;
+    parts_ = parts;
+    next_ = 1;
+    pending_ = parts - 1;
+    ++gen_;
+    cv_.notify_all();
+    lk.unlock();
+    part(0);
+    lk.lock();
+    for (;;) {  // help with parts no worker has taken yet, then wait for the rest
+      if (next_ < parts_) {
+        const int w = next_++;
+        lk.unlock();
+        part(w);
+        lk.lock();
+        if (--pending_ == 0) break;
+        continue;
+      }
+      if (pending_ == 0) break;
+      done_.wait(lk);
+    }
+  }
+
+ private:
+  CopyPool() {
+    nthreads_ = std::max(0, std::min(15, bm_host::resolve_threads(0) - 1));
+    for (int i = 0; i < nthreads_; ++i) std::thread([this] { loop(); }).detach();
+  }
+  void part(int w) {
+    const size_t lo = n_ * (size_t)w / (size_t)parts_, hi = n_ * (size_t)(w + 1) / (size_t)parts_;
+    std::memcpy(dst_ + lo, src_ + lo, hi - lo);
+  }
+  void loop() {
+    std::unique_lock<std::mutex> lk(mu_);
+    unsigned long long seen = gen_;
+    for (;;) {
+      cv_.wait(lk, [&] { return gen_ != seen && next_ < parts_; });
+      while (next_ < parts_) {
+        const int w = next_++;
+        lk.unlock();
+        part(w);
+        lk.lock();
+        if (--pending_ == 0) done_.notify_all();
+      }
+      seen = gen_;
+    }
+  }
+  std::mutex job_mu_, mu_;
+  std::condition_variable cv_, done_;
+  char* dst_ = nullptr;
+  const char* src_ = nullptr;
+  size_t n_ = 0;
+  int parts_ = 0, next_ = 0, pending_ = 0, nthreads_ = 0;
+  unsigned long long gen_ = 0;
+};
+
+void par_copy(void* dst, const void* src, size_t n) { CopyPool::get().copy(dst, src, n); }
 
 // Enqueues a host -> device copy on st (returns once the host buffer may be reused).
 bm_status xfer_h2d(bm_handle* h, void* dst, const void* src, size_t n, cudaStream_t st) {

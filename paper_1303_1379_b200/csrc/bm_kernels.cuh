@@ -304,7 +304,10 @@ struct BuCand {
   unsigned j0;
   unsigned j1;
 };
-constexpr int kCandCap = 160;  // per-warp queue: < 32 left over + one screened chunk of 128 rows
+#ifndef BM_BU_SLOTS
+#define BM_BU_SLOTS 1  // candidates per lane in a pulled sweep (1: bu_sweep_q, 2: bu_sweep_q2)
+#endif
+constexpr int kCandCap = BM_BU_SLOTS == 2 ? 192 : 160;  // per-warp queue: < 32 x slots left over + one screened chunk of 128 rows
 
 struct Smem {
   union {  // a top-down window (a pulled level keeps its candidate queues in wbuf)
@@ -1174,6 +1177,229 @@ __device__ __forceinline__ void bu_sweep_q(const Params& p, Smem& sm, unsigned o
   flush_count(sm, kStRowsPulled, c_rows);
 }
 
+// The same pulled level with two candidates per lane (BM_BU_SLOTS=2): each
+// round probes two columns of each of the lane's two rows, so twice as many
+// row searches are in flight per warp (the sweep is bound by the latency of
+// its radj -> bitmap -> root chains, not by bandwidth).
+template <bool WR, bool IMP>
+__device__ __forceinline__ void bu_sweep_q2(const Params& p, Smem& sm, unsigned out_base, Slot* out, int out_slot,
+                                            int lv, int pf, unsigned* fb_next, bool marked_in) {
+  constexpr int kWarps = kThreads / 32;
+  constexpr unsigned kChunk = 128;
+  constexpr unsigned kWStage = 128;
+  static_assert(sizeof(BuCand) * kCandCap * kWarps + sizeof(int2) * kWStage * kWarps <= sizeof(int2) * kWBuf,
+                "candidate queues and winner stages must fit in wbuf");
+  constexpr int kP = 2;  // probes per slot per round
+  const unsigned* fb = p.fbit[lv % kNumFbit];
+  const unsigned long long pol = policy_evict_first();
+  unsigned* const path_flag = path_flag_of(p, pf);
+#if BM_MG
+  const unsigned long long rlo = (unsigned long long)p.row_lo, rhi = (unsigned long long)p.row_hi;
+#else
+  const unsigned long long rlo = 0, rhi = (unsigned long long)p.nr;
+#endif
+  unsigned c_trav = 0, c_nvis = 0, c_rows = 0;
+  const unsigned warp = threadIdx.x >> 5, lane = lane_id();
+  const unsigned lt = (1u << lane) - 1u;
+  BuCand* const q = reinterpret_cast<BuCand*>(sm.wbuf) + warp * kCandCap;
+  int2* const wst = reinterpret_cast<int2*>(reinterpret_cast<BuCand*>(sm.wbuf) + kWarps * kCandCap) + warp * kWStage;
+  const unsigned long long nchunks = (rhi - rlo + kChunk - 1) / kChunk;
+  const unsigned long long W = (unsigned long long)gridDim.x * kWarps;
+  unsigned long long chunk = (unsigned long long)blockIdx.x * kWarps + warp;
+  unsigned qh = 0, qt = 0, nwin = 0;
+  int rr[2] = {-1, -1}, vv[2] = {0, 0};
+  unsigned j[2] = {0, 0}, j1[2] = {0, 0};
+  for (;;) {
+    const unsigned idle0 = __ballot_sync(kFull, rr[0] < 0), idle1 = __ballot_sync(kFull, rr[1] < 0);
+    const unsigned need = (unsigned)(__popc(idle0) + __popc(idle1));
+    while (qt - qh < need && chunk < nchunks) {
+      const unsigned left = qt - qh;
+      BuCand keep[2];
+      if (lane < left) keep[0] = q[qh + lane];
+      if (lane + 32 < left) keep[1] = q[qh + lane + 32];
+      __syncwarp();
+      if (lane < left) q[lane] = keep[0];
+      if (lane + 32 < left) q[lane + 32] = keep[1];
+      qh = 0;
+      qt = left;
+      const unsigned long long r0 = rlo + chunk * kChunk;
+      chunk += W;
+#if BM_BU_PF
+      if (chunk < nchunks) {
+        const unsigned long long rn = rlo + chunk * kChunk;
+        const unsigned long long rend = min(rhi, rn + kChunk);
+        const unsigned long long rr0 = rn + (unsigned long long)lane * (8 / p.rs);
+        if (rr0 < rend) prefetch_l2n(RML(p, rr0));
+        if (lane < 16) {
+          const unsigned long long ro = rn + (unsigned long long)lane * 8;
+          if (ro <= rend) prefetch_l2n(p.roffs + ro);
+        }
+      }
+#endif
+      int v[4];
+      unsigned o[4], onext;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const unsigned long long r = r0 + (unsigned long long)k * 32 + lane;
+        v[k] = r < rhi ? ld_cg(RML(p, r)) : -3;
+        o[k] = r <= rhi ? ld_ro(p.roffs + r) : 0u;
+      }
+      {
+        const unsigned long long r = r0 + 4 * 32;
+        onext = (lane == 0 && r <= rhi) ? ld_ro(p.roffs + r) : 0u;
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        unsigned e = __shfl_down_sync(kFull, o[k], 1);
+        const unsigned nxt0 = __shfl_sync(kFull, k < 3 ? o[(k + 1) & 3] : onext, 0);
+        if (lane == 31) e = nxt0;
+        const bool is_cand = (v[k] >= 0 && !(v[k] & kVisBit)) || v[k] == -1;
+        const unsigned m = __ballot_sync(kFull, is_cand && e > o[k]);
+        if (is_cand && e > o[k]) {
+          BuCand c;
+          c.row = (int)(r0 + (unsigned long long)k * 32 + lane);
+          c.val = v[k];
+          c.j0 = o[k];
+          c.j1 = e;
+          q[qt + __popc(m & lt)] = c;
+#if BM_BU_PF
+          prefetch_l2n(p.radj + o[k]);
+#endif
+        }
+        qt += __popc(m);
+      }
+      __syncwarp();
+    }
+    {  // idle slots take queued candidates: slot 0 lanes first, then slot 1, in lane order
+      const unsigned avail = qt - qh;
+      const unsigned n0 = min((unsigned)__popc(idle0), avail);
+      const unsigned k0 = __popc(idle0 & lt);
+      if (rr[0] < 0 && k0 < avail) {
+        const BuCand c = q[qh + k0];
+        rr[0] = c.row; vv[0] = c.val; j[0] = c.j0; j1[0] = c.j1;
+        c_rows++;
+      }
+      const unsigned k1 = n0 + __popc(idle1 & lt);
+      if (rr[1] < 0 && k1 < avail) {
+        const BuCand c = q[qh + k1];
+        rr[1] = c.row; vv[1] = c.val; j[1] = c.j0; j1[1] = c.j1;
+        c_rows++;
+      }
+      qh += min(need, avail);
+    }
+    if (!__any_sync(kFull, rr[0] >= 0 || rr[1] >= 0)) break;
+    int cs[2][kP];
+    unsigned wd[2][kP];
+#pragma unroll
+    for (int s = 0; s < 2; ++s)
+#pragma unroll
+      for (int k = 0; k < kP; ++k) cs[s][k] = (rr[s] >= 0 && j[s] + k < j1[s]) ? ld_stream(p.radj + j[s] + k, pol) : -1;
+#pragma unroll
+    for (int s = 0; s < 2; ++s)
+#pragma unroll
+      for (int k = 0; k < kP; ++k)
+        wd[s][k] = cs[s][k] >= 0 ? ld_ca(reinterpret_cast<const int*>(fb) + (cs[s][k] >> 5)) : 0u;
+    bool win[2] = {false, false}, ep[2] = {false, false};
+    int cw[2] = {0, 0}, rootw[2] = {0, 0}, myrow[2] = {rr[0], rr[1]};
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      if (rr[s] < 0) continue;
+      bool done = false;
+#pragma unroll
+      for (int k = 0; k < kP; ++k) {
+        const int c = cs[s][k];
+        if (done || c < 0) continue;
+        c_trav++;
+        if (!((wd[s][k] >> (c & 31)) & 1)) continue;
+        const int root = WR ? ld_cg(CR(p, c)) : c;
+        if (WR && marked_in && root_dead(p, root)) continue;
+        if (vv[s] >= 0) {
+          st_plain(RML(p, rr[s]), vv[s] | kVisBit);
+          st_plain(PRL(p, rr[s]), c);
+          if (fb_next) {
+            atomicOr(fb_next + (vv[s] >> 5), 1u << (vv[s] & 31));
+            if (WR) st_plain(CR(p, vv[s]), root);
+          }
+          win[s] = true;
+          cw[s] = vv[s];
+          rootw[s] = root;
+          done = true;
+          continue;
+        }
+        const bool one = WR && p.ep_one;
+        if (one && root_dead(p, root)) continue;
+        bool mine = true;
+        if (one) mine = at_cas(BF(p, root), kStartLevel, IMP ? -rr[s] : kFoundMark) == kStartLevel;
+        else if (WR) st_rlx(BF(p, root), IMP ? -rr[s] : kFoundMark);
+        if (!mine) continue;
+        if (WR) mark_dead(p, root);
+        st_rlx(RML(p, rr[s]), -2);
+        st_plain(PRL(p, rr[s]), c);
+        ep[s] = true;
+        if (ld_rlx(path_flag) == 0u) st_rlx(path_flag, 1u);
+        done = true;
+      }
+      j[s] += kP;
+      if (done || j[s] >= j1[s]) rr[s] = -1;
+    }
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      const unsigned m = __ballot_sync(kFull, win[s]);
+      if (win[s]) wst[nwin + __popc(m & lt)] = make_int2(cw[s], rootw[s]);
+      nwin += __popc(m);
+      c_nvis += win[s] ? 1u : 0u;
+    }
+    if (nwin > kWStage - 64) {
+      __syncwarp();
+#if BM_MG
+      if (routed(p)) {
+        warp_flush_mg(p, sm, wst, nwin, out_slot, pol);
+      } else
+#endif
+      {
+        unsigned base = 0;
+        if (lane == 0) base = (unsigned)(atomicAdd(&out->packed, (unsigned long long)nwin << 33) >> 33);
+        base = __shfl_sync(kFull, base, 0) + out_base;
+        for (unsigned i = lane; i < nwin; i += 32) st_stream(p.P + base + i, wst[i], pol);
+      }
+      __syncwarp();
+      nwin = 0;
+    }
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      const unsigned m = __ballot_sync(kFull, ep[s]);
+      if (m) {
+        unsigned eb = 0;
+        if (lane == 0) eb = atomicAdd(&p.ctl->n_ep, (unsigned)__popc(m));
+        eb = __shfl_sync(kFull, eb, 0) + __popc(m & lt);
+        if (ep[s]) st_plain(p.EP + eb, myrow[s]);
+      }
+    }
+  }
+  if (nwin) {
+    __syncwarp();
+#if BM_MG
+    if (routed(p)) {
+      warp_flush_mg(p, sm, wst, nwin, out_slot, pol);
+    } else
+#endif
+    {
+      unsigned base = 0;
+      if (lane == 0) base = (unsigned)(atomicAdd(&out->packed, (unsigned long long)nwin << 33) >> 33);
+      base = __shfl_sync(kFull, base, 0) + out_base;
+      for (unsigned i = lane; i < nwin; i += 32) st_stream(p.P + base + i, wst[i], pol);
+    }
+  }
+  flush_count(sm, kStTrav, c_trav);
+  flush_count(sm, kStNvis, c_nvis);
+  flush_count(sm, kStRowsPulled, c_rows);
+}
+#if BM_BU_SLOTS == 2
+#define BU_SWEEP bu_sweep_q2
+#else
+#define BU_SWEEP bu_sweep_q
+#endif
+
 // ---------------------------------------------------------------------------
 // One BFS level (GPUBFS, Alg. 2, gpu_match.cpp:42-70; GPUBFS-WR, Alg. 4,
 // gpu_match.cpp:99-133) over the frontier F[ls, ls+n) holding T edges.
@@ -1975,7 +2201,7 @@ __device__ PhaseOut run_phase(const Params& p, Smem& sm, int cur, int parity, bo
         bu_share(p, lv);
         grid_sync(p);
       }
-      bu_sweep_q<WR, IMP>(p, sm, ls + n, outs, (lv + 1) % 3, lv, parity, nullptr, false);
+      BU_SWEEP<WR, IMP>(p, sm, ls + n, outs, (lv + 1) % 3, lv, parity, nullptr, false);
       if (threadIdx.x == 0) sm.cnt[kStPulledLevels] += is_leader() ? 1 : 0;
     } else {
       // store claims when even one entry per frontier edge of the team fits every inbox
@@ -2108,7 +2334,7 @@ __device__ PhaseOut run_phase(const Params& p, Smem& sm, int cur, int parity, bo
       } else if (is_leader()) {
         sm.cnt[kStCexp] += n;  // (entries; bu_prep counts the live ones)
       }
-      bu_sweep_q<WR, IMP>(p, sm, ls + n, outs, (lv + 1) % 3, lv, parity, fb_next, marked);
+      BU_SWEEP<WR, IMP>(p, sm, ls + n, outs, (lv + 1) % 3, lv, parity, fb_next, marked);
       if (threadIdx.x == 0) sm.cnt[kStPulledLevels] += is_leader() ? 1 : 0;
     } else {
       // Claims by plain store (no atomic round trip; two discoverers racing on one
