@@ -140,6 +140,31 @@ def known_answers():
     return {}
 
 
+def random_access_ceiling(trav, k_ms):
+    """The path's other ceiling: every traversed edge needs at least one random
+    4-byte access to the row state, which on B200 runs at the rate the
+    microbenchmark (scripts/ubench_gather.cu, committed as
+    profiles/ubench_gather.jsonl) measures for the C5-sized table, not at the
+    HBM copy bandwidth. t_min = traversed edges / best gather rate."""
+    path = os.path.join(ROOT, "profiles", "ubench_gather.jsonl")
+    if not os.path.exists(path):
+        return None
+    rows = [json.loads(l) for l in open(path) if l.strip()]
+    big = max(r["table_mb"] for r in rows)
+    best = {}
+    for r in rows:
+        if r["table_mb"] == big:
+            best[r["kind"]] = max(best.get(r["kind"], 0.0), r["gps"])
+    g = best.get("gather")
+    if not g:
+        return None
+    t_min = trav / (g * 1e9) * 1e3
+    return {"table_mb": big, "gather_gps": g, "claim_gps": best.get("claim"), "atomic_gps": best.get("atomicOr"),
+            "traversed_edges": trav, "t_min_ms": t_min, "frac": t_min / k_ms,
+            "model": "one random 4-byte row-state gather per traversed edge at the best measured gather rate",
+            "source": "profiles/ubench_gather.jsonl (scripts/ubench_gather.cu on this pool's B200)"}
+
+
 def measured_peak():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -715,7 +740,8 @@ def run_b200(args):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                          "kernel": "bm::driver_kernel (persistent, whole run)",
-                         "algorithmic_bytes_per_launch": b_units, "survey_formula_bytes": b_survey},
+                         "algorithmic_bytes_per_launch": b_units, "survey_formula_bytes": b_survey,
+                         "random_access_ceiling": random_access_ceiling(mean_of("edges_traversed"), k_ms)},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "bottom_up": {"mode": args.bottom_up, "pulled_dense_levels": bool(pulled),

@@ -822,9 +822,10 @@ __device__ __forceinline__ void bu_clear(const Params& p, int b) {
 }
 // The frontier comes as (col, root) pairs (levels >= 1 of a pulled-capable
 // run) or as entries (level 0). Counts the live entries as columns expanded.
+// write_root = false (lazy roots, see bu_sweep_q): only the bitmap is built.
 template <bool WR>
 __device__ __forceinline__ void bu_prep(const Params& p, Smem& sm, const int4* F, bool pairs, unsigned ls,
-                                        unsigned n, int lv) {
+                                        unsigned n, int lv, bool write_root = true) {
   unsigned* fb = p.fbit[lv % kNumFbit];
   unsigned live = 0;
   constexpr int K = 8;  // entries per thread in flight (the loop is latency-bound otherwise)
@@ -856,7 +857,7 @@ __device__ __forceinline__ void bu_prep(const Params& p, Smem& sm, const int4* F
       if (on[i]) {
         live++;
         atomicOr(fb + (col[i] >> 5), 1u << (col[i] & 31));
-        st_plain(p.croot + col[i], WR ? root[i] : col[i]);
+        if (write_root) st_plain(p.croot + col[i], WR ? root[i] : col[i]);
       }
   }
   flush_count(sm, kStCexp, live);
@@ -877,6 +878,10 @@ constexpr bool BU_MARK = BM_BU_MARK != 0;
 #define BM_BU_PF 1  // pulled levels: L2 prefetch of the next chunk's row state/offsets and of each candidate's columns
                     // (A/B on C5: screen cycles -34 %, -3.5 % per phase)
 #endif
+#ifndef BM_BU_LAZY
+#define BM_BU_LAZY 1  // pulled levels with few rows left resolve their hits' roots instead of scattering them
+#endif
+constexpr bool BU_LAZY = BM_BU_LAZY != 0;
 #ifndef BM_BU_CYC
 #define BM_BU_CYC 0  // 1: per-part warp cycle counters in pulled levels (profiling builds)
 #endif
@@ -914,9 +919,14 @@ __device__ __forceinline__ void bu_share(const Params& p, int lv) {
 // marked_in: this level's bitmap was marked that way by the level before, so
 // it still holds columns of trees that have found their path since (WR skips
 // them at the hit, as bu_prep would have left them out).
+// lazy_root: this level's bu_prep wrote no roots (few rows are left to claim, so
+// scattering one root per frontier column would cost more than resolving the
+// roots of the hits): a hit column c's root is that of the column that
+// discovered its mate row, croot[pred[cmatch[c]]], which the level before
+// (pulled, with roots) wrote.
 template <bool WR, bool IMP>
 __device__ __forceinline__ void bu_sweep_q(const Params& p, Smem& sm, unsigned out_base, Slot* out, int out_slot,
-                                           int lv, int pf, unsigned* fb_next, bool marked_in) {
+                                           int lv, int pf, unsigned* fb_next, bool marked_in, bool lazy_root = false) {
   constexpr int kWarps = kThreads / 32;
   constexpr unsigned kChunk = 128;
   constexpr unsigned kWStage = 128;  // winners staged per warp
@@ -1074,11 +1084,17 @@ __device__ __forceinline__ void bu_sweep_q(const Params& p, Smem& sm, unsigned o
         if (done || c < 0) continue;
         c_trav++;
         if (!((wd[k] >> (c & 31)) & 1)) continue;
+        int root = c;
+        if (WR && lazy_root) {
+          root = ld_cg(CR(p, ld_cg(PR(p, ld_rlx(CM(p, c))))));
+          if (root_dead(p, root)) continue;  // (bu_prep filtered by the pairs' roots; the tree may have died since)
+        } else if (WR) {
 #if BM_BU_HINT
-        const int root = WR ? ld_cg_hint(CR(p, c), pol) : c;
+          root = ld_cg_hint(CR(p, c), pol);
 #else
-        const int root = WR ? ld_cg(CR(p, c)) : c;
+          root = ld_cg(CR(p, c));
 #endif
+        }
         // (WR) a tree that found its path after this bitmap was built expands no further
         if (WR && marked_in && root_dead(p, root)) continue;
         if (vv >= 0) {  // matched row: its column joins the frontier below c's tree
@@ -1183,7 +1199,7 @@ __device__ __forceinline__ void bu_sweep_q(const Params& p, Smem& sm, unsigned o
 // its radj -> bitmap -> root chains, not by bandwidth).
 template <bool WR, bool IMP>
 __device__ __forceinline__ void bu_sweep_q2(const Params& p, Smem& sm, unsigned out_base, Slot* out, int out_slot,
-                                            int lv, int pf, unsigned* fb_next, bool marked_in) {
+                                            int lv, int pf, unsigned* fb_next, bool marked_in, bool /*lazy*/ = false) {
   constexpr int kWarps = kThreads / 32;
   constexpr unsigned kChunk = 128;
   constexpr unsigned kWStage = 128;
@@ -2151,6 +2167,7 @@ __device__ PhaseOut run_phase(const Params& p, Smem& sm, int cur, int parity, bo
   bool found = false;
   bool in_pairs = false;  // this level's entries are (col, root) pairs in P (pulled-capable kernels)
   unsigned dirty = 0;     // frontier bitmaps holding marks (bit b: fbit[b]); grid-uniform
+  bool croot_prev = false;  // the level before was pulled and wrote its frontier's roots (lazy roots)
   const unsigned long long pol_mat = policy_evict_first();
 #if BM_MG
   if (routed(p)) {
@@ -2304,6 +2321,7 @@ __device__ PhaseOut run_phase(const Params& p, Smem& sm, int cur, int parity, bo
       found = ld_rlx(&ctl->solo_found) != 0;
       out.launches = (long long)ld_rlx((const unsigned long long*)&ctl->solo_launches);
       in_pairs = false;  // solo levels push entries
+      croot_prev = false;
       if (ld_rlx(&ctl->solo_stop)) break;
       continue;
     }
@@ -2324,17 +2342,22 @@ __device__ PhaseOut run_phase(const Params& p, Smem& sm, int cur, int parity, bo
     // a wide pushed level over a row state far beyond L2 goes bucketed (push_bucketed)
     const bool bucketed = BU && !bu && !solo && p.tb && !fb_next && (unsigned long long)T >= p.pb_min_edges &&
                           (unsigned long long)T <= p.pb_max_edges;
+    // Lazy roots: when few rows are left to claim (fewer than a third of the
+    // frontier), bu_prep skips the scattered root store of every frontier column
+    // and the hits resolve their roots through the level before (bu_sweep_q).
+    const long long unvisited = (long long)p.nr - (long long)ls - (long long)n;
+    const bool lazy = BU_LAZY && WR && bu && croot_prev && in_pairs && BM_BU_SLOTS == 1 && 3 * unvisited < (long long)n;
     if (bu) {
       const bool marked = (dirty >> (lv % kNumFbit)) & 1u;  // the level before marked this one
       if (!marked) {
-        bu_prep<WR>(p, sm, F, in_pairs, ls, n, lv);
+        bu_prep<WR>(p, sm, F, in_pairs, ls, n, lv, !lazy);
         grid_sync(p);
         dirty |= 1u << (lv % kNumFbit);
         tl_mark(p, kTlPrep, n);
       } else if (is_leader()) {
         sm.cnt[kStCexp] += n;  // (entries; bu_prep counts the live ones)
       }
-      BU_SWEEP<WR, IMP>(p, sm, ls + n, outs, (lv + 1) % 3, lv, parity, fb_next, marked);
+      BU_SWEEP<WR, IMP>(p, sm, ls + n, outs, (lv + 1) % 3, lv, parity, fb_next, marked, lazy);
       if (threadIdx.x == 0) sm.cnt[kStPulledLevels] += is_leader() ? 1 : 0;
     } else {
       // Claims by plain store (no atomic round trip; two discoverers racing on one
@@ -2350,6 +2373,7 @@ __device__ PhaseOut run_phase(const Params& p, Smem& sm, int cur, int parity, bo
                                   in, outs, kStartLevel + lv, parity, pairs_out, claim_store, (lv + 1) % 3, fb_next);
     }
     if (fb_next) dirty |= 1u << ((lv + 1) % kNumFbit);
+    croot_prev = bu && !lazy;  // the next level may resolve its roots through this one's
 
     const long long tb = clk();
     if (solo) {
