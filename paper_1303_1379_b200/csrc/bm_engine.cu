@@ -720,7 +720,7 @@ Params make_params(bm_handle* h, const bm_match_opts& o) {
     h->bu_frac = atof(fr);
     h->bu_rule = 0;
   }
-  h->bu_alpha = h->rs == 2 ? 14.f : 4.f;
+  h->bu_alpha = h->rs == 2 ? 8.f : 4.f;  // (C5 sweep with bucketed pushed levels: 6-10 flat, 14 +7 % per phase)
   if (const char* a = getenv("BM_BU_ALPHA")) h->bu_alpha = (float)atof(a);
   h->bu_beta = 24.0;
   if (const char* b = getenv("BM_BU_BETA")) h->bu_beta = atof(b);
