@@ -878,6 +878,9 @@ constexpr bool BU_MARK = BM_BU_MARK != 0;
 #define BM_BU_PF 1  // pulled levels: L2 prefetch of the next chunk's row state/offsets and of each candidate's columns
                     // (A/B on C5: screen cycles -34 %, -3.5 % per phase)
 #endif
+#ifndef BM_V2ST
+#define BM_V2ST 1  // interleaved row state: a claim by store writes {mate | visited, pred} in one 8-byte store
+#endif
 #ifndef BM_BU_LAZY
 #define BM_BU_LAZY 1  // pulled levels with few rows left resolve their hits' roots instead of scattering them
 #endif
@@ -1098,8 +1101,12 @@ __device__ __forceinline__ void bu_sweep_q(const Params& p, Smem& sm, unsigned o
         // (WR) a tree that found its path after this bitmap was built expands no further
         if (WR && marked_in && root_dead(p, root)) continue;
         if (vv >= 0) {  // matched row: its column joins the frontier below c's tree
-          st_plain(RML(p, rr), vv | kVisBit);
-          st_plain(PRL(p, rr), c);
+          if (BM_V2ST && p.rs == 2) {  // interleaved {mate, pred}: one 8-byte store
+            st_plain(reinterpret_cast<int2*>(RML(p, rr)), make_int2(vv | kVisBit, c));
+          } else {
+            st_plain(RML(p, rr), vv | kVisBit);
+            st_plain(PRL(p, rr), c);
+          }
           if (fb_next) {  // the next level's frontier, ready for a pull
             atomicOr(fb_next + (vv >> 5), 1u << (vv & 31));
             if (WR) st_plain(CR(p, vv), root);
@@ -1584,7 +1591,10 @@ __device__ __forceinline__ void expand_level(const Params& p, Smem& sm, int4* F,
           old[k] = kVisBit;
           if (c >= 0 && !(c & kVisBit) && (!WR || p.claim_mode == 0 || !root_dead(p, sm.root[sl[k]]))) {
             if (claim_store) {  // racy claim: a rare concurrent discoverer pushes the column twice
-              st_plain(RM(p, row[k]), c | kVisBit);
+              if (BM_V2ST && p.rs == 2)  // interleaved: the claim and the predecessor in one 8-byte store
+                st_plain(reinterpret_cast<int2*>(RM(p, row[k])), make_int2(c | kVisBit, sm.col[sl[k]]));
+              else
+                st_plain(RM(p, row[k]), c | kVisBit);
               old[k] = c;
             } else {
               old[k] = at_or(RM(p, row[k]), kVisBit);
@@ -1603,7 +1613,7 @@ __device__ __forceinline__ void expand_level(const Params& p, Smem& sm, int4* F,
                 if (BM_PF == 2) prefetch_l2(p.offs + c);  // the flush reads offs[c], offs[c+1]
                 if (BM_PF == 1) asm volatile("prefetch.global.L2 [%0];" ::"l"(p.offs + c));
               }
-              st_stream(PR(p, row[k]), col, pol);
+              if (!(BM_V2ST && claim_store && p.rs == 2)) st_stream(PR(p, row[k]), col, pol);
               if (p.trace) st_plain(BF(p, c), level + 1);
               if (BU && fb_next) {  // a wide level marks its successor's bitmap (see bu_sweep_q)
                 atomicOr(fb_next + (c >> 5), 1u << (c & 31));
@@ -1925,7 +1935,10 @@ __device__ __noinline__ void push_bucketed(const Params& p, Smem& sm, int4* F, u
       old[k] = kVisBit;
       if (c >= 0 && !(c & kVisBit) && (!WR || p.claim_mode == 0 || !root_dead(p, rootk[k]))) {
         if (claim_store) {
-          st_plain(RM(p, row[k]), c | kVisBit);
+          if (BM_V2ST && p.rs == 2)
+            st_plain(reinterpret_cast<int2*>(RM(p, row[k])), make_int2(c | kVisBit, colk[k]));
+          else
+            st_plain(RM(p, row[k]), c | kVisBit);
           old[k] = c;
         } else {
           old[k] = at_or(RM(p, row[k]), kVisBit);
@@ -1941,7 +1954,7 @@ __device__ __noinline__ void push_bucketed(const Params& p, Smem& sm, int4* F, u
         if (!(old[k] & kVisBit)) {
           wins |= 1u << k;
           if (!(BU && pairs_out)) prefetch_l2(p.offs + c);  // the flush reads offs[c], offs[c+1]
-          st_stream(PR(p, row[k]), col, pol);
+          if (!(BM_V2ST && claim_store && p.rs == 2)) st_stream(PR(p, row[k]), col, pol);
           if (p.trace) st_plain(BF(p, c), level + 1);
         }
       } else if (c == -1) {
