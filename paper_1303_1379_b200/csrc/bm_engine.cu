@@ -1267,8 +1267,8 @@ bm_status bm_run(bm_handle* h, const bm_match_opts* opts, int64_t* cardinality, 
   }
   s = prepare_fresh(h);
   if (s != BM_OK) return s;
-  return drive(h, *opts, true, cardinality, counters, per_iter, cap, cb, user, done,
-               opts->init == BM_INIT_GIVEN);
+  // (given: validated by bm_load_matching; GPU-built: valid by construction)
+  return drive(h, *opts, true, cardinality, counters, per_iter, cap, cb, user, done, true);
 }
 
 bm_status bm_resume(bm_handle* h, const bm_match_opts* opts, int64_t* cardinality, bm_counters* counters,
@@ -1364,7 +1364,8 @@ bm_status bm_match(bm_handle* h, const bm_match_opts* opts, int32_t* rmatch, int
   int32_t done = 0;
   bm_match_opts o = *opts;
   o.max_phases = 0;  // the one-call entry always runs to the maximum
-  s = drive(h, o, true, cardinality, counters, per_iter, cap, cb, user, &done);
+  // a given initial matching is validated in the kernel's setup; the GPU-built one needs no check
+  s = drive(h, o, true, cardinality, counters, per_iter, cap, cb, user, &done, opts->init != BM_INIT_GIVEN);
   if (s != BM_OK) return s;
   return bm_download_matching(h, rmatch, cmatch);
 }

@@ -145,7 +145,9 @@ struct alignas(128) Ctrl {
   unsigned pad2b[24];
   unsigned long long invalid;
   unsigned long long isolated;
-  unsigned long long pad3[14];
+  unsigned long long init_rows;  // setup's check of a given initial matching: matched rows ...
+  unsigned long long init_cols;  // ... and matched columns whose row points back
+  unsigned long long pad3[12];
   unsigned long long stats[kNumStats];
   // run state carried between launches (written by block 0 / thread 0 on exit)
   long long outer;
@@ -2668,12 +2670,22 @@ __global__ void __launch_bounds__(kThreads, BM_MINB) driver_kernel(Params p) {
           if (ld_cg(p.cmatch + c) != -1) continue;
           const unsigned b = ld_ro(p.offs + c), e = ld_ro(p.offs + c + 1);
           if (pass == 0 && e - b != 1) continue;  // one-sided Karp-Sipser: degree-1 columns first
-          for (unsigned j = b; j < e; ++j) {
-            const int r = ld_ro(p.adj + j);
-            if (ld_rlx(RM(p, r)) == -1 && at_cas(RM(p, r), -1, (int)c) == -1) {
-              st_plain(p.cmatch + c, r);
-              break;
-            }
+          // The column's rows in batches of 8 with all their states gathered at
+          // once (first-fit, matching.cpp:13-26, but one round trip per batch
+          // instead of one per row), then a CAS on the first free one(s).
+          bool got = false;
+          for (unsigned j0 = b; j0 < e && !got; j0 += 8) {
+            int rw[8], st[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) rw[k] = j0 + k < e ? ld_ro(p.adj + j0 + k) : -1;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) st[k] = rw[k] >= 0 ? ld_rlx(RM(p, rw[k])) : 0;
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+              if (!got && st[k] == -1 && at_cas(RM(p, rw[k]), -1, (int)c) == -1) {
+                st_plain(p.cmatch + c, rw[k]);
+                got = true;
+              }
           }
         }
         grid_sync(p);
@@ -2681,7 +2693,7 @@ __global__ void __launch_bounds__(kThreads, BM_MINB) driver_kernel(Params p) {
       }
     }
     // ---- setup: validate init, bfs_array init, roots of phase 1 ----
-    unsigned long long bad = 0, iso = 0;
+    unsigned long long bad = 0, iso = 0, mrows = 0, mcols = 0;
     for (unsigned long long b = c_lo + (unsigned long long)blockIdx.x * kThreads; b < c_hi; b += global_threads()) {
       const unsigned long long c = b + threadIdx.x;
       bool root = false;
@@ -2692,6 +2704,7 @@ __global__ void __launch_bounds__(kThreads, BM_MINB) driver_kernel(Params p) {
           if (r < -1 || r >= p.nr) bad++;
           else if (r >= 0 && ld_cg(RM(p, r)) != (int)c) bad++;
           else if (r >= 0 && !has_edge(p.adj, ld_ro(p.offs + c), ld_ro(p.offs + c + 1), r, p.sorted)) bad++;
+          else if (r >= 0) mcols++;
         }
         st_plain(p.bfs + c, r >= 0 ? kUnvisited : kStartLevel);
         if (r < 0) {
@@ -2705,32 +2718,42 @@ __global__ void __launch_bounds__(kThreads, BM_MINB) driver_kernel(Params p) {
       if (cta_reserve(sm, root ? 1u : 0u, root ? deg : 0u, 0u, &ctl->roots, &ctl->n_ep, slot, unused) && root)
         put_entry(p.F0, 0u, p.gidx0, slot, (int)c, (int)c, beg, deg);
     }
+    // Rows need no gather: every matched column's row points back to it (above),
+    // so cmatch is injective into the matched rows; equal counts make it onto,
+    // i.e. every matched row's column points back too (validate, matching.cpp:70-104).
     if (!p.init_checked)
       for (unsigned long long r = r_lo + global_thread(); r < r_hi; r += global_threads()) {
         const int v = ld_cg(RML(p, r));
         if (v < -1 || v >= p.nc) bad++;
-        else if (v >= 0 && ld_cg(CM(p, v)) != (int)r) bad++;
+        else if (v >= 0) mrows++;
       }
     bad = warp_sum(bad);
     iso = warp_sum(iso);
+    mrows = warp_sum(mrows);
+    mcols = warp_sum(mcols);
     if (lane_id() == 0) {
       if (bad) atomicAdd(&ctl->invalid, bad);
       if (iso) atomicAdd(&ctl->isolated, iso);
+      if (mrows) atomicAdd(&ctl->init_rows, mrows);
+      if (mcols) atomicAdd(&ctl->init_cols, mcols);
     }
     grid_sync(p);
     tl_mark(p, kTlSetup, 0);
 #if BM_MG
-    unsigned long long inv_tot = 0, iso_tot = 0, roots_tot = 0;  // team totals
+    unsigned long long inv_tot = 0, iso_tot = 0, roots_tot = 0, mr_tot = 0, mc_tot = 0;  // team totals
     for (int q = 0; q < p.world; ++q) {
+      mr_tot += ld_rlx(&p.peer[q].ctl->init_rows);
+      mc_tot += ld_rlx(&p.peer[q].ctl->init_cols);
       inv_tot += ld_rlx(&p.peer[q].ctl->invalid);
       iso_tot += ld_rlx(&p.peer[q].ctl->isolated);
       roots_tot += ld_rlx(&p.peer[q].ctl->roots.packed) >> 33;
     }
 #else
     const unsigned long long inv_tot = ld_rlx(&ctl->invalid), iso_tot = ld_rlx(&ctl->isolated);
+    const unsigned long long mr_tot = ld_rlx(&ctl->init_rows), mc_tot = ld_rlx(&ctl->init_cols);
     const unsigned long long roots_tot = ld_rlx(&ctl->roots.packed) >> 33;
 #endif
-    if (inv_tot != 0ull) {
+    if (inv_tot != 0ull || (!p.init_checked && mr_tot != mc_tot)) {
       if (is_leader()) ctl->error = kErrInvalidInit;
       return;
     }

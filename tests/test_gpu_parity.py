@@ -447,6 +447,33 @@ def test_initial_matching_pair_must_be_an_edge(engine):
     assert bm.cardinality(r.matching) == 2
 
 
+def test_asymmetric_initial_matching_rejected(engine, oracle):
+    """The setup's row check is a count (matched rows == matched columns whose
+    row points back), not a gather: a row that claims a column which does not
+    point back must still be caught, on the in-kernel (bm_match) and the
+    load-time (bm_load_matching) checks, while valid matchings pass."""
+    g = bm.generate_random_bipartite(3000, 3000, 4.0, 5)
+    good = bm.cheap_matching(g)
+    assert bm.cardinality(engine.match(g, good).matching) == oracle.maximum(g)
+    c0 = int(np.flatnonzero(good.cmatch >= 0)[0])
+    r0 = int(good.cmatch[c0])
+    free_rows = np.flatnonzero(good.rmatch < 0)
+    bad1 = good.copy()
+    bad1.rmatch[free_rows[0]] = c0  # a second row claims c0, which points to r0
+    bad2 = good.copy()
+    bad2.cmatch[c0] = -1  # r0 still claims c0, which now points nowhere
+    bad3 = good.copy()
+    bad3.rmatch[r0] = -1  # c0 claims r0, which points nowhere
+    for m in (bad1, bad2, bad3):
+        with pytest.raises(ValueError):
+            engine.match(g, m)
+        engine.upload(g, force=True)
+        engine.load_matching(m)
+        with pytest.raises(ValueError):
+            engine.run()
+    assert bm.cardinality(engine.match(g, good).matching) == oracle.maximum(g)
+
+
 @pytest.mark.parametrize("spec", [{}, {"BM_BU_FRAC": "1.0"}, {"BM_BU_ALPHA": "100", "BM_SOLO_EDGES": "0"}])
 def test_lazy_frontier_self_check(oracle, monkeypatch, spec):
     """Pulled-capable runs hand wide levels on as (col, root) pairs and build
