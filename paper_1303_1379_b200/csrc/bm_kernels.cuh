@@ -2666,26 +2666,45 @@ __global__ void __launch_bounds__(kThreads, BM_MINB) driver_kernel(Params p) {
     // ---- optional GPU initial matching (parallel first-fit with CAS) ----
     if (p.init_mode != BM_INIT_GIVEN) {
       for (int pass = (p.init_mode == BM_INIT_GPU_KS ? 0 : 1); pass < 2; ++pass) {
-        for (unsigned long long c = c_lo + global_thread(); c < c_hi; c += global_threads()) {
-          if (ld_cg(p.cmatch + c) != -1) continue;
-          const unsigned b = ld_ro(p.offs + c), e = ld_ro(p.offs + c + 1);
-          if (pass == 0 && e - b != 1) continue;  // one-sided Karp-Sipser: degree-1 columns first
-          // The column's rows in batches of 8 with all their states gathered at
-          // once (first-fit, matching.cpp:13-26, but one round trip per batch
-          // instead of one per row), then a CAS on the first free one(s).
-          bool got = false;
-          for (unsigned j0 = b; j0 < e && !got; j0 += 8) {
-            int rw[8], st[8];
+        // Parallel first-fit (matching.cpp:13-26) with CAS: each thread walks two
+        // columns at once, gathering 4 of each column's rows' states per round
+        // (first-fit needs ~3 probes per column on average as the matching fills),
+        // so a round trip serves up to 8 probes instead of one.
+        const unsigned long long GT = global_threads();
+        for (unsigned long long c0 = c_lo + global_thread(); c0 < c_hi; c0 += 2 * GT) {
+          unsigned long long cc[2] = {c0, c0 + GT};
+          bool act[2];
+          unsigned j[2], e[2];
 #pragma unroll
-            for (int k = 0; k < 8; ++k) rw[k] = j0 + k < e ? ld_ro(p.adj + j0 + k) : -1;
+          for (int i = 0; i < 2; ++i) {
+            act[i] = cc[i] < c_hi && ld_cg(p.cmatch + cc[i]) == -1;
+            j[i] = act[i] ? ld_ro(p.offs + cc[i]) : 0u;
+            e[i] = act[i] ? ld_ro(p.offs + cc[i] + 1) : 0u;
+            if (pass == 0 && e[i] - j[i] != 1) act[i] = false;  // one-sided Karp-Sipser: degree-1 columns first
+            if (j[i] >= e[i]) act[i] = false;
+          }
+          while (act[0] || act[1]) {
+            int rw[2][4], st[2][4];
 #pragma unroll
-            for (int k = 0; k < 8; ++k) st[k] = rw[k] >= 0 ? ld_rlx(RM(p, rw[k])) : 0;
+            for (int i = 0; i < 2; ++i)
 #pragma unroll
-            for (int k = 0; k < 8; ++k)
-              if (!got && st[k] == -1 && at_cas(RM(p, rw[k]), -1, (int)c) == -1) {
-                st_plain(p.cmatch + c, rw[k]);
-                got = true;
-              }
+              for (int k = 0; k < 4; ++k) rw[i][k] = act[i] && j[i] + k < e[i] ? ld_ro(p.adj + j[i] + k) : -1;
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+#pragma unroll
+              for (int k = 0; k < 4; ++k) st[i][k] = rw[i][k] >= 0 ? ld_rlx(RM(p, rw[i][k])) : 0;
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+              if (!act[i]) continue;
+#pragma unroll
+              for (int k = 0; k < 4; ++k)
+                if (act[i] && st[i][k] == -1 && at_cas(RM(p, rw[i][k]), -1, (int)cc[i]) == -1) {
+                  st_plain(p.cmatch + cc[i], rw[i][k]);
+                  act[i] = false;
+                }
+              j[i] += 4;
+              if (j[i] >= e[i]) act[i] = false;
+            }
           }
         }
         grid_sync(p);
@@ -2694,29 +2713,51 @@ __global__ void __launch_bounds__(kThreads, BM_MINB) driver_kernel(Params p) {
     }
     // ---- setup: validate init, bfs_array init, roots of phase 1 ----
     unsigned long long bad = 0, iso = 0, mrows = 0, mcols = 0;
-    for (unsigned long long b = c_lo + (unsigned long long)blockIdx.x * kThreads; b < c_hi; b += global_threads()) {
-      const unsigned long long c = b + threadIdx.x;
-      bool root = false;
-      unsigned beg = 0, deg = 0;
-      if (c < c_hi) {
-        const int r = ld_cg(p.cmatch + c);
-        if (!p.init_checked) {
-          if (r < -1 || r >= p.nr) bad++;
-          else if (r >= 0 && ld_cg(RM(p, r)) != (int)c) bad++;
-          else if (r >= 0 && !has_edge(p.adj, ld_ro(p.offs + c), ld_ro(p.offs + c + 1), r, p.sorted)) bad++;
-          else if (r >= 0) mcols++;
-        }
-        st_plain(p.bfs + c, r >= 0 ? kUnvisited : kStartLevel);
-        if (r < 0) {
-          beg = ld_ro(p.offs + c);
-          deg = ld_ro(p.offs + c + 1) - beg;
-          if (deg > 0) root = true; else iso++;
+    // A CTA takes kSetupK x kThreads consecutive columns per step and reserves
+    // their roots' frontier slots with ONE cta_reserve (one per 256 columns cost
+    // 4.5 ms at C5: 390K barrier-separated reservations on one counter).
+    constexpr int kSetupK = 8;
+    for (unsigned long long b = c_lo + (unsigned long long)blockIdx.x * kThreads * kSetupK; b < c_hi;
+         b += global_threads() * kSetupK) {
+      unsigned rootm = 0, beg[kSetupK], deg[kSetupK], cnt = 0, sum = 0;
+#pragma unroll
+      for (int k = 0; k < kSetupK; ++k) {
+        const unsigned long long c = b + (unsigned long long)k * kThreads + threadIdx.x;
+        beg[k] = 0;
+        deg[k] = 0;
+        if (c < c_hi) {
+          const int r = ld_cg(p.cmatch + c);
+          if (!p.init_checked) {
+            if (r < -1 || r >= p.nr) bad++;
+            else if (r >= 0 && ld_cg(RM(p, r)) != (int)c) bad++;
+            else if (r >= 0 && !has_edge(p.adj, ld_ro(p.offs + c), ld_ro(p.offs + c + 1), r, p.sorted)) bad++;
+            else if (r >= 0) mcols++;
+          }
+          st_plain(p.bfs + c, r >= 0 ? kUnvisited : kStartLevel);
+          if (r < 0) {
+            beg[k] = ld_ro(p.offs + c);
+            deg[k] = ld_ro(p.offs + c + 1) - beg[k];
+            if (deg[k] > 0) {
+              rootm |= 1u << k;
+              cnt++;
+              sum += deg[k];
+            } else {
+              iso++;
+            }
+          }
         }
       }
       unsigned long long slot;
       unsigned unused;
-      if (cta_reserve(sm, root ? 1u : 0u, root ? deg : 0u, 0u, &ctl->roots, &ctl->n_ep, slot, unused) && root)
-        put_entry(p.F0, 0u, p.gidx0, slot, (int)c, (int)c, beg, deg);
+      if (cta_reserve(sm, cnt, sum, 0u, &ctl->roots, &ctl->n_ep, slot, unused)) {
+#pragma unroll
+        for (int k = 0; k < kSetupK; ++k)
+          if (rootm & (1u << k)) {
+            const int c = (int)(b + (unsigned long long)k * kThreads + threadIdx.x);
+            put_entry(p.F0, 0u, p.gidx0, slot, c, c, beg[k], deg[k]);
+            slot += (1ull << 33) + deg[k];
+          }
+      }
     }
     // Rows need no gather: every matched column's row points back to it (above),
     // so cmatch is injective into the matched rows; equal counts make it onto,
