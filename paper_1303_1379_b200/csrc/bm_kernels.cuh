@@ -2666,29 +2666,37 @@ __global__ void __launch_bounds__(kThreads, BM_MINB) driver_kernel(Params p) {
     // ---- optional GPU initial matching (parallel first-fit with CAS) ----
     if (p.init_mode != BM_INIT_GIVEN) {
       for (int pass = (p.init_mode == BM_INIT_GPU_KS ? 0 : 1); pass < 2; ++pass) {
-        // Parallel first-fit (matching.cpp:13-26) with CAS: each thread walks two
-        // columns at once, gathering 4 of each column's rows' states per round
-        // (first-fit needs ~3 probes per column on average as the matching fills),
-        // so a round trip serves up to 8 probes instead of one.
+        // Parallel greedy (the GPU cheap init: a maximal matching like first-fit,
+        // matching.cpp:13-26) with CAS: each thread walks two columns at once,
+        // gathering 4 of each column's rows' states per round. A column starts at
+        // a hashed position of its adjacency and wraps around: in ascending row
+        // order every column would first try the lowest row ids, which the
+        // earliest columns have taken (30 ms of probing and CAS conflicts at C5).
         const unsigned long long GT = global_threads();
         for (unsigned long long c0 = c_lo + global_thread(); c0 < c_hi; c0 += 2 * GT) {
           unsigned long long cc[2] = {c0, c0 + GT};
           bool act[2];
-          unsigned j[2], e[2];
+          unsigned j[2], e[2], b0[2], sh[2];
 #pragma unroll
           for (int i = 0; i < 2; ++i) {
             act[i] = cc[i] < c_hi && ld_cg(p.cmatch + cc[i]) == -1;
-            j[i] = act[i] ? ld_ro(p.offs + cc[i]) : 0u;
-            e[i] = act[i] ? ld_ro(p.offs + cc[i] + 1) : 0u;
-            if (pass == 0 && e[i] - j[i] != 1) act[i] = false;  // one-sided Karp-Sipser: degree-1 columns first
-            if (j[i] >= e[i]) act[i] = false;
+            b0[i] = act[i] ? ld_ro(p.offs + cc[i]) : 0u;
+            e[i] = act[i] ? ld_ro(p.offs + cc[i] + 1) - b0[i] : 0u;  // (degree)
+            if (pass == 0 && e[i] != 1) act[i] = false;  // one-sided Karp-Sipser: degree-1 columns first
+            if (e[i] == 0) act[i] = false;
+            sh[i] = e[i] ? (unsigned)((cc[i] * 2654435761ull) >> 7) % e[i] : 0u;
+            j[i] = 0;  // probes done
           }
           while (act[0] || act[1]) {
             int rw[2][4], st[2][4];
 #pragma unroll
             for (int i = 0; i < 2; ++i)
 #pragma unroll
-              for (int k = 0; k < 4; ++k) rw[i][k] = act[i] && j[i] + k < e[i] ? ld_ro(p.adj + j[i] + k) : -1;
+              for (int k = 0; k < 4; ++k) {
+                unsigned q = sh[i] + j[i] + k;
+                if (q >= e[i]) q -= e[i];
+                rw[i][k] = act[i] && j[i] + k < e[i] ? ld_ro(p.adj + b0[i] + q) : -1;
+              }
 #pragma unroll
             for (int i = 0; i < 2; ++i)
 #pragma unroll
