@@ -880,6 +880,9 @@ constexpr bool BU_MARK = BM_BU_MARK != 0;
 #define BM_BU_PF 1  // pulled levels: L2 prefetch of the next chunk's row state/offsets and of each candidate's columns
                     // (A/B on C5: screen cycles -34 %, -3.5 % per phase)
 #endif
+#ifndef BM_INIT_HASH
+#define BM_INIT_HASH 0
+#endif
 #ifndef BM_V2ST
 #define BM_V2ST 1  // interleaved row state: a claim by store writes {mate | visited, pred} in one 8-byte store
 #endif
@@ -2668,10 +2671,11 @@ __global__ void __launch_bounds__(kThreads, BM_MINB) driver_kernel(Params p) {
       for (int pass = (p.init_mode == BM_INIT_GPU_KS ? 0 : 1); pass < 2; ++pass) {
         // Parallel greedy (the GPU cheap init: a maximal matching like first-fit,
         // matching.cpp:13-26) with CAS: each thread walks two columns at once,
-        // gathering 4 of each column's rows' states per round. A column starts at
-        // a hashed position of its adjacency and wraps around: in ascending row
-        // order every column would first try the lowest row ids, which the
-        // earliest columns have taken (30 ms of probing and CAS conflicts at C5).
+        // gathering 4 of each column's rows' states per round. BM_INIT_HASH=1
+        // starts each column at a hashed position of its adjacency instead of its
+        // lowest row: the init drops from 30 to 20 ms at C5, but the phases that
+        // follow took longer (C5 kernel 139 -> 147 ms, 3 runs each), so first-fit
+        // order stays the default.
         const unsigned long long GT = global_threads();
         for (unsigned long long c0 = c_lo + global_thread(); c0 < c_hi; c0 += 2 * GT) {
           unsigned long long cc[2] = {c0, c0 + GT};
@@ -2684,7 +2688,7 @@ __global__ void __launch_bounds__(kThreads, BM_MINB) driver_kernel(Params p) {
             e[i] = act[i] ? ld_ro(p.offs + cc[i] + 1) - b0[i] : 0u;  // (degree)
             if (pass == 0 && e[i] != 1) act[i] = false;  // one-sided Karp-Sipser: degree-1 columns first
             if (e[i] == 0) act[i] = false;
-            sh[i] = e[i] ? (unsigned)((cc[i] * 2654435761ull) >> 7) % e[i] : 0u;
+            sh[i] = (BM_INIT_HASH && e[i]) ? (unsigned)((cc[i] * 2654435761ull) >> 7) % e[i] : 0u;
             j[i] = 0;  // probes done
           }
           while (act[0] || act[1]) {

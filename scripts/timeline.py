@@ -19,13 +19,16 @@ def main():
     cfg = sys.argv[1] if len(sys.argv) > 1 else "C2"
     algo = sys.argv[2] if len(sys.argv) > 2 and not sys.argv[2].startswith("--") else "apfb-wr"
     div = int(sys.argv[sys.argv.index("--div") + 1]) if "--div" in sys.argv else 1
-    bu = "--bu" in sys.argv
+    bu = True if "--bu" in sys.argv else (False if "--push" in sys.argv else "auto")  # default: AUTO, as bench.py
+
     g, known = bench.build_graph(cfg, div)
     init = bm.cheap_matching(g)
     shortest, kernel, improved = bench.ALGOS[algo]
     eng = bm.Engine(0)
     eng.upload(g)
     eng.load_matching(init)
+    if bu == "auto":
+        eng.prepare_row_index()  # as bench.py: qualifying graphs pull their dense levels
     for _ in range(2):
         eng.run(shortest=shortest, kernel=bm.BfsKernel(kernel), improved=improved, bottom_up=bu)
     card, ct, done = eng.run(shortest=shortest, kernel=bm.BfsKernel(kernel), improved=improved, bottom_up=bu)
