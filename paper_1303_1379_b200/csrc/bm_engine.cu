@@ -176,6 +176,7 @@ struct bm_handle {
   long long nonempty = 0;     // columns with at least one edge (upload)
   int2* P = nullptr;          // lazy-frontier pairs (nc), pulled-capable runs only
   int4* tb = nullptr;         // bucketed pushed levels: (row, col, root) triples (ensure_pb)
+  int2* left = nullptr;       // pulled levels' leftover lists: 3 x nr (row, row state)
   unsigned long long pb_max = 0;
   int pb_shift = 0, pb_nb = 0;
   unsigned pb_cap = 0;
@@ -444,6 +445,7 @@ bm_status transpose_alloc(bm_handle* h, int nc, int nr, long long E, int* shift_
   BM_CUDA(dalloc(h->caps, h->fbit, (size_t)kNumFbit * h->nfbit_words));
   BM_CUDA(dalloc(h->caps, h->croot, (size_t)nc));
   BM_CUDA(dalloc(h->caps, h->P, (size_t)nc + kFSlack(nc)));
+  BM_CUDA(dalloc(h->caps, h->left, (size_t)3 * nr));
   int shift = 0;
   {
     const long long nb_min = std::max<long long>(1, (E * (long long)sizeof(int) + (32ll << 20) - 1) >> 25);
@@ -761,6 +763,11 @@ Params make_params(bm_handle* h, const bm_match_opts& o) {
   p.claim_store = 1;
   if (const char* cs = getenv("BM_CLAIM_STORE")) p.claim_store = atoi(cs);
   p.tb = (h->pb_max && p.roffs) ? h->tb : nullptr;
+  {
+    const char* lf = getenv("BM_BU_LEFT");  // 0: every pulled level screens every row
+    const bool use = p.roffs && h->left && !(lf && atoi(lf) == 0);
+    for (int k = 0; k < 3; ++k) p.left[k] = use ? h->left + (size_t)k * h->nr : nullptr;
+  }
   p.pb_min_edges = 1ull << 22;
   if (const char* pm = getenv("BM_PB_MIN")) p.pb_min_edges = (unsigned long long)atoll(pm);
   p.pb_max_edges = h->pb_max;
@@ -1021,6 +1028,7 @@ bm_status bm_destroy(bm_handle* h) {
   dfree(h->croot);
   dfree(h->P);
   dfree(h->tb);
+  dfree(h->left);
   dfree(h->gidx[0]);
   dfree(h->gidx[1]);
   dfree(h->wlog);

@@ -127,7 +127,8 @@ struct alignas(128) Ctrl {
   unsigned pb_cur[2][64];
   unsigned pb_ovf[2];
   unsigned pb_ticket[2];
-  unsigned pad1c[28];
+  unsigned n_left[3];  // pulled levels' leftover lists, by level mod 3 (see Params::left)
+  unsigned pad1c[25];
   unsigned n_log;
   unsigned log_overflow;
   unsigned n_tl;
@@ -255,6 +256,11 @@ struct Params {
   // when it is pushed, first turns them into edge-tiled entries (materialize).
   // Winners of a pulled level never need their offsets gathered.
   int2* P;                 // pairs, indexed like F (level entries [ls, ls + n))
+  // Leftovers of a pulled level: the candidates that found no frontier column,
+  // i.e. exactly the rows still unvisited afterwards (with their row state). A
+  // pulled level after a pulled level takes its candidates from that list
+  // instead of screening every row again. Rotating by level mod 3 (nr each).
+  int2* left[3];
   unsigned long long pairs_min_edges;  // a pushed level this wide emits pairs
   long long phase_bound;
   unsigned long long fcap;  // frontier entries a phase may append (F0/F1 and P hold nc + kFSlack)
@@ -932,9 +938,15 @@ __device__ __forceinline__ void bu_share(const Params& p, int lv) {
 // roots of the hits): a hit column c's root is that of the column that
 // discovered its mate row, croot[pred[cmatch[c]]], which the level before
 // (pulled, with roots) wrote.
+// lin / n_in (nullable): take the candidates from the level before's leftover
+// list instead of screening every row (Params::left); lout / n_out (nullable):
+// append this level's leftovers (candidates that found no frontier column,
+// i.e. every row that is still unvisited afterwards).
 template <bool WR, bool IMP>
 __device__ __forceinline__ void bu_sweep_q(const Params& p, Smem& sm, unsigned out_base, Slot* out, int out_slot,
-                                           int lv, int pf, unsigned* fb_next, bool marked_in, bool lazy_root = false) {
+                                           int lv, int pf, unsigned* fb_next, bool marked_in, bool lazy_root = false,
+                                           const int2* lin = nullptr, unsigned n_in = 0, int2* lout = nullptr,
+                                           unsigned* n_out = nullptr) {
   constexpr int kWarps = kThreads / 32;
   constexpr unsigned kChunk = 128;
   constexpr unsigned kWStage = 128;  // winners staged per warp
@@ -957,7 +969,7 @@ __device__ __forceinline__ void bu_sweep_q(const Params& p, Smem& sm, unsigned o
   const unsigned warp = threadIdx.x >> 5, lane = lane_id();
   BuCand* const q = reinterpret_cast<BuCand*>(sm.wbuf) + warp * kCandCap;
   int2* const wst = reinterpret_cast<int2*>(reinterpret_cast<BuCand*>(sm.wbuf) + kWarps * kCandCap) + warp * kWStage;
-  const unsigned long long nchunks = (rhi - rlo + kChunk - 1) / kChunk;
+  const unsigned long long nchunks = lin ? (n_in + kChunk - 1) / kChunk : (rhi - rlo + kChunk - 1) / kChunk;
   const unsigned long long W = (unsigned long long)gridDim.x * kWarps;
   unsigned long long chunk = (unsigned long long)blockIdx.x * kWarps + warp;
   unsigned qh = 0, qt = 0;  // queued candidates q[qh, qt) (warp-uniform)
@@ -977,6 +989,35 @@ __device__ __forceinline__ void bu_sweep_q(const Params& p, Smem& sm, unsigned o
       if (lane < left) q[lane] = keep;
       qh = 0;
       qt = left;
+      if (lin) {  // the level before's leftovers: (row, row state), every one a candidate
+        const unsigned long long i0 = chunk * kChunk;
+        chunk += W;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const unsigned long long i = i0 + (unsigned long long)k * 32 + lane;
+          BuCand c;
+          c.row = -1;
+          c.val = 0;
+          c.j0 = c.j1 = 0;
+          if (i < n_in) {
+            const int2 ent = ld_cg(lin + i);
+            c.row = ent.x;
+            c.val = ent.y;
+            c.j0 = ld_ro(p.roffs + ent.x);
+            c.j1 = ld_ro(p.roffs + ent.x + 1);
+          }
+          const unsigned m = __ballot_sync(kFull, c.row >= 0);
+          if (c.row >= 0) {
+            q[qt + __popc(m & ((1u << lane) - 1))] = c;
+#if BM_BU_PF
+            prefetch_l2n(p.radj + c.j0);
+#endif
+          }
+          qt += __popc(m);
+        }
+        __syncwarp();
+        continue;
+      }
       const unsigned long long r0 = rlo + chunk * kChunk;
       chunk += W;
 #if BM_BU_PF
@@ -1137,7 +1178,16 @@ __device__ __forceinline__ void bu_sweep_q(const Params& p, Smem& sm, unsigned o
         done = true;
       }
       j += kBuProbe;
-      if (done || j >= j1) rr = -1;
+      if (done || j >= j1) {
+        if (!done && lout) {  // no frontier column: still unvisited after this level
+          cg::coalesced_group g = cg::coalesced_threads();
+          unsigned b = 0;
+          if (g.thread_rank() == 0) b = atomicAdd(n_out, g.size());
+          b = g.shfl(b, 0) + g.thread_rank();
+          st_plain(lout + b, make_int2(rr, vv));
+        }
+        rr = -1;
+      }
     }
     if (BM_BU_CYC) {
       __syncwarp();
@@ -2186,6 +2236,7 @@ __device__ PhaseOut run_phase(const Params& p, Smem& sm, int cur, int parity, bo
   bool in_pairs = false;  // this level's entries are (col, root) pairs in P (pulled-capable kernels)
   unsigned dirty = 0;     // frontier bitmaps holding marks (bit b: fbit[b]); grid-uniform
   bool croot_prev = false;  // the level before was pulled and wrote its frontier's roots (lazy roots)
+  bool list_prev = false;   // the level before was pulled and listed its leftovers (Params::left)
   const unsigned long long pol_mat = policy_evict_first();
 #if BM_MG
   if (routed(p)) {
@@ -2340,6 +2391,7 @@ __device__ PhaseOut run_phase(const Params& p, Smem& sm, int cur, int parity, bo
       out.launches = (long long)ld_rlx((const unsigned long long*)&ctl->solo_launches);
       in_pairs = false;  // solo levels push entries
       croot_prev = false;
+      list_prev = false;
       if (ld_rlx(&ctl->solo_stop)) break;
       continue;
     }
@@ -2375,7 +2427,14 @@ __device__ PhaseOut run_phase(const Params& p, Smem& sm, int cur, int parity, bo
       } else if (is_leader()) {
         sm.cnt[kStCexp] += n;  // (entries; bu_prep counts the live ones)
       }
-      BU_SWEEP<WR, IMP>(p, sm, ls + n, outs, (lv + 1) % 3, lv, parity, fb_next, marked, lazy);
+      if (p.left[0]) {  // leftover lists (single-GPU pulled levels)
+        const int2* lin = list_prev ? p.left[(lv + 2) % 3] : nullptr;
+        const unsigned n_in = list_prev ? ld_rlx(&ctl->n_left[(lv + 2) % 3]) : 0u;
+        bu_sweep_q<WR, IMP>(p, sm, ls + n, outs, (lv + 1) % 3, lv, parity, fb_next, marked, lazy, lin, n_in,
+                            p.left[lv % 3], &ctl->n_left[lv % 3]);
+      } else {
+        BU_SWEEP<WR, IMP>(p, sm, ls + n, outs, (lv + 1) % 3, lv, parity, fb_next, marked, lazy);
+      }
       if (threadIdx.x == 0) sm.cnt[kStPulledLevels] += is_leader() ? 1 : 0;
     } else {
       // Claims by plain store (no atomic round trip; two discoverers racing on one
@@ -2392,6 +2451,7 @@ __device__ PhaseOut run_phase(const Params& p, Smem& sm, int cur, int parity, bo
     }
     if (fb_next) dirty |= 1u << ((lv + 1) % kNumFbit);
     croot_prev = bu && !lazy;  // the next level may resolve its roots through this one's
+    list_prev = bu && p.left[0] != nullptr;  // this level wrote its leftovers
 
     const long long tb = clk();
     if (solo) {
@@ -2399,6 +2459,7 @@ __device__ PhaseOut run_phase(const Params& p, Smem& sm, int cur, int parity, bo
       __syncthreads();
     } else {
       grid_sync(p);
+      if (is_leader()) ctl->n_left[(lv + 2) % 3] = 0;  // the level before's list: consumed or unused; next written at lv + 2
       if (bucketed && is_leader()) {  // next used two levels on (after another barrier)
         for (int b = 0; b < p.pb_nb; ++b) ctl->pb_cur[lv & 1][b] = 0;
         ctl->pb_ovf[lv & 1] = 0;
@@ -2431,6 +2492,7 @@ __device__ PhaseOut run_phase(const Params& p, Smem& sm, int cur, int parity, bo
     }
     if (solo && (stop || T > p.solo_edges)) {  // block 0 hands the BFS back to the grid
       if (threadIdx.x == 0) {
+        for (int k = 0; k < 3; ++k) ctl->n_left[k] = 0;  // (solo levels list nothing; the grid restarts clean)
         ctl->solo_lv = lv;
         ctl->solo_stop = stop ? 1 : 0;
         ctl->solo_ls = ls;
@@ -2593,6 +2655,7 @@ __device__ PhaseOut run_phase(const Params& p, Smem& sm, int cur, int parity, bo
   }
   if (is_leader()) {
     ctl->n_ep = 0u;
+    for (int k = 0; k < 3; ++k) ctl->n_left[k] = 0u;
     ctl->n_log = 0u;
     ctl->log_overflow = 0u;
   }

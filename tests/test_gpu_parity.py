@@ -277,12 +277,16 @@ def test_unsorted_columns_and_upload_checks(engine, oracle):
     assert bm.cardinality(res.matching) == want
 
 
-def test_bottom_up_levels_parity(oracle, corpus, monkeypatch):
+@pytest.mark.parametrize("left", ["1", "0"], ids=["leftover_lists", "screen_all"])
+def test_bottom_up_levels_parity(oracle, corpus, monkeypatch, left):
     """Every level bottom-up (BM_BU_FRAC=0, no single-CTA levels): the pulled
     levels must give the same maxima as the oracle on the corpus and on larger
-    graphs, under every driver/kernel combination."""
+    graphs, under every driver/kernel combination — with consecutive pulled
+    levels taking their candidates from the level before's leftover list, and
+    with every level screening every row (BM_BU_LEFT=0)."""
     monkeypatch.setenv("BM_BU_FRAC", "0")
     monkeypatch.setenv("BM_SOLO_EDGES", "0")
+    monkeypatch.setenv("BM_BU_LEFT", left)
     eng = bm.Engine(0)
     eng.bottom_up = True
     graphs = [g for g, _ in corpus[:120] + corpus[-4:]] + [
