@@ -764,8 +764,13 @@ Params make_params(bm_handle* h, const bm_match_opts& o) {
   if (const char* cs = getenv("BM_CLAIM_STORE")) p.claim_store = atoi(cs);
   p.tb = (h->pb_max && p.roffs) ? h->tb : nullptr;
   {
-    const char* lf = getenv("BM_BU_LEFT");  // 0: every pulled level screens every row
-    const bool use = p.roffs && h->left && !(lf && atoi(lf) == 0);
+    // Leftover lists pay where screening every row means streaming a row state
+    // far beyond L2 (interleaved layout): C5 -2 % per phase; on C2, whose row
+    // state stays in L2, the lists' scattered offset reads cost more (+6 %).
+    // BM_BU_LEFT=1|0 forces them on|off.
+    const char* lf = getenv("BM_BU_LEFT");
+    const bool want = lf && *lf ? atoi(lf) != 0 : h->rs == 2;
+    const bool use = p.roffs && h->left && want;
     for (int k = 0; k < 3; ++k) p.left[k] = use ? h->left + (size_t)k * h->nr : nullptr;
   }
   p.pb_min_edges = 1ull << 22;
