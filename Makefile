@@ -35,6 +35,7 @@ endif
 REF_LIB   := oracle/_ref/libbmatch_ref.so
 SHIM_TEST := oracle/_ref/shim_test
 SUITE     := oracle/_ref/b200_suite
+SHIM_E2E  := oracle/_ref/shim_e2e
 
 .PHONY: all ref shimtest suite clean
 all: $(LIB) $(ORACLE) $(GENORACLE)
@@ -81,7 +82,13 @@ $(SHIM_TEST): tests/cpp/shim_test.cpp include/bmatch_b200.hpp include/bmatch_b20
 	    -Wl,-rpath,'$$ORIGIN' -Wl,-rpath,'$$ORIGIN/../../paper_1303_1379_b200'
 
 # The paper's evaluation artefacts through the reference's run_suite (tools/b200_suite.cpp).
-suite: $(SUITE)
+suite: $(SUITE) $(SHIM_E2E)
+
+# The drop-in path's end-to-end time (reference types in, std::vector storage).
+$(SHIM_E2E): tools/shim_e2e.cpp include/bmatch_b200.hpp include/bmatch_b200.h include/bmatch_b200_gen.h $(REF_LIB) $(LIB)
+	$(CXX) -std=c++20 -O2 -Wall -Wextra -pthread -I$(REF_ROOT)/include $(REF_INC) -Iinclude \
+	    -o $@ tools/shim_e2e.cpp $(REF_LIB) $(LIB) \
+	    -Wl,-rpath,'$$ORIGIN' -Wl,-rpath,'$$ORIGIN/../../paper_1303_1379_b200'
 
 $(SUITE): tools/b200_suite.cpp include/bmatch_b200.hpp include/bmatch_b200.h include/bmatch_b200_gen.h $(REF_LIB) $(LIB)
 	$(CXX) -std=c++20 -O2 -Wall -Wextra -pthread -I$(REF_ROOT)/include $(REF_INC) -Iinclude \
