@@ -227,6 +227,11 @@ bm_status   bm_download_matching(bm_handle* h, int32_t* rmatch, int32_t* cmatch)
  * launches of the last bm_run/bm_resume/bm_match, and how many kernels that
  * run launched (driver launches plus the initial-state copy kernel). */
 bm_status   bm_last_kernel_time(bm_handle* h, double* ms, int32_t* launches);
+/* BFS launches (levels) of every outer iteration of the last bm_run / bm_resume /
+ * bm_match (PhaseCounters::bfs_launches_per_iteration): *n receives the count,
+ * out (nullable) up to cap entries. Lets a caller pass a small per_iter buffer
+ * to bm_match and fetch the rest only when the run had more phases. */
+bm_status   bm_last_phase_launches(bm_handle* h, int64_t* out, int64_t cap, int64_t* n);
 
 /* Fault injection for the failure-path tests (no reference counterpart; every
  * key defaults to off). PHASE_BOUND: replaces the nc+1 termination bound of

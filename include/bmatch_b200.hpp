@@ -135,7 +135,9 @@ inline DriverResult run(const BipartiteCsr& g, MatchingState init, bool shortest
   o.init = BM_INIT_GIVEN;
   o.bottom_up = BM_BU_AUTO;  // pull dense levels where the engine judges it pays
   bm_counters ct{};
-  std::vector<int64_t> launches((size_t)g.nc + 2);
+  // A small per-phase buffer (a buffer of nc + 2 entries, zeroed on every call,
+  // cost 160 ms of page faults at 1e8 columns); longer runs fetch the rest after.
+  std::vector<int64_t> launches((size_t)std::min<int64_t>((int64_t)g.nc + 2, 1024));
   int64_t card = 0;
   ObserverCtx ctx{&observer, nullptr};
   const bm_status s =
@@ -143,6 +145,12 @@ inline DriverResult run(const BipartiteCsr& g, MatchingState init, bool shortest
                (int64_t)launches.size(), observer ? &observer_trampoline : nullptr, observer ? &ctx : nullptr);
   if (ctx.error) std::rethrow_exception(ctx.error);
   throw_on(s);
+  if (ct.outer_iterations > (int64_t)launches.size()) {
+    launches.resize((size_t)ct.outer_iterations);
+    int64_t n = 0;
+    throw_on(bm_last_phase_launches(eng.get(), launches.data(), (int64_t)launches.size(), &n));
+    ct.n_phase_records = n;
+  }
   DriverResult res;
   res.matching = std::move(init);
   res.counters.outer_iterations = ct.outer_iterations;

@@ -116,6 +116,7 @@ _PROTOS = {
     "bm_bottom_up_auto": (C.c_int, [_vp, _i32p]),
     "bm_prepare_row_index": (C.c_int, [_vp]),
     "bm_download_row_index": (C.c_int, [_vp, C.POINTER(C.c_uint32), _i32p]),
+    "bm_last_phase_launches": (C.c_int, [_vp, _i64p, C.c_int64, _i64p]),
     "bm_match": (C.c_int, [_vp, C.POINTER(bm_match_opts), _i32p, _i32p, _i64p, C.POINTER(bm_counters),
                            _i64p, C.c_int64, PHASE_CB, _vp]),
     "bm_load_matching": (C.c_int, [_vp, _i32p, _i32p]),

@@ -1331,6 +1331,17 @@ bm_status bm_last_kernel_time(bm_handle* h, double* ms, int32_t* launches) {
   return BM_OK;
 }
 
+bm_status bm_last_phase_launches(bm_handle* h, int64_t* out, int64_t cap, int64_t* n) {
+  bm_status s = check_handle(h, false);
+  if (s != BM_OK) return s;
+  if (n) *n = (int64_t)h->phase_launches.size();
+  if (out && cap > 0) {
+    const size_t k = std::min<size_t>(h->phase_launches.size(), (size_t)cap);
+    for (size_t i = 0; i < k; ++i) out[i] = h->phase_launches[i];
+  }
+  return BM_OK;
+}
+
 bm_status bm_debug_stats(bm_handle* h, uint64_t* out, int64_t cap, int64_t* n) {
   bm_status s = check_handle(h, false);
   if (s != BM_OK) return s;
