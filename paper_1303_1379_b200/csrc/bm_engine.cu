@@ -674,7 +674,7 @@ bm_status ensure_pb(bm_handle* h) {
     h->pb_max = 0;
     return BM_OK;
   }
-  unsigned long long tmax = std::min<unsigned long long>((unsigned long long)h->E, 1ull << 27);
+  unsigned long long tmax = std::min<unsigned long long>((unsigned long long)h->E, 1ull << 28);
   if (const char* m = getenv("BM_PB_MAX")) tmax = std::min<unsigned long long>(tmax, (unsigned long long)atoll(m));
   const unsigned long long rows_target = (24ull << 20) / (4ull * h->rs);
   int shift = 0;

@@ -886,6 +886,9 @@ constexpr bool BU_MARK = BM_BU_MARK != 0;
 #define BM_BU_PF 1  // pulled levels: L2 prefetch of the next chunk's row state/offsets and of each candidate's columns
                     // (A/B on C5: screen cycles -34 %, -3.5 % per phase)
 #endif
+#ifndef BM_PB_MARK
+#define BM_PB_MARK 0  // 1: bucketed pushed levels mark their pulled successor's bitmap and roots (no bu_prep)
+#endif
 #ifndef BM_INIT_HASH
 #define BM_INIT_HASH 0
 #endif
@@ -1771,7 +1774,8 @@ __device__ __forceinline__ void expand_level(const Params& p, Smem& sm, int4* F,
 template <bool WR, bool IMP, bool BU>
 __device__ __noinline__ void push_bucketed(const Params& p, Smem& sm, int4* F, unsigned ls, unsigned n, unsigned T,
                                             const unsigned* gin, unsigned* gout, Slot* in, Slot* out, int level,
-                                            int pf, bool pairs_out, bool claim_store, int par) {
+                                            int pf, bool pairs_out, bool claim_store, int par,
+                                            unsigned* fb_next = nullptr) {
   const unsigned tid = threadIdx.x;
   Ctrl* ctl = p.ctl;
   unsigned c_trav = 0, c_cexp = 0, c_nvis = 0, c_entries = 0;
@@ -2011,6 +2015,10 @@ __device__ __noinline__ void push_bucketed(const Params& p, Smem& sm, int4* F, u
           if (!(BU && pairs_out)) prefetch_l2(p.offs + c);  // the flush reads offs[c], offs[c+1]
           if (!(BM_V2ST && claim_store && p.rs == 2)) st_stream(PR(p, row[k]), col, pol);
           if (p.trace) st_plain(BF(p, c), level + 1);
+          if (BU && fb_next) {  // (BM_PB_MARK) the pulled successor's bitmap and roots, marked here
+            atomicOr(fb_next + (c >> 5), 1u << (c & 31));
+            if (WR) st_plain(CR(p, c), root);
+          }
         }
       } else if (c == -1) {
         const bool one = WR && p.ep_one;
@@ -2408,10 +2416,11 @@ __device__ PhaseOut run_phase(const Params& p, Smem& sm, int cur, int parity, bo
     // A wide level also marks its winners in the next level's bitmap (and their
     // roots in croot), so that a pulled successor starts at once (no bu_prep pass
     // of its own: one scattered croot store per column fewer, and one grid barrier).
-    unsigned* const fb_next = pairs_out && BU_MARK ? p.fbit[(lv + 1) % kNumFbit] : nullptr;
     // a wide pushed level over a row state far beyond L2 goes bucketed (push_bucketed)
-    const bool bucketed = BU && !bu && !solo && p.tb && !fb_next && (unsigned long long)T >= p.pb_min_edges &&
+    const bool bucketed = BU && !bu && !solo && p.tb && (unsigned long long)T >= p.pb_min_edges &&
                           (unsigned long long)T <= p.pb_max_edges;
+    unsigned* const fb_next =
+        pairs_out && (BU_MARK || (BM_PB_MARK && bucketed)) ? p.fbit[(lv + 1) % kNumFbit] : nullptr;
     // Lazy roots: when few rows are left to claim (fewer than a third of the
     // frontier), bu_prep skips the scattered root store of every frontier column
     // and the hits resolve their roots through the level before (bu_sweep_q).
@@ -2444,7 +2453,7 @@ __device__ PhaseOut run_phase(const Params& p, Smem& sm, int cur, int parity, bo
       const bool claim_store = p.claim_store && (unsigned long long)ls + n + T <= p.fcap;
       if (bucketed)
         push_bucketed<WR, IMP, BU>(p, sm, F, ls, n, T, (lv & 1) ? p.gidx1 : p.gidx0, (lv & 1) ? p.gidx0 : p.gidx1,
-                                   in, outs, kStartLevel + lv, parity, pairs_out, claim_store, lv & 1);
+                                   in, outs, kStartLevel + lv, parity, pairs_out, claim_store, lv & 1, fb_next);
       else
         expand_level<WR, IMP, BU>(p, sm, F, ls, n, T, (lv & 1) ? p.gidx1 : p.gidx0, (lv & 1) ? p.gidx0 : p.gidx1,
                                   in, outs, kStartLevel + lv, parity, pairs_out, claim_store, (lv + 1) % 3, fb_next);
