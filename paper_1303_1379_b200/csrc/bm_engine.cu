@@ -745,6 +745,7 @@ Params make_params(bm_handle* h, const bm_match_opts& o) {
   p.log_cap = h->log_cap;
   p.trace = 0;
   p.claim_mode = o.claim_policy;
+  if (const char* cm = getenv("BM_CLAIM_MODE")) p.claim_mode = atoi(cm);  // tuning override
   p.ep_one = (o.bfs_kernel == BM_BFS_WR && o.endpoint_policy != BM_EP_EVERY) ? 1 : 0;
   p.solo_edges = kSoloEdges;
   if (const char* se = getenv("BM_SOLO_EDGES")) p.solo_edges = (unsigned)atol(se);  // tuning / tests

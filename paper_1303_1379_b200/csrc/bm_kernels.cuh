@@ -886,6 +886,9 @@ constexpr bool BU_MARK = BM_BU_MARK != 0;
 #define BM_BU_PF 1  // pulled levels: L2 prefetch of the next chunk's row state/offsets and of each candidate's columns
                     // (A/B on C5: screen cycles -34 %, -3.5 % per phase)
 #endif
+#ifndef BM_BU_DEADHIT
+#define BM_BU_DEADHIT 0  // 1: a pulled hit on a column of a tree that found its path since bu_prep is skipped
+#endif
 #ifndef BM_PB_MARK
 #define BM_PB_MARK 0  // 1: bucketed pushed levels mark their pulled successor's bitmap and roots (no bu_prep)
 #endif
@@ -1147,8 +1150,10 @@ __device__ __forceinline__ void bu_sweep_q(const Params& p, Smem& sm, unsigned o
           root = ld_cg(CR(p, c));
 #endif
         }
-        // (WR) a tree that found its path after this bitmap was built expands no further
-        if (WR && marked_in && root_dead(p, root)) continue;
+        // (WR) a tree that found its path after this bitmap was built expands no
+        // further (gpu_match.cpp:106-108 tests the root mark when the column is
+        // expanded; a pulled level expands at the hit)
+        if (WR && (marked_in || BM_BU_DEADHIT) && root_dead(p, root)) continue;
         if (vv >= 0) {  // matched row: its column joins the frontier below c's tree
           if (BM_V2ST && p.rs == 2) {  // interleaved {mate, pred}: one 8-byte store
             st_plain(reinterpret_cast<int2*>(RML(p, rr)), make_int2(vv | kVisBit, c));
