@@ -445,7 +445,10 @@ bm_status transpose_alloc(bm_handle* h, int nc, int nr, long long E, int* shift_
   BM_CUDA(dalloc(h->caps, h->fbit, (size_t)kNumFbit * h->nfbit_words));
   BM_CUDA(dalloc(h->caps, h->croot, (size_t)nc));
   BM_CUDA(dalloc(h->caps, h->P, (size_t)nc + kFSlack(nc)));
-  BM_CUDA(dalloc(h->caps, h->left, (size_t)3 * nr));
+  if (dalloc(h->caps, h->left, (size_t)3 * nr) != cudaSuccess) {  // optional (leftover lists): screen instead
+    cudaGetLastError();
+    h->left = nullptr;
+  }
   int shift = 0;
   {
     const long long nb_min = std::max<long long>(1, (E * (long long)sizeof(int) + (32ll << 20) - 1) >> 25);
@@ -689,7 +692,11 @@ bm_status ensure_pb(bm_handle* h) {
     h->pb_max = 0;
     return BM_OK;
   }
-  BM_CUDA(dalloc(h->caps, h->tb, need));
+  if (dalloc(h->caps, h->tb, need) != cudaSuccess) {  // an optimisation: without the memory, push unbucketed
+    cudaGetLastError();
+    h->pb_max = 0;
+    return BM_OK;
+  }
   h->pb_max = tmax;
   h->pb_shift = shift;
   h->pb_nb = nb;
