@@ -1,0 +1,6 @@
+# session 3 closing check: smoke, the whole GPU suite, the default bench line (C5)
+cd "${GRAFT_REPO_ROOT:-/root/repo}"; mkdir -p gpurun_out/final3
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/final3/smoke.log 2>&1; tail -1 gpurun_out/final3/smoke.log
+timeout 1800 python -m pytest tests -q -m gpu > gpurun_out/final3/pytest.log 2>&1; tail -2 gpurun_out/final3/pytest.log
+timeout 1500 python bench.py > gpurun_out/final3/bench_C5.json 2> gpurun_out/final3/bench_C5.err
+tail -1 gpurun_out/final3/bench_C5.json | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('C5', round(d['ms_per_step'],2), 'phases', d['counters_mean']['outer_iterations'], 'e2e', round(d['e2e']['ms_per_step'],1), 'cpu', d['cpu_baseline']['seconds'], d['parity']['ok'], d['clocks'])"
