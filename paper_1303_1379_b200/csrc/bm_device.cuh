@@ -127,23 +127,6 @@ __device__ __forceinline__ unsigned ld_rlx_hint(const unsigned* p, unsigned long
   asm volatile("ld.relaxed.gpu.global.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol) : "memory");
   return v;
 }
-__device__ __forceinline__ int ld_ca_hint(const int* p, unsigned long long pol) {
-  int v;
-  asm volatile("ld.global.ca.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
-  return v;
-}
-__device__ __forceinline__ int ld_cg_hint(const int* p, unsigned long long pol) {
-  int v;
-  asm volatile("ld.global.cg.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
-  return v;
-}
-__device__ __forceinline__ int4 ld_cg_hint(const int4* p, unsigned long long pol) {
-  int4 v;
-  asm volatile("ld.global.cg.L2::cache_hint.v4.b32 {%0,%1,%2,%3}, [%4], %5;"
-               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-               : "l"(p), "l"(pol));
-  return v;
-}
 __device__ __forceinline__ unsigned ld_ro_hint(const unsigned* p, unsigned long long pol) {
   unsigned v;
   asm("ld.global.nc.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
@@ -152,13 +135,6 @@ __device__ __forceinline__ unsigned ld_ro_hint(const unsigned* p, unsigned long 
 __device__ __forceinline__ int ld_stream(const int* p, unsigned long long pol) {
   int v;
   asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
-  return v;
-}
-__device__ __forceinline__ int4 ld_stream4(const int4* p, unsigned long long pol) {  // read-only, 16 B aligned
-  int4 v;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.b32 {%0,%1,%2,%3}, [%4], %5;"
-               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-               : "l"(p), "l"(pol));
   return v;
 }
 __device__ __forceinline__ int4 ld_cg_stream(const int4* p, unsigned long long pol) {

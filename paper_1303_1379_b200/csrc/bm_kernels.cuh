@@ -312,10 +312,7 @@ struct BuCand {
   unsigned j0;
   unsigned j1;
 };
-#ifndef BM_BU_SLOTS
-#define BM_BU_SLOTS 1  // candidates per lane in a pulled sweep (1: bu_sweep_q, 2: bu_sweep_q2)
-#endif
-constexpr int kCandCap = BM_BU_SLOTS == 2 ? 192 : 160;  // per-warp queue: < 32 x slots left over + one screened chunk of 128 rows
+constexpr int kCandCap = 160;  // per-warp queue: < 32 left over + one screened chunk of 128 rows
 
 struct Smem {
   union {  // a top-down window (a pulled level keeps its candidate queues in wbuf)
@@ -874,26 +871,9 @@ __device__ __forceinline__ void bu_prep(const Params& p, Smem& sm, const int4* F
 #ifndef BM_BU_PROBE
 #define BM_BU_PROBE 4
 #endif
-#ifndef BM_BU_MARK
-#define BM_BU_MARK 0  // 1: wide levels mark the next level's frontier bitmap at claim time instead of a bu_prep
-                      // pass (A/B on B200: +20 % on C5, +29 % on C2 -- the stores in the latency-bound loops cost more)
-#endif
-constexpr bool BU_MARK = BM_BU_MARK != 0;
-#ifndef BM_BU_VEC
-#define BM_BU_VEC 0  // pulled probes: 1 = one aligned int4 load per round, 0 = four scalar loads
-#endif
 #ifndef BM_BU_PF
 #define BM_BU_PF 1  // pulled levels: L2 prefetch of the next chunk's row state/offsets and of each candidate's columns
                     // (A/B on C5: screen cycles -34 %, -3.5 % per phase)
-#endif
-#ifndef BM_BU_DEADHIT
-#define BM_BU_DEADHIT 0  // 1: a pulled hit on a column of a tree that found its path since bu_prep is skipped
-#endif
-#ifndef BM_PB_MARK
-#define BM_PB_MARK 0  // 1: bucketed pushed levels mark their pulled successor's bitmap and roots (no bu_prep)
-#endif
-#ifndef BM_INIT_HASH
-#define BM_INIT_HASH 0
 #endif
 #ifndef BM_V2ST
 #define BM_V2ST 1  // interleaved row state: a claim by store writes {mate | visited, pred} in one 8-byte store
@@ -904,10 +884,6 @@ constexpr bool BU_MARK = BM_BU_MARK != 0;
 constexpr bool BU_LAZY = BM_BU_LAZY != 0;
 #ifndef BM_BU_CYC
 #define BM_BU_CYC 0  // 1: per-part warp cycle counters in pulled levels (profiling builds)
-#endif
-#ifndef BM_BU_HINT
-#define BM_BU_HINT 0  // pulled levels: 1 = the streamed row screen, roots and visited sweep evict_first,
-                      // the frontier-bitmap probes evict_last (keep the bitmap in L2)
 #endif
 // Warp-autonomous pulled level. Every warp owns chunks of 128 consecutive rows
 // (grid-stride over the warps of the grid) and keeps a queue of candidate rows
@@ -934,11 +910,6 @@ __device__ __forceinline__ void bu_share(const Params& p, int lv) {
 }
 #endif
 
-// fb_next (nullable): the next level's bitmap, marked here for every winner
-// together with its root (croot), so that a pulled successor needs no bu_prep.
-// marked_in: this level's bitmap was marked that way by the level before, so
-// it still holds columns of trees that have found their path since (WR skips
-// them at the hit, as bu_prep would have left them out).
 // lazy_root: this level's bu_prep wrote no roots (few rows are left to claim, so
 // scattering one root per frontier column would cost more than resolving the
 // roots of the hits): a hit column c's root is that of the column that
@@ -950,7 +921,7 @@ __device__ __forceinline__ void bu_share(const Params& p, int lv) {
 // i.e. every row that is still unvisited afterwards).
 template <bool WR, bool IMP>
 __device__ __forceinline__ void bu_sweep_q(const Params& p, Smem& sm, unsigned out_base, Slot* out, int out_slot,
-                                           int lv, int pf, unsigned* fb_next, bool marked_in, bool lazy_root = false,
+                                           int lv, int pf, bool lazy_root = false,
                                            const int2* lin = nullptr, unsigned n_in = 0, int2* lout = nullptr,
                                            unsigned* n_out = nullptr) {
   constexpr int kWarps = kThreads / 32;
@@ -962,8 +933,6 @@ __device__ __forceinline__ void bu_sweep_q(const Params& p, Smem& sm, unsigned o
   constexpr int kBuProbe = BM_BU_PROBE;
   const unsigned* fb = p.fbit[lv % kNumFbit];
   const unsigned long long pol = policy_evict_first();
-  const unsigned long long keep = policy_evict_last();
-  (void)keep;
   unsigned* const path_flag = path_flag_of(p, pf);
 #if BM_MG
   const unsigned long long rlo = (unsigned long long)p.row_lo, rhi = (unsigned long long)p.row_hi;  // own rows
@@ -1046,13 +1015,8 @@ __device__ __forceinline__ void bu_sweep_q(const Params& p, Smem& sm, unsigned o
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         const unsigned long long r = r0 + (unsigned long long)k * 32 + lane;
-#if BM_BU_HINT
-        v[k] = r < rhi ? ld_cg_hint(RML(p, r), pol) : -3;
-        o[k] = r <= rhi ? ld_ro_hint(p.roffs + r, pol) : 0u;  // roffs[rhi] ends the last row
-#else
         v[k] = r < rhi ? ld_cg(RML(p, r)) : -3;
         o[k] = r <= rhi ? ld_ro(p.roffs + r) : 0u;  // roffs[rhi] ends the last row
-#endif
       }
       {
         const unsigned long long r = r0 + 4 * 32;
@@ -1108,30 +1072,11 @@ __device__ __forceinline__ void bu_sweep_q(const Params& p, Smem& sm, unsigned o
     if (rr >= 0) {
       int cs[kBuProbe];
       unsigned wd[kBuProbe];
-#if BM_BU_VEC
-      // one aligned 16-byte load per round: the row's entries of that group (one
-      // L2 request instead of four)
-      static_assert(kBuProbe == 4, "BM_BU_VEC probes aligned groups of 4");
-      {
-        const unsigned g0 = j & ~3u;
-        const int4 v = ld_stream4(reinterpret_cast<const int4*>(p.radj + g0), pol);
-        cs[0] = (g0 >= j && g0 < j1) ? v.x : -1;
-        cs[1] = (g0 + 1 >= j && g0 + 1 < j1) ? v.y : -1;
-        cs[2] = (g0 + 2 >= j && g0 + 2 < j1) ? v.z : -1;
-        cs[3] = (g0 + 3 < j1) ? v.w : -1;
-        j = g0;  // (advanced by kBuProbe below)
-      }
-#else
 #pragma unroll
       for (int k = 0; k < kBuProbe; ++k) cs[k] = j + k < j1 ? ld_stream(p.radj + j + k, pol) : -1;
-#endif
 #pragma unroll
       for (int k = 0; k < kBuProbe; ++k)
-#if BM_BU_HINT
-        wd[k] = cs[k] >= 0 ? ld_ca_hint(reinterpret_cast<const int*>(fb) + (cs[k] >> 5), keep) : 0u;
-#else
         wd[k] = cs[k] >= 0 ? ld_ca(reinterpret_cast<const int*>(fb) + (cs[k] >> 5)) : 0u;
-#endif
       bool done = false;
 #pragma unroll
       for (int k = 0; k < kBuProbe; ++k) {
@@ -1144,26 +1089,14 @@ __device__ __forceinline__ void bu_sweep_q(const Params& p, Smem& sm, unsigned o
           root = ld_cg(CR(p, ld_cg(PR(p, ld_rlx(CM(p, c))))));
           if (root_dead(p, root)) continue;  // (bu_prep filtered by the pairs' roots; the tree may have died since)
         } else if (WR) {
-#if BM_BU_HINT
-          root = ld_cg_hint(CR(p, c), pol);
-#else
           root = ld_cg(CR(p, c));
-#endif
         }
-        // (WR) a tree that found its path after this bitmap was built expands no
-        // further (gpu_match.cpp:106-108 tests the root mark when the column is
-        // expanded; a pulled level expands at the hit)
-        if (WR && (marked_in || BM_BU_DEADHIT) && root_dead(p, root)) continue;
         if (vv >= 0) {  // matched row: its column joins the frontier below c's tree
           if (BM_V2ST && p.rs == 2) {  // interleaved {mate, pred}: one 8-byte store
             st_plain(reinterpret_cast<int2*>(RML(p, rr)), make_int2(vv | kVisBit, c));
           } else {
             st_plain(RML(p, rr), vv | kVisBit);
             st_plain(PRL(p, rr), c);
-          }
-          if (fb_next) {  // the next level's frontier, ready for a pull
-            atomicOr(fb_next + (vv >> 5), 1u << (vv & 31));
-            if (WR) st_plain(CR(p, vv), root);
           }
           win = true;
           cw = vv;
@@ -1263,228 +1196,6 @@ __device__ __forceinline__ void bu_sweep_q(const Params& p, Smem& sm, unsigned o
   flush_count(sm, kStRowsPulled, c_rows);
 }
 
-// The same pulled level with two candidates per lane (BM_BU_SLOTS=2): each
-// round probes two columns of each of the lane's two rows, so twice as many
-// row searches are in flight per warp (the sweep is bound by the latency of
-// its radj -> bitmap -> root chains, not by bandwidth).
-template <bool WR, bool IMP>
-__device__ __forceinline__ void bu_sweep_q2(const Params& p, Smem& sm, unsigned out_base, Slot* out, int out_slot,
-                                            int lv, int pf, unsigned* fb_next, bool marked_in, bool /*lazy*/ = false) {
-  constexpr int kWarps = kThreads / 32;
-  constexpr unsigned kChunk = 128;
-  constexpr unsigned kWStage = 128;
-  static_assert(sizeof(BuCand) * kCandCap * kWarps + sizeof(int2) * kWStage * kWarps <= sizeof(int2) * kWBuf,
-                "candidate queues and winner stages must fit in wbuf");
-  constexpr int kP = 2;  // probes per slot per round
-  const unsigned* fb = p.fbit[lv % kNumFbit];
-  const unsigned long long pol = policy_evict_first();
-  unsigned* const path_flag = path_flag_of(p, pf);
-#if BM_MG
-  const unsigned long long rlo = (unsigned long long)p.row_lo, rhi = (unsigned long long)p.row_hi;
-#else
-  const unsigned long long rlo = 0, rhi = (unsigned long long)p.nr;
-#endif
-  unsigned c_trav = 0, c_nvis = 0, c_rows = 0;
-  const unsigned warp = threadIdx.x >> 5, lane = lane_id();
-  const unsigned lt = (1u << lane) - 1u;
-  BuCand* const q = reinterpret_cast<BuCand*>(sm.wbuf) + warp * kCandCap;
-  int2* const wst = reinterpret_cast<int2*>(reinterpret_cast<BuCand*>(sm.wbuf) + kWarps * kCandCap) + warp * kWStage;
-  const unsigned long long nchunks = (rhi - rlo + kChunk - 1) / kChunk;
-  const unsigned long long W = (unsigned long long)gridDim.x * kWarps;
-  unsigned long long chunk = (unsigned long long)blockIdx.x * kWarps + warp;
-  unsigned qh = 0, qt = 0, nwin = 0;
-  int rr[2] = {-1, -1}, vv[2] = {0, 0};
-  unsigned j[2] = {0, 0}, j1[2] = {0, 0};
-  for (;;) {
-    const unsigned idle0 = __ballot_sync(kFull, rr[0] < 0), idle1 = __ballot_sync(kFull, rr[1] < 0);
-    const unsigned need = (unsigned)(__popc(idle0) + __popc(idle1));
-    while (qt - qh < need && chunk < nchunks) {
-      const unsigned left = qt - qh;
-      BuCand keep[2];
-      if (lane < left) keep[0] = q[qh + lane];
-      if (lane + 32 < left) keep[1] = q[qh + lane + 32];
-      __syncwarp();
-      if (lane < left) q[lane] = keep[0];
-      if (lane + 32 < left) q[lane + 32] = keep[1];
-      qh = 0;
-      qt = left;
-      const unsigned long long r0 = rlo + chunk * kChunk;
-      chunk += W;
-#if BM_BU_PF
-      if (chunk < nchunks) {
-        const unsigned long long rn = rlo + chunk * kChunk;
-        const unsigned long long rend = min(rhi, rn + kChunk);
-        const unsigned long long rr0 = rn + (unsigned long long)lane * (8 / p.rs);
-        if (rr0 < rend) prefetch_l2n(RML(p, rr0));
-        if (lane < 16) {
-          const unsigned long long ro = rn + (unsigned long long)lane * 8;
-          if (ro <= rend) prefetch_l2n(p.roffs + ro);
-        }
-      }
-#endif
-      int v[4];
-      unsigned o[4], onext;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const unsigned long long r = r0 + (unsigned long long)k * 32 + lane;
-        v[k] = r < rhi ? ld_cg(RML(p, r)) : -3;
-        o[k] = r <= rhi ? ld_ro(p.roffs + r) : 0u;
-      }
-      {
-        const unsigned long long r = r0 + 4 * 32;
-        onext = (lane == 0 && r <= rhi) ? ld_ro(p.roffs + r) : 0u;
-      }
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        unsigned e = __shfl_down_sync(kFull, o[k], 1);
-        const unsigned nxt0 = __shfl_sync(kFull, k < 3 ? o[(k + 1) & 3] : onext, 0);
-        if (lane == 31) e = nxt0;
-        const bool is_cand = (v[k] >= 0 && !(v[k] & kVisBit)) || v[k] == -1;
-        const unsigned m = __ballot_sync(kFull, is_cand && e > o[k]);
-        if (is_cand && e > o[k]) {
-          BuCand c;
-          c.row = (int)(r0 + (unsigned long long)k * 32 + lane);
-          c.val = v[k];
-          c.j0 = o[k];
-          c.j1 = e;
-          q[qt + __popc(m & lt)] = c;
-#if BM_BU_PF
-          prefetch_l2n(p.radj + o[k]);
-#endif
-        }
-        qt += __popc(m);
-      }
-      __syncwarp();
-    }
-    {  // idle slots take queued candidates: slot 0 lanes first, then slot 1, in lane order
-      const unsigned avail = qt - qh;
-      const unsigned n0 = min((unsigned)__popc(idle0), avail);
-      const unsigned k0 = __popc(idle0 & lt);
-      if (rr[0] < 0 && k0 < avail) {
-        const BuCand c = q[qh + k0];
-        rr[0] = c.row; vv[0] = c.val; j[0] = c.j0; j1[0] = c.j1;
-        c_rows++;
-      }
-      const unsigned k1 = n0 + __popc(idle1 & lt);
-      if (rr[1] < 0 && k1 < avail) {
-        const BuCand c = q[qh + k1];
-        rr[1] = c.row; vv[1] = c.val; j[1] = c.j0; j1[1] = c.j1;
-        c_rows++;
-      }
-      qh += min(need, avail);
-    }
-    if (!__any_sync(kFull, rr[0] >= 0 || rr[1] >= 0)) break;
-    int cs[2][kP];
-    unsigned wd[2][kP];
-#pragma unroll
-    for (int s = 0; s < 2; ++s)
-#pragma unroll
-      for (int k = 0; k < kP; ++k) cs[s][k] = (rr[s] >= 0 && j[s] + k < j1[s]) ? ld_stream(p.radj + j[s] + k, pol) : -1;
-#pragma unroll
-    for (int s = 0; s < 2; ++s)
-#pragma unroll
-      for (int k = 0; k < kP; ++k)
-        wd[s][k] = cs[s][k] >= 0 ? ld_ca(reinterpret_cast<const int*>(fb) + (cs[s][k] >> 5)) : 0u;
-    bool win[2] = {false, false}, ep[2] = {false, false};
-    int cw[2] = {0, 0}, rootw[2] = {0, 0}, myrow[2] = {rr[0], rr[1]};
-#pragma unroll
-    for (int s = 0; s < 2; ++s) {
-      if (rr[s] < 0) continue;
-      bool done = false;
-#pragma unroll
-      for (int k = 0; k < kP; ++k) {
-        const int c = cs[s][k];
-        if (done || c < 0) continue;
-        c_trav++;
-        if (!((wd[s][k] >> (c & 31)) & 1)) continue;
-        const int root = WR ? ld_cg(CR(p, c)) : c;
-        if (WR && marked_in && root_dead(p, root)) continue;
-        if (vv[s] >= 0) {
-          st_plain(RML(p, rr[s]), vv[s] | kVisBit);
-          st_plain(PRL(p, rr[s]), c);
-          if (fb_next) {
-            atomicOr(fb_next + (vv[s] >> 5), 1u << (vv[s] & 31));
-            if (WR) st_plain(CR(p, vv[s]), root);
-          }
-          win[s] = true;
-          cw[s] = vv[s];
-          rootw[s] = root;
-          done = true;
-          continue;
-        }
-        const bool one = WR && p.ep_one;
-        if (one && root_dead(p, root)) continue;
-        bool mine = true;
-        if (one) mine = at_cas(BF(p, root), kStartLevel, IMP ? -rr[s] : kFoundMark) == kStartLevel;
-        else if (WR) st_rlx(BF(p, root), IMP ? -rr[s] : kFoundMark);
-        if (!mine) continue;
-        if (WR) mark_dead(p, root);
-        st_rlx(RML(p, rr[s]), -2);
-        st_plain(PRL(p, rr[s]), c);
-        ep[s] = true;
-        if (ld_rlx(path_flag) == 0u) st_rlx(path_flag, 1u);
-        done = true;
-      }
-      j[s] += kP;
-      if (done || j[s] >= j1[s]) rr[s] = -1;
-    }
-#pragma unroll
-    for (int s = 0; s < 2; ++s) {
-      const unsigned m = __ballot_sync(kFull, win[s]);
-      if (win[s]) wst[nwin + __popc(m & lt)] = make_int2(cw[s], rootw[s]);
-      nwin += __popc(m);
-      c_nvis += win[s] ? 1u : 0u;
-    }
-    if (nwin > kWStage - 64) {
-      __syncwarp();
-#if BM_MG
-      if (routed(p)) {
-        warp_flush_mg(p, sm, wst, nwin, out_slot, pol);
-      } else
-#endif
-      {
-        unsigned base = 0;
-        if (lane == 0) base = (unsigned)(atomicAdd(&out->packed, (unsigned long long)nwin << 33) >> 33);
-        base = __shfl_sync(kFull, base, 0) + out_base;
-        for (unsigned i = lane; i < nwin; i += 32) st_stream(p.P + base + i, wst[i], pol);
-      }
-      __syncwarp();
-      nwin = 0;
-    }
-#pragma unroll
-    for (int s = 0; s < 2; ++s) {
-      const unsigned m = __ballot_sync(kFull, ep[s]);
-      if (m) {
-        unsigned eb = 0;
-        if (lane == 0) eb = atomicAdd(&p.ctl->n_ep, (unsigned)__popc(m));
-        eb = __shfl_sync(kFull, eb, 0) + __popc(m & lt);
-        if (ep[s]) st_plain(p.EP + eb, myrow[s]);
-      }
-    }
-  }
-  if (nwin) {
-    __syncwarp();
-#if BM_MG
-    if (routed(p)) {
-      warp_flush_mg(p, sm, wst, nwin, out_slot, pol);
-    } else
-#endif
-    {
-      unsigned base = 0;
-      if (lane == 0) base = (unsigned)(atomicAdd(&out->packed, (unsigned long long)nwin << 33) >> 33);
-      base = __shfl_sync(kFull, base, 0) + out_base;
-      for (unsigned i = lane; i < nwin; i += 32) st_stream(p.P + base + i, wst[i], pol);
-    }
-  }
-  flush_count(sm, kStTrav, c_trav);
-  flush_count(sm, kStNvis, c_nvis);
-  flush_count(sm, kStRowsPulled, c_rows);
-}
-#if BM_BU_SLOTS == 2
-#define BU_SWEEP bu_sweep_q2
-#else
-#define BU_SWEEP bu_sweep_q
-#endif
 
 // ---------------------------------------------------------------------------
 // One BFS level (GPUBFS, Alg. 2, gpu_match.cpp:42-70; GPUBFS-WR, Alg. 4,
@@ -1492,7 +1203,7 @@ __device__ __forceinline__ void bu_sweep_q2(const Params& p, Smem& sm, unsigned 
 template <bool WR, bool IMP, bool BU>
 __device__ __forceinline__ void expand_level(const Params& p, Smem& sm, int4* F, unsigned ls, unsigned n, unsigned T,
                              const unsigned* gin, unsigned* gout, Slot* in, Slot* out, int level, int pf,
-                             bool pairs_out, bool claim_store, int out_slot, unsigned* fb_next = nullptr) {
+                             bool pairs_out, bool claim_store, int out_slot) {
   if (T == 0) return;
   const unsigned tid = threadIdx.x;
   unsigned c_trav = 0, c_cexp = 0, c_nvis = 0, c_entries = 0;
@@ -1678,10 +1389,6 @@ __device__ __forceinline__ void expand_level(const Params& p, Smem& sm, int4* F,
               }
               if (!(BM_V2ST && claim_store && p.rs == 2)) st_stream(PR(p, row[k]), col, pol);
               if (p.trace) st_plain(BF(p, c), level + 1);
-              if (BU && fb_next) {  // a wide level marks its successor's bitmap (see bu_sweep_q)
-                atomicOr(fb_next + (c >> 5), 1u << (c & 31));
-                if (WR) st_plain(CR(p, c), root);
-              }
             }
           } else if (c == -1) {
             // ONE_PER_TREE: a tree that already holds an endpoint leaves the row alone
@@ -1779,8 +1486,7 @@ __device__ __forceinline__ void expand_level(const Params& p, Smem& sm, int4* F,
 template <bool WR, bool IMP, bool BU>
 __device__ __noinline__ void push_bucketed(const Params& p, Smem& sm, int4* F, unsigned ls, unsigned n, unsigned T,
                                             const unsigned* gin, unsigned* gout, Slot* in, Slot* out, int level,
-                                            int pf, bool pairs_out, bool claim_store, int par,
-                                            unsigned* fb_next = nullptr) {
+                                            int pf, bool pairs_out, bool claim_store, int par) {
   const unsigned tid = threadIdx.x;
   Ctrl* ctl = p.ctl;
   unsigned c_trav = 0, c_cexp = 0, c_nvis = 0, c_entries = 0;
@@ -2020,10 +1726,6 @@ __device__ __noinline__ void push_bucketed(const Params& p, Smem& sm, int4* F, u
           if (!(BU && pairs_out)) prefetch_l2(p.offs + c);  // the flush reads offs[c], offs[c+1]
           if (!(BM_V2ST && claim_store && p.rs == 2)) st_stream(PR(p, row[k]), col, pol);
           if (p.trace) st_plain(BF(p, c), level + 1);
-          if (BU && fb_next) {  // (BM_PB_MARK) the pulled successor's bitmap and roots, marked here
-            atomicOr(fb_next + (c >> 5), 1u << (c & 31));
-            if (WR) st_plain(CR(p, c), root);
-          }
         }
       } else if (c == -1) {
         const bool one = WR && p.ep_one;
@@ -2156,16 +1858,9 @@ __device__ __forceinline__ void sweep_visited(const Params& p) {
   const unsigned long long GT = global_threads();
   for (unsigned long long k0 = global_thread(); k0 < n4; k0 += K * GT) {
     int4 v[K];
-#if BM_BU_HINT
-    const unsigned long long pol = policy_evict_first();
-#pragma unroll
-    for (int i = 0; i < K; ++i)
-      if (k0 + i * GT < n4) v[i] = ld_cg_hint(r4 + k0 + i * GT, pol);
-#else
 #pragma unroll
     for (int i = 0; i < K; ++i)
       if (k0 + i * GT < n4) v[i] = ld_cg(r4 + k0 + i * GT);
-#endif
 #pragma unroll
     for (int i = 0; i < K; ++i) {
       if (k0 + i * GT >= n4) continue;
@@ -2300,7 +1995,7 @@ __device__ PhaseOut run_phase(const Params& p, Smem& sm, int cur, int parity, bo
         bu_share(p, lv);
         grid_sync(p);
       }
-      BU_SWEEP<WR, IMP>(p, sm, ls + n, outs, (lv + 1) % 3, lv, parity, nullptr, false);
+      bu_sweep_q<WR, IMP>(p, sm, ls + n, outs, (lv + 1) % 3, lv, parity);
       if (threadIdx.x == 0) sm.cnt[kStPulledLevels] += is_leader() ? 1 : 0;
     } else {
       // store claims when even one entry per frontier edge of the team fits every inbox
@@ -2418,37 +2113,26 @@ __device__ PhaseOut run_phase(const Params& p, Smem& sm, int cur, int parity, bo
     if (solo) __syncthreads();
     // a wide level hands its winners on as pairs (see Params::P)
     const bool pairs_out = BU && p.roffs && !p.trace && !solo && (bu || (unsigned long long)T >= p.pairs_min_edges);
-    // A wide level also marks its winners in the next level's bitmap (and their
-    // roots in croot), so that a pulled successor starts at once (no bu_prep pass
-    // of its own: one scattered croot store per column fewer, and one grid barrier).
-    // a wide pushed level over a row state far beyond L2 goes bucketed (push_bucketed)
+    // A wide pushed level over a row state far beyond L2 goes bucketed (push_bucketed).
+    // (Marking the successor's bitmap at claim time instead of a bu_prep pass was
+    // measured and lost: +20 % per phase on C5 unbucketed, +12 % bucketed.)
     const bool bucketed = BU && !bu && !solo && p.tb && (unsigned long long)T >= p.pb_min_edges &&
                           (unsigned long long)T <= p.pb_max_edges;
-    unsigned* const fb_next =
-        pairs_out && (BU_MARK || (BM_PB_MARK && bucketed)) ? p.fbit[(lv + 1) % kNumFbit] : nullptr;
     // Lazy roots: when few rows are left to claim (fewer than a third of the
     // frontier), bu_prep skips the scattered root store of every frontier column
     // and the hits resolve their roots through the level before (bu_sweep_q).
     const long long unvisited = (long long)p.nr - (long long)ls - (long long)n;
-    const bool lazy = BU_LAZY && WR && bu && croot_prev && in_pairs && BM_BU_SLOTS == 1 && 3 * unvisited < (long long)n;
+    const bool lazy = BU_LAZY && WR && bu && croot_prev && in_pairs && 3 * unvisited < (long long)n;
     if (bu) {
-      const bool marked = (dirty >> (lv % kNumFbit)) & 1u;  // the level before marked this one
-      if (!marked) {
-        bu_prep<WR>(p, sm, F, in_pairs, ls, n, lv, !lazy);
-        grid_sync(p);
-        dirty |= 1u << (lv % kNumFbit);
-        tl_mark(p, kTlPrep, n);
-      } else if (is_leader()) {
-        sm.cnt[kStCexp] += n;  // (entries; bu_prep counts the live ones)
-      }
-      if (p.left[0]) {  // leftover lists (single-GPU pulled levels)
-        const int2* lin = list_prev ? p.left[(lv + 2) % 3] : nullptr;
-        const unsigned n_in = list_prev ? ld_rlx(&ctl->n_left[(lv + 2) % 3]) : 0u;
-        bu_sweep_q<WR, IMP>(p, sm, ls + n, outs, (lv + 1) % 3, lv, parity, fb_next, marked, lazy, lin, n_in,
-                            p.left[lv % 3], &ctl->n_left[lv % 3]);
-      } else {
-        BU_SWEEP<WR, IMP>(p, sm, ls + n, outs, (lv + 1) % 3, lv, parity, fb_next, marked, lazy);
-      }
+      bu_prep<WR>(p, sm, F, in_pairs, ls, n, lv, !lazy);
+      grid_sync(p);
+      dirty |= 1u << (lv % kNumFbit);
+      tl_mark(p, kTlPrep, n);
+      const bool lists = p.left[0] != nullptr;  // leftover lists (single-GPU pulled levels)
+      const int2* lin = lists && list_prev ? p.left[(lv + 2) % 3] : nullptr;
+      const unsigned n_in = lin ? ld_rlx(&ctl->n_left[(lv + 2) % 3]) : 0u;
+      bu_sweep_q<WR, IMP>(p, sm, ls + n, outs, (lv + 1) % 3, lv, parity, lazy, lin, n_in,
+                          lists ? p.left[lv % 3] : nullptr, lists ? &ctl->n_left[lv % 3] : nullptr);
       if (threadIdx.x == 0) sm.cnt[kStPulledLevels] += is_leader() ? 1 : 0;
     } else {
       // Claims by plain store (no atomic round trip; two discoverers racing on one
@@ -2458,12 +2142,11 @@ __device__ PhaseOut run_phase(const Params& p, Smem& sm, int cur, int parity, bo
       const bool claim_store = p.claim_store && (unsigned long long)ls + n + T <= p.fcap;
       if (bucketed)
         push_bucketed<WR, IMP, BU>(p, sm, F, ls, n, T, (lv & 1) ? p.gidx1 : p.gidx0, (lv & 1) ? p.gidx0 : p.gidx1,
-                                   in, outs, kStartLevel + lv, parity, pairs_out, claim_store, lv & 1, fb_next);
+                                   in, outs, kStartLevel + lv, parity, pairs_out, claim_store, lv & 1);
       else
         expand_level<WR, IMP, BU>(p, sm, F, ls, n, T, (lv & 1) ? p.gidx1 : p.gidx0, (lv & 1) ? p.gidx0 : p.gidx1,
-                                  in, outs, kStartLevel + lv, parity, pairs_out, claim_store, (lv + 1) % 3, fb_next);
+                                  in, outs, kStartLevel + lv, parity, pairs_out, claim_store, (lv + 1) % 3);
     }
-    if (fb_next) dirty |= 1u << ((lv + 1) % kNumFbit);
     croot_prev = bu && !lazy;  // the next level may resolve its roots through this one's
     list_prev = bu && p.left[0] != nullptr;  // this level wrote its leftovers
 
@@ -2748,16 +2431,12 @@ __global__ void __launch_bounds__(kThreads, BM_MINB) driver_kernel(Params p) {
       for (int pass = (p.init_mode == BM_INIT_GPU_KS ? 0 : 1); pass < 2; ++pass) {
         // Parallel greedy (the GPU cheap init: a maximal matching like first-fit,
         // matching.cpp:13-26) with CAS: each thread walks two columns at once,
-        // gathering 4 of each column's rows' states per round. BM_INIT_HASH=1
-        // starts each column at a hashed position of its adjacency instead of its
-        // lowest row: the init drops from 30 to 20 ms at C5, but the phases that
-        // follow took longer (C5 kernel 139 -> 147 ms, 3 runs each), so first-fit
-        // order stays the default.
+        // gathering 4 of each column's rows' states per round, in first-fit order.
         const unsigned long long GT = global_threads();
         for (unsigned long long c0 = c_lo + global_thread(); c0 < c_hi; c0 += 2 * GT) {
           unsigned long long cc[2] = {c0, c0 + GT};
           bool act[2];
-          unsigned j[2], e[2], b0[2], sh[2];
+          unsigned j[2], e[2], b0[2];
 #pragma unroll
           for (int i = 0; i < 2; ++i) {
             act[i] = cc[i] < c_hi && ld_cg(p.cmatch + cc[i]) == -1;
@@ -2765,7 +2444,6 @@ __global__ void __launch_bounds__(kThreads, BM_MINB) driver_kernel(Params p) {
             e[i] = act[i] ? ld_ro(p.offs + cc[i] + 1) - b0[i] : 0u;  // (degree)
             if (pass == 0 && e[i] != 1) act[i] = false;  // one-sided Karp-Sipser: degree-1 columns first
             if (e[i] == 0) act[i] = false;
-            sh[i] = (BM_INIT_HASH && e[i]) ? (unsigned)((cc[i] * 2654435761ull) >> 7) % e[i] : 0u;
             j[i] = 0;  // probes done
           }
           while (act[0] || act[1]) {
@@ -2773,11 +2451,7 @@ __global__ void __launch_bounds__(kThreads, BM_MINB) driver_kernel(Params p) {
 #pragma unroll
             for (int i = 0; i < 2; ++i)
 #pragma unroll
-              for (int k = 0; k < 4; ++k) {
-                unsigned q = sh[i] + j[i] + k;
-                if (q >= e[i]) q -= e[i];
-                rw[i][k] = act[i] && j[i] + k < e[i] ? ld_ro(p.adj + b0[i] + q) : -1;
-              }
+              for (int k = 0; k < 4; ++k) rw[i][k] = act[i] && j[i] + k < e[i] ? ld_ro(p.adj + b0[i] + j[i] + k) : -1;
 #pragma unroll
             for (int i = 0; i < 2; ++i)
 #pragma unroll
