@@ -45,6 +45,16 @@ constexpr unsigned kSoloEdges = BM_SOLO_EDGES;  // widest level block 0 expands 
 // store claims can create (see expand_level). A level claims by store only when
 // even one entry per frontier edge would fit, so the capacity can never overflow.
 constexpr size_t kFSlack(long long nc) { return (size_t)(nc / 4 + 4096); }
+// Inlining of the level functions into the persistent kernel (A/B knobs): a
+// separately compiled function gets its own register allocation instead of
+// sharing the driver's.
+#define BM_NOINLINE_FN __device__ __noinline__  // (for -DBM_SWEEP_INLINE=BM_NOINLINE_FN)
+#ifndef BM_SWEEP_INLINE
+#define BM_SWEEP_INLINE __device__ __forceinline__
+#endif
+#ifndef BM_EXPAND_INLINE
+#define BM_EXPAND_INLINE __device__ __forceinline__
+#endif
 constexpr int kStartLevel = 2;        // L0 (gpu_match.cpp:275)
 constexpr int kUnvisited = kStartLevel - 1;
 constexpr int kFoundMark = kStartLevel - 2;
@@ -829,7 +839,7 @@ __device__ __forceinline__ void bu_clear(const Params& p, int b) {
 // run) or as entries (level 0). Counts the live entries as columns expanded.
 // write_root = false (lazy roots, see bu_sweep_q): only the bitmap is built.
 template <bool WR>
-__device__ __forceinline__ void bu_prep(const Params& p, Smem& sm, const int4* F, bool pairs, unsigned ls,
+BM_SWEEP_INLINE void bu_prep(const Params& p, Smem& sm, const int4* F, bool pairs, unsigned ls,
                                         unsigned n, int lv, bool write_root = true) {
   unsigned* fb = p.fbit[lv % kNumFbit];
   unsigned live = 0;
@@ -920,7 +930,7 @@ __device__ __forceinline__ void bu_share(const Params& p, int lv) {
 // append this level's leftovers (candidates that found no frontier column,
 // i.e. every row that is still unvisited afterwards).
 template <bool WR, bool IMP>
-__device__ __forceinline__ void bu_sweep_q(const Params& p, Smem& sm, unsigned out_base, Slot* out, int out_slot,
+BM_SWEEP_INLINE void bu_sweep_q(const Params& p, Smem& sm, unsigned out_base, Slot* out, int out_slot,
                                            int lv, int pf, bool lazy_root = false,
                                            const int2* lin = nullptr, unsigned n_in = 0, int2* lout = nullptr,
                                            unsigned* n_out = nullptr) {
@@ -1201,7 +1211,7 @@ __device__ __forceinline__ void bu_sweep_q(const Params& p, Smem& sm, unsigned o
 // One BFS level (GPUBFS, Alg. 2, gpu_match.cpp:42-70; GPUBFS-WR, Alg. 4,
 // gpu_match.cpp:99-133) over the frontier F[ls, ls+n) holding T edges.
 template <bool WR, bool IMP, bool BU>
-__device__ __forceinline__ void expand_level(const Params& p, Smem& sm, int4* F, unsigned ls, unsigned n, unsigned T,
+BM_EXPAND_INLINE void expand_level(const Params& p, Smem& sm, int4* F, unsigned ls, unsigned n, unsigned T,
                              const unsigned* gin, unsigned* gout, Slot* in, Slot* out, int level, int pf,
                              bool pairs_out, bool claim_store, int out_slot) {
   if (T == 0) return;
