@@ -327,6 +327,14 @@ class Engine:
         """Build the row index now (bm_prepare_row_index), so "auto" pulls from the next run."""
         check(lib.bm_prepare_row_index(self._h))
 
+    def last_phase_launches(self) -> list:
+        """BFS launches per outer iteration of the last run (bm_last_phase_launches)."""
+        n = C.c_int64()
+        check(lib.bm_last_phase_launches(self._h, None, 0, C.byref(n)))
+        out = np.zeros(max(n.value, 1), np.int64)
+        check(lib.bm_last_phase_launches(self._h, out.ctypes.data_as(C.POINTER(C.c_int64)), n.value, C.byref(n)))
+        return [int(x) for x in out[:n.value]]
+
     def row_index(self):
         """The row index the pulled levels read (bm_download_row_index): (roffs[nr+1], radj[E])."""
         nc, nr, ne = self.graph_info()

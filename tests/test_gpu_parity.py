@@ -533,3 +533,13 @@ def test_bucketed_push_parity(oracle, corpus, monkeypatch, spec):
     tl = [k for k, _, _ in eng.timeline()]
     assert "bucketed" in tl  # the path ran (last run's timeline)
     eng.close()
+
+
+def test_last_phase_launches_match_counters(engine, oracle):
+    """bm_last_phase_launches returns the per-phase BFS launch counts that
+    bm_match reports in PhaseCounters (the C++ shim fetches long runs this way)."""
+    g = bm.generate_random_bipartite(50000, 50000, 6.0, 21)
+    res = engine.match(g, bm.cheap_matching(g))
+    launches = engine.last_phase_launches()
+    assert launches == list(res.counters.bfs_launches_per_iteration)
+    assert len(launches) == res.counters.outer_iterations >= 1
