@@ -55,6 +55,9 @@ constexpr size_t kFSlack(long long nc) { return (size_t)(nc / 4 + 4096); }
 #ifndef BM_EXPAND_INLINE
 #define BM_EXPAND_INLINE __device__ __forceinline__
 #endif
+#ifndef BM_EXPAND_OOL
+#define BM_EXPAND_OOL 1  // pulled-capable kernels call expand_level out of line (expand_level_ool)
+#endif
 constexpr int kStartLevel = 2;        // L0 (gpu_match.cpp:275)
 constexpr int kUnvisited = kStartLevel - 1;
 constexpr int kFoundMark = kStartLevel - 2;
@@ -1479,6 +1482,26 @@ BM_EXPAND_INLINE void expand_level(const Params& p, Smem& sm, int4* F, unsigned 
   flush_count(sm, kStEntries, c_entries);
 }
 
+// expand_level compiled out of line, for the pulled-capable kernels: there it
+// gets its own register allocation instead of sharing the driver's (A/B: C5
+// -7 %, C2 -9 % per phase), while inlining stays better for the push-only
+// kernels (C3 +21 %, C4 +17 % out of line).
+template <bool WR, bool IMP, bool BU>
+__device__ __noinline__ void expand_level_ool(const Params& p, Smem& sm, int4* F, unsigned ls, unsigned n, unsigned T,
+                                              const unsigned* gin, unsigned* gout, Slot* in, Slot* out, int level,
+                                              int pf, bool pairs_out, bool claim_store, int out_slot) {
+  expand_level<WR, IMP, BU>(p, sm, F, ls, n, T, gin, gout, in, out, level, pf, pairs_out, claim_store, out_slot);
+}
+template <bool WR, bool IMP, bool BU>
+__device__ __forceinline__ void expand_level_any(const Params& p, Smem& sm, int4* F, unsigned ls, unsigned n,
+                                                 unsigned T, const unsigned* gin, unsigned* gout, Slot* in, Slot* out,
+                                                 int level, int pf, bool pairs_out, bool claim_store, int out_slot) {
+  if constexpr (BU && BM_EXPAND_OOL)
+    expand_level_ool<WR, IMP, BU>(p, sm, F, ls, n, T, gin, gout, in, out, level, pf, pairs_out, claim_store, out_slot);
+  else
+    expand_level<WR, IMP, BU>(p, sm, F, ls, n, T, gin, gout, in, out, level, pf, pairs_out, claim_store, out_slot);
+}
+
 // ---------------------------------------------------------------------------
 // Bucketed pushed level: the same level as expand_level (gpubfs / gpubfs_wr,
 // gpu_match.cpp:42-70, 99-133) for wide levels over a row state far beyond L2,
@@ -2010,7 +2033,7 @@ __device__ PhaseOut run_phase(const Params& p, Smem& sm, int cur, int parity, bo
     } else {
       // store claims when even one entry per frontier edge of the team fits every inbox
       const bool claim_store = p.claim_store && sm.mg_tot[3] + T_tot <= p.fcap;
-      expand_level<WR, IMP, BU>(p, sm, F, ls, n, T, (lv & 1) ? p.gidx1 : p.gidx0, (lv & 1) ? p.gidx0 : p.gidx1,
+      expand_level_any<WR, IMP, BU>(p, sm, F, ls, n, T, (lv & 1) ? p.gidx1 : p.gidx0, (lv & 1) ? p.gidx0 : p.gidx1,
                                 in, outs, kStartLevel + lv, parity, true, claim_store, (lv + 1) % 3);
     }
     const long long tb = clk();
@@ -2154,7 +2177,7 @@ __device__ PhaseOut run_phase(const Params& p, Smem& sm, int cur, int parity, bo
         push_bucketed<WR, IMP, BU>(p, sm, F, ls, n, T, (lv & 1) ? p.gidx1 : p.gidx0, (lv & 1) ? p.gidx0 : p.gidx1,
                                    in, outs, kStartLevel + lv, parity, pairs_out, claim_store, lv & 1);
       else
-        expand_level<WR, IMP, BU>(p, sm, F, ls, n, T, (lv & 1) ? p.gidx1 : p.gidx0, (lv & 1) ? p.gidx0 : p.gidx1,
+        expand_level_any<WR, IMP, BU>(p, sm, F, ls, n, T, (lv & 1) ? p.gidx1 : p.gidx0, (lv & 1) ? p.gidx0 : p.gidx1,
                                   in, outs, kStartLevel + lv, parity, pairs_out, claim_store, (lv + 1) % 3);
     }
     croot_prev = bu && !lazy;  // the next level may resolve its roots through this one's
