@@ -55,6 +55,10 @@ constexpr size_t kFSlack(long long nc) { return (size_t)(nc / 4 + 4096); }
 #ifndef BM_EXPAND_INLINE
 #define BM_EXPAND_INLINE __device__ __forceinline__
 #endif
+#ifndef BM_PB_FN
+#define BM_PB_FN BM_NOINLINE_FN  // push_bucketed: out of line (BM_PB_FN=BM_INLINE_FN to inline it)
+#endif
+#define BM_INLINE_FN __device__ __forceinline__
 #ifndef BM_EXPAND_OOL
 #define BM_EXPAND_OOL 1  // pulled-capable kernels call expand_level out of line (expand_level_ool)
 #endif
@@ -1517,7 +1521,7 @@ __device__ __forceinline__ void expand_level_any(const Params& p, Smem& sm, int4
 // Claims, endpoints and winners are expand_level's; only their order differs,
 // which the reference's races leave open too.
 template <bool WR, bool IMP, bool BU>
-__device__ __noinline__ void push_bucketed(const Params& p, Smem& sm, int4* F, unsigned ls, unsigned n, unsigned T,
+BM_PB_FN void push_bucketed(const Params& p, Smem& sm, int4* F, unsigned ls, unsigned n, unsigned T,
                                             const unsigned* gin, unsigned* gout, Slot* in, Slot* out, int level,
                                             int pf, bool pairs_out, bool claim_store, int par) {
   const unsigned tid = threadIdx.x;
