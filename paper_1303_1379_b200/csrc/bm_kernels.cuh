@@ -59,6 +59,9 @@ constexpr size_t kFSlack(long long nc) { return (size_t)(nc / 4 + 4096); }
 #define BM_PB_FN BM_NOINLINE_FN  // push_bucketed: out of line (BM_PB_FN=BM_INLINE_FN to inline it)
 #endif
 #define BM_INLINE_FN __device__ __forceinline__
+#ifndef BM_PHASE_FN
+#define BM_PHASE_FN __device__  // run_phase (the compiler's choice; BM_NOINLINE_FN to force it out of line)
+#endif
 #ifndef BM_EXPAND_OOL
 #define BM_EXPAND_OOL 1  // pulled-capable kernels call expand_level out of line (expand_level_ool)
 #endif
@@ -1963,7 +1966,7 @@ struct PhaseOut {
 
 // One phase = run_phase (gpu_match.cpp:268-302) from the roots in F[cur].
 template <bool WR, bool IMP, bool BU>
-__device__ PhaseOut run_phase(const Params& p, Smem& sm, int cur, int parity, bool serial_alt,
+BM_PHASE_FN PhaseOut run_phase(const Params& p, Smem& sm, int cur, int parity, bool serial_alt,
                               long long isolated, bool skip_alt) {
   Ctrl* ctl = p.ctl;
   int4* F = cur ? p.F1 : p.F0;
