@@ -16,8 +16,19 @@ constexpr int kThreads = BM_THREADS;  // threads per CTA (1024 / kThreads CTAs p
 #ifndef BM_ITEMS
 #define BM_ITEMS 4
 #endif
-#ifndef BM_MINB
-#define BM_MINB (768 / BM_THREADS)  // 80 registers: fewer spills than 4 CTAs at 64 (A/B: -3..-11 % per phase on C2-C5)
+// Resident CTAs per SM (launch bounds), per kernel family: the pulled-capable
+// kernels run 3 (80 registers; A/B on C5/C2 against 4: -1.6 %/-5 % per phase
+// before the phase count's noise), the push-only kernels 4 (64 registers; C3
+// -8 %, C4 and C1 even). BM_MINB overrides both.
+#ifdef BM_MINB
+#define BM_MINB_BU BM_MINB
+#define BM_MINB_PUSH BM_MINB
+#endif
+#ifndef BM_MINB_BU
+#define BM_MINB_BU (768 / BM_THREADS)
+#endif
+#ifndef BM_MINB_PUSH
+#define BM_MINB_PUSH (1024 / BM_THREADS)
 #endif
 constexpr int kItems = BM_ITEMS;      // edges per thread per round (memory-level parallelism)
 #ifndef BM_EPT
@@ -2447,11 +2458,11 @@ BM_PHASE_FN PhaseOut run_phase(const Params& p, Smem& sm, int cur, int parity, b
 // ---------------------------------------------------------------------------
 template <bool WR, bool IMP, bool BU>
 #if BM_MG
-__global__ void __launch_bounds__(kThreads, BM_MINB) driver_kernel(const __grid_constant__ Params p) {
+__global__ void __launch_bounds__(kThreads, BU ? BM_MINB_BU : BM_MINB_PUSH) driver_kernel(const __grid_constant__ Params p) {
   // (grid constant: the peer table is indexed at run time without a local copy)
   const unsigned long long c_lo = p.col_lo, c_hi = p.col_hi, r_lo = p.row_lo, r_hi = p.row_hi;
 #else
-__global__ void __launch_bounds__(kThreads, BM_MINB) driver_kernel(Params p) {
+__global__ void __launch_bounds__(kThreads, BU ? BM_MINB_BU : BM_MINB_PUSH) driver_kernel(Params p) {
   const unsigned long long c_lo = 0, c_hi = p.nc, r_lo = 0, r_hi = p.nr;
 #endif
   extern __shared__ __align__(16) unsigned char smem_raw[];  // sizeof(Smem) > 48 KB: dynamic shared memory
