@@ -63,6 +63,12 @@ constexpr size_t kFSlack(long long nc) { return (size_t)(nc / 4 + 4096); }
 #ifndef BM_SWEEP_INLINE
 #define BM_SWEEP_INLINE __device__ __forceinline__
 #endif
+#ifndef BM_PREP_INLINE
+#define BM_PREP_INLINE __device__ __forceinline__
+#endif
+#ifndef BM_MAT_INLINE
+#define BM_MAT_INLINE __device__ __forceinline__
+#endif
 #ifndef BM_EXPAND_INLINE
 #define BM_EXPAND_INLINE __device__ __forceinline__
 #endif
@@ -795,7 +801,7 @@ __device__ __forceinline__ void warp_flush_mg(const Params& p, const Smem& sm, c
 // edge total. Every CTA of the caller's set must call it (a grid barrier must
 // follow before the entries are read).
 constexpr int kMatItems = 4;
-__device__ __forceinline__ void materialize(const Params& p, Smem& sm, int4* F, unsigned ls, unsigned n,
+BM_MAT_INLINE void materialize(const Params& p, Smem& sm, int4* F, unsigned ls, unsigned n,
                                             unsigned* gin, Slot* in, unsigned long long pol, bool solo) {
   const unsigned long long G = solo ? 1ull : gridDim.x;
   const unsigned long long B0 = solo ? 0ull : blockIdx.x;
@@ -860,7 +866,7 @@ __device__ __forceinline__ void bu_clear(const Params& p, int b) {
 // run) or as entries (level 0). Counts the live entries as columns expanded.
 // write_root = false (lazy roots, see bu_sweep_q): only the bitmap is built.
 template <bool WR>
-BM_SWEEP_INLINE void bu_prep(const Params& p, Smem& sm, const int4* F, bool pairs, unsigned ls,
+BM_PREP_INLINE void bu_prep(const Params& p, Smem& sm, const int4* F, bool pairs, unsigned ls,
                                         unsigned n, int lv, bool write_root = true) {
   unsigned* fb = p.fbit[lv % kNumFbit];
   unsigned live = 0;
