@@ -76,6 +76,9 @@ constexpr size_t kFSlack(long long nc) { return (size_t)(nc / 4 + 4096); }
 #define BM_PB_FN BM_NOINLINE_FN  // push_bucketed: out of line (BM_PB_FN=BM_INLINE_FN to inline it)
 #endif
 #define BM_INLINE_FN __device__ __forceinline__
+#ifndef BM_TAIL_FN
+#define BM_TAIL_FN __device__ __forceinline__  // phase_tail (BM_NOINLINE_FN: out of line)
+#endif
 #ifndef BM_PHASE_FN
 #define BM_PHASE_FN __device__  // run_phase (the compiler's choice; BM_NOINLINE_FN to force it out of line)
 #endif
@@ -1982,6 +1985,206 @@ struct PhaseOut {
 };
 
 // One phase = run_phase (gpu_match.cpp:268-302) from the roots in F[cur].
+// The end of a phase: ALTERNATE, FIX and the next phase's roots (run_phase's
+// tail; returns the cardinality after the phase). A separate function so that
+// its registers are allocated apart from the level loop's (BM_TAIL_FN).
+template <bool WR, bool IMP, bool BU>
+BM_TAIL_FN long long phase_tail(const Params& p, Smem& sm, int cur, int parity, bool serial_alt, long long isolated,
+                                bool skip_alt, unsigned n0, unsigned long long rp) {
+  Ctrl* ctl = p.ctl;
+  int4* F = cur ? p.F1 : p.F0;
+  int4* Fn = cur ? p.F0 : p.F1;
+  // ---- ALTERNATE (gpu_match.cpp:158-218) ----
+  if (is_leader()) *path_flag_of(p, parity ^ 1) = 0u;  // flag of the next phase
+  const unsigned n_ep = ld_rlx(&ctl->n_ep);
+  unsigned walks = 0, steps = 0, resets = 0;
+  if (skip_alt) {
+    // fault injection: a raced ALTERNATE that augmented nothing, so the driver
+    // must take the serial retry (gpu_match.cpp:328-343)
+  } else if (!serial_alt) {
+    if (!IMP) {
+      for (unsigned long long k = global_thread(); k < n_ep; k += global_threads())
+        alternate_walk(p, walks, steps, ld_cg(p.EP + k));
+    } else {
+      for (unsigned long long k = global_thread(); k < n0; k += global_threads()) {
+        const int c = ld_cg(reinterpret_cast<const int*>(F + k));
+        const int mark = ld_rlx(p.bfs + c);
+        if (mark <= 0) alternate_walk(p, walks, steps, -mark);  // live levels are >= 1 (L0 = 2)
+      }
+    }
+  } else if (is_leader()) {
+    // Serial retry (gpu_match.cpp:328-343): one thread walks every endpoint
+    // in turn; the first walk cannot meet a claimed column, so the phase
+    // always augments when a path exists.
+#if BM_MG
+    if (p.rank == 0)  // rank 0 walks every rank's endpoints (or roots), in rank order
+      for (int q = 0; q < p.world; ++q) {
+        if (!IMP) {
+          const unsigned nq = ld_rlx(&p.peer[q].ctl->n_ep);
+          for (unsigned k = 0; k < nq; ++k) alternate_walk(p, walks, steps, ld_cg(p.peer[q].EP + k));
+        } else {
+          const int4* Fq = cur ? p.peer[q].F1 : p.peer[q].F0;
+          const unsigned nq = (unsigned)(ld_rlx(&p.peer[q].ctl->roots.packed) >> 33);
+          for (unsigned k = 0; k < nq; ++k) {
+            const int c = ld_cg(reinterpret_cast<const int*>(Fq + k));
+            const int mark = ld_rlx(BF(p, c));
+            if (mark <= 0) alternate_walk(p, walks, steps, -mark);
+          }
+        }
+      }
+#else
+    if (!IMP) {
+      for (unsigned k = 0; k < n_ep; ++k) alternate_walk(p, walks, steps, ld_cg(p.EP + k));
+    } else {
+      for (unsigned k = 0; k < n0; ++k) {
+        const int c = ld_cg(reinterpret_cast<const int*>(F + k));
+        const int mark = ld_rlx(p.bfs + c);
+        if (mark <= 0) alternate_walk(p, walks, steps, -mark);
+      }
+    }
+#endif
+  }
+  flush_count(sm, kStWalks, walks);
+  flush_count(sm, kStSteps, steps);
+  grid_sync(p);
+  tl_mark(p, kTlAlt, 0);
+
+  // ---- FIXMATCHING rules 1+2 over the rows ALTERNATE wrote or left behind ----
+#if BM_MG
+  bool dense = false;  // team-wide: a rank whose log overflowed lost rows of other ranks too
+  for (int q = 0; q < p.world; ++q) dense = dense || ld_rlx(&p.peer[q].ctl->log_overflow) != 0u;
+#else
+  const bool dense = ld_rlx(&ctl->log_overflow) != 0u;
+#endif
+  const unsigned n_log = dense ? 0u : min(ld_rlx(&ctl->n_log), p.log_cap);
+  if (!dense) {
+    for (unsigned long long k = global_thread(); k < n_log; k += global_threads())
+      fix_row(p, resets, ld_cg(reinterpret_cast<const int*>(p.wlog + k)));
+    for (unsigned long long k = global_thread(); k < n_ep; k += global_threads())
+      fix_row(p, resets, ld_cg(p.EP + k));
+  } else {  // log overflow: the reference's full pass (over this rank's rows)
+#if BM_MG
+    const unsigned long long r_lo = p.row_lo, r_hi = p.row_hi;
+#else
+    const unsigned long long r_lo = 0, r_hi = p.nr;
+#endif
+    for (unsigned long long r = r_lo + global_thread(); r < r_hi; r += global_threads()) fix_row(p, resets, (int)r);
+  }
+  if (WR)
+    for (unsigned long long k = global_thread(); k < (unsigned long long)p.ndead_words; k += global_threads())
+      st_plain(reinterpret_cast<int*>(p.dead) + k, 0);
+
+  if (is_leader()) {
+    for (int s = 0; s < 3; ++s) {
+      ctl->lvl[s].packed = 0;
+      ctl->lvl[s].tile = 0;
+    }
+    ctl->roots.packed = 0;
+    ctl->roots.tile = 0;
+    ctl->mat[0].packed = 0;
+    ctl->mat[1].packed = 0;
+  }
+  grid_sync(p);
+  tl_mark(p, kTlFixRows, dense ? 1u : 0u);
+
+  // ---- FIXMATCHING rule 3 over the columns ALTERNATE wrote; a non-root column
+  //      it unmatches becomes a root of the next phase ----
+#if BM_MG
+  const unsigned long long c_lo = p.col_lo;  // dense: this rank's columns
+  const unsigned long long ncheck = dense ? (unsigned long long)(p.col_hi - p.col_lo) : n_log;
+#else
+  const unsigned long long c_lo = 0;
+  const unsigned long long ncheck = dense ? (unsigned long long)p.nc : n_log;
+#endif
+  for (unsigned long long b = (unsigned long long)blockIdx.x * kThreads; b < ncheck; b += global_threads()) {
+    const unsigned long long k = b + threadIdx.x;
+    bool push = false;
+    int c = -1;
+    unsigned beg = 0, deg = 0;
+    if (k < ncheck) {
+      c = dense ? (int)(c_lo + k) : ld_cg(reinterpret_cast<const int*>(p.wlog + k) + 1);
+      if (c >= 0 && fix_col(p, resets, c)) {
+        // roots of this phase are handled below; others enter the root set once
+        if (dense) {
+          push = ld_rlx(BF(p, c)) == kUnvisited;
+          if (push) st_rlx(BF(p, c), kStartLevel);
+        } else {
+          push = at_cas(BF(p, c), kUnvisited, kStartLevel) == kUnvisited;
+        }
+#if BM_MG
+        if (push && owner_col(p, c) != p.rank) {
+          // another rank's column: route it to its owner's next roots (it was matched, so it has an edge)
+          const int q = owner_col(p, c);
+          const unsigned sl = (unsigned)(atomicAdd_system(&p.peer[q].ctl->rootp.packed, 1ull << 33) >> 33);
+          st_plain(p.peer[q].P + sl, make_int2(c, c));
+          push = false;
+        }
+#endif
+        if (push) {
+          beg = ld_ro(p.offs + c);
+          deg = ld_ro(p.offs + c + 1) - beg;
+          push = deg > 0;
+        }
+      }
+    }
+    unsigned long long slot;
+    unsigned unused;
+    if (cta_reserve(sm, push ? 1u : 0u, push ? deg : 0u, 0u, &ctl->roots, &ctl->n_ep, slot, unused) && push)
+      put_entry(Fn, 0u, p.gidx0, slot, c, c, beg, deg);
+  }
+  if (is_leader()) {
+    ctl->n_ep = 0u;
+    for (int k = 0; k < 3; ++k) ctl->n_left[k] = 0u;
+    ctl->n_log = 0u;
+    ctl->log_overflow = 0u;
+  }
+  grid_sync(p);
+  tl_mark(p, kTlFixCols, n_log);
+
+  // ---- this phase's roots: still unmatched -> root again; matched -> bfs 1 ----
+  for (unsigned long long b = (unsigned long long)blockIdx.x * kThreads; b < n0; b += global_threads()) {
+    const unsigned long long k = b + threadIdx.x;
+    bool push = false;
+    int c = -1;
+    unsigned beg = 0, deg = 0;
+    if (k < n0) {
+      const int4 ent = ld_cg(F + k);
+      c = ent.x;
+      if (ld_rlx(p.cmatch + c) < 0) {
+        push = true;
+        beg = (unsigned)ent.z;
+        const unsigned nxt = (k + 1 < n0) ? ld_cg_u(F + k + 1) : (unsigned)(rp & kEdgeMask);
+        deg = nxt - (unsigned)ent.w;
+        st_plain(p.bfs + c, kStartLevel);
+      } else {
+        st_plain(p.bfs + c, kUnvisited);
+      }
+    }
+    unsigned long long slot;
+    unsigned unused;
+    if (cta_reserve(sm, push ? 1u : 0u, push ? deg : 0u, 0u, &ctl->roots, &ctl->n_ep, slot, unused) && push)
+      put_entry(Fn, 0u, p.gidx0, slot, c, c, beg, deg);
+  }
+  flush_count(sm, kStResets, resets);
+  grid_sync(p);
+#if BM_MG
+  if (routed(p)) {  // the roots other ranks routed here join this rank's roots
+    const unsigned n_rp = (unsigned)(ld_rlx(&ctl->rootp.packed) >> 33);
+    if (n_rp) materialize(p, sm, Fn, 0u, n_rp, p.gidx0, &ctl->roots, policy_evict_first(), false);
+    grid_sync(p);  // (every rank: the barrier is team-wide)
+    if (is_leader()) ctl->rootp.packed = 0;
+  }
+  long long roots_tot = 0;
+  for (int q = 0; q < p.world; ++q) roots_tot += (long long)(ld_rlx(&p.peer[q].ctl->roots.packed) >> 33);
+  tl_mark(p, kTlRoots, (unsigned)roots_tot);
+  return (long long)p.nc - isolated - roots_tot;
+#else
+  const unsigned long long np = ld_rlx(&ctl->roots.packed);
+  tl_mark(p, kTlRoots, (unsigned)(np >> 33));
+  return (long long)p.nc - isolated - (long long)(np >> 33);
+#endif
+}
+
 template <bool WR, bool IMP, bool BU>
 BM_PHASE_FN PhaseOut run_phase(const Params& p, Smem& sm, int cur, int parity, bool serial_alt,
                               long long isolated, bool skip_alt) {
@@ -2269,195 +2472,7 @@ BM_PHASE_FN PhaseOut run_phase(const Params& p, Smem& sm, int cur, int parity, b
   grid_sync(p);
   if (p.stop_after_bfs) return out;
 
-  // ---- ALTERNATE (gpu_match.cpp:158-218) ----
-  if (is_leader()) *path_flag_of(p, parity ^ 1) = 0u;  // flag of the next phase
-  const unsigned n_ep = ld_rlx(&ctl->n_ep);
-  unsigned walks = 0, steps = 0, resets = 0;
-  if (skip_alt) {
-    // fault injection: a raced ALTERNATE that augmented nothing, so the driver
-    // must take the serial retry (gpu_match.cpp:328-343)
-  } else if (!serial_alt) {
-    if (!IMP) {
-      for (unsigned long long k = global_thread(); k < n_ep; k += global_threads())
-        alternate_walk(p, walks, steps, ld_cg(p.EP + k));
-    } else {
-      for (unsigned long long k = global_thread(); k < n0; k += global_threads()) {
-        const int c = ld_cg(reinterpret_cast<const int*>(F + k));
-        const int mark = ld_rlx(p.bfs + c);
-        if (mark <= 0) alternate_walk(p, walks, steps, -mark);  // live levels are >= 1 (L0 = 2)
-      }
-    }
-  } else if (is_leader()) {
-    // Serial retry (gpu_match.cpp:328-343): one thread walks every endpoint
-    // in turn; the first walk cannot meet a claimed column, so the phase
-    // always augments when a path exists.
-#if BM_MG
-    if (p.rank == 0)  // rank 0 walks every rank's endpoints (or roots), in rank order
-      for (int q = 0; q < p.world; ++q) {
-        if (!IMP) {
-          const unsigned nq = ld_rlx(&p.peer[q].ctl->n_ep);
-          for (unsigned k = 0; k < nq; ++k) alternate_walk(p, walks, steps, ld_cg(p.peer[q].EP + k));
-        } else {
-          const int4* Fq = cur ? p.peer[q].F1 : p.peer[q].F0;
-          const unsigned nq = (unsigned)(ld_rlx(&p.peer[q].ctl->roots.packed) >> 33);
-          for (unsigned k = 0; k < nq; ++k) {
-            const int c = ld_cg(reinterpret_cast<const int*>(Fq + k));
-            const int mark = ld_rlx(BF(p, c));
-            if (mark <= 0) alternate_walk(p, walks, steps, -mark);
-          }
-        }
-      }
-#else
-    if (!IMP) {
-      for (unsigned k = 0; k < n_ep; ++k) alternate_walk(p, walks, steps, ld_cg(p.EP + k));
-    } else {
-      for (unsigned k = 0; k < n0; ++k) {
-        const int c = ld_cg(reinterpret_cast<const int*>(F + k));
-        const int mark = ld_rlx(p.bfs + c);
-        if (mark <= 0) alternate_walk(p, walks, steps, -mark);
-      }
-    }
-#endif
-  }
-  flush_count(sm, kStWalks, walks);
-  flush_count(sm, kStSteps, steps);
-  grid_sync(p);
-  tl_mark(p, kTlAlt, 0);
-
-  // ---- FIXMATCHING rules 1+2 over the rows ALTERNATE wrote or left behind ----
-#if BM_MG
-  bool dense = false;  // team-wide: a rank whose log overflowed lost rows of other ranks too
-  for (int q = 0; q < p.world; ++q) dense = dense || ld_rlx(&p.peer[q].ctl->log_overflow) != 0u;
-#else
-  const bool dense = ld_rlx(&ctl->log_overflow) != 0u;
-#endif
-  const unsigned n_log = dense ? 0u : min(ld_rlx(&ctl->n_log), p.log_cap);
-  if (!dense) {
-    for (unsigned long long k = global_thread(); k < n_log; k += global_threads())
-      fix_row(p, resets, ld_cg(reinterpret_cast<const int*>(p.wlog + k)));
-    for (unsigned long long k = global_thread(); k < n_ep; k += global_threads())
-      fix_row(p, resets, ld_cg(p.EP + k));
-  } else {  // log overflow: the reference's full pass (over this rank's rows)
-#if BM_MG
-    const unsigned long long r_lo = p.row_lo, r_hi = p.row_hi;
-#else
-    const unsigned long long r_lo = 0, r_hi = p.nr;
-#endif
-    for (unsigned long long r = r_lo + global_thread(); r < r_hi; r += global_threads()) fix_row(p, resets, (int)r);
-  }
-  if (WR)
-    for (unsigned long long k = global_thread(); k < (unsigned long long)p.ndead_words; k += global_threads())
-      st_plain(reinterpret_cast<int*>(p.dead) + k, 0);
-
-  if (is_leader()) {
-    for (int s = 0; s < 3; ++s) {
-      ctl->lvl[s].packed = 0;
-      ctl->lvl[s].tile = 0;
-    }
-    ctl->roots.packed = 0;
-    ctl->roots.tile = 0;
-    ctl->mat[0].packed = 0;
-    ctl->mat[1].packed = 0;
-  }
-  grid_sync(p);
-  tl_mark(p, kTlFixRows, dense ? 1u : 0u);
-
-  // ---- FIXMATCHING rule 3 over the columns ALTERNATE wrote; a non-root column
-  //      it unmatches becomes a root of the next phase ----
-#if BM_MG
-  const unsigned long long c_lo = p.col_lo;  // dense: this rank's columns
-  const unsigned long long ncheck = dense ? (unsigned long long)(p.col_hi - p.col_lo) : n_log;
-#else
-  const unsigned long long c_lo = 0;
-  const unsigned long long ncheck = dense ? (unsigned long long)p.nc : n_log;
-#endif
-  for (unsigned long long b = (unsigned long long)blockIdx.x * kThreads; b < ncheck; b += global_threads()) {
-    const unsigned long long k = b + threadIdx.x;
-    bool push = false;
-    int c = -1;
-    unsigned beg = 0, deg = 0;
-    if (k < ncheck) {
-      c = dense ? (int)(c_lo + k) : ld_cg(reinterpret_cast<const int*>(p.wlog + k) + 1);
-      if (c >= 0 && fix_col(p, resets, c)) {
-        // roots of this phase are handled below; others enter the root set once
-        if (dense) {
-          push = ld_rlx(BF(p, c)) == kUnvisited;
-          if (push) st_rlx(BF(p, c), kStartLevel);
-        } else {
-          push = at_cas(BF(p, c), kUnvisited, kStartLevel) == kUnvisited;
-        }
-#if BM_MG
-        if (push && owner_col(p, c) != p.rank) {
-          // another rank's column: route it to its owner's next roots (it was matched, so it has an edge)
-          const int q = owner_col(p, c);
-          const unsigned sl = (unsigned)(atomicAdd_system(&p.peer[q].ctl->rootp.packed, 1ull << 33) >> 33);
-          st_plain(p.peer[q].P + sl, make_int2(c, c));
-          push = false;
-        }
-#endif
-        if (push) {
-          beg = ld_ro(p.offs + c);
-          deg = ld_ro(p.offs + c + 1) - beg;
-          push = deg > 0;
-        }
-      }
-    }
-    unsigned long long slot;
-    unsigned unused;
-    if (cta_reserve(sm, push ? 1u : 0u, push ? deg : 0u, 0u, &ctl->roots, &ctl->n_ep, slot, unused) && push)
-      put_entry(Fn, 0u, p.gidx0, slot, c, c, beg, deg);
-  }
-  if (is_leader()) {
-    ctl->n_ep = 0u;
-    for (int k = 0; k < 3; ++k) ctl->n_left[k] = 0u;
-    ctl->n_log = 0u;
-    ctl->log_overflow = 0u;
-  }
-  grid_sync(p);
-  tl_mark(p, kTlFixCols, n_log);
-
-  // ---- this phase's roots: still unmatched -> root again; matched -> bfs 1 ----
-  for (unsigned long long b = (unsigned long long)blockIdx.x * kThreads; b < n0; b += global_threads()) {
-    const unsigned long long k = b + threadIdx.x;
-    bool push = false;
-    int c = -1;
-    unsigned beg = 0, deg = 0;
-    if (k < n0) {
-      const int4 ent = ld_cg(F + k);
-      c = ent.x;
-      if (ld_rlx(p.cmatch + c) < 0) {
-        push = true;
-        beg = (unsigned)ent.z;
-        const unsigned nxt = (k + 1 < n0) ? ld_cg_u(F + k + 1) : (unsigned)(rp & kEdgeMask);
-        deg = nxt - (unsigned)ent.w;
-        st_plain(p.bfs + c, kStartLevel);
-      } else {
-        st_plain(p.bfs + c, kUnvisited);
-      }
-    }
-    unsigned long long slot;
-    unsigned unused;
-    if (cta_reserve(sm, push ? 1u : 0u, push ? deg : 0u, 0u, &ctl->roots, &ctl->n_ep, slot, unused) && push)
-      put_entry(Fn, 0u, p.gidx0, slot, c, c, beg, deg);
-  }
-  flush_count(sm, kStResets, resets);
-  grid_sync(p);
-#if BM_MG
-  if (routed(p)) {  // the roots other ranks routed here join this rank's roots
-    const unsigned n_rp = (unsigned)(ld_rlx(&ctl->rootp.packed) >> 33);
-    if (n_rp) materialize(p, sm, Fn, 0u, n_rp, p.gidx0, &ctl->roots, policy_evict_first(), false);
-    grid_sync(p);  // (every rank: the barrier is team-wide)
-    if (is_leader()) ctl->rootp.packed = 0;
-  }
-  long long roots_tot = 0;
-  for (int q = 0; q < p.world; ++q) roots_tot += (long long)(ld_rlx(&p.peer[q].ctl->roots.packed) >> 33);
-  tl_mark(p, kTlRoots, (unsigned)roots_tot);
-  out.after = (long long)p.nc - isolated - roots_tot;
-#else
-  const unsigned long long np = ld_rlx(&ctl->roots.packed);
-  tl_mark(p, kTlRoots, (unsigned)(np >> 33));
-  out.after = (long long)p.nc - isolated - (long long)(np >> 33);
-#endif
+  out.after = phase_tail<WR, IMP, BU>(p, sm, cur, parity, serial_alt, isolated, skip_alt, n0, rp);
   return out;
 }
 
