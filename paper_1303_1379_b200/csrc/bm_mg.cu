@@ -21,6 +21,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <string>
 #include <vector>
 
@@ -76,6 +77,21 @@ template <typename T>
 cudaError_t dnew(T*& p, size_t count) {
   dfree(p);
   return cudaMalloc(reinterpret_cast<void**>(&p), std::max<size_t>(count, 1) * sizeof(T));
+}
+// Grows a buffer only when it is too small, so that re-uploading a graph of the
+// same size reuses the allocations (a free + malloc of GB-sized buffers per
+// upload cost more than the copy).
+using CapMap = std::map<const void*, size_t>;
+template <typename T>
+cudaError_t dgrow(CapMap& caps, T*& p, size_t count) {
+  count = std::max<size_t>(count, 1);
+  size_t& cap = caps[&p];
+  if (p && cap >= count) return cudaSuccess;
+  dfree(p);
+  cap = 0;
+  const cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&p), count * sizeof(T));
+  if (e == cudaSuccess) cap = count;
+  return e;
 }
 
 // The buffers a rank shares, in blob order.
@@ -139,6 +155,9 @@ struct bm_mg {
   // peers
   bmg::PeerPtrs peer[kMaxRanks];
   void* opened[kMaxRanks][kNumShared] = {};
+  CapMap caps;                            // capacities of the dgrow buffers
+  long long* stage64 = nullptr;           // the slice's int64 offsets, before narrowing on the device
+  unsigned long long* scratch = nullptr;  // upload check counters
   int2* peer_outbox[kMaxRanks] = {};
   unsigned* peer_out_idx[kMaxRanks] = {};
   MgTeam* team_ptr = nullptr;
@@ -242,6 +261,8 @@ bm_status bm_mg_destroy(bm_mg* h) {
   if (h->stream) cudaStreamSynchronize(h->stream);
   close_peers(h);
   dfree(h->offs);
+  dfree(h->stage64);
+  dfree(h->scratch);
   dfree(h->adj);
   dfree(h->rm);
   dfree(h->pred_plain);
@@ -309,51 +330,54 @@ bm_status bm_mg_upload(bm_mg* h, int32_t nc, int32_t nr, int64_t e_total, const 
   const int ncl = h->chi - h->clo, nrl = h->rhi - h->rlo;
   const long long E = cxadj[ncl];
   if (cxadj[0] != 0 || E < 0 || E >= (1ll << 32) - 1) return fail(BM_ERR_INVALID_ARG, "bad slice offsets");
-  for (int c = 0; c < ncl; ++c)
-    if (cxadj[c + 1] < cxadj[c]) return fail(BM_ERR_INVALID_ARG, "cxadj slice must be non-decreasing");
   h->E = E;
   h->E_total = e_total;
-  long long nonempty = 0;
-  bool sorted = true;
-  for (int c = 0; c < ncl; ++c) {
-    if (cxadj[c + 1] > cxadj[c]) nonempty++;
-    for (long long j = cxadj[c]; j < cxadj[c + 1]; ++j) {
-      if (cadj[j] < 0 || cadj[j] >= nr) return fail(BM_ERR_INVALID_ARG, "row index out of range in cadj");
-      if (j > cxadj[c] && cadj[j - 1] >= cadj[j]) sorted = false;
-    }
-  }
-  h->sorted = sorted ? 1 : 0;
-  h->nonempty = nonempty;
+  // The slice is checked on the device while it lands (check_csr, csr_graph.cpp:45-64):
+  // offsets non-decreasing and narrowed to u32, rows in range, per-column order.
+  BM_CUDA(dgrow(h->caps, h->stage64, (size_t)ncl + 1));
+  BM_CUDA(dgrow(h->caps, h->scratch, 8));
+  BM_CUDA(dgrow(h->caps, h->offs, (size_t)ncl + 1));
+  BM_CUDA(dgrow(h->caps, h->adj, (size_t)E));
+  BM_CUDA(cudaMemsetAsync(h->scratch, 0, sizeof(unsigned long long) * 8, h->stream));
+  BM_CUDA(cudaMemcpyAsync(h->stage64, cxadj, sizeof(long long) * ((size_t)ncl + 1), cudaMemcpyHostToDevice, h->stream));
+  const int cblocks = std::max(1, std::min(h->sms * 8, (ncl + 256) / 256));
+  bmg::convert_offsets_kernel<<<cblocks, 256, 0, h->stream>>>(h->stage64, h->offs, ncl, E, h->scratch, h->scratch + 4);
+  if (E) BM_CUDA(cudaMemcpyAsync(h->adj, cadj, sizeof(int) * (size_t)E, cudaMemcpyHostToDevice, h->stream));
+  const int ablocks = (int)std::max<long long>(1, std::min<long long>((long long)h->sms * 8, (E + 255) / 256));
+  if (E) bmg::check_adj_flat_kernel<<<ablocks, 256, 0, h->stream>>>(h->adj, 0, E, nr, h->scratch + 1, h->scratch + 2);
+  if (ncl) bmg::col_start_pairs_kernel<<<cblocks, 256, 0, h->stream>>>(h->offs, h->adj, ncl, h->scratch + 3);
+  BM_CUDA(cudaGetLastError());
+  unsigned long long chk[5] = {0, 0, 0, 0, 0};
+  BM_CUDA(cudaMemcpyAsync(chk, h->scratch, sizeof(chk), cudaMemcpyDeviceToHost, h->stream));
+  BM_CUDA(cudaStreamSynchronize(h->stream));
+  if (chk[0]) return fail(BM_ERR_INVALID_ARG, "cxadj slice must be non-decreasing");
+  if (chk[1]) return fail(BM_ERR_INVALID_ARG, "row index out of range in cadj");
+  h->sorted = (chk[2] - chk[3]) == 0 ? 1 : 0;
+  h->nonempty = (long long)ncl - (long long)chk[4];
   h->rs = ((size_t)nr * sizeof(int) > ((size_t)72 << 20)) ? 2 : 1;
   if (const char* lay = getenv("BM_ROW_LAYOUT")) h->rs = strcmp(lay, "plain") ? 2 : 1;
   // frontier capacity: the same on every rank (the store-claim rule compares against it)
   int maxc = 0;
   for (int q = 0; q < h->world; ++q) maxc = std::max(maxc, cb[q + 1] - cb[q]);
   h->fcap = (long long)maxc + (long long)bmg::kFSlack(maxc);
-  std::vector<unsigned> offs32(ncl + 1);
-  for (int c = 0; c <= ncl; ++c) offs32[c] = (unsigned)cxadj[c];
-  BM_CUDA(dnew(h->offs, ncl + 1));
-  BM_CUDA(dnew(h->adj, E));
-  BM_CUDA(cudaMemcpy(h->offs, offs32.data(), sizeof(unsigned) * (ncl + 1), cudaMemcpyHostToDevice));
-  if (E) BM_CUDA(cudaMemcpy(h->adj, cadj, sizeof(int) * E, cudaMemcpyHostToDevice));
-  BM_CUDA(dnew(h->rm, (size_t)2 * std::max(nrl, 1)));
-  BM_CUDA(dnew(h->pred_plain, nrl));
-  BM_CUDA(dnew(h->rtmp, nrl));
-  BM_CUDA(dnew(h->cmatch, ncl));
-  BM_CUDA(dnew(h->bfs, ncl));
-  BM_CUDA(dnew(h->croot, ncl));
+  BM_CUDA(dgrow(h->caps, h->rm, (size_t)2 * std::max(nrl, 1)));
+  BM_CUDA(dgrow(h->caps, h->pred_plain, nrl));
+  BM_CUDA(dgrow(h->caps, h->rtmp, nrl));
+  BM_CUDA(dgrow(h->caps, h->cmatch, ncl));
+  BM_CUDA(dgrow(h->caps, h->bfs, ncl));
+  BM_CUDA(dgrow(h->caps, h->croot, ncl));
   h->ndead_words = h->nfbit_words = (nc + 31) / 32;
-  BM_CUDA(dnew(h->dead, h->ndead_words));
-  BM_CUDA(dnew(h->fbit, (size_t)kNumFbit * h->nfbit_words));
-  BM_CUDA(dnew(h->P, h->fcap));
-  BM_CUDA(dnew(h->F[0], h->fcap));
-  BM_CUDA(dnew(h->F[1], h->fcap));
-  BM_CUDA(dnew(h->EP, std::max(nr, 1)));
+  BM_CUDA(dgrow(h->caps, h->dead, h->ndead_words));
+  BM_CUDA(dgrow(h->caps, h->fbit, (size_t)kNumFbit * h->nfbit_words));
+  BM_CUDA(dgrow(h->caps, h->P, h->fcap));
+  BM_CUDA(dgrow(h->caps, h->F[0], h->fcap));
+  BM_CUDA(dgrow(h->caps, h->F[1], h->fcap));
+  BM_CUDA(dgrow(h->caps, h->EP, std::max(nr, 1)));
   const size_t ngran = (size_t)(E / bmg::kGran) + 2;
-  BM_CUDA(dnew(h->gidx[0], ngran));
-  BM_CUDA(dnew(h->gidx[1], ngran));
+  BM_CUDA(dgrow(h->caps, h->gidx[0], ngran));
+  BM_CUDA(dgrow(h->caps, h->gidx[1], ngran));
   h->log_cap = (unsigned)std::min<long long>((long long)nr + nc + 1024, 0xffffffffll);
-  BM_CUDA(dnew(h->wlog, h->log_cap));
+  BM_CUDA(dgrow(h->caps, h->wlog, h->log_cap));
   BM_CUDA(cudaMemset(h->pred_plain, 0xff, sizeof(int) * std::max(nrl, 1)));
   BM_CUDA(cudaMemset(h->rm, 0xff, sizeof(int) * 2 * std::max(nrl, 1)));  // mates -1, interleaved preds -1
   BM_CUDA(cudaMemset(h->fbit, 0, sizeof(unsigned) * kNumFbit * h->nfbit_words));
@@ -366,8 +390,8 @@ bm_status bm_mg_upload(bm_mg* h, int32_t nc, int32_t nr, int64_t e_total, const 
     h->nb = (int)(((long long)nr + (1ll << shift) - 1) >> shift);
     if (h->nb > bmg::kMaxBuckets) return fail(BM_ERR_INVALID_ARG, "row index: too many buckets");
   }
-  BM_CUDA(dnew(h->outbox, E));
-  BM_CUDA(dnew(h->out_idx, 2 * bmg::kMaxBuckets + 4));
+  BM_CUDA(dgrow(h->caps, h->outbox, E));
+  BM_CUDA(dgrow(h->caps, h->out_idx, 2 * bmg::kMaxBuckets + 4));
   h->deg_col = (double)e_total / (double)std::max(1ll, (long long)nc);  // refined below by the team
   h->deg_row = (double)e_total / (double)std::max(1, nr);
   h->row_index = false;
@@ -519,7 +543,7 @@ bm_status bm_mg_row_index_end(bm_mg* h) {
     seg_n[q] = n;
     total += n;
   }
-  BM_CUDA(dnew(h->inbox, total));
+  BM_CUDA(dgrow(h->caps, h->inbox, total));
   long long at = 0;
   for (int q = 0; q < h->world; ++q) {
     if (seg_n[q]) BM_CUDA(cudaMemcpyAsync(h->inbox + at, h->peer_outbox[q] + seg_lo[q], sizeof(int2) * seg_n[q],
@@ -528,8 +552,8 @@ bm_status bm_mg_row_index_end(bm_mg* h) {
   }
   h->inbox_n = total;
   long long mine = 0;  // edges of this rank's rows (straddling buckets also carry other ranks' rows)
-  BM_CUDA(dnew(h->roffs, (size_t)nrl + 1));
-  BM_CUDA(dnew(h->rcursor, (size_t)nrl + 1));
+  BM_CUDA(dgrow(h->caps, h->roffs, (size_t)nrl + 1));
+  BM_CUDA(dgrow(h->caps, h->rcursor, (size_t)nrl + 1));
   BM_CUDA(cudaMemsetAsync(h->rcursor, 0, sizeof(unsigned) * ((size_t)nrl + 1), h->stream));
   unsigned* tickets = h->out_idx + 2 * bmg::kMaxBuckets;
   BM_CUDA(cudaMemsetAsync(tickets, 0, sizeof(unsigned) * 2, h->stream));
@@ -539,7 +563,7 @@ bm_status bm_mg_row_index_end(bm_mg* h) {
   size_t tb = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, tb, h->rcursor, h->roffs, nrl + 1, h->stream);
   if (tb > h->scan_bytes) {
-    BM_CUDA(dnew(h->scan_tmp, tb));
+    BM_CUDA(dgrow(h->caps, h->scan_tmp, tb));
     h->scan_bytes = tb;
   }
   cub::DeviceScan::ExclusiveSum(h->scan_tmp, tb, h->rcursor, h->roffs, nrl + 1, h->stream);
@@ -547,7 +571,7 @@ bm_status bm_mg_row_index_end(bm_mg* h) {
   BM_CUDA(cudaMemcpyAsync(&last, h->roffs + nrl, sizeof(unsigned), cudaMemcpyDeviceToHost, h->stream));
   BM_CUDA(cudaStreamSynchronize(h->stream));
   mine = last;
-  BM_CUDA(dnew(h->radj, mine + 4));  // (+4: the pulled probes read aligned groups of 4)
+  BM_CUDA(dgrow(h->caps, h->radj, mine + 4));  // (+4: the pulled probes read aligned groups of 4)
   BM_CUDA(cudaMemcpyAsync(h->rcursor, h->roffs, sizeof(unsigned) * ((size_t)nrl + 1), cudaMemcpyDeviceToDevice,
                           h->stream));
   if (total) bmg::pair_pass_kernel<true><<<grid, 256, 0, h->stream>>>(h->inbox, (unsigned)total, tickets + 1,

@@ -110,3 +110,29 @@ def test_multigpu_pulled_levels_every_level(oracle, monkeypatch):
             res, m = team.match(init, shortest=shortest, kernel=kernel, improved=improved, bottom_up="on")
             _check_one(g, res.cardinality, m.rmatch, m.cmatch, oracle)
     team.close()
+
+
+@pytest.mark.gpu
+def test_multigpu_upload_checks_and_reuse(oracle):
+    """The slice is checked on the device (check_csr, csr_graph.cpp:45-64): a row
+    out of range or decreasing offsets fail the upload with invalid_argument;
+    re-uploading graphs of other sizes into the same team (buffers grown, not
+    reallocated, when they fit) keeps every maximum."""
+    import numpy as np
+    import paper_1303_1379_b200 as bm
+    from paper_1303_1379_b200.partition import LocalTeam
+    team = LocalTeam(2)
+    g = bm.generate_random_bipartite(20000, 15000, 5.0, 77)
+    bad = g.cadj.copy()
+    bad[len(bad) // 3] = g.nr
+    with pytest.raises(ValueError):
+        team.upload(bm.BipartiteCsr(g.nc, g.nr, g.cxadj.copy(), bad))
+    cx = g.cxadj.copy()
+    cx[g.nc // 4] = cx[g.nc // 4 + 1] + 2
+    with pytest.raises(ValueError):
+        team.upload(bm.BipartiteCsr(g.nc, g.nr, cx, g.cadj.copy()))
+    for h in [g, bm.generate_random_bipartite(5000, 6000, 3.0, 5), bm.generate_rmat(14, 8.0, 9), g]:
+        team.upload(h, row_index=True)
+        res, m = team.match(bm.cheap_matching(h), bottom_up="auto")
+        _check_one(h, res.cardinality, m.rmatch, m.cmatch, oracle)
+    team.close()
