@@ -419,15 +419,22 @@ def run_partitioned(args):
     e2e = None
     if not args.no_e2e:
         lo, hi = pm.cb[rank], pm.cb[rank + 1]
-        cx = torch.from_numpy(np.ascontiguousarray(g.cxadj[lo:hi + 1] - g.cxadj[lo])).pin_memory()
-        adj = torch.from_numpy(np.ascontiguousarray(g.cadj[int(g.cxadj[lo]):int(g.cxadj[hi])])).pin_memory()
+        rlo, rhi = pm.rb[rank], pm.rb[rank + 1]
+        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
+        cx = pin(g.cxadj[lo:hi + 1] - g.cxadj[lo])
+        adj = pin(g.cadj[int(g.cxadj[lo]):int(g.cxadj[hi])])
+        # pinned host buffers for this rank's initial-matching slices and results, as the
+        # single-GPU e2e uses
+        r_sl, c_sl = pin(init.rmatch[rlo:rhi]), pin(init.cmatch[lo:hi])
+        out_r, out_c = pin(np.empty(rhi - rlo, np.int32)), pin(np.empty(hi - lo, np.int32))
         e_ms = []
         for i in range(args.warmup + args.steps):
             x.barrier()
             t0 = time.perf_counter()
             pm.upload(g, row_index=pulled, slices=(cx.numpy(), adj.numpy()))
-            pm.match(init, shortest=shortest, kernel=kernel, improved=improved, bottom_up=bu)
-            rs, cs = rk.download()
+            pm.match(init, shortest=shortest, kernel=kernel, improved=improved, bottom_up=bu,
+                     slices=(r_sl.numpy(), c_sl.numpy()))
+            rs, cs = rk.download(out=(out_r.numpy(), out_c.numpy()))
             t1 = time.perf_counter()
             if i >= args.warmup:
                 e_ms.append(1e3 * (t1 - t0))

@@ -141,9 +141,14 @@ class GpuRank:
     def row_index_end(self):
         check(lib.bm_mg_row_index_end(self._h))
 
-    def load(self, m: MatchingState):
-        r = np.ascontiguousarray(m.rmatch[self.rb[self.rank]:self.rb[self.rank + 1]], np.int32)
-        c = np.ascontiguousarray(m.cmatch[self.cb[self.rank]:self.cb[self.rank + 1]], np.int32)
+    def load(self, m: MatchingState, slices=None):
+        """The initial matching of this rank's rows and columns (taken from the whole
+        arrays of m, or given directly as `slices` = (rows, cols), e.g. pinned)."""
+        if slices is not None:
+            r, c = slices
+        else:
+            r = np.ascontiguousarray(m.rmatch[self.rb[self.rank]:self.rb[self.rank + 1]], np.int32)
+            c = np.ascontiguousarray(m.cmatch[self.cb[self.rank]:self.cb[self.rank + 1]], np.int32)
         check(lib.bm_mg_load_matching(self._h, _ptr(r, C.c_int32), _ptr(c, C.c_int32)))
 
     def launch(self, opts: bm_match_opts):
@@ -155,9 +160,12 @@ class GpuRank:
         check(lib.bm_mg_finish(self._h, C.byref(card), C.byref(ct)))
         return card.value, ct
 
-    def download(self):
-        r = np.empty(self.rb[self.rank + 1] - self.rb[self.rank], np.int32)
-        c = np.empty(self.cb[self.rank + 1] - self.cb[self.rank], np.int32)
+    def download(self, out=None):
+        """This rank's rows and columns; `out` = (rows, cols) caller arrays (e.g. pinned)."""
+        if out is None:
+            out = (np.empty(self.rb[self.rank + 1] - self.rb[self.rank], np.int32),
+                   np.empty(self.cb[self.rank + 1] - self.cb[self.rank], np.int32))
+        r, c = out
         check(lib.bm_mg_download(self._h, _ptr(r, C.c_int32), _ptr(c, C.c_int32)))
         return r, c
 
@@ -312,9 +320,12 @@ class PartitionedMatcher:
         self.g, self.cb, self.rb = g, cb, rb
 
     def match(self, init: MatchingState, *, shortest=False, kernel=BfsKernel.GpubfsWr, improved=False,
-              bottom_up="auto", init_mode="given") -> TeamResult:
+              bottom_up="auto", init_mode="given", slices=None) -> TeamResult:
         opts = _opts_for(shortest, kernel, improved, bottom_up, init_mode)
-        self.b.load(init)
+        if slices is None:
+            self.b.load(init)
+        else:
+            self.b.load(init, slices=slices)
         self.x.barrier()  # no kernel touches a peer's state before that peer loaded it
         self.b.launch(opts)
         card, ct = self.b.finish()
