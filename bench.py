@@ -522,7 +522,9 @@ def run_b200(args):
 
     eng = bm.Engine(local)
     eng.set_stream(stream.cuda_stream)
+    t_upload = time.perf_counter()
     eng.upload(g)
+    t_upload = 1e3 * (time.perf_counter() - t_upload)
     eng.load_matching(init)
     flush = torch.empty(args.flush_mb << 20, dtype=torch.uint8, device=dev)
 
@@ -752,7 +754,11 @@ def run_b200(args):
             "cpu_baseline": cpu,
             "e2e": e2e,
             "bottom_up": {"mode": args.bottom_up, "pulled_dense_levels": bool(pulled),
-                          "row_index_ms": row_index_ms[-1] if row_index_ms else None},
+                          "row_index_ms": row_index_ms[-1] if row_index_ms else None,
+                          # at >= 2^26 rows the upload builds the row index beside the copy, so
+                          # bm_prepare_row_index finds it ready: its cost is inside upload_ms (and e2e)
+                          "row_index_with_upload": bool(auto_level == 2),
+                          "upload_ms": t_upload},
             "alternative": alt,
             "gpu_launches": launches,
             "clocks": sampler.summary(),
