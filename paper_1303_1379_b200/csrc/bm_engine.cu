@@ -180,6 +180,8 @@ struct bm_handle {
   unsigned long long pb_max = 0;
   int pb_shift = 0, pb_nb = 0;
   unsigned pb_cap = 0;
+  int pp_shift = 0, pp_nb = 0;  // bucketed bu_prep (column buckets in tb)
+  unsigned pp_cap = 0;
   unsigned* roffs = nullptr;
   int* radj = nullptr;
   unsigned* rcursor = nullptr;
@@ -701,6 +703,22 @@ bm_status ensure_pb(bm_handle* h) {
   h->pb_shift = shift;
   h->pb_nb = nb;
   h->pb_cap = cap;
+  // column buckets of the bucketed bu_prep: <= 16-24 MB of croot each, pairs (int2) in the same buffer
+  h->pp_nb = 0;
+  const char* pe = getenv("BM_PP");
+  if (!(pe && atoi(pe) == 0)) {
+    const unsigned long long fcap = (unsigned long long)h->nc + kFSlack(h->nc);
+    int cshift = 0;
+    while ((2ull << cshift) <= (24ull << 20) / 4) ++cshift;
+    while ((((unsigned long long)h->nc - 1) >> cshift) + 1 > (unsigned long long)kPbMax) ++cshift;
+    const int cnb = (int)((((unsigned long long)std::max(h->nc, 1) - 1) >> cshift) + 1);
+    const unsigned long long ccap = (fcap * 5 / 4) / cnb + slack;
+    if ((unsigned long long)cnb * ccap + fcap <= 2ull * need && ccap < 0xffff0000ull) {
+      h->pp_nb = cnb;
+      h->pp_shift = cshift;
+      h->pp_cap = (unsigned)ccap;
+    }
+  }
   return BM_OK;
 }
 
@@ -787,6 +805,11 @@ Params make_params(bm_handle* h, const bm_match_opts& o) {
   p.pb_shift = h->pb_shift;
   p.pb_nb = h->pb_nb;
   p.pb_cap = h->pb_cap;
+  p.pp_nb = h->pb_max ? h->pp_nb : 0;
+  p.pp_shift = h->pp_shift;
+  p.pp_cap = h->pp_cap;
+  p.pp_min = 1ull << 22;
+  if (const char* pm = getenv("BM_PP_MIN")) p.pp_min = (unsigned long long)atoll(pm);
   if (h->dbg_phase_bound > 0) p.phase_bound = h->dbg_phase_bound;
   p.sorted = h->sorted;
   p.check = getenv("BM_CHECK") ? atoi(getenv("BM_CHECK")) : 0;

@@ -314,6 +314,13 @@ struct Params {
   int pb_shift;             // bucket of row r = r >> pb_shift
   int pb_nb;                // buckets (<= kPbMax)
   unsigned pb_cap;          // triples per bucket region
+  // Bucketed bu_prep (bu_prep_bucketed): the frontier's (col, root) pairs grouped by
+  // column range in the same buffer (as int2), so the root stores and bitmap
+  // atomics of a bucket stay inside an L2-sized window. 0 buckets: off.
+  int pp_shift;             // bucket of column c = c >> pp_shift
+  int pp_nb;
+  unsigned pp_cap;          // pairs per bucket region (int2 units of tb)
+  unsigned long long pp_min; // a pulled level with at least this many frontier entries
   unsigned long long* tl;  // stage timeline: (tag, %globaltimer ns) pairs written by the leader
   unsigned tl_cap;
 #if BM_MG
@@ -908,6 +915,121 @@ BM_PREP_INLINE void bu_prep(const Params& p, Smem& sm, const int4* F, bool pairs
   flush_count(sm, kStCexp, live);
 }
 
+
+// bu_prep in two passes for wide frontiers with roots (the first pulled level of
+// a C5 phase: ~45 M columns): pass 1 drops dead trees' entries and writes the
+// live (col, root) pairs into the region of their column's bucket (CTA-staged
+// runs, one reservation per bucket per window; an overflow region takes any
+// skew); after a grid barrier, pass 2 takes the buckets in order (chunks handed
+// out from a ticket), so each bucket's root stores and bitmap atomics hit an
+// L2-resident window of croot / fbit instead of a random DRAM sector each.
+template <bool WR>
+__device__ __noinline__ void bu_prep_bucketed(const Params& p, Smem& sm, const int4* F, bool pairs, unsigned ls,
+                                              unsigned n, int lv, int par) {
+  Ctrl* ctl = p.ctl;
+  unsigned* fb = p.fbit[lv % kNumFbit];
+  int2* const buf = reinterpret_cast<int2*>(p.tb);
+  const int nb = p.pp_nb, shift = p.pp_shift;
+  const unsigned cap = p.pp_cap;
+  const unsigned long long ovf0 = (unsigned long long)nb * cap;
+  unsigned* const cur = ctl->pb_cur[par];
+  const unsigned long long pol = policy_evict_first();
+  const unsigned tid = threadIdx.x;
+  unsigned live = 0;
+  constexpr int K = 8;
+  constexpr unsigned W = kThreads * K;  // entries per CTA window
+  // ---- pass 1: partition the live entries by column bucket ----
+  for (unsigned long long w0 = (unsigned long long)blockIdx.x * W; w0 < n; w0 += (unsigned long long)gridDim.x * W) {
+    for (int b = tid; b < nb; b += kThreads) sm.pb_hist[b] = 0;
+    __syncthreads();
+    int col[K], root[K];
+    unsigned rank[K];
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      const unsigned long long k = w0 + (unsigned long long)i * kThreads + tid;
+      col[i] = -1;
+      root[i] = 0;
+      if (k < n) {
+        if (pairs) {
+          const int2 pr = ld_cg(p.P + ls + k);
+          col[i] = pr.x;
+          root[i] = pr.y;
+        } else {
+          const int4 ent = ld_cg(F + ls + k);
+          col[i] = ent.x;
+          root[i] = ent.y;
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      if (col[i] >= 0 && WR && root_dead(p, root[i])) col[i] = -1;
+      rank[i] = col[i] >= 0 ? atomicAdd(&sm.pb_hist[col[i] >> shift], 1u) : 0u;
+    }
+    __syncthreads();
+    for (int b = tid; b < nb; b += kThreads) {
+      const unsigned h = sm.pb_hist[b];
+      if (h) {
+        const unsigned base = atomicAdd(cur + b, h);
+        sm.pb_base[b] = base;
+        const unsigned fit = base >= cap ? 0u : min(h, cap - base);
+        if (fit < h) sm.pb_obase[b] = atomicAdd(&ctl->pb_ovf[par], h - fit);
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      if (col[i] < 0) continue;
+      live++;
+      const int b = col[i] >> shift;
+      const unsigned pos = sm.pb_base[b] + rank[i];
+      const unsigned long long idx =
+          pos < cap ? (unsigned long long)b * cap + pos : ovf0 + sm.pb_obase[b] + (pos - max(sm.pb_base[b], cap));
+      st_stream(buf + idx, make_int2(col[i], WR ? root[i] : col[i]), pol);
+    }
+    __syncthreads();
+  }
+  flush_count(sm, kStCexp, live);
+  grid_sync(p);
+  // ---- pass 2: bucket by bucket, the bitmap and the roots ----
+  constexpr unsigned CH = kThreads * K;
+  if (tid == 0) {
+    unsigned acc = 0;
+    for (int b = 0; b < nb; ++b) {
+      sm.pb_pre[b] = acc;
+      acc += (min(ld_rlx(cur + b), cap) + CH - 1) / CH;
+    }
+    sm.pb_pre[nb] = acc;
+    acc += (ld_rlx(&ctl->pb_ovf[par]) + CH - 1) / CH;
+    sm.pb_pre[nb + 1] = acc;
+  }
+  __syncthreads();
+  const unsigned total = sm.pb_pre[nb + 1];
+  for (;;) {
+    if (tid == 0) sm.tile = atomicAdd(&ctl->pb_ticket[par], 1u);
+    __syncthreads();
+    const unsigned t = sm.tile;
+    __syncthreads();
+    if (t >= total) break;
+    int b = 0;
+    while (b < nb && sm.pb_pre[b + 1] <= t) ++b;
+    const unsigned long long r0 = b < nb ? (unsigned long long)b * cap : ovf0;
+    const unsigned m = b < nb ? min(ld_rlx(cur + b), cap) : ld_rlx(&ctl->pb_ovf[par]);
+    const unsigned j0 = (t - sm.pb_pre[b]) * CH;
+    int2 pr[K];
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      const unsigned jj = j0 + i * kThreads + tid;
+      pr[i] = jj < m ? ld_cg(buf + r0 + jj) : make_int2(-1, 0);
+    }
+#pragma unroll
+    for (int i = 0; i < K; ++i)
+      if (pr[i].x >= 0) {
+        atomicOr(fb + (pr[i].x >> 5), 1u << (pr[i].x & 31));
+        st_plain(p.croot + pr[i].x, pr[i].y);
+      }
+  }
+}
 #ifndef BM_BU_PROBE
 #define BM_BU_PROBE 4
 #endif
@@ -2383,8 +2505,12 @@ BM_PHASE_FN PhaseOut run_phase(const Params& p, Smem& sm, int cur, int parity, b
     // and the hits resolve their roots through the level before (bu_sweep_q).
     const long long unvisited = (long long)p.nr - (long long)ls - (long long)n;
     const bool lazy = BU_LAZY && WR && bu && croot_prev && in_pairs && 3 * unvisited < (long long)n;
+    const bool prep_bucketed = bu && !lazy && p.tb && p.pp_nb > 0 && (unsigned long long)n >= p.pp_min;
     if (bu) {
-      bu_prep<WR>(p, sm, F, in_pairs, ls, n, lv, !lazy);
+      if (prep_bucketed)
+        bu_prep_bucketed<WR>(p, sm, F, in_pairs, ls, n, lv, lv & 1);
+      else
+        bu_prep<WR>(p, sm, F, in_pairs, ls, n, lv, !lazy);
       grid_sync(p);
       dirty |= 1u << (lv % kNumFbit);
       tl_mark(p, kTlPrep, n);
@@ -2417,8 +2543,8 @@ BM_PHASE_FN PhaseOut run_phase(const Params& p, Smem& sm, int cur, int parity, b
     } else {
       grid_sync(p);
       if (is_leader()) ctl->n_left[(lv + 2) % 3] = 0;  // the level before's list: consumed or unused; next written at lv + 2
-      if (bucketed && is_leader()) {  // next used two levels on (after another barrier)
-        for (int b = 0; b < p.pb_nb; ++b) ctl->pb_cur[lv & 1][b] = 0;
+      if ((bucketed || prep_bucketed) && is_leader()) {  // next used two levels on (after another barrier)
+        for (int b = 0; b < kPbMax; ++b) ctl->pb_cur[lv & 1][b] = 0;
         ctl->pb_ovf[lv & 1] = 0;
         ctl->pb_ticket[lv & 1] = 0;
       }

@@ -543,3 +543,31 @@ def test_last_phase_launches_match_counters(engine, oracle):
     launches = engine.last_phase_launches()
     assert launches == list(res.counters.bfs_launches_per_iteration)
     assert len(launches) == res.counters.outer_iterations >= 1
+
+
+@pytest.mark.parametrize("spec", [{}, {"BM_PB_SLACK": "0"}], ids=["regions", "overflow"])
+def test_bucketed_prep_parity(oracle, corpus, monkeypatch, spec):
+    """Bucketed bu_prep (column buckets, bu_prep_bucketed): forced on every pulled
+    level with roots (interleaved row state, every level pulled); with no slack
+    in the bucket regions the skewed graphs take the overflow region. Same maxima
+    as the oracle under every driver/kernel combination."""
+    env = {"BM_ROW_LAYOUT": "interleave", "BM_PP_MIN": "0", "BM_SOLO_EDGES": "0", "BM_BU_AUTO": "1",
+           "BM_BU_FRAC": "0"}
+    env.update(spec)
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    eng = bm.Engine(0)
+    eng.bottom_up = True
+    graphs = [g for g, _ in corpus[:200:4] + corpus[-4:]] + [
+        bm.generate_random_bipartite(20000, 20000, 4.0, 3), bm.generate_planted(30000, 8.0, 4),
+        bm.generate_rmat(13, 8.0, 2), bm.generate_banded(20000, 3, 0.1, 7)[0]]
+    for g in graphs:
+        init = bm.cheap_matching(g)
+        want = oracle.maximum(g)
+        for shortest, kernel, improved in [(False, bm.BfsKernel.GpubfsWr, False), (True, bm.BfsKernel.GpubfsWr, True),
+                                           (False, bm.BfsKernel.Gpubfs, False)]:
+            m = eng.match(g, init, shortest=shortest, kernel=kernel, improved=improved).matching
+            assert bm.cardinality(m) == want, (g.name, shortest, kernel)
+            assert oracle.validate(g, m.rmatch, m.cmatch) == 0
+            assert oracle.is_maximum(g, m.rmatch, m.cmatch) == 1
+    eng.close()
