@@ -365,7 +365,8 @@ class Engine:
         return ms.value, n.value
 
     TL_KINDS = {0: "start", 1: "init", 2: "setup", 3: "level", 4: "alternate", 5: "fix_rows", 6: "fix_cols",
-                7: "roots", 8: "end", 9: "level_edges", 10: "materialize", 11: "pull_prep", 12: "bucketed"}
+                7: "roots", 8: "end", 9: "level_edges", 10: "materialize", 11: "pull_prep", 12: "bucketed",
+                13: "late_level", 14: "late"}
 
     def timeline(self):
         """Stage timeline of the last run: list of (kind, arg, t_ns) from the device clock."""
@@ -382,7 +383,8 @@ class Engine:
     STAT_NAMES = ["edges_traversed", "columns_scanned", "columns_visited", "frontier_entries", "walks",
                   "walk_steps", "fix_resets", "levels", "serial_retries", "dense_fix", "cyc_tile", "cyc_window",
                   "cyc_rounds", "cyc_flush", "cyc_barrier", "cyc_other", "rows_pulled", "pulled_levels",
-                  "materialized", "cyc_bu_screen", "cyc_bu_probe", "cyc_bu_flush", "bu_rounds"]
+                  "materialized", "cyc_bu_screen", "cyc_bu_probe", "cyc_bu_flush", "bu_rounds",
+                  "late_phases", "late_paths"]
 
     def debug_stats(self) -> dict:
         buf = np.zeros(32, np.uint64)

@@ -177,6 +177,13 @@ struct bm_handle {
   int2* P = nullptr;          // lazy-frontier pairs (nc), pulled-capable runs only
   int4* tb = nullptr;         // bucketed pushed levels: (row, col, root) triples (ensure_pb)
   int2* left = nullptr;       // pulled levels' leftover lists: 3 x nr (row, row state)
+  // late phases (ensure_late): stamps of the meet-in-the-middle search
+  int2* lt_col = nullptr;
+  int* lt_croot = nullptr;
+  int* lt_row = nullptr;
+  int* lt_epoch = nullptr;
+  bool lt_ready = false;
+  int lt_nc = -1, lt_nr = -1;  // the sizes the stamps were last cleared for
   unsigned long long pb_max = 0;
   int pb_shift = 0, pb_nb = 0;
   unsigned pb_cap = 0;
@@ -722,6 +729,41 @@ bm_status ensure_pb(bm_handle* h) {
   return BM_OK;
 }
 
+// Late phases (late_phase, bm_kernels.cuh): phases with few roots first try a
+// bounded meet-in-the-middle search. Needs the row index (pulled-capable runs)
+// and per-column / per-row stamps, allocated here once per graph size. The
+// stamps are epochs that only grow, so they are cleared only when the sizes
+// change. BM_LATE=1|0 forces the late phases on|off (default: graphs with at
+// least 2^22 columns); an allocation failure leaves them off.
+bool late_wanted(const bm_handle* h) {
+  const char* e = getenv("BM_LATE");
+  if (e && *e) return atoi(e) != 0;
+  return h->nc >= (1 << 22);
+}
+
+bm_status ensure_late(bm_handle* h) {
+  h->lt_ready = false;
+  if (!late_wanted(h) || h->nc <= 0 || h->nr <= 0) return BM_OK;
+  const void* was[3] = {h->lt_col, h->lt_row, h->lt_epoch};
+  if (dalloc(h->caps, h->lt_col, (size_t)h->nc) != cudaSuccess ||
+      dalloc(h->caps, h->lt_croot, (size_t)h->nc) != cudaSuccess ||
+      dalloc(h->caps, h->lt_row, (size_t)h->nr) != cudaSuccess || dalloc(h->caps, h->lt_epoch, 1) != cudaSuccess) {
+    cudaGetLastError();
+    h->lt_nc = h->lt_nr = -1;
+    return BM_OK;
+  }
+  if (h->lt_nc != h->nc || h->lt_nr != h->nr || was[0] != h->lt_col || was[1] != h->lt_row ||
+      was[2] != h->lt_epoch) {
+    BM_CUDA(cudaMemsetAsync(h->lt_col, 0, sizeof(int2) * (size_t)h->nc, h->stream));
+    BM_CUDA(cudaMemsetAsync(h->lt_row, 0, sizeof(int) * (size_t)h->nr, h->stream));
+    BM_CUDA(cudaMemsetAsync(h->lt_epoch, 0, sizeof(int), h->stream));
+    h->lt_nc = h->nc;
+    h->lt_nr = h->nr;
+  }
+  h->lt_ready = true;
+  return BM_OK;
+}
+
 Params make_params(bm_handle* h, const bm_match_opts& o) {
   Params p{};
   p.nc = h->nc;
@@ -810,6 +852,24 @@ Params make_params(bm_handle* h, const bm_match_opts& o) {
   p.pp_cap = h->pp_cap;
   p.pp_min = 1ull << 22;
   if (const char* pm = getenv("BM_PP_MIN")) p.pp_min = (unsigned long long)atoll(pm);
+  {
+    const bool late = h->lt_ready && p.roffs && h->P;
+    p.lt_col = late ? h->lt_col : nullptr;
+    p.lt_croot = h->lt_croot;
+    p.lt_row = h->lt_row;
+    p.lt_epoch = h->lt_epoch;
+    p.lt_qcap = (unsigned)std::min<size_t>(((size_t)h->nc + kFSlack(h->nc)) / 2, 0x7fffffff);
+    auto env_u = [](const char* k, unsigned long long d) {
+      const char* v = getenv(k);
+      return v && *v ? (unsigned long long)atoll(v) : d;
+    };
+    p.lt_max_roots = (unsigned)env_u("BM_LATE_ROOTS", 65536);
+    p.lt_bcap = (unsigned)env_u("BM_LATE_BCAP", 1u << 21);
+    p.lt_fcap = (unsigned)env_u("BM_LATE_FCAP", 1u << 22);
+    p.lt_fper = (unsigned)env_u("BM_LATE_FPER", 1024);
+    p.lt_blv = (int)env_u("BM_LATE_BLV", 16);
+    p.lt_flv = (int)env_u("BM_LATE_FLV", 64);
+  }
   if (h->dbg_phase_bound > 0) p.phase_bound = h->dbg_phase_bound;
   p.sorted = h->sorted;
   p.check = getenv("BM_CHECK") ? atoi(getenv("BM_CHECK")) : 0;
@@ -847,6 +907,8 @@ bm_status drive(bm_handle* h, const bm_match_opts& o, bool fresh, int64_t* cardi
   }
   if (bu) {
     bm_status ps = ensure_pb(h);
+    if (ps != BM_OK) return ps;
+    ps = ensure_late(h);
     if (ps != BM_OK) return ps;
   }
   Params p = make_params(h, o);
@@ -1065,6 +1127,10 @@ bm_status bm_destroy(bm_handle* h) {
   dfree(h->P);
   dfree(h->tb);
   dfree(h->left);
+  dfree(h->lt_col);
+  dfree(h->lt_croot);
+  dfree(h->lt_row);
+  dfree(h->lt_epoch);
   dfree(h->gidx[0]);
   dfree(h->gidx[1]);
   dfree(h->wlog);

@@ -144,6 +144,8 @@ enum Stat : int {
   kStCycBuProbe,    // ... probe rounds
   kStCycBuFlush,    // ... winner and endpoint flushes
   kStBuRounds,      // ... probe rounds (warp-level)
+  kStLatePhases,    // late phases run (late_phase), including ones that found nothing
+  kStLatePaths,     // augmenting paths they flipped
   kNumStats
 };
 
@@ -169,6 +171,11 @@ struct alignas(128) Ctrl {
   unsigned pb_ticket[2];
   unsigned n_left[3];  // pulled levels' leftover lists, by level mod 3 (see Params::left)
   unsigned pad1c[25];
+  // late phases (late_phase): backward / forward queue counts by level mod 3, paths recorded
+  unsigned lt_b[3];
+  unsigned lt_f[3];
+  unsigned lt_nep;
+  unsigned pad1e[25];
   unsigned n_log;
   unsigned log_overflow;
   unsigned n_tl;
@@ -323,6 +330,18 @@ struct Params {
   unsigned long long pp_min; // a pulled level with at least this many frontier entries
   unsigned long long* tl;  // stage timeline: (tag, %globaltimer ns) pairs written by the leader
   unsigned tl_cap;
+  // Late phases (late_phase; single GPU, pulled-capable runs; lt_col == nullptr: off)
+  int2* lt_col;             // per column {epoch, row}: claimed by the backward search from that row
+                            // ({epoch, -2} on a root: its tree holds a path)
+  int* lt_croot;            // per column: the free row its backward tree started from
+  int* lt_row;              // per row: epoch when a forward tree claimed it (on a free row: when it was used)
+  int* lt_epoch;            // late phases so far (persistent across runs: the stamps are never reset)
+  unsigned lt_qcap;         // entries per queue (two queues in P)
+  unsigned lt_max_roots;    // a phase with at most this many roots is tried as a late phase first
+  unsigned lt_bcap;         // backward search: stop once it claimed this many columns ...
+  unsigned lt_fcap;         // forward search: ... this many frontier entries
+  unsigned lt_fper;         // ... or 64K + this many per root still without a path
+  int lt_blv, lt_flv;       // ... or after this many levels
 #if BM_MG
   int world, rank;
   int col_lo, col_hi, row_lo, row_hi;  // this rank's columns and rows
@@ -336,7 +355,9 @@ struct Params {
 
 enum TlTag : unsigned {
   kTlStart = 0, kTlInit = 1, kTlSetup = 2, kTlLevel = 3, kTlAlt = 4, kTlFixRows = 5, kTlFixCols = 6,
-  kTlRoots = 7, kTlEnd = 8, kTlLevelEdges = 9, kTlMat = 10, kTlPrep = 11, kTlBucket = 12
+  kTlRoots = 7, kTlEnd = 8, kTlLevelEdges = 9, kTlMat = 10, kTlPrep = 11, kTlBucket = 12,
+  kTlLateLevel = 13,  // a late phase's level: arg = entries (top bit: backward)
+  kTlLate = 14        // a late phase ended: arg = paths flipped
 };
 
 __device__ __forceinline__ void tl_mark(const Params& p, unsigned kind, unsigned arg) {
@@ -743,8 +764,8 @@ __device__ __forceinline__ void flush_pairs(const Params& p, Smem& sm, unsigned 
   if (threadIdx.x == 0) sm.nw = 0;
 }
 
-#if BM_MG
 __device__ __forceinline__ unsigned lanemask_lt() { return (1u << lane_id()) - 1u; }
+#if BM_MG
 // Multi-GPU: routes the winners staged in sm.wbuf to their columns' owners —
 // per destination one slot reservation on the owner's level counter, then the
 // pairs are stored straight into the owner's inbox (peer memory, NVLink).
@@ -2602,6 +2623,286 @@ BM_PHASE_FN PhaseOut run_phase(const Params& p, Smem& sm, int cur, int parity, b
   return out;
 }
 
+#if !BM_MG
+// ---------------------------------------------------------------------------
+// Late phases (an engine extension, single GPU, pulled-capable runs of
+// GPUBFS-WR under APFB). Once few roots are left, a phase still sweeps most of
+// the graph: each tree must grow until it meets one of the few free rows. A
+// late phase meets in the middle instead:
+//   1. a bounded backward search from the free rows over the row index,
+//      alternating like the forward one (row -> its columns -> their mates);
+//      each column it claims records the row it came from and its free row;
+//   2. a bounded forward search from the roots; a tree's row whose mate the
+//      backward search claimed (or a free row) ends the tree with a path,
+//      provided the tree and that backward tree are both still unused (CAS on
+//      the root's and the free row's stamps); such rows are dead ends either way;
+//   3. each path is flipped: the backward part toward its free row, then the
+//      forward part toward its root.
+// One path per root and per free row, and forward trees never pass through a
+// backward row, so the paths are vertex-disjoint and need no FIX. A late phase
+// that finds nothing hands over to a full phase (run_phase), which alone ends
+// the driver: a full phase without a path proves the matching maximum, as in
+// the reference (gpu_match.cpp:306-359).
+__device__ __forceinline__ unsigned lt_append(unsigned* cnt) {
+  cg::coalesced_group g = cg::coalesced_threads();
+  unsigned base = 0;
+  if (g.thread_rank() == 0) base = atomicAdd(cnt, g.size());
+  return g.shfl(base, 0) + g.thread_rank();
+}
+__device__ __forceinline__ int lt_stamp(const int2* a, long long i) {
+  return ld_rlx(reinterpret_cast<const int*>(a + i));
+}
+// Lanes of a warp that step in lockstep reserve their queue slots with one atomic.
+__device__ __forceinline__ unsigned lt_reserve(unsigned* cnt, bool want) {
+  const unsigned m = __ballot_sync(kFull, want);
+  if (!m) return 0u;
+  const int leader = __ffs(m) - 1;
+  unsigned base = 0;
+  if ((int)lane_id() == leader) base = atomicAdd(cnt, (unsigned)__popc(m));
+  base = __shfl_sync(kFull, base, leader);
+  return base + (unsigned)__popc(m & lanemask_lt());
+}
+__device__ __forceinline__ void lt_seed(const Params& p, unsigned qcap, int2* q, int r) {
+  if (ld_ro(p.roffs + r + 1) == ld_ro(p.roffs + r)) return;  // no edge
+  const unsigned s = lt_append(&p.ctl->lt_b[0]);
+  if (s < qcap) st_plain(q + s, make_int2(r, r));
+}
+// The tree rooted at R takes its one path (false: it already has one).
+__device__ __forceinline__ bool lt_take_root(const Params& p, int R, int ep) {
+  unsigned long long* w = reinterpret_cast<unsigned long long*>(p.lt_col + R);
+  const unsigned long long old = ld_rlx(w);
+  if ((int)(unsigned)old == ep) return false;
+  return atomicCAS(w, old, (unsigned long long)(unsigned)ep | (0xfffffffeull << 32)) == old;
+}
+
+__device__ __noinline__ long long late_phase(const Params& p, Smem& sm, int cur, long long isolated,
+                                             unsigned& levels, unsigned& paths) {
+  Ctrl* ctl = p.ctl;
+  const int4* F = cur ? p.F1 : p.F0;
+  int4* Fn = cur ? p.F0 : p.F1;
+  const unsigned long long rp = ld_rlx(&ctl->roots.packed);
+  const unsigned n0 = (unsigned)(rp >> 33);
+  grid_sync(p);  // every thread has read the roots' slot
+  if (is_leader()) {
+    st_rlx(p.lt_epoch, ld_rlx(p.lt_epoch) + 1);
+    ctl->roots.packed = 0;
+    ctl->roots.tile = 0;
+    for (int k = 0; k < 3; ++k) {
+      ctl->lt_b[k] = 0;
+      ctl->lt_f[k] = 0;
+    }
+    ctl->lt_nep = 0;
+  }
+  grid_sync(p);
+  const int ep = ld_rlx(p.lt_epoch);
+  const unsigned qcap = p.lt_qcap;
+  int2* Q[2] = {p.P, p.P + qcap};
+  // A warp takes 4 entries at a time, 8 lanes per entry, stepping through the
+  // entries' edges in lockstep (one queue atomic per step: lt_reserve).
+  const unsigned gl = lane_id() & 7u;
+  const unsigned long long w4 = (global_thread() >> 5) * 4, nw4 = (global_threads() >> 5) * 4;
+
+  // ---- backward seeds: the free rows with an edge (one streaming pass over the row state) ----
+  {
+    const int per = p.rs == 2 ? 2 : 4;  // rows per int4
+    const unsigned long long n4 = (unsigned long long)p.nr / per;
+    const int4* r4 = reinterpret_cast<const int4*>(p.rm);
+    for (unsigned long long k = global_thread(); k < n4; k += global_threads()) {
+      const int4 v = ld_cg(r4 + k);
+      if (per == 2) {
+        if (v.x == -1) lt_seed(p, qcap, Q[0], (int)(2 * k));
+        if (v.z == -1) lt_seed(p, qcap, Q[0], (int)(2 * k + 1));
+      } else {
+        if (v.x == -1) lt_seed(p, qcap, Q[0], (int)(4 * k));
+        if (v.y == -1) lt_seed(p, qcap, Q[0], (int)(4 * k + 1));
+        if (v.z == -1) lt_seed(p, qcap, Q[0], (int)(4 * k + 2));
+        if (v.w == -1) lt_seed(p, qcap, Q[0], (int)(4 * k + 3));
+      }
+    }
+    for (unsigned long long r = n4 * per + global_thread(); r < (unsigned long long)p.nr; r += global_threads())
+      if (ld_cg(RML(p, r)) == -1) lt_seed(p, qcap, Q[0], (int)r);
+  }
+  grid_sync(p);
+
+  // ---- backward levels: (row, free row) entries ----
+  unsigned blv = 0;
+  unsigned long long btot = 0;
+  for (;;) {
+    const unsigned n = min(ld_rlx(&ctl->lt_b[blv % 3]), qcap);
+    if (n == 0 || (int)blv >= p.lt_blv || btot + n > p.lt_bcap) break;
+    if (is_leader()) ctl->lt_b[(blv + 2) % 3] = 0;  // last read before the previous barrier
+    unsigned* outc = &ctl->lt_b[(blv + 1) % 3];
+    const int2* in = Q[blv & 1];
+    int2* nxt = Q[(blv + 1) & 1];
+    for (unsigned long long kb = w4; kb < n; kb += nw4) {
+      const unsigned long long k = kb + (lane_id() >> 3);
+      int2 e = make_int2(-1, -1);
+      unsigned j = 0, j1 = 0;
+      if (k < n) {
+        e = ld_cg(in + k);
+        j = ld_ro(p.roffs + e.x) + gl;
+        j1 = ld_ro(p.roffs + e.x + 1);
+      }
+      while (__any_sync(kFull, j < j1)) {
+        bool push = false;
+        int m = -1;
+        if (j < j1) {
+          const int c = ld_ro(p.radj + j);
+          m = ld_rlx(p.cmatch + c);
+          if (m >= 0) {  // (a free column is a root of the forward search)
+            unsigned long long* w = reinterpret_cast<unsigned long long*>(p.lt_col + c);
+            const unsigned long long old = ld_rlx(w);
+            if ((int)(unsigned)old != ep &&
+                atomicCAS(w, old, (unsigned long long)(unsigned)ep | ((unsigned long long)(unsigned)e.x << 32)) == old) {
+              st_plain(p.lt_croot + c, e.y);
+              push = true;
+            }
+          }
+          j += 8;
+        }
+        const unsigned s = lt_reserve(outc, push);
+        if (push && s < qcap) st_plain(nxt + s, make_int2(m, e.y));
+      }
+    }
+    grid_sync(p);
+    tl_mark(p, kTlLateLevel, n | 0x80000000u);
+    btot += min(ld_rlx(outc), qcap);
+    ++blv;
+  }
+
+  // ---- forward levels: (column, root) entries; level 0 = the roots ----
+  unsigned flv = 0, nf = n0;
+  unsigned long long ftot = 0;
+  for (;;) {
+    // bounded: a level is expanded only while the search stays within lt_fcap entries and
+    // within lt_fper entries per root still without a path (trees that found no path that
+    // far are most likely without one: the full phase takes them)
+    const unsigned nep_now = ld_rlx(&ctl->lt_nep);
+    const unsigned long long lim =
+        min((unsigned long long)p.lt_fcap, 65536ull + (unsigned long long)p.lt_fper * (n0 - min(nep_now, n0)));
+    if (nf == 0 || nep_now >= n0 || (int)flv >= p.lt_flv || ftot + nf > lim) break;
+    if (is_leader()) ctl->lt_f[(flv + 2) % 3] = 0;
+    unsigned* outc = &ctl->lt_f[(flv + 1) % 3];
+    const int2* in = Q[flv & 1];
+    int2* nxt = Q[(flv + 1) & 1];
+    for (unsigned long long kb = w4; kb < nf; kb += nw4) {
+      const unsigned long long k = kb + (lane_id() >> 3);
+      int col = -1, R = -1;
+      unsigned j = 0, j1 = 0;
+      if (k < nf) {
+        if (flv == 0) {
+          col = R = ld_cg(reinterpret_cast<const int*>(F + k));
+        } else {
+          const int2 e = ld_cg(in + k);
+          col = e.x;
+          R = e.y;
+        }
+        if (lt_stamp(p.lt_col, R) != ep) {  // (else the tree has its path)
+          j = ld_ro(p.offs + col) + gl;
+          j1 = ld_ro(p.offs + col + 1);
+        }
+      }
+      while (__any_sync(kFull, j < j1)) {
+        bool push = false;
+        int m = -1;
+        if (j < j1) {
+          const int r = ld_ro(p.adj + j);
+          j += 8;
+          const int old = ld_rlx(p.lt_row + r);
+          if (old != ep && atomicCAS(p.lt_row + r, old, ep) == old) {
+            st_rlx(PR(p, r), col);
+            m = ld_rlx(RML(p, r));
+            bool got = false;
+            if (m < 0) {  // a free row (this claim also used it up)
+              got = lt_take_root(p, R, ep);
+            } else if (lt_stamp(p.lt_col, m) == ep) {  // a backward row: meet, or a dead end
+              const int fr = ld_rlx(p.lt_croot + m);
+              const int of = ld_rlx(p.lt_row + fr);
+              if (of != ep && atomicCAS(p.lt_row + fr, of, ep) == of) {
+                got = lt_take_root(p, R, ep);
+                if (!got) st_rlx(p.lt_row + fr, 0);  // hand the free row back
+              }
+            } else {
+              push = true;
+            }
+            if (got) st_plain(p.EP + atomicAdd(&ctl->lt_nep, 1u), r);  // (one per root: < n0 <= nr)
+          }
+        }
+        const unsigned s = lt_reserve(outc, push);
+        if (push && s < qcap) st_plain(nxt + s, make_int2(m, R));
+      }
+    }
+    grid_sync(p);
+    tl_mark(p, kTlLateLevel, nf);
+    ftot += nf;
+    nf = min(ld_rlx(outc), qcap);
+    ++flv;
+  }
+
+  // ---- flip the paths ----
+  const unsigned nep = ld_rlx(&ctl->lt_nep);
+  for (unsigned long long k = global_thread(); k < nep; k += global_threads()) {
+    const int e = ld_cg(p.EP + k);
+    long long steps = 0;
+    int c = ld_rlx(RML(p, e));
+    while (c >= 0) {  // backward part: e's column moves to the row the backward search reached it from
+      const int r2 = ld_rlx(reinterpret_cast<const int*>(p.lt_col + c) + 1);
+      const int c2 = ld_rlx(RML(p, r2));
+      st_rlx(RML(p, r2), c);
+      st_rlx(p.cmatch + c, r2);
+      c = c2;
+      if (++steps > p.nc) {
+        ctl->error = kErrWalk;
+        break;
+      }
+    }
+    int row = e;
+    while (row >= 0) {  // forward part, toward the root
+      const int col = ld_rlx(PR(p, row));
+      const int mr = ld_rlx(p.cmatch + col);
+      st_rlx(p.cmatch + col, row);
+      st_rlx(RML(p, row), col);
+      row = mr;
+      if (++steps > p.nc) {
+        ctl->error = kErrWalk;
+        break;
+      }
+    }
+  }
+  grid_sync(p);
+
+  // ---- the roots left (as phase_tail's last step) ----
+  for (unsigned long long b = (unsigned long long)blockIdx.x * kThreads; b < n0; b += global_threads()) {
+    const unsigned long long k = b + threadIdx.x;
+    bool push = false;
+    int c = -1;
+    unsigned beg = 0, deg = 0;
+    if (k < n0) {
+      const int4 ent = ld_cg(F + k);
+      c = ent.x;
+      if (ld_rlx(p.cmatch + c) < 0) {
+        push = true;
+        beg = (unsigned)ent.z;
+        const unsigned nxt = (k + 1 < n0) ? ld_cg_u(F + k + 1) : (unsigned)(rp & kEdgeMask);
+        deg = nxt - (unsigned)ent.w;
+      } else {
+        st_plain(p.bfs + c, kUnvisited);
+      }
+    }
+    unsigned long long slot;
+    unsigned unused;
+    if (cta_reserve(sm, push ? 1u : 0u, push ? deg : 0u, 0u, &ctl->roots, &ctl->n_ep, slot, unused) && push)
+      put_entry(Fn, 0u, p.gidx0, slot, c, c, beg, deg);
+  }
+  grid_sync(p);
+  const unsigned long long np = ld_rlx(&ctl->roots.packed);
+  levels = blv + flv;
+  paths = nep;
+  tl_mark(p, kTlLate, nep);
+  return (long long)p.nc - isolated - (long long)(np >> 33);
+}
+#endif
+
 // ---------------------------------------------------------------------------
 template <bool WR, bool IMP, bool BU>
 #if BM_MG
@@ -2778,6 +3079,12 @@ __global__ void __launch_bounds__(kThreads, BU ? BM_MINB_BU : BM_MINB_PUSH) driv
 
   // ---- driver loop (run_driver, gpu_match.cpp:306-359) ----
   bool done = false;
+#if !BM_MG
+  // late phases (late_phase): APFB over GPUBFS-WR with the row index, no probes
+  const bool late_on = BU && WR && !IMP && !p.apsb && p.lt_col != nullptr && p.roffs != nullptr && !p.trace &&
+                       !p.stop_after_bfs && p.dbg_skip_alt_phase == 0;
+  bool late_ok = late_on;
+#endif
   for (;;) {
     if (outer + 1 > p.phase_bound) {
       if (is_leader()) ctl->error = kErrBound;
@@ -2785,6 +3092,42 @@ __global__ void __launch_bounds__(kThreads, BU ? BM_MINB_BU : BM_MINB_PUSH) driv
     }
     ++outer;
     const long long before = card;
+    long long late_levels = 0;
+#if !BM_MG
+    if constexpr (BU && WR && !IMP) {
+      const unsigned nroots = (unsigned)(ld_rlx(&ctl->roots.packed) >> 33);
+      if (late_ok && nroots > 0 && nroots <= p.lt_max_roots) {
+        unsigned lvls = 0, paths = 0;
+        const long long after = late_phase(p, sm, cur, isolated, lvls, paths);
+        cur ^= 1;
+        if (is_leader()) {
+          sm.cnt[kStLatePhases]++;
+          sm.cnt[kStLatePaths] += paths;
+        }
+        if (after > before) {
+          if (is_leader()) {
+            if (recs < p.rec_cap) {
+              PhaseRec r;
+              r.launches = lvls;
+              r.before = before;
+              r.after = after;
+              r.found = 1;
+              r.retry = 0;
+              p.recs[recs] = r;
+            }
+            sm.cnt[kStLevels] += lvls;
+          }
+          ++recs;
+          card = after;
+          if (ld_rlx((const unsigned*)&ctl->error) != 0u) break;
+          if (recs >= p.max_phases || recs >= p.rec_cap) break;
+          continue;
+        }
+        late_ok = false;  // nothing found: this phase runs in full
+        late_levels = lvls;
+      }
+    }
+#endif
     PhaseOut ph = run_phase<WR, IMP, BU>(p, sm, cur, parity, false, isolated, outer == p.dbg_skip_alt_phase);
     if (p.stop_after_bfs) {
       if (is_leader()) {
@@ -2796,7 +3139,7 @@ __global__ void __launch_bounds__(kThreads, BU ? BM_MINB_BU : BM_MINB_PUSH) driv
     }
     cur ^= 1;
     parity ^= 1;
-    long long launches = ph.launches;
+    long long launches = ph.launches + late_levels;
     long long after = ph.after;
     bool retried = false;
     if (ph.found && after <= before) {
@@ -2827,6 +3170,9 @@ __global__ void __launch_bounds__(kThreads, BU ? BM_MINB_BU : BM_MINB_PUSH) driv
       done = true;
       break;
     }
+#if !BM_MG
+    late_ok = late_on;  // the full phase found paths: the next one may be late again
+#endif
 #if BM_MG
     bool err = false;  // any rank's error stops every rank (they all read it after the same barrier)
     for (int q = 0; q < p.world; ++q) err = err || ld_rlx((const unsigned*)&p.peer[q].ctl->error) != 0u;

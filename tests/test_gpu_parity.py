@@ -359,6 +359,43 @@ def test_mixed_pushed_and_pulled_levels_parity(oracle, corpus, monkeypatch):
     eng.close()
 
 
+@pytest.mark.parametrize("bounds", [{}, {"BM_LATE_BCAP": "40", "BM_LATE_FCAP": "200", "BM_LATE_BLV": "2"},
+                                    {"BM_LATE_ROOTS": "2000000000"}], ids=["default", "tight", "every_phase"])
+def test_late_phase_parity(oracle, corpus, monkeypatch, bounds):
+    """Late phases (BM_LATE=1; bm_kernels.cuh late_phase): phases with few roots
+    first try a bounded meet-in-the-middle search whose vertex-disjoint paths
+    are flipped without FIX; a late phase that finds nothing hands over to a
+    full phase, which alone ends the driver. Every maximum must equal the
+    oracle's, the matching must be valid and maximum, and each late phase must
+    augment (strictly increasing cardinality per recorded phase) — with the
+    default bounds, with bounds so tight that most late phases give up, and
+    with every phase tried late (from the unmatched state too)."""
+    monkeypatch.setenv("BM_LATE", "1")
+    for k, v in bounds.items():
+        monkeypatch.setenv(k, v)
+    eng = bm.Engine(0)
+    eng.bottom_up = True
+    graphs = [g for g, _ in corpus[::4]] + [
+        bm.generate_random_bipartite(20000, 20000, 4.0, 3), bm.generate_random_bipartite(30000, 20000, 3.0, 5),
+        bm.generate_random_bipartite(20000, 30000, 3.0, 6), bm.generate_planted(30000, 8.0, 4),
+        bm.generate_rmat(13, 8.0, 2), bm.generate_banded(30000, 3, 0.1, 6)[0]]
+    late_paths = 0
+    for g in graphs:
+        want = oracle.maximum(g)
+        for init in [bm.cheap_matching(g), None]:
+            events = []
+            res = eng.match(g, init, kernel=bm.BfsKernel.GpubfsWr, observer=events.append)
+            m = res.matching
+            assert bm.cardinality(m) == want, g.name
+            assert oracle.validate(g, m.rmatch, m.cmatch) == 0
+            assert oracle.is_maximum(g, m.rmatch, m.cmatch) == 1
+            for ev in events[:-1]:
+                assert ev.cardinality_after > ev.cardinality_before, g.name
+            late_paths += eng.debug_stats()["late_paths"]
+    assert late_paths > 0
+    eng.close()
+
+
 # ---- failure paths of run_driver (fault injection through bm_debug_set) ----
 
 @pytest.mark.parametrize("cfg", CONFIGS, ids=[c[0] for c in CONFIGS])
