@@ -2734,6 +2734,7 @@ __device__ __noinline__ long long late_phase(const Params& p, Smem& sm, int cur,
     unsigned* outc = &ctl->lt_b[(blv + 1) % 3];
     const int2* in = Q[blv & 1];
     int2* nxt = Q[(blv + 1) & 1];
+    unsigned c_trav = 0, c_ent = 0, c_vis = 0;
     for (unsigned long long kb = w4; kb < n; kb += nw4) {
       const unsigned long long k = kb + (lane_id() >> 3);
       int2 e = make_int2(-1, -1);
@@ -2742,6 +2743,7 @@ __device__ __noinline__ long long late_phase(const Params& p, Smem& sm, int cur,
         e = ld_cg(in + k);
         j = ld_ro(p.roffs + e.x) + gl;
         j1 = ld_ro(p.roffs + e.x + 1);
+        c_ent += gl == 0 ? 1u : 0u;
       }
       while (__any_sync(kFull, j < j1)) {
         bool push = false;
@@ -2756,14 +2758,19 @@ __device__ __noinline__ long long late_phase(const Params& p, Smem& sm, int cur,
                 atomicCAS(w, old, (unsigned long long)(unsigned)ep | ((unsigned long long)(unsigned)e.x << 32)) == old) {
               st_plain(p.lt_croot + c, e.y);
               push = true;
+              c_vis++;
             }
           }
           j += 8;
+          c_trav++;
         }
         const unsigned s = lt_reserve(outc, push);
         if (push && s < qcap) st_plain(nxt + s, make_int2(m, e.y));
       }
     }
+    flush_count(sm, kStTrav, c_trav);
+    flush_count(sm, kStCexp, c_ent);
+    flush_count(sm, kStNvis, c_vis);
     grid_sync(p);
     tl_mark(p, kTlLateLevel, n | 0x80000000u);
     btot += min(ld_rlx(outc), qcap);
@@ -2785,6 +2792,7 @@ __device__ __noinline__ long long late_phase(const Params& p, Smem& sm, int cur,
     unsigned* outc = &ctl->lt_f[(flv + 1) % 3];
     const int2* in = Q[flv & 1];
     int2* nxt = Q[(flv + 1) & 1];
+    unsigned c_trav = 0, c_ent = 0, c_vis = 0;
     for (unsigned long long kb = w4; kb < nf; kb += nw4) {
       const unsigned long long k = kb + (lane_id() >> 3);
       int col = -1, R = -1;
@@ -2800,6 +2808,7 @@ __device__ __noinline__ long long late_phase(const Params& p, Smem& sm, int cur,
         if (lt_stamp(p.lt_col, R) != ep) {  // (else the tree has its path)
           j = ld_ro(p.offs + col) + gl;
           j1 = ld_ro(p.offs + col + 1);
+          c_ent += gl == 0 ? 1u : 0u;
         }
       }
       while (__any_sync(kFull, j < j1)) {
@@ -2808,8 +2817,10 @@ __device__ __noinline__ long long late_phase(const Params& p, Smem& sm, int cur,
         if (j < j1) {
           const int r = ld_ro(p.adj + j);
           j += 8;
+          c_trav++;
           const int old = ld_rlx(p.lt_row + r);
           if (old != ep && atomicCAS(p.lt_row + r, old, ep) == old) {
+            c_vis++;
             st_rlx(PR(p, r), col);
             m = ld_rlx(RML(p, r));
             bool got = false;
@@ -2832,6 +2843,9 @@ __device__ __noinline__ long long late_phase(const Params& p, Smem& sm, int cur,
         if (push && s < qcap) st_plain(nxt + s, make_int2(m, R));
       }
     }
+    flush_count(sm, kStTrav, c_trav);
+    flush_count(sm, kStCexp, c_ent);
+    flush_count(sm, kStNvis, c_vis);
     grid_sync(p);
     tl_mark(p, kTlLateLevel, nf);
     ftot += nf;
@@ -2841,9 +2855,11 @@ __device__ __noinline__ long long late_phase(const Params& p, Smem& sm, int cur,
 
   // ---- flip the paths ----
   const unsigned nep = ld_rlx(&ctl->lt_nep);
+  unsigned c_walks = 0, c_steps = 0;
   for (unsigned long long k = global_thread(); k < nep; k += global_threads()) {
     const int e = ld_cg(p.EP + k);
     long long steps = 0;
+    c_walks++;
     int c = ld_rlx(RML(p, e));
     while (c >= 0) {  // backward part: e's column moves to the row the backward search reached it from
       const int r2 = ld_rlx(reinterpret_cast<const int*>(p.lt_col + c) + 1);
@@ -2868,7 +2884,10 @@ __device__ __noinline__ long long late_phase(const Params& p, Smem& sm, int cur,
         break;
       }
     }
+    c_steps += (unsigned)steps;
   }
+  flush_count(sm, kStWalks, c_walks);
+  flush_count(sm, kStSteps, c_steps);
   grid_sync(p);
 
   // ---- the roots left (as phase_tail's last step) ----

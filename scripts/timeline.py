@@ -50,7 +50,7 @@ def main():
         cur_phase[kind] += dt
         if kind == "level":
             levels.append((len(phases), arg, dt))
-        if kind == "roots":
+        if kind in ("roots", "late"):  # a full phase's or a late phase's end
             phases.append(dict(cur_phase))
             cur_phase = defaultdict(float)
     total = (tl[-1][2] - tl[0][2]) / 1e3
