@@ -384,7 +384,7 @@ class Engine:
                   "walk_steps", "fix_resets", "levels", "serial_retries", "dense_fix", "cyc_tile", "cyc_window",
                   "cyc_rounds", "cyc_flush", "cyc_barrier", "cyc_other", "rows_pulled", "pulled_levels",
                   "materialized", "cyc_bu_screen", "cyc_bu_probe", "cyc_bu_flush", "bu_rounds",
-                  "late_phases", "late_paths"]
+                  "late_phases", "late_paths", "late_proofs"]
 
     def debug_stats(self) -> dict:
         buf = np.zeros(32, np.uint64)

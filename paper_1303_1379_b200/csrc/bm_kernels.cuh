@@ -146,6 +146,7 @@ enum Stat : int {
   kStBuRounds,      // ... probe rounds (warp-level)
   kStLatePhases,    // late phases run (late_phase), including ones that found nothing
   kStLatePaths,     // augmenting paths they flipped
+  kStLateProofs,    // runs ended by a late phase's exhausted backward search (no full phase needed)
   kNumStats
 };
 
@@ -175,7 +176,9 @@ struct alignas(128) Ctrl {
   unsigned lt_b[3];
   unsigned lt_f[3];
   unsigned lt_nep;
-  unsigned pad1e[25];
+  unsigned lt_hit;  // the backward search met a free column (a path may exist)
+  unsigned lt_ovf;  // a backward queue dropped an entry (the search was not exhaustive)
+  unsigned pad1e[23];
   unsigned n_log;
   unsigned log_overflow;
   unsigned n_tl;
@@ -2666,6 +2669,7 @@ __device__ __forceinline__ void lt_seed(const Params& p, unsigned qcap, int2* q,
   if (ld_ro(p.roffs + r + 1) == ld_ro(p.roffs + r)) return;  // no edge
   const unsigned s = lt_append(&p.ctl->lt_b[0]);
   if (s < qcap) st_plain(q + s, make_int2(r, r));
+  else st_rlx(&p.ctl->lt_ovf, 1u);
 }
 // The tree rooted at R takes its one path (false: it already has one).
 __device__ __forceinline__ bool lt_take_root(const Params& p, int R, int ep) {
@@ -2676,7 +2680,7 @@ __device__ __forceinline__ bool lt_take_root(const Params& p, int R, int ep) {
 }
 
 __device__ __noinline__ long long late_phase(const Params& p, Smem& sm, int cur, long long isolated,
-                                             unsigned& levels, unsigned& paths) {
+                                             unsigned& levels, unsigned& paths, bool& proven) {
   Ctrl* ctl = p.ctl;
   const int4* F = cur ? p.F1 : p.F0;
   int4* Fn = cur ? p.F0 : p.F1;
@@ -2692,6 +2696,8 @@ __device__ __noinline__ long long late_phase(const Params& p, Smem& sm, int cur,
       ctl->lt_f[k] = 0;
     }
     ctl->lt_nep = 0;
+    ctl->lt_hit = 0;
+    ctl->lt_ovf = 0;
   }
   grid_sync(p);
   const int ep = ld_rlx(p.lt_epoch);
@@ -2727,9 +2733,14 @@ __device__ __noinline__ long long late_phase(const Params& p, Smem& sm, int cur,
   // ---- backward levels: (row, free row) entries ----
   unsigned blv = 0;
   unsigned long long btot = 0;
+  bool exhausted = false;  // the backward search ran out of rows (not out of bounds)
   for (;;) {
     const unsigned n = min(ld_rlx(&ctl->lt_b[blv % 3]), qcap);
-    if (n == 0 || (int)blv >= p.lt_blv || btot + n > p.lt_bcap) break;
+    if (n == 0) {
+      exhausted = true;
+      break;
+    }
+    if ((int)blv >= p.lt_blv || btot + n > p.lt_bcap) break;
     if (is_leader()) ctl->lt_b[(blv + 2) % 3] = 0;  // last read before the previous barrier
     unsigned* outc = &ctl->lt_b[(blv + 1) % 3];
     const int2* in = Q[blv & 1];
@@ -2751,7 +2762,9 @@ __device__ __noinline__ long long late_phase(const Params& p, Smem& sm, int cur,
         if (j < j1) {
           const int c = ld_ro(p.radj + j);
           m = ld_rlx(p.cmatch + c);
-          if (m >= 0) {  // (a free column is a root of the forward search)
+          if (m < 0) {  // a free column: an augmenting path may exist (the forward search starts there)
+            if (ld_rlx(&ctl->lt_hit) == 0u) st_rlx(&ctl->lt_hit, 1u);
+          } else {
             unsigned long long* w = reinterpret_cast<unsigned long long*>(p.lt_col + c);
             const unsigned long long old = ld_rlx(w);
             if ((int)(unsigned)old != ep &&
@@ -2766,6 +2779,7 @@ __device__ __noinline__ long long late_phase(const Params& p, Smem& sm, int cur,
         }
         const unsigned s = lt_reserve(outc, push);
         if (push && s < qcap) st_plain(nxt + s, make_int2(m, e.y));
+        if (push && s >= qcap) st_rlx(&ctl->lt_ovf, 1u);
       }
     }
     flush_count(sm, kStTrav, c_trav);
@@ -2917,6 +2931,11 @@ __device__ __noinline__ long long late_phase(const Params& p, Smem& sm, int cur,
   const unsigned long long np = ld_rlx(&ctl->roots.packed);
   levels = blv + flv;
   paths = nep;
+  // No path, and the alternating search from every free row ran to its end
+  // without meeting a free column: no augmenting path exists (Berge), so the
+  // matching is maximum — the same certificate a full phase without a path
+  // gives, taken from the free rows' side.
+  proven = nep == 0 && exhausted && ld_rlx(&ctl->lt_hit) == 0u && ld_rlx(&ctl->lt_ovf) == 0u;
   tl_mark(p, kTlLate, nep);
   return (long long)p.nc - isolated - (long long)(np >> 33);
 }
@@ -3117,7 +3136,8 @@ __global__ void __launch_bounds__(kThreads, BU ? BM_MINB_BU : BM_MINB_PUSH) driv
       const unsigned nroots = (unsigned)(ld_rlx(&ctl->roots.packed) >> 33);
       if (late_ok && nroots > 0 && nroots <= p.lt_max_roots) {
         unsigned lvls = 0, paths = 0;
-        const long long after = late_phase(p, sm, cur, isolated, lvls, paths);
+        bool proven = false;
+        const long long after = late_phase(p, sm, cur, isolated, lvls, paths, proven);
         cur ^= 1;
         if (is_leader()) {
           sm.cnt[kStLatePhases]++;
@@ -3141,6 +3161,25 @@ __global__ void __launch_bounds__(kThreads, BU ? BM_MINB_BU : BM_MINB_PUSH) driv
           if (ld_rlx((const unsigned*)&ctl->error) != 0u) break;
           if (recs >= p.max_phases || recs >= p.rec_cap) break;
           continue;
+        }
+        if (proven) {  // maximum: this late phase is the run's last phase
+          if (is_leader()) {
+            if (recs < p.rec_cap) {
+              PhaseRec r;
+              r.launches = lvls;
+              r.before = before;
+              r.after = after;
+              r.found = 0;
+              r.retry = 0;
+              p.recs[recs] = r;
+            }
+            sm.cnt[kStLevels] += lvls;
+            sm.cnt[kStLateProofs]++;
+          }
+          ++recs;
+          card = after;
+          done = true;
+          break;
         }
         late_ok = false;  // nothing found: this phase runs in full
         late_levels = lvls;

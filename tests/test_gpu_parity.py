@@ -367,7 +367,10 @@ def test_late_phase_parity(oracle, corpus, monkeypatch, bounds):
     are flipped without FIX; a late phase that finds nothing hands over to a
     full phase, which alone ends the driver. Every maximum must equal the
     oracle's, the matching must be valid and maximum, and each late phase must
-    augment (strictly increasing cardinality per recorded phase) — with the
+    augment (strictly increasing cardinality per recorded phase). A late phase
+    that finds nothing but whose backward search from every free row ran to its
+    end without meeting a free column ends the run (no augmenting path exists);
+    the oracle's is_maximum checks those endings too. All this with the
     default bounds, with bounds so tight that most late phases give up, and
     with every phase tried late (from the unmatched state too)."""
     monkeypatch.setenv("BM_LATE", "1")
@@ -379,7 +382,7 @@ def test_late_phase_parity(oracle, corpus, monkeypatch, bounds):
         bm.generate_random_bipartite(20000, 20000, 4.0, 3), bm.generate_random_bipartite(30000, 20000, 3.0, 5),
         bm.generate_random_bipartite(20000, 30000, 3.0, 6), bm.generate_planted(30000, 8.0, 4),
         bm.generate_rmat(13, 8.0, 2), bm.generate_banded(30000, 3, 0.1, 6)[0]]
-    late_paths = 0
+    late_paths = proofs = 0
     for g in graphs:
         want = oracle.maximum(g)
         for init in [bm.cheap_matching(g), None]:
@@ -391,8 +394,12 @@ def test_late_phase_parity(oracle, corpus, monkeypatch, bounds):
             assert oracle.is_maximum(g, m.rmatch, m.cmatch) == 1
             for ev in events[:-1]:
                 assert ev.cardinality_after > ev.cardinality_before, g.name
-            late_paths += eng.debug_stats()["late_paths"]
+            st = eng.debug_stats()
+            late_paths += st["late_paths"]
+            proofs += st["late_proofs"]
     assert late_paths > 0
+    if not bounds:
+        assert proofs > 0  # some runs end on a late phase's exhausted backward search
     eng.close()
 
 
