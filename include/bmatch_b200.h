@@ -37,7 +37,11 @@
  * interleaved, i.e. far beyond L2), BM_BU_AUTO
  * (0|1: overrides the AUTO decision), BM_SOLO_EDGES
  * (widest level run by one CTA, default 1024), BM_PERSIST_MB (L2 persisting
- * window on the row state, default off).
+ * window on the row state, default off), BM_LATE=0|1 (late phases: phases
+ * with at most BM_LATE_ROOTS roots, default max(65536, nc / 200), first try a bounded
+ * meet-in-the-middle search; default on for pulling runs of graphs with at
+ * least 2^22 columns; bounds BM_LATE_BCAP, BM_LATE_FCAP, BM_LATE_FPER,
+ * BM_LATE_BLV, BM_LATE_FLV).
  */
 #ifndef BMATCH_B200_H
 #define BMATCH_B200_H
@@ -250,7 +254,9 @@ bm_status   bm_debug_set(bm_handle* h, int32_t key, int64_t value);
  * 9 the preceding level's frontier edges (arg; same timestamp), 10 the
  * preceding pushed level's pairs turned into entries (materialize), 11 the
  * preceding pulled level's frontier bitmap built (pull prep), 12 the
- * preceding bucketed pushed level's partition pass done.
+ * preceding bucketed pushed level's partition pass done, 13 a late phase's
+ * level (arg = entries; top bit set: backward), 14 a late phase's end
+ * (arg = paths flipped).
  * Written by one thread after each grid barrier (a few ns per stage). */
 bm_status   bm_timeline(bm_handle* h, uint64_t* out, int64_t cap, int64_t* n);
 
