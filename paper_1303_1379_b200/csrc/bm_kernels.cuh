@@ -2655,6 +2655,10 @@ __device__ __forceinline__ unsigned lt_append(unsigned* cnt) {
 __device__ __forceinline__ int lt_stamp(const int2* a, long long i) {
   return ld_rlx(reinterpret_cast<const int*>(a + i));
 }
+#ifndef BM_LT_U
+#define BM_LT_U 1
+#endif
+constexpr int kLtU = BM_LT_U;  // late levels: edges per lane per step (A/B on C5: 1 25.8 ms, 2 26.0, 4 26.8)
 // Lanes of a warp that step in lockstep reserve their queue slots with one atomic.
 __device__ __forceinline__ unsigned lt_reserve(unsigned* cnt, bool want) {
   const unsigned m = __ballot_sync(kFull, want);
@@ -2756,30 +2760,41 @@ __device__ __noinline__ long long late_phase(const Params& p, Smem& sm, int cur,
         j1 = ld_ro(p.roffs + e.x + 1);
         c_ent += gl == 0 ? 1u : 0u;
       }
+      // kLtU edges per lane per step, their loads and CASes issued back to back
+      const unsigned long long nw = (unsigned long long)(unsigned)ep | ((unsigned long long)(unsigned)e.x << 32);
       while (__any_sync(kFull, j < j1)) {
-        bool push = false;
-        int m = -1;
-        if (j < j1) {
-          const int c = ld_ro(p.radj + j);
-          m = ld_rlx(p.cmatch + c);
-          if (m < 0) {  // a free column: an augmenting path may exist (the forward search starts there)
-            if (ld_rlx(&ctl->lt_hit) == 0u) st_rlx(&ctl->lt_hit, 1u);
-          } else {
-            unsigned long long* w = reinterpret_cast<unsigned long long*>(p.lt_col + c);
-            const unsigned long long old = ld_rlx(w);
-            if ((int)(unsigned)old != ep &&
-                atomicCAS(w, old, (unsigned long long)(unsigned)ep | ((unsigned long long)(unsigned)e.x << 32)) == old) {
-              st_plain(p.lt_croot + c, e.y);
+        int cc[kLtU], mm[kLtU];
+        unsigned long long ow[kLtU], got[kLtU];
+#pragma unroll
+        for (int u = 0; u < kLtU; ++u) cc[u] = j + 8u * u < j1 ? ld_ro(p.radj + j + 8u * u) : -1;
+#pragma unroll
+        for (int u = 0; u < kLtU; ++u) mm[u] = cc[u] >= 0 ? ld_rlx(p.cmatch + cc[u]) : -1;
+#pragma unroll
+        for (int u = 0; u < kLtU; ++u)
+          ow[u] = mm[u] >= 0 ? ld_rlx(reinterpret_cast<const unsigned long long*>(p.lt_col + cc[u])) : 0ull;
+#pragma unroll
+        for (int u = 0; u < kLtU; ++u)
+          got[u] = (mm[u] >= 0 && (int)(unsigned)ow[u] != ep)
+                       ? atomicCAS(reinterpret_cast<unsigned long long*>(p.lt_col + cc[u]), ow[u], nw)
+                       : ~ow[u];
+#pragma unroll
+        for (int u = 0; u < kLtU; ++u) {
+          bool push = false;
+          if (cc[u] >= 0) {
+            c_trav++;
+            if (mm[u] < 0) {  // a free column: an augmenting path may exist (the forward search starts there)
+              if (ld_rlx(&ctl->lt_hit) == 0u) st_rlx(&ctl->lt_hit, 1u);
+            } else if (got[u] == ow[u]) {
+              st_plain(p.lt_croot + cc[u], e.y);
               push = true;
               c_vis++;
             }
           }
-          j += 8;
-          c_trav++;
+          const unsigned s = lt_reserve(outc, push);
+          if (push && s < qcap) st_plain(nxt + s, make_int2(mm[u], e.y));
+          if (push && s >= qcap) st_rlx(&ctl->lt_ovf, 1u);
         }
-        const unsigned s = lt_reserve(outc, push);
-        if (push && s < qcap) st_plain(nxt + s, make_int2(m, e.y));
-        if (push && s >= qcap) st_rlx(&ctl->lt_ovf, 1u);
+        j += 8u * kLtU;
       }
     }
     flush_count(sm, kStTrav, c_trav);
@@ -2826,22 +2841,34 @@ __device__ __noinline__ long long late_phase(const Params& p, Smem& sm, int cur,
         }
       }
       while (__any_sync(kFull, j < j1)) {
-        bool push = false;
-        int m = -1;
-        if (j < j1) {
-          const int r = ld_ro(p.adj + j);
-          j += 8;
-          c_trav++;
-          const int old = ld_rlx(p.lt_row + r);
-          if (old != ep && atomicCAS(p.lt_row + r, old, ep) == old) {
+        int rr[kLtU], old[kLtU], cas[kLtU], mm[kLtU], stm[kLtU];
+        bool won[kLtU];
+#pragma unroll
+        for (int u = 0; u < kLtU; ++u) rr[u] = j + 8u * u < j1 ? ld_ro(p.adj + j + 8u * u) : -1;
+#pragma unroll
+        for (int u = 0; u < kLtU; ++u) old[u] = rr[u] >= 0 ? ld_rlx(p.lt_row + rr[u]) : ep;
+#pragma unroll
+        for (int u = 0; u < kLtU; ++u) cas[u] = old[u] != ep ? atomicCAS(p.lt_row + rr[u], old[u], ep) : ep;
+#pragma unroll
+        for (int u = 0; u < kLtU; ++u) {
+          won[u] = old[u] != ep && cas[u] == old[u];
+          if (won[u]) st_rlx(PR(p, rr[u]), col);
+        }
+#pragma unroll
+        for (int u = 0; u < kLtU; ++u) mm[u] = won[u] ? ld_rlx(RML(p, rr[u])) : -1;
+#pragma unroll
+        for (int u = 0; u < kLtU; ++u) stm[u] = mm[u] >= 0 ? lt_stamp(p.lt_col, mm[u]) : 0;
+#pragma unroll
+        for (int u = 0; u < kLtU; ++u) {
+          bool push = false;
+          if (rr[u] >= 0) c_trav++;
+          if (won[u]) {
             c_vis++;
-            st_rlx(PR(p, r), col);
-            m = ld_rlx(RML(p, r));
             bool got = false;
-            if (m < 0) {  // a free row (this claim also used it up)
+            if (mm[u] < 0) {  // a free row (this claim also used it up)
               got = lt_take_root(p, R, ep);
-            } else if (lt_stamp(p.lt_col, m) == ep) {  // a backward row: meet, or a dead end
-              const int fr = ld_rlx(p.lt_croot + m);
+            } else if (stm[u] == ep) {  // a backward row: meet, or a dead end
+              const int fr = ld_rlx(p.lt_croot + mm[u]);
               const int of = ld_rlx(p.lt_row + fr);
               if (of != ep && atomicCAS(p.lt_row + fr, of, ep) == of) {
                 got = lt_take_root(p, R, ep);
@@ -2850,11 +2877,12 @@ __device__ __noinline__ long long late_phase(const Params& p, Smem& sm, int cur,
             } else {
               push = true;
             }
-            if (got) st_plain(p.EP + atomicAdd(&ctl->lt_nep, 1u), r);  // (one per root: < n0 <= nr)
+            if (got) st_plain(p.EP + atomicAdd(&ctl->lt_nep, 1u), rr[u]);  // (one per root: < n0 <= nr)
           }
+          const unsigned s = lt_reserve(outc, push);
+          if (push && s < qcap) st_plain(nxt + s, make_int2(mm[u], R));
         }
-        const unsigned s = lt_reserve(outc, push);
-        if (push && s < qcap) st_plain(nxt + s, make_int2(m, R));
+        j += 8u * kLtU;
       }
     }
     flush_count(sm, kStTrav, c_trav);
