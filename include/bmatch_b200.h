@@ -199,7 +199,8 @@ bm_status   bm_prepare_row_index(bm_handle* h);
  * bm_upload_csc builds the row index while it copies the adjacency (chunk by
  * chunk, on a second stream; only the final scatter is left when the copy
  * ends, and the next run waits for it) on graphs where AUTO pulls from the
- * first run (>= 2^26 rows and E >= 6 nc). BM_PREBUILD=1|0 forces it on|off. */
+ * first run (>= 2^26 rows and E >= 6 nc), or of >= 2^22 rows whose sampled
+ * columns pass AUTO's test (late phases). BM_PREBUILD=1|0 forces it on|off. */
 bm_status   bm_download_row_index(bm_handle* h, uint32_t* roffs, int32_t* radj);
 
 /* ---- matching: the reference-shaped one-call entry ----------------------
