@@ -2860,11 +2860,10 @@ __device__ __noinline__ long long late_phase(const Params& p, Smem& sm, int cur,
         for (int u = 0; u < kLtU; ++u) stm[u] = mm[u] >= 0 ? lt_stamp(p.lt_col, mm[u]) : 0;
 #pragma unroll
         for (int u = 0; u < kLtU; ++u) {
-          bool push = false;
+          bool push = false, got = false;
           if (rr[u] >= 0) c_trav++;
           if (won[u]) {
             c_vis++;
-            bool got = false;
             if (mm[u] < 0) {  // a free row (this claim also used it up)
               got = lt_take_root(p, R, ep);
             } else if (stm[u] == ep) {  // a backward row: meet, or a dead end
@@ -2877,8 +2876,9 @@ __device__ __noinline__ long long late_phase(const Params& p, Smem& sm, int cur,
             } else {
               push = true;
             }
-            if (got) st_plain(p.EP + atomicAdd(&ctl->lt_nep, 1u), rr[u]);  // (one per root: < n0 <= nr)
           }
+          const unsigned se = lt_reserve(&ctl->lt_nep, got);  // (one path per root: < n0 <= nr)
+          if (got) st_plain(p.EP + se, rr[u]);
           const unsigned s = lt_reserve(outc, push);
           if (push && s < qcap) st_plain(nxt + s, make_int2(mm[u], R));
         }
