@@ -866,9 +866,11 @@ Params make_params(bm_handle* h, const bm_match_opts& o) {
     // (C5 A/B: roots <= nc / 200 with a 16 M forward bound -8 % against 65536 and 4 M;
     //  C2 keeps 65536: its phase 0 late costs +6 %)
     p.lt_max_roots = (unsigned)env_u("BM_LATE_ROOTS", std::max(65536, h->nc / 200));
-    p.lt_bcap = (unsigned)env_u("BM_LATE_BCAP", 1u << 21);
+    // backward bound nc / 10 within [256 K, 2 M] (A/B: C2 0.5-1 M -26 % against 2 M; C5 1 M +7 %,
+    // 1.5-2 M even); forward 2048 entries per live root (C5 -1.4 % against 1024)
+    p.lt_bcap = (unsigned)env_u("BM_LATE_BCAP", std::min(1 << 21, std::max(1 << 18, h->nc / 10)));
     p.lt_fcap = (unsigned)env_u("BM_LATE_FCAP", 1u << 24);
-    p.lt_fper = (unsigned)env_u("BM_LATE_FPER", 1024);
+    p.lt_fper = (unsigned)env_u("BM_LATE_FPER", 2048);
     p.lt_blv = (int)env_u("BM_LATE_BLV", 16);
     p.lt_flv = (int)env_u("BM_LATE_FLV", 64);
   }
